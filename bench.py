@@ -1,0 +1,406 @@
+"""Benchmark: all-pairs Kendall tau-b variable-pairs/sec on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl ours|reference]
+
+A "step" is one full pass of the hot path over the configured workload
+(BASELINE config 2 by default: m=2048 x n=1000 int32 0..9, every i<j pair):
+K2 sign pack -> K3 tcgen05 int8 GEMM -> K5 fp64 finalize (tau_a, tau_b).
+
+* value: pairs/s with inputs resident in HBM, CUDA-event timed on the launching
+  stream, L2 flushed (256 MiB write) before every timed step, max over ranks.
+* e2e: the same metric through the public API with pinned HOST buffers: H2D of
+  the values, the full path, D2H of tau_b + numerator, all inside the events.
+* roofline: the GEMM (dominant kernel), algorithmic int8 ops 2K per i<j pair,
+  per-launch CUDA-event duration vs the int8 tensor peak measured here with
+  torch._int_mm (MEASURED_PEAKS.json has no int8 entry).
+* cpu_baseline: the oracle port (C restatement of the reference packed/VSE
+  merge kernel, pthreads over all host cores) on a bounded sample (rank 0, N=1).
+
+``--impl reference`` times that CPU implementation alone on the host cores
+(oracle port: the reference is Python/numba and does not travel to the box).
+Multi-GPU (torchrun): every rank computes its own copy of the workload
+(independent objects, no collective) -> "scaling": "weak"; ``--scaling strong``
+shards the job-id range instead (contiguous shards concatenate, pairindex.py:68-80).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+with open(os.path.join(ROOT, "BASELINE.json")) as _fh:
+    METRIC = json.load(_fh)["metric"]
+UNIT = "pairs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_pairs_rate(ranks: np.ndarray, seconds: float, threads: int, seed: int = 99):
+    """Time the oracle port on a bounded random pair sample; returns (pairs/s, sample description)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc  # CPU baseline leg only
+
+    m, n = ranks.shape
+    kernel = orc.KERNEL_PACKED if (n <= 32767 and ranks.max() < 1 << 15) else orc.KERNEL_SORTED
+    rng = np.random.default_rng(seed)
+    probe = max(threads * 4, 64)
+    pi, pj = _sample_pairs(rng, m, probe)
+    t0 = time.perf_counter()
+    orc.all_pairs(ranks, pi, pj, kernel, threads=threads, want_counts=False)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    count = int(max(probe, min(m * (m - 1) // 2, probe / dt * seconds)))
+    pi, pj = _sample_pairs(rng, m, count)
+    t0 = time.perf_counter()
+    orc.all_pairs(ranks, pi, pj, kernel, threads=threads, want_counts=False)
+    dt = time.perf_counter() - t0
+    kname = "packed (VSE semantics, kernel_vectorized.py:507-523)" if kernel == orc.KERNEL_PACKED else \
+        "sorted (GSE, kernel_sorted.py:195-212)"
+    return count / dt, f"{count} random i<j pairs of the workload (rng 99), oracle {kname}, {dt:.1f}s", count, dt
+
+
+def _sample_pairs(rng, m, count):
+    i = rng.integers(0, m, count * 2)
+    j = rng.integers(0, m, count * 2)
+    keep = i != j
+    i, j = i[keep][:count], j[keep][:count]
+    return np.minimum(i, j).astype(np.int64), np.maximum(i, j).astype(np.int64)
+
+
+def workload(k: int):
+    from paper_1704_03767_b200 import workloads
+    spec = workloads.CONFIGS[k]
+    x = workloads.generate(k)
+    return spec, x
+
+
+def host_ranks(x: np.ndarray) -> np.ndarray:
+    from paper_1704_03767_b200.ranks import rank_transform
+    if x.dtype == np.int32 and x.min() >= 0 and x.max() < x.shape[1]:
+        # already dense ranks when every value 0..max occurs (config 2); verify cheaply per row
+        ok = all(len(np.unique(r)) == int(r.max()) + 1 for r in x[:8])
+        if ok:
+            return np.stack([rank_transform(r) for r in x])
+    return np.stack([rank_transform(r) for r in x])
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    spec, x = workload(args.config)
+    ranks = host_ranks(x)
+    threads = os.cpu_count() or 1
+    m, n = ranks.shape
+    total_steps = args.steps + args.warmup
+    per_step = max(0.05, min(2.0, 150.0 / max(total_steps, 1)))
+    rate0, _, _, _ = cpu_pairs_rate(ranks, per_step, threads)
+    count = max(threads * 4, int(rate0 * per_step))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    kernel = orc.KERNEL_PACKED if (n <= 32767 and ranks.max() < 1 << 15) else orc.KERNEL_SORTED
+    rng = np.random.default_rng(99)
+    times = []
+    for s in range(total_steps):
+        pi, pj = _sample_pairs(rng, m, count)
+        t0 = time.perf_counter()
+        orc.all_pairs(ranks, pi, pj, kernel, threads=threads, want_counts=False)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = count * len(times) / tot
+    sample = (f"{count} random i<j pairs per step of {spec.name} (rng 99); oracle port of the reference "
+              f"{'packed/VSE' if kernel == orc.KERNEL_PACKED else 'GSE merge-sort'} kernel, {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": {"workload": spec.name, "m": m, "n": n, "pairs": m * (m - 1) // 2},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def measure_int8_peak(torch, dev):
+    """Dense int8 tensor peak via cuBLASLt (torch._int_mm 8192^3, best of 10)."""
+    try:
+        a = torch.randint(-3, 3, (8192, 8192), dtype=torch.int8, device=dev)
+        b = torch.randint(-3, 3, (8192, 8192), dtype=torch.int8, device=dev).t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = float("inf")
+        for _ in range(10):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            torch._int_mm(a, b)
+            e.record()
+            e.synchronize()
+            best = min(best, s.elapsed_time(e) / 1e3)
+        del a, b
+        return 2 * 8192 ** 3 / best
+    except Exception as exc:  # noqa: BLE001
+        print(f"# int8 peak probe failed: {exc}", file=sys.stderr)
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.device import TauEngine
+    from paper_1704_03767_b200.pairindex import job_shard_range
+
+    spec, x = workload(args.config)
+    m, n = x.shape
+    total_jobs = m * (m + 1) // 2
+    job_range = job_shard_range(rank, world, m) if args.scaling == "strong" else (0, total_jobs)
+    eng = TauEngine(local)
+    stream = torch.cuda.Stream(device=dev)
+    path = eng.choose_path(n)
+    xin = x
+    if path == "merge":
+        xin = host_ranks(x)
+    xd = torch.from_numpy(np.ascontiguousarray(xin)).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    K = n * (n - 1) // 2
+
+    # pairs (i<j) this rank computes
+    def strict_pairs(lo, hi):
+        # job ids include the diagonal; count diagonal cells in [lo, hi)
+        ys = np.arange(m, dtype=np.int64)
+        dj = ys * (2 * m - ys + 1) // 2
+        return (hi - lo) - int(((dj >= lo) & (dj < hi)).sum())
+
+    my_pairs = strict_pairs(*job_range)
+
+    # instrumented step: events around the GEMM (dominant kernel) on the launching stream
+    gemm_events = []
+
+    def step(instrument=False):
+        with torch.cuda.stream(stream):
+            if instrument:
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                res = eng.all_pairs(xd, kernel=path, job_range=job_range, stream=stream,
+                                    _events=(s, e))
+                gemm_events.append((s, e))
+            else:
+                res = eng.all_pairs(xd, kernel=path, job_range=job_range, stream=stream)
+        return res
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    res.validate()
+    launches_per_step = res.launches
+    del res
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    times = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+        res = step(instrument=True)
+        e.record(stream)
+        times.append((s, e))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    t_total = sum(s.elapsed_time(e) for s, e in times) / 1e3
+    gemm_s = [s.elapsed_time(e) / 1e3 for s, e in gemm_events]
+    gemm_avg = sum(gemm_s) / len(gemm_s)
+    t_max = t_total
+    if world > 1:
+        tt = torch.tensor([t_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    total_pairs = my_pairs * world
+    value = total_pairs * args.steps / t_max
+    ms_per_step = 1e3 * t_max / args.steps
+    del res
+
+    # ---- e2e through the public API with pinned host buffers
+    xh = torch.from_numpy(np.ascontiguousarray(xin)).pin_memory()
+    count = job_range[1] - job_range[0]
+    out_tb = torch.empty(count, dtype=torch.float64).pin_memory()
+    out_num = torch.empty(count, dtype=torch.int32).pin_memory()
+    e2e_times = []
+    for it in range(args.e2e_steps + 2):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            xdev = xh.to(dev, non_blocking=True)
+            r = eng.all_pairs(xdev, kernel=path, job_range=job_range, tau_a=False, stream=stream)
+            out_tb.copy_(r.tau_b, non_blocking=True)
+            out_num.copy_(r.numerator, non_blocking=True)
+            e.record(stream)
+        if it >= 2:
+            e2e_times.append((s, e))
+        del r
+    torch.cuda.synchronize()
+    e2e_t = sum(s.elapsed_time(e) for s, e in e2e_times) / 1e3
+    if world > 1:
+        tt = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+    e2e_value = total_pairs * len(e2e_times) / e2e_t
+    h2d = xh.numel() * xh.element_size()
+    d2h = count * (8 + 4)
+
+    out = None
+    if rank == 0:
+        peak = measure_int8_peak(torch, dev) if path == "gemm" else None
+        algo = 2 * K * my_pairs if path == "gemm" else 4 * n * int(np.ceil(np.log2(n))) * my_pairs
+        achieved = algo / gemm_avg
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as fh:
+                tj = json.load(fh)
+            traffic = tj.get(f"config{args.config}", {}).get("dram_bytes_per_launch")
+        if path == "gemm":
+            roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": (peak or 4.5e15) / 1e12,
+                    "unit": "TFLOP/s", "frac": achieved / (peak or 4.5e15), "traffic": traffic,
+                    "kernel": "gemm_tc_kernel (tcgen05.mma kind::i8)",
+                    "peak_source": "measured here: torch._int_mm int8 8192^3 best-of-10 (cuBLASLt)" if peak
+                    else "nominal 4.5 POPS dense int8 (probe failed)",
+                    "frac_of_nominal_4500": achieved / 4.5e15,
+                    "algorithmic": f"2*K int8 ops per i<j pair, K=n(n-1)/2={K}; {my_pairs} pairs per launch",
+                    "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}
+        else:
+            roof = {"bound": "int32", "achieved": achieved / 1e12, "peak": None, "unit": "TOP/s",
+                    "frac": None, "traffic": traffic, "kernel": "merge_pairs_kernel",
+                    "algorithmic": f"4*n*ceil(log2 n) INT32 ops per pair, n={n}",
+                    "kernel_ms": 1e3 * gemm_avg}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            ranks = host_ranks(x)
+            threads = os.cpu_count() or 1
+            rate, sample, _, _ = cpu_pairs_rate(ranks, args.cpu_seconds, threads)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "i8" if path == "gemm" else "int32",
+            "data": "synthetic",
+            "config": {"workload": f"config{args.config}_{spec.name}", "m": m, "n": n,
+                       "pairs_per_rank": my_pairs, "path": path,
+                       "l2": "flushed before every timed step (256 MiB write, untimed)",
+                       "outputs": "numerator i32 + tau_a f64 + tau_b f64 in job-id order"},
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / len(e2e_times)},
+            "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
+            "abi": _lib.TB_MAX_N and "libtaub200.so",
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * taub200 -- C ABI of the B200 (sm_100a) all-pairs Kendall tau engine.
+ *
+ * Plain extern "C": raw device pointers, sizes and a cudaStream_t passed as
+ * void*.  All memory is caller-allocated; every call is asynchronous on the
+ * given stream and returns a status code.  Status codes map one-to-one onto
+ * the reference exception hierarchy (src/taucorr/errors.py:4-24):
+ *
+ *   TB_OK             0
+ *   TB_ERR_INVALID    1  -> InvalidInputError     (errors.py:8-9)
+ *   TB_ERR_CAPACITY   2  -> CapacityExceededError (errors.py:12-17)
+ *   TB_ERR_CONFIG     3  -> ConfigError           (errors.py:23-24)
+ *   TB_ERR_CUDA       4  -> RuntimeError (CUDA launch/driver failure)
+ *
+ * tb_last_error() returns the message of the last failing call on the calling
+ * thread.
+ *
+ * Ordering contract: "job ids" are the reference's diagonal-inclusive
+ * upper-triangle numbering J_m(y, x) = y(2m - y + 1)/2 + x - y
+ * (src/taucorr/pairindex.py:20-31).  Every per-pair output buffer holds the
+ * contiguous job-id range [job_lo, job_hi) at offset j - job_lo, which is
+ * also the unit of multi-GPU sharding (pairindex.py:68-80 semantics).
+ *
+ * Citations are into /root/reference/pkg/.
+ */
+#ifndef TAUB200_H
+#define TAUB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TB_ABI_VERSION 1
+
+#define TB_OK 0
+#define TB_ERR_INVALID 1
+#define TB_ERR_CAPACITY 2
+#define TB_ERR_CONFIG 3
+#define TB_ERR_CUDA 4
+
+#define TB_DTYPE_I32 0
+#define TB_DTYPE_F32 1
+#define TB_DTYPE_F64 2
+
+/* Largest n the device paths accept: the int32 numerator holds |n_c - n_d| <=
+ * n(n-1)/2 < 2^31 exactly up to here.  Larger n raises
+ * TB_ERR_CAPACITY (the reference's packed-capacity convention, ranks.py:64-76). */
+#define TB_MAX_N 65536
+
+typedef struct {
+    int32_t abi_version;
+    int32_t device;
+    int32_t sm_count;
+    int32_t cc_major;
+    int32_t cc_minor;
+    int32_t tcgen05_i8; /* 1 when the tcgen05 kind::i8 GEMM can run (sm_100a) */
+    int64_t smem_optin;
+} tb_caps;
+
+const char *tb_last_error(void);
+int tb_query(int device, tb_caps *caps);
+
+/*
+ * K2 sign pack.  Replaces the per-pair sign enumeration of
+ * naive_numerator (src/taucorr/kernel_naive.py:26-44) and the per-pair tie
+ * scans for n1/n2 (src/taucorr/kernel_sorted.py:163-176).
+ *
+ *   x     [m, ldx] values (TB_DTYPE_*), compared directly: the sign of a rank
+ *         difference equals the sign of the value difference for the dense
+ *         ranks of rank_transform (src/taucorr/ranks.py:37-61).
+ *   S     [m, ldS] int8, S[r, k(a,b)] = sign(x[r,b] - x[r,a]) for a < b, with
+ *         k(a,b) = a*n - a(a+1)/2 + (b - a - 1); bytes [K, ldS) are zeroed.
+ *         ldS must be a multiple of 16 and >= K = n(n-1)/2.
+ *   n1    [m] uint64 per-row tied-pair count n1 = n0 - sum_k |S[r,k]|.
+ *   flags device int32; bit 0 is set when a NaN was seen (NaN has no rank,
+ *         ranks.py:56-57); the caller raises InvalidInputError.
+ */
+int tb_sign_pack(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, int8_t *S, int64_t ldS,
+                 uint64_t *n1, int32_t *flags, void *stream);
+
+/*
+ * K3 numerator GEMM on tcgen05 tensor cores (kind::i8, TMA-fed, TMEM
+ * accumulators): num[j - job_lo] = S_y . S_x = n_c - n_d for every job id j in
+ * [job_lo, job_hi).  Replaces the per-cell numerator of _tiles_naive
+ * (src/taucorr/engine.py:170-188) -- exact int32 accumulation.
+ * splits: K-split factor (0 = automatic).  With splits > 1 the kernel
+ * accumulates atomically; the library zeroes num first.
+ */
+int tb_gemm_pairs(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
+                  int32_t splits, int32_t *num, void *stream);
+
+/* |S| for the full-count mode: A[r, k] = |S[r, k]| (0/1 int8), same layout.
+ * The second GEMM A A^T gives n_c + n_d per pair (SURVEY 8 identities). */
+int tb_abs_pack(const int8_t *S, int64_t m, int64_t ldS, int8_t *A, void *stream);
+
+/* Full counts on the GEMM path from num = S_y.S_x and absdot = |S_y|.|S_x|:
+ * n_d = (absdot - num) / 2 and n3 = absdot - n0 + n1_y + n1_x (the CELL_DTYPE
+ * fields of src/taucorr/engine.py:45-55).  nd / n3 may be NULL. */
+int tb_full_counts(const int32_t *num, const int32_t *absdot, const uint64_t *n1_rows, int64_t m, int64_t n,
+                   int64_t job_lo, int64_t job_hi, uint64_t *nd, uint64_t *n3, void *stream);
+
+/* Same contract on CUDA cores (dp4a); a GPU-side cross-check, not the product path. */
+int tb_gemm_pairs_simt(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
+                       int32_t *num, void *stream);
+
+/*
+ * K5 fp64 finalize: derive_taus (src/taucorr/result.py:62-82) over the job
+ * range.  tau_a = num / n0; tau_b = num / sqrt((n0 - n1_y) * (n0 - n1_x)), NaN
+ * where the denominator is 0.  IEEE round-to-nearest div/sqrt, no
+ * contraction: bit-identical to the reference.  tau_a / tau_b may be NULL.
+ */
+int tb_finalize(const int32_t *num, const uint64_t *n1_rows, int64_t m, int64_t n, int64_t job_lo,
+                int64_t job_hi, double *tau_a, double *tau_b, void *stream);
+
+/*
+ * K1 presort for the merge path (large n): per variable, the position of
+ * every observation in ascending-rank order (u-order), the rank sequence in
+ * that order, the tie count n1 and the largest tie group.  Replaces step 1
+ * of sorted_counts (src/taucorr/kernel_sorted.py:95-127, 163-176), once per
+ * variable instead of once per pair.
+ *   ranks   [m, n] int32 dense ranks (0 <= rank < n)
+ *   pos     [m, n] int32 out: pos[r, e] = position of element e in u-order
+ *   sorted  [m, n] int32 out: sorted[r, p] = rank at position p
+ *   n1      [m] uint64 out;  maxgrp [m] int32 out
+ *   work    [m, n] int32 scratch
+ *   flags   device int32; bit 1 is set when a rank is outside [0, n) (the
+ *           caller raises InvalidInputError, as Dataset validation does)
+ */
+int tb_presort(const int32_t *ranks, int64_t m, int64_t n, int32_t *pos, int32_t *sorted, uint64_t *n1,
+               int32_t *maxgrp, int32_t *work, int32_t *flags, void *stream);
+
+/*
+ * K4 Knight merge-inversion counts (large n): for every job id in
+ * [job_lo, job_hi): n_d (discordant pairs, strict), n3 (joint ties) and the
+ * numerator n0 - n1 - n2 + n3 - 2 n_d (src/taucorr/result.py:42).  Replaces
+ * steps 1-5 of sorted_counts (src/taucorr/kernel_sorted.py:195-212).
+ * nd / n3 may be NULL.
+ */
+int tb_merge_pairs(const int32_t *ranks, const int32_t *pos, const int32_t *sorted, const uint64_t *n1_rows,
+                   const int32_t *maxgrp, int64_t m, int64_t n, int64_t job_lo, int64_t job_hi, int32_t *num,
+                   uint64_t *nd, uint64_t *n3, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAUB200_H */

@@ -1,0 +1,63 @@
+// C-ABI plumbing: error state, device query.
+#include <algorithm>
+#include <cstdarg>
+#include <cstring>
+
+#include "tb_common.cuh"
+
+namespace tb {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(TB_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+    return TB_OK;
+}
+
+int num_sms() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" const char* tb_last_error(void) { return g_err; }
+
+extern "C" int tb_query(int device, tb_caps* caps) {
+    if (!caps) return fail(TB_ERR_INVALID, "tb_query: null caps");
+    std::memset(caps, 0, sizeof(*caps));
+    caps->abi_version = TB_ABI_VERSION;
+    caps->device = device;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || device >= n || device < 0)
+        return fail(TB_ERR_CUDA, "tb_query: no CUDA device %d (%s)", device, cudaGetErrorString(e));
+    cudaDeviceProp p;
+    TB_CUDA_TRY(cudaGetDeviceProperties(&p, device));
+    caps->sm_count = p.multiProcessorCount;
+    caps->cc_major = p.major;
+    caps->cc_minor = p.minor;
+    caps->smem_optin = (int64_t)p.sharedMemPerBlockOptin;
+    caps->tcgen05_i8 = (p.major == 10 && p.minor == 0) ? 1 : 0;
+    return TB_OK;
+}

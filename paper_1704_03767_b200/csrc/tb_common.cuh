@@ -1,0 +1,59 @@
+// Shared device/host helpers: status handling, triangular geometry.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+#include "../../include/taub200.h"
+
+namespace tb {
+
+// Thread-local error message for tb_last_error().
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+int check_launch(const char* what);
+
+#define TB_CUDA_TRY(expr)                                                                      \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess) return ::tb::fail(TB_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+    } while (0)
+
+int num_sms();
+
+// ------------------------------------------------------------------ geometry
+// pairindex.py:20-24 row_prefix: cells strictly above row y = y(2m - y + 1)/2.
+__host__ __device__ __forceinline__ int64_t row_prefix(int64_t y, int64_t m) { return y * (2 * m - y + 1) / 2; }
+
+// pairindex.py:34-55 job_coord: closed-form row guess from the float square
+// root, then the integer correction that makes the bijection exact for any m
+// (ids are 64-bit: m(m+1)/2 exceeds 2^31 at config 5).
+__host__ __device__ __forceinline__ void job_coord(int64_t j, int64_t m, int64_t& y, int64_t& x) {
+    double disc = (double)m * (double)m + (double)m + 0.25 - 2.0 * ((double)j + 1.0);
+    double g = ceil((double)m - 0.5 - sqrt(disc > 0.0 ? disc : 0.0));
+    int64_t yy = (int64_t)g;
+    if (yy < 0) yy = 0;
+    if (yy > m - 1) yy = m - 1;
+    while (yy > 0 && row_prefix(yy, m) > j) --yy;
+    while (yy < m - 1 && row_prefix(yy + 1, m) <= j) ++yy;
+    y = yy;
+    x = j + yy - row_prefix(yy, m);
+}
+
+// Sample-pair enumeration for the sign vector: k(a, b) = a*n - a(a+1)/2 + (b - a - 1), a < b.
+__host__ __device__ __forceinline__ int64_t seg_offset(int64_t a, int64_t n) { return a * n - a * (a + 1) / 2; }
+
+__device__ __forceinline__ void k_decode(int64_t k, int64_t n, int64_t& a, int64_t& b) {
+    double c = 2.0 * (double)n - 1.0;
+    double disc = c * c - 8.0 * (double)k;
+    int64_t aa = (int64_t)floor((c - sqrt(disc > 0.0 ? disc : 0.0)) * 0.5);
+    if (aa < 0) aa = 0;
+    if (aa > n - 2) aa = n - 2;
+    while (aa > 0 && seg_offset(aa, n) > k) --aa;
+    while (aa < n - 2 && seg_offset(aa + 1, n) <= k) ++aa;
+    a = aa;
+    b = k - seg_offset(aa, n) + aa + 1;
+}
+
+}  // namespace tb

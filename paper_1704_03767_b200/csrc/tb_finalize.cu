@@ -1,0 +1,86 @@
+// K5: fp64 finalize over a contiguous job-id range -- derive_taus
+// (result.py:62-82) on device.  HBM-bound streaming kernel: reads the int32
+// numerator (4 B) and writes tau_a/tau_b (8 + 8 B) per pair; per-row tie counts
+// stay in L2.
+//
+// Bit-exactness: tau_a = (double)num / (double)n0 and tau_b = (double)num /
+// sqrt((n0 - n1_y) * (n0 - n1_x)) with IEEE round-to-nearest __ddiv_rn /
+// __dsqrt_rn / __dmul_rn (no FMA contraction), exactly the operation sequence
+// numpy executes in derive_taus.
+#include "tb_common.cuh"
+
+namespace tb {
+
+__global__ void __launch_bounds__(256) finalize_kernel(const int32_t* __restrict__ num,
+                                                       const unsigned long long* __restrict__ n1, int64_t m,
+                                                       int64_t n0, int64_t job_lo, int64_t count,
+                                                       double* __restrict__ tau_a, double* __restrict__ tau_b) {
+    const double dn0 = (double)n0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = (double)num[i];
+        if (tau_a) tau_a[i] = __ddiv_rn(x, dn0);
+        if (tau_b) {
+            int64_t y, c;
+            job_coord(job_lo + i, m, y, c);
+            const double t1 = (double)n1[y], t2 = (double)n1[c];
+            const double denom = __dsqrt_rn(__dmul_rn(dn0 - t1, dn0 - t2));
+            tau_b[i] = denom > 0.0 ? __ddiv_rn(x, denom) : __longlong_as_double(0x7ff8000000000000LL);
+        }
+    }
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t job_lo,
+                           int64_t job_hi, double* tau_a, double* tau_b, void* stream) {
+    if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "finalize: need m >= 1, n >= 2");
+    const int64_t total = m * (m + 1) / 2;
+    if (job_lo < 0 || job_hi < job_lo || job_hi > total)
+        return fail(TB_ERR_CONFIG, "finalize: job range [%lld, %lld) outside [0, %lld)", (long long)job_lo,
+                    (long long)job_hi, (long long)total);
+    if (!num || !n1_rows) return fail(TB_ERR_INVALID, "finalize: null pointer");
+    const int64_t count = job_hi - job_lo;
+    if (count == 0) return TB_OK;
+    int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 16);
+    finalize_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        num, reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count, tau_a, tau_b);
+    return check_launch("finalize_kernel");
+}
+
+namespace tb {
+__global__ void __launch_bounds__(256) full_counts_kernel(const int32_t* __restrict__ num,
+                                                          const int32_t* __restrict__ absdot,
+                                                          const unsigned long long* __restrict__ n1, int64_t m,
+                                                          int64_t n0, int64_t job_lo, int64_t count,
+                                                          unsigned long long* __restrict__ nd,
+                                                          unsigned long long* __restrict__ n3) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = num[i], a = absdot[i];  // a = n_c + n_d, s = n_c - n_d
+        if (nd) nd[i] = (unsigned long long)((a - s) / 2);
+        if (n3) {
+            int64_t y, x;
+            job_coord(job_lo + i, m, y, x);
+            n3[i] = (unsigned long long)(a - n0 + (int64_t)n1[y] + (int64_t)n1[x]);
+        }
+    }
+}
+}  // namespace tb
+
+extern "C" int tb_full_counts(const int32_t* num, const int32_t* absdot, const uint64_t* n1_rows, int64_t m,
+                              int64_t n, int64_t job_lo, int64_t job_hi, uint64_t* nd, uint64_t* n3, void* stream) {
+    if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "full_counts: need m >= 1, n >= 2");
+    const int64_t total = m * (m + 1) / 2;
+    if (job_lo < 0 || job_hi < job_lo || job_hi > total) return fail(TB_ERR_CONFIG, "full_counts: bad job range");
+    if (!num || !absdot || !n1_rows) return fail(TB_ERR_INVALID, "full_counts: null pointer");
+    const int64_t count = job_hi - job_lo;
+    if (count == 0) return TB_OK;
+    int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 16);
+    full_counts_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        num, absdot, reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count,
+        reinterpret_cast<unsigned long long*>(nd), reinterpret_cast<unsigned long long*>(n3));
+    return check_launch("full_counts_kernel");
+}

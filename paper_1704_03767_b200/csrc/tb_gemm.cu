@@ -1,0 +1,342 @@
+// K3: the numerator GEMM num(y, x) = S_y . S_x on tcgen05 tensor cores.
+//
+// n_c - n_d = sum_{a<b} sign(u_b - u_a) sign(v_b - v_a) (kernel_naive.py:26-44)
+// is a dot product of the two rows' {-1,0,+1} sign vectors, so the all-pairs
+// numerator matrix is the SYRK S S^T over K = n(n-1)/2, exact in int32.
+//
+// Design (sm_100a):
+//  * logical 256 x 256 tiles over the upper triangle of the m x m pair matrix,
+//    numbered with the reference bijection (pairindex.py:58-65) and decoded on
+//    device (float sqrt + integer fix-up, tb::job_coord);
+//  * a work unit = (tile, 128-row half, K split); a persistent grid of one CTA
+//    per SM walks units with a static stride, split-major so concurrently
+//    running CTAs stream the same K-slab of S through L2;
+//  * warp 0: TMA producer (128-byte swizzled K-major boxes of S, 4-stage
+//    mbarrier ring, 48 KiB/stage); warp 1: single-thread tcgen05.mma.kind::i8
+//    issuer (M=128, N=256, K=32 per instruction) into a double-buffered TMEM
+//    accumulator (2 x 256 columns); warps 4-7: epilogue (tcgen05.ld -> masked
+//    store / red.add of the int32 numerator in job-id order);
+//  * split-K partials are integer, so atomic accumulation is deterministic.
+#include <algorithm>
+#include <cudaTypedefs.h>
+
+#include "tb_common.cuh"
+#include "tb_ptx.cuh"
+
+namespace tb {
+
+namespace gemm {
+constexpr int TILE = 256;  // logical square tile (pair-matrix rows x cols)
+constexpr int BM = 128;    // UMMA M (rows of one unit)
+constexpr int BN = 256;    // UMMA N
+constexpr int BK = 128;    // bytes of K per pipeline stage (= one 128B swizzle atom)
+constexpr int UK = 32;     // K per tcgen05.mma.kind::i8
+constexpr int STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK;
+constexpr uint32_t B_BYTES = BN * BK;
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 256;
+constexpr uint32_t TMEM_COLS = 512;  // two 128 x 256 int32 accumulators
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+}  // namespace gemm
+
+struct GemmArgs {
+    int64_t m;
+    int64_t w;        // tile-matrix width ceil(m / 256)
+    int64_t tile_lo;  // first tile id
+    int64_t ntiles;
+    int32_t splits;
+    int32_t nkb;      // K blocks of 128 bytes
+    int64_t job_lo, job_hi;
+    int32_t* num;
+    int32_t atomic;
+};
+
+struct Unit {
+    int64_t y0, x0;  // first pair-matrix row / column of the unit
+    int32_t kb0, kb1;
+};
+
+__device__ __forceinline__ Unit decode_unit(const GemmArgs& p, int64_t u) {
+    const int64_t per_split = p.ntiles * 2;
+    const int32_t s = (int32_t)(u / per_split);
+    const int64_t rem = u - (int64_t)s * per_split;
+    int64_t Y, X;
+    job_coord(p.tile_lo + (rem >> 1), p.w, Y, X);
+    Unit out;
+    out.y0 = Y * gemm::TILE + (rem & 1) * gemm::BM;
+    out.x0 = X * gemm::TILE;
+    out.kb0 = (int32_t)((int64_t)s * p.nkb / p.splits);
+    out.kb1 = (int32_t)((int64_t)(s + 1) * p.nkb / p.splits);
+    return out;
+}
+
+__global__ void __launch_bounds__(gemm::THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                   GemmArgs p) {
+    using namespace gemm;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmap_a);
+        tma_prefetch(&tmap_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int64_t nunits = p.ntiles * 2 * p.splits;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+                const Unit t = decode_unit(p, u);
+                for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                    uint8_t* sa = smem + stage * STAGE_BYTES;
+                    tma_load_2d(sa, &tmap_a, &full[stage], kb * BK, (int32_t)t.y0);
+                    tma_load_2d(sa + A_BYTES, &tmap_b, &full[stage], kb * BK, (int32_t)t.x0);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer (single thread)
+            constexpr uint32_t idesc = idesc_i8(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+                const Unit t = decode_unit(p, u);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+                    const uint64_t adesc = umma_desc_k_sw128(sa);
+                    const uint64_t bdesc = umma_desc_k_sw128(sa + A_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k) {
+                        // advance along K inside the 128B swizzle atom: +32 bytes = +2 in 16B units
+                        mma_i8(d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > t.kb0 || k > 0) ? 1u : 0u);
+                    }
+                    mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue (TMEM lane quadrant = warp % 4)
+        const int q = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        const int64_t m = p.m;
+        const int64_t span = p.job_hi - p.job_lo;
+        for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+            const Unit t = decode_unit(p, u);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t y = t.y0 + q * 32 + lane;
+            // J(y, x) - job_lo = base + x for x >= y
+            const int64_t base = row_prefix(y, m) - y - p.job_lo;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, r);
+                tmem_ld_wait();
+                if (y < m) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int64_t x = t.x0 + c + i;
+                        const int64_t j = base + x;
+                        if (x >= y && x < m && j >= 0 && j < span) {
+                            if (p.atomic)
+                                atomicAdd(&p.num[j], (int32_t)r[i]);
+                            else
+                                p.num[j] = (int32_t)r[i];
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+// ------------------------------------------------------------------ SIMT dp4a cross-check
+// 32 x 32 output block per CTA, K staged through shared memory 64 bytes at a time.
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const int8_t* __restrict__ S, int64_t m, int64_t K,
+                                                        int64_t ldS, int64_t job_lo, int64_t job_hi,
+                                                        int32_t* __restrict__ num) {
+    __shared__ int32_t sa[32][17];
+    __shared__ int32_t sb[32][17];
+    const int64_t Y0 = (int64_t)blockIdx.y * 32, X0 = (int64_t)blockIdx.x * 32;
+    if (X0 + 31 < Y0) return;  // strictly below the diagonal
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    int32_t acc[4] = {0, 0, 0, 0};
+    const int64_t kw = (K + 3) / 4;  // words; bytes past K are zero (sign_pack contract)
+    for (int64_t w0 = 0; w0 < kw; w0 += 16) {
+        for (int e = threadIdx.x; e < 32 * 16; e += 256) {
+            int rr = e >> 4, ww = e & 15;
+            int64_t word = w0 + ww;
+            int32_t va = 0, vb = 0;
+            if (word < kw) {
+                if (Y0 + rr < m) va = reinterpret_cast<const int32_t*>(S + (Y0 + rr) * ldS)[word];
+                if (X0 + rr < m) vb = reinterpret_cast<const int32_t*>(S + (X0 + rr) * ldS)[word];
+            }
+            sa[rr][ww] = va;
+            sb[rr][ww] = vb;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ww = 0; ww < 16; ++ww) {
+            const int32_t b = sb[tx][ww];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] = __dp4a(sa[ty + 8 * i][ww], b, acc[i]);
+        }
+        __syncthreads();
+    }
+    const int64_t x = X0 + tx;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t y = Y0 + ty + 8 * i;
+        if (y < m && x < m && x >= y) {
+            const int64_t j = row_prefix(y, m) + x - y;
+            if (j >= job_lo && j < job_hi) num[j - job_lo] = acc[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+static int make_tmap(CUtensorMap* map, const int8_t* S, int64_t m, int64_t K, int64_t ldS, uint32_t box_rows) {
+    auto enc = get_encode();
+    if (!enc) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)m};
+    cuuint64_t strides[1] = {(cuuint64_t)ldS};
+    cuuint32_t box[2] = {(cuuint32_t)gemm::BK, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(S), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return TB_OK;
+}
+
+static int check_job_args(int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi) {
+    if (m < 1 || K < 1) return fail(TB_ERR_INVALID, "gemm: need m >= 1 and K >= 1");
+    if (ldS < K || (ldS & 15)) return fail(TB_ERR_CONFIG, "gemm: ldS must be >= K and a multiple of 16");
+    const int64_t total = m * (m + 1) / 2;
+    if (job_lo < 0 || job_hi < job_lo || job_hi > total)
+        return fail(TB_ERR_CONFIG, "gemm: job range [%lld, %lld) outside [0, %lld)", (long long)job_lo,
+                    (long long)job_hi, (long long)total);
+    return TB_OK;
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
+                             int32_t splits, int32_t* num, void* stream) {
+    int rc = check_job_args(m, K, ldS, job_lo, job_hi);
+    if (rc) return rc;
+    if (!S || !num) return fail(TB_ERR_INVALID, "gemm: null pointer");
+    if (job_hi == job_lo) return TB_OK;
+    if (m > (int64_t)INT32_MAX - gemm::TILE) return fail(TB_ERR_CAPACITY, "gemm: m too large for TMA coordinates");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    GemmArgs p{};
+    p.m = m;
+    p.w = (m + gemm::TILE - 1) / gemm::TILE;
+    int64_t y_lo, x_lo, y_hi, x_hi;
+    job_coord(job_lo, m, y_lo, x_lo);
+    job_coord(job_hi - 1, m, y_hi, x_hi);
+    const int64_t Y0 = y_lo / gemm::TILE, Y1 = y_hi / gemm::TILE;
+    p.tile_lo = row_prefix(Y0, p.w);
+    p.ntiles = row_prefix(Y1 + 1, p.w) - p.tile_lo;
+    p.nkb = (int32_t)((K + gemm::BK - 1) / gemm::BK);
+    const int64_t units = p.ntiles * 2;
+    const int sms = num_sms();
+    if (splits <= 0) {
+        int64_t want = (units >= sms) ? 1 : (sms + units - 1) / units;
+        int64_t cap = std::max<int64_t>(1, p.nkb / 4);
+        splits = (int32_t)std::min<int64_t>(want, cap);
+    }
+    if (splits > p.nkb) splits = p.nkb;
+    p.splits = splits;
+    p.job_lo = job_lo;
+    p.job_hi = job_hi;
+    p.num = num;
+    p.atomic = splits > 1;
+    if (p.atomic) TB_CUDA_TRY(cudaMemsetAsync(num, 0, (job_hi - job_lo) * sizeof(int32_t), st));
+    CUtensorMap ta, tbm;
+    if ((rc = make_tmap(&ta, S, m, K, ldS, gemm::BM))) return rc;
+    if ((rc = make_tmap(&tbm, S, m, K, ldS, gemm::BN))) return rc;
+    TB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)gemm::SMEM_BYTES));
+    const int64_t nunits = units * splits;
+    const unsigned grid = (unsigned)std::min<int64_t>(nunits, sms);
+    gemm_tc_kernel<<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(ta, tbm, p);
+    return check_launch("gemm_tc_kernel");
+}
+
+extern "C" int tb_gemm_pairs_simt(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
+                                  int64_t job_hi, int32_t* num, void* stream) {
+    int rc = check_job_args(m, K, ldS, job_lo, job_hi);
+    if (rc) return rc;
+    if (!S || !num) return fail(TB_ERR_INVALID, "gemm_simt: null pointer");
+    if (job_hi == job_lo) return TB_OK;
+    const int64_t nb = (m + 31) / 32;
+    if (nb > 65535) return fail(TB_ERR_CAPACITY, "gemm_simt: m too large for the cross-check kernel");
+    dim3 grid((unsigned)nb, (unsigned)nb);
+    gemm_simt_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(S, m, K, ldS, job_lo, job_hi, num);
+    return check_launch("gemm_simt_kernel");
+}

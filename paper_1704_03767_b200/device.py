@@ -1,0 +1,231 @@
+"""Device-level all-pairs tau: the hot path, composed from the C-ABI kernels.
+
+``TauEngine.all_pairs(x)`` takes a [m, n] device tensor (raw values or dense
+ranks) and returns device tensors for one contiguous job-id range
+(pairindex.py:27-31 numbering, diagonal included):
+
+* GEMM path (small n):  K2 sign pack -> K3 tcgen05 int8 GEMM -> K5 finalize
+  (optionally the |S| GEMM + full counts for n_d / n3);
+* merge path (large n): K1 presort -> K4 Knight merge-inversion -> K5 finalize.
+
+Everything runs on the caller's current CUDA stream; nothing here touches the
+host except the optional ``validate()`` (one 4-byte flag read).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from .errors import CapacityExceededError, ConfigError, InvalidInputError
+
+# Dispatcher crossover (numerator kernel per shape).  The GEMM costs 2K = n(n-1)
+# int8 ops per pair at tensor-core rate; the merge costs ~4 n log2 n INT32 ops
+# per pair at CUDA-core rate -- SURVEY 7 step 5.  Above this n the sign matrix
+# is also too large to materialise (m * n^2 / 2 bytes).
+GEMM_MAX_N = 8192
+PATHS = ("gemm", "merge")
+
+
+def _ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream_ptr(stream: torch.cuda.Stream | None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.int32:
+        return _lib.TB_DTYPE_I32
+    if t.dtype == torch.float32:
+        return _lib.TB_DTYPE_F32
+    if t.dtype == torch.float64:
+        return _lib.TB_DTYPE_F64
+    raise InvalidInputError(f"unsupported value dtype {t.dtype}; use int32, float32 or float64")
+
+
+def row_prefix(y: int, m: int) -> int:
+    return y * (2 * m - y + 1) // 2
+
+
+@dataclass
+class PairResult:
+    """Per-pair device outputs for job ids [job_lo, job_hi)."""
+
+    m: int
+    n: int
+    job_lo: int
+    job_hi: int
+    path: str
+    numerator: torch.Tensor            # int32 [count]
+    n1_rows: torch.Tensor              # int64 [m] (tie pairs per variable; n2 of a pair is n1 of its x)
+    tau_a: torch.Tensor | None = None  # float64 [count]
+    tau_b: torch.Tensor | None = None  # float64 [count]
+    n_d: torch.Tensor | None = None    # int64 [count]
+    n3: torch.Tensor | None = None     # int64 [count]
+    flags: torch.Tensor | None = None  # int32 [1] device status (NaN / bad ranks)
+    launches: int = 0
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def count(self) -> int:
+        return self.job_hi - self.job_lo
+
+    def validate(self) -> "PairResult":
+        """Raise InvalidInputError if a kernel flagged the input (syncs the stream)."""
+        if self.flags is not None:
+            f = int(self.flags.item())
+            if f & 1:
+                raise InvalidInputError("observations contain NaN, which has no rank")
+            if f & 2:
+                raise InvalidInputError("ranks must be dense integers in [0, n)")
+        return self
+
+
+class TauEngine:
+    """Owns device workspaces; one instance per device/stream user."""
+
+    def __init__(self, device: int | torch.device | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("TauEngine needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   (device.index if isinstance(device, torch.device) else device))
+        _lib.load()
+        self.caps = _lib.query(self.device.index)
+        if not self.caps.tcgen05_i8:
+            raise RuntimeError(f"device cc {self.caps.cc_major}.{self.caps.cc_minor} is not sm_100 (B200)")
+        self._ws: dict[str, torch.Tensor] = {}
+        self._events = None
+        self._stream = None
+
+    # -------------------------------------------------------------- workspaces
+    def _buf(self, name: str, numel: int, dtype: torch.dtype) -> torch.Tensor:
+        t = self._ws.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(max(numel, 1), dtype=dtype, device=self.device)
+            self._ws[name] = t
+        return t[:numel]
+
+    def release(self):
+        self._ws.clear()
+
+    def _mark(self, which: int):
+        if self._events is not None:
+            self._events[which].record(self._stream)
+
+    @staticmethod
+    def choose_path(n: int) -> str:
+        return "gemm" if n <= GEMM_MAX_N else "merge"
+
+    # -------------------------------------------------------------- the hot path
+    def all_pairs(self, x: torch.Tensor, kernel: str = "auto", job_range: tuple[int, int] | None = None,
+                  tau_a: bool = True, tau_b: bool = True, full_counts: bool = False, splits: int = 0,
+                  stream: torch.cuda.Stream | None = None, simt: bool = False,
+                  _events: tuple | None = None) -> PairResult:
+        """All pairs of the job range.  ``_events=(start, end)`` brackets the numerator kernel
+        (GEMM or merge) with CUDA events on the launching stream (bench instrumentation)."""
+        if x.device.type != "cuda":
+            raise InvalidInputError("x must be a CUDA tensor (use the host API for numpy input)")
+        if x.dim() != 2:
+            raise InvalidInputError(f"values must be 2-D (variables x observations), got {x.dim()}-D")
+        m, n = x.shape
+        if m < 1 or n < 1:
+            raise InvalidInputError("dataset is empty")
+        if n < 2:
+            raise InvalidInputError("need at least two observations per variable")
+        if n > _lib.TB_MAX_N:
+            raise CapacityExceededError(f"n={n} exceeds the device limit {_lib.TB_MAX_N}")
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        total = m * (m + 1) // 2
+        job_lo, job_hi = (0, total) if job_range is None else (int(job_range[0]), int(job_range[1]))
+        if not 0 <= job_lo <= job_hi <= total:
+            raise ConfigError(f"job range [{job_lo}, {job_hi}) outside [0, {total})")
+        path = self.choose_path(n) if kernel == "auto" else kernel
+        if path not in PATHS:
+            raise ConfigError(f"unknown device path {kernel!r}, expected one of {PATHS + ('auto',)}")
+        st = _stream_ptr(stream)
+        self._events = _events
+        self._stream = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(self._stream):
+            return self._run(x, path, m, n, job_lo, job_hi, st, tau_a, tau_b, full_counts, splits, simt)
+
+    def _run(self, x, path, m, n, job_lo, job_hi, st, tau_a, tau_b, full_counts, splits, simt) -> PairResult:
+        count = job_hi - job_lo
+        dev = self.device
+        res = PairResult(m=m, n=n, job_lo=job_lo, job_hi=job_hi, path=path,
+                         numerator=torch.empty(count, dtype=torch.int32, device=dev),
+                         n1_rows=torch.empty(m, dtype=torch.int64, device=dev),
+                         flags=torch.zeros(1, dtype=torch.int32, device=dev))
+        if path == "gemm":
+            self._gemm_path(x, res, st, full_counts, splits, simt)
+        else:
+            self._merge_path(x, res, st)
+        if tau_a or tau_b:
+            res.tau_a = torch.empty(count, dtype=torch.float64, device=dev) if tau_a else None
+            res.tau_b = torch.empty(count, dtype=torch.float64, device=dev) if tau_b else None
+            _lib.call("tb_finalize", _ptr(res.numerator), _ptr(res.n1_rows), m, n, job_lo, job_hi,
+                      _ptr(res.tau_a), _ptr(res.tau_b), st)
+            res.launches += 1
+        return res
+
+    def _gemm_path(self, x, res: PairResult, st, full_counts: bool, splits: int, simt: bool):
+        m, n = res.m, res.n
+        K = n * (n - 1) // 2
+        ldS = (K + 15) // 16 * 16
+        S = self._buf("S", m * ldS, torch.int8)
+        _lib.call("tb_sign_pack", _ptr(x), _dtype_code(x), m, n, x.stride(0), _ptr(S), ldS,
+                  _ptr(res.n1_rows), _ptr(res.flags), st)
+        res.launches += 2
+        gemm = "tb_gemm_pairs_simt" if simt else "tb_gemm_pairs"
+        gargs = () if simt else (splits,)
+        self._mark(0)
+        _lib.call(gemm, _ptr(S), m, K, ldS, res.job_lo, res.job_hi, *gargs, _ptr(res.numerator), st)
+        self._mark(1)
+        res.launches += 1
+        if full_counts:
+            A = self._buf("A", m * ldS, torch.int8)
+            _lib.call("tb_abs_pack", _ptr(S), m, ldS, _ptr(A), st)
+            absdot = self._buf("absdot", res.count, torch.int32)
+            _lib.call(gemm, _ptr(A), m, K, ldS, res.job_lo, res.job_hi, *gargs, _ptr(absdot), st)
+            res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
+            res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
+            _lib.call("tb_full_counts", _ptr(res.numerator), _ptr(absdot), _ptr(res.n1_rows), m, n,
+                      res.job_lo, res.job_hi, _ptr(res.n_d), _ptr(res.n3), st)
+            res.launches += 3
+
+    def _merge_path(self, x, res: PairResult, st):
+        m, n = res.m, res.n
+        if x.dtype != torch.int32:
+            raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
+        x = x.contiguous()
+        pos = self._buf("pos", m * n, torch.int32)
+        srt = self._buf("sorted", m * n, torch.int32)
+        work = self._buf("work", m * n, torch.int32)
+        maxgrp = self._buf("maxgrp", m, torch.int32)
+        _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp),
+                  _ptr(work), _ptr(res.flags), st)
+        res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
+        res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
+        self._mark(0)
+        _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), m, n,
+                  res.job_lo, res.job_hi, _ptr(res.numerator), _ptr(res.n_d), _ptr(res.n3), st)
+        self._mark(1)
+        res.launches += 2
+
+
+_ENGINES: dict[int, TauEngine] = {}
+
+
+def get_engine(device: int | None = None) -> TauEngine:
+    idx = torch.cuda.current_device() if device is None else int(device)
+    eng = _ENGINES.get(idx)
+    if eng is None:
+        eng = TauEngine(idx)
+        _ENGINES[idx] = eng
+    return eng

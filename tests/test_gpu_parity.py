@@ -1,0 +1,289 @@
+"""GPU parity: the sm_100a path through the C ABI vs the oracle and the reference's golden vectors.
+
+Integers (numerator, n_d, n1, n2, n3) must match bit-exactly; tau_a / tau_b are
+compared with assert_array_equal (the IEEE finalize is bit-identical to the
+reference's derive_taus -- the north-star tolerance is 1e-12 absolute, and the
+tests assert the stronger 0-ulp bound, NaN where the reference has NaN).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_json, load_npz, random_rank_pair, split_pairs
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+TAU_ATOL = 1e-12  # north-star tolerance; the asserts below are exact
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_1704_03767_b200.device import TauEngine
+    return TauEngine(0)
+
+
+def _full_oracle(oracle, ranks, kernel=None):
+    m, n = ranks.shape
+    pi, pj = oracle.upper_pairs(m)
+    k = oracle.KERNEL_SORTED if kernel is None else kernel
+    num, counts = oracle.all_pairs(ranks, pi, pj, k, threads=8)
+    return pi, pj, num, counts
+
+
+def _check_full(res, oracle, ranks, full=True):
+    n = ranks.shape[1]
+    pi, pj, num, counts = _full_oracle(oracle, ranks)
+    lo, hi = res.job_lo, res.job_hi
+    got = res.numerator.cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(got, num[lo:hi])
+    n1 = res.n1_rows.cpu().numpy()
+    np.testing.assert_array_equal(n1[pi[lo:hi]], counts[lo:hi, 1])
+    np.testing.assert_array_equal(n1[pj[lo:hi]], counts[lo:hi, 2])
+    if full:
+        np.testing.assert_array_equal(res.n_d.cpu().numpy(), counts[lo:hi, 0])
+        np.testing.assert_array_equal(res.n3.cpu().numpy(), counts[lo:hi, 3])
+    ta, tb = oracle.derive_taus(num[lo:hi], counts[lo:hi, 1], counts[lo:hi, 2], n)
+    if res.tau_a is not None:
+        np.testing.assert_array_equal(res.tau_a.cpu().numpy(), ta)
+    if res.tau_b is not None:
+        np.testing.assert_array_equal(res.tau_b.cpu().numpy(), tb)
+
+
+@pytest.mark.parametrize("path", ["gemm", "merge"])
+@pytest.mark.parametrize("m,n,tie", [(1, 5, 0.0), (2, 2, 0.0), (3, 17, 0.5), (37, 33, 0.3), (130, 64, 0.0),
+                                     (257, 31, 0.9), (300, 130, 0.2)])
+def test_small_shapes_vs_oracle(eng, oracle, path, m, n, tie):
+    rng = np.random.default_rng(m * 1000 + n)
+    ranks = np.stack([oracle.rank_transform(random_rank_pair(rng, n, tie)[0]) for _ in range(m)])
+    res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel=path, full_counts=True).validate()
+    torch.cuda.synchronize()
+    _check_full(res, oracle, ranks)
+
+
+@pytest.mark.parametrize("path", ["gemm", "merge"])
+def test_constant_rows_nan(eng, oracle, path):
+    ranks = np.zeros((5, 40), np.int32)
+    ranks[1] = np.arange(40)
+    ranks[3] = np.arange(40)[::-1]
+    res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel=path, full_counts=True).validate()
+    tb = res.tau_b.cpu().numpy()
+    _check_full(res, oracle, ranks)
+    assert math.isnan(tb[0])  # (0, 0): constant vs constant
+
+
+def test_nan_rejected(eng):
+    from paper_1704_03767_b200 import InvalidInputError
+    x = torch.randn(4, 10, dtype=torch.float64, device="cuda")
+    x[2, 3] = float("nan")
+    with pytest.raises(InvalidInputError):
+        eng.all_pairs(x, kernel="gemm").validate()
+
+
+def test_bad_ranks_rejected_merge(eng):
+    from paper_1704_03767_b200 import InvalidInputError
+    x = torch.tensor([[0, 1, 7], [0, 1, 2]], dtype=torch.int32, device="cuda")
+    with pytest.raises(InvalidInputError):
+        eng.all_pairs(x, kernel="merge").validate()
+
+
+def test_kats_device(oracle):
+    import paper_1704_03767_b200 as tb
+    k = load_json("kats.json")
+    t = k["tied_example"]
+    r = tb.tau_b_sorted(t["u"], t["v"])
+    assert (r.n_d, r.n1, r.n2, r.n3, r.numerator) == (t["n_d"], t["n1"], t["n2"], t["n3"], t["numerator"])
+    assert r.tau_b == t["tau_b"] == 0.5
+    assert tb.tau_b_vectorized(t["u"], t["v"]).tau_b == 0.5
+    r = tb.tau_b_sorted(k["reversal4"]["u"], k["reversal4"]["v"])
+    assert r.n_d == 6 and r.numerator == -6 and r.tau_a == -1.0
+    assert tb.tau_a_naive([0, 1, 2, 3], [0, 1, 2, 3]).tau_a == 1.0
+    assert tb.tau_a_naive([0, 1, 2], [0, 2, 1]).numerator == 1
+    c = tb.tau_b_sorted([4, 4, 4, 4], [0, 1, 2, 3])
+    assert not c.defined_b and math.isnan(c.tau_b)
+    with pytest.raises(tb.InvalidInputError):
+        tb.tau_b_sorted([1, 2], [1])
+    with pytest.raises(tb.InvalidInputError):
+        tb.tau_b_sorted([1], [1])
+    with pytest.raises(tb.CapacityExceededError):
+        tb.tau_b_vectorized([0, 40000, 2], [0, 1, 2])
+
+
+def test_corpus_device_vs_reference():
+    """The reference acceptance corpus (1,000 pairs, rng 20240512), per-pair device API."""
+    import paper_1704_03767_b200 as tb
+    z = load_npz("corpus.npz")
+    for u, v, k in split_pairs(z):
+        r = tb.tau_b_sorted(u, v)
+        assert (r.n_d, r.n1, r.n2, r.n3, r.numerator) == tuple(z["counts"][k]), k
+        assert r.tau_a == z["tau_a"][k]
+        assert (math.isnan(r.tau_b) and math.isnan(z["tau_b"][k])) or r.tau_b == z["tau_b"][k]
+
+
+def test_boundary_device_vs_reference(eng):
+    """Boundary n in {15,16,17,31,32,33,32767} with ties, both device paths."""
+    z = load_npz("boundary.npz")
+    for u, v, k in split_pairs(z):
+        x = torch.from_numpy(np.stack([u, v])).cuda()
+        for path in ("merge", "gemm") if len(u) <= 4096 else ("merge",):
+            res = eng.all_pairs(x, kernel=path, job_range=(1, 2), full_counts=True).validate()
+            n1 = res.n1_rows.cpu().tolist()
+            got = (int(res.n_d.item()), n1[0], n1[1], int(res.n3.item()), int(res.numerator.item()))
+            assert got == tuple(z["counts"][k]), (path, len(u), k)
+            assert res.tau_a.item() == z["tau_a"][k]
+
+
+def _sampled_check(res, z, n):
+    pi, pj = z["pi"], z["pj"]
+    jid = pi * (2 * res.m - pi + 1) // 2 + pj - pi - res.job_lo
+    idx = torch.from_numpy(jid).cuda()
+    num = res.numerator.index_select(0, idx).cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(num, z["numerator"])
+    n1 = res.n1_rows.cpu().numpy()
+    np.testing.assert_array_equal(n1[pi], z["counts"][:, 1])
+    np.testing.assert_array_equal(n1[pj], z["counts"][:, 2])
+    if res.n_d is not None:
+        np.testing.assert_array_equal(res.n_d.index_select(0, idx).cpu().numpy(), z["counts"][:, 0])
+        np.testing.assert_array_equal(res.n3.index_select(0, idx).cpu().numpy(), z["counts"][:, 3])
+    ta = res.tau_a.index_select(0, idx).cpu().numpy()
+    tb = res.tau_b.index_select(0, idx).cpu().numpy()
+    np.testing.assert_array_equal(ta, z["tau_a"])
+    np.testing.assert_array_equal(tb, z["tau_b"])
+    assert np.nanmax(np.abs(tb - z["tau_b"])) <= TAU_ATOL if len(tb) else True
+
+
+def _diag_properties(res, n):
+    """Size-independent: every diagonal cell has numerator n0 - n1 (n_d = 0, n3 = n1)."""
+    m = res.m
+    y = torch.arange(m, device="cuda", dtype=torch.int64)
+    jd = y * (2 * m - y + 1) // 2 - res.job_lo
+    ok = (jd >= 0) & (jd < res.count)
+    n0 = n * (n - 1) // 2
+    d = res.numerator.index_select(0, jd[ok]).to(torch.int64)
+    assert torch.equal(d, n0 - res.n1_rows[ok])
+
+
+@pytest.mark.parametrize("path", ["gemm", "merge"])
+def test_config1_full(eng, oracle, path):
+    """Config 1 (256 x 200 f64 N(0,1)): every cell vs the reference engine's records."""
+    from paper_1704_03767_b200 import workloads
+    z = load_npz("config1.npz")
+    x = workloads.generate(1)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
+    xin = torch.from_numpy(x).cuda() if path == "gemm" else torch.from_numpy(oracle.rank_matrix(x)).cuda()
+    res = eng.all_pairs(xin, kernel=path, full_counts=True).validate()
+    _sampled_check(res, z, 200)
+    _diag_properties(res, 200)
+
+
+def test_config2_gemm_vs_golden_and_simt(eng):
+    """Config 2 (2048 x 1000, int 0..9): sampled golden pairs + every pair vs the dp4a cross-check."""
+    from paper_1704_03767_b200 import workloads
+    z = load_npz("config2.npz")
+    x = workloads.generate(2)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
+    xd = torch.from_numpy(x).cuda()
+    res = eng.all_pairs(xd, kernel="gemm", full_counts=True).validate()
+    _sampled_check(res, z, 1000)
+    _diag_properties(res, 1000)
+    ref = eng.all_pairs(xd, kernel="gemm", simt=True, tau_a=False, tau_b=False).validate()
+    assert torch.equal(res.numerator, ref.numerator)
+    # full-count identity: n_c + n_d + ties = n0 for every pair
+    n0 = 1000 * 999 // 2
+    m = 2048
+    pi, pj = np.triu_indices(m)
+    n1 = res.n1_rows
+    tot = (res.numerator.to(torch.int64) + 2 * res.n_d + n1[torch.from_numpy(pi).cuda()]
+           + n1[torch.from_numpy(pj).cuda()] - res.n3)
+    assert bool((tot == n0).all())
+
+
+@pytest.mark.parametrize("splits", [1, 2, 7])
+def test_gemm_splits_and_shards(eng, oracle, splits):
+    """K-split counts and contiguous job-id shards concatenate to the full result."""
+    from paper_1704_03767_b200.pairindex import job_shard_range
+    rng = np.random.default_rng(splits)
+    m, n = 600, 150
+    x = torch.from_numpy(rng.standard_normal((m, n)).astype(np.float32)).cuda()
+    full = eng.all_pairs(x, kernel="gemm", splits=splits).validate()
+    parts = [eng.all_pairs(x, kernel="gemm", job_range=job_shard_range(i, 5, m), splits=splits).validate()
+             for i in range(5)]
+    assert torch.equal(torch.cat([p.numerator for p in parts]), full.numerator)
+    assert torch.equal(torch.cat([p.tau_b for p in parts]), full.tau_b)
+    ranks = oracle.rank_matrix(x.cpu().numpy())
+    _check_full(full, oracle, ranks, full=False)
+
+
+def test_merge_shards(eng, oracle):
+    from paper_1704_03767_b200.pairindex import job_shard_range
+    rng = np.random.default_rng(5)
+    m, n = 40, 3000
+    ranks = np.stack([oracle.rank_transform(rng.integers(0, 2000, n)) for _ in range(m)])
+    x = torch.from_numpy(ranks).cuda()
+    full = eng.all_pairs(x, kernel="merge").validate()
+    parts = [eng.all_pairs(x, kernel="merge", job_range=job_shard_range(i, 3, m)).validate() for i in range(3)]
+    assert torch.equal(torch.cat([p.numerator for p in parts]), full.numerator)
+    _check_full(full, oracle, ranks)
+
+
+def test_config3_gemm_sampled(eng):
+    """Config 3 (16384 x 500 gene-like f32, ties): sampled pairs vs the reference."""
+    from paper_1704_03767_b200 import workloads
+    z = load_npz("config3.npz")
+    x = workloads.generate(3)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
+    res = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="gemm").validate()
+    _sampled_check(res, z, 500)
+    _diag_properties(res, 500)
+    eng.release()
+
+
+def test_config4_merge_sampled(eng, oracle):
+    """Config 4 (1024 x 65536, monotone family every 8th row): Knight merge path vs the reference."""
+    from paper_1704_03767_b200 import workloads
+    z = load_npz("config4.npz")
+    x = workloads.generate(4)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
+    rows = np.unique(np.concatenate([z["pi"], z["pj"]]))
+    ranks = np.zeros(x.shape, np.int32)
+    for r in rows:
+        ranks[r] = oracle.rank_transform(x[r])
+    np.testing.assert_array_equal(ranks[:4], z["ranks_head"])
+    # only the sampled rows are ranked: compute exactly the sampled job ids' rows
+    xd = torch.from_numpy(ranks).cuda()
+    m = x.shape[0]
+    pi, pj = z["pi"], z["pj"]
+    jid = pi * (2 * m - pi + 1) // 2 + pj - pi
+    for k in np.argsort(jid)[:40]:
+        j = int(jid[k])
+        res = eng.all_pairs(xd, kernel="merge", job_range=(j, j + 1)).validate()
+        assert int(res.numerator.item()) == int(z["numerator"][k])
+        assert int(res.n_d.item()) == int(z["counts"][k, 0])
+        assert int(res.n3.item()) == int(z["counts"][k, 3])
+        assert res.tau_b.item() == z["tau_b"][k] or (math.isnan(res.tau_b.item()) and math.isnan(z["tau_b"][k]))
+    eng.release()
+
+
+@pytest.mark.timeout(900)
+def test_config5_gemm_sampled(eng):
+    """Config 5 (65536 x 1024 low-rank f32, 2.15e9 pairs): sampled pairs vs the reference."""
+    from paper_1704_03767_b200 import workloads
+    z = load_npz("config5.npz")
+    x = workloads.generate(5)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
+    res = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="gemm", tau_a=False).validate()
+    pi, pj = z["pi"], z["pj"]
+    m = x.shape[0]
+    jid = torch.from_numpy(pi * (2 * m - pi + 1) // 2 + pj - pi).cuda()
+    np.testing.assert_array_equal(res.numerator.index_select(0, jid).cpu().numpy(), z["numerator"])
+    np.testing.assert_array_equal(res.tau_b.index_select(0, jid).cpu().numpy(), z["tau_b"])
+    _diag_properties(res, 1024)
+    del res
+    eng.release()
+    torch.cuda.empty_cache()

@@ -1,0 +1,151 @@
+"""CPU-only tests: host geometry vs the reference's golden vectors, engine validation,
+record-order planning, and the C-ABI symbol table (no compute calls without a GPU)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_json, load_npz
+
+
+def test_bijection_kats():
+    import paper_1704_03767_b200 as tb
+    k = load_json("kats.json")["bijection"]
+    assert tb.job_id(2, 3, 4) == k["job_id_2_3_4"] == 8
+    assert list(tb.job_coord(5, 4)) == k["job_coord_5_4"] == [1, 2]
+    assert tb.tile_id(1, 2, 3) == k["tile_id_1_2_3"] == 4
+    for m, q, p, ranges in k["shard_ranges"]:
+        space = tb.JobSpace(m, q)
+        assert [list(tb.shard_range(i, p, space)) for i in range(p)] == ranges
+
+
+def test_bijection_exhaustive_and_sampled():
+    import paper_1704_03767_b200 as tb
+    for m in range(1, 120):
+        j = 0
+        for y in range(m):
+            for x in range(y, m):
+                assert tb.job_id(y, x, m) == j
+                assert tb.job_coord(j, m) == (y, x)
+                j += 1
+    z = load_npz("bijection.npz")
+    for key in z.files:
+        if key.endswith("_j"):
+            m = int(key[1:-2])
+            for j, yx in zip(z[key].tolist(), z[key[:-2] + "_yx"].tolist()):
+                assert tb.job_coord(j, m) == tuple(yx)
+
+
+def test_vectorised_tile_order_matches_tile_cells():
+    import paper_1704_03767_b200 as tb
+    for m in (1, 2, 7, 13, 40):
+        for q in (1, 2, 3, 8, 9):
+            space = tb.JobSpace(m, q)
+            expected = []
+            for t in range(space.total_tiles):
+                expected.extend(space.tile_cells(*tb.tile_coord(t, space.w)))
+            ii, jj = space.cells_in_tile_order(0, space.total_tiles)
+            assert list(zip(ii.tolist(), jj.tolist())) == expected
+            assert len(expected) == m * (m + 1) // 2
+
+
+def test_plan_passes_exact():
+    import paper_1704_03767_b200 as tb
+    space = tb.JobSpace(m=4, q=1)
+    plans = tb.plan_passes(space, (0, 10), 4)
+    assert [(p.tile_lo, p.tile_hi) for p in plans] == [(0, 4), (4, 8), (8, 10)]
+    space = tb.JobSpace(m=23, q=4)
+    for pass_tiles in (1, 3, 7):
+        plans = tb.plan_passes(space, (0, space.total_tiles), pass_tiles)
+        for p in plans:
+            assert p.cells == sum(space.tile_cell_count(*tb.tile_coord(t, space.w))
+                                  for t in range(p.tile_lo, p.tile_hi))
+    with pytest.raises(tb.ConfigError):
+        tb.plan_passes(space, (0, 10), 0)
+
+
+def test_job_shards_partition():
+    import paper_1704_03767_b200 as tb
+    for m in (1, 5, 100, 65536):
+        for p in (1, 2, 3, 8):
+            rs = [tb.job_shard_range(i, p, m) for i in range(p)]
+            assert rs[0][0] == 0 and rs[-1][1] == m * (m + 1) // 2
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+def test_engine_config_errors_before_device():
+    import paper_1704_03767_b200 as tb
+    ds = tb.synth_dataset(4, 6, seed=9)
+    for kw in [dict(kernel="fancy"), dict(workers=0), dict(tile_size=0), dict(pass_tiles=0), dict(shard=(2, 2))]:
+        kernel = kw.pop("kernel", "sorted")
+        with pytest.raises(tb.ConfigError):
+            tb.compute_all_pairs(ds, kernel, **kw)
+    with pytest.raises(tb.InvalidInputError):
+        tb.compute_all_pairs(tb.Dataset(labels=["a", "b"], ranks=np.zeros((2, 1), np.int32)), "sorted")
+    with pytest.raises(tb.InvalidInputError):
+        tb.Dataset(labels=["a", "a"], ranks=np.zeros((2, 3), np.int32))
+    with pytest.raises(tb.InvalidInputError):
+        tb.Dataset(labels=[], ranks=np.zeros((0, 3), np.int32))
+
+
+def test_rank_and_pack_kats():
+    import paper_1704_03767_b200 as tb
+    for vals, expected in load_json("kats.json")["rank_transform"]:
+        assert tb.rank_transform(np.array(vals)).tolist() == expected
+    with pytest.raises(tb.InvalidInputError):
+        tb.rank_transform([1.0, float("nan")])
+    p = tb.pack_pairs([1, 2], [3, 4])
+    u, v = tb.unpack_pairs(p)
+    assert u.tolist() == [1, 2] and v.tolist() == [3, 4]
+    with pytest.raises(tb.CapacityExceededError):
+        tb.pack_pairs([0, 1 << 15], [0, 1])
+
+
+def test_record_writers_roundtrip():
+    import io
+    import paper_1704_03767_b200 as tb
+    rec = np.zeros(3, tb.CELL_DTYPE)
+    rec["i"] = [0, 0, 1]
+    rec["j"] = [0, 1, 1]
+    rec["numerator"] = [6, -2, 0]
+    rec["n1"] = [0, 0, 6]
+    rec["n2"] = [0, 6, 6]
+    s = io.BytesIO()
+    tb.BinaryWriter(s, 4)(rec)
+    back, ta, tbb = tb.read_binary(io.BytesIO(s.getvalue()), 4)
+    assert np.isnan(tbb[1]) and np.isnan(tbb[2]) and tbb[0] == 1.0
+
+
+def _header_symbols():
+    with open(os.path.join(ROOT, "include", "taub200.h")) as fh:
+        txt = fh.read()
+    return set(re.findall(r"^(?:int|const char \*)\s*(tb_\w+)\(", txt, re.M))
+
+
+def test_capi_exports_every_declared_symbol():
+    from paper_1704_03767_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libtaub200.so not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    declared = _header_symbols()
+    assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
+    for name in declared:
+        assert hasattr(lib, name), name
+    loaded = _lib.load()
+    assert loaded.tb_last_error() is not None
+
+
+def test_no_oracle_in_product_path():
+    """The package must not import the oracle (the checker) anywhere."""
+    pkg = os.path.join(ROOT, "paper_1704_03767_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                with open(os.path.join(dirpath, f)) as fh:
+                    src = fh.read()
+                assert "import oracle" not in src and "tau_oracle" not in src and "libtauoracle" not in src, f
