@@ -70,13 +70,18 @@ int tb_query(int device, tb_caps *caps);
  *   x     [m, ldx] values (TB_DTYPE_*), compared directly: the sign of a rank
  *         difference equals the sign of the value difference for the dense
  *         ranks of rank_transform (src/taucorr/ranks.py:37-61).
- *   S     [m, ldS] int8, S[r, k(a,b)] = sign(x[r,b] - x[r,a]) for a < b, with
- *         k(a,b) = a*n - a(a+1)/2 + (b - a - 1); bytes [K, ldS) are zeroed.
- *         ldS must be a multiple of 16 and >= K = n(n-1)/2.
+ *   S     [m, ldS] int8 in the "diagonal" sample-pair order: pairs (a, a+d)
+ *         grouped by offset d = 1..n-1, each d-segment n-d signs long and
+ *         zero-padded to a multiple of 16 bytes:
+ *           S[r, off(d) + a] = sign(x[r, a+d] - x[r, a]),
+ *           off(d) = 16 * sum_{d'<d} ceil((n - d') / 16).
+ *         K = tb_sign_k(n) (>= n(n-1)/2); bytes [K, ldS) are zeroed; ldS must
+ *         be a multiple of 16 and >= K.  Padding zeros add nothing to S_u.S_v.
  *   n1    [m] uint64 per-row tied-pair count n1 = n0 - sum_k |S[r,k]|.
  *   flags device int32; bit 0 is set when a NaN was seen (NaN has no rank,
  *         ranks.py:56-57); the caller raises InvalidInputError.
  */
+int64_t tb_sign_k(int64_t n);
 int tb_sign_pack(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, int8_t *S, int64_t ldS,
                  uint64_t *n1, int32_t *flags, void *stream);
 

@@ -18,6 +18,8 @@
 //    store / red.add of the int32 numerator in job-id order);
 //  * split-K partials are integer, so atomic accumulation is deterministic.
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 #include <cudaTypedefs.h>
 
 #include "tb_common.cuh"
@@ -200,6 +202,198 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
     }
 }
 
+
+// ============================================================================ K3 v2: 2-SM pairs
+// A CTA pair (cluster of 2, tcgen05 cta_group::2) owns a 256-row x 512-column unit of the pair
+// matrix: M = 256 split across the two CTAs (128 rows of A each), N = 512 issued as two N=256 MMAs
+// into TMEM columns [0,256) and [256,512); each CTA stages only its 128-row half of each N block,
+// so per SM the operand traffic per MMA is half of the 1-SM kernel's (L2-bandwidth relief).
+// Units are (512 x 512 tile of the upper triangle, 256-row half); the host orders them in
+// 2048 x 2048 super-tiles (L2 reuse across the concurrently running pairs) and the device decodes
+// each tile id with the reference bijection (tb::job_coord).  N blocks lying entirely below the
+// diagonal are skipped (no load, no MMA).
+namespace gemm2 {
+constexpr int TILE = 512;
+constexpr int UM = 256;       // pair M
+constexpr int BM = 128;       // rows of A per CTA
+constexpr int BN = 256;       // N per MMA
+constexpr int BNH = 128;      // rows of B per CTA per N block
+constexpr int BK = 128;
+constexpr int UK = 32;
+constexpr int STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK;        // 16 KiB
+constexpr uint32_t B_BYTES = BNH * BK;       // 16 KiB per N block
+constexpr uint32_t STAGE_BYTES = A_BYTES + 2 * B_BYTES;
+constexpr int THREADS = 256;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+}  // namespace gemm2
+
+struct Gemm2Args {
+    int64_t m;
+    int64_t w;             // 512-tile matrix width
+    const int32_t* units;  // tile_id * 2 + half, rasterised
+    int64_t nunits;        // per split
+    int32_t splits;
+    int32_t nkb;
+    int64_t job_lo, job_hi;
+    int32_t* num;
+    int32_t atomic;
+};
+
+struct Unit2 {
+    int64_t y0, x0;   // pair rows y0..y0+255, columns x0..x0+511
+    int32_t h_lo;     // first N block needed (1 if block 0 is entirely below the diagonal)
+    int32_t kb0, kb1;
+};
+
+__device__ __forceinline__ Unit2 decode_unit2(const Gemm2Args& p, int64_t u) {
+    const int32_t s = (int32_t)(u / p.nunits);
+    const int64_t i = u - (int64_t)s * p.nunits;
+    const int32_t e = p.units[i];
+    int64_t Y, X;
+    job_coord(e >> 1, p.w, Y, X);
+    Unit2 o;
+    o.y0 = Y * gemm2::TILE + (e & 1) * gemm2::UM;
+    o.x0 = X * gemm2::TILE;
+    o.h_lo = (o.x0 + gemm2::BN - 1 < o.y0) ? 1 : 0;
+    o.kb0 = (int32_t)((int64_t)s * p.nkb / p.splits);
+    o.kb1 = (int32_t)((int64_t)(s + 1) * p.nkb / p.splits);
+    return o;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap, Gemm2Args p) {
+    using namespace gemm2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int64_t pair = blockIdx.x >> 1;
+    const int64_t npairs = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmap);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 8);  // 4 epilogue warps x 2 CTAs
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int64_t total = p.nunits * p.splits;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t u = pair; u < total; u += npairs) {
+                const Unit2 t = decode_unit2(p, u);
+                const uint32_t bytes = 2 * (A_BYTES + (2 - t.h_lo) * B_BYTES);
+                for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
+                    const uint32_t fb = mapa_shared(&full[stage], 0);
+                    uint8_t* sa = smem + stage * STAGE_BYTES;
+                    tma_load_2d_2sm(sa, &tmap, fb, kb * BK, (int32_t)(t.y0 + rank * BM));
+                    for (int h = t.h_lo; h < 2; ++h)
+                        tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap, fb, kb * BK,
+                                        (int32_t)(t.x0 + h * BN + rank * BNH));
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {  // ---------------- MMA issuer (leader CTA, one thread)
+            constexpr uint32_t idesc = idesc_i8(UM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t u = pair; u < total; u += npairs) {
+                const Unit2 t = decode_unit2(p, u);
+                mbar_wait(tempty, acc_phase ^ 1);
+                tc_fence_after();
+                for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+                    const uint64_t adesc = umma_desc_k_sw128(sa);
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k) {
+                        const uint32_t acc = (kb > t.kb0 || k > 0) ? 1u : 0u;
+                        for (int h = t.h_lo; h < 2; ++h) {
+                            const uint64_t bdesc = umma_desc_k_sw128(sa + A_BYTES + h * B_BYTES);
+                            mma_i8_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+                        }
+                    }
+                    mma_commit_2sm(&empty[stage], 0x3);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit_2sm(tfull, 0x3);
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue (both CTAs)
+        const int q = warp & 3;
+        uint32_t acc_phase = 0;
+        const int64_t m = p.m;
+        const int64_t span = p.job_hi - p.job_lo;
+        const uint32_t tempty_leader = mapa_shared(tempty, 0);
+        for (int64_t u = pair; u < total; u += npairs) {
+            const Unit2 t = decode_unit2(p, u);
+            mbar_wait(tfull, acc_phase);
+            tc_fence_after();
+            const int64_t y = t.y0 + rank * BM + q * 32 + lane;
+            const int64_t base = row_prefix(y, m) - y - p.job_lo;
+            for (int h = t.h_lo; h < 2; ++h) {
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + h * BN + c, r);
+                    tmem_ld_wait();
+                    if (y < m) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int64_t x = t.x0 + h * BN + c + i;
+                            const int64_t j = base + x;
+                            if (x >= y && x < m && j >= 0 && j < span) {
+                                if (p.atomic)
+                                    atomicAdd(&p.num[j], (int32_t)r[i]);
+                                else
+                                    p.num[j] = (int32_t)r[i];
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader);
+            acc_phase ^= 1;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+    }
+}
+
 // ------------------------------------------------------------------ SIMT dp4a cross-check
 // 32 x 32 output block per CTA, K staged through shared memory 64 bytes at a time.
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const int8_t* __restrict__ S, int64_t m, int64_t K,
@@ -281,6 +475,109 @@ static int check_job_args(int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int
     return TB_OK;
 }
 
+
+// Rasterised unit table for the 2-SM kernel: (tile id on the 512-tile matrix) * 2 + half, ordered
+// by 4 x 4 super-tiles, row-halves outer, so ~74 concurrently running pairs share A and B rows
+// through L2.  Cached per (m, job range).
+struct UnitTable {
+    int64_t m = -1, lo = -1, hi = -1;
+    int32_t* dev = nullptr;
+    int64_t count = 0, cap = 0;
+};
+static UnitTable g_units;
+
+static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t st, const int32_t** out,
+                       int64_t* count) {
+    if (g_units.m == m && g_units.lo == job_lo && g_units.hi == job_hi) {
+        *out = g_units.dev;
+        *count = g_units.count;
+        return TB_OK;
+    }
+    const int64_t T = gemm2::TILE, G = 4;
+    const int64_t w = (m + T - 1) / T;
+    const int64_t W = (w + G - 1) / G;
+    int64_t y_lo, x_lo, y_hi, x_hi;
+    job_coord(job_lo, m, y_lo, x_lo);
+    job_coord(job_hi - 1, m, y_hi, x_hi);
+    std::vector<int32_t> v;
+    for (int64_t SY = 0; SY < W; ++SY)
+        for (int64_t SX = SY; SX < W; ++SX)
+            for (int64_t LY = 0; LY < G; ++LY)
+                for (int64_t r = 0; r < 2; ++r)
+                    for (int64_t LX = 0; LX < G; ++LX) {
+                        const int64_t Y = SY * G + LY, X = SX * G + LX;
+                        if (Y > X || X >= w) continue;
+                        const int64_t r0 = Y * T + r * gemm2::UM;
+                        if (r0 >= m) continue;
+                        const int64_t r1 = std::min(r0 + gemm2::UM, m) - 1;  // last row of the unit
+                        if (r1 < y_lo || r0 > y_hi) continue;                 // outside the job range rows
+                        if (X * T + T - 1 < r0) continue;                      // entirely below the diagonal
+                        const int64_t tid = row_prefix(Y, w) + X - Y;
+                        if (tid * 2 + 1 > INT32_MAX) return fail(TB_ERR_CAPACITY, "gemm: too many tiles");
+                        v.push_back((int32_t)(tid * 2 + r));
+                    }
+    if ((int64_t)v.size() > g_units.cap) {
+        if (g_units.dev) cudaFree(g_units.dev);
+        g_units.dev = nullptr;
+        TB_CUDA_TRY(cudaMalloc(&g_units.dev, std::max<size_t>(v.size(), 1) * sizeof(int32_t)));
+        g_units.cap = (int64_t)v.size();
+    }
+    if (!v.empty())
+        TB_CUDA_TRY(cudaMemcpyAsync(g_units.dev, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    TB_CUDA_TRY(cudaStreamSynchronize(st));  // v is pageable and dies here
+    g_units.m = m;
+    g_units.lo = job_lo;
+    g_units.hi = job_hi;
+    g_units.count = (int64_t)v.size();
+    *out = g_units.dev;
+    *count = g_units.count;
+    return TB_OK;
+}
+
+// Split-K choice: minimise waves(U*s / pairs) * (nkb/s * t_kb + t_epi).
+static int32_t pick_splits(int64_t units, int32_t nkb, int pairs) {
+    const double t_kb = 1.0, t_epi = 40.0;  // k-block of the 2-SM kernel ~0.5 us; epilogue ~20 us
+    int32_t best = 1;
+    double best_t = 1e300;
+    for (int32_t s = 1; s <= std::max(1, nkb / 8) && s <= 64; ++s) {
+        const int64_t waves = (units * s + pairs - 1) / pairs;
+        const double t = waves * ((double)nkb / s * t_kb + t_epi + (s > 1 ? t_epi : 0.0));
+        if (t < best_t * 0.999) { best_t = t; best = s; }
+    }
+    return best;
+}
+
+static int gemm_v2(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
+                   int32_t splits, int32_t* num, cudaStream_t st) {
+    int rc;
+    const int32_t* units = nullptr;
+    int64_t nunits = 0;
+    if ((rc = build_units(m, job_lo, job_hi, st, &units, &nunits))) return rc;
+    Gemm2Args p{};
+    p.m = m;
+    p.w = (m + gemm2::TILE - 1) / gemm2::TILE;
+    p.units = units;
+    p.nunits = nunits;
+    p.nkb = (int32_t)((K + gemm2::BK - 1) / gemm2::BK);
+    const int pairs = std::max(1, num_sms() / 2);
+    if (splits <= 0) splits = pick_splits(nunits, p.nkb, pairs);
+    if (splits > p.nkb) splits = p.nkb;
+    p.splits = splits;
+    p.job_lo = job_lo;
+    p.job_hi = job_hi;
+    p.num = num;
+    p.atomic = splits > 1;
+    if (p.atomic) TB_CUDA_TRY(cudaMemsetAsync(num, 0, (job_hi - job_lo) * sizeof(int32_t), st));
+    CUtensorMap tm;
+    if ((rc = make_tmap(&tm, S, m, K, ldS, gemm2::BM))) return rc;
+    TB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)gemm2::SMEM_BYTES));
+    const int64_t work = nunits * splits;
+    const unsigned grid = (unsigned)(2 * std::min<int64_t>(work, pairs));
+    gemm_tc2_kernel<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(tm, p);
+    return check_launch("gemm_tc2_kernel");
+}
+
 }  // namespace tb
 
 using namespace tb;
@@ -293,6 +590,8 @@ extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS,
     if (job_hi == job_lo) return TB_OK;
     if (m > (int64_t)INT32_MAX - gemm::TILE) return fail(TB_ERR_CAPACITY, "gemm: m too large for TMA coordinates");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const char* variant = std::getenv("TB_GEMM_VARIANT");
+    if (!(variant && variant[0] == '1')) return gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, num, st);
     GemmArgs p{};
     p.m = m;
     p.w = (m + gemm::TILE - 1) / gemm::TILE;

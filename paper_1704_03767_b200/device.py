@@ -176,7 +176,7 @@ class TauEngine:
 
     def _gemm_path(self, x, res: PairResult, st, full_counts: bool, splits: int, simt: bool):
         m, n = res.m, res.n
-        K = n * (n - 1) // 2
+        K = int(_lib.load().tb_sign_k(n))  # padded diagonal layout, >= n(n-1)/2
         ldS = (K + 15) // 16 * 16
         S = self._buf("S", m * ldS, torch.int8)
         _lib.call("tb_sign_pack", _ptr(x), _dtype_code(x), m, n, x.stride(0), _ptr(S), ldS,

@@ -124,7 +124,7 @@ def test_record_writers_roundtrip():
 def _header_symbols():
     with open(os.path.join(ROOT, "include", "taub200.h")) as fh:
         txt = fh.read()
-    return set(re.findall(r"^(?:int|const char \*)\s*(tb_\w+)\(", txt, re.M))
+    return set(re.findall(r"^(?:int|int64_t|const char \*)\s*(tb_\w+)\(", txt, re.M))
 
 
 def test_capi_exports_every_declared_symbol():
