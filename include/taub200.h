@@ -63,27 +63,31 @@ const char *tb_last_error(void);
 int tb_query(int device, tb_caps *caps);
 
 /*
- * K2 sign pack.  Replaces the per-pair sign enumeration of
- * naive_numerator (src/taucorr/kernel_naive.py:26-44) and the per-pair tie
- * scans for n1/n2 (src/taucorr/kernel_sorted.py:163-176).
- *
- *   x     [m, ldx] values (TB_DTYPE_*), compared directly: the sign of a rank
- *         difference equals the sign of the value difference for the dense
- *         ranks of rank_transform (src/taucorr/ranks.py:37-61).
+ * K0 rank transform (rank_transform, src/taucorr/ranks.py:37-61, for all rows
+ * at once): dense 0-based ranks, ties share a rank, -0.0 == +0.0.
+ *   x     [m, ldx] values (TB_DTYPE_*), n <= 8192 (the GEMM path)
+ *   R     [m, ldr] uint16 ranks out (ldr >= n, multiple of 8; [n, ldr) zeroed)
+ *   n1    [m] uint64 per-row tied-pair count sum_t t(t-1)/2 (kernel_sorted.py:163-176)
+ *   flags device int32; bit 0 is set when a NaN was seen (ranks.py:56-57)
+ */
+int tb_rank_rows(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, uint16_t *R, int64_t ldr,
+                 uint64_t *n1, int32_t *flags, void *stream);
+
+/*
+ * K2 sign pack.  Replaces the per-pair sign enumeration of naive_numerator
+ * (src/taucorr/kernel_naive.py:26-44), materialising each variable's sign
+ * vector once.
+ *   R     [m, ldr] uint16 dense ranks (< 2^15; tb_rank_rows output), ldr even
  *   S     [m, ldS] int8 in the "diagonal" sample-pair order: pairs (a, a+d)
  *         grouped by offset d = 1..n-1, each d-segment n-d signs long and
  *         zero-padded to a multiple of 16 bytes:
- *           S[r, off(d) + a] = sign(x[r, a+d] - x[r, a]),
+ *           S[r, off(d) + a] = sign(R[r, a+d] - R[r, a]),
  *           off(d) = 16 * sum_{d'<d} ceil((n - d') / 16).
  *         K = tb_sign_k(n) (>= n(n-1)/2); bytes [K, ldS) are zeroed; ldS must
  *         be a multiple of 16 and >= K.  Padding zeros add nothing to S_u.S_v.
- *   n1    [m] uint64 per-row tied-pair count n1 = n0 - sum_k |S[r,k]|.
- *   flags device int32; bit 0 is set when a NaN was seen (NaN has no rank,
- *         ranks.py:56-57); the caller raises InvalidInputError.
  */
 int64_t tb_sign_k(int64_t n);
-int tb_sign_pack(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, int8_t *S, int64_t ldS,
-                 uint64_t *n1, int32_t *flags, void *stream);
+int tb_sign_pack(const uint16_t *R, int64_t m, int64_t n, int64_t ldr, int8_t *S, int64_t ldS, void *stream);
 
 /*
  * K3 numerator GEMM on tcgen05 tensor cores (kind::i8, TMA-fed, TMEM

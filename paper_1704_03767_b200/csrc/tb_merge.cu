@@ -126,9 +126,40 @@ __global__ void __launch_bounds__(PS_THREADS) presort_kernel(const int32_t* __re
 constexpr int MG_THREADS = 1024;
 constexpr int MG_HALF = 32768;  // largest block sorted in shared memory
 
-// Merge sort keys[0, L) (L power of two) with ping-pong buffer tmp[0, L),
-// returning this thread's share of the strict inversion count.  Result ends
-// in keys.
+// Shared-memory key index swizzle: merge-path threads own contiguous output segments, which would
+// put every lane of a warp in the same two banks (16-way conflicts).  XOR-ing the low five bits of
+// the 32-bit word index with the next five spreads a warp's segments over all 32 banks; the map is
+// a bijection on every aligned 64-key block.
+__device__ __forceinline__ int sw(int e) {
+    const int w = e >> 1;
+    return ((w ^ ((w >> 5) & 31)) << 1) | (e & 1);
+}
+
+// Branch-free sequential merge of `count` outputs of the runs A = src[s, s+W), B = src[s+W, s+2W)
+// starting from (i, j); returns the strict-inversion contribution (kernel_sorted.py:72-73 rule:
+// a right element strictly smaller than the left head adds the unconsumed left length).
+__device__ __forceinline__ uint32_t merge_seq(const uint16_t* src, uint16_t* dst, int s, int W, int i, int j,
+                                              int out0, int count) {
+    uint32_t inv = 0;
+    uint32_t a = i < W ? src[sw(s + i)] : 0u;
+    uint32_t b = j < W ? src[sw(s + W + j)] : 0u;
+    for (int o = 0; o < count; ++o) {
+        const bool takeA = (j >= W) || ((i < W) && (a <= b));
+        dst[sw(out0 + o)] = (uint16_t)(takeA ? a : b);
+        inv += takeA ? 0u : (uint32_t)(W - i);
+        i += takeA;
+        j += !takeA;
+        const int idx = takeA ? (s + i) : (s + W + j);
+        const bool ok = takeA ? (i < W) : (j < W);
+        const uint32_t v = ok ? src[sw(idx)] : 0u;
+        a = takeA ? v : a;
+        b = takeA ? b : v;
+    }
+    return inv;
+}
+
+// Merge sort keys[0, L) (L power of two) with ping-pong buffer tmp[0, L), returning this thread's
+// share of the strict inversion count.  Result ends in keys.  All indices are logical (swizzled).
 __device__ uint32_t sort_count_block(uint16_t* keys, uint16_t* tmp, int L) {
     uint32_t inv = 0;
     uint16_t* src = keys;
@@ -141,48 +172,17 @@ __device__ uint32_t sort_count_block(uint16_t* keys, uint16_t* tmp, int L) {
             const int d0 = threadIdx.x * E;
             const int P = 2 * W;
             if (P <= E) {
-                // whole merge pairs per thread
-                for (int s = d0; s < d0 + E; s += P) {
-                    const uint16_t* A = src + s;
-                    const uint16_t* B = src + s + W;
-                    int i = 0, j = 0;
-                    for (int o = 0; o < P; ++o) {
-                        bool takeA = (j >= W) || (i < W && A[i] <= B[j]);
-                        if (takeA) {
-                            dst[s + o] = A[i++];
-                        } else {
-                            dst[s + o] = B[j++];
-                            inv += (uint32_t)(W - i);
-                        }
-                    }
-                }
+                for (int s = d0; s < d0 + E; s += P) inv += merge_seq(src, dst, s, W, 0, 0, s, P);
             } else {
                 const int s = (d0 / P) * P;  // pair start
                 const int d = d0 - s;        // diagonal inside the pair
-                const uint16_t* A = src + s;
-                const uint16_t* B = src + s + W;
                 int lo = d > W ? d - W : 0, hi = d < W ? d : W;
                 while (lo < hi) {  // merge-path search: i = #A among the first d outputs
-                    int mid = (lo + hi) >> 1;
-                    if (A[mid] <= B[d - mid - 1]) lo = mid + 1;
+                    const int mid = (lo + hi) >> 1;
+                    if (src[sw(s + mid)] <= src[sw(s + W + d - mid - 1)]) lo = mid + 1;
                     else hi = mid;
                 }
-                int i = lo, j = d - lo;
-                uint16_t a = i < W ? A[i] : 0xFFFF;
-                uint16_t b = j < W ? B[j] : 0xFFFF;
-                for (int o = 0; o < E; ++o) {
-                    bool takeA = (j >= W) || (i < W && a <= b);
-                    if (takeA) {
-                        dst[s + d + o] = a;
-                        ++i;
-                        a = i < W ? A[i] : 0xFFFF;
-                    } else {
-                        dst[s + d + o] = b;
-                        inv += (uint32_t)(W - i);
-                        ++j;
-                        b = j < W ? B[j] : 0xFFFF;
-                    }
-                }
+                inv += merge_seq(src, dst, s, W, lo, d - lo, s + d, E);
             }
         }
         __syncthreads();
@@ -191,7 +191,7 @@ __device__ uint32_t sort_count_block(uint16_t* keys, uint16_t* tmp, int L) {
         dst = t;
     }
     if (src != keys) {
-        for (int i = threadIdx.x; i < L; i += T) keys[i] = src[i];
+        for (int i = threadIdx.x; i < L; i += T) keys[sw(i)] = src[sw(i)];
         __syncthreads();
     }
     return inv;
@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         const int32_t* rv = p.ranks + x * n;    // v ranks
 
         // pads (max key) first, then scatter w[pos_u[e]] = rank_v[e]
-        for (int64_t i = n + tid; i < (int64_t)p.B * L; i += MG_THREADS) keys[i] = 0xFFFF;
-        for (int64_t e = tid; e < n; e += MG_THREADS) keys[pu[e]] = (uint16_t)rv[e];
+        for (int64_t i = n + tid; i < (int64_t)p.B * L; i += MG_THREADS) keys[sw((int)i)] = 0xFFFF;
+        for (int64_t e = tid; e < n; e += MG_THREADS) keys[sw(pu[e])] = (uint16_t)rv[e];
         __syncthreads();
 
         // within-u-group pairs: inv_g and joint ties (n3)
@@ -238,9 +238,9 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         for (int64_t q = tid; q + 1 < n; q += MG_THREADS) {
             const int32_t g = su[q];
             if (su[q + 1] != g) continue;
-            const uint16_t wq = keys[q];
+            const uint16_t wq = keys[sw((int)q)];
             for (int64_t t = q + 1; t < n && su[t] == g; ++t) {
-                const uint16_t wt = keys[t];
+                const uint16_t wt = keys[sw((int)t)];
                 inv_g += (wq > wt);
                 ties += (wq == wt);
             }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         // inv(w)
         uint32_t inv = sort_count_block(keys, tmp, L);
         if (p.B == 2) {
-            inv += sort_count_block(keys + L, tmp, L);
+            inv += sort_count_block(keys + L, tmp, L);  // L >= 64 here: swizzle blocks stay aligned
             // cross inversions: for each b in block 1, # of block-0 keys > b
             const int64_t L2 = n - L1;
             const int64_t per = (L2 + MG_THREADS - 1) / MG_THREADS;
@@ -258,17 +258,17 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
             if (b0 < b1) {
                 const uint16_t* H1 = keys;
                 const uint16_t* H2 = keys + L;
-                uint16_t b = H2[b0];
+                uint16_t b = H2[sw((int)b0)];
                 int64_t lo = 0, hi = L1;  // upper_bound(H1, b)
                 while (lo < hi) {
                     int64_t mid = (lo + hi) >> 1;
-                    if (H1[mid] <= b) lo = mid + 1;
+                    if (H1[sw((int)mid)] <= b) lo = mid + 1;
                     else hi = mid;
                 }
                 int64_t ub = lo;
                 for (int64_t k = b0; k < b1; ++k) {
-                    b = H2[k];
-                    while (ub < L1 && H1[ub] <= b) ++ub;
+                    b = H2[sw((int)k)];
+                    while (ub < L1 && H1[sw((int)ub)] <= b) ++ub;
                     inv += (uint32_t)(L1 - ub);
                 }
             }

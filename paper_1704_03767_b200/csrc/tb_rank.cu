@@ -1,0 +1,288 @@
+// K0: device rank transform -- rank_transform (ranks.py:37-61) for every row at once.
+//
+// Dense 0-based ranks (ties share a rank, distinct ranks are exactly 0..k-1), NaN rejected
+// (ranks.py:56-57), -0.0 == +0.0 (np.unique's equality), plus the per-row tied-pair count
+// n1 = sum_t t(t-1)/2 (kernel_sorted.py:163-176) as a by-product of the sort.
+//
+// One CTA per row, n <= 8192 (the GEMM path): the row's (order-preserving key, index) pairs are
+// bitonic-sorted in shared memory (lexicographic on (key, index), so pad slots sort last), a
+// block scan over "new value" flags yields the dense ranks, and run starts give n1.
+#include "tb_common.cuh"
+
+namespace tb {
+
+constexpr int RK_THREADS = 512;
+constexpr int RK_MAX_N = 8192;
+
+__device__ __forceinline__ uint64_t order_key(int32_t v) { return (uint64_t)((uint32_t)v ^ 0x80000000u); }
+__device__ __forceinline__ uint64_t order_key(float v) {
+    uint32_t b = __float_as_uint(v == 0.0f ? 0.0f : v);  // -0.0 -> +0.0
+    return (uint64_t)((b & 0x80000000u) ? ~b : (b | 0x80000000u));
+}
+__device__ __forceinline__ uint64_t order_key(double v) {
+    uint64_t b = (uint64_t)__double_as_longlong(v == 0.0 ? 0.0 : v);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RK_THREADS) rank_rows_kernel(const T* __restrict__ x, int64_t n, int64_t ldx,
+                                                               uint16_t* __restrict__ R, int64_t ldr,
+                                                               unsigned long long* __restrict__ n1,
+                                                               int32_t* __restrict__ flags, int Np) {
+    extern __shared__ __align__(16) uint8_t rk_smem[];
+    uint64_t* key = reinterpret_cast<uint64_t*>(rk_smem);
+    uint16_t* idx = reinterpret_cast<uint16_t*>(key + Np);
+    uint16_t* start = idx + Np;  // run start position per dense rank
+    __shared__ int32_t wsum[RK_THREADS / 32];
+    __shared__ unsigned long long wties[RK_THREADS / 32];
+    const int64_t r = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int nn = (int)n;
+
+    bool bad = false;
+    for (int i = tid; i < Np; i += RK_THREADS) {
+        if (i < nn) {
+            const T v = x[r * ldx + i];
+            bad |= (v != v);
+            key[i] = order_key(v);
+        } else {
+            key[i] = ~0ull;
+        }
+        idx[i] = (uint16_t)i;
+    }
+    if (bad) atomicOr(flags, 1);
+    __syncthreads();
+
+    // bitonic sort on (key, idx)
+    for (int k = 2; k <= Np; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < Np; i += RK_THREADS) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const uint64_t ki = key[i], kl = key[l];
+                    const uint16_t ii = idx[i], il = idx[l];
+                    const bool gt = ki > kl || (ki == kl && ii > il);
+                    const bool up = (i & k) == 0;
+                    if (gt == up) {
+                        key[i] = kl;
+                        key[l] = ki;
+                        idx[i] = il;
+                        idx[l] = ii;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    // dense ranks: inclusive scan of "new value" flags over positions [0, n)
+    const int per = (Np + RK_THREADS - 1) / RK_THREADS;
+    const int p0 = tid * per, p1 = min(p0 + per, nn);
+    int local = 0;
+    for (int p = p0; p < p1; ++p) local += (p == 0 || key[p] != key[p - 1]);
+    int incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((tid & 31) >= o) incl += t;
+    }
+    if ((tid & 31) == 31) wsum[tid >> 5] = incl;
+    __syncthreads();
+    if (tid < 32) {
+        const int s = tid < RK_THREADS / 32 ? wsum[tid] : 0;
+        int si = s;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, si, o);
+            if (tid >= o) si += t;
+        }
+        if (tid < RK_THREADS / 32) wsum[tid] = si - s;
+    }
+    __syncthreads();
+    int rank = wsum[tid >> 5] + incl - local - 1;
+    for (int p = p0; p < p1; ++p) {
+        if (p == 0 || key[p] != key[p - 1]) {
+            ++rank;
+            start[rank] = (uint16_t)p;
+        }
+        R[r * ldr + idx[p]] = (uint16_t)rank;
+        idx[p] = (uint16_t)rank;  // reuse: rank at sorted position p
+    }
+    __syncthreads();
+    unsigned long long ties = 0;
+    for (int p = p0; p < p1; ++p) ties += (unsigned long long)(p - start[idx[p]]);
+    for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
+    if ((tid & 31) == 0) wties[tid >> 5] = ties;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < RK_THREADS / 32; ++w) t += wties[w];
+        n1[r] = t;
+    }
+    // zero the row padding [n, ldr) so vector loads of R see defined values
+    for (int64_t i = nn + tid; i < ldr; i += RK_THREADS) R[r * ldr + i] = 0;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Warp-per-row variant for Np = 32 E <= 1024 (the GEMM-path shapes): lane l holds sorted slots
+// [E l, E l + E) of 48-bit composites (order key << 16 | index) in registers; bitonic stages with
+// a partner stride below E run inside the lane, larger strides exchange through shuffles.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E], int lane) {
+#pragma unroll 1
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j >= E; j >>= 1) {  // cross-lane
+            const int lm = j / E;
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                const int e = E * lane + i;
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, v[i], lm);
+                const bool up = (e & k) == 0;
+                const bool low = (e & j) == 0;
+                const uint64_t mn = v[i] < o ? v[i] : o, mx = v[i] < o ? o : v[i];
+                v[i] = (low == up) ? mn : mx;
+            }
+        }
+#pragma unroll
+        for (int j = E / 2; j > 0; j >>= 1) {  // in-lane
+            if (j >= k) continue;
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                if (i & j) continue;
+                const int e = E * lane + i;
+                const bool up = (e & k) == 0;
+                const uint64_t a = v[i], b = v[i + j];
+                const bool sw = (a > b) == up;
+                v[i] = sw ? b : a;
+                v[i + j] = sw ? a : b;
+            }
+        }
+    }
+}
+
+template <typename T, int E>
+__global__ void __launch_bounds__(256) rank_rows_warp_kernel(const T* __restrict__ x, int64_t m, int64_t n,
+                                                             int64_t ldx, uint16_t* __restrict__ R, int64_t ldr,
+                                                             unsigned long long* __restrict__ n1,
+                                                             int32_t* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= m) return;
+    const int nn = (int)n;
+    uint64_t v[E];
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        const int e = lane + 32 * i;  // coalesced load, any slot assignment works before the sort
+        uint64_t key = 0xFFFFFFFFull;
+        if (e < nn) {
+            const T xv = x[r * ldx + e];
+            bad |= (xv != xv);
+            key = order_key(xv);
+        }
+        v[i] = (key << 16) | (uint64_t)e;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1);
+    warp_bitonic<E>(v, lane);
+    // dense ranks over slots [0, n): flag = key differs from the previous slot's key
+    const uint64_t prev_last = __shfl_up_sync(0xffffffffu, v[E - 1], 1);
+    int cnt = 0;
+    int last_start = -1;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        const int p = E * lane + i;
+        const uint64_t pk = i ? v[i - 1] : prev_last;
+        const bool f = p < nn && (p == 0 || (pk >> 16) != (v[i] >> 16));
+        cnt += f;
+        if (f) last_start = p;
+    }
+    int incl = cnt;
+    int mstart = last_start;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        const int ms = __shfl_up_sync(0xffffffffu, mstart, o);
+        if (lane >= o) {
+            incl += t;
+            mstart = max(mstart, ms);
+        }
+    }
+    int rank = incl - cnt - 1;
+    int start = __shfl_up_sync(0xffffffffu, mstart, 1);
+    if (lane == 0) start = 0;
+    unsigned long long ties = 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        const int p = E * lane + i;
+        if (p < nn) {
+            const uint64_t pk = i ? v[i - 1] : prev_last;
+            if (p == 0 || (pk >> 16) != (v[i] >> 16)) {
+                ++rank;
+                start = p;
+            }
+            ties += (unsigned long long)(p - start);
+            R[r * ldr + (int)(v[i] & 0xFFFF)] = (uint16_t)rank;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
+    if (lane == 0) n1[r] = ties;
+    for (int64_t i = nn + lane; i < ldr; i += 32) R[r * ldr + i] = 0;
+}
+
+template <typename T>
+static int launch_rank_warp(const T* x, int64_t m, int64_t n, int64_t ldx, uint16_t* R, int64_t ldr,
+                            unsigned long long* n1, int32_t* flags, int Np, cudaStream_t st) {
+    const unsigned grid = (unsigned)((m + 7) / 8);
+    switch (Np / 32) {
+        case 1: rank_rows_warp_kernel<T, 1><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
+        case 2: rank_rows_warp_kernel<T, 2><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
+        case 4: rank_rows_warp_kernel<T, 4><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
+        case 8: rank_rows_warp_kernel<T, 8><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
+        case 16: rank_rows_warp_kernel<T, 16><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
+        case 32: rank_rows_warp_kernel<T, 32><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
+        default: return fail(TB_ERR_CONFIG, "rank_rows: bad warp sort size");
+    }
+    return check_launch("rank_rows_warp_kernel");
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" int tb_rank_rows(const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, uint16_t* R, int64_t ldr,
+                            uint64_t* n1, int32_t* flags, void* stream) {
+    if (m < 1 || n < 1) return fail(TB_ERR_INVALID, "rank_rows: empty input");
+    if (n > RK_MAX_N) return fail(TB_ERR_CAPACITY, "rank_rows: n=%lld exceeds %d", (long long)n, RK_MAX_N);
+    if (ldx < n || ldr < n || (ldr & 7)) return fail(TB_ERR_CONFIG, "rank_rows: bad leading dimensions");
+    if (!x || !R || !n1 || !flags) return fail(TB_ERR_INVALID, "rank_rows: null pointer");
+    if (m > INT32_MAX) return fail(TB_ERR_CAPACITY, "rank_rows: m too large");
+    int Np = 1;
+    while (Np < n) Np <<= 1;
+    const size_t smem = (size_t)Np * (8 + 2 + 2);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* n1u = reinterpret_cast<unsigned long long*>(n1);
+    if (Np <= 1024 && dtype != TB_DTYPE_F64) {  // 32-bit keys: warp-per-row register sort
+        if (Np < 32) Np = 32;
+        if (dtype == TB_DTYPE_I32) return launch_rank_warp((const int32_t*)x, m, n, ldx, R, ldr, n1u, flags, Np, st);
+        return launch_rank_warp((const float*)x, m, n, ldx, R, ldr, n1u, flags, Np, st);
+    }
+    switch (dtype) {
+        case TB_DTYPE_I32:
+            cudaFuncSetAttribute(rank_rows_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            rank_rows_kernel<int32_t><<<(unsigned)m, RK_THREADS, smem, st>>>(
+                (const int32_t*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np);
+            break;
+        case TB_DTYPE_F32:
+            cudaFuncSetAttribute(rank_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            rank_rows_kernel<float><<<(unsigned)m, RK_THREADS, smem, st>>>(
+                (const float*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np);
+            break;
+        case TB_DTYPE_F64:
+            cudaFuncSetAttribute(rank_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            rank_rows_kernel<double><<<(unsigned)m, RK_THREADS, smem, st>>>(
+                (const double*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np);
+            break;
+        default:
+            return fail(TB_ERR_INVALID, "rank_rows: unknown dtype %d", dtype);
+    }
+    return check_launch("rank_rows_kernel");
+}

@@ -1,21 +1,12 @@
-// K2: sign pack.  S[r, k(a,b)] = sign(x[r,b] - x[r,a]) as int8, plus the
-// per-row tied-pair count n1 = n0 - sum |S| (the n1/n2 scans of
-// kernel_sorted.py:163-176, done once per variable instead of once per pair).
-//
-// One CTA owns (row r, a strided set of 8 KiB chunks of k).  The row's values
-// sit in shared memory; consecutive threads produce consecutive bytes of k
-// (so consecutive threads read consecutive x[b] -- conflict-free), bytes are
-// staged in shared memory and written out with 16-byte coalesced stores.
-// HBM-bound on the S write (m * ldS bytes).
+// K2: sign pack -- each variable's {-1, 0, +1} sign vector over all sample pairs, materialised
+// once (int8) for the tcgen05 GEMM.  Replaces the per-pair sign enumeration of naive_numerator
+// (kernel_naive.py:26-44).  Input: dense uint16 ranks from K0 (tb_rank.cu).
+// HBM-write-bound on S (m * ldS bytes): one CTA per (row, K-range), 16-byte coalesced stores.
 #include "tb_common.cuh"
 
 namespace tb {
 
 constexpr int SP_THREADS = 256;
-constexpr int SP_DCHUNK = 64;  // offsets d handled per work item
-
-// Row value i lives at shared index i + i/16: lanes reading indices 16 apart hit distinct banks.
-__device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
 
 // S layout ("diagonal"): sample pairs are ordered by offset d = b - a (1..n-1), then by a; each
 // d-segment holds n - d signs zero-padded to a multiple of 16 bytes:
@@ -30,133 +21,146 @@ __host__ __device__ __forceinline__ int64_t diag_off(int64_t d, int64_t n) {
 }
 __host__ __device__ __forceinline__ int64_t diag_k(int64_t n) { return diag_off(n, n); }
 
-// One warp = 32 consecutive 16-sample groups (a0 = 16 g) x a run of SP_DCHUNK offsets d.  A lane
-// keeps its own 16 values and a 32-value sliding window x[a0 + d ..] in registers: per d it loads
-// one new value, emits 16 signs as one uint4 (the warp writes 512 contiguous bytes), slides.
-template <typename T>
-__global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const T* __restrict__ x, int64_t m, int64_t n,
-                                                              int64_t ldx, int8_t* __restrict__ S, int64_t ldS,
-                                                              int64_t K, unsigned long long* __restrict__ nz,
-                                                              int32_t* __restrict__ flags) {
-    extern __shared__ __align__(16) uint8_t sp_smem[];
-    T* xs = reinterpret_cast<T*>(sp_smem);
-    const int64_t r = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int nn = (int)n;
-    const int slack = nn + 48;  // window reads run up to 31 past n (masked)
-
-    bool bad = false;
-    for (int i = tid; i < slack; i += SP_THREADS) {
-        T v = i < nn ? x[r * ldx + i] : T(0);
-        bad |= (v != v);  // NaN has no rank (ranks.py:56-57)
-        xs[spad(i)] = v;
+// Segment-major emission: the 16-byte chunks of a row's S are enumerated in memory order,
+// chunk c <-> (offset d, group g) with S bytes [off(d) + 16 g, +16) = signs of samples
+// a = 16 g .. 16 g + 15 at offset d.  Consecutive threads take consecutive chunks, so every warp
+// store is 512 contiguous bytes and a CTA fills its whole K-range (no partial L2 sectors); each
+// chunk reads its own and window words with 128-bit loads from shifted shared-memory row copies.
+//   D = (w | 0x8000) - o and E = (o | 0x8000) - w per halfword  (2 IADD3, no cross-lane borrow),
+//   ge/le = sign-replicated high bytes of D/E                 (PRMT 0xFDB9),
+//   byte  = (ge ^ le) & (le | 0x01)                            (one LOP3: +1 / -1 / 0).
+__device__ __forceinline__ uint32_t prmt_signs(uint32_t lo, uint32_t hi) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(r) : "r"(lo), "r"(hi));
+    return r;
+}
+__device__ __forceinline__ uint32_t sign_bytes(uint32_t ge, uint32_t le) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x2C;" : "=r"(r) : "r"(ge), "r"(le), "r"(0x01010101u));
+    return r;
+}
+// smallest N in [1, n-1] with ceil16_prefix(N) >= t
+__device__ __forceinline__ int inv_prefix(int64_t t, int n) {
+    int lo = 1, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ceil16_prefix(mid) >= t) hi = mid;
+        else lo = mid + 1;
     }
-    if (bad) atomicOr(flags, 1);
+    return lo;
+}
+
+__device__ __forceinline__ uint4 lds128(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+// Signs of the 16 samples of one chunk from its 8 own and 8 window rank-pair words.
+__device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint32_t (&own)[8]) {
+    uint32_t out[4];
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+        const int k0 = 2 * qq, k1 = 2 * qq + 1;
+        const uint32_t ge = prmt_signs(y[k0] + 0x80008000u - own[k0], y[k1] + 0x80008000u - own[k1]);
+        const uint32_t le = prmt_signs(own[k0] + 0x80008000u - y[k0], own[k1] + 0x80008000u - y[k1]);
+        out[qq] = sign_bytes(ge, le);
+    }
+    return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+// Shared memory holds 8 shifted copies of the row's rank pairs, C[o][s][j] = pair at halfword
+// 2 (j + s) + o, so the window of chunk (d, g) -- halfwords 16 g + d .. +15 -- is 8 words starting
+// at the 16-byte-aligned index 8 g + ((d >> 1) & ~3) of copy (d & 1, (d >> 1) & 3): two 128-bit
+// loads, no per-lane shifting.
+__global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __restrict__ R, int64_t n,
+                                                              int64_t ldr, int8_t* __restrict__ S, int64_t ldS,
+                                                              int64_t K, int nwc) {
+    extern __shared__ __align__(16) uint32_t sp_words[];  // [8][nwc]
+    const int64_t r = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nn = (int)n;
+    const uint16_t* rr = R + r * ldr;
+    for (int j = tid; j < nwc; j += SP_THREADS) {
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+#pragma unroll
+            for (int sh = 0; sh < 4; ++sh) {
+                const int h = 2 * (j + sh) + o;  // halfword index of the pair's low half
+                const uint32_t lo = h < nn ? rr[h] : 0u, hi = h + 1 < nn ? rr[h + 1] : 0u;
+                sp_words[(o * 4 + sh) * nwc + j] = lo | (hi << 16);
+            }
+        }
+    }
     __syncthreads();
 
     int8_t* row = S + r * ldS;
-    uint32_t cnt = 0;
-    const int ngroups = (nn - 1 + 15) >> 4;          // groups with a0 < n - 1
-    const int gblocks = (ngroups + 31) >> 5;
-    const int nchunks = (nn - 1 + SP_DCHUNK - 1) / SP_DCHUNK;
-    const int items = nchunks * gblocks;
-    const int warps = SP_THREADS / 32;
-    for (int it = blockIdx.y * warps + (tid >> 5); it < items; it += gridDim.y * warps) {
-        const int c = it / gblocks, gb = it - c * gblocks;
-        const int g = gb * 32 + lane;
-        const int a0 = g * 16;
-        const int d_lo = 1 + c * SP_DCHUNK;
-        const int d_hi = min(1 + (c + 1) * SP_DCHUNK, nn - a0);  // group g exists while a0 < n - d
-        if (d_lo >= d_hi) continue;
-        T own[16], win[32];
+    const int64_t nchunks = K >> 4;
+    const int64_t per = (nchunks + gridDim.y - 1) / gridDim.y;
+    const int64_t b_lo = (int64_t)blockIdx.y * per, b_hi = min(b_lo + per, nchunks);
+    const int64_t wper = (b_hi - b_lo + (SP_THREADS / 32) - 1) / (SP_THREADS / 32);
+    const int64_t c_lo = b_lo + warp * wper, c_hi = min(c_lo + wper, b_hi);
+    int64_t c = c_lo + lane;
+    if (c < c_hi) {
+        // decode chunk c -> (d, g): off(d)/16 = P(n-1) - P(n-d) <= c < P(n-1) - P(n-d-1)
+        const int64_t top = ceil16_prefix(nn - 1);
+        const int N = inv_prefix(top - c, nn);  // n - d
+        int d = nn - N;
+        int g = (int)(c - (top - ceil16_prefix(N)));
+        int G = (nn - d + 15) >> 4;
+        for (; c < c_hi; c += 32) {
+            const uint32_t* own_p = sp_words + 8 * g;
+            const uint32_t* win_p = sp_words + ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + 8 * g + ((d >> 1) & ~3);
+            const uint4 o0 = lds128(own_p), o1 = lds128(own_p + 4);
+            const uint4 w0 = lds128(win_p), w1 = lds128(win_p + 4);
+            const uint32_t own[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+            const uint32_t y[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            uint4 v = chunk_signs(y, own);
+            const int lim = nn - d - 16 * g;  // samples 16 g + i valid for i < lim
+            if (lim < 16) {
+                uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int i = 0; i < 16; ++i) own[i] = xs[spad(a0 + i)];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) win[i] = xs[spad(a0 + d_lo + i)];
-        int64_t off = diag_off(d_lo, n) + 16 * g;
-        for (int db = d_lo; db < d_hi; db += 16) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) win[16 + i] = xs[spad(a0 + db + 16 + i)];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int d = db + j;
-                if (d < d_hi) {
-                    const int lim = nn - d - a0;  // samples a0 + i valid for i < lim
-                    uint32_t w[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const T xb = win[i + j], xa = own[i];
-                        const uint32_t gt = xb > xa, lt = xb < xa;
-                        const uint32_t byte = (i < lim) ? (gt | (lt * 0xFFu)) : 0u;
-                        w[i >> 2] |= byte << ((i & 3) * 8);
-                    }
-                    *reinterpret_cast<uint4*>(row + off) = make_uint4(w[0], w[1], w[2], w[3]);
-                    cnt += __popc(w[0] & 0x01010101u) + __popc(w[1] & 0x01010101u) +
-                           __popc(w[2] & 0x01010101u) + __popc(w[3] & 0x01010101u);
-                    off += 16 * ((nn - d + 15) >> 4);
+                for (int qq = 0; qq < 4; ++qq) {
+                    const int cnt = min(max(lim - 4 * qq, 0), 4);
+                    w4[qq] &= cnt == 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u);
                 }
+                v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             }
-#pragma unroll
-            for (int i = 0; i < 16; ++i) win[i] = win[16 + i];
+            *reinterpret_cast<uint4*>(row + 16 * c) = v;
+            g += 32;
+            while (g >= G && d < nn - 1) {
+                g -= G;
+                ++d;
+                G = (nn - d + 15) >> 4;
+            }
         }
     }
     // zero the row tail [K, ldS)
     for (int64_t k = K + ((int64_t)blockIdx.y * SP_THREADS + tid) * 16; k < ldS; k += (int64_t)gridDim.y * SP_THREADS * 16)
         *reinterpret_cast<uint4*>(row + k) = make_uint4(0u, 0u, 0u, 0u);
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0 && cnt) atomicAdd(&nz[r], (unsigned long long)cnt);
-}
-
-__global__ void nz_to_n1_kernel(unsigned long long* n1, int64_t m, unsigned long long n0) {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r < m) n1[r] = n0 - n1[r];
 }
 
 }  // namespace tb
 
 using namespace tb;
 
-extern "C" int tb_sign_pack(const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, int8_t* S, int64_t ldS,
-                            uint64_t* n1, int32_t* flags, void* stream) {
+extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr, int8_t* S, int64_t ldS,
+                            void* stream) {
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "sign_pack: need m >= 1 and n >= 2 (got m=%lld n=%lld)",
                                     (long long)m, (long long)n);
-    if (n > TB_MAX_N) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld exceeds %d", (long long)n, TB_MAX_N);
+    if (n > 32767) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld exceeds 32767 (15-bit ranks)", (long long)n);
     const int64_t K = diag_k(n);
     if (ldS < K || (ldS & 15)) return fail(TB_ERR_CONFIG, "sign_pack: ldS=%lld must be >= K=%lld and 16-aligned",
                                            (long long)ldS, (long long)K);
-    if (ldx < n) return fail(TB_ERR_CONFIG, "sign_pack: ldx < n");
-    if (!x || !S || !n1 || !flags) return fail(TB_ERR_INVALID, "sign_pack: null pointer");
-    size_t esz = dtype == TB_DTYPE_F64 ? 8 : 4;
-    size_t smem = ((size_t)(n + 48 + (n + 48) / 16 + 1) * esz + 15) & ~size_t(15);
-    if (smem > 200 * 1024) return fail(TB_ERR_CAPACITY, "sign_pack: row of n=%lld does not fit shared memory", (long long)n);
+    if (ldr < n || (ldr & 1)) return fail(TB_ERR_CONFIG, "sign_pack: ldr must be even and >= n");
+    if (!R || !S) return fail(TB_ERR_INVALID, "sign_pack: null pointer");
+    const int nwc = (int)(((n + 1) / 2 + 16 + 3) & ~3);  // words per shifted copy (window reads overrun n)
+    const size_t smem = (size_t)8 * nwc * sizeof(uint32_t);
+    if (smem > 200 * 1024) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld too large for the shared row copies", (long long)n);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    TB_CUDA_TRY(cudaMemsetAsync(n1, 0, m * sizeof(uint64_t), st));
-    const int64_t items = ((n - 1 + SP_DCHUNK - 1) / SP_DCHUNK) * (((n - 1 + 15) / 16 + 31) / 32);
-    const int64_t nblk = (items + SP_THREADS / 32 - 1) / (SP_THREADS / 32);
+    const int64_t nblk = (K / 16 + 16 * SP_THREADS - 1) / (16 * SP_THREADS);  // >= 16 chunks per thread
     int64_t want = (8 * (int64_t)num_sms() + m - 1) / m;  // >= ~8 CTAs per SM in total
     int gy = (int)std::min<int64_t>(std::max<int64_t>(want, 1), std::min<int64_t>(nblk, 65535));
     dim3 grid((unsigned)m, gy);
-    auto* nz = reinterpret_cast<unsigned long long*>(n1);
-    switch (dtype) {
-        case TB_DTYPE_I32:
-            cudaFuncSetAttribute(signpack_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            signpack_kernel<int32_t><<<grid, SP_THREADS, smem, st>>>((const int32_t*)x, m, n, ldx, S, ldS, K, nz, flags);
-            break;
-        case TB_DTYPE_F32:
-            cudaFuncSetAttribute(signpack_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            signpack_kernel<float><<<grid, SP_THREADS, smem, st>>>((const float*)x, m, n, ldx, S, ldS, K, nz, flags);
-            break;
-        case TB_DTYPE_F64:
-            cudaFuncSetAttribute(signpack_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            signpack_kernel<double><<<grid, SP_THREADS, smem, st>>>((const double*)x, m, n, ldx, S, ldS, K, nz, flags);
-            break;
-        default:
-            return fail(TB_ERR_INVALID, "sign_pack: unknown dtype %d", dtype);
-    }
-    int rc = check_launch("signpack_kernel");
-    if (rc) return rc;
-    nz_to_n1_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(nz, m, (unsigned long long)(n * (n - 1) / 2));
-    return check_launch("nz_to_n1_kernel");
+    TB_CUDA_TRY(cudaFuncSetAttribute(signpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    signpack_kernel<<<grid, SP_THREADS, smem, st>>>(R, n, ldr, S, ldS, K, nwc);
+    return check_launch("signpack_kernel");
 }
 
 // |S| (0/1 int8) for the full-count GEMM, 16 bytes per thread.

@@ -26,7 +26,7 @@ from .errors import CapacityExceededError, ConfigError, InvalidInputError
 # int8 ops per pair at tensor-core rate; the merge costs ~4 n log2 n INT32 ops
 # per pair at CUDA-core rate -- SURVEY 7 step 5.  Above this n the sign matrix
 # is also too large to materialise (m * n^2 / 2 bytes).
-GEMM_MAX_N = 8192
+GEMM_MAX_N = 8192  # also the device rank transform's row limit (tb_rank_rows)
 PATHS = ("gemm", "merge")
 
 
@@ -178,9 +178,12 @@ class TauEngine:
         m, n = res.m, res.n
         K = int(_lib.load().tb_sign_k(n))  # padded diagonal layout, >= n(n-1)/2
         ldS = (K + 15) // 16 * 16
-        S = self._buf("S", m * ldS, torch.int8)
-        _lib.call("tb_sign_pack", _ptr(x), _dtype_code(x), m, n, x.stride(0), _ptr(S), ldS,
+        ldr = (n + 7) // 8 * 8
+        R = self._buf("R", m * ldr, torch.int16)
+        _lib.call("tb_rank_rows", _ptr(x), _dtype_code(x), m, n, x.stride(0), _ptr(R), ldr,
                   _ptr(res.n1_rows), _ptr(res.flags), st)
+        S = self._buf("S", m * ldS, torch.int8)
+        _lib.call("tb_sign_pack", _ptr(R), m, n, ldr, _ptr(S), ldS, st)
         res.launches += 2
         gemm = "tb_gemm_pairs_simt" if simt else "tb_gemm_pairs"
         gargs = () if simt else (splits,)
