@@ -239,17 +239,17 @@ struct Gemm2Args {
     int64_t job_lo, job_hi;
     int32_t* num;
     int32_t atomic;
+    int64_t iters_per_pair;  // > 0: stream-K schedule over the (unit, k-block) iteration space
 };
 
 struct Unit2 {
     int64_t y0, x0;   // pair rows y0..y0+255, columns x0..x0+511
     int32_t h_lo;     // first N block needed (1 if block 0 is entirely below the diagonal)
     int32_t kb0, kb1;
+    bool partial;     // covers only part of K: accumulate atomically
 };
 
-__device__ __forceinline__ Unit2 decode_unit2(const Gemm2Args& p, int64_t u) {
-    const int32_t s = (int32_t)(u / p.nunits);
-    const int64_t i = u - (int64_t)s * p.nunits;
+__device__ __forceinline__ Unit2 unit_geometry(const Gemm2Args& p, int64_t i) {
     const int32_t e = p.units[i];
     int64_t Y, X;
     job_coord(e >> 1, p.w, Y, X);
@@ -257,9 +257,51 @@ __device__ __forceinline__ Unit2 decode_unit2(const Gemm2Args& p, int64_t u) {
     o.y0 = Y * gemm2::TILE + (e & 1) * gemm2::UM;
     o.x0 = X * gemm2::TILE;
     o.h_lo = (o.x0 + gemm2::BN - 1 < o.y0) ? 1 : 0;
-    o.kb0 = (int32_t)((int64_t)s * p.nkb / p.splits);
-    o.kb1 = (int32_t)((int64_t)(s + 1) * p.nkb / p.splits);
     return o;
+}
+
+// Work sequence of one CTA pair.  Static schedule: units u = pair, pair + npairs, ... of the
+// split-major list (unit i, K split s).  Stream-K schedule: the pair's contiguous slice
+// [pair * ipp, (pair + 1) * ipp) of the flattened (unit, k-block) space, cut at unit boundaries.
+struct WorkIter {
+    int64_t cur, end, step;
+};
+__device__ __forceinline__ WorkIter work_begin(const Gemm2Args& p, int64_t pair, int64_t npairs) {
+    WorkIter w;
+    if (p.iters_per_pair > 0) {
+        const int64_t total = p.nunits * (int64_t)p.nkb;
+        w.cur = min(pair * p.iters_per_pair, total);
+        w.end = min(w.cur + p.iters_per_pair, total);
+        w.step = 0;
+    } else {
+        w.cur = pair;
+        w.end = p.nunits * p.splits;
+        w.step = npairs;
+    }
+    return w;
+}
+__device__ __forceinline__ bool work_next(const Gemm2Args& p, WorkIter& w, Unit2& t) {
+    if (w.cur >= w.end) return false;
+    if (w.step == 0) {
+        const int64_t i = w.cur / p.nkb;
+        const int32_t kb0 = (int32_t)(w.cur - i * p.nkb);
+        const int64_t rem = w.end - w.cur;
+        const int32_t kb1 = (int32_t)(rem < (int64_t)(p.nkb - kb0) ? kb0 + rem : p.nkb);
+        t = unit_geometry(p, i);
+        t.kb0 = kb0;
+        t.kb1 = kb1;
+        t.partial = kb0 > 0 || kb1 < p.nkb;
+        w.cur += kb1 - kb0;
+    } else {
+        const int32_t s = (int32_t)(w.cur / p.nunits);
+        const int64_t i = w.cur - (int64_t)s * p.nunits;
+        t = unit_geometry(p, i);
+        t.kb0 = (int32_t)((int64_t)s * p.nkb / p.splits);
+        t.kb1 = (int32_t)((int64_t)(s + 1) * p.nkb / p.splits);
+        t.partial = p.splits > 1;
+        w.cur += w.step;
+    }
+    return true;
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
@@ -295,14 +337,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int64_t total = p.nunits * p.splits;
-
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t u = pair; u < total; u += npairs) {
-                const Unit2 t = decode_unit2(p, u);
+            WorkIter wi = work_begin(p, pair, npairs);
+            Unit2 t;
+            while (work_next(p, wi, t)) {
                 const uint32_t bytes = 2 * (A_BYTES + (2 - t.h_lo) * B_BYTES);
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -323,8 +364,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             uint32_t acc_phase = 0;
-            for (int64_t u = pair; u < total; u += npairs) {
-                const Unit2 t = decode_unit2(p, u);
+            WorkIter wi = work_begin(p, pair, npairs);
+            Unit2 t;
+            while (work_next(p, wi, t)) {
                 mbar_wait(tempty, acc_phase ^ 1);
                 tc_fence_after();
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
@@ -353,8 +395,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         const int64_t m = p.m;
         const int64_t span = p.job_hi - p.job_lo;
         const uint32_t tempty_leader = mapa_shared(tempty, 0);
-        for (int64_t u = pair; u < total; u += npairs) {
-            const Unit2 t = decode_unit2(p, u);
+        WorkIter wi = work_begin(p, pair, npairs);
+        Unit2 t;
+        while (work_next(p, wi, t)) {
             mbar_wait(tfull, acc_phase);
             tc_fence_after();
             const int64_t y = t.y0 + rank * BM + q * 32 + lane;
@@ -371,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
                             const int64_t x = t.x0 + h * BN + c + i;
                             const int64_t j = base + x;
                             if (x >= y && x < m && j >= 0 && j < span) {
-                                if (p.atomic)
+                                if (t.partial)
                                     atomicAdd(&p.num[j], (int32_t)r[i]);
                                 else
                                     p.num[j] = (int32_t)r[i];
@@ -560,20 +603,34 @@ static int gemm_v2(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t j
     p.nunits = nunits;
     p.nkb = (int32_t)((K + gemm2::BK - 1) / gemm2::BK);
     const int pairs = std::max(1, num_sms() / 2);
-    if (splits <= 0) splits = pick_splits(nunits, p.nkb, pairs);
+    p.iters_per_pair = 0;
+    // Stream-K (TB_GEMM_SCHED=streamk) balances small problems exactly, but its pairs sit at different
+    // K positions and lose the K-lockstep L2 reuse of S that the split-major static schedule gets
+    // (measured: config 2 GEMM 975 us stream-K vs 874 us static), so static is the default.
+    const char* sched = std::getenv("TB_GEMM_SCHED");
+    const bool streamk = splits <= 0 && sched && sched[0] == 's' && sched[1] == 't';
+    if (streamk) {
+        // stream-K: equal contiguous slices of the (unit, k-block) space; at most ~2 partial units per pair
+        const int64_t total = nunits * (int64_t)p.nkb;
+        p.iters_per_pair = std::max<int64_t>(8, (total + pairs - 1) / pairs);
+        splits = 1;
+    } else if (splits <= 0) {
+        splits = pick_splits(nunits, p.nkb, pairs);
+    }
     if (splits > p.nkb) splits = p.nkb;
     p.splits = splits;
     p.job_lo = job_lo;
     p.job_hi = job_hi;
     p.num = num;
-    p.atomic = splits > 1;
+    p.atomic = streamk || splits > 1;
     if (p.atomic) TB_CUDA_TRY(cudaMemsetAsync(num, 0, (job_hi - job_lo) * sizeof(int32_t), st));
     CUtensorMap tm;
     if ((rc = make_tmap(&tm, S, m, K, ldS, gemm2::BM))) return rc;
     TB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)gemm2::SMEM_BYTES));
-    const int64_t work = nunits * splits;
-    const unsigned grid = (unsigned)(2 * std::min<int64_t>(work, pairs));
+    const int64_t work = streamk ? (nunits * (int64_t)p.nkb + p.iters_per_pair - 1) / p.iters_per_pair
+                                 : nunits * splits;
+    const unsigned grid = (unsigned)(2 * std::max<int64_t>(1, std::min<int64_t>(work, pairs)));
     gemm_tc2_kernel<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(tm, p);
     return check_launch("gemm_tc2_kernel");
 }
