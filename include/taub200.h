@@ -44,6 +44,15 @@ extern "C" {
 #define TB_DTYPE_F32 1
 #define TB_DTYPE_F64 2
 
+/* Sign-matrix element formats (S of tb_sign_pack / tb_gemm_pairs):
+ *   TB_SIGN_I8    int8 -1/0/+1, one per byte      -> tcgen05 kind::i8 (exact int32 sums)
+ *   TB_SIGN_E4M3  e4m3 -1/0/+1, one per byte      -> tcgen05 kind::f8f6f4 (f32 sums; experiment)
+ *   TB_SIGN_E2M1  e2m1 -1/0/+1, two per byte      -> tcgen05 kind::mxf4, unit scales (f32 sums,
+ *                 exact while K < 2^24, i.e. n <= 5792); the default GEMM format */
+#define TB_SIGN_I8 0
+#define TB_SIGN_E4M3 1
+#define TB_SIGN_E2M1 2
+
 /* Largest n the device paths accept: the int32 numerator holds |n_c - n_d| <=
  * n(n-1)/2 < 2^31 exactly up to here.  Larger n raises
  * TB_ERR_CAPACITY (the reference's packed-capacity convention, ranks.py:64-76). */
@@ -83,26 +92,31 @@ int tb_rank_rows(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, ui
  *         zero-padded to a multiple of 16 bytes:
  *           S[r, off(d) + a] = sign(R[r, a+d] - R[r, a]),
  *           off(d) = 16 * sum_{d'<d} ceil((n - d') / 16).
- *         K = tb_sign_k(n) (>= n(n-1)/2); bytes [K, ldS) are zeroed; ldS must
- *         be a multiple of 16 and >= K.  Padding zeros add nothing to S_u.S_v.
+ *         K = tb_sign_k(n) (>= n(n-1)/2) elements: K bytes for TB_SIGN_I8/E4M3,
+ *         K/2 bytes for TB_SIGN_E2M1 (element 2i in the low nibble); the row tail
+ *         up to ldS is zeroed; ldS (bytes) must be a multiple of 16.  Padding zeros
+ *         add nothing to S_u.S_v.
  */
 int64_t tb_sign_k(int64_t n);
-int tb_sign_pack(const uint16_t *R, int64_t m, int64_t n, int64_t ldr, int8_t *S, int64_t ldS, void *stream);
+int tb_sign_pack(const uint16_t *R, int64_t m, int64_t n, int64_t ldr, int8_t *S, int64_t ldS, int format,
+                 void *stream);
 
 /*
- * K3 numerator GEMM on tcgen05 tensor cores (kind::i8, TMA-fed, TMEM
- * accumulators): num[j - job_lo] = S_y . S_x = n_c - n_d for every job id j in
+ * K3 numerator GEMM on tcgen05 tensor cores (TMA-fed, TMEM accumulators, 2-SM
+ * CTA pairs): num[j - job_lo] = S_y . S_x = n_c - n_d for every job id j in
  * [job_lo, job_hi).  Replaces the per-cell numerator of _tiles_naive
- * (src/taucorr/engine.py:170-188) -- exact int32 accumulation.
+ * (src/taucorr/engine.py:170-188).  Exact: int32 sums (TB_SIGN_I8) or f32 sums
+ * of +-1 below 2^24 (TB_SIGN_E2M1 requires K < 2^24).  K is the element count
+ * (tb_sign_k(n)); format selects kind::i8 / f8f6f4 / mxf4.
  * splits: K-split factor (0 = automatic).  With splits > 1 the kernel
  * accumulates atomically; the library zeroes num first.
  */
-int tb_gemm_pairs(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
+int tb_gemm_pairs(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo, int64_t job_hi,
                   int32_t splits, int32_t *num, void *stream);
 
 /* |S| for the full-count mode: A[r, k] = |S[r, k]| (0/1 int8), same layout.
  * The second GEMM A A^T gives n_c + n_d per pair (SURVEY 8 identities). */
-int tb_abs_pack(const int8_t *S, int64_t m, int64_t ldS, int8_t *A, void *stream);
+int tb_abs_pack(const int8_t *S, int64_t m, int64_t ldS, int format, int8_t *A, void *stream);
 
 /* Full counts on the GEMM path from num = S_y.S_x and absdot = |S_y|.|S_x|:
  * n_d = (absdot - num) / 2 and n3 = absdot - n0 + n1_y + n1_x (the CELL_DTYPE
@@ -110,7 +124,7 @@ int tb_abs_pack(const int8_t *S, int64_t m, int64_t ldS, int8_t *A, void *stream
 int tb_full_counts(const int32_t *num, const int32_t *absdot, const uint64_t *n1_rows, int64_t m, int64_t n,
                    int64_t job_lo, int64_t job_hi, uint64_t *nd, uint64_t *n3, void *stream);
 
-/* Same contract on CUDA cores (dp4a); a GPU-side cross-check, not the product path. */
+/* Same contract on CUDA cores (dp4a, TB_SIGN_I8 only); a GPU-side cross-check, not the product path. */
 int tb_gemm_pairs_simt(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
                        int32_t *num, void *stream);
 

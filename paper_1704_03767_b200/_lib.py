@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 TB_OK, TB_ERR_INVALID, TB_ERR_CAPACITY, TB_ERR_CONFIG, TB_ERR_CUDA = 0, 1, 2, 3, 4
 TB_DTYPE_I32, TB_DTYPE_F32, TB_DTYPE_F64 = 0, 1, 2
+TB_SIGN_I8, TB_SIGN_E4M3, TB_SIGN_E2M1 = 0, 1, 2
 TB_MAX_N = 65536
 
 # Every exported symbol and its ctypes signature (kept in sync with include/taub200.h;
@@ -30,9 +31,9 @@ SIGNATURES = {
     "tb_query": ([ctypes.c_int, _p], ctypes.c_int),
     "tb_sign_k": ([_i64], _i64),
     "tb_rank_rows": ([_p, ctypes.c_int, _i64, _i64, _i64, _p, _i64, _p, _p, _p], ctypes.c_int),
-    "tb_sign_pack": ([_p, _i64, _i64, _i64, _p, _i64, _p], ctypes.c_int),
-    "tb_abs_pack": ([_p, _i64, _i64, _p, _p], ctypes.c_int),
-    "tb_gemm_pairs": ([_p, _i64, _i64, _i64, _i64, _i64, _i32, _p, _p], ctypes.c_int),
+    "tb_sign_pack": ([_p, _i64, _i64, _i64, _p, _i64, ctypes.c_int, _p], ctypes.c_int),
+    "tb_abs_pack": ([_p, _i64, _i64, ctypes.c_int, _p, _p], ctypes.c_int),
+    "tb_gemm_pairs": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _p], ctypes.c_int),
     "tb_gemm_pairs_simt": ([_p, _i64, _i64, _i64, _i64, _i64, _p, _p], ctypes.c_int),
     "tb_finalize": ([_p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "tb_full_counts": ([_p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),

@@ -240,6 +240,7 @@ struct Gemm2Args {
     int32_t* num;
     int32_t atomic;
     int64_t iters_per_pair;  // > 0: stream-K schedule over the (unit, k-block) iteration space
+    int32_t fp8;             // experiment: e4m3 operands, f32 accumulators (kind::f8f6f4)
 };
 
 struct Unit2 {
@@ -360,7 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {  // ---------------- MMA issuer (leader CTA, one thread)
-            constexpr uint32_t idesc = idesc_i8(UM, BN);
+            const uint32_t idesc = p.fp8 ? idesc_f8(UM, BN) : idesc_i8(UM, BN);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t acc_phase = 0;
@@ -379,7 +380,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
                         const uint32_t acc = (kb > t.kb0 || k > 0) ? 1u : 0u;
                         for (int h = t.h_lo; h < 2; ++h) {
                             const uint64_t bdesc = umma_desc_k_sw128(sa + A_BYTES + h * B_BYTES);
-                            mma_i8_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+                            if (p.fp8)
+                                mma_f8_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+                            else
+                                mma_i8_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
                         }
                     }
                     mma_commit_2sm(&empty[stage], 0x3);
@@ -414,10 +418,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
                             const int64_t x = t.x0 + h * BN + c + i;
                             const int64_t j = base + x;
                             if (x >= y && x < m && j >= 0 && j < span) {
+                                const int32_t val = p.fp8 ? __float2int_rn(__uint_as_float(r[i])) : (int32_t)r[i];
                                 if (t.partial)
-                                    atomicAdd(&p.num[j], (int32_t)r[i]);
+                                    atomicAdd(&p.num[j], val);
                                 else
-                                    p.num[j] = (int32_t)r[i];
+                                    p.num[j] = val;
                             }
                         }
                     }
@@ -494,7 +499,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-static int make_tmap(CUtensorMap* map, const int8_t* S, int64_t m, int64_t K, int64_t ldS, uint32_t box_rows) {
+int make_tmap(CUtensorMap* map, const int8_t* S, int64_t m, int64_t K, int64_t ldS, uint32_t box_rows) {
     auto enc = get_encode();
     if (!enc) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)m};
@@ -578,7 +583,7 @@ static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t s
 }
 
 // Split-K choice: minimise waves(U*s / pairs) * (nkb/s * t_kb + t_epi).
-static int32_t pick_splits(int64_t units, int32_t nkb, int pairs) {
+int32_t pick_splits(int64_t units, int32_t nkb, int pairs) {
     const double t_kb = 1.0, t_epi = 40.0;  // k-block of the 2-SM kernel ~0.5 us; epilogue ~20 us
     int32_t best = 1;
     double best_t = 1e300;
@@ -591,7 +596,7 @@ static int32_t pick_splits(int64_t units, int32_t nkb, int pairs) {
 }
 
 static int gemm_v2(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
-                   int32_t splits, int32_t* num, cudaStream_t st) {
+                   int32_t splits, int format, int32_t* num, cudaStream_t st) {
     int rc;
     const int32_t* units = nullptr;
     int64_t nunits = 0;
@@ -623,6 +628,7 @@ static int gemm_v2(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t j
     p.job_hi = job_hi;
     p.num = num;
     p.atomic = streamk || splits > 1;
+    p.fp8 = format == TB_SIGN_E4M3 ? 1 : 0;
     if (p.atomic) TB_CUDA_TRY(cudaMemsetAsync(num, 0, (job_hi - job_lo) * sizeof(int32_t), st));
     CUtensorMap tm;
     if ((rc = make_tmap(&tm, S, m, K, ldS, gemm2::BM))) return rc;
@@ -639,16 +645,24 @@ static int gemm_v2(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t j
 
 using namespace tb;
 
-extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
-                             int32_t splits, int32_t* num, void* stream) {
-    int rc = check_job_args(m, K, ldS, job_lo, job_hi);
+namespace tb {
+int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi, int32_t splits,
+             int32_t* num, cudaStream_t st);
+}
+
+extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
+                             int64_t job_hi, int32_t splits, int32_t* num, void* stream) {
+    if (format < TB_SIGN_I8 || format > TB_SIGN_E2M1) return fail(TB_ERR_CONFIG, "gemm: unknown format %d", format);
+    int rc = check_job_args(m, format == TB_SIGN_E2M1 ? K / 2 : K, ldS, job_lo, job_hi);
     if (rc) return rc;
     if (!S || !num) return fail(TB_ERR_INVALID, "gemm: null pointer");
     if (job_hi == job_lo) return TB_OK;
     if (m > (int64_t)INT32_MAX - gemm::TILE) return fail(TB_ERR_CAPACITY, "gemm: m too large for TMA coordinates");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (format == TB_SIGN_E2M1) return gemm_fp4(S, m, K, ldS, job_lo, job_hi, splits, num, st);
     const char* variant = std::getenv("TB_GEMM_VARIANT");
-    if (!(variant && variant[0] == '1')) return gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, num, st);
+    if (!(variant && variant[0] == '1')) return gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, format, num, st);
+    if (format != TB_SIGN_I8) return fail(TB_ERR_CONFIG, "gemm v1: int8 only");
     GemmArgs p{};
     p.m = m;
     p.w = (m + gemm::TILE - 1) / gemm::TILE;

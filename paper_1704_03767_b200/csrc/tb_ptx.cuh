@@ -167,6 +167,23 @@ __device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t a_desc, uin
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// FP8 (e4m3 x e4m3 -> f32) variant, kind::f8f6f4 -- the FP32-accumulation exactness experiment.
+__device__ __forceinline__ void mma_f8_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__host__ __device__ constexpr uint32_t idesc_f8(uint32_t M, uint32_t N) {
+    return (1u << 4)            // D format F32
+           | (0u << 7)          // A E4M3
+           | (0u << 10)         // B E4M3
+           | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
 // Arrive (once per CTA in `mask`) on the mbarrier at the same offset in each CTA when all prior
 // tcgen05 async ops of this thread complete.
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
@@ -177,4 +194,50 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
+}  // namespace tb
+
+// ====================================================================== block-scaled FP4 (kind::mxf4)
+namespace tb {
+// Host helpers shared by the GEMM kernels (tb_gemm.cu): 2-D UINT8 tensor map over S [m, K bytes]
+// (row stride ldS) with 128-byte swizzled boxes of 128 x box_rows; split-K wave model.
+int make_tmap(CUtensorMap* map, const int8_t* S, int64_t m, int64_t K, int64_t ldS, uint32_t box_rows);
+int32_t pick_splits(int64_t units, int32_t nkb, int pairs);
+
+// D[tmem] (+)= (A . SFA) (B . SFB)^T, packed e2m1 operands (two per byte, K = 64 per instruction),
+// ue8m0 scale factors read from TMEM, f32 accumulators; cta_group::2.
+__device__ __forceinline__ void mma_mxf4_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+        : "memory");
+}
+// Block-scaled instruction descriptor: E2M1 x E2M1, UE8M0 scales, K-major, dense K = 64, sf ids 0.
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t M, uint32_t N) {
+    return (1u << 7)            // A E2M1
+           | (1u << 10)         // B E2M1
+           | ((N >> 3) << 17)   // N / 8
+           | (1u << 23)         // scale format UE8M0
+           | ((M >> 4) << 24);  // M / 16
+}
+// 32 lanes x 32 bit, 32 consecutive columns per thread.
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, uint32_t v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(v)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 32 lanes x 32 bit, 16 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
 }  // namespace tb

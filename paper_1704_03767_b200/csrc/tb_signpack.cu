@@ -2,6 +2,8 @@
 // once (int8) for the tcgen05 GEMM.  Replaces the per-pair sign enumeration of naive_numerator
 // (kernel_naive.py:26-44).  Input: dense uint16 ranks from K0 (tb_rank.cu).
 // HBM-write-bound on S (m * ldS bytes): one CTA per (row, K-range), 16-byte coalesced stores.
+#include <cstdlib>
+
 #include "tb_common.cuh"
 
 namespace tb {
@@ -53,6 +55,9 @@ __device__ __forceinline__ int inv_prefix(int64_t t, int n) {
 __device__ __forceinline__ uint4 lds128(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
 // Signs of the 16 samples of one chunk from its 8 own and 8 window rank-pair words.
+// FMT 0: int8 (+1 = 0x01, -1 = 0xFF); FMT 1: e4m3 (0x38 / 0xB8, the kind::f8f6f4 experiment);
+// FMT 2: e2m1 (+1 = 0x2, -1 = 0xA) left in the low nibble of each byte (packed by the caller).
+template <int FMT>
 __device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint32_t (&own)[8]) {
     uint32_t out[4];
 #pragma unroll
@@ -60,7 +65,15 @@ __device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint3
         const int k0 = 2 * qq, k1 = 2 * qq + 1;
         const uint32_t ge = prmt_signs(y[k0] + 0x80008000u - own[k0], y[k1] + 0x80008000u - own[k1]);
         const uint32_t le = prmt_signs(own[k0] + 0x80008000u - y[k0], own[k1] + 0x80008000u - y[k1]);
-        out[qq] = sign_bytes(ge, le);
+        if (FMT == 1) {
+            const uint32_t t = ge ^ le;
+            out[qq] = (t & 0x38383838u) | (t & le & 0x80808080u);
+        } else if (FMT == 2) {
+            const uint32_t t = ge ^ le;
+            out[qq] = (t & 0x02020202u) | (t & le & 0x08080808u);
+        } else {
+            out[qq] = sign_bytes(ge, le);
+        }
     }
     return make_uint4(out[0], out[1], out[2], out[3]);
 }
@@ -69,6 +82,14 @@ __device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint3
 // 2 (j + s) + o, so the window of chunk (d, g) -- halfwords 16 g + d .. +15 -- is 8 words starting
 // at the 16-byte-aligned index 8 g + ((d >> 1) & ~3) of copy (d & 1, (d >> 1) & 3): two 128-bit
 // loads, no per-lane shifting.
+// e2m1 nibbles: bytes (n0, n1, n2, n3) of each word -> bytes (n1 n0, n3 n2); two words -> one.
+__device__ __forceinline__ uint32_t pack_nibbles(uint32_t a, uint32_t b) {
+    a = (a | (a >> 4)) & 0x00FF00FFu;
+    b = (b | (b >> 4)) & 0x00FF00FFu;
+    return __byte_perm(a, b, 0x6420);
+}
+
+template <int FMT>
 __global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __restrict__ R, int64_t n,
                                                               int64_t ldr, int8_t* __restrict__ S, int64_t ldS,
                                                               int64_t K, int nwc) {
@@ -111,7 +132,7 @@ __global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __
             const uint4 w0 = lds128(win_p), w1 = lds128(win_p + 4);
             const uint32_t own[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
             const uint32_t y[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-            uint4 v = chunk_signs(y, own);
+            uint4 v = chunk_signs<FMT>(y, own);
             const int lim = nn - d - 16 * g;  // samples 16 g + i valid for i < lim
             if (lim < 16) {
                 uint32_t w4[4] = {v.x, v.y, v.z, v.w};
@@ -122,7 +143,10 @@ __global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __
                 }
                 v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             }
-            *reinterpret_cast<uint4*>(row + 16 * c) = v;
+            if (FMT == 2)
+                *reinterpret_cast<uint2*>(row + 8 * c) = make_uint2(pack_nibbles(v.x, v.y), pack_nibbles(v.z, v.w));
+            else
+                *reinterpret_cast<uint4*>(row + 16 * c) = v;
             g += 32;
             while (g >= G && d < nn - 1) {
                 g -= G;
@@ -131,9 +155,10 @@ __global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __
             }
         }
     }
-    // zero the row tail [K, ldS)
-    for (int64_t k = K + ((int64_t)blockIdx.y * SP_THREADS + tid) * 16; k < ldS; k += (int64_t)gridDim.y * SP_THREADS * 16)
-        *reinterpret_cast<uint4*>(row + k) = make_uint4(0u, 0u, 0u, 0u);
+    // zero the row tail [K bytes, ldS)
+    const int64_t kb = FMT == 2 ? K / 2 : K;
+    for (int64_t k = kb + ((int64_t)blockIdx.y * SP_THREADS + tid) * 8; k < ldS; k += (int64_t)gridDim.y * SP_THREADS * 8)
+        *reinterpret_cast<uint2*>(row + k) = make_uint2(0u, 0u);
 }
 
 }  // namespace tb
@@ -141,13 +166,16 @@ __global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __
 using namespace tb;
 
 extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr, int8_t* S, int64_t ldS,
-                            void* stream) {
+                            int format, void* stream) {
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "sign_pack: need m >= 1 and n >= 2 (got m=%lld n=%lld)",
                                     (long long)m, (long long)n);
     if (n > 32767) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld exceeds 32767 (15-bit ranks)", (long long)n);
     const int64_t K = diag_k(n);
-    if (ldS < K || (ldS & 15)) return fail(TB_ERR_CONFIG, "sign_pack: ldS=%lld must be >= K=%lld and 16-aligned",
-                                           (long long)ldS, (long long)K);
+    if (format < 0 || format > 2) return fail(TB_ERR_CONFIG, "sign_pack: unknown format %d", format);
+    const int64_t kbytes = format == TB_SIGN_E2M1 ? K / 2 : K;
+    if (ldS < kbytes || (ldS & 15))
+        return fail(TB_ERR_CONFIG, "sign_pack: ldS=%lld must be >= %lld and 16-aligned", (long long)ldS,
+                    (long long)kbytes);
     if (ldr < n || (ldr & 1)) return fail(TB_ERR_CONFIG, "sign_pack: ldr must be even and >= n");
     if (!R || !S) return fail(TB_ERR_INVALID, "sign_pack: null pointer");
     const int nwc = (int)(((n + 1) / 2 + 16 + 3) & ~3);  // words per shifted copy (window reads overrun n)
@@ -158,33 +186,43 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
     int64_t want = (8 * (int64_t)num_sms() + m - 1) / m;  // >= ~8 CTAs per SM in total
     int gy = (int)std::min<int64_t>(std::max<int64_t>(want, 1), std::min<int64_t>(nblk, 65535));
     dim3 grid((unsigned)m, gy);
-    TB_CUDA_TRY(cudaFuncSetAttribute(signpack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    signpack_kernel<<<grid, SP_THREADS, smem, st>>>(R, n, ldr, S, ldS, K, nwc);
+#define TB_SP_LAUNCH(F)                                                                                   \
+    TB_CUDA_TRY(cudaFuncSetAttribute(signpack_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    signpack_kernel<F><<<grid, SP_THREADS, smem, st>>>(R, n, ldr, S, ldS, K, nwc)
+    if (format == TB_SIGN_E2M1) {
+        TB_SP_LAUNCH(2);
+    } else if (format == TB_SIGN_E4M3) {
+        TB_SP_LAUNCH(1);
+    } else {
+        TB_SP_LAUNCH(0);
+    }
+#undef TB_SP_LAUNCH
     return check_launch("signpack_kernel");
 }
 
 // |S| (0/1 int8) for the full-count GEMM, 16 bytes per thread.
 namespace tb {
-__global__ void abs_pack_kernel(const uint4* __restrict__ S, uint4* __restrict__ A, int64_t nvec) {
+__global__ void abs_pack_kernel(const uint4* __restrict__ S, uint4* __restrict__ A, int64_t nvec, uint32_t mask) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
         uint4 v = S[i];
-        // bytes are 0x00, 0x01 or 0xFF: |s| = s & 1
-        v.x &= 0x01010101u;
-        v.y &= 0x01010101u;
-        v.z &= 0x01010101u;
-        v.w &= 0x01010101u;
+        // int8 bytes 0x00/0x01/0xFF: |s| = s & 1; e2m1 nibbles 0x0/0x2/0xA: |s| clears the sign bits
+        v.x &= mask;
+        v.y &= mask;
+        v.z &= mask;
+        v.w &= mask;
         A[i] = v;
     }
 }
 }  // namespace tb
 
-extern "C" int tb_abs_pack(const int8_t* S, int64_t m, int64_t ldS, int8_t* A, void* stream) {
+extern "C" int tb_abs_pack(const int8_t* S, int64_t m, int64_t ldS, int format, int8_t* A, void* stream) {
     if (m < 1 || ldS < 16 || (ldS & 15)) return fail(TB_ERR_CONFIG, "abs_pack: bad shape");
     if (!S || !A) return fail(TB_ERR_INVALID, "abs_pack: null pointer");
     const int64_t nvec = m * ldS / 16;
     const int64_t blocks = std::min<int64_t>((nvec + 255) / 256, (int64_t)num_sms() * 8);
     abs_pack_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const uint4*>(S), reinterpret_cast<uint4*>(A), nvec);
+        reinterpret_cast<const uint4*>(S), reinterpret_cast<uint4*>(A), nvec,
+        format == TB_SIGN_E2M1 ? 0x77777777u : (format == TB_SIGN_E4M3 ? 0x7F7F7F7Fu : 0x01010101u));
     return check_launch("abs_pack_kernel");
 }
 

@@ -118,6 +118,14 @@ class TauEngine:
         if self._events is not None:
             self._events[which].record(self._stream)
 
+    sign_format_override: int | None = None  # tests / experiments: force TB_SIGN_*
+
+    def sign_format(self, K: int) -> int:
+        """e2m1 (kind::mxf4) while the f32 sums stay exact (K < 2^24), else int8 (kind::i8)."""
+        if self.sign_format_override is not None:
+            return self.sign_format_override
+        return _lib.TB_SIGN_E2M1 if K < (1 << 24) else _lib.TB_SIGN_I8
+
     @staticmethod
     def choose_path(n: int) -> str:
         return "gemm" if n <= GEMM_MAX_N else "merge"
@@ -176,26 +184,33 @@ class TauEngine:
 
     def _gemm_path(self, x, res: PairResult, st, full_counts: bool, splits: int, simt: bool):
         m, n = res.m, res.n
-        K = int(_lib.load().tb_sign_k(n))  # padded diagonal layout, >= n(n-1)/2
-        ldS = (K + 15) // 16 * 16
+        K = int(_lib.load().tb_sign_k(n))  # padded diagonal layout, >= n(n-1)/2 elements
+        fmt = self.sign_format(K) if not simt else _lib.TB_SIGN_I8
+        kbytes = K // 2 if fmt == _lib.TB_SIGN_E2M1 else K
+        ldS = (kbytes + 15) // 16 * 16
         ldr = (n + 7) // 8 * 8
         R = self._buf("R", m * ldr, torch.int16)
         _lib.call("tb_rank_rows", _ptr(x), _dtype_code(x), m, n, x.stride(0), _ptr(R), ldr,
                   _ptr(res.n1_rows), _ptr(res.flags), st)
         S = self._buf("S", m * ldS, torch.int8)
-        _lib.call("tb_sign_pack", _ptr(R), m, n, ldr, _ptr(S), ldS, st)
+        _lib.call("tb_sign_pack", _ptr(R), m, n, ldr, _ptr(S), ldS, fmt, st)
         res.launches += 2
-        gemm = "tb_gemm_pairs_simt" if simt else "tb_gemm_pairs"
-        gargs = () if simt else (splits,)
+        def gemm(src, out):
+            if simt:
+                _lib.call("tb_gemm_pairs_simt", _ptr(src), m, K, ldS, res.job_lo, res.job_hi, _ptr(out), st)
+            else:
+                _lib.call("tb_gemm_pairs", _ptr(src), m, K, ldS, fmt, res.job_lo, res.job_hi, splits, _ptr(out), st)
+
+        res.extra["sign_format"] = fmt
         self._mark(0)
-        _lib.call(gemm, _ptr(S), m, K, ldS, res.job_lo, res.job_hi, *gargs, _ptr(res.numerator), st)
+        gemm(S, res.numerator)
         self._mark(1)
         res.launches += 1
         if full_counts:
             A = self._buf("A", m * ldS, torch.int8)
-            _lib.call("tb_abs_pack", _ptr(S), m, ldS, _ptr(A), st)
+            _lib.call("tb_abs_pack", _ptr(S), m, ldS, fmt, _ptr(A), st)
             absdot = self._buf("absdot", res.count, torch.int32)
-            _lib.call(gemm, _ptr(A), m, K, ldS, res.job_lo, res.job_hi, *gargs, _ptr(absdot), st)
+            gemm(A, absdot)
             res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
             res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
             _lib.call("tb_full_counts", _ptr(res.numerator), _ptr(absdot), _ptr(res.n1_rows), m, n,

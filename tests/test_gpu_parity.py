@@ -287,3 +287,23 @@ def test_config5_gemm_sampled(eng):
     del res
     eng.release()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_sign_formats_agree(eng, k):
+    """kind::mxf4 (e2m1, f32 sums), kind::f8f6f4 (e4m3) and kind::i8 give identical numerators."""
+    from paper_1704_03767_b200 import _lib, workloads
+    x = torch.from_numpy(workloads.generate(k)).cuda()
+    outs = {}
+    try:
+        for fmt in (_lib.TB_SIGN_I8, _lib.TB_SIGN_E4M3, _lib.TB_SIGN_E2M1):
+            eng.sign_format_override = fmt
+            r = eng.all_pairs(x, kernel="gemm", tau_a=False, tau_b=False, full_counts=(k == 1)).validate()
+            outs[fmt] = (r.numerator.clone(), None if r.n_d is None else r.n_d.clone())
+    finally:
+        eng.sign_format_override = None
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][0], outs[2][0])
+    if k == 1:
+        assert torch.equal(outs[0][1], outs[2][1])
+    eng.release()
