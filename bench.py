@@ -4,15 +4,18 @@
 
 A "step" is one full pass of the hot path over the configured workload
 (BASELINE config 2 by default: m=2048 x n=1000 int32 0..9, every i<j pair):
-K2 sign pack -> K3 tcgen05 int8 GEMM -> K5 fp64 finalize (tau_a, tau_b).
+K0 rank -> K2 sign pack -> K3 tcgen05 sign GEMM (kind::mxf4, e2m1 signs) ->
+K5 fp64 finalize (tau_a, tau_b).
 
 * value: pairs/s with inputs resident in HBM, CUDA-event timed on the launching
   stream, L2 flushed (256 MiB write) before every timed step, max over ranks.
-* e2e: the same metric through the public API with pinned HOST buffers: H2D of
-  the values, the full path, D2H of tau_b + numerator, all inside the events.
-* roofline: the GEMM (dominant kernel), algorithmic int8 ops 2K per i<j pair,
-  per-launch CUDA-event duration vs the int8 tensor peak measured here with
-  torch._int_mm (MEASURED_PEAKS.json has no int8 entry).
+* e2e: the same metric through the public host API (TauEngine.all_pairs_host)
+  with pinned HOST buffers: H2D of the values, the full path, D2H of tau_b for
+  every job id, all inside the events.
+* roofline: the GEMM (dominant kernel), algorithmic ops 2K per i<j pair
+  (K = n(n-1)/2 sample pairs), per-launch CUDA-event duration vs the dense
+  tensor peak of the MMA kind it runs (FP4: nominal 9 PFLOP/s, B200_PROFILING.md;
+  int8: measured here with torch._int_mm since MEASURED_PEAKS.json has no int8).
 * cpu_baseline: the oracle port (C restatement of the reference packed/VSE
   merge kernel, pthreads over all host cores) on a bounded sample (rank 0, N=1).
 
@@ -280,6 +283,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     res.validate()
     launches_per_step = res.launches
+    sign_format = res.extra.get("sign_format")
     del res
 
     if world > 1:
@@ -313,24 +317,21 @@ def run_ours(args):
     ms_per_step = 1e3 * t_max / args.steps
     del res
 
-    # ---- e2e through the public API with pinned host buffers
+    # ---- e2e through the public API with pinned host buffers: H2D values -> device path -> tau_b D2H
     xh = torch.from_numpy(np.ascontiguousarray(xin)).pin_memory()
-    count = job_range[1] - job_range[0]
-    out_tb = torch.empty(count, dtype=torch.float64).pin_memory()
-    out_num = torch.empty(count, dtype=torch.int32).pin_memory()
+    out_tb = torch.empty(total_jobs, dtype=torch.float64).pin_memory()
     e2e_times = []
+    e2e_launches = 0
     for it in range(args.e2e_steps + 2):
         with torch.cuda.stream(stream):
             flush.zero_()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
-            xdev = xh.to(dev, non_blocking=True)
-            r = eng.all_pairs(xdev, kernel=path, job_range=job_range, tau_a=False, stream=stream)
-            out_tb.copy_(r.tau_b, non_blocking=True)
-            out_num.copy_(r.numerator, non_blocking=True)
+            r = eng.all_pairs_host(xh, out_tb, kernel=path, stream=stream)
             e.record(stream)
         if it >= 2:
             e2e_times.append((s, e))
+        e2e_launches = r.launches
         del r
     torch.cuda.synchronize()
     e2e_t = sum(s.elapsed_time(e) for s, e in e2e_times) / 1e3
@@ -338,9 +339,10 @@ def run_ours(args):
         tt = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_t = float(tt.item())
-    e2e_value = total_pairs * len(e2e_times) / e2e_t
+    e2e_pairs = strict_pairs(0, total_jobs) * world
+    e2e_value = e2e_pairs * len(e2e_times) / e2e_t
     h2d = xh.numel() * xh.element_size()
-    d2h = count * (8 + 4)
+    d2h = total_jobs * 8
 
     out = None
     if rank == 0:
@@ -354,13 +356,21 @@ def run_ours(args):
                 tj = json.load(fh)
             traffic = tj.get(f"config{args.config}", {}).get("dram_bytes_per_launch")
         if path == "gemm":
-            roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": (peak or 4.5e15) / 1e12,
-                    "unit": "TFLOP/s", "frac": achieved / (peak or 4.5e15), "traffic": traffic,
-                    "kernel": "gemm_tc_kernel (tcgen05.mma kind::i8)",
-                    "peak_source": "measured here: torch._int_mm int8 8192^3 best-of-10 (cuBLASLt)" if peak
-                    else "nominal 4.5 POPS dense int8 (probe failed)",
-                    "frac_of_nominal_4500": achieved / 4.5e15,
-                    "algorithmic": f"2*K int8 ops per i<j pair, K=n(n-1)/2={K}; {my_pairs} pairs per launch",
+            fp4 = sign_format == _lib.TB_SIGN_E2M1
+            if fp4:
+                pk, src = 9.0e15, "nominal dense FP4 (kind::mxf4) 9 PFLOP/s, B200_PROFILING.md table (no measured FP4 entry)"
+            else:
+                pk = peak or 4.5e15
+                src = ("measured here: torch._int_mm int8 8192^3 best-of-10 (cuBLASLt)" if peak
+                       else "nominal 4.5 POPS dense int8 (probe failed)")
+            roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk / 1e12,
+                    "unit": "TFLOP/s", "frac": achieved / pk, "traffic": traffic,
+                    "kernel": "gemm_fp4_kernel (tcgen05.mma kind::mxf4, 2-SM)" if fp4
+                    else "gemm_tc2_kernel (tcgen05.mma kind::i8, 2-SM)",
+                    "peak_source": src,
+                    "frac_of_measured_int8_peak": (achieved / peak) if peak else None,
+                    "measured_int8_peak_tops": peak / 1e12 if peak else None,
+                    "algorithmic": f"2*K ops per i<j pair, K=n(n-1)/2={K} sample pairs; {my_pairs} pairs per launch",
                     "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}
         else:
             roof = {"bound": "int32", "achieved": achieved / 1e12, "peak": None, "unit": "TOP/s",
@@ -384,7 +394,9 @@ def run_ours(args):
                        "outputs": "numerator i32 + tau_a f64 + tau_b f64 in job-id order"},
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / len(e2e_times)},
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / len(e2e_times),
+                    "api": "TauEngine.all_pairs_host (pinned host values in, tau_b f64 for every job id out; "
+                           "row bands overlap D2H with compute)", "gpu_launches_per_step": e2e_launches},
             "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
             "abi": _lib.TB_MAX_N and "libtaub200.so",
         }

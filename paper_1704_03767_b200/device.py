@@ -182,7 +182,8 @@ class TauEngine:
             res.launches += 1
         return res
 
-    def _gemm_path(self, x, res: PairResult, st, full_counts: bool, splits: int, simt: bool):
+    def _gemm_prepare(self, x, res: PairResult, st, simt: bool = False):
+        """K0 rank transform + K2 sign pack of every row: the GEMM operand S (m x K signs)."""
         m, n = res.m, res.n
         K = int(_lib.load().tb_sign_k(n))  # padded diagonal layout, >= n(n-1)/2 elements
         fmt = self.sign_format(K) if not simt else _lib.TB_SIGN_I8
@@ -195,46 +196,129 @@ class TauEngine:
         S = self._buf("S", m * ldS, torch.int8)
         _lib.call("tb_sign_pack", _ptr(R), m, n, ldr, _ptr(S), ldS, fmt, st)
         res.launches += 2
-        def gemm(src, out):
-            if simt:
-                _lib.call("tb_gemm_pairs_simt", _ptr(src), m, K, ldS, res.job_lo, res.job_hi, _ptr(out), st)
-            else:
-                _lib.call("tb_gemm_pairs", _ptr(src), m, K, ldS, fmt, res.job_lo, res.job_hi, splits, _ptr(out), st)
-
         res.extra["sign_format"] = fmt
+        return S, K, ldS, fmt
+
+    def _gemm_numerator(self, src, out, m, K, ldS, fmt, job_lo, job_hi, st, splits=0, simt=False):
+        if simt:
+            _lib.call("tb_gemm_pairs_simt", _ptr(src), m, K, ldS, job_lo, job_hi, _ptr(out), st)
+        else:
+            _lib.call("tb_gemm_pairs", _ptr(src), m, K, ldS, fmt, job_lo, job_hi, splits, _ptr(out), st)
+
+    def _gemm_path(self, x, res: PairResult, st, full_counts: bool, splits: int, simt: bool):
+        m, n = res.m, res.n
+        S, K, ldS, fmt = self._gemm_prepare(x, res, st, simt)
         self._mark(0)
-        gemm(S, res.numerator)
+        self._gemm_numerator(S, res.numerator, m, K, ldS, fmt, res.job_lo, res.job_hi, st, splits, simt)
         self._mark(1)
         res.launches += 1
         if full_counts:
             A = self._buf("A", m * ldS, torch.int8)
             _lib.call("tb_abs_pack", _ptr(S), m, ldS, fmt, _ptr(A), st)
             absdot = self._buf("absdot", res.count, torch.int32)
-            gemm(A, absdot)
+            self._gemm_numerator(A, absdot, m, K, ldS, fmt, res.job_lo, res.job_hi, st, splits, simt)
             res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
             res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
             _lib.call("tb_full_counts", _ptr(res.numerator), _ptr(absdot), _ptr(res.n1_rows), m, n,
                       res.job_lo, res.job_hi, _ptr(res.n_d), _ptr(res.n3), st)
             res.launches += 3
 
-    def _merge_path(self, x, res: PairResult, st):
+    # -------------------------------------------------------------- host-buffer entry point
+    @staticmethod
+    def bands(m: int, nbands: int, align: int = 256) -> list[int]:
+        """Row boundaries splitting the pair triangle into ~equal-pair bands, aligned to the GEMM row block."""
+        cuts = [0]
+        for i in range(1, nbands):
+            f = i / nbands
+            r = int(round(m * (1.0 - (1.0 - f) ** 0.5) / align)) * align
+            if cuts[-1] < r < m:
+                cuts.append(r)
+        cuts.append(m)
+        return cuts
+
+    def all_pairs_host(self, x_host: torch.Tensor, tau_b_out: torch.Tensor, kernel: str = "auto",
+                       nbands: int = 4, stream: torch.cuda.Stream | None = None,
+                       copy_stream: torch.cuda.Stream | None = None) -> PairResult:
+        """End-to-end from host buffers: H2D of the values, the device path, tau_b back to host.
+
+        The job range is cut into row bands; band i's tau_b copy (on ``copy_stream``) overlaps
+        band i+1's numerator kernel.  ``x_host`` and ``tau_b_out`` should be pinned; the call is
+        asynchronous on ``stream`` (which finally waits for the copies).
+        """
+        st_t = stream if stream is not None else torch.cuda.current_stream()
+        cp_t = copy_stream if copy_stream is not None else self._copy_stream()
+        m, n = x_host.shape
+        total = m * (m + 1) // 2
+        if tau_b_out.numel() < total:
+            raise ConfigError(f"tau_b_out holds {tau_b_out.numel()} values, need {total}")
+        path = self.choose_path(n) if kernel == "auto" else kernel
+        st = _stream_ptr(st_t)
+        self._events, self._stream = None, st_t
+        with torch.cuda.stream(st_t):
+            x = x_host.to(self.device, non_blocking=True)
+            if path == "merge" and x.dtype != torch.int32:
+                raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
+            res = PairResult(m=m, n=n, job_lo=0, job_hi=total, path=path,
+                             numerator=self._buf("num_all", total, torch.int32),
+                             n1_rows=torch.empty(m, dtype=torch.int64, device=self.device),
+                             flags=torch.zeros(1, dtype=torch.int32, device=self.device))
+            res.tau_b = self._buf("taub_all", total, torch.float64)
+            if path == "gemm":
+                S, K, ldS, fmt = self._gemm_prepare(x, res, st)
+            else:
+                pos, srt, maxgrp = self._merge_prepare(x, res, st)
+            cuts = self.bands(m, nbands)
+            for r0, r1 in zip(cuts[:-1], cuts[1:]):
+                lo, hi = r0 * (2 * m - r0 + 1) // 2, r1 * (2 * m - r1 + 1) // 2
+                num = res.numerator[lo:hi]
+                if path == "gemm":
+                    self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st)
+                else:
+                    _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), m,
+                              n, lo, hi, _ptr(num), None, None, st)
+                tb = res.tau_b[lo:hi]
+                _lib.call("tb_finalize", _ptr(num), _ptr(res.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
+                res.launches += 2
+                ev = torch.cuda.Event()
+                ev.record(st_t)
+                cp_t.wait_event(ev)
+                with torch.cuda.stream(cp_t):
+                    tau_b_out[lo:hi].copy_(tb, non_blocking=True)
+            st_t.wait_stream(cp_t)
+        return res
+
+    def _copy_stream(self) -> torch.cuda.Stream:
+        cs = getattr(self, "_cs", None)
+        if cs is None:
+            cs = torch.cuda.Stream(device=self.device)
+            self._cs = cs
+        return cs
+
+    def _merge_prepare(self, x, res: PairResult, st):
+        """K1 presort of every variable (u-order positions, sorted ranks, n1, largest tie group)."""
         m, n = res.m, res.n
         if x.dtype != torch.int32:
             raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
-        x = x.contiguous()
         pos = self._buf("pos", m * n, torch.int32)
         srt = self._buf("sorted", m * n, torch.int32)
         work = self._buf("work", m * n, torch.int32)
         maxgrp = self._buf("maxgrp", m, torch.int32)
         _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp),
                   _ptr(work), _ptr(res.flags), st)
+        res.launches += 1
+        return pos, srt, maxgrp
+
+    def _merge_path(self, x, res: PairResult, st):
+        m, n = res.m, res.n
+        x = x.contiguous()
+        pos, srt, maxgrp = self._merge_prepare(x, res, st)
         res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
         res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
         self._mark(0)
         _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), m, n,
                   res.job_lo, res.job_hi, _ptr(res.numerator), _ptr(res.n_d), _ptr(res.n3), st)
         self._mark(1)
-        res.launches += 2
+        res.launches += 1
 
 
 _ENGINES: dict[int, TauEngine] = {}
