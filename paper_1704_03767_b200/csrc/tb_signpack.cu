@@ -90,7 +90,7 @@ __device__ __forceinline__ uint32_t pack_nibbles(uint32_t a, uint32_t b) {
 }
 
 template <int FMT>
-__global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __restrict__ R, int64_t n,
+__global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t* __restrict__ R, int64_t n,
                                                               int64_t ldr, int8_t* __restrict__ S, int64_t ldS,
                                                               int64_t K, int nwc) {
     extern __shared__ __align__(16) uint32_t sp_words[];  // [8][nwc]
@@ -112,12 +112,12 @@ __global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __
     __syncthreads();
 
     int8_t* row = S + r * ldS;
-    const int64_t nchunks = K >> 4;
-    const int64_t per = (nchunks + gridDim.y - 1) / gridDim.y;
-    const int64_t b_lo = (int64_t)blockIdx.y * per, b_hi = min(b_lo + per, nchunks);
-    const int64_t wper = (b_hi - b_lo + (SP_THREADS / 32) - 1) / (SP_THREADS / 32);
-    const int64_t c_lo = b_lo + warp * wper, c_hi = min(c_lo + wper, b_hi);
-    int64_t c = c_lo + lane;
+    const int nchunks = (int)(K >> 4);  // < 2^31: K < 2^34 for n <= 32767... K/16 < 2^30
+    const int per = (nchunks + (int)gridDim.y - 1) / (int)gridDim.y;
+    const int b_lo = (int)blockIdx.y * per, b_hi = min(b_lo + per, nchunks);
+    const int wper = (b_hi - b_lo + (SP_THREADS / 32) - 1) / (SP_THREADS / 32);
+    const int c_lo = b_lo + warp * wper, c_hi = min(c_lo + wper, b_hi);
+    int c = c_lo + lane;
     if (c < c_hi) {
         // decode chunk c -> (d, g): off(d)/16 = P(n-1) - P(n-d) <= c < P(n-1) - P(n-d-1)
         const int64_t top = ceil16_prefix(nn - 1);
@@ -125,9 +125,11 @@ __global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __
         int d = nn - N;
         int g = (int)(c - (top - ceil16_prefix(N)));
         int G = (nn - d + 15) >> 4;
-        for (; c < c_hi; c += 32) {
+        // window base of offset d: copy (d & 1, (d >> 1) & 3), 16-byte-aligned word (d >> 1) & ~3
+        int wbase = ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + ((d >> 1) & ~3);
+        for (;;) {
             const uint32_t* own_p = sp_words + 8 * g;
-            const uint32_t* win_p = sp_words + ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + 8 * g + ((d >> 1) & ~3);
+            const uint32_t* win_p = sp_words + wbase + 8 * g;
             const uint4 o0 = lds128(own_p), o1 = lds128(own_p + 4);
             const uint4 w0 = lds128(win_p), w1 = lds128(win_p + 4);
             const uint32_t own[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
@@ -144,14 +146,19 @@ __global__ void __launch_bounds__(SP_THREADS) signpack_kernel(const uint16_t* __
                 v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             }
             if (FMT == 2)
-                *reinterpret_cast<uint2*>(row + 8 * c) = make_uint2(pack_nibbles(v.x, v.y), pack_nibbles(v.z, v.w));
+                *reinterpret_cast<uint2*>(row + 8u * (uint32_t)c) = make_uint2(pack_nibbles(v.x, v.y), pack_nibbles(v.z, v.w));
             else
-                *reinterpret_cast<uint4*>(row + 16 * c) = v;
+                *reinterpret_cast<uint4*>(row + 16 * (int64_t)c) = v;
+            c += 32;
+            if (c >= c_hi) break;
             g += 32;
-            while (g >= G && d < nn - 1) {
-                g -= G;
-                ++d;
-                G = (nn - d + 15) >> 4;
+            if (g >= G) {
+                do {
+                    g -= G;
+                    ++d;
+                    G = (nn - d + 15) >> 4;
+                } while (g >= G);
+                wbase = ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + ((d >> 1) & ~3);
             }
         }
     }
