@@ -373,10 +373,14 @@ def run_ours(args):
                     "algorithmic": f"2*K ops per i<j pair, K=n(n-1)/2={K} sample pairs; {my_pairs} pairs per launch",
                     "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}
         else:
-            roof = {"bound": "int32", "achieved": achieved / 1e12, "peak": None, "unit": "TOP/s",
-                    "frac": None, "traffic": traffic, "kernel": "merge_pairs_kernel",
-                    "algorithmic": f"4*n*ceil(log2 n) INT32 ops per pair, n={n}",
-                    "kernel_ms": 1e3 * gemm_avg}
+            # nominal INT32 issue: 128 lanes/clk/SM (Blackwell unified FP32/INT32 cores) x SMs x max SM clock
+            props = torch.cuda.get_device_properties(dev)
+            int32_peak = 128 * props.multi_processor_count * 1.965e9
+            roof = {"bound": "int32", "achieved": achieved / 1e12, "peak": int32_peak / 1e12, "unit": "TOP/s",
+                    "frac": achieved / int32_peak, "traffic": traffic, "kernel": "merge_pairs_kernel",
+                    "peak_source": f"nominal INT32 issue 128 lanes/clk/SM x {props.multi_processor_count} SMs x 1.965 GHz",
+                    "algorithmic": f"4*n*ceil(log2 n) INT32 ops per i<j pair, n={n}; {my_pairs} pairs per launch",
+                    "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             ranks = host_ranks(x)

@@ -122,18 +122,46 @@ __global__ void __launch_bounds__(PS_THREADS) presort_kernel(const int32_t* __re
     }
 }
 
+// Compact tie-group list per variable: groups[r, 2k] = first u-order position, groups[r, 2k+1] =
+// length, for every rank value held by >= 2 observations (order of k arbitrary); ngroups[r] = count.
+__global__ void __launch_bounds__(256) tie_groups_kernel(const int32_t* __restrict__ sorted, int64_t n,
+                                                         int32_t* __restrict__ groups,
+                                                         int32_t* __restrict__ ngroups) {
+    const int64_t r = blockIdx.x;
+    const int32_t* so = sorted + r * n;
+    int32_t* gr = groups + r * n;
+    __shared__ int32_t cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (int64_t p = threadIdx.x; p + 1 < n; p += blockDim.x) {
+        const int32_t v = so[p];
+        if ((p == 0 || so[p - 1] != v) && so[p + 1] == v) {
+            int64_t lo = p + 1, hi = n;  // first position with a larger rank
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (so[mid] == v) lo = mid + 1;
+                else hi = mid;
+            }
+            const int32_t k = atomicAdd(&cnt, 1);
+            gr[2 * k] = (int32_t)p;
+            gr[2 * k + 1] = (int32_t)(lo - p);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) ngroups[r] = cnt;
+}
+
 // ===================================================================== K4
 constexpr int MG_THREADS = 1024;
+constexpr int MG_SMALL_GROUP = 64;  // tie groups up to this size: one thread per group
 constexpr int MG_HALF = 32768;  // largest block sorted in shared memory
 
-// Shared-memory key index swizzle: merge-path threads own contiguous output segments, which would
-// put every lane of a warp in the same two banks (16-way conflicts).  XOR-ing the low five bits of
-// the 32-bit word index with the next five spreads a warp's segments over all 32 banks; the map is
-// a bijection on every aligned 64-key block.
-__device__ __forceinline__ int sw(int e) {
-    const int w = e >> 1;
-    return ((w ^ ((w >> 5) & 31)) << 1) | (e & 1);
-}
+// Shared-memory key layout: 2 pad keys (one 32-bit word) after every 32 keys.  Merge-path threads
+// own contiguous output segments, so a warp's cursors sit ~16 keys apart; the padding spreads them
+// (and the per-thread 16-word runs of load_run/store_words, 17 words apart) over all 32 banks.
+// Logical key e lives at padded index e + 2 (e >> 5); word w at w + (w >> 4).
+__device__ __forceinline__ int sw(int e) { return e + ((e >> 5) << 1); }
+__device__ __forceinline__ int swp_words(int w) { return w + (w >> 4); }
 
 // Branch-free sequential merge of `count` outputs of the runs A = src[s, s+W), B = src[s+W, s+2W)
 // starting from (i, j); returns the strict-inversion contribution (kernel_sorted.py:72-73 rule:
@@ -197,10 +225,172 @@ __device__ uint32_t sort_count_block(uint16_t* keys, uint16_t* tmp, int L) {
     return inv;
 }
 
+// ---------------------------------------------------------------------------------------------
+// K4 v2 sort-and-count.  Thread t owns keys [E t, E t + E) of the block.
+//
+// Level 1..log2(E) (runs up to E keys) run in registers: bitonic merges of composite keys
+// (key << 1 | origin), origin 0 for the left run A and 1 for the right run B of each merge.  A
+// correct sort of the composites is a stable merge with A first on ties, so the B element of
+// B-rank j at merged position p has exactly h - (p - j) A elements strictly greater than it:
+// inv(A, B) = h^2 + h(h-1)/2 - sum(positions of B elements)   (h = run length).
+//
+// Levels log2(E)+1 .. log2(L) are merge-path merges: each thread merges its E outputs into
+// registers (statically indexed, fully unrolled) counting the reference's way (right element
+// strictly smaller => + unconsumed left length, kernel_sorted.py:72-73), then writes them back.
+//
+// Shared-memory traffic of a thread's E keys uses 32-bit words at swizzled addresses: the thread's
+// E/2 words are w = (E/2) t + q and the swizzle (sw, above) makes each of those loads/stores
+// conflict-free across a warp.
+template <int E>
+__device__ __forceinline__ void load_run(const uint16_t* keys, int t, uint32_t (&v)[E]) {
+    const uint32_t* wk = reinterpret_cast<const uint32_t*>(keys);
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q) {
+        const int w = (E / 2) * t + q;
+        const uint32_t word = wk[swp_words(w)];
+        v[2 * q] = word & 0xFFFFu;
+        v[2 * q + 1] = word >> 16;
+    }
+}
+template <int E>
+__device__ __forceinline__ void store_words(uint16_t* keys, int t, const uint32_t (&ow)[E / 2]) {
+    uint32_t* wk = reinterpret_cast<uint32_t*>(keys);
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q) {
+        const int w = (E / 2) * t + q;
+        wk[swp_words(w)] = ow[q];
+    }
+}
+template <int E>
+__device__ __forceinline__ void store_run(uint16_t* keys, int t, const uint32_t (&v)[E]) {
+    uint32_t* wk = reinterpret_cast<uint32_t*>(keys);
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q) {
+        const int w = (E / 2) * t + q;
+        wk[swp_words(w)] = (v[2 * q] & 0xFFFFu) | (v[2 * q + 1] << 16);
+    }
+}
+
+// Sort v[0..E) ascending (values are 16-bit keys), returning the strict inversion count.
+template <int E>
+__device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
+    uint32_t inv = 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] <<= 1;
+#pragma unroll
+    for (int k = 2; k <= E; k <<= 1) {
+        const int h = k / 2;
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = (v[i] & ~1u) | ((i % k) >= h ? 1u : 0u);
+        // first stage: compare i with its mirror in the run (turns two ascending runs into halves)
+#pragma unroll
+        for (int base = 0; base < E; base += k) {
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const uint32_t a = v[base + i], b = v[base + k - 1 - i];
+                v[base + i] = min(a, b);
+                v[base + k - 1 - i] = max(a, b);
+            }
+        }
+        // half-cleaners
+#pragma unroll
+        for (int j = h / 2; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                if (i & j) continue;
+                const uint32_t a = v[i], b = v[i + j];
+                v[i] = min(a, b);
+                v[i + j] = max(a, b);
+            }
+        }
+        uint32_t pos = 0;
+#pragma unroll
+        for (int i = 0; i < E; ++i) pos += (v[i] & 1u) * (uint32_t)(i % k);
+        inv += (uint32_t)(E / k) * (uint32_t)(h * h + h * (h - 1) / 2) - pos;
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] >>= 1;
+    return inv;
+}
+
+template <int E>
+__device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L) {
+    const int t = threadIdx.x;
+    const int active = L / E;  // L is a multiple of E
+    uint32_t inv = 0;
+    if (t < active) {
+        uint32_t v[E];
+        load_run<E>(keys, t, v);
+        inv += reg_sort_count<E>(v);
+        store_run<E>(keys, t, v);
+    }
+    __syncthreads();
+    uint16_t* src = keys;
+    uint16_t* dst = tmp;
+    for (int W = E; W < L; W <<= 1) {
+        if (t < active) {
+            const int d0 = t * E;
+            const int P = 2 * W;
+            const int s = (d0 / P) * P;  // pair start
+            const int d = d0 - s;        // diagonal inside the pair (W >= E: a thread never spans pairs)
+            int lo = d > W ? d - W : 0, hi = d < W ? d : W;
+            while (lo < hi) {  // merge-path search: i = #A among the first d outputs
+                const int mid = (lo + hi) >> 1;
+                if (src[sw(s + mid)] <= src[sw(s + W + d - mid - 1)]) lo = mid + 1;
+                else hi = mid;
+            }
+            int i = lo, j = d - lo;
+            uint32_t a = src[sw(min(s + i, s + W - 1))];
+            uint32_t b = src[sw(min(s + W + j, s + 2 * W - 1))];
+            uint32_t ow[E / 2];
+#pragma unroll
+            for (int o = 0; o < E; ++o) {
+                const bool takeA = (j >= W) || ((i < W) && (a <= b));
+                const uint32_t val = takeA ? a : b;
+                if (o & 1) ow[o >> 1] |= val << 16;
+                else ow[o >> 1] = val;
+                inv += takeA ? 0u : (uint32_t)(W - i);
+                i += takeA;
+                j += !takeA;
+                const int idx = min(takeA ? (s + i) : (s + W + j), s + 2 * W - 1);  // exhausted runs: value unused
+                const uint32_t nv = src[sw(idx)];
+                a = takeA ? nv : a;
+                b = takeA ? b : nv;
+            }
+            store_words<E>(dst, t, ow);
+        }
+        __syncthreads();
+        uint16_t* tt = src;
+        src = dst;
+        dst = tt;
+    }
+    if (src != keys) {
+        if (t < active) {
+            uint32_t v[E];
+            load_run<E>(src, t, v);
+            store_run<E>(keys, t, v);
+        }
+        __syncthreads();
+    }
+    return inv;
+}
+
+__device__ __forceinline__ uint32_t sort_count_any(uint16_t* keys, uint16_t* tmp, int L) {
+    if (L >= 32 * MG_THREADS) return sort_count_block_v2<32>(keys, tmp, L);
+    if (L >= 16 * MG_THREADS) return sort_count_block_v2<16>(keys, tmp, L);
+    if (L >= 8 * MG_THREADS) return sort_count_block_v2<8>(keys, tmp, L);
+    if (L >= 4 * MG_THREADS) return sort_count_block_v2<4>(keys, tmp, L);
+    if (L >= 2 * MG_THREADS) return sort_count_block_v2<2>(keys, tmp, L);
+    return sort_count_block(keys, tmp, L);
+}
+
 struct MergeArgs {
     const int32_t* ranks;
     const int32_t* pos;
     const int32_t* sorted;
+    const int32_t* maxgrp;
+    const int32_t* groups;
+    const int32_t* ngroups;
     const unsigned long long* n1;
     int64_t m, n, n0;
     int64_t job_lo, count;
@@ -213,8 +403,8 @@ struct MergeArgs {
 
 __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p) {
     extern __shared__ __align__(16) uint8_t mg_smem[];
-    uint16_t* keys = reinterpret_cast<uint16_t*>(mg_smem);  // B * L
-    uint16_t* tmp = keys + (size_t)p.B * p.L;               // L
+    uint16_t* keys = reinterpret_cast<uint16_t*>(mg_smem);  // B * L keys (padded layout)
+    uint16_t* tmp = keys + sw(p.B * p.L) + 2;               // L keys (padded layout)
     __shared__ int64_t red[32];
     const int tid = threadIdx.x;
     const int64_t n = p.n;
@@ -230,11 +420,38 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
 
         // pads (max key) first, then scatter w[pos_u[e]] = rank_v[e]
         for (int64_t i = n + tid; i < (int64_t)p.B * L; i += MG_THREADS) keys[sw((int)i)] = 0xFFFF;
-        for (int64_t e = tid; e < n; e += MG_THREADS) keys[sw(pu[e])] = (uint16_t)rv[e];
+        if ((n & 3) == 0) {  // 16-byte loads of u-positions and v-ranks
+            const int4* pu4 = reinterpret_cast<const int4*>(pu);
+            const int4* rv4 = reinterpret_cast<const int4*>(rv);
+            for (int64_t e = tid; e < (n >> 2); e += MG_THREADS) {
+                const int4 P = pu4[e], V = rv4[e];
+                keys[sw(P.x)] = (uint16_t)V.x;
+                keys[sw(P.y)] = (uint16_t)V.y;
+                keys[sw(P.z)] = (uint16_t)V.z;
+                keys[sw(P.w)] = (uint16_t)V.w;
+            }
+        } else {
+            for (int64_t e = tid; e < n; e += MG_THREADS) keys[sw(pu[e])] = (uint16_t)rv[e];
+        }
         __syncthreads();
 
         // within-u-group pairs: inv_g and joint ties (n3)
         uint32_t inv_g = 0, ties = 0;
+        if (p.maxgrp[y] <= MG_SMALL_GROUP) {  // few small groups (the usual case): walk the compact list
+            const int32_t* gl = p.groups + y * n;
+            const int32_t ng = p.ngroups[y];
+            for (int32_t k = tid; k < ng; k += MG_THREADS) {
+                const int32_t g0 = gl[2 * k], gl_len = gl[2 * k + 1];
+                for (int32_t qa = g0; qa < g0 + gl_len; ++qa) {
+                    const uint16_t wq = keys[sw(qa)];
+                    for (int32_t qb = qa + 1; qb < g0 + gl_len; ++qb) {
+                        const uint16_t wt = keys[sw(qb)];
+                        inv_g += (wq > wt);
+                        ties += (wq == wt);
+                    }
+                }
+            }
+        } else
         for (int64_t q = tid; q + 1 < n; q += MG_THREADS) {
             const int32_t g = su[q];
             if (su[q + 1] != g) continue;
@@ -248,16 +465,16 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         __syncthreads();
 
         // inv(w)
-        uint32_t inv = sort_count_block(keys, tmp, L);
+        uint32_t inv = sort_count_any(keys, tmp, L);
         if (p.B == 2) {
-            inv += sort_count_block(keys + L, tmp, L);  // L >= 64 here: swizzle blocks stay aligned
+            inv += sort_count_any(keys + sw(L), tmp, L);  // L = 32768: sw(L + i) = sw(L) + sw(i)
             // cross inversions: for each b in block 1, # of block-0 keys > b
             const int64_t L2 = n - L1;
             const int64_t per = (L2 + MG_THREADS - 1) / MG_THREADS;
             const int64_t b0 = tid * per, b1 = min(b0 + per, L2);
             if (b0 < b1) {
                 const uint16_t* H1 = keys;
-                const uint16_t* H2 = keys + L;
+                const uint16_t* H2 = keys + sw(L);
                 uint16_t b = H2[sw((int)b0)];
                 int64_t lo = 0, hi = L1;  // upper_bound(H1, b)
                 while (lo < hi) {
@@ -294,21 +511,25 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
 using namespace tb;
 
 extern "C" int tb_presort(const int32_t* ranks, int64_t m, int64_t n, int32_t* pos, int32_t* sorted, uint64_t* n1,
-                          int32_t* maxgrp, int32_t* work, int32_t* flags, void* stream) {
+                          int32_t* maxgrp, int32_t* work, int32_t* ngroups, int32_t* flags, void* stream) {
     if (m < 1 || n < 1) return fail(TB_ERR_INVALID, "presort: empty input");
     if (n > TB_MAX_N) return fail(TB_ERR_CAPACITY, "presort: n=%lld exceeds %d", (long long)n, TB_MAX_N);
-    if (!ranks || !pos || !sorted || !n1 || !maxgrp || !work || !flags)
+    if (!ranks || !pos || !sorted || !n1 || !maxgrp || !work || !ngroups || !flags)
         return fail(TB_ERR_INVALID, "presort: null pointer");
     if (m > INT32_MAX) return fail(TB_ERR_CAPACITY, "presort: m too large");
     presort_kernel<<<(unsigned)m, PS_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
         ranks, n, pos, sorted, reinterpret_cast<unsigned long long*>(n1), maxgrp, work, flags);
-    return check_launch("presort_kernel");
+    int rc = check_launch("presort_kernel");
+    if (rc) return rc;
+    tie_groups_kernel<<<(unsigned)m, 256, 0, static_cast<cudaStream_t>(stream)>>>(sorted, n, work, ngroups);
+    return check_launch("tie_groups_kernel");
 }
 
 extern "C" int tb_merge_pairs(const int32_t* ranks, const int32_t* pos, const int32_t* sorted,
-                              const uint64_t* n1_rows, const int32_t* maxgrp, int64_t m, int64_t n, int64_t job_lo,
-                              int64_t job_hi, int32_t* num, uint64_t* nd, uint64_t* n3, void* stream) {
-    (void)maxgrp;
+                              const uint64_t* n1_rows, const int32_t* maxgrp, const int32_t* groups,
+                              const int32_t* ngroups, int64_t m, int64_t n, int64_t job_lo, int64_t job_hi,
+                              int32_t* num, uint64_t* nd, uint64_t* n3, void* stream) {
+    if (!maxgrp || !groups || !ngroups) return fail(TB_ERR_INVALID, "merge: null tie-group arrays");
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "merge: need m >= 1 and n >= 2");
     if (n > TB_MAX_N) return fail(TB_ERR_CAPACITY, "merge: n=%lld exceeds %d", (long long)n, TB_MAX_N);
     const int64_t total = m * (m + 1) / 2;
@@ -319,6 +540,9 @@ extern "C" int tb_merge_pairs(const int32_t* ranks, const int32_t* pos, const in
     a.ranks = ranks;
     a.pos = pos;
     a.sorted = sorted;
+    a.maxgrp = maxgrp;
+    a.groups = groups;
+    a.ngroups = ngroups;
     a.n1 = reinterpret_cast<const unsigned long long*>(n1_rows);
     a.m = m;
     a.n = n;
@@ -333,7 +557,8 @@ extern "C" int tb_merge_pairs(const int32_t* ranks, const int32_t* pos, const in
     a.num = num;
     a.nd = reinterpret_cast<unsigned long long*>(nd);
     a.n3 = reinterpret_cast<unsigned long long*>(n3);
-    size_t smem = (size_t)(a.B + 1) * L * sizeof(uint16_t);
+    const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> 5) + 2 + L + 2 * ((size_t)L >> 5) + 2;
+    size_t smem = padded * sizeof(uint16_t);
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = std::min<int64_t>(a.count, (int64_t)num_sms());
     merge_pairs_kernel<<<(unsigned)grid, MG_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(a);

@@ -274,8 +274,8 @@ class TauEngine:
                 if path == "gemm":
                     self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st)
                 else:
-                    _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), m,
-                              n, lo, hi, _ptr(num), None, None, st)
+                    _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp[0]),
+                              _ptr(maxgrp[1]), _ptr(maxgrp[2]), m, n, lo, hi, _ptr(num), None, None, st)
                 tb = res.tau_b[lo:hi]
                 _lib.call("tb_finalize", _ptr(num), _ptr(res.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
                 res.launches += 2
@@ -303,19 +303,21 @@ class TauEngine:
         srt = self._buf("sorted", m * n, torch.int32)
         work = self._buf("work", m * n, torch.int32)
         maxgrp = self._buf("maxgrp", m, torch.int32)
+        ngroups = self._buf("ngroups", m, torch.int32)
         _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp),
-                  _ptr(work), _ptr(res.flags), st)
-        res.launches += 1
-        return pos, srt, maxgrp
+                  _ptr(work), _ptr(ngroups), _ptr(res.flags), st)
+        res.launches += 2
+        return pos, srt, (maxgrp, work, ngroups)
 
     def _merge_path(self, x, res: PairResult, st):
         m, n = res.m, res.n
         x = x.contiguous()
-        pos, srt, maxgrp = self._merge_prepare(x, res, st)
+        pos, srt, (maxgrp, groups, ngroups) = self._merge_prepare(x, res, st)
         res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
         res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
         self._mark(0)
-        _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), m, n,
+        _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), _ptr(groups),
+                  _ptr(ngroups), m, n,
                   res.job_lo, res.job_hi, _ptr(res.numerator), _ptr(res.n_d), _ptr(res.n3), st)
         self._mark(1)
         res.launches += 1
