@@ -227,6 +227,40 @@ def measure_int8_peak(torch, dev):
         return None
 
 
+def measure_fp4_peak(torch, dev):
+    """Library MXFP4 GEMM throughput: cuBLASLt block-scaled e2m1 (torch.nn.functional.scaled_mm,
+    BlockWise1x32 ue8m0 scales) 8192 x 8192 x 32768, best of 5 -- the attainable FP4 tensor rate
+    a stock library reaches on this GPU (tools/probe_fp4_peak.py, profiles/r01_fp4_library_peak.json)."""
+    try:
+        import torch.nn.functional as F
+        M = N = 8192
+        K = 32768
+        a = torch.randint(0, 256, (M, K // 2), dtype=torch.uint8, device=dev).view(torch.float4_e2m1fn_x2)
+        b = torch.randint(0, 256, (N, K // 2), dtype=torch.uint8, device=dev).view(torch.float4_e2m1fn_x2)
+        sa = torch.full((M, K // 32), 127, dtype=torch.uint8, device=dev).view(torch.float8_e8m0fnu)
+        sb = torch.full((N, K // 32), 127, dtype=torch.uint8, device=dev).view(torch.float8_e8m0fnu)
+
+        def f():
+            return F.scaled_mm(a, b.t(), sa, F.ScalingType.BlockWise1x32, sb, F.ScalingType.BlockWise1x32,
+                               swizzle_a=F.SwizzleType.SWIZZLE_32_4_4, swizzle_b=F.SwizzleType.SWIZZLE_32_4_4,
+                               output_dtype=torch.bfloat16)
+        for _ in range(3):
+            f()
+        best = float("inf")
+        for _ in range(5):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            f()
+            e.record()
+            e.synchronize()
+            best = min(best, s.elapsed_time(e) / 1e3)
+        del a, b, sa, sb
+        return 2.0 * M * N * K / best
+    except Exception as exc:  # noqa: BLE001
+        print(f"# fp4 library peak probe failed: {exc}", file=sys.stderr)
+        return None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -357,6 +391,7 @@ def run_ours(args):
             traffic = tj.get(f"config{args.config}", {}).get("dram_bytes_per_launch")
         if path == "gemm":
             fp4 = sign_format == _lib.TB_SIGN_E2M1
+            fp4_lib = measure_fp4_peak(torch, dev) if fp4 else None
             if fp4:
                 pk, src = 9.0e15, "nominal dense FP4 (kind::mxf4) 9 PFLOP/s, B200_PROFILING.md table (no measured FP4 entry)"
             else:
@@ -369,6 +404,8 @@ def run_ours(args):
                     else "gemm_tc2_kernel (tcgen05.mma kind::i8, 2-SM)",
                     "peak_source": src,
                     "frac_of_measured_int8_peak": (achieved / peak) if peak else None,
+                    "measured_fp4_library_tflops": fp4_lib / 1e12 if fp4_lib else None,
+                    "frac_of_measured_fp4_library": (achieved / fp4_lib) if fp4_lib else None,
                     "measured_int8_peak_tops": peak / 1e12 if peak else None,
                     "algorithmic": f"2*K ops per i<j pair, K=n(n-1)/2={K} sample pairs; {my_pairs} pairs per launch",
                     "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}

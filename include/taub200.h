@@ -70,6 +70,9 @@ typedef struct {
 
 const char *tb_last_error(void);
 int tb_query(int device, tb_caps *caps);
+/* Number of kernels this library has launched since load (all threads, all devices): the
+ * launch-count evidence bench.py reports as gpu_launches. */
+int64_t tb_launch_count(void);
 
 /*
  * K0 rank transform (rank_transform, src/taucorr/ranks.py:37-61, for all rows

@@ -28,6 +28,7 @@ _i32 = ctypes.c_int32
 _p = ctypes.c_void_p
 SIGNATURES = {
     "tb_last_error": ([], ctypes.c_char_p),
+    "tb_launch_count": ([], ctypes.c_int64),
     "tb_query": ([ctypes.c_int, _p], ctypes.c_int),
     "tb_sign_k": ([_i64], _i64),
     "tb_rank_rows": ([_p, ctypes.c_int, _i64, _i64, _i64, _p, _i64, _p, _p, _p], ctypes.c_int),

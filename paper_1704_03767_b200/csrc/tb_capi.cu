@@ -1,3 +1,4 @@
+#include <atomic>
 // C-ABI plumbing: error state, device query.
 #include <algorithm>
 #include <cstdarg>
@@ -24,7 +25,10 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+static std::atomic<int64_t> g_launches{0};
+
 int check_launch(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TB_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
     return TB_OK;
@@ -42,6 +46,8 @@ int num_sms() {
 using namespace tb;
 
 extern "C" const char* tb_last_error(void) { return g_err; }
+
+extern "C" int64_t tb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int tb_query(int device, tb_caps* caps) {
     if (!caps) return fail(TB_ERR_INVALID, "tb_query: null caps");

@@ -22,6 +22,12 @@ int check_launch(const char* what);
 
 int num_sms();
 
+// Split-K accumulation (tb_finalize.cu): an f32 device buffer of span (rounded up to 4) sums the
+// split partials with vector reds (exact: every partial and every running sum is an integer of
+// magnitude < 2^24 when K < 2^24), then accum_convert writes the int32 numerators.
+int accum_workspace(int64_t span, float** ws, cudaStream_t st);
+int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st);
+
 // ------------------------------------------------------------------ geometry
 // pairindex.py:20-24 row_prefix: cells strictly above row y = y(2m - y + 1)/2.
 __host__ __device__ __forceinline__ int64_t row_prefix(int64_t y, int64_t m) { return y * (2 * m - y + 1) / 2; }

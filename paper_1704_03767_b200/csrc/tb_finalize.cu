@@ -68,6 +68,37 @@ __global__ void __launch_bounds__(256) full_counts_kernel(const int32_t* __restr
         }
     }
 }
+// ------------------------------------------------------------------ split-K accumulation
+static float* g_accum = nullptr;
+static size_t g_accum_bytes = 0;
+
+int accum_workspace(int64_t span, float** ws, cudaStream_t st) {
+    const size_t bytes = (size_t)((span + 3) & ~int64_t(3)) * sizeof(float);
+    if (bytes > g_accum_bytes) {
+        if (g_accum) TB_CUDA_TRY(cudaFree(g_accum));
+        g_accum = nullptr;
+        g_accum_bytes = 0;
+        TB_CUDA_TRY(cudaMalloc(&g_accum, bytes));
+        g_accum_bytes = bytes;
+    }
+    TB_CUDA_TRY(cudaMemsetAsync(g_accum, 0, bytes, st));
+    *ws = g_accum;
+    return TB_OK;
+}
+
+__global__ void __launch_bounds__(256) accum_convert_kernel(const float* __restrict__ ws, int64_t span,
+                                                           int32_t* __restrict__ num) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < span; i += (int64_t)gridDim.x * blockDim.x)
+        num[i] = __float2int_rn(ws[i]);
+}
+
+int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st) {
+    if (span <= 0) return TB_OK;
+    const int64_t blocks = std::min<int64_t>((span + 255) / 256, (int64_t)num_sms() * 8);
+    accum_convert_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, span, num);
+    return check_launch("accum_convert_kernel");
+}
+
 }  // namespace tb
 
 extern "C" int tb_full_counts(const int32_t* num, const int32_t* absdot, const uint64_t* n1_rows, int64_t m,

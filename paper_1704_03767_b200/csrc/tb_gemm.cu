@@ -532,15 +532,20 @@ struct UnitTable {
     int32_t* dev = nullptr;
     int64_t count = 0, cap = 0;
 };
-static UnitTable g_units;
+static UnitTable g_unit_cache[8];  // per (m, job range): the banded host path cycles through a few
+static int g_unit_next = 0;
 
 static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t st, const int32_t** out,
                        int64_t* count) {
-    if (g_units.m == m && g_units.lo == job_lo && g_units.hi == job_hi) {
-        *out = g_units.dev;
-        *count = g_units.count;
-        return TB_OK;
-    }
+    for (const UnitTable& c : g_unit_cache)
+        if (c.m == m && c.lo == job_lo && c.hi == job_hi) {
+            *out = c.dev;
+            *count = c.count;
+            return TB_OK;
+        }
+    UnitTable& g_units = g_unit_cache[g_unit_next];
+    g_unit_next = (g_unit_next + 1) % 8;
+    g_units.m = -1;
     const int64_t T = gemm2::TILE, G = 4;
     const int64_t w = (m + T - 1) / T;
     const int64_t W = (w + G - 1) / G;

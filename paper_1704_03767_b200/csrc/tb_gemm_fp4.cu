@@ -38,37 +38,39 @@ constexpr uint32_t STAGE_BYTES = A_BYTES + NB * B_BYTES;
 constexpr int THREADS = 256;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t SF_COL = 480;
-constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+constexpr int STG_LD = 17;    // epilogue staging tile: 32 rows x 16 columns, padded row stride
+constexpr uint32_t STG_BYTES = 4 * (32 * STG_LD * 4 + 32 * 8);  // 4 epilogue warps: tile + row bases
+constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + STG_BYTES;
 }  // namespace g4
 
 struct Gemm4Args {
     int64_t m;
-    const int32_t* units;  // (row block << 16) | column block, rasterised
-    int64_t nunits;        // per split
-    int32_t splits;
-    int32_t nkb;           // 128-byte K blocks
+    const int4* items;     // {(row block << 16) | column block, kb0, kb1, 0}; pair p runs p, p + P, ...
+    int64_t nitems;
+    int32_t partial;       // some unit is split over K: every item accumulates into acc
     int64_t job_lo, job_hi;
     int32_t* num;
+    float* acc;      // split-K: f32 sums (exact integers < 2^24), red.global.add.v4.f32
+    unsigned long long* trace;  // TB_TRACE=1 (diagnostics): per CTA, per item: [accumulator ready, epilogue done]
 };
 
 struct Unit4 {
     int64_t y0, x0;
-    int32_t h_lo;
+    int32_t h_lo, h_hi;  // N blocks [h_lo, h_hi) hold upper-triangle columns inside the matrix
     int32_t kb0, kb1;
     bool partial;
 };
 
 __device__ __forceinline__ bool next_unit4(const Gemm4Args& p, int64_t& cur, int64_t step, Unit4& t) {
-    if (cur >= p.nunits * p.splits) return false;
-    const int32_t s = (int32_t)(cur / p.nunits);
-    const int64_t i = cur - (int64_t)s * p.nunits;
-    const int32_t e = p.units[i];
-    t.y0 = (int64_t)(e >> 16) * g4::UM;
-    t.x0 = (int64_t)(e & 0xFFFF) * g4::UN;
+    if (cur >= p.nitems) return false;
+    const int4 it = __ldg(&p.items[cur]);
+    t.y0 = (int64_t)(it.x >> 16) * g4::UM;
+    t.x0 = (int64_t)(it.x & 0xFFFF) * g4::UN;
     t.h_lo = (t.x0 + g4::BN - 1 < t.y0) ? 1 : 0;
-    t.kb0 = (int32_t)((int64_t)s * p.nkb / p.splits);
-    t.kb1 = (int32_t)((int64_t)(s + 1) * p.nkb / p.splits);
-    t.partial = p.splits > 1;
+    t.h_hi = (t.x0 + g4::BN >= p.m) ? 1 : g4::NB;
+    t.kb0 = it.y;
+    t.kb1 = it.z;
+    t.partial = p.partial != 0;
     cur += step;
     return true;
 }
@@ -123,14 +125,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             int64_t cur = pair;
             Unit4 t;
             while (next_unit4(p, cur, npairs, t)) {
-                const uint32_t bytes = 2 * (A_BYTES + (NB - t.h_lo) * B_BYTES);
+                const uint32_t bytes = 2 * (A_BYTES + (t.h_hi - t.h_lo) * B_BYTES);
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
                     uint8_t* sa = smem + stage * STAGE_BYTES;
                     tma_load_2d_2sm(sa, &tmap_a, fb, kb * BK, (int32_t)(t.y0 + rank * BM));
-                    for (int h = t.h_lo; h < NB; ++h)
+                    for (int h = t.h_lo; h < t.h_hi; ++h)
                         tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
                                         (int32_t)(t.x0 + h * BN + rank * BNH));
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -157,7 +159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < BK / UKB; ++k) {
                         const uint32_t acc = (kb > t.kb0 || k > 0) ? 1u : 0u;
-                        for (int h = t.h_lo; h < NB; ++h) {
+                        for (int h = t.h_lo; h < t.h_hi; ++h) {
                             const uint64_t bdesc = umma_desc_k_sw128(sa + A_BYTES + h * B_BYTES);
                             mma_mxf4_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k, idesc, sf, sf, acc);
                         }
@@ -170,42 +172,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             }
         }
     } else if (warp >= 4) {  // ---------------- epilogue (both CTAs)
+        // Each warp drains its 32 TMEM lanes (rows) in 32 x 16 chunks and writes them back
+        // transposed through shared memory: half a warp covers 16 consecutive columns of one row,
+        // i.e. 16 consecutive job ids, so every store / red instruction touches 2 short runs
+        // instead of 32 rows m ints apart.
         const int q = warp & 3;
+        int32_t* stg = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256) + q * (32 * STG_LD + 64);
+        int64_t* rowbase = reinterpret_cast<int64_t*>(stg + 32 * STG_LD);
         uint32_t acc_phase = 0;
         const int64_t m = p.m;
         const int64_t span = p.job_hi - p.job_lo;
         const uint32_t tempty_leader = mapa_shared(tempty, 0);
+        const int half = lane >> 4, col = lane & 15;
         int64_t cur = pair;
         Unit4 t;
         while (next_unit4(p, cur, npairs, t)) {
+            const int64_t y0 = t.y0 + rank * BM + q * 32;
+            {
+                const int64_t y = y0 + lane;
+                rowbase[lane] = (y < m) ? row_prefix(y, m) - y - p.job_lo : INT64_MIN / 2;
+            }
+            __syncwarp();
             mbar_wait(tfull, acc_phase);
             tc_fence_after();
-            const int64_t y = t.y0 + rank * BM + q * 32 + lane;
-            const int64_t base = row_prefix(y, m) - y - p.job_lo;
-            for (int h = t.h_lo; h < NB; ++h) {
+            int item = (int)((cur - pair) / npairs) - 1;
+            if (p.trace && q == 0 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2] = globaltimer();
+            for (int h = t.h_lo; h < t.h_hi; ++h) {
 #pragma unroll 1
                 for (int c = 0; c < BN; c += 16) {
                     uint32_t r[16];
                     tmem_ld_32x32b_x16(tmem_base + (uint32_t(q * 32) << 16) + h * BN + c, r);
                     tmem_ld_wait();
-                    if (y < m) {
+                    const int64_t xc = t.x0 + h * BN + c;
+                    if (xc >= m || xc + 15 < y0) continue;  // chunk right of the matrix or below the diagonal
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int64_t x = t.x0 + h * BN + c + i;
-                            const int64_t j = base + x;
-                            if (x >= y && x < m && j >= 0 && j < span) {
-                                const int32_t v = __float2int_rn(__uint_as_float(r[i]));
-                                if (t.partial)
-                                    atomicAdd(&p.num[j], v);
-                                else
-                                    p.num[j] = v;
+                    for (int i = 0; i < 16; ++i) stg[lane * STG_LD + i] = (int32_t)r[i];
+                    __syncwarp();
+                    if (t.partial) {
+                        // 32 rows x up to 5 aligned quads of job ids; lanes outside the row's valid
+                        // [ja, jb) add 0, so every red covers one aligned 16-byte quad.
+#pragma unroll 1
+                        for (int task = lane; task < 160; task += 32) {
+                            const int rr = task / 5, qi = task - rr * 5;
+                            const int64_t y = y0 + rr;
+                            const int64_t j0 = rowbase[rr] + xc;  // job id of column xc in row y
+                            const int64_t xa = xc > y ? xc : y;
+                            const int64_t xb = (xc + 16 < m) ? xc + 16 : m;
+                            int64_t ja = rowbase[rr] + xa, jb = rowbase[rr] + xb;
+                            if (ja < 0) ja = 0;
+                            if (jb > span) jb = span;
+                            const int64_t q = (ja & ~int64_t(3)) + 4 * qi;
+                            if (ja >= jb || q >= jb) continue;
+                            float v[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int64_t jj = q + e;
+                                v[e] = (jj >= ja && jj < jb) ? __int_as_float(stg[rr * STG_LD + (int)(jj - j0)]) : 0.0f;
                             }
+                            red_add_v4_f32(p.acc + q, v[0], v[1], v[2], v[3]);
+                        }
+                    } else {
+                        const int64_t x = xc + col;
+#pragma unroll 4
+                        for (int k = 0; k < 16; ++k) {
+                            const int rr = 2 * k + half;
+                            const int64_t y = y0 + rr;
+                            const int64_t j = rowbase[rr] + x;
+                            if (x >= y && x < m && j >= 0 && j < span)
+                                p.num[j] = __float2int_rn(__int_as_float(stg[rr * STG_LD + col]));
                         }
                     }
+                    __syncwarp();
                 }
             }
             tc_fence_before();
             __syncwarp();
+            if (p.trace && q == 0 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2 + 1] = globaltimer();
             if (lane == 0) mbar_arrive_cluster(tempty_leader);
             acc_phase ^= 1;
         }
@@ -218,53 +260,118 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     }
 }
 
-struct Unit4Table {
-    int64_t m = -1, lo = -1, hi = -1;
-    int32_t* dev = nullptr;
-    int64_t count = 0, cap = 0;
-};
-static Unit4Table g_units4;
-
+// ------------------------------------------------------------------ host work plan
 // Units (256-row block Yb, 480-column block Xb) that intersect the job range's rows and the upper
 // triangle, ordered by 8 x 4 super-blocks (2048 rows x 1920 columns) so concurrently running pairs
-// share S rows through L2.
-static int build_units4(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t st, const int32_t** out,
-                        int64_t* count) {
-    if (g_units4.m == m && g_units4.lo == job_lo && g_units4.hi == job_hi) {
-        *out = g_units4.dev;
-        *count = g_units4.count;
-        return TB_OK;
-    }
+// share S rows through L2.  A unit carries 1 or 2 live N blocks (diagonal / right-edge units skip a
+// block); its K range is split into s_u items and items are listed split-round-major, pair p
+// running items p, p + P, ... (the K-lockstep order that lets concurrent pairs share S k-blocks in
+// L2).  Items of one N block stream 31 KiB per stage instead of 46 KiB and cost ~2/3 of a two-block
+// item, so the plan gives two-block units 3k splits and one-block units 2k (equal-cost items) or a
+// uniform split, whichever a simulation of the static schedule finishes first.
+struct Plan4 {
+    int64_t m = -1, lo = -1, hi = -1;
+    int32_t nkb = -1, forced = -1, pairs = -1;
+    int4* dev = nullptr;
+    int64_t count = 0, cap = 0;
+    int32_t partial = 0;
+};
+// Plans are cached per (geometry, job range): the banded host path cycles through a few ranges.
+static Plan4 g_plans4[8];
+static int g_plans4_next = 0;
+
+static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<int32_t>& code, std::vector<int32_t>& nb) {
     const int64_t RB = (m + g4::UM - 1) / g4::UM, CB = (m + g4::UN - 1) / g4::UN;
     const int64_t GR = 8, GC = 4;
     int64_t y_lo, x_lo, y_hi, x_hi;
     job_coord(job_lo, m, y_lo, x_lo);
     job_coord(job_hi - 1, m, y_hi, x_hi);
-    std::vector<int32_t> v;
     for (int64_t SY = 0; SY < (RB + GR - 1) / GR; ++SY)
         for (int64_t SX = 0; SX < (CB + GC - 1) / GC; ++SX)
             for (int64_t yb = SY * GR; yb < std::min(RB, (SY + 1) * GR); ++yb)
                 for (int64_t xb = SX * GC; xb < std::min(CB, (SX + 1) * GC); ++xb) {
                     const int64_t r0 = yb * g4::UM, r1 = std::min(r0 + g4::UM, m) - 1;
-                    if (xb * g4::UN + g4::UN - 1 < r0) continue;  // entirely below the diagonal
-                    if (r1 < y_lo || r0 > y_hi) continue;          // outside the job range rows
-                    v.push_back((int32_t)((yb << 16) | xb));
+                    const int64_t x0 = xb * g4::UN;
+                    if (x0 + g4::UN - 1 < r0) continue;  // entirely below the diagonal
+                    if (r1 < y_lo || r0 > y_hi) continue;  // outside the job range rows
+                    const int h_lo = (x0 + g4::BN - 1 < r0) ? 1 : 0;
+                    const int h_hi = (x0 + g4::BN >= m) ? 1 : g4::NB;
+                    code.push_back((int32_t)((yb << 16) | xb));
+                    nb.push_back(h_hi - h_lo);
                 }
-    if ((int64_t)v.size() > g_units4.cap) {
-        if (g_units4.dev) cudaFree(g_units4.dev);
-        g_units4.dev = nullptr;
-        TB_CUDA_TRY(cudaMalloc(&g_units4.dev, std::max<size_t>(v.size(), 1) * sizeof(int32_t)));
-        g_units4.cap = (int64_t)v.size();
+}
+
+// Items for per-unit split counts s(nb); returns the simulated makespan (k-block time units).
+static double plan_items4(const std::vector<int32_t>& code, const std::vector<int32_t>& nb, int32_t nkb, int32_t s1,
+                          int32_t s2, int pairs, std::vector<int4>* out) {
+    const double c_kb[3] = {0.0, 0.67, 1.0};  // relative k-block cost by live N blocks
+    const double t_epi = 36.0;                // one epilogue ~ 36 two-block k-blocks (~20 us)
+    std::vector<double> load(pairs, 0.0);
+    const int32_t rounds = std::max(s1, s2);
+    int64_t idx = 0;
+    for (int32_t r = 0; r < rounds; ++r)
+        for (size_t u = 0; u < code.size(); ++u) {
+            const int32_t su = nb[u] == 2 ? s2 : s1;
+            if (r >= su) continue;
+            const int32_t kb0 = (int32_t)((int64_t)r * nkb / su), kb1 = (int32_t)((int64_t)(r + 1) * nkb / su);
+            load[idx % pairs] += (kb1 - kb0) * c_kb[nb[u]] + t_epi;
+            if (out) out->push_back(make_int4(code[u], kb0, kb1, 0));
+            ++idx;
+        }
+    return *std::max_element(load.begin(), load.end());
+}
+
+static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, int32_t forced, int pairs,
+                       cudaStream_t st, const Plan4** out) {
+    for (const Plan4& c : g_plans4)
+        if (c.m == m && c.lo == job_lo && c.hi == job_hi && c.nkb == nkb && c.forced == forced && c.pairs == pairs) {
+            *out = &c;
+            return TB_OK;
+        }
+    Plan4& g_plan4 = g_plans4[g_plans4_next];
+    g_plans4_next = (g_plans4_next + 1) % 8;
+    g_plan4.m = -1;
+    std::vector<int32_t> code, nb;
+    list_units4(m, job_lo, job_hi, code, nb);
+    int32_t b1 = 1, b2 = 1;
+    if (forced > 0) {
+        b1 = b2 = std::min(forced, nkb);
+    } else {
+        double best = plan_items4(code, nb, nkb, 1, 1, pairs, nullptr);
+        const int32_t kmax = std::max(1, nkb / 8);
+        for (int32_t k = 1; k <= 64 && k <= kmax; ++k) {
+            const int32_t cand[2][2] = {{k, k}, {2 * k, 3 * k}};
+            for (auto& c : cand) {
+                if (c[1] > nkb) continue;
+                const double t = plan_items4(code, nb, nkb, c[0], c[1], pairs, nullptr);
+                if (t < best * 0.999) { best = t; b1 = c[0]; b2 = c[1]; }
+            }
+        }
     }
-    if (!v.empty())
-        TB_CUDA_TRY(cudaMemcpyAsync(g_units4.dev, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    std::vector<int4> items;
+    const double span_est = plan_items4(code, nb, nkb, b1, b2, pairs, &items);
+    const char* trace = std::getenv("TB_TRACE");
+    if (trace && trace[0] == '1')
+        fprintf(stderr, "plan4: m %lld units %zu nkb %d splits (1-block %d, 2-block %d) items %zu est %.0f\n",
+                (long long)m, code.size(), nkb, b1, b2, items.size(), span_est);
+    if ((int64_t)items.size() > g_plan4.cap) {
+        if (g_plan4.dev) cudaFree(g_plan4.dev);
+        g_plan4.dev = nullptr;
+        TB_CUDA_TRY(cudaMalloc(&g_plan4.dev, std::max<size_t>(items.size(), 1) * sizeof(int4)));
+        g_plan4.cap = (int64_t)items.size();
+    }
+    if (!items.empty())
+        TB_CUDA_TRY(cudaMemcpyAsync(g_plan4.dev, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
     TB_CUDA_TRY(cudaStreamSynchronize(st));
-    g_units4.m = m;
-    g_units4.lo = job_lo;
-    g_units4.hi = job_hi;
-    g_units4.count = (int64_t)v.size();
-    *out = g_units4.dev;
-    *count = g_units4.count;
+    g_plan4.m = m;
+    g_plan4.lo = job_lo;
+    g_plan4.hi = job_hi;
+    g_plan4.nkb = nkb;
+    g_plan4.forced = forced;
+    g_plan4.pairs = pairs;
+    g_plan4.count = (int64_t)items.size();
+    g_plan4.partial = (b1 > 1 || b2 > 1) ? 1 : 0;
+    *out = &g_plan4;
     return TB_OK;
 }
 
@@ -273,32 +380,54 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     if (K >= (int64_t(1) << 24)) return fail(TB_ERR_CAPACITY, "gemm fp4: K=%lld needs exact f32 sums (< 2^24)", (long long)K);
     if (m >= (int64_t(1) << 16) * g4::UM) return fail(TB_ERR_CAPACITY, "gemm fp4: m too large");
     int rc;
-    const int32_t* units = nullptr;
-    int64_t nunits = 0;
-    if ((rc = build_units4(m, job_lo, job_hi, st, &units, &nunits))) return rc;
     Gemm4Args p{};
     p.m = m;
-    p.units = units;
-    p.nunits = nunits;
     const int64_t kbytes = K / 2;
-    p.nkb = (int32_t)((kbytes + g4::BK - 1) / g4::BK);
+    const int32_t nkb = (int32_t)((kbytes + g4::BK - 1) / g4::BK);
     const int pairs = std::max(1, num_sms() / 2);
-    if (splits <= 0) splits = pick_splits(nunits, p.nkb, pairs);
-    if (splits > p.nkb) splits = p.nkb;
-    p.splits = splits;
+    const Plan4* plan = nullptr;
+    if ((rc = build_plan4(m, job_lo, job_hi, nkb, splits, pairs, st, &plan))) return rc;
+    p.items = plan->dev;
+    p.nitems = plan->count;
+    p.partial = plan->partial;
     p.job_lo = job_lo;
     p.job_hi = job_hi;
     p.num = num;
-    if (splits > 1) TB_CUDA_TRY(cudaMemsetAsync(num, 0, (job_hi - job_lo) * sizeof(int32_t), st));
+    if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
     CUtensorMap ta, tbm;
     if ((rc = make_tmap(&ta, S, m, kbytes, ldS, g4::BM))) return rc;
     if ((rc = make_tmap(&tbm, S, m, kbytes, ldS, g4::BNH))) return rc;
     TB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)g4::SMEM_BYTES));
-    const int64_t work = nunits * splits;
-    const unsigned grid = (unsigned)(2 * std::max<int64_t>(1, std::min<int64_t>(work, pairs)));
+    const unsigned grid = (unsigned)(2 * std::max<int64_t>(1, std::min<int64_t>(p.nitems, pairs)));
+    const char* trace = std::getenv("TB_TRACE");
+    std::vector<unsigned long long> tr;
+    if (trace && trace[0] == '1') {
+        TB_CUDA_TRY(cudaMalloc(&p.trace, grid * 16 * sizeof(unsigned long long)));
+        TB_CUDA_TRY(cudaMemsetAsync(p.trace, 0, grid * 16 * sizeof(unsigned long long), st));
+        TB_CUDA_TRY(cudaStreamSynchronize(st));
+    }
     gemm_fp4_kernel<<<grid, g4::THREADS, g4::SMEM_BYTES, st>>>(ta, tbm, p);
-    return check_launch("gemm_fp4_kernel");
+    if ((rc = check_launch("gemm_fp4_kernel"))) return rc;
+    if (p.trace) {
+        TB_CUDA_TRY(cudaStreamSynchronize(st));
+        tr.resize(grid * 16);
+        TB_CUDA_TRY(cudaMemcpy(tr.data(), p.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+        cudaFree(p.trace);
+        unsigned long long t0 = ~0ull, tend = 0;
+        for (size_t i = 0; i < tr.size(); ++i) if (tr[i]) { t0 = std::min(t0, tr[i]); tend = std::max(tend, tr[i]); }
+        for (int it = 0; it < 8; ++it) {
+            double sa = 0, se = 0, mn = 1e30, mx = 0; int n = 0;
+            for (unsigned b = 0; b < grid; ++b) {
+                unsigned long long a = tr[(b * 8 + it) * 2], e = tr[(b * 8 + it) * 2 + 1];
+                if (!a || !e) continue;
+                sa += (a - t0) * 1e-3; se += (e - a) * 1e-3; mn = std::min(mn, (a - t0) * 1e-3); mx = std::max(mx, (a - t0) * 1e-3); ++n;
+            }
+            if (n) fprintf(stderr, "item %d: ctas %d  tfull at mean %.1f us [%.1f, %.1f]  epilogue mean %.1f us\n", it, n, sa / n, mn, mx, se / n);
+        }
+        fprintf(stderr, "span first tfull -> last epilogue end %.1f us (items %lld)\n", (tend - t0) * 1e-3, (long long)p.nitems);
+    }
+    return p.partial ? accum_convert(p.acc, job_hi - job_lo, num, st) : TB_OK;
 }
 
 }  // namespace tb

@@ -166,6 +166,7 @@ class TauEngine:
     def _run(self, x, path, m, n, job_lo, job_hi, st, tau_a, tau_b, full_counts, splits, simt) -> PairResult:
         count = job_hi - job_lo
         dev = self.device
+        c0 = _lib.load().tb_launch_count()
         res = PairResult(m=m, n=n, job_lo=job_lo, job_hi=job_hi, path=path,
                          numerator=torch.empty(count, dtype=torch.int32, device=dev),
                          n1_rows=torch.empty(m, dtype=torch.int64, device=dev),
@@ -179,7 +180,7 @@ class TauEngine:
             res.tau_b = torch.empty(count, dtype=torch.float64, device=dev) if tau_b else None
             _lib.call("tb_finalize", _ptr(res.numerator), _ptr(res.n1_rows), m, n, job_lo, job_hi,
                       _ptr(res.tau_a), _ptr(res.tau_b), st)
-            res.launches += 1
+        res.launches = _lib.load().tb_launch_count() - c0
         return res
 
     def _gemm_prepare(self, x, res: PairResult, st, simt: bool = False):
@@ -195,7 +196,6 @@ class TauEngine:
                   _ptr(res.n1_rows), _ptr(res.flags), st)
         S = self._buf("S", m * ldS, torch.int8)
         _lib.call("tb_sign_pack", _ptr(R), m, n, ldr, _ptr(S), ldS, fmt, st)
-        res.launches += 2
         res.extra["sign_format"] = fmt
         return S, K, ldS, fmt
 
@@ -211,7 +211,6 @@ class TauEngine:
         self._mark(0)
         self._gemm_numerator(S, res.numerator, m, K, ldS, fmt, res.job_lo, res.job_hi, st, splits, simt)
         self._mark(1)
-        res.launches += 1
         if full_counts:
             A = self._buf("A", m * ldS, torch.int8)
             _lib.call("tb_abs_pack", _ptr(S), m, ldS, fmt, _ptr(A), st)
@@ -221,7 +220,6 @@ class TauEngine:
             res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
             _lib.call("tb_full_counts", _ptr(res.numerator), _ptr(absdot), _ptr(res.n1_rows), m, n,
                       res.job_lo, res.job_hi, _ptr(res.n_d), _ptr(res.n3), st)
-            res.launches += 3
 
     # -------------------------------------------------------------- host-buffer entry point
     @staticmethod
@@ -258,6 +256,7 @@ class TauEngine:
             x = x_host.to(self.device, non_blocking=True)
             if path == "merge" and x.dtype != torch.int32:
                 raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
+            c0 = _lib.load().tb_launch_count()
             res = PairResult(m=m, n=n, job_lo=0, job_hi=total, path=path,
                              numerator=self._buf("num_all", total, torch.int32),
                              n1_rows=torch.empty(m, dtype=torch.int64, device=self.device),
@@ -278,13 +277,13 @@ class TauEngine:
                               _ptr(maxgrp[1]), _ptr(maxgrp[2]), m, n, lo, hi, _ptr(num), None, None, st)
                 tb = res.tau_b[lo:hi]
                 _lib.call("tb_finalize", _ptr(num), _ptr(res.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
-                res.launches += 2
                 ev = torch.cuda.Event()
                 ev.record(st_t)
                 cp_t.wait_event(ev)
                 with torch.cuda.stream(cp_t):
                     tau_b_out[lo:hi].copy_(tb, non_blocking=True)
             st_t.wait_stream(cp_t)
+            res.launches = _lib.load().tb_launch_count() - c0
         return res
 
     def _copy_stream(self) -> torch.cuda.Stream:
@@ -306,7 +305,6 @@ class TauEngine:
         ngroups = self._buf("ngroups", m, torch.int32)
         _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp),
                   _ptr(work), _ptr(ngroups), _ptr(res.flags), st)
-        res.launches += 2
         return pos, srt, (maxgrp, work, ngroups)
 
     def _merge_path(self, x, res: PairResult, st):
@@ -320,7 +318,6 @@ class TauEngine:
                   _ptr(ngroups), m, n,
                   res.job_lo, res.job_hi, _ptr(res.numerator), _ptr(res.n_d), _ptr(res.n3), st)
         self._mark(1)
-        res.launches += 1
 
 
 _ENGINES: dict[int, TauEngine] = {}
