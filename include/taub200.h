@@ -96,9 +96,12 @@ int tb_rank_rows(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, ui
  *           S[r, off(d) + a] = sign(R[r, a+d] - R[r, a]),
  *           off(d) = 16 * sum_{d'<d} ceil((n - d') / 16).
  *         K = tb_sign_k(n) (>= n(n-1)/2) elements: K bytes for TB_SIGN_I8/E4M3,
- *         K/2 bytes for TB_SIGN_E2M1 (element 2i in the low nibble); the row tail
- *         up to ldS is zeroed; ldS (bytes) must be a multiple of 16.  Padding zeros
- *         add nothing to S_u.S_v.
+ *         K/2 bytes for TB_SIGN_E2M1; the row tail up to ldS is zeroed; ldS (bytes)
+ *         must be a multiple of 16.  Padding zeros add nothing to S_u.S_v.
+ *         TB_SIGN_E2M1 permutes the 16 samples of each 16-sample group (group g of
+ *         segment d, 8 bytes): sample 8w + 4h + j sits in 32-bit word w ^ s, byte j,
+ *         nibble h, with s = bit 2 of g; ties may be written as -0 (0x8).  The order
+ *         is the same in every row, so S_u.S_v is unchanged.
  */
 int64_t tb_sign_k(int64_t n);
 int tb_sign_pack(const uint16_t *R, int64_t m, int64_t n, int64_t ldr, int8_t *S, int64_t ldS, int format,

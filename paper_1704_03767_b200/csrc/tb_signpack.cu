@@ -55,8 +55,8 @@ __device__ __forceinline__ int inv_prefix(int64_t t, int n) {
 __device__ __forceinline__ uint4 lds128(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
 // Signs of the 16 samples of one chunk from its 8 own and 8 window rank-pair words.
-// FMT 0: int8 (+1 = 0x01, -1 = 0xFF); FMT 1: e4m3 (0x38 / 0xB8, the kind::f8f6f4 experiment);
-// FMT 2: e2m1 (+1 = 0x2, -1 = 0xA) left in the low nibble of each byte (packed by the caller).
+// FMT 0: int8 (+1 = 0x01, -1 = 0xFF); FMT 1: e4m3 (0x38 / 0xB8, the kind::f8f6f4 experiment).
+// FMT 2 (e2m1) has its own loop below (chunk_e2m1).
 template <int FMT>
 __device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint32_t (&own)[8]) {
     uint32_t out[4];
@@ -68,9 +68,6 @@ __device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint3
         if (FMT == 1) {
             const uint32_t t = ge ^ le;
             out[qq] = (t & 0x38383838u) | (t & le & 0x80808080u);
-        } else if (FMT == 2) {
-            const uint32_t t = ge ^ le;
-            out[qq] = (t & 0x02020202u) | (t & le & 0x08080808u);
         } else {
             out[qq] = sign_bytes(ge, le);
         }
@@ -78,22 +75,58 @@ __device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint3
     return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
+// e2m1 chunk, 16 signs -> 8 bytes.  Within the chunk, sample 8 w + 4 h + j (w, h in {0,1},
+// j in 0..3) sits in word w, byte j, nibble h: the dot product only needs every row to use the same
+// order, and this one packs with byte merges instead of nibble shuffles.  Ties may come out as -0
+// (0x8), which multiplies like 0.
+//   yb: window words with bit 15 of each halfword set (w + 0x8000), own: plain rank pairs.
+//   D = yb - o = w - o + 0x8000 per halfword (no borrow: w - o in [-32767, 32767]) -> bit 15: w >= o
+//   E = 0x10000 - D per halfword = (-D) + 0x00010000                       -> bit 15: w <= o
+// D and E are IMADs (FMA pipe; `neg1` is a runtime -1 so ptxas keeps them off the ALU pipe), the
+// PRMT sign-replicates the high bytes and three LOP3s per word build the nibbles.
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ uint32_t lop3_sel(uint32_t a, uint32_t b, uint32_t m) {  // (a & m) | (b & ~m)
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "r"(m));
+    return r;
+}
+__device__ __forceinline__ uint32_t nib_code(uint32_t ge, uint32_t le) {  // ((ge ^ le) & 0x2) | (le & 0x8) per nibble
+    const uint32_t x = (ge ^ le) & 0x22222222u;
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xF8;" : "=r"(r) : "r"(x), "r"(le), "r"(0x88888888u));  // x | (le & c)
+    return r;
+}
+__device__ __forceinline__ uint2 chunk_e2m1(const uint32_t (&yb)[8], const uint32_t (&own)[8], uint32_t neg1,
+                                            uint32_t k10000) {
+    uint32_t ge[4], le[4];
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+        const uint32_t d0 = imad(own[2 * qq], neg1, yb[2 * qq]);
+        const uint32_t d1 = imad(own[2 * qq + 1], neg1, yb[2 * qq + 1]);
+        const uint32_t e0 = imad(d0, neg1, k10000);
+        const uint32_t e1 = imad(d1, neg1, k10000);
+        ge[qq] = prmt_signs(d0, d1);
+        le[qq] = prmt_signs(e0, e1);
+    }
+    const uint32_t w0 = nib_code(lop3_sel(ge[0], ge[1], 0x0F0F0F0Fu), lop3_sel(le[0], le[1], 0x0F0F0F0Fu));
+    const uint32_t w1 = nib_code(lop3_sel(ge[2], ge[3], 0x0F0F0F0Fu), lop3_sel(le[2], le[3], 0x0F0F0F0Fu));
+    return make_uint2(w0, w1);
+}
+
 // Shared memory holds 8 shifted copies of the row's rank pairs, C[o][s][j] = pair at halfword
 // 2 (j + s) + o, so the window of chunk (d, g) -- halfwords 16 g + d .. +15 -- is 8 words starting
 // at the 16-byte-aligned index 8 g + ((d >> 1) & ~3) of copy (d & 1, (d >> 1) & 3): two 128-bit
 // loads, no per-lane shifting.
-// e2m1 nibbles: bytes (n0, n1, n2, n3) of each word -> bytes (n1 n0, n3 n2); two words -> one.
-__device__ __forceinline__ uint32_t pack_nibbles(uint32_t a, uint32_t b) {
-    a = (a | (a >> 4)) & 0x00FF00FFu;
-    b = (b | (b >> 4)) & 0x00FF00FFu;
-    return __byte_perm(a, b, 0x6420);
-}
 
 template <int FMT>
 __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t* __restrict__ R, int64_t n,
                                                               int64_t ldr, int8_t* __restrict__ S, int64_t ldS,
-                                                              int64_t K, int nwc) {
-    extern __shared__ __align__(16) uint32_t sp_words[];  // [8][nwc]
+                                                              int64_t K, int nwc, uint32_t neg1) {
+    extern __shared__ __align__(16) uint32_t sp_words[];  // [8][nwc] (+ [nwc] plain own copy for e2m1)
     const int64_t r = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nn = (int)n;
@@ -105,9 +138,17 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
             for (int sh = 0; sh < 4; ++sh) {
                 const int h = 2 * (j + sh) + o;  // halfword index of the pair's low half
                 const uint32_t lo = h < nn ? rr[h] : 0u, hi = h + 1 < nn ? rr[h + 1] : 0u;
-                sp_words[(o * 4 + sh) * nwc + j] = lo | (hi << 16);
+                const uint32_t wv = lo | (hi << 16);
+                sp_words[(o * 4 + sh) * nwc + j] = FMT == 2 ? (wv | 0x80008000u) : wv;
+                if (FMT == 2 && o == 0 && sh == 0) sp_words[8 * nwc + j] = wv;
             }
         }
+    }
+    if (FMT == 2 && tid < 32) {  // tail masks: [swapped][lim] for the last chunk of a segment
+        const int lim = tid & 15, swp = tid >> 4;
+        uint32_t mk[2] = {0u, 0u};
+        for (int i = 0; i < lim; ++i) mk[i >> 3] |= 0xFu << (8 * (i & 3) + 4 * ((i >> 2) & 1));
+        reinterpret_cast<uint2*>(sp_words + 9 * nwc)[tid] = swp ? make_uint2(mk[1], mk[0]) : make_uint2(mk[0], mk[1]);
     }
     __syncthreads();
 
@@ -127,7 +168,52 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
         int G = (nn - d + 15) >> 4;
         // window base of offset d: copy (d & 1, (d >> 1) & 3), 16-byte-aligned word (d >> 1) & ~3
         int wbase = ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + ((d >> 1) & ~3);
-        for (;;) {
+        if (FMT == 2) {
+            // Bank swizzle: chunks with bit 2 of g set read their second 16 bytes first, so 8
+            // consecutive chunks' 128-bit loads cover all 32 banks.  Their two output words come out
+            // swapped -- a fixed per-chunk sample order, identical in every row.  A 32-chunk step
+            // keeps bit 2 of g, so the swizzle (and the pointers) only change at a segment crossing.
+            const uint2* masks = reinterpret_cast<const uint2*>(sp_words + 9 * nwc);
+            uint2* outp = reinterpret_cast<uint2*>(row) + c;
+            int sw = ((g >> 2) & 1) * 4;
+            const uint32_t* own_p = sp_words + 8 * nwc + 8 * g + sw;
+            const uint32_t* win_p = sp_words + wbase + 8 * g + sw;
+            int lim = nn - d - 16 * g;  // samples 16 g + i valid for i < lim
+            for (;;) {
+                const uint4 o0 = lds128(own_p), o1 = lds128(own_p + (4 - 2 * sw));
+                const uint4 w0 = lds128(win_p), w1 = lds128(win_p + (4 - 2 * sw));
+                const uint32_t own[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+                const uint32_t y[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                uint2 v2 = chunk_e2m1(y, own, neg1, 0x00010000u);
+                if (lim < 16) {
+                    const uint2 mk = masks[lim + 4 * sw];
+                    v2.x &= mk.x;
+                    v2.y &= mk.y;
+                }
+                *outp = v2;
+                c += 32;
+                if (c >= c_hi) break;
+                outp += 32;
+                g += 32;
+                own_p += 256;
+                win_p += 256;
+                lim -= 512;
+                if (g >= G) {
+                    do {
+                        g -= G;
+                        ++d;
+                        G = (nn - d + 15) >> 4;
+                    } while (g >= G);
+                    wbase = ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + ((d >> 1) & ~3);
+                    sw = ((g >> 2) & 1) * 4;
+                    own_p = sp_words + 8 * nwc + 8 * g + sw;
+                    win_p = sp_words + wbase + 8 * g + sw;
+                    lim = nn - d - 16 * g;
+                }
+            }
+        }
+        for (; FMT != 2;) {
+            const int lim = nn - d - 16 * g;  // samples 16 g + i valid for i < lim
             const uint32_t* own_p = sp_words + 8 * g;
             const uint32_t* win_p = sp_words + wbase + 8 * g;
             const uint4 o0 = lds128(own_p), o1 = lds128(own_p + 4);
@@ -135,7 +221,6 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
             const uint32_t own[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
             const uint32_t y[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
             uint4 v = chunk_signs<FMT>(y, own);
-            const int lim = nn - d - 16 * g;  // samples 16 g + i valid for i < lim
             if (lim < 16) {
                 uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -145,10 +230,7 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
                 }
                 v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
             }
-            if (FMT == 2)
-                *reinterpret_cast<uint2*>(row + 8u * (uint32_t)c) = make_uint2(pack_nibbles(v.x, v.y), pack_nibbles(v.z, v.w));
-            else
-                *reinterpret_cast<uint4*>(row + 16 * (int64_t)c) = v;
+            *reinterpret_cast<uint4*>(row + 16 * (int64_t)c) = v;
             c += 32;
             if (c >= c_hi) break;
             g += 32;
@@ -186,7 +268,7 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
     if (ldr < n || (ldr & 1)) return fail(TB_ERR_CONFIG, "sign_pack: ldr must be even and >= n");
     if (!R || !S) return fail(TB_ERR_INVALID, "sign_pack: null pointer");
     const int nwc = (int)(((n + 1) / 2 + 16 + 3) & ~3);  // words per shifted copy (window reads overrun n)
-    const size_t smem = (size_t)8 * nwc * sizeof(uint32_t);
+    const size_t smem = (size_t)(format == TB_SIGN_E2M1 ? 9 : 8) * nwc * sizeof(uint32_t) + 32 * sizeof(uint2);
     if (smem > 200 * 1024) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld too large for the shared row copies", (long long)n);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t nblk = (K / 16 + 16 * SP_THREADS - 1) / (16 * SP_THREADS);  // >= 16 chunks per thread
@@ -195,7 +277,7 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
     dim3 grid((unsigned)m, gy);
 #define TB_SP_LAUNCH(F)                                                                                   \
     TB_CUDA_TRY(cudaFuncSetAttribute(signpack_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    signpack_kernel<F><<<grid, SP_THREADS, smem, st>>>(R, n, ldr, S, ldS, K, nwc)
+    signpack_kernel<F><<<grid, SP_THREADS, smem, st>>>(R, n, ldr, S, ldS, K, nwc, 0xFFFFFFFFu)
     if (format == TB_SIGN_E2M1) {
         TB_SP_LAUNCH(2);
     } else if (format == TB_SIGN_E4M3) {
