@@ -183,19 +183,28 @@ class TauEngine:
         res.launches = _lib.load().tb_launch_count() - c0
         return res
 
-    def _gemm_prepare(self, x, res: PairResult, st, simt: bool = False):
-        """K0 rank transform + K2 sign pack of every row: the GEMM operand S (m x K signs)."""
-        m, n = res.m, res.n
+    def _gemm_layout(self, n: int, simt: bool = False):
+        """(K, sign format, row stride of S in bytes, row stride of R) for n samples."""
         K = int(_lib.load().tb_sign_k(n))  # padded diagonal layout, >= n(n-1)/2 elements
         fmt = self.sign_format(K) if not simt else _lib.TB_SIGN_I8
         kbytes = K // 2 if fmt == _lib.TB_SIGN_E2M1 else K
-        ldS = (kbytes + 15) // 16 * 16
-        ldr = (n + 7) // 8 * 8
+        return K, fmt, (kbytes + 15) // 16 * 16, (n + 7) // 8 * 8
+
+    def _gemm_prepare(self, x, res: PairResult, st, simt: bool = False, row_chunks=None):
+        """K0 rank transform + K2 sign pack of every row: the GEMM operand S (m x K signs).
+
+        ``row_chunks`` = [(r0, r1, wait_fn)]: prepare rows [r0, r1) after ``wait_fn()`` (the
+        host entry point waits for each chunk's H2D copy); default one chunk of all rows."""
+        m, n = res.m, res.n
+        K, fmt, ldS, ldr = self._gemm_layout(n, simt)
         R = self._buf("R", m * ldr, torch.int16)
-        _lib.call("tb_rank_rows", _ptr(x), _dtype_code(x), m, n, x.stride(0), _ptr(R), ldr,
-                  _ptr(res.n1_rows), _ptr(res.flags), st)
         S = self._buf("S", m * ldS, torch.int8)
-        _lib.call("tb_sign_pack", _ptr(R), m, n, ldr, _ptr(S), ldS, fmt, st)
+        for r0, r1, wait in (row_chunks or [(0, m, None)]):
+            if wait is not None:
+                wait()
+            _lib.call("tb_rank_rows", _ptr(x[r0:r1]), _dtype_code(x), r1 - r0, n, x.stride(0),
+                      _ptr(R[r0 * ldr:]), ldr, _ptr(res.n1_rows[r0:]), _ptr(res.flags), st)
+            _lib.call("tb_sign_pack", _ptr(R[r0 * ldr:]), r1 - r0, n, ldr, _ptr(S[r0 * ldS:]), ldS, fmt, st)
         res.extra["sign_format"] = fmt
         return S, K, ldS, fmt
 
@@ -223,20 +232,23 @@ class TauEngine:
 
     # -------------------------------------------------------------- host-buffer entry point
     @staticmethod
-    def bands(m: int, nbands: int, align: int = 256) -> list[int]:
-        """Row boundaries splitting the pair triangle into ~equal-pair bands, aligned to the GEMM row block."""
-        cuts = [0]
-        for i in range(1, nbands):
-            f = i / nbands
-            r = int(round(m * (1.0 - (1.0 - f) ** 0.5) / align)) * align
+    def bands(m: int, nbands: int = 3, align: int = 256, fracs: tuple | None = None) -> list[int]:
+        """Row boundaries splitting the pair triangle into bands holding the given fractions of the
+        pairs (default: equal), aligned to the GEMM row block."""
+        if fracs is None:
+            fracs = (1.0 / nbands,) * nbands
+        cuts, acc = [0], 0.0
+        for fr in fracs[:-1]:
+            acc += fr
+            r = int(round(m * (1.0 - (1.0 - min(acc, 1.0)) ** 0.5) / align)) * align
             if cuts[-1] < r < m:
                 cuts.append(r)
         cuts.append(m)
         return cuts
 
     def all_pairs_host(self, x_host: torch.Tensor, tau_b_out: torch.Tensor, kernel: str = "auto",
-                       nbands: int = 4, stream: torch.cuda.Stream | None = None,
-                       copy_stream: torch.cuda.Stream | None = None) -> PairResult:
+                       band_fracs: tuple = (0.55, 0.30, 0.15), stream: torch.cuda.Stream | None = None,
+                       copy_stream: torch.cuda.Stream | None = None, h2d_chunks: int = 2) -> PairResult:
         """End-to-end from host buffers: H2D of the values, the device path, tau_b back to host.
 
         The job range is cut into row bands; band i's tau_b copy (on ``copy_stream``) overlaps
@@ -252,10 +264,21 @@ class TauEngine:
         path = self.choose_path(n) if kernel == "auto" else kernel
         st = _stream_ptr(st_t)
         self._events, self._stream = None, st_t
+        if path == "merge" and x_host.dtype != torch.int32:
+            raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
         with torch.cuda.stream(st_t):
-            x = x_host.to(self.device, non_blocking=True)
-            if path == "merge" and x.dtype != torch.int32:
-                raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
+            # H2D in row chunks on the copy stream; rank + sign pack of chunk i overlap chunk i+1's copy
+            x = self._buf("x_dev", m * n, x_host.dtype).view(m, n)
+            nchunk = max(1, min(h2d_chunks, m // 256)) if path == "gemm" else 1
+            cuts_h = [m * i // nchunk // 8 * 8 for i in range(nchunk)] + [m]
+            cp_t.wait_stream(st_t)  # the previous call's kernels are done with x
+            chunks = []
+            for r0, r1 in zip(cuts_h[:-1], cuts_h[1:]):
+                with torch.cuda.stream(cp_t):
+                    x[r0:r1].copy_(x_host[r0:r1], non_blocking=True)
+                    ev_c = torch.cuda.Event()
+                    ev_c.record(cp_t)
+                chunks.append((r0, r1, ev_c))
             c0 = _lib.load().tb_launch_count()
             res = PairResult(m=m, n=n, job_lo=0, job_hi=total, path=path,
                              numerator=self._buf("num_all", total, torch.int32),
@@ -263,10 +286,13 @@ class TauEngine:
                              flags=torch.zeros(1, dtype=torch.int32, device=self.device))
             res.tau_b = self._buf("taub_all", total, torch.float64)
             if path == "gemm":
-                S, K, ldS, fmt = self._gemm_prepare(x, res, st)
+                S, K, ldS, fmt = self._gemm_prepare(
+                    x, res, st, row_chunks=[(r0, r1, (lambda e=ev: st_t.wait_event(e))) for r0, r1, ev in chunks])
             else:
+                for _, _, ev in chunks:
+                    st_t.wait_event(ev)
                 pos, srt, maxgrp = self._merge_prepare(x, res, st)
-            cuts = self.bands(m, nbands)
+            cuts = self.bands(m, len(band_fracs), fracs=band_fracs)
             for r0, r1 in zip(cuts[:-1], cuts[1:]):
                 lo, hi = r0 * (2 * m - r0 + 1) // 2, r1 * (2 * m - r1 + 1) // 2
                 num = res.numerator[lo:hi]

@@ -319,7 +319,7 @@ def test_host_entry_point_bands(eng, oracle, path, m, n):
     xh = torch.from_numpy(x).pin_memory()
     total = m * (m + 1) // 2
     out = torch.full((total,), -7.0, dtype=torch.float64).pin_memory()
-    eng.all_pairs_host(xh, out, kernel=path, nbands=4)
+    eng.all_pairs_host(xh, out, kernel=path, band_fracs=(0.4, 0.3, 0.2, 0.1), h2d_chunks=3)
     torch.cuda.synchronize()
     ref = eng.all_pairs(torch.from_numpy(x).cuda(), kernel=path, tau_a=False).validate()
     np.testing.assert_array_equal(out.numpy(), ref.tau_b.cpu().numpy())
