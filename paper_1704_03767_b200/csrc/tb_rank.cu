@@ -7,6 +7,8 @@
 // One CTA per row, n <= 8192 (the GEMM path): the row's (order-preserving key, index) pairs are
 // bitonic-sorted in shared memory (lexicographic on (key, index), so pad slots sort last), a
 // block scan over "new value" flags yields the dense ranks, and run starts give n1.
+#include <type_traits>
+
 #include "tb_common.cuh"
 
 namespace tb {
@@ -183,6 +185,54 @@ __global__ void __launch_bounds__(256) rank_rows_warp_kernel(const T* __restrict
         v[i] = (key << 16) | (uint64_t)e;
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1);
+    if constexpr (std::is_same<T, int32_t>::value) {
+        // Small-range integer rows (codes, counts, Likert scales: max - min < 1024): dense ranks
+        // from a per-warp histogram -- present values in value order get consecutive ranks -- and
+        // n1 = sum c (c - 1) / 2 over the counts.  O(n + range) instead of the bitonic sort.
+        constexpr int HR = 1024;
+        __shared__ int32_t hist[8][HR];
+        uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+            if (lane + 32 * i < nn) {
+                const uint32_t k = (uint32_t)(v[i] >> 16);
+                kmin = min(kmin, k);
+                kmax = max(kmax, k);
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        }
+        if (kmax - kmin < (uint32_t)HR) {
+            int32_t* h = hist[threadIdx.x >> 5];
+            const int rounds = (int)((kmax - kmin) >> 5) + 1;
+            for (int j = 0; j < rounds; ++j) h[32 * j + lane] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < E; ++i)
+                if (lane + 32 * i < nn) atomicAdd(&h[(uint32_t)(v[i] >> 16) - kmin], 1);
+            __syncwarp();
+            int base = 0;
+            unsigned long long ties = 0;
+            for (int j = 0; j < rounds; ++j) {
+                const int c = h[32 * j + lane];
+                const unsigned b = __ballot_sync(0xffffffffu, c > 0);
+                h[32 * j + lane] = base + __popc(b & ((1u << lane) - 1u));
+                base += __popc(b);
+                ties += (unsigned long long)c * (unsigned long long)(c - 1) / 2ull;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                const int e = lane + 32 * i;
+                if (e < nn) R[r * ldr + e] = (uint16_t)h[(uint32_t)(v[i] >> 16) - kmin];
+            }
+            for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
+            if (lane == 0) n1[r] = ties;
+            for (int64_t i = nn + lane; i < ldr; i += 32) R[r * ldr + i] = 0;
+            return;
+        }
+    }
     warp_bitonic<E>(v, lane);
     // dense ranks over slots [0, n): flag = key differs from the previous slot's key
     const uint64_t prev_last = __shfl_up_sync(0xffffffffu, v[E - 1], 1);

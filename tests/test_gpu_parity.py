@@ -323,3 +323,36 @@ def test_host_entry_point_bands(eng, oracle, path, m, n):
     torch.cuda.synchronize()
     ref = eng.all_pairs(torch.from_numpy(x).cuda(), kernel=path, tau_a=False).validate()
     np.testing.assert_array_equal(out.numpy(), ref.tau_b.cpu().numpy())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [np.int32, np.float32, np.float64])
+def test_rank_rows_vs_oracle(oracle, dtype):
+    """K0 dense ranks + tie counts vs the oracle's rank_transform (ranks.py:37-61), int32 rows on
+    both sides of the 1024-wide histogram path (range 1023 / 1024, negative values, constants)."""
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.device import _ptr, _stream_ptr, _dtype_code
+    rng = np.random.default_rng(404)
+    for n in (7, 33, 500, 1000, 1024, 2000):
+        rows = [rng.integers(-5, 5, n), rng.integers(0, 1024, n), rng.integers(0, 1025, n),
+                rng.integers(-2**31, 2**31 - 1, n), np.full(n, 7), rng.integers(100, 103, n),
+                rng.standard_normal(n) * 1000, np.arange(n)[::-1]]
+        x = np.stack(rows).astype(dtype)
+        if dtype is not np.int32:
+            x[0, : n // 3] = -0.0
+        m = x.shape[0]
+        ldr = (n + 7) // 8 * 8
+        xd = torch.from_numpy(x).cuda()
+        R = torch.empty(m * ldr, dtype=torch.int16, device="cuda")
+        n1 = torch.empty(m, dtype=torch.int64, device="cuda")
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.call("tb_rank_rows", _ptr(xd), _dtype_code(xd), m, n, n, _ptr(R), ldr, _ptr(n1), _ptr(flags),
+                  _stream_ptr(None))
+        torch.cuda.synchronize()
+        got = R.view(m, ldr)[:, :n].cpu().numpy().astype(np.int64)
+        for r in range(m):
+            ref = oracle.rank_transform(x[r])
+            np.testing.assert_array_equal(got[r], ref, err_msg=f"n={n} row={r}")
+            _, c = np.unique(ref, return_counts=True)
+            assert int(n1[r]) == int((c * (c - 1) // 2).sum()), (n, r)
+        assert int(flags.item()) == 0
