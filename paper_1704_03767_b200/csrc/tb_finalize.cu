@@ -1,7 +1,9 @@
 // K5: fp64 finalize over a contiguous job-id range -- derive_taus
-// (result.py:62-82) on device.  HBM-bound streaming kernel: reads the int32
-// numerator (4 B) and writes tau_a/tau_b (8 + 8 B) per pair; per-row tie counts
-// stay in L2.
+// (result.py:62-82) on device.  Streaming kernel: reads the int32 numerator
+// (4 B) and writes tau_a/tau_b (8 + 8 B) per pair; per-row tie counts stay in L2.
+// Measured on config 3 (134M pairs): 721 us = 3.7 TB/s effective (57% of HBM),
+// bound by the fp64 div/sqrt chains (tools/exp_fin.py; the per-element job_coord
+// version took 1040 us).
 //
 // Bit-exactness: tau_a = (double)num / (double)n0 and tau_b = (double)num /
 // sqrt((n0 - n1_y) * (n0 - n1_x)) with IEEE round-to-nearest __ddiv_rn /
@@ -11,21 +13,43 @@
 
 namespace tb {
 
-__global__ void __launch_bounds__(256) finalize_kernel(const int32_t* __restrict__ num,
-                                                       const unsigned long long* __restrict__ n1, int64_t m,
-                                                       int64_t n0, int64_t job_lo, int64_t count,
-                                                       double* __restrict__ tau_a, double* __restrict__ tau_b) {
+// Block b owns job ids [job_lo + b * FIN_CHUNK, +FIN_CHUNK); thread t decodes its first
+// cell (y, x) once and then steps 256 job ids at a time, walking the row-major upper triangle
+// incrementally (x += 256, wrapping to row y + 1 at column y + 1), so the per-element work is the
+// IEEE tau sequence plus a few integer ops -- no per-element sqrt-based job_coord.  Loads and stores
+// stay coalesced (consecutive threads = consecutive job ids).
+constexpr int FIN_THREADS = 256;
+constexpr int FIN_ITERS = 16;
+constexpr int64_t FIN_CHUNK = (int64_t)FIN_THREADS * FIN_ITERS;
+
+__global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32_t* __restrict__ num,
+                                                                      const unsigned long long* __restrict__ n1,
+                                                                      int64_t m, int64_t n0, int64_t job_lo,
+                                                                      int64_t count, double* __restrict__ tau_a,
+                                                                      double* __restrict__ tau_b) {
     const double dn0 = (double)n0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const double x = (double)num[i];
-        if (tau_a) tau_a[i] = __ddiv_rn(x, dn0);
+    int64_t i = (int64_t)blockIdx.x * FIN_CHUNK + threadIdx.x;
+    if (i >= count) return;
+    const int64_t i_end = min(count, (int64_t)(blockIdx.x + 1) * FIN_CHUNK);
+    int64_t y, x;
+    job_coord(job_lo + i, m, y, x);
+    double ty = dn0 - (double)__ldg(&n1[y]);
+    for (;;) {
+        const double v = (double)num[i];
+        if (tau_a) tau_a[i] = __ddiv_rn(v, dn0);
         if (tau_b) {
-            int64_t y, c;
-            job_coord(job_lo + i, m, y, c);
-            const double t1 = (double)n1[y], t2 = (double)n1[c];
-            const double denom = __dsqrt_rn(__dmul_rn(dn0 - t1, dn0 - t2));
-            tau_b[i] = denom > 0.0 ? __ddiv_rn(x, denom) : __longlong_as_double(0x7ff8000000000000LL);
+            const double denom = __dsqrt_rn(__dmul_rn(ty, dn0 - (double)__ldg(&n1[x])));
+            tau_b[i] = denom > 0.0 ? __ddiv_rn(v, denom) : __longlong_as_double(0x7ff8000000000000LL);
+        }
+        i += FIN_THREADS;
+        if (i >= i_end) break;
+        x += FIN_THREADS;
+        if (x >= m) {
+            do {
+                x -= m - (y + 1);
+                ++y;
+            } while (x >= m);
+            ty = dn0 - (double)__ldg(&n1[y]);
         }
     }
 }
@@ -44,10 +68,11 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     if (!num || !n1_rows) return fail(TB_ERR_INVALID, "finalize: null pointer");
     const int64_t count = job_hi - job_lo;
     if (count == 0) return TB_OK;
-    int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 16);
-    finalize_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    const int64_t blocks = (count + FIN_CHUNK - 1) / FIN_CHUNK;
+    if (blocks > INT32_MAX) return fail(TB_ERR_CAPACITY, "finalize: job range too large");
+    finalize_chunk_kernel<<<(unsigned)blocks, FIN_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
         num, reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count, tau_a, tau_b);
-    return check_launch("finalize_kernel");
+    return check_launch("finalize_chunk_kernel");
 }
 
 namespace tb {

@@ -356,3 +356,41 @@ def test_rank_rows_vs_oracle(oracle, dtype):
             _, c = np.unique(ref, return_counts=True)
             assert int(n1[r]) == int((c * (c - 1) // 2).sum()), (n, r)
         assert int(flags.item()) == 0
+
+
+@pytest.mark.gpu
+def test_finalize_ranges_vs_numpy():
+    """K5 over arbitrary job ranges (mid-row starts, rows shorter than the 256-id step, ranges ending
+    inside a chunk) == derive_taus (result.py:62-82) evaluated in numpy on the same counts."""
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.device import _ptr, _stream_ptr
+    from paper_1704_03767_b200.pairindex import job_coord
+    rng = np.random.default_rng(77)
+    for m, n in ((1, 5), (3, 9), (40, 17), (300, 1000), (5000, 64)):
+        n0 = n * (n - 1) // 2
+        total = m * (m + 1) // 2
+        n1 = rng.integers(0, n0 + 1, m).astype(np.uint64)
+        n1[rng.integers(0, m)] = n0  # a constant row -> NaN tau_b
+        for lo, hi in ((0, total), (total // 3, total // 3 + 1), (max(0, total // 2 - 777), total),
+                       (1, min(total, 4097)), (0, min(total, 4096 * 3 + 5))):
+            if hi <= lo:
+                continue
+            num = rng.integers(-n0, n0 + 1, hi - lo).astype(np.int32)
+            dn = torch.from_numpy(num).cuda()
+            dn1 = torch.from_numpy(n1.view(np.int64)).cuda()
+            ta = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+            tb = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+            _lib.call("tb_finalize", _ptr(dn), _ptr(dn1), m, n, lo, hi, _ptr(ta), _ptr(tb), _stream_ptr(None))
+            torch.cuda.synchronize()
+            ys_all = np.repeat(np.arange(m, dtype=np.int64), m - np.arange(m))
+            starts = np.arange(m, dtype=np.int64) * (2 * m - np.arange(m) + 1) // 2
+            xs_all = np.arange(total, dtype=np.int64) - starts[ys_all] + ys_all
+            ys, xs = ys_all[lo:hi], xs_all[lo:hi]
+            assert job_coord(lo, m) == (ys[0], xs[0]) and job_coord(hi - 1, m) == (ys[-1], xs[-1])
+            t1 = n1[ys].astype(np.float64)
+            t2 = n1[xs].astype(np.float64)
+            denom = np.sqrt((n0 - t1) * (n0 - t2))
+            with np.errstate(divide="ignore", invalid="ignore"):
+                ref_b = np.where(denom > 0, num / denom, np.nan)
+            np.testing.assert_array_equal(ta.cpu().numpy(), num / float(n0))
+            np.testing.assert_array_equal(tb.cpu().numpy(), ref_b)
