@@ -51,6 +51,7 @@ struct Gemm4Args {
     int64_t job_lo, job_hi;
     int32_t* num;
     float* acc;      // split-K: f32 sums (exact integers < 2^24), red.global.add.v4.f32
+    int32_t n_edge;  // N of the partial last 240-column block (m % 240 rounded up to 16), 0 if none
     unsigned long long* trace;  // TB_TRACE=1 (diagnostics): per CTA, per item: [accumulator ready, epilogue done]
 };
 
@@ -77,7 +78,7 @@ __device__ __forceinline__ bool next_unit4(const Gemm4Args& p, int64_t& cur, int
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     gemm_fp4_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    Gemm4Args p) {
+                    const __grid_constant__ CUtensorMap tmap_be, Gemm4Args p) {
     using namespace g4;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -97,6 +98,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_a);
         tma_prefetch(&tmap_b);
+        if (p.n_edge) tma_prefetch(&tmap_be);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -124,17 +126,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             uint32_t phase = 0;
             int64_t cur = pair;
             Unit4 t;
+            const uint32_t be_rows = (uint32_t)p.n_edge / 2;
             while (next_unit4(p, cur, npairs, t)) {
-                const uint32_t bytes = 2 * (A_BYTES + (t.h_hi - t.h_lo) * B_BYTES);
+                // the block holding column m - 1 may be partial: it loads n_edge / 2 rows per CTA
+                uint32_t bytes = 2 * A_BYTES;
+                for (int h = t.h_lo; h < t.h_hi; ++h)
+                    bytes += 2 * ((t.x0 + h * BN + BN > p.m) ? be_rows * BK : B_BYTES);
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
                     uint8_t* sa = smem + stage * STAGE_BYTES;
                     tma_load_2d_2sm(sa, &tmap_a, fb, kb * BK, (int32_t)(t.y0 + rank * BM));
-                    for (int h = t.h_lo; h < t.h_hi; ++h)
-                        tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
-                                        (int32_t)(t.x0 + h * BN + rank * BNH));
+                    for (int h = t.h_lo; h < t.h_hi; ++h) {
+                        if (t.x0 + h * BN + BN > p.m)
+                            tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_be, fb, kb * BK,
+                                            (int32_t)(t.x0 + h * BN + rank * be_rows));
+                        else
+                            tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
+                                            (int32_t)(t.x0 + h * BN + rank * BNH));
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -142,6 +153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     } else if (warp == 1) {
         if (leader && lane == 0) {  // ---------------- MMA issuer (leader CTA, one thread)
             constexpr uint32_t idesc = idesc_mxf4(UM, BN);
+            const uint32_t idesc_e = idesc_mxf4(UM, (uint32_t)(p.n_edge ? p.n_edge : BN));
             const uint32_t sf = tmem_base + SF_COL;
             int stage = 0;
             uint32_t phase = 0;
@@ -161,7 +173,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                         const uint32_t acc = (kb > t.kb0 || k > 0) ? 1u : 0u;
                         for (int h = t.h_lo; h < t.h_hi; ++h) {
                             const uint64_t bdesc = umma_desc_k_sw128(sa + A_BYTES + h * B_BYTES);
-                            mma_mxf4_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k, idesc, sf, sf, acc);
+                            mma_mxf4_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k,
+                                         (t.x0 + h * BN + BN > p.m) ? idesc_e : idesc, sf, sf, acc);
                         }
                     }
                     mma_commit_2sm(&empty[stage], 0x3);
@@ -280,7 +293,8 @@ struct Plan4 {
 static Plan4 g_plans4[8];
 static int g_plans4_next = 0;
 
-static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<int32_t>& code, std::vector<int32_t>& nb) {
+static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<int32_t>& code, std::vector<int32_t>& nb,
+                        std::vector<int32_t>& ncols) {
     const int64_t RB = (m + g4::UM - 1) / g4::UM, CB = (m + g4::UN - 1) / g4::UN;
     const int64_t GR = 8, GC = 4;
     int64_t y_lo, x_lo, y_hi, x_hi;
@@ -298,23 +312,30 @@ static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<i
                     const int h_hi = (x0 + g4::BN >= m) ? 1 : g4::NB;
                     code.push_back((int32_t)((yb << 16) | xb));
                     nb.push_back(h_hi - h_lo);
+                    int32_t cols = 0;  // MMA columns issued (the partial block runs N = round16(live))
+                    for (int h = h_lo; h < h_hi; ++h)
+                        cols += (x0 + h * g4::BN + g4::BN > m) ? (int32_t)(((m - x0 - h * g4::BN) + 15) / 16 * 16) : g4::BN;
+                    ncols.push_back(cols);
                 }
 }
 
-// Items for per-unit split counts s(nb); returns the simulated makespan (k-block time units).
-static double plan_items4(const std::vector<int32_t>& code, const std::vector<int32_t>& nb, int32_t nkb, int32_t s1,
-                          int32_t s2, int pairs, std::vector<int4>* out) {
-    const double c_kb[3] = {0.0, 0.67, 1.0};  // relative k-block cost by live N blocks
-    const double t_epi = 36.0;                // one epilogue ~ 36 two-block k-blocks (~20 us)
+// Relative k-block cost of a unit: the A-operand share plus the MMA / B share of its issued columns
+// (one full block = 0.67, two = 1.0, the partial edge block in proportion).
+static double unit_cost4(int32_t ncols) { return 0.34 + 0.66 * ncols / 480.0; }
+
+// Items for per-unit split counts su[u]; returns the simulated makespan of the static schedule
+// (items split-round-major, pair p runs p, p + P, ...), in two-block k-block units.
+static double plan_items4(const std::vector<int32_t>& code, const std::vector<int32_t>& ncols,
+                          const std::vector<int32_t>& su, int32_t nkb, int pairs, std::vector<int4>* out) {
+    const double t_epi = 36.0;  // one epilogue ~ 36 two-block k-blocks (~20 us)
     std::vector<double> load(pairs, 0.0);
-    const int32_t rounds = std::max(s1, s2);
+    const int32_t rounds = *std::max_element(su.begin(), su.end());
     int64_t idx = 0;
     for (int32_t r = 0; r < rounds; ++r)
         for (size_t u = 0; u < code.size(); ++u) {
-            const int32_t su = nb[u] == 2 ? s2 : s1;
-            if (r >= su) continue;
-            const int32_t kb0 = (int32_t)((int64_t)r * nkb / su), kb1 = (int32_t)((int64_t)(r + 1) * nkb / su);
-            load[idx % pairs] += (kb1 - kb0) * c_kb[nb[u]] + t_epi;
+            if (r >= su[u]) continue;
+            const int32_t kb0 = (int32_t)((int64_t)r * nkb / su[u]), kb1 = (int32_t)((int64_t)(r + 1) * nkb / su[u]);
+            load[idx % pairs] += (kb1 - kb0) * unit_cost4(ncols[u]) + t_epi;
             if (out) out->push_back(make_int4(code[u], kb0, kb1, 0));
             ++idx;
         }
@@ -331,29 +352,39 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
     Plan4& g_plan4 = g_plans4[g_plans4_next];
     g_plans4_next = (g_plans4_next + 1) % 8;
     g_plan4.m = -1;
-    std::vector<int32_t> code, nb;
-    list_units4(m, job_lo, job_hi, code, nb);
-    int32_t b1 = 1, b2 = 1;
-    if (forced > 0) {
-        b1 = b2 = std::min(forced, nkb);
-    } else {
-        double best = plan_items4(code, nb, nkb, 1, 1, pairs, nullptr);
-        const int32_t kmax = std::max(1, nkb / 8);
-        for (int32_t k = 1; k <= 64 && k <= kmax; ++k) {
-            const int32_t cand[2][2] = {{k, k}, {2 * k, 3 * k}};
-            for (auto& c : cand) {
-                if (c[1] > nkb) continue;
-                const double t = plan_items4(code, nb, nkb, c[0], c[1], pairs, nullptr);
-                if (t < best * 0.999) { best = t; b1 = c[0]; b2 = c[1]; }
+    std::vector<int32_t> code, nb, ncols;
+    list_units4(m, job_lo, job_hi, code, nb, ncols);
+    std::vector<int32_t> su(code.size(), 1), best_su;
+    double best = 0.0;
+    if (!code.empty()) {
+        if (forced > 0) {
+            std::fill(su.begin(), su.end(), std::min(forced, nkb));
+            best_su = su;
+        } else {
+            // equal-cost items: unit u gets round(cost_u * nkb / T) splits for a target item cost T;
+            // T = c_max * nkb / k for k = 1, 1.5, 2, ... 64 (k = 1: no split); best simulated makespan wins
+            const double c_max = unit_cost4(480);
+            best_su = su;
+            best = plan_items4(code, ncols, su, nkb, pairs, nullptr);
+            const int32_t kmax = std::max(1, std::min(64, nkb / 8));
+            for (int32_t k2 = 3; k2 <= 2 * kmax; ++k2) {  // T = c_max * nkb / (k2 / 2): half steps
+                const double T = 2.0 * c_max * nkb / k2;
+                for (size_t u = 0; u < code.size(); ++u) {
+                    const double s_real = unit_cost4(ncols[u]) * nkb / T;
+                    su[u] = (int32_t)std::max<int64_t>(1, std::min<int64_t>(nkb, std::llround(s_real)));
+                }
+                const double t = plan_items4(code, ncols, su, nkb, pairs, nullptr);
+                if (t < best * 0.999) { best = t; best_su = su; }
             }
         }
     }
     std::vector<int4> items;
-    const double span_est = plan_items4(code, nb, nkb, b1, b2, pairs, &items);
+    const double span_est = code.empty() ? 0.0 : plan_items4(code, ncols, best_su, nkb, pairs, &items);
+    const int32_t smax = best_su.empty() ? 1 : *std::max_element(best_su.begin(), best_su.end());
     const char* trace = std::getenv("TB_TRACE");
     if (trace && trace[0] == '1')
-        fprintf(stderr, "plan4: m %lld units %zu nkb %d splits (1-block %d, 2-block %d) items %zu est %.0f\n",
-                (long long)m, code.size(), nkb, b1, b2, items.size(), span_est);
+        fprintf(stderr, "plan4: m %lld units %zu nkb %d max splits %d items %zu est %.0f\n", (long long)m,
+                code.size(), nkb, smax, items.size(), span_est);
     if ((int64_t)items.size() > g_plan4.cap) {
         if (g_plan4.dev) cudaFree(g_plan4.dev);
         g_plan4.dev = nullptr;
@@ -370,7 +401,7 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
     g_plan4.forced = forced;
     g_plan4.pairs = pairs;
     g_plan4.count = (int64_t)items.size();
-    g_plan4.partial = (b1 > 1 || b2 > 1) ? 1 : 0;
+    g_plan4.partial = smax > 1 ? 1 : 0;
     *out = &g_plan4;
     return TB_OK;
 }
@@ -394,9 +425,11 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.job_hi = job_hi;
     p.num = num;
     if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
-    CUtensorMap ta, tbm;
+    CUtensorMap ta, tbm, tbe;
     if ((rc = make_tmap(&ta, S, m, kbytes, ldS, g4::BM))) return rc;
     if ((rc = make_tmap(&tbm, S, m, kbytes, ldS, g4::BNH))) return rc;
+    p.n_edge = (int32_t)(((m % g4::BN) + 15) / 16 * 16);  // multiple of 16 in [16, 240] or 0
+    if ((rc = make_tmap(&tbe, S, m, kbytes, ldS, p.n_edge ? (uint32_t)p.n_edge / 2 : g4::BNH))) return rc;
     TB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)g4::SMEM_BYTES));
     const unsigned grid = (unsigned)(2 * std::max<int64_t>(1, std::min<int64_t>(p.nitems, pairs)));
@@ -407,7 +440,7 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
         TB_CUDA_TRY(cudaMemsetAsync(p.trace, 0, grid * 16 * sizeof(unsigned long long), st));
         TB_CUDA_TRY(cudaStreamSynchronize(st));
     }
-    gemm_fp4_kernel<<<grid, g4::THREADS, g4::SMEM_BYTES, st>>>(ta, tbm, p);
+    gemm_fp4_kernel<<<grid, g4::THREADS, g4::SMEM_BYTES, st>>>(ta, tbm, tbe, p);
     if ((rc = check_launch("gemm_fp4_kernel"))) return rc;
     if (p.trace) {
         TB_CUDA_TRY(cudaStreamSynchronize(st));
