@@ -5,7 +5,7 @@ from paper_1704_03767_b200.device import TauEngine
 eng = TauEngine(0)
 for k in [int(a) for a in (sys.argv[1:] or ["2", "3"])]:
     x = torch.from_numpy(workloads.generate(k)).cuda()
-    for skip in (["0", "6", "1"] if k == 3 else ["0"]):
+    for skip in ("0",):
         os.environ["TB_EXP_SKIP_EPI"] = skip
         ts = []
         for _ in range(5):
