@@ -90,18 +90,18 @@ int tb_rank_rows(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, ui
  * (src/taucorr/kernel_naive.py:26-44), materialising each variable's sign
  * vector once.
  *   R     [m, ldr] uint16 dense ranks (< 2^15; tb_rank_rows output), ldr even
- *   S     [m, ldS] int8 in the "diagonal" sample-pair order: pairs (a, a+d)
- *         grouped by offset d = 1..n-1, each d-segment n-d signs long and
- *         zero-padded to a multiple of 16 bytes:
- *           S[r, off(d) + a] = sign(R[r, a+d] - R[r, a]),
- *           off(d) = 16 * sum_{d'<d} ceil((n - d') / 16).
- *         K = tb_sign_k(n) (>= n(n-1)/2) elements: K bytes for TB_SIGN_I8/E4M3,
- *         K/2 bytes for TB_SIGN_E2M1; the row tail up to ldS is zeroed; ldS (bytes)
- *         must be a multiple of 16.  Padding zeros add nothing to S_u.S_v.
- *         TB_SIGN_E2M1 permutes the 16 samples of each 16-sample group (group g of
- *         segment d, 8 bytes): sample 8w + 4h + j sits in 32-bit word w ^ s, byte j,
- *         nibble h, with s = bit 2 of g; ties may be written as -0 (0x8).  The order
- *         is the same in every row, so S_u.S_v is unchanged.
+ *   S     [m, ldS] signs sign(R[r, b] - R[r, a]) of the n(n-1)/2 sample pairs a < b, one fixed
+ *         order for every row (any order gives S_u.S_v = n_c - n_d), in 16-pair chunks (16 bytes
+ *         int8/e4m3, 8 bytes e2m1).  "Block" order, nbf = n / 16 full 16-sample blocks:
+ *           1. pairs between full blocks A < B (row-major), chunk a_l of (A, B) = (16A + a_l, 16B + s);
+ *           2. pairs inside a full block: columns j and 16 - j share a chunk (s < j: (s, j), else
+ *              (s - j, 16 - j)), the column-8 halves of blocks 2P and 2P + 1 share one;
+ *           3. pairs ending at a tail sample b >= 16 nbf: a = 0 .. b-1 in chunks of 16.
+ *         Unused slots (the tail of a section-3 segment, a lone column-8 half) are zero.
+ *         K = tb_sign_k(n) = n(n-1)/2 + O(n/16) elements: K bytes for TB_SIGN_I8/E4M3, K/2 bytes
+ *         for TB_SIGN_E2M1; the row tail up to ldS is zeroed; ldS (bytes) must be a multiple of 16.
+ *         TB_SIGN_E2M1 stores chunk sample 8w + 4h + j in 32-bit word w, byte j, nibble h, and may
+ *         write ties as -0 (0x8).
  */
 int64_t tb_sign_k(int64_t n);
 int tb_sign_pack(const uint16_t *R, int64_t m, int64_t n, int64_t ldr, int8_t *S, int64_t ldS, int format,

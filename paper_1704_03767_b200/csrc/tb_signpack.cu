@@ -1,62 +1,58 @@
 // K2: sign pack -- each variable's {-1, 0, +1} sign vector over all sample pairs, materialised
-// once (int8) for the tcgen05 GEMM.  Replaces the per-pair sign enumeration of naive_numerator
-// (kernel_naive.py:26-44).  Input: dense uint16 ranks from K0 (tb_rank.cu).
-// HBM-write-bound on S (m * ldS bytes): one CTA per (row, K-range), 16-byte coalesced stores.
-#include <cstdlib>
-
+// once for the tcgen05 GEMM.  Replaces the per-pair sign enumeration of naive_numerator
+// (kernel_naive.py:26-44): S_u . S_v over any fixed ordering of the n(n-1)/2 pairs (a < b) with
+// S_u[k(a,b)] = sign(r_u[b] - r_u[a]) is n_c - n_d.  Input: dense uint16 ranks from K0 (tb_rank.cu).
 #include "tb_common.cuh"
 
 namespace tb {
 
 constexpr int SP_THREADS = 256;
 
-// S layout ("diagonal"): sample pairs are ordered by offset d = b - a (1..n-1), then by a; each
-// d-segment holds n - d signs zero-padded to a multiple of 16 bytes:
-//   S[r, off(d) + a] = sign(x[r, a + d] - x[r, a]),  off(d) = 16 * sum_{d' < d} ceil((n - d') / 16).
-// Zero padding adds nothing to S_u . S_v; it costs <= 16/(n-1) extra MMA work (1.6% at n = 1000).
-__host__ __device__ __forceinline__ int64_t ceil16_prefix(int64_t N) {  // sum_{j=1..N} ceil(j/16)
-    const int64_t q = N >> 4, r = N & 15;
-    return 8 * q * (q + 1) + r * (q + 1);
+// ---------------------------------------------------------------------------------------------
+// "Block" layout of the sample pairs.  S is a sequence of 16-pair chunks (one 16-byte int8/e4m3
+// row segment, or 8 bytes of e2m1); with nbf = floor(n / 16) full 16-sample blocks and nt = n mod 16
+// tail samples:
+//   section 1  pairs between two different full blocks A < B (row-major over (A, B)), 16 chunks per
+//              block pair: chunk a_l of (A, B) holds (a = 16A + a_l, b = 16B + s), s = 0..15;
+//   section 2  pairs inside one full block: per block, 15 b-columns paired j / 16 - j into 7 chunks
+//              (s < j: (s, j); s >= j: (s - j, 16 - j)), and the two b = 8 columns of consecutive
+//              blocks share one chunk (block A0: s < 8 -> (s, 8); block A1: (s - 8, 8));
+//   section 3  pairs ending at a tail sample b = 16 nbf + t: a = 0 .. b-1 in chunks of 16.
+// Only the last chunk of a section-3 segment and a lone section-2 half chunk are partial, so
+// K = 16 * chunks = n(n-1)/2 + O(n / 16) (n = 1000: 499,584 for 499,500 pairs).
+struct SpLayout {
+    int64_t nbf, nt, c1, c2, c3;
+};
+__host__ __device__ __forceinline__ SpLayout sp_layout(int64_t n) {
+    SpLayout L;
+    L.nbf = n / 16;
+    L.nt = n % 16;
+    L.c1 = 16 * (L.nbf * (L.nbf - 1) / 2);
+    L.c2 = 7 * L.nbf + (L.nbf + 1) / 2;
+    L.c3 = L.nt * L.nbf + (L.nt > 0 ? L.nt - 1 : 0);
+    return L;
 }
-__host__ __device__ __forceinline__ int64_t diag_off(int64_t d, int64_t n) {
-    return 16 * (ceil16_prefix(n - 1) - ceil16_prefix(n - d));
+__host__ __device__ __forceinline__ int64_t sp_k(int64_t n) {
+    const SpLayout L = sp_layout(n);
+    return 16 * (L.c1 + L.c2 + L.c3);
 }
-__host__ __device__ __forceinline__ int64_t diag_k(int64_t n) { return diag_off(n, n); }
 
-// Segment-major emission: the 16-byte chunks of a row's S are enumerated in memory order,
-// chunk c <-> (offset d, group g) with S bytes [off(d) + 16 g, +16) = signs of samples
-// a = 16 g .. 16 g + 15 at offset d.  Consecutive threads take consecutive chunks, so every warp
-// store is 512 contiguous bytes and a CTA fills its whole K-range (no partial L2 sectors); each
-// chunk reads its own and window words with 128-bit loads from shifted shared-memory row copies.
-//   D = (w | 0x8000) - o and E = (o | 0x8000) - w per halfword  (2 IADD3, no cross-lane borrow),
-//   ge/le = sign-replicated high bytes of D/E                 (PRMT 0xFDB9),
-//   byte  = (ge ^ le) & (le | 0x01)                            (one LOP3: +1 / -1 / 0).
+// Packed-halfword sign arithmetic on two sample pairs per 32-bit word (ranks < 2^15):
+//   D = (w | 0x8000) - o per halfword (no borrow) -> bit 15: w >= o;  E = 0x10000 - D -> w <= o;
+// a sign-replicating PRMT turns the high bytes into >= / <= masks.
 __device__ __forceinline__ uint32_t prmt_signs(uint32_t lo, uint32_t hi) {
     uint32_t r;
     asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(r) : "r"(lo), "r"(hi));
     return r;
 }
-__device__ __forceinline__ uint32_t sign_bytes(uint32_t ge, uint32_t le) {
+__device__ __forceinline__ uint32_t sign_bytes(uint32_t ge, uint32_t le) {  // (ge ^ le) & (le | 1)
     uint32_t r;
     asm("lop3.b32 %0, %1, %2, %3, 0x2C;" : "=r"(r) : "r"(ge), "r"(le), "r"(0x01010101u));
     return r;
 }
-// smallest N in [1, n-1] with ceil16_prefix(N) >= t
-__device__ __forceinline__ int inv_prefix(int64_t t, int n) {
-    int lo = 1, hi = n - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (ceil16_prefix(mid) >= t) hi = mid;
-        else lo = mid + 1;
-    }
-    return lo;
-}
-
 __device__ __forceinline__ uint4 lds128(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
-// Signs of the 16 samples of one chunk from its 8 own and 8 window rank-pair words.
-// FMT 0: int8 (+1 = 0x01, -1 = 0xFF); FMT 1: e4m3 (0x38 / 0xB8, the kind::f8f6f4 experiment).
-// FMT 2 (e2m1) has its own loop below (chunk_e2m1).
+// int8 (FMT 0: +1 = 0x01, -1 = 0xFF) / e4m3 (FMT 1: 0x38 / 0xB8) chunk: 16 bytes, sample s in byte s.
 template <int FMT>
 __device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint32_t (&own)[8]) {
     uint32_t out[4];
@@ -75,15 +71,10 @@ __device__ __forceinline__ uint4 chunk_signs(const uint32_t (&y)[8], const uint3
     return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
-// e2m1 chunk, 16 signs -> 8 bytes.  Within the chunk, sample 8 w + 4 h + j (w, h in {0,1},
-// j in 0..3) sits in word w, byte j, nibble h: the dot product only needs every row to use the same
-// order, and this one packs with byte merges instead of nibble shuffles.  Ties may come out as -0
-// (0x8), which multiplies like 0.
-//   yb: window words with bit 15 of each halfword set (w + 0x8000), own: plain rank pairs.
-//   D = yb - o = w - o + 0x8000 per halfword (no borrow: w - o in [-32767, 32767]) -> bit 15: w >= o
-//   E = 0x10000 - D per halfword = (-D) + 0x00010000                       -> bit 15: w <= o
-// D and E are IMADs (FMA pipe; `neg1` is a runtime -1 so ptxas keeps them off the ALU pipe), the
-// PRMT sign-replicates the high bytes and three LOP3s per word build the nibbles.
+// e2m1 chunk (FMT 2), 16 signs -> 8 bytes: sample 8 w + 4 h + j sits in word w, byte j, nibble h
+// (byte merges instead of nibble shuffles; every row uses the same order).  +1 = 0x2, -1 = 0xA, ties
+// may come out as -0 (0x8).  yb: window words with bit 15 of each halfword set; own: plain words.
+// D and E are IMADs (FMA pipe; `neg1` is a runtime -1 so ptxas keeps them off the ALU pipe).
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
@@ -94,21 +85,20 @@ __device__ __forceinline__ uint32_t lop3_sel(uint32_t a, uint32_t b, uint32_t m)
     asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "r"(m));
     return r;
 }
-__device__ __forceinline__ uint32_t nib_code(uint32_t ge, uint32_t le) {  // ((ge ^ le) & 0x2) | (le & 0x8) per nibble
+__device__ __forceinline__ uint32_t nib_code(uint32_t ge, uint32_t le) {  // ((ge ^ le) & 0x2) | (le & 0x8)
     const uint32_t x = (ge ^ le) & 0x22222222u;
     uint32_t r;
-    asm("lop3.b32 %0, %1, %2, %3, 0xF8;" : "=r"(r) : "r"(x), "r"(le), "r"(0x88888888u));  // x | (le & c)
+    asm("lop3.b32 %0, %1, %2, %3, 0xF8;" : "=r"(r) : "r"(x), "r"(le), "r"(0x88888888u));
     return r;
 }
-__device__ __forceinline__ uint2 chunk_e2m1(const uint32_t (&yb)[8], const uint32_t (&own)[8], uint32_t neg1,
-                                            uint32_t k10000) {
+__device__ __forceinline__ uint2 chunk_e2m1(const uint32_t (&yb)[8], const uint32_t (&own)[8], uint32_t neg1) {
     uint32_t ge[4], le[4];
 #pragma unroll
     for (int qq = 0; qq < 4; ++qq) {
         const uint32_t d0 = imad(own[2 * qq], neg1, yb[2 * qq]);
         const uint32_t d1 = imad(own[2 * qq + 1], neg1, yb[2 * qq + 1]);
-        const uint32_t e0 = imad(d0, neg1, k10000);
-        const uint32_t e1 = imad(d1, neg1, k10000);
+        const uint32_t e0 = imad(d0, neg1, 0x00010000u);
+        const uint32_t e1 = imad(d1, neg1, 0x00010000u);
         ge[qq] = prmt_signs(d0, d1);
         le[qq] = prmt_signs(e0, e1);
     }
@@ -117,135 +107,164 @@ __device__ __forceinline__ uint2 chunk_e2m1(const uint32_t (&yb)[8], const uint3
     return make_uint2(w0, w1);
 }
 
-// Shared memory holds 8 shifted copies of the row's rank pairs, C[o][s][j] = pair at halfword
-// 2 (j + s) + o, so the window of chunk (d, g) -- halfwords 16 g + d .. +15 -- is 8 words starting
-// at the 16-byte-aligned index 8 g + ((d >> 1) & ~3) of copy (d & 1, (d >> 1) & 3): two 128-bit
-// loads, no per-lane shifting.
+// Sections 2 and 3 (~3% of the chunks): per-sample (a, b) lists -> own / window words and the
+// number of valid leading samples.
+__device__ __forceinline__ int sp_slow_chunk(int64_t c, const SpLayout& L, const uint16_t* r16, const uint32_t* wp,
+                                             uint32_t (&own)[8], uint32_t (&y)[8]) {
+    const int nbf = (int)L.nbf;
+    const int64_t k2 = c - L.c1;
+    if (k2 < L.c2) {
+        const int P = (int)(k2 / 15), k = (int)(k2 - 15 * (int64_t)P);
+        const int A0 = 2 * P, A1 = 2 * P + 1;
+        if (k < 14 && (k < 7 || A1 < nbf)) {  // a paired j / 16 - j chunk of block blk
+            const int blk = k < 7 ? A0 : A1, j = k < 7 ? k + 1 : k - 6;
+            const uint16_t* rb = r16 + 16 * blk;
+            const uint32_t w1 = rb[j], w2 = rb[16 - j];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int s0 = 2 * q, s1 = 2 * q + 1;
+                own[q] = (uint32_t)rb[s0 < j ? s0 : s0 - j] | ((uint32_t)rb[s1 < j ? s1 : s1 - j] << 16);
+                y[q] = (s0 < j ? w1 : w2) | ((s1 < j ? w1 : w2) << 16);
+            }
+            return 16;
+        }
+        // the b = 8 columns of A0 and A1 (or A0 alone: 8 valid samples)
+        const int B1 = A1 < nbf ? A1 : A0;
+        const uint32_t w1 = r16[16 * A0 + 8], w2 = r16[16 * B1 + 8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            own[q] = wp[8 * A0 + q];
+            own[q + 4] = wp[8 * B1 + q];
+            y[q] = w1 * 0x10001u;
+            y[q + 4] = w2 * 0x10001u;
+        }
+        return A1 < nbf ? 16 : 8;
+    }
+    int64_t k3 = k2 - L.c2;  // tail segment t has nbf + (t > 0) chunks
+    int t = 0;
+    while (k3 >= L.nbf + (t > 0 ? 1 : 0)) {
+        k3 -= L.nbf + (t > 0 ? 1 : 0);
+        ++t;
+    }
+    const int b = 16 * nbf + t, i = (int)k3;
+    const uint4 o0 = lds128(wp + 8 * i), o1 = lds128(wp + 8 * i + 4);
+    own[0] = o0.x; own[1] = o0.y; own[2] = o0.z; own[3] = o0.w;
+    own[4] = o1.x; own[5] = o1.y; own[6] = o1.z; own[7] = o1.w;
+    const uint32_t rbb = (uint32_t)r16[b] * 0x10001u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = rbb;
+    return min(16, b - 16 * i);
+}
 
+// One CTA per (row, K-range); warps take contiguous chunk ranges and consecutive lanes consecutive
+// chunks (coalesced stores).  Section 1 needs no per-lane decode after the start: a 32-chunk step is
+// exactly two block pairs, and a_l = c mod 16 stays fixed.  The window of block B is 8 aligned words
+// shared by the 16 lanes on that block (broadcast loads); own is one broadcast rank.
 template <int FMT>
 __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t* __restrict__ R, int64_t n,
                                                               int64_t ldr, int8_t* __restrict__ S, int64_t ldS,
-                                                              int64_t K, int nwc, uint32_t neg1) {
-    extern __shared__ __align__(16) uint32_t sp_words[];  // [8][nwc] (+ [nwc] plain own copy for e2m1)
+                                                              int nw, uint32_t neg1) {
+    extern __shared__ __align__(16) uint32_t sp_words[];  // wp[nw] plain pairs, wb[nw] biased, masks[17]
+    uint32_t* wp = sp_words;
+    uint32_t* wb = sp_words + nw;
+    uint4* masks = reinterpret_cast<uint4*>(sp_words + 2 * nw);
     const int64_t r = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nn = (int)n;
     const uint16_t* rr = R + r * ldr;
-    for (int j = tid; j < nwc; j += SP_THREADS) {
-#pragma unroll
-        for (int o = 0; o < 2; ++o) {
-#pragma unroll
-            for (int sh = 0; sh < 4; ++sh) {
-                const int h = 2 * (j + sh) + o;  // halfword index of the pair's low half
-                const uint32_t lo = h < nn ? rr[h] : 0u, hi = h + 1 < nn ? rr[h + 1] : 0u;
-                const uint32_t wv = lo | (hi << 16);
-                sp_words[(o * 4 + sh) * nwc + j] = FMT == 2 ? (wv | 0x80008000u) : wv;
-                if (FMT == 2 && o == 0 && sh == 0) sp_words[8 * nwc + j] = wv;
-            }
-        }
+    for (int j = tid; j < nw; j += SP_THREADS) {
+        const int h = 2 * j;
+        const uint32_t lo = h < nn ? rr[h] : 0u, hi = h + 1 < nn ? rr[h + 1] : 0u;
+        wp[j] = lo | (hi << 16);
+        wb[j] = lo | (hi << 16) | 0x80008000u;
     }
-    if (FMT == 2 && tid < 32) {  // tail masks: [swapped][lim] for the last chunk of a segment
-        const int lim = tid & 15, swp = tid >> 4;
-        uint32_t mk[2] = {0u, 0u};
-        for (int i = 0; i < lim; ++i) mk[i >> 3] |= 0xFu << (8 * (i & 3) + 4 * ((i >> 2) & 1));
-        reinterpret_cast<uint2*>(sp_words + 9 * nwc)[tid] = swp ? make_uint2(mk[1], mk[0]) : make_uint2(mk[0], mk[1]);
+    if (tid <= 16) {  // masks[v]: the first v samples of a chunk kept
+        uint32_t mk0 = 0u, mk1 = 0u, mk2 = 0u, mk3 = 0u;
+        for (int s = 0; s < tid; ++s) {
+            const int wi = FMT == 2 ? (s >> 3) : (s >> 2);
+            const uint32_t bits = FMT == 2 ? 0xFu << (8 * (s & 3) + 4 * ((s >> 2) & 1)) : 0xFFu << (8 * (s & 3));
+            mk0 |= wi == 0 ? bits : 0u;
+            mk1 |= wi == 1 ? bits : 0u;
+            mk2 |= wi == 2 ? bits : 0u;
+            mk3 |= wi == 3 ? bits : 0u;
+        }
+        masks[tid] = make_uint4(mk0, mk1, mk2, mk3);
     }
     __syncthreads();
+    const uint16_t* r16 = reinterpret_cast<const uint16_t*>(wp);
+    const uint32_t* win = FMT == 2 ? wb : wp;
 
+    const SpLayout L = sp_layout(n);
+    const int nchunks = (int)(L.c1 + L.c2 + L.c3);  // < 2^31 (n <= 32767)
+    const int c1 = (int)L.c1;
     int8_t* row = S + r * ldS;
-    const int nchunks = (int)(K >> 4);  // < 2^31: K < 2^34 for n <= 32767... K/16 < 2^30
     const int per = (nchunks + (int)gridDim.y - 1) / (int)gridDim.y;
     const int b_lo = (int)blockIdx.y * per, b_hi = min(b_lo + per, nchunks);
     const int wper = (b_hi - b_lo + (SP_THREADS / 32) - 1) / (SP_THREADS / 32);
     const int c_lo = b_lo + warp * wper, c_hi = min(c_lo + wper, b_hi);
     int c = c_lo + lane;
-    if (c < c_hi) {
-        // decode chunk c -> (d, g): off(d)/16 = P(n-1) - P(n-d) <= c < P(n-1) - P(n-d-1)
-        const int64_t top = ceil16_prefix(nn - 1);
-        const int N = inv_prefix(top - c, nn);  // n - d
-        int d = nn - N;
-        int g = (int)(c - (top - ceil16_prefix(N)));
-        int G = (nn - d + 15) >> 4;
-        // window base of offset d: copy (d & 1, (d >> 1) & 3), 16-byte-aligned word (d >> 1) & ~3
-        int wbase = ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + ((d >> 1) & ~3);
-        if (FMT == 2) {
-            // Bank swizzle: chunks with bit 2 of g set read their second 16 bytes first, so 8
-            // consecutive chunks' 128-bit loads cover all 32 banks.  Their two output words come out
-            // swapped -- a fixed per-chunk sample order, identical in every row.  A 32-chunk step
-            // keeps bit 2 of g, so the swizzle (and the pointers) only change at a segment crossing.
-            const uint2* masks = reinterpret_cast<const uint2*>(sp_words + 9 * nwc);
-            uint2* outp = reinterpret_cast<uint2*>(row) + c;
-            int sw = ((g >> 2) & 1) * 4;
-            const uint32_t* own_p = sp_words + 8 * nwc + 8 * g + sw;
-            const uint32_t* win_p = sp_words + wbase + 8 * g + sw;
-            int lim = nn - d - 16 * g;  // samples 16 g + i valid for i < lim
-            for (;;) {
-                const uint4 o0 = lds128(own_p), o1 = lds128(own_p + (4 - 2 * sw));
-                const uint4 w0 = lds128(win_p), w1 = lds128(win_p + (4 - 2 * sw));
-                const uint32_t own[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-                const uint32_t y[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-                uint2 v2 = chunk_e2m1(y, own, neg1, 0x00010000u);
-                if (lim < 16) {
-                    const uint2 mk = masks[lim + 4 * sw];
-                    v2.x &= mk.x;
-                    v2.y &= mk.y;
-                }
-                *outp = v2;
-                c += 32;
-                if (c >= c_hi) break;
-                outp += 32;
-                g += 32;
-                own_p += 256;
-                win_p += 256;
-                lim -= 512;
-                if (g >= G) {
-                    do {
-                        g -= G;
-                        ++d;
-                        G = (nn - d + 15) >> 4;
-                    } while (g >= G);
-                    wbase = ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + ((d >> 1) & ~3);
-                    sw = ((g >> 2) & 1) * 4;
-                    own_p = sp_words + 8 * nwc + 8 * g + sw;
-                    win_p = sp_words + wbase + 8 * g + sw;
-                    lim = nn - d - 16 * g;
-                }
-            }
-        }
-        for (; FMT != 2;) {
-            const int lim = nn - d - 16 * g;  // samples 16 g + i valid for i < lim
-            const uint32_t* own_p = sp_words + 8 * g;
-            const uint32_t* win_p = sp_words + wbase + 8 * g;
-            const uint4 o0 = lds128(own_p), o1 = lds128(own_p + 4);
-            const uint4 w0 = lds128(win_p), w1 = lds128(win_p + 4);
-            const uint32_t own[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+    const int nbf = (int)L.nbf;
+    // ---- section 1: block pairs (A < B); per step B += 2, own changes only with A
+    const int c1_end = min(c_hi, c1);
+    if (c < c1_end) {
+        const int al = c & 15;
+        const int bid = c >> 4;
+        const double f = (double)nbf - 0.5;
+        int A = (int)(f - sqrt(f * f - 2.0 * (double)bid));
+        if (A < 0) A = 0;
+        auto start = [nbf](int x) { return x * (nbf - 1) - x * (x - 1) / 2; };
+        while (A > 0 && start(A) > bid) --A;
+        while (A < nbf - 1 && start(A + 1) <= bid) ++A;
+        int B = bid - start(A) + A + 1;
+        uint32_t o2 = (uint32_t)r16[16 * A + al] * 0x10001u;
+        const uint32_t* wptr = win + 8 * B;
+        for (;;) {
+            const uint4 w0 = lds128(wptr), w1 = lds128(wptr + 4);
             const uint32_t y[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-            uint4 v = chunk_signs<FMT>(y, own);
-            if (lim < 16) {
-                uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int qq = 0; qq < 4; ++qq) {
-                    const int cnt = min(max(lim - 4 * qq, 0), 4);
-                    w4[qq] &= cnt == 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u);
-                }
-                v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-            }
-            *reinterpret_cast<uint4*>(row + 16 * (int64_t)c) = v;
+            const uint32_t own[8] = {o2, o2, o2, o2, o2, o2, o2, o2};
+            if (FMT == 2)
+                *reinterpret_cast<uint2*>(row + 8 * (int64_t)c) = chunk_e2m1(y, own, neg1);
+            else
+                *reinterpret_cast<uint4*>(row + 16 * (int64_t)c) = chunk_signs<FMT>(y, own);
             c += 32;
-            if (c >= c_hi) break;
-            g += 32;
-            if (g >= G) {
+            if (c >= c1_end) break;
+            B += 2;
+            wptr += 16;
+            if (B >= nbf) {  // row A + 1 starts at B = A + 2
                 do {
-                    g -= G;
-                    ++d;
-                    G = (nn - d + 15) >> 4;
-                } while (g >= G);
-                wbase = ((d & 1) * 4 + ((d >> 1) & 3)) * nwc + ((d >> 1) & ~3);
+                    ++A;
+                    B += A + 1 - nbf;
+                } while (B >= nbf && A < nbf - 1);
+                wptr = win + 8 * B;
+                o2 = (uint32_t)r16[16 * A + al] * 0x10001u;
             }
         }
     }
+    // ---- sections 2 and 3 (~3% of the chunks): per-sample lists, partial chunks masked
+    for (; c < c_hi; c += 32) {
+        uint32_t own[8], y[8];
+        const int valid = sp_slow_chunk(c, L, r16, wp, own, y);
+        if (FMT == 2) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) y[q] |= 0x80008000u;
+            uint2 v2 = chunk_e2m1(y, own, neg1);
+            if (valid < 16) {
+                const uint4 mk = masks[valid];
+                v2.x &= mk.x;
+                v2.y &= mk.y;
+            }
+            *reinterpret_cast<uint2*>(row + 8 * (int64_t)c) = v2;
+        } else {
+            uint4 v = chunk_signs<FMT>(y, own);
+            if (valid < 16) {
+                const uint4 mk = masks[valid];
+                v.x &= mk.x; v.y &= mk.y; v.z &= mk.z; v.w &= mk.w;
+            }
+            *reinterpret_cast<uint4*>(row + 16 * (int64_t)c) = v;
+        }
+    }
     // zero the row tail [K bytes, ldS)
-    const int64_t kb = FMT == 2 ? K / 2 : K;
+    const int64_t kb = (FMT == 2 ? 8 : 16) * (int64_t)nchunks;
     for (int64_t k = kb + ((int64_t)blockIdx.y * SP_THREADS + tid) * 8; k < ldS; k += (int64_t)gridDim.y * SP_THREADS * 8)
         *reinterpret_cast<uint2*>(row + k) = make_uint2(0u, 0u);
 }
@@ -259,7 +278,7 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "sign_pack: need m >= 1 and n >= 2 (got m=%lld n=%lld)",
                                     (long long)m, (long long)n);
     if (n > 32767) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld exceeds 32767 (15-bit ranks)", (long long)n);
-    const int64_t K = diag_k(n);
+    const int64_t K = sp_k(n);
     if (format < 0 || format > 2) return fail(TB_ERR_CONFIG, "sign_pack: unknown format %d", format);
     const int64_t kbytes = format == TB_SIGN_E2M1 ? K / 2 : K;
     if (ldS < kbytes || (ldS & 15))
@@ -267,9 +286,8 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
                     (long long)kbytes);
     if (ldr < n || (ldr & 1)) return fail(TB_ERR_CONFIG, "sign_pack: ldr must be even and >= n");
     if (!R || !S) return fail(TB_ERR_INVALID, "sign_pack: null pointer");
-    const int nwc = (int)(((n + 1) / 2 + 16 + 3) & ~3);  // words per shifted copy (window reads overrun n)
-    const size_t smem = (size_t)(format == TB_SIGN_E2M1 ? 9 : 8) * nwc * sizeof(uint32_t) + 32 * sizeof(uint2);
-    if (smem > 200 * 1024) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld too large for the shared row copies", (long long)n);
+    const int nw = (int)(((n + 1) / 2 + 8 + 3) & ~3);  // rank-pair words (window loads of the last block)
+    const size_t smem = (size_t)2 * nw * sizeof(uint32_t) + 17 * sizeof(uint4);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t nblk = (K / 16 + 16 * SP_THREADS - 1) / (16 * SP_THREADS);  // >= 16 chunks per thread
     int64_t want = (8 * (int64_t)num_sms() + m - 1) / m;  // >= ~8 CTAs per SM in total
@@ -277,7 +295,7 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
     dim3 grid((unsigned)m, gy);
 #define TB_SP_LAUNCH(F)                                                                                   \
     TB_CUDA_TRY(cudaFuncSetAttribute(signpack_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    signpack_kernel<F><<<grid, SP_THREADS, smem, st>>>(R, n, ldr, S, ldS, K, nwc, 0xFFFFFFFFu)
+    signpack_kernel<F><<<grid, SP_THREADS, smem, st>>>(R, n, ldr, S, ldS, nw, 0xFFFFFFFFu)
     if (format == TB_SIGN_E2M1) {
         TB_SP_LAUNCH(2);
     } else if (format == TB_SIGN_E4M3) {
@@ -315,4 +333,4 @@ extern "C" int tb_abs_pack(const int8_t* S, int64_t m, int64_t ldS, int format, 
     return check_launch("abs_pack_kernel");
 }
 
-extern "C" int64_t tb_sign_k(int64_t n) { return n >= 2 ? tb::diag_k(n) : 0; }
+extern "C" int64_t tb_sign_k(int64_t n) { return n >= 2 ? tb::sp_k(n) : 0; }

@@ -149,3 +149,18 @@ def test_no_oracle_in_product_path():
                 with open(os.path.join(dirpath, f)) as fh:
                     src = fh.read()
                 assert "import oracle" not in src and "tau_oracle" not in src and "libtauoracle" not in src, f
+
+
+def test_sign_k_block_layout():
+    """tb_sign_k(n): 16 x (chunks of the block layout), >= n(n-1)/2 with < 16 * (n / 16 + 16) slack."""
+    from paper_1704_03767_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libtaub200.so not built")
+    lib = _lib.load()
+    for n in list(range(2, 70)) + [255, 256, 500, 1000, 1024, 5793, 8192, 32767]:
+        nbf, nt = divmod(n, 16)
+        chunks = 16 * (nbf * (nbf - 1) // 2) + 7 * nbf + (nbf + 1) // 2 + nt * nbf + max(nt - 1, 0)
+        k = int(lib.tb_sign_k(n))
+        assert k == 16 * chunks, n
+        assert n * (n - 1) // 2 <= k < n * (n - 1) // 2 + 16 * (nbf + 16), n
+    assert int(lib.tb_sign_k(1000)) == 499584
