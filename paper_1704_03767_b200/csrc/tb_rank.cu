@@ -162,14 +162,80 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E], int lane) {
     }
 }
 
+// Small-range integer rows (codes, counts, Likert scales: max - min < 1024): dense ranks from a
+// per-warp histogram -- present values in value order get consecutive ranks -- and n1 = sum
+// c (c - 1) / 2 over the counts, O(n + range).  A lean kernel of its own (raw 32-bit keys, few
+// registers, full occupancy); rows with a wider range are marked n1[r] = RK_TODO for the sort.
+constexpr unsigned long long RK_TODO = ~0ull;
+
+template <int E>
+__global__ void __launch_bounds__(256) rank_rows_hist_kernel(const int32_t* __restrict__ x, int64_t m, int64_t n,
+                                                             int64_t ldx, uint16_t* __restrict__ R, int64_t ldr,
+                                                             unsigned long long* __restrict__ n1) {
+    constexpr int HR = 1024;
+    __shared__ int32_t hist[8][HR];
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= m) return;
+    const int nn = (int)n;
+    uint32_t k[E];
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        const int e = lane + 32 * i;
+        k[i] = e < nn ? (uint32_t)x[r * ldx + e] ^ 0x80000000u : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+        if (lane + 32 * i < nn) {
+            kmin = min(kmin, k[i]);
+            kmax = max(kmax, k[i]);
+        }
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (kmax - kmin >= (uint32_t)HR) {
+        if (lane == 0) n1[r] = RK_TODO;
+        return;
+    }
+    int32_t* h = hist[threadIdx.x >> 5];
+    const int rounds = (int)((kmax - kmin) >> 5) + 1;
+    for (int j = 0; j < rounds; ++j) h[32 * j + lane] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+        if (lane + 32 * i < nn) atomicAdd(&h[k[i] - kmin], 1);
+    __syncwarp();
+    int base = 0;
+    unsigned long long ties = 0;
+    for (int j = 0; j < rounds; ++j) {
+        const int c = h[32 * j + lane];
+        const unsigned b = __ballot_sync(0xffffffffu, c > 0);
+        h[32 * j + lane] = base + __popc(b & ((1u << lane) - 1u));
+        base += __popc(b);
+        ties += (unsigned long long)c * (unsigned long long)(c - 1) / 2ull;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        const int e = lane + 32 * i;
+        if (e < nn) R[r * ldr + e] = (uint16_t)h[k[i] - kmin];
+    }
+    for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
+    if (lane == 0) n1[r] = ties;
+    for (int64_t i = nn + lane; i < ldr; i += 32) R[r * ldr + i] = 0;
+}
+
 template <typename T, int E>
 __global__ void __launch_bounds__(256) rank_rows_warp_kernel(const T* __restrict__ x, int64_t m, int64_t n,
                                                              int64_t ldx, uint16_t* __restrict__ R, int64_t ldr,
                                                              unsigned long long* __restrict__ n1,
-                                                             int32_t* __restrict__ flags) {
+                                                             int32_t* __restrict__ flags, int only_marked) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r >= m) return;
+    if (only_marked && n1[r] != RK_TODO) return;  // already ranked by rank_rows_hist_kernel
     const int nn = (int)n;
     uint64_t v[E];
     bool bad = false;
@@ -185,54 +251,6 @@ __global__ void __launch_bounds__(256) rank_rows_warp_kernel(const T* __restrict
         v[i] = (key << 16) | (uint64_t)e;
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1);
-    if constexpr (std::is_same<T, int32_t>::value) {
-        // Small-range integer rows (codes, counts, Likert scales: max - min < 1024): dense ranks
-        // from a per-warp histogram -- present values in value order get consecutive ranks -- and
-        // n1 = sum c (c - 1) / 2 over the counts.  O(n + range) instead of the bitonic sort.
-        constexpr int HR = 1024;
-        __shared__ int32_t hist[8][HR];
-        uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
-#pragma unroll
-        for (int i = 0; i < E; ++i)
-            if (lane + 32 * i < nn) {
-                const uint32_t k = (uint32_t)(v[i] >> 16);
-                kmin = min(kmin, k);
-                kmax = max(kmax, k);
-            }
-        for (int o = 16; o > 0; o >>= 1) {
-            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-        }
-        if (kmax - kmin < (uint32_t)HR) {
-            int32_t* h = hist[threadIdx.x >> 5];
-            const int rounds = (int)((kmax - kmin) >> 5) + 1;
-            for (int j = 0; j < rounds; ++j) h[32 * j + lane] = 0;
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < E; ++i)
-                if (lane + 32 * i < nn) atomicAdd(&h[(uint32_t)(v[i] >> 16) - kmin], 1);
-            __syncwarp();
-            int base = 0;
-            unsigned long long ties = 0;
-            for (int j = 0; j < rounds; ++j) {
-                const int c = h[32 * j + lane];
-                const unsigned b = __ballot_sync(0xffffffffu, c > 0);
-                h[32 * j + lane] = base + __popc(b & ((1u << lane) - 1u));
-                base += __popc(b);
-                ties += (unsigned long long)c * (unsigned long long)(c - 1) / 2ull;
-            }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < E; ++i) {
-                const int e = lane + 32 * i;
-                if (e < nn) R[r * ldr + e] = (uint16_t)h[(uint32_t)(v[i] >> 16) - kmin];
-            }
-            for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
-            if (lane == 0) n1[r] = ties;
-            for (int64_t i = nn + lane; i < ldr; i += 32) R[r * ldr + i] = 0;
-            return;
-        }
-    }
     warp_bitonic<E>(v, lane);
     // dense ranks over slots [0, n): flag = key differs from the previous slot's key
     const uint64_t prev_last = __shfl_up_sync(0xffffffffu, v[E - 1], 1);
@@ -282,15 +300,34 @@ template <typename T>
 static int launch_rank_warp(const T* x, int64_t m, int64_t n, int64_t ldx, uint16_t* R, int64_t ldr,
                             unsigned long long* n1, int32_t* flags, int Np, cudaStream_t st) {
     const unsigned grid = (unsigned)((m + 7) / 8);
+    int only_marked = 0;
+    if constexpr (std::is_same<T, int32_t>::value) {  // histogram pass first; the sort takes the rest
+        only_marked = 1;
+#define TB_RK_HIST(E) rank_rows_hist_kernel<E><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1); break
+        switch (Np / 32) {
+            case 1: TB_RK_HIST(1);
+            case 2: TB_RK_HIST(2);
+            case 4: TB_RK_HIST(4);
+            case 8: TB_RK_HIST(8);
+            case 16: TB_RK_HIST(16);
+            case 32: TB_RK_HIST(32);
+            default: return fail(TB_ERR_CONFIG, "rank_rows: bad warp sort size");
+        }
+#undef TB_RK_HIST
+        int rc = check_launch("rank_rows_hist_kernel");
+        if (rc) return rc;
+    }
+#define TB_RK_WARP(E) rank_rows_warp_kernel<T, E><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags, only_marked); break
     switch (Np / 32) {
-        case 1: rank_rows_warp_kernel<T, 1><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
-        case 2: rank_rows_warp_kernel<T, 2><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
-        case 4: rank_rows_warp_kernel<T, 4><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
-        case 8: rank_rows_warp_kernel<T, 8><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
-        case 16: rank_rows_warp_kernel<T, 16><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
-        case 32: rank_rows_warp_kernel<T, 32><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags); break;
+        case 1: TB_RK_WARP(1);
+        case 2: TB_RK_WARP(2);
+        case 4: TB_RK_WARP(4);
+        case 8: TB_RK_WARP(8);
+        case 16: TB_RK_WARP(16);
+        case 32: TB_RK_WARP(32);
         default: return fail(TB_ERR_CONFIG, "rank_rows: bad warp sort size");
     }
+#undef TB_RK_WARP
     return check_launch("rank_rows_warp_kernel");
 }
 

@@ -17,8 +17,8 @@ def call(name, *a):
     return r
 dv._lib.call = call
 verbose = os.environ.get("TL_VERBOSE") == "1"
-for fr in [(1.0,), (0.34, 0.33, 0.33), (0.55, 0.30, 0.15), (0.6, 0.25, 0.15), (0.5, 0.25, 0.15, 0.1), (0.7, 0.2, 0.1), (0.45, 0.3, 0.15, 0.1)]:
-    for hc in (1, 2):
+for fr in [(0.55, 0.30, 0.15), (0.6, 0.3, 0.1), (0.5, 0.3, 0.2), (0.65, 0.25, 0.1), (0.45, 0.3, 0.15, 0.1)]:
+    for hc in (1, 2, 3):
         tt = []
         for it in range(8):
             marks.clear()
