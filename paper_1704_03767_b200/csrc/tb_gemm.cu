@@ -4,18 +4,16 @@
 // is a dot product of the two rows' {-1,0,+1} sign vectors, so the all-pairs
 // numerator matrix is the SYRK S S^T over K = n(n-1)/2, exact in int32.
 //
-// Design (sm_100a):
-//  * logical 256 x 256 tiles over the upper triangle of the m x m pair matrix,
-//    numbered with the reference bijection (pairindex.py:58-65) and decoded on
-//    device (float sqrt + integer fix-up, tb::job_coord);
-//  * a work unit = (tile, 128-row half, K split); a persistent grid of one CTA
-//    per SM walks units with a static stride, split-major so concurrently
-//    running CTAs stream the same K-slab of S through L2;
-//  * warp 0: TMA producer (128-byte swizzled K-major boxes of S, 4-stage
-//    mbarrier ring, 48 KiB/stage); warp 1: single-thread tcgen05.mma.kind::i8
-//    issuer (M=128, N=256, K=32 per instruction) into a double-buffered TMEM
-//    accumulator (2 x 256 columns); warps 4-7: epilogue (tcgen05.ld -> masked
-//    store / red.add of the int32 numerator in job-id order);
+// This file holds the int8 (kind::i8) / e4m3 (kind::f8f6f4) generation of the GEMM, used when the
+// FP4 path's f32 sums could overflow 2^24 (K >= 2^24, n > ~5790; tb_gemm_fp4.cu is the default), the
+// SIMT dp4a cross-check kernel and the shared TMA helpers.
+//  * units = 256-row x 512-column blocks of the upper triangle (512-tiles decoded on device with the
+//    reference bijection, pairindex.py:58-65), rasterised in 2048 x 2048 super-blocks, split-K;
+//  * a persistent grid of CTA pairs (cta_group::2) walks units split-major so concurrently running
+//    pairs stream the same K-slab of S through L2;
+//  * warp 0: TMA producer (128-byte swizzled K-major boxes, 4-stage mbarrier ring); warp 1 of the
+//    leader CTA: single-thread tcgen05.mma issuer (M=256, two N=256 blocks, K=32 per instruction);
+//    warps 4-7 of both CTAs: epilogue (tcgen05.ld -> masked store / red.add in job-id order);
 //  * split-K partials are integer, so atomic accumulation is deterministic.
 #include <algorithm>
 #include <cstdlib>
@@ -27,191 +25,6 @@
 
 namespace tb {
 
-namespace gemm {
-constexpr int TILE = 256;  // logical square tile (pair-matrix rows x cols)
-constexpr int BM = 128;    // UMMA M (rows of one unit)
-constexpr int BN = 256;    // UMMA N
-constexpr int BK = 128;    // bytes of K per pipeline stage (= one 128B swizzle atom)
-constexpr int UK = 32;     // K per tcgen05.mma.kind::i8
-constexpr int STAGES = 4;
-constexpr uint32_t A_BYTES = BM * BK;
-constexpr uint32_t B_BYTES = BN * BK;
-constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int THREADS = 256;
-constexpr uint32_t TMEM_COLS = 512;  // two 128 x 256 int32 accumulators
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
-}  // namespace gemm
-
-struct GemmArgs {
-    int64_t m;
-    int64_t w;        // tile-matrix width ceil(m / 256)
-    int64_t tile_lo;  // first tile id
-    int64_t ntiles;
-    int32_t splits;
-    int32_t nkb;      // K blocks of 128 bytes
-    int64_t job_lo, job_hi;
-    int32_t* num;
-    int32_t atomic;
-};
-
-struct Unit {
-    int64_t y0, x0;  // first pair-matrix row / column of the unit
-    int32_t kb0, kb1;
-};
-
-__device__ __forceinline__ Unit decode_unit(const GemmArgs& p, int64_t u) {
-    const int64_t per_split = p.ntiles * 2;
-    const int32_t s = (int32_t)(u / per_split);
-    const int64_t rem = u - (int64_t)s * per_split;
-    int64_t Y, X;
-    job_coord(p.tile_lo + (rem >> 1), p.w, Y, X);
-    Unit out;
-    out.y0 = Y * gemm::TILE + (rem & 1) * gemm::BM;
-    out.x0 = X * gemm::TILE;
-    out.kb0 = (int32_t)((int64_t)s * p.nkb / p.splits);
-    out.kb1 = (int32_t)((int64_t)(s + 1) * p.nkb / p.splits);
-    return out;
-}
-
-__global__ void __launch_bounds__(gemm::THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                   GemmArgs p) {
-    using namespace gemm;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-
-    if (warp == 0 && lane == 0) {
-        tma_prefetch(&tmap_a);
-        tma_prefetch(&tmap_b);
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    const int64_t nunits = p.ntiles * 2 * p.splits;
-
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
-                const Unit t = decode_unit(p, u);
-                for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-                    uint8_t* sa = smem + stage * STAGE_BYTES;
-                    tma_load_2d(sa, &tmap_a, &full[stage], kb * BK, (int32_t)t.y0);
-                    tma_load_2d(sa + A_BYTES, &tmap_b, &full[stage], kb * BK, (int32_t)t.x0);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer (single thread)
-            constexpr uint32_t idesc = idesc_i8(BM, BN);
-            int stage = 0;
-            uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
-                const Unit t = decode_unit(p, u);
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d = tmem_base + acc * BN;
-                for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-                    const uint64_t adesc = umma_desc_k_sw128(sa);
-                    const uint64_t bdesc = umma_desc_k_sw128(sa + A_BYTES);
-#pragma unroll
-                    for (int k = 0; k < BK / UK; ++k) {
-                        // advance along K inside the 128B swizzle atom: +32 bytes = +2 in 16B units
-                        mma_i8(d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > t.kb0 || k > 0) ? 1u : 0u);
-                    }
-                    mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-                mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
-            }
-        }
-    } else if (warp >= 4) {  // ---------------- epilogue (TMEM lane quadrant = warp % 4)
-        const int q = warp & 3;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        const int64_t m = p.m;
-        const int64_t span = p.job_hi - p.job_lo;
-        for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
-            const Unit t = decode_unit(p, u);
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            const int64_t y = t.y0 + q * 32 + lane;
-            // J(y, x) - job_lo = base + x for x >= y
-            const int64_t base = row_prefix(y, m) - y - p.job_lo;
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, r);
-                tmem_ld_wait();
-                if (y < m) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int64_t x = t.x0 + c + i;
-                        const int64_t j = base + x;
-                        if (x >= y && x < m && j >= 0 && j < span) {
-                            if (p.atomic)
-                                atomicAdd(&p.num[j], (int32_t)r[i]);
-                            else
-                                p.num[j] = (int32_t)r[i];
-                        }
-                    }
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
-        }
-    }
-    __syncthreads();
-    if (warp == 2) {
-        tc_fence_after();
-        tmem_dealloc<TMEM_COLS>(tmem_base);
-    }
-}
-
-
-// ============================================================================ K3 v2: 2-SM pairs
-// A CTA pair (cluster of 2, tcgen05 cta_group::2) owns a 256-row x 512-column unit of the pair
-// matrix: M = 256 split across the two CTAs (128 rows of A each), N = 512 issued as two N=256 MMAs
-// into TMEM columns [0,256) and [256,512); each CTA stages only its 128-row half of each N block,
-// so per SM the operand traffic per MMA is half of the 1-SM kernel's (L2-bandwidth relief).
-// Units are (512 x 512 tile of the upper triangle, 256-row half); the host orders them in
-// 2048 x 2048 super-tiles (L2 reuse across the concurrently running pairs) and the device decodes
-// each tile id with the reference bijection (tb::job_coord).  N blocks lying entirely below the
-// diagonal are skipped (no load, no MMA).
 namespace gemm2 {
 constexpr int TILE = 512;
 constexpr int UM = 256;       // pair M
@@ -239,7 +52,6 @@ struct Gemm2Args {
     int64_t job_lo, job_hi;
     int32_t* num;
     int32_t atomic;
-    int64_t iters_per_pair;  // > 0: stream-K schedule over the (unit, k-block) iteration space
     int32_t fp8;             // experiment: e4m3 operands, f32 accumulators (kind::f8f6f4)
 };
 
@@ -261,47 +73,27 @@ __device__ __forceinline__ Unit2 unit_geometry(const Gemm2Args& p, int64_t i) {
     return o;
 }
 
-// Work sequence of one CTA pair.  Static schedule: units u = pair, pair + npairs, ... of the
-// split-major list (unit i, K split s).  Stream-K schedule: the pair's contiguous slice
-// [pair * ipp, (pair + 1) * ipp) of the flattened (unit, k-block) space, cut at unit boundaries.
+// Work sequence of one CTA pair: units u = pair, pair + npairs, ... of the split-major list
+// (unit i, K split s).
 struct WorkIter {
     int64_t cur, end, step;
 };
 __device__ __forceinline__ WorkIter work_begin(const Gemm2Args& p, int64_t pair, int64_t npairs) {
     WorkIter w;
-    if (p.iters_per_pair > 0) {
-        const int64_t total = p.nunits * (int64_t)p.nkb;
-        w.cur = min(pair * p.iters_per_pair, total);
-        w.end = min(w.cur + p.iters_per_pair, total);
-        w.step = 0;
-    } else {
-        w.cur = pair;
-        w.end = p.nunits * p.splits;
-        w.step = npairs;
-    }
+    w.cur = pair;
+    w.end = p.nunits * p.splits;
+    w.step = npairs;
     return w;
 }
 __device__ __forceinline__ bool work_next(const Gemm2Args& p, WorkIter& w, Unit2& t) {
     if (w.cur >= w.end) return false;
-    if (w.step == 0) {
-        const int64_t i = w.cur / p.nkb;
-        const int32_t kb0 = (int32_t)(w.cur - i * p.nkb);
-        const int64_t rem = w.end - w.cur;
-        const int32_t kb1 = (int32_t)(rem < (int64_t)(p.nkb - kb0) ? kb0 + rem : p.nkb);
-        t = unit_geometry(p, i);
-        t.kb0 = kb0;
-        t.kb1 = kb1;
-        t.partial = kb0 > 0 || kb1 < p.nkb;
-        w.cur += kb1 - kb0;
-    } else {
-        const int32_t s = (int32_t)(w.cur / p.nunits);
-        const int64_t i = w.cur - (int64_t)s * p.nunits;
-        t = unit_geometry(p, i);
-        t.kb0 = (int32_t)((int64_t)s * p.nkb / p.splits);
-        t.kb1 = (int32_t)((int64_t)(s + 1) * p.nkb / p.splits);
-        t.partial = p.splits > 1;
-        w.cur += w.step;
-    }
+    const int32_t s = (int32_t)(w.cur / p.nunits);
+    const int64_t i = w.cur - (int64_t)s * p.nunits;
+    t = unit_geometry(p, i);
+    t.kb0 = (int32_t)((int64_t)s * p.nkb / p.splits);
+    t.kb1 = (int32_t)((int64_t)(s + 1) * p.nkb / p.splits);
+    t.partial = p.splits > 1;
+    w.cur += w.step;
     return true;
 }
 
@@ -504,7 +296,7 @@ int make_tmap(CUtensorMap* map, const int8_t* S, int64_t m, int64_t K, int64_t l
     if (!enc) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)m};
     cuuint64_t strides[1] = {(cuuint64_t)ldS};
-    cuuint32_t box[2] = {(cuuint32_t)gemm::BK, box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)gemm2::BK, box_rows};  // 128-byte K boxes (SW128 atom width)
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(S), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -613,34 +405,22 @@ static int gemm_v2(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t j
     p.nunits = nunits;
     p.nkb = (int32_t)((K + gemm2::BK - 1) / gemm2::BK);
     const int pairs = std::max(1, num_sms() / 2);
-    p.iters_per_pair = 0;
-    // Stream-K (TB_GEMM_SCHED=streamk) balances small problems exactly, but its pairs sit at different
-    // K positions and lose the K-lockstep L2 reuse of S that the split-major static schedule gets
-    // (measured: config 2 GEMM 975 us stream-K vs 874 us static), so static is the default.
-    const char* sched = std::getenv("TB_GEMM_SCHED");
-    const bool streamk = splits <= 0 && sched && sched[0] == 's' && sched[1] == 't';
-    if (streamk) {
-        // stream-K: equal contiguous slices of the (unit, k-block) space; at most ~2 partial units per pair
-        const int64_t total = nunits * (int64_t)p.nkb;
-        p.iters_per_pair = std::max<int64_t>(8, (total + pairs - 1) / pairs);
-        splits = 1;
-    } else if (splits <= 0) {
-        splits = pick_splits(nunits, p.nkb, pairs);
-    }
+    // (a stream-K schedule was measured slower here -- its pairs sit at different K offsets and lose
+    // the K-lockstep L2 reuse of S: config 2 GEMM 975 vs 874 us -- so the split-major static one stays)
+    if (splits <= 0) splits = pick_splits(nunits, p.nkb, pairs);
     if (splits > p.nkb) splits = p.nkb;
     p.splits = splits;
     p.job_lo = job_lo;
     p.job_hi = job_hi;
     p.num = num;
-    p.atomic = streamk || splits > 1;
+    p.atomic = splits > 1;
     p.fp8 = format == TB_SIGN_E4M3 ? 1 : 0;
     if (p.atomic) TB_CUDA_TRY(cudaMemsetAsync(num, 0, (job_hi - job_lo) * sizeof(int32_t), st));
     CUtensorMap tm;
     if ((rc = make_tmap(&tm, S, m, K, ldS, gemm2::BM))) return rc;
     TB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)gemm2::SMEM_BYTES));
-    const int64_t work = streamk ? (nunits * (int64_t)p.nkb + p.iters_per_pair - 1) / p.iters_per_pair
-                                 : nunits * splits;
+    const int64_t work = nunits * splits;
     const unsigned grid = (unsigned)(2 * std::max<int64_t>(1, std::min<int64_t>(work, pairs)));
     gemm_tc2_kernel<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(tm, p);
     return check_launch("gemm_tc2_kernel");
@@ -662,45 +442,10 @@ extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS,
     if (rc) return rc;
     if (!S || !num) return fail(TB_ERR_INVALID, "gemm: null pointer");
     if (job_hi == job_lo) return TB_OK;
-    if (m > (int64_t)INT32_MAX - gemm::TILE) return fail(TB_ERR_CAPACITY, "gemm: m too large for TMA coordinates");
+    if (m > (int64_t)INT32_MAX - gemm2::TILE) return fail(TB_ERR_CAPACITY, "gemm: m too large for TMA coordinates");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (format == TB_SIGN_E2M1) return gemm_fp4(S, m, K, ldS, job_lo, job_hi, splits, num, st);
-    const char* variant = std::getenv("TB_GEMM_VARIANT");
-    if (!(variant && variant[0] == '1')) return gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, format, num, st);
-    if (format != TB_SIGN_I8) return fail(TB_ERR_CONFIG, "gemm v1: int8 only");
-    GemmArgs p{};
-    p.m = m;
-    p.w = (m + gemm::TILE - 1) / gemm::TILE;
-    int64_t y_lo, x_lo, y_hi, x_hi;
-    job_coord(job_lo, m, y_lo, x_lo);
-    job_coord(job_hi - 1, m, y_hi, x_hi);
-    const int64_t Y0 = y_lo / gemm::TILE, Y1 = y_hi / gemm::TILE;
-    p.tile_lo = row_prefix(Y0, p.w);
-    p.ntiles = row_prefix(Y1 + 1, p.w) - p.tile_lo;
-    p.nkb = (int32_t)((K + gemm::BK - 1) / gemm::BK);
-    const int64_t units = p.ntiles * 2;
-    const int sms = num_sms();
-    if (splits <= 0) {
-        int64_t want = (units >= sms) ? 1 : (sms + units - 1) / units;
-        int64_t cap = std::max<int64_t>(1, p.nkb / 4);
-        splits = (int32_t)std::min<int64_t>(want, cap);
-    }
-    if (splits > p.nkb) splits = p.nkb;
-    p.splits = splits;
-    p.job_lo = job_lo;
-    p.job_hi = job_hi;
-    p.num = num;
-    p.atomic = splits > 1;
-    if (p.atomic) TB_CUDA_TRY(cudaMemsetAsync(num, 0, (job_hi - job_lo) * sizeof(int32_t), st));
-    CUtensorMap ta, tbm;
-    if ((rc = make_tmap(&ta, S, m, K, ldS, gemm::BM))) return rc;
-    if ((rc = make_tmap(&tbm, S, m, K, ldS, gemm::BN))) return rc;
-    TB_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)gemm::SMEM_BYTES));
-    const int64_t nunits = units * splits;
-    const unsigned grid = (unsigned)std::min<int64_t>(nunits, sms);
-    gemm_tc_kernel<<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(ta, tbm, p);
-    return check_launch("gemm_tc_kernel");
+    return gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, format, num, st);
 }
 
 extern "C" int tb_gemm_pairs_simt(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
