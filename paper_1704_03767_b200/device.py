@@ -247,8 +247,9 @@ class TauEngine:
         return cuts
 
     def all_pairs_host(self, x_host: torch.Tensor, tau_b_out: torch.Tensor, kernel: str = "auto",
-                       band_fracs: tuple = (0.55, 0.30, 0.15), stream: torch.cuda.Stream | None = None,
-                       copy_stream: torch.cuda.Stream | None = None, h2d_chunks: int = 2) -> PairResult:
+                       band_fracs: tuple = (0.65, 0.25, 0.10), stream: torch.cuda.Stream | None = None,
+                       copy_stream: torch.cuda.Stream | None = None, h2d_chunks: int = 2,
+                       h2d_piece_bytes: int = 4 << 20) -> PairResult:
         """End-to-end from host buffers: H2D of the values, the device path, tau_b back to host.
 
         The job range is cut into row bands; band i's tau_b copy (on ``copy_stream``) overlaps
@@ -273,9 +274,15 @@ class TauEngine:
             cuts_h = [m * i // nchunk // 8 * 8 for i in range(nchunk)] + [m]
             cp_t.wait_stream(st_t)  # the previous call's kernels are done with x
             chunks = []
+            row_bytes = n * x_host.element_size()
+            piece_rows = max(1, h2d_piece_bytes // max(1, row_bytes))
             for r0, r1 in zip(cuts_h[:-1], cuts_h[1:]):
                 with torch.cuda.stream(cp_t):
-                    x[r0:r1].copy_(x_host[r0:r1], non_blocking=True)
+                    # copies of >= 8 MiB run at ~13 GB/s on the pool's hosts in a sustained pattern
+                    # (tools/probe_h2d*.py), <= 4 MiB at ~50 GB/s: upload in pieces
+                    for p0 in range(r0, r1, piece_rows):
+                        p1 = min(r1, p0 + piece_rows)
+                        x[p0:p1].copy_(x_host[p0:p1], non_blocking=True)
                     ev_c = torch.cuda.Event()
                     ev_c.record(cp_t)
                 chunks.append((r0, r1, ev_c))

@@ -17,17 +17,18 @@ def call(name, *a):
     return r
 dv._lib.call = call
 verbose = os.environ.get("TL_VERBOSE") == "1"
-for fr in [(0.55, 0.30, 0.15), (0.6, 0.3, 0.1), (0.5, 0.3, 0.2), (0.65, 0.25, 0.1), (0.45, 0.3, 0.15, 0.1)]:
-    for hc in (1, 2, 3):
+for fr in [(0.55, 0.30, 0.15), (0.65, 0.25, 0.1)]:
+  for pb in (1 << 20, 2 << 20, 4 << 20, 64 << 20):
+    for hc in (1, 2):
         tt = []
         for it in range(8):
             marks.clear()
             s = torch.cuda.Event(enable_timing=True); s.record()
-            eng.all_pairs_host(xh, out, band_fracs=fr, h2d_chunks=hc)
+            eng.all_pairs_host(xh, out, band_fracs=fr, h2d_chunks=hc, h2d_piece_bytes=pb)
             e = torch.cuda.Event(enable_timing=True); e.record(); torch.cuda.synchronize()
             tt.append(s.elapsed_time(e))
         tt.sort()
-        print(f"bands {fr} h2d_chunks {hc}: median {tt[4]:.3f} ms  min {tt[0]:.3f}", flush=True)
+        print(f"bands {fr} piece {pb >> 20} MiB h2d_chunks {hc}: median {tt[4]:.3f} ms  min {tt[0]:.3f}", flush=True)
         if verbose:
             for name, ev in marks:
                 print(f"   {name:22s} done at {s.elapsed_time(ev):.3f}")
