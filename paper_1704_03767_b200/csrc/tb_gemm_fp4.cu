@@ -314,7 +314,7 @@ struct Plan4 {
     int32_t partial = 0;
 };
 // Plans are cached per (geometry, job range): the banded host path cycles through a few ranges.
-static Plan4 g_plans4[8];
+static Plan4 g_plans4[16];
 static int g_plans4_next = 0;
 
 static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<int32_t>& code, std::vector<int32_t>& nb,
@@ -374,7 +374,7 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
             return TB_OK;
         }
     Plan4& g_plan4 = g_plans4[g_plans4_next];
-    g_plans4_next = (g_plans4_next + 1) % 8;
+    g_plans4_next = (g_plans4_next + 1) % 16;
     g_plan4.m = -1;
     std::vector<int32_t> code, nb, ncols;
     list_units4(m, job_lo, job_hi, code, nb, ncols);
@@ -397,6 +397,23 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
                     const double s_real = unit_cost4(ncols[u]) * nkb / T;
                     su[u] = (int32_t)std::max<int64_t>(1, std::min<int64_t>(nkb, std::llround(s_real)));
                 }
+                const double t = plan_items4(code, ncols, su, nkb, pairs, nullptr);
+                if (t < best * 0.999) { best = t; best_su = su; }
+            }
+            // fill idle pairs: split the most expensive item's unit once more while items < pairs
+            int64_t nitems = 0;
+            for (int32_t v : best_su) nitems += v;
+            su = best_su;
+            while (nitems < pairs) {
+                size_t arg = 0;
+                double worst = -1.0;
+                for (size_t u = 0; u < code.size(); ++u) {
+                    const double c = unit_cost4(ncols[u]) * nkb / su[u];
+                    if (su[u] < nkb && c > worst) { worst = c; arg = u; }
+                }
+                if (worst < 0) break;
+                ++su[arg];
+                ++nitems;
                 const double t = plan_items4(code, ncols, su, nkb, pairs, nullptr);
                 if (t < best * 0.999) { best = t; best_su = su; }
             }
@@ -483,6 +500,16 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
             if (n) fprintf(stderr, "item %d: ctas %d  tfull at mean %.1f us [%.1f, %.1f]  epilogue mean %.1f us\n", it, n, sa / n, mn, mx, se / n);
         }
         fprintf(stderr, "span first tfull -> last epilogue end %.1f us (items %lld)\n", (tend - t0) * 1e-3, (long long)p.nitems);
+        if (trace[1] == 'u') {  // TB_TRACE=1u: first item of every pair with its unit geometry
+            std::vector<int4> items(p.nitems);
+            cudaMemcpy(items.data(), p.items, items.size() * sizeof(int4), cudaMemcpyDeviceToHost);
+            for (unsigned b = 0; b < grid; b += 2) {
+                const int4 it = items[b / 2];
+                const long long yb = it.x >> 16, xb = it.x & 0xFFFF;
+                fprintf(stderr, "  pair %3u unit (%lld,%lld) kb [%d,%d) tfull %.1f us\n", b / 2, yb, xb, it.y, it.z,
+                        tr[b * 16] ? (tr[b * 16] - t0) * 1e-3 : -1.0);
+            }
+        }
     }
     return p.partial ? accum_convert(p.acc, job_hi - job_lo, num, st) : TB_OK;
 }
