@@ -156,6 +156,70 @@ __device__ __forceinline__ int sp_slow_chunk(int64_t c, const SpLayout& L, const
     return min(16, b - 16 * i);
 }
 
+// e2m1 chunks [c_lo, c_hi) of one row (c_lo even): each lane takes two adjacent chunks (a_l, a_l + 1
+// of one block pair share the window: one pair of window loads, one rank-pair load, one 16-byte
+// store; a warp writes 512 contiguous bytes) and steps 64 chunks = 4 block pairs.
+__device__ __forceinline__ void sp_e2m1_range(int c_lo, int c_hi, int lane, const SpLayout& L, const uint16_t* r16,
+                                              const uint32_t* wp, const uint32_t* wb, const uint4* masks,
+                                              int8_t* row, uint32_t neg1) {
+    const int c1 = (int)L.c1, nbf = (int)L.nbf;
+    int c = c_lo + 2 * lane;
+    const int c1_end = min(c_hi, c1);  // c1 is a multiple of 16: a pair never straddles it
+    if (c < c1_end) {
+        const int al = c & 15;  // even
+        const int bid = c >> 4;
+        const double f = (double)nbf - 0.5;
+        int A = (int)(f - sqrt(f * f - 2.0 * (double)bid));
+        if (A < 0) A = 0;
+        auto start = [nbf](int x) { return x * (nbf - 1) - x * (x - 1) / 2; };
+        while (A > 0 && start(A) > bid) --A;
+        while (A < nbf - 1 && start(A + 1) <= bid) ++A;
+        int B = bid - start(A) + A + 1;
+        uint32_t ow = wp[(16 * A + al) >> 1];  // ranks of a_l, a_l + 1
+        const uint32_t* wptr = wb + 8 * B;
+        uint4* outp = reinterpret_cast<uint4*>(row + 8 * (int64_t)c);
+        for (;;) {
+            const uint4 w0 = lds128(wptr), w1 = lds128(wptr + 4);
+            const uint32_t y[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            const uint32_t oa = __byte_perm(ow, 0, 0x1010), ob = __byte_perm(ow, 0, 0x3232);
+            const uint32_t owa[8] = {oa, oa, oa, oa, oa, oa, oa, oa};
+            const uint32_t owb[8] = {ob, ob, ob, ob, ob, ob, ob, ob};
+            const uint2 va = chunk_e2m1(y, owa, neg1), vb = chunk_e2m1(y, owb, neg1);
+            *outp = make_uint4(va.x, va.y, vb.x, vb.y);
+            c += 64;
+            if (c >= c1_end) break;
+            outp += 32;
+            B += 4;
+            wptr += 32;
+            if (B >= nbf) {  // row A + 1 starts at B = A + 2
+                do {
+                    ++A;
+                    B += A + 1 - nbf;
+                } while (B >= nbf && A < nbf - 1);
+                wptr = wb + 8 * B;
+                ow = wp[(16 * A + al) >> 1];
+            }
+        }
+    }
+    // sections 2 and 3 (~3% of the chunks): per-sample lists, partial chunks masked
+    for (; c < c_hi; c += 64) {
+#pragma unroll 1
+        for (int k = 0; k < 2 && c + k < c_hi; ++k) {
+            uint32_t own[8], y[8];
+            const int valid = sp_slow_chunk(c + k, L, r16, wp, own, y);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) y[q] |= 0x80008000u;
+            uint2 v2 = chunk_e2m1(y, own, neg1);
+            if (valid < 16) {
+                const uint4 mk = masks[valid];
+                v2.x &= mk.x;
+                v2.y &= mk.y;
+            }
+            *reinterpret_cast<uint2*>(row + 8 * (int64_t)(c + k)) = v2;
+        }
+    }
+}
+
 // One CTA per (row, K-range); warps take contiguous chunk ranges and consecutive lanes consecutive
 // chunks (coalesced stores).  Section 1 needs no per-lane decode after the start: a 32-chunk step is
 // exactly two block pairs, and a_l = c mod 16 stays fixed.  The window of block B is 8 aligned words
@@ -198,10 +262,14 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
     const int nchunks = (int)(L.c1 + L.c2 + L.c3);  // < 2^31 (n <= 32767)
     const int c1 = (int)L.c1;
     int8_t* row = S + r * ldS;
-    const int per = (nchunks + (int)gridDim.y - 1) / (int)gridDim.y;
-    const int b_lo = (int)blockIdx.y * per, b_hi = min(b_lo + per, nchunks);
-    const int wper = (b_hi - b_lo + (SP_THREADS / 32) - 1) / (SP_THREADS / 32);
-    const int c_lo = b_lo + warp * wper, c_hi = min(c_lo + wper, b_hi);
+    // CTA / warp ranges start on even chunks: the e2m1 loop gives each lane two adjacent chunks
+    const int per = ((nchunks + (int)gridDim.y - 1) / (int)gridDim.y + 1) & ~1;
+    const int b_lo = min((int)blockIdx.y * per, nchunks), b_hi = min(b_lo + per, nchunks);
+    const int wper = ((b_hi - b_lo + (SP_THREADS / 32) - 1) / (SP_THREADS / 32) + 1) & ~1;
+    const int c_lo = min(b_lo + warp * wper, b_hi), c_hi = min(c_lo + wper, b_hi);
+    if (FMT == 2) {
+        sp_e2m1_range(c_lo, c_hi, lane, L, r16, wp, win, masks, row, neg1);
+    } else {
     int c = c_lo + lane;
     const int nbf = (int)L.nbf;
     // ---- section 1: block pairs (A < B); per step B += 2, own changes only with A
@@ -262,6 +330,7 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
             }
             *reinterpret_cast<uint4*>(row + 16 * (int64_t)c) = v;
         }
+    }
     }
     // zero the row tail [K bytes, ldS)
     const int64_t kb = (FMT == 2 ? 8 : 16) * (int64_t)nchunks;

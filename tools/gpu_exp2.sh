@@ -1,2 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python tools/exp_bands.py 3 > gpurun_out/exp_bands.log 2>&1; echo ex=$?
+timeout 1800 python -m pytest tests -m gpu -q --timeout 900 -x > gpurun_out/pytest.log 2>&1; echo pytest=$?
+timeout 600 python bench.py --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/bench_c2.log 2>&1; echo bench=$?
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/plain_bench.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum,sm__inst_executed.sum --clock-control none -k regex:signpack -c 2 --csv --log-file gpurun_out/sp_launch.csv \
+    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_l.log 2>&1; echo launches=$?
