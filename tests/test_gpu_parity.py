@@ -394,3 +394,17 @@ def test_finalize_ranges_vs_numpy():
                 ref_b = np.where(denom > 0, num / denom, np.nan)
             np.testing.assert_array_equal(ta.cpu().numpy(), num / float(n0))
             np.testing.assert_array_equal(tb.cpu().numpy(), ref_b)
+
+
+@pytest.mark.gpu
+def test_gemm_int8_beyond_fp4_range(eng, oracle):
+    """n = 6000: K >= 2^24 switches the GEMM from e2m1 (f32 sums) to int8 (kind::i8); every pair
+    against the oracle, with ties, including the e2m1/int8 boundary n = 5793 / 5794."""
+    from paper_1704_03767_b200 import _lib
+    for n, m in ((5793, 24), (5794, 24), (6000, 40)):
+        K = int(_lib.load().tb_sign_k(n))
+        rng = np.random.default_rng(n)
+        ranks = np.stack([oracle.rank_transform(rng.integers(0, n // 4, n)) for _ in range(m)])
+        res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="gemm").validate()
+        assert res.extra["sign_format"] == (_lib.TB_SIGN_E2M1 if K < (1 << 24) else _lib.TB_SIGN_I8)
+        _check_full(res, oracle, ranks, full=False)

@@ -1,6 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 1800 python -m pytest tests -m gpu -q --timeout 900 -x > gpurun_out/pytest.log 2>&1; echo pytest=$?
-timeout 600 python bench.py --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/bench_c2.log 2>&1; echo bench=$?
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/plain_bench.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum,sm__inst_executed.sum --clock-control none -k regex:signpack -c 2 --csv --log-file gpurun_out/sp_launch.csv \
-    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_l.log 2>&1; echo launches=$?
+timeout 1800 python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout 900 -x -k "int8_beyond" > gpurun_out/pytest_int8.log 2>&1; echo pytest=$?
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; echo smoke=$?
