@@ -107,7 +107,17 @@ class TauEngine:
     def _buf(self, name: str, numel: int, dtype: torch.dtype) -> torch.Tensor:
         t = self._ws.get(name)
         if t is None or t.numel() < numel or t.dtype != dtype:
-            t = torch.empty(max(numel, 1), dtype=dtype, device=self.device)
+            if t is not None:
+                del self._ws[name]
+                t = None
+            try:
+                t = torch.empty(max(numel, 1), dtype=dtype, device=self.device)
+            except torch.OutOfMemoryError as exc:  # e.g. S = m x K/2 bytes beyond this GPU's HBM
+                nbytes = numel * torch.empty(0, dtype=dtype).element_size()
+                raise CapacityExceededError(
+                    f"device workspace {name!r} needs {nbytes / 2**30:.1f} GiB, more than is free on "
+                    f"{self.device}; split the variables into blocks (fewer rows per call) or use the merge "
+                    f"path (kernel='merge', O(m n) memory)") from exc
             self._ws[name] = t
         return t[:numel]
 

@@ -408,3 +408,14 @@ def test_gemm_int8_beyond_fp4_range(eng, oracle):
         res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="gemm").validate()
         assert res.extra["sign_format"] == (_lib.TB_SIGN_E2M1 if K < (1 << 24) else _lib.TB_SIGN_I8)
         _check_full(res, oracle, ranks, full=False)
+
+
+@pytest.mark.gpu
+def test_gemm_workspace_beyond_hbm_is_capacity_error(eng):
+    """S = m x K bytes beyond the GPU (m = 6000, n = 8192, int8: ~201 GB) -> CapacityExceededError."""
+    import paper_1704_03767_b200 as tb
+    x = torch.zeros((6000, 8192), dtype=torch.float32, device="cuda")
+    with pytest.raises(tb.CapacityExceededError):
+        eng.all_pairs(x, kernel="gemm")
+    eng.release()
+    torch.cuda.empty_cache()
