@@ -95,3 +95,20 @@ def test_sink_failure_propagates():
 
     with pytest.raises(OSError, match="disk full"):
         tb.compute_all_pairs(ds, "sorted", tile_size=2, pass_tiles=2, sink=broken)
+
+
+@pytest.mark.parametrize("kernel", ["sorted", "gemm"])
+def test_devices_split_matches_reference_stream(kernel):
+    """compute_all_pairs(devices=[...]) splits the job range across GPUs (here the same GPU listed
+    twice / three times) and still produces the reference byte stream, also per shard."""
+    import paper_1704_03767_b200 as tb
+    gold = load_json("engine_streams.json")
+    ds = tb.synth_dataset(512, 48, tie_fraction=0.3, seed=512)
+    for devs in ([0, 0], [0, 0, 0]):
+        blob = _stream(ds, kernel, 4, devices=devs, pass_tiles=97)
+        assert hashlib.sha256(blob).hexdigest() == gold["m512_n48_t0.3_s512_q4"], (kernel, devs)
+    full = _stream(ds, kernel, 4)
+    parts = b"".join(_stream(ds, kernel, 4, shard=(i, 3), devices=[0, 0]) for i in range(3))
+    assert parts == full
+    with pytest.raises(tb.ConfigError):
+        tb.compute_all_pairs(ds, kernel, device=0, devices=[0])

@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python tools/exp_splits_c2.py 2 > gpurun_out/exp_splits.log 2>&1; echo ex=$?
+timeout 1800 python -m pytest tests -m gpu -q --timeout 900 -x > gpurun_out/pytest.log 2>&1; echo pytest=$?
