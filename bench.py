@@ -263,6 +263,22 @@ def measure_fp4_peak(torch, dev):
         return None
 
 
+def measure_mxf4_ceiling():
+    """FLOP/s of the GEMM's own MMA stream (tcgen05 kind::mxf4, 2-SM, M=256, two N=240 accumulators
+    alternating) issued back to back with no operand traffic (csrc/tb_probe.cu): the practical tensor
+    ceiling for the numerator GEMM on this GPU."""
+    try:
+        import ctypes
+        lib = ctypes.CDLL(os.path.join(ROOT, "paper_1704_03767_b200", "libtbprobe.so"))
+        lib.tb_probe_mxf4_flops.restype = ctypes.c_double
+        lib.tb_probe_mxf4_flops.argtypes = [ctypes.c_int]
+        v = float(lib.tb_probe_mxf4_flops(3))
+        return v if v > 0 else None
+    except OSError as exc:
+        print(f"# mxf4 probe unavailable: {exc}", file=sys.stderr)
+        return None
+
+
 def measure_int32_peak():
     """INT32 lane-ops/s of dependency-free IADD3/LOP3 chains on all SMs (csrc/tb_probe.cu)."""
     try:
@@ -427,6 +443,7 @@ def run_ours(args):
         if path == "gemm":
             fp4 = sign_format == _lib.TB_SIGN_E2M1
             fp4_lib = measure_fp4_peak(torch, dev) if fp4 else None
+            mma_ceiling = measure_mxf4_ceiling() if fp4 else None
             if fp4:
                 pk, src = 9.0e15, "nominal dense FP4 (kind::mxf4) 9 PFLOP/s, B200_PROFILING.md table (no measured FP4 entry)"
             else:
@@ -441,6 +458,8 @@ def run_ours(args):
                     "frac_of_measured_int8_peak": (achieved / peak) if peak else None,
                     "measured_fp4_library_tflops": fp4_lib / 1e12 if fp4_lib else None,
                     "frac_of_measured_fp4_library": (achieved / fp4_lib) if fp4_lib else None,
+                    "measured_mma_ceiling_tflops": mma_ceiling / 1e12 if mma_ceiling else None,
+                    "frac_of_measured_mma_ceiling": (achieved / mma_ceiling) if mma_ceiling else None,
                     "measured_int8_peak_tops": peak / 1e12 if peak else None,
                     "algorithmic": f"2*K ops per i<j pair, K=n(n-1)/2={K} sample pairs; {my_pairs} pairs per launch",
                     "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}

@@ -167,10 +167,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {  // ---------------- MMA issuer (leader CTA, one thread)
+        if (leader) {  // ---------------- MMA issuer (leader CTA, warp 1; one elected lane issues)
+            // The issue loop is kept branch- and arithmetic-light: one thread feeds the 2-SM tensor pipe,
+            // and per-MMA overhead (descriptor builds, runtime-bounded loops) left it idle ~30% of the
+            // time (csrc/tb_probe.cu: the same MMA stream issued fully unrolled reaches ~99% of peak).
+            // Descriptors are base + constant offsets; each k-block issues a fully unrolled sequence.
             constexpr uint32_t idesc = idesc_mxf4(UM, BN);
             const uint32_t idesc_e = idesc_mxf4(UM, (uint32_t)(p.n_edge ? p.n_edge : BN));
             const uint32_t sf = tmem_base + SF_COL;
+            const uint64_t desc0 = umma_desc_k_sw128(smem_u32(smem));  // stage 0, A operand
+            constexpr uint64_t STAGE_D = STAGE_BYTES >> 4, B0_D = A_BYTES >> 4, B1_D = (A_BYTES + B_BYTES) >> 4;
+            const uint32_t d0 = tmem_base, d1 = tmem_base + BN;
             int stage = 0;
             uint32_t phase = 0;
             uint32_t acc_phase = 0;
@@ -179,24 +186,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             while (next_unit4(p, cur, npairs, t)) {
                 mbar_wait(tempty, acc_phase ^ 1);
                 tc_fence_after();
+                const uint32_t id0 = (t.x0 + BN > p.m) ? idesc_e : idesc;
+                const uint32_t id1 = (t.x0 + 2 * BN > p.m) ? idesc_e : idesc;
+                const int mode = t.h_lo == 0 ? (t.h_hi == NB ? 2 : 0) : 1;  // 2: both blocks, 0 / 1: that block
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-                    const uint64_t adesc = umma_desc_k_sw128(sa);
+                    const uint64_t ad = desc0 + (uint64_t)stage * STAGE_D;
+                    const uint32_t a0 = kb > t.kb0 ? 1u : 0u;
+                    if (mode == 2) {
 #pragma unroll
-                    for (int k = 0; k < BK / UKB; ++k) {
-                        const uint32_t acc = (kb > t.kb0 || k > 0) ? 1u : 0u;
-                        for (int h = t.h_lo; h < t.h_hi; ++h) {
-                            const uint64_t bdesc = umma_desc_k_sw128(sa + A_BYTES + h * B_BYTES);
-                            mma_mxf4_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k,
-                                         (t.x0 + h * BN + BN > p.m) ? idesc_e : idesc, sf, sf, acc);
+                        for (int k = 0; k < BK / UKB; ++k) {
+                            const uint32_t acc = k ? 1u : a0;
+                            mma_mxf4_2sm_warp(d0, ad + 2 * k, ad + B0_D + 2 * k, id0, sf, sf, acc);
+                            mma_mxf4_2sm_warp(d1, ad + 2 * k, ad + B1_D + 2 * k, id1, sf, sf, acc);
                         }
+                    } else if (mode == 1) {
+#pragma unroll
+                        for (int k = 0; k < BK / UKB; ++k)
+                            mma_mxf4_2sm_warp(d1, ad + 2 * k, ad + B1_D + 2 * k, id1, sf, sf, k ? 1u : a0);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < BK / UKB; ++k)
+                            mma_mxf4_2sm_warp(d0, ad + 2 * k, ad + B0_D + 2 * k, id0, sf, sf, k ? 1u : a0);
                     }
-                    mma_commit_2sm(&empty[stage], 0x3);
+                    mma_commit_2sm_warp(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit_2sm(tfull, 0x3);
+                mma_commit_2sm_warp(tfull, 0x3);
                 acc_phase ^= 1;
             }
         }

@@ -5,6 +5,9 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "tb_common.cuh"
+#include "tb_ptx.cuh"
+
 namespace {
 
 __device__ __forceinline__ uint32_t iadd3(uint32_t a, uint32_t b, uint32_t c) {
@@ -39,7 +42,81 @@ __global__ void __launch_bounds__(256) int32_probe_kernel(uint32_t* out, int ite
     if (s == 0x12345678u) out[0] = s;  // keeps the chains alive
 }
 
+// tcgen05.mma.cta_group::2.kind::mxf4.block_scale, M=256, the GEMM's two N=240 accumulators issued
+// alternately, back to back from shared memory by one thread per CTA pair (no TMA, no epilogue):
+// the MMA pipe's sustained rate for the numerator GEMM's instruction stream.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mxf4_probe_kernel(int iters) {
+    using namespace tb;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 64 * 1024);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+    const int warp = threadIdx.x >> 5;
+    const bool leader = cluster_ctarank() == 0;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc_2sm<512>(slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    tmem_st_32x32b_x32(tmem + (uint32_t(warp * 32) << 16) + 480, 0x7F7F7F7Fu);
+    tmem_st_wait();
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (leader && threadIdx.x == 0) {
+        constexpr uint32_t idesc = idesc_mxf4(256, 240);
+        const uint32_t sf = tmem + 480;
+        const uint64_t adesc = umma_desc_k_sw128(smem_u32(smem));
+        const uint64_t bdesc = umma_desc_k_sw128(smem_u32(smem + 16384));
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                for (int h = 0; h < 2; ++h) mma_mxf4_2sm(tmem + h * 240, adesc + 2 * k, bdesc + 2 * k, idesc, sf, sf, 1u);
+        mma_commit_2sm(bar, 0x3);
+        mbar_wait(bar, 0);
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_2sm<512>(tmem);
+    }
+}
+
 }  // namespace
+
+// Returns the FLOP/s (2 per MAC) of the MMA stream above on every SM pair, best of `reps`; 0 on error.
+extern "C" double tb_probe_mxf4_flops(int reps) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int pairs = sms / 2, iters = 4096;
+    const size_t smem = 64 * 1024 + 2048;
+    if (cudaFuncSetAttribute(mxf4_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 0.0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < reps + 1; ++r) {
+        cudaEventRecord(e0);
+        mxf4_probe_kernel<<<2 * pairs, 128, smem>>>(r == 0 ? 64 : iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (cudaGetLastError() != cudaSuccess) return 0.0;
+    const double flops = 2.0 * 256 * 240 * 64 * 8.0 * iters * pairs;
+    return flops / (best * 1e-3);
+}
 
 // Returns INT32 lane-ops per second (IADD3 + LOP3 mix; ptxas fuses each add pair into one IADD3),
 // best of `reps` launches on the current device; 0 on error.

@@ -214,6 +214,28 @@ __device__ __forceinline__ void mma_mxf4_2sm(uint32_t d_tmem, uint64_t a_desc, u
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
         : "memory");
 }
+// Warp-wide forms: the whole (converged) warp runs the issue loop, so descriptor arithmetic stays
+// warp-uniform (uniform registers, no per-MMA broadcast loop), and one elect.sync-chosen lane -- the
+// same lane every time -- issues the MMA / commit.
+__device__ __forceinline__ void mma_mxf4_2sm_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_2sm_warp(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
 // Block-scaled instruction descriptor: E2M1 x E2M1, UE8M0 scales, K-major, dense K = 64, sf ids 0.
 __host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t M, uint32_t N) {
     return (1u << 7)            // A E2M1
