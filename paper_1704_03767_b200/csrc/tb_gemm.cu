@@ -152,8 +152,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {  // ---------------- MMA issuer (leader CTA, one thread)
+        if (leader) {  // ---------------- MMA issuer (leader CTA, warp 1; one elected lane issues)
+            // warp-uniform loop, base + offset descriptors, unrolled MMAs (see tb_gemm_fp4.cu)
             const uint32_t idesc = p.fp8 ? idesc_f8(UM, BN) : idesc_i8(UM, BN);
+            const uint64_t desc0 = umma_desc_k_sw128(smem_u32(smem));  // stage 0, A operand
+            constexpr uint64_t STAGE_D = STAGE_BYTES >> 4, B0_D = A_BYTES >> 4, B1_D = (A_BYTES + B_BYTES) >> 4;
             int stage = 0;
             uint32_t phase = 0;
             uint32_t acc_phase = 0;
@@ -165,23 +168,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-                    const uint64_t adesc = umma_desc_k_sw128(sa);
+                    const uint64_t ad = desc0 + (uint64_t)stage * STAGE_D;
+                    const uint32_t a0 = kb > t.kb0 ? 1u : 0u;
+                    if (p.fp8) {
 #pragma unroll
-                    for (int k = 0; k < BK / UK; ++k) {
-                        const uint32_t acc = (kb > t.kb0 || k > 0) ? 1u : 0u;
-                        for (int h = t.h_lo; h < 2; ++h) {
-                            const uint64_t bdesc = umma_desc_k_sw128(sa + A_BYTES + h * B_BYTES);
-                            if (p.fp8)
-                                mma_f8_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
-                            else
-                                mma_i8_2sm(tmem_base + h * BN, adesc + 2 * k, bdesc + 2 * k, idesc, acc);
+                        for (int k = 0; k < BK / UK; ++k) {
+                            if (t.h_lo == 0) mma_f8_2sm_warp(tmem_base, ad + 2 * k, ad + B0_D + 2 * k, idesc, k ? 1u : a0);
+                            mma_f8_2sm_warp(tmem_base + BN, ad + 2 * k, ad + B1_D + 2 * k, idesc, k ? 1u : a0);
                         }
+                    } else if (t.h_lo == 0) {
+#pragma unroll
+                        for (int k = 0; k < BK / UK; ++k) {
+                            mma_i8_2sm_warp(tmem_base, ad + 2 * k, ad + B0_D + 2 * k, idesc, k ? 1u : a0);
+                            mma_i8_2sm_warp(tmem_base + BN, ad + 2 * k, ad + B1_D + 2 * k, idesc, k ? 1u : a0);
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < BK / UK; ++k)
+                            mma_i8_2sm_warp(tmem_base + BN, ad + 2 * k, ad + B1_D + 2 * k, idesc, k ? 1u : a0);
                     }
-                    mma_commit_2sm(&empty[stage], 0x3);
+                    mma_commit_2sm_warp(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit_2sm(tfull, 0x3);
+                mma_commit_2sm_warp(tfull, 0x3);
                 acc_phase ^= 1;
             }
         }
