@@ -13,6 +13,7 @@
 // (256-row block, 480-column block) pairs listed by the host in 2048 x 1920 super-blocks; split-K
 // and the warp roles follow the int8 kernel (tb_gemm.cu).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 #include <cudaTypedefs.h>
@@ -45,19 +46,20 @@ constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + STG_BYTES;
 
 struct Gemm4Args {
     int64_t m;
-    const int4* items;     // {(row block << 16) | column block, kb0, kb1, 0}; pair p runs p, p + P, ...
+    const int4* items;     // {256-row block, kb0, kb1, (240-col block b0 << 16) | b1 (0xFFFF: none)}
     int64_t nitems;
     int32_t partial;       // some unit is split over K: every item accumulates into acc
     int64_t job_lo, job_hi;
     int32_t* num;
     float* acc;      // split-K: f32 sums (exact integers < 2^24), red.global.add.v4.f32
-    int32_t n_edge;  // N of the partial last 240-column block (m % 240 rounded up to 16), 0 if none
     unsigned long long* trace;  // TB_TRACE=1 (diagnostics): per CTA, per item: [accumulator ready, epilogue done]
 };
 
 struct Unit4 {
-    int64_t y0, x0;
-    int32_t h_lo, h_hi;  // N blocks [h_lo, h_hi) hold upper-triangle columns inside the matrix
+    int64_t y0;
+    int64_t xs[2];       // first column of each 240-column block (two consecutive blocks of one row block)
+    int32_t nblk;        // 1 or 2 blocks
+    int32_t nb[2];       // MMA N per block: 240, or the partial last block rounded up to 16
     int32_t kb0, kb1;
     bool partial;
 };
@@ -65,10 +67,16 @@ struct Unit4 {
 __device__ __forceinline__ bool next_unit4(const Gemm4Args& p, int64_t& cur, int64_t step, Unit4& t) {
     if (cur >= p.nitems) return false;
     const int4 it = __ldg(&p.items[cur]);
-    t.y0 = (int64_t)(it.x >> 16) * g4::UM;
-    t.x0 = (int64_t)(it.x & 0xFFFF) * g4::UN;
-    t.h_lo = (t.x0 + g4::BN - 1 < t.y0) ? 1 : 0;
-    t.h_hi = (t.x0 + g4::BN >= p.m) ? 1 : g4::NB;
+    t.y0 = (int64_t)it.x * g4::UM;
+    const int32_t b0 = (int32_t)((uint32_t)it.w >> 16), b1 = it.w & 0xFFFF;
+    t.nblk = b1 == 0xFFFF ? 1 : 2;
+    t.xs[0] = (int64_t)b0 * g4::BN;
+    t.xs[1] = (int64_t)(b1 == 0xFFFF ? b0 : b1) * g4::BN;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int64_t live = p.m - t.xs[h];
+        t.nb[h] = live >= g4::BN ? g4::BN : (int32_t)((live + 15) & ~int64_t(15));
+    }
     t.kb0 = it.y;
     t.kb1 = it.z;
     t.partial = p.partial != 0;
@@ -94,7 +102,7 @@ __device__ __forceinline__ void epi_red_row(float* quad0, const uint32_t (&v)[16
 }
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     gemm_fp4_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    const __grid_constant__ CUtensorMap tmap_be, Gemm4Args p) {
+                    Gemm4Args p) {
     using namespace g4;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -114,7 +122,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_a);
         tma_prefetch(&tmap_b);
-        if (p.n_edge) tma_prefetch(&tmap_be);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -142,26 +149,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             uint32_t phase = 0;
             int64_t cur = pair;
             Unit4 t;
-            const uint32_t be_rows = (uint32_t)p.n_edge / 2;
             while (next_unit4(p, cur, npairs, t)) {
-                // the block holding column m - 1 may be partial: it loads n_edge / 2 rows per CTA
-                uint32_t bytes = 2 * A_BYTES;
-                for (int h = t.h_lo; h < t.h_hi; ++h)
-                    bytes += 2 * ((t.x0 + h * BN + BN > p.m) ? be_rows * BK : B_BYTES);
+                // each block loads a full 120-row box per CTA; the 2-SM MMA with N reads N / 2 rows of
+                // each CTA, so CTA 1's box starts at N / 2 (partial blocks need no other tensor map)
+                const uint32_t bytes = 2 * (A_BYTES + t.nblk * B_BYTES);
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
                     uint8_t* sa = smem + stage * STAGE_BYTES;
                     tma_load_2d_2sm(sa, &tmap_a, fb, kb * BK, (int32_t)(t.y0 + rank * BM));
-                    for (int h = t.h_lo; h < t.h_hi; ++h) {
-                        if (t.x0 + h * BN + BN > p.m)
-                            tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_be, fb, kb * BK,
-                                            (int32_t)(t.x0 + h * BN + rank * be_rows));
-                        else
-                            tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
-                                            (int32_t)(t.x0 + h * BN + rank * BNH));
-                    }
+                    for (int h = 0; h < t.nblk; ++h)
+                        tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
+                                        (int32_t)(t.xs[h] + rank * (t.nb[h] / 2)));
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -173,7 +173,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             // time (csrc/tb_probe.cu: the same MMA stream issued fully unrolled reaches ~99% of peak).
             // Descriptors are base + constant offsets; each k-block issues a fully unrolled sequence.
             constexpr uint32_t idesc = idesc_mxf4(UM, BN);
-            const uint32_t idesc_e = idesc_mxf4(UM, (uint32_t)(p.n_edge ? p.n_edge : BN));
             const uint32_t sf = tmem_base + SF_COL;
             const uint64_t desc0 = umma_desc_k_sw128(smem_u32(smem));  // stage 0, A operand
             constexpr uint64_t STAGE_D = STAGE_BYTES >> 4, B0_D = A_BYTES >> 4, B1_D = (A_BYTES + B_BYTES) >> 4;
@@ -186,9 +185,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             while (next_unit4(p, cur, npairs, t)) {
                 mbar_wait(tempty, acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t id0 = (t.x0 + BN > p.m) ? idesc_e : idesc;
-                const uint32_t id1 = (t.x0 + 2 * BN > p.m) ? idesc_e : idesc;
-                const int mode = t.h_lo == 0 ? (t.h_hi == NB ? 2 : 0) : 1;  // 2: both blocks, 0 / 1: that block
+                const uint32_t id0 = t.nb[0] == BN ? idesc : idesc_mxf4(UM, (uint32_t)t.nb[0]);
+                const uint32_t id1 = t.nb[1] == BN ? idesc : idesc_mxf4(UM, (uint32_t)t.nb[1]);
+                const int mode = t.nblk;  // 2: both blocks, 1: block 0 only
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -201,10 +200,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                             mma_mxf4_2sm_warp(d0, ad + 2 * k, ad + B0_D + 2 * k, id0, sf, sf, acc);
                             mma_mxf4_2sm_warp(d1, ad + 2 * k, ad + B1_D + 2 * k, id1, sf, sf, acc);
                         }
-                    } else if (mode == 1) {
-#pragma unroll
-                        for (int k = 0; k < BK / UKB; ++k)
-                            mma_mxf4_2sm_warp(d1, ad + 2 * k, ad + B1_D + 2 * k, id1, sf, sf, k ? 1u : a0);
                     } else {
 #pragma unroll
                         for (int k = 0; k < BK / UKB; ++k)
@@ -245,13 +240,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             tc_fence_after();
             int item = (int)((cur - pair) / npairs) - 1;
             if (p.trace && q == 0 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2] = globaltimer();
-            for (int h = t.h_lo; h < t.h_hi; ++h) {
+            for (int h = 0; h < t.nblk; ++h) {
 #pragma unroll 1
                 for (int c = 0; c < BN; c += 16) {
                     uint32_t r[16];
                     tmem_ld_32x32b_x16(tmem_base + (uint32_t(q * 32) << 16) + h * BN + c, r);
                     tmem_ld_wait();
-                    const int64_t xc = t.x0 + h * BN + c;
+                    const int64_t xc = t.xs[h] + c;
                     if (xc >= m || xc + 15 < y0) continue;  // chunk right of the matrix or below the diagonal
                     if (t.partial) {
                         // split partials: lane per row straight from registers, aligned red.v4.f32 quads
@@ -336,39 +331,50 @@ static int g_plans4_next = 0;
 
 static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<int32_t>& code, std::vector<int32_t>& nb,
                         std::vector<int32_t>& ncols) {
-    const int64_t RB = (m + g4::UM - 1) / g4::UM, CB = (m + g4::UN - 1) / g4::UN;
-    const int64_t GR = 8, GC = 4;
+    // A unit = one 256-row block x two consecutive 240-column blocks.  Row block yb's blocks run from
+    // the first one touching its diagonal, b = floor(256 yb / 240), to the last column of the matrix,
+    // and are paired left to right (an odd count leaves one single-block unit), so diagonal and
+    // right-edge remnants share units instead of each becoming a half-empty one.  Units are listed
+    // per 8-row-block group (2048 rows) in windows of 8 column blocks, so concurrently running pairs
+    // share S rows through L2.
+    const int64_t RB = (m + g4::UM - 1) / g4::UM, GR = 8;
+    const int64_t b_last = (m - 1) / g4::BN;
     int64_t y_lo, x_lo, y_hi, x_hi;
     job_coord(job_lo, m, y_lo, x_lo);
     job_coord(job_hi - 1, m, y_hi, x_hi);
-    for (int64_t SY = 0; SY < (RB + GR - 1) / GR; ++SY)
-        for (int64_t SX = 0; SX < (CB + GC - 1) / GC; ++SX)
-            for (int64_t yb = SY * GR; yb < std::min(RB, (SY + 1) * GR); ++yb)
-                for (int64_t xb = SX * GC; xb < std::min(CB, (SX + 1) * GC); ++xb) {
-                    const int64_t r0 = yb * g4::UM, r1 = std::min(r0 + g4::UM, m) - 1;
-                    const int64_t x0 = xb * g4::UN;
-                    if (x0 + g4::UN - 1 < r0) continue;  // entirely below the diagonal
-                    if (r1 < y_lo || r0 > y_hi) continue;  // outside the job range rows
-                    const int h_lo = (x0 + g4::BN - 1 < r0) ? 1 : 0;
-                    const int h_hi = (x0 + g4::BN >= m) ? 1 : g4::NB;
-                    code.push_back((int32_t)((yb << 16) | xb));
-                    nb.push_back(h_hi - h_lo);
-                    int32_t cols = 0;  // MMA columns issued (the partial block runs N = round16(live))
-                    for (int h = h_lo; h < h_hi; ++h)
-                        cols += (x0 + h * g4::BN + g4::BN > m) ? (int32_t)(((m - x0 - h * g4::BN) + 15) / 16 * 16) : g4::BN;
-                    ncols.push_back(cols);
-                }
+    auto nmma = [m](int64_t b) -> int32_t {
+        const int64_t live = m - b * g4::BN;
+        return live >= g4::BN ? g4::BN : (int32_t)((live + 15) / 16 * 16);
+    };
+    struct U { int64_t win, yb, b0, b1; };
+    for (int64_t SY = 0; SY < (RB + GR - 1) / GR; ++SY) {
+        std::vector<U> g;
+        for (int64_t yb = SY * GR; yb < std::min(RB, (SY + 1) * GR); ++yb) {
+            const int64_t r0 = yb * g4::UM, r1 = std::min(r0 + g4::UM, m) - 1;
+            if (r1 < y_lo || r0 > y_hi) continue;  // outside the job range rows
+            for (int64_t b = r0 / g4::BN; b <= b_last; b += 2)
+                g.push_back(U{b / 8, yb, b, b + 1 <= b_last ? b + 1 : -1});
+        }
+        std::stable_sort(g.begin(), g.end(), [](const U& a, const U& b) { return a.win < b.win; });
+        for (const U& u : g) {
+            code.push_back((int32_t)u.yb);
+            nb.push_back((int32_t)((u.b0 << 16) | (u.b1 < 0 ? 0xFFFF : u.b1)));
+            ncols.push_back(nmma(u.b0) + (u.b1 < 0 ? 0 : nmma(u.b1)));
+        }
+    }
 }
 
 // Relative k-block cost of a unit: the A-operand share plus the MMA / B share of its issued columns
-// (one full block = 0.67, two = 1.0, the partial edge block in proportion).
-static double unit_cost4(int32_t ncols) { return 0.34 + 0.66 * ncols / 480.0; }
+// (one full block = 0.6, two = 1.0, the partial edge block in proportion; TB_TRACE item timings).
+static double unit_cost4(int32_t ncols) { return 0.2 + 0.8 * ncols / 480.0; }  // 1 block ~0.6 (measured)
 
 // Items for per-unit split counts su[u]; returns the simulated makespan of the static schedule
 // (items split-round-major, pair p runs p, p + P, ...), in two-block k-block units.
-static double plan_items4(const std::vector<int32_t>& code, const std::vector<int32_t>& ncols,
-                          const std::vector<int32_t>& su, int32_t nkb, int pairs, std::vector<int4>* out) {
-    const double t_epi = 36.0;  // one epilogue ~ 36 two-block k-blocks (~20 us)
+static double plan_items4(const std::vector<int32_t>& code, const std::vector<int32_t>& blocks,
+                          const std::vector<int32_t>& ncols, const std::vector<int32_t>& su, int32_t nkb, int pairs,
+                          std::vector<int4>* out) {
+    const double t_epi = 100.0;  // per item: epilogue ~20 us + split-red contention + refill (fitted to
+                                 // measured 1- vs 2-wave plans on config 2), in two-block k-blocks
     std::vector<double> load(pairs, 0.0);
     const int32_t rounds = *std::max_element(su.begin(), su.end());
     int64_t idx = 0;
@@ -377,7 +383,7 @@ static double plan_items4(const std::vector<int32_t>& code, const std::vector<in
             if (r >= su[u]) continue;
             const int32_t kb0 = (int32_t)((int64_t)r * nkb / su[u]), kb1 = (int32_t)((int64_t)(r + 1) * nkb / su[u]);
             load[idx % pairs] += (kb1 - kb0) * unit_cost4(ncols[u]) + t_epi;
-            if (out) out->push_back(make_int4(code[u], kb0, kb1, 0));
+            if (out) out->push_back(make_int4(code[u], kb0, kb1, blocks[u]));
             ++idx;
         }
     return *std::max_element(load.begin(), load.end());
@@ -402,19 +408,25 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
             std::fill(su.begin(), su.end(), std::min(forced, nkb));
             best_su = su;
         } else {
-            // equal-cost items: unit u gets round(cost_u * nkb / T) splits for a target item cost T;
+            // equal-cost items: unit u gets ceil(cost_u * nkb / T) splits for a target item cost T;
             // T = c_max * nkb / k for k = 1, 1.5, 2, ... 64 (k = 1: no split); best simulated makespan wins
             const double c_max = unit_cost4(480);
             best_su = su;
-            best = plan_items4(code, ncols, su, nkb, pairs, nullptr);
+            best = plan_items4(code, nb, ncols, su, nkb, pairs, nullptr);
             const int32_t kmax = std::max(1, std::min(64, nkb / 8));
             for (int32_t k2 = 3; k2 <= 2 * kmax; ++k2) {  // T = c_max * nkb / (k2 / 2): half steps
                 const double T = 2.0 * c_max * nkb / k2;
                 for (size_t u = 0; u < code.size(); ++u) {
+                    // ceil, not round: no item may exceed the target (a rounded-down unit sets the makespan)
                     const double s_real = unit_cost4(ncols[u]) * nkb / T;
-                    su[u] = (int32_t)std::max<int64_t>(1, std::min<int64_t>(nkb, std::llround(s_real)));
+                    su[u] = (int32_t)std::max<int64_t>(1, std::min<int64_t>(nkb, (int64_t)std::ceil(s_real - 1e-9)));
                 }
-                const double t = plan_items4(code, ncols, su, nkb, pairs, nullptr);
+                const double t = plan_items4(code, nb, ncols, su, nkb, pairs, nullptr);
+                if (std::getenv("TB_TRACE_PLAN")) {
+                    int64_t ni = 0;
+                    for (int32_t v : su) ni += v;
+                    fprintf(stderr, "  cand k2 %d items %lld est %.0f\n", k2, (long long)ni, t);
+                }
                 if (t < best * 0.999) { best = t; best_su = su; }
             }
             // fill idle pairs: split the most expensive item's unit once more while items < pairs
@@ -431,13 +443,13 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
                 if (worst < 0) break;
                 ++su[arg];
                 ++nitems;
-                const double t = plan_items4(code, ncols, su, nkb, pairs, nullptr);
+                const double t = plan_items4(code, nb, ncols, su, nkb, pairs, nullptr);
                 if (t < best * 0.999) { best = t; best_su = su; }
             }
         }
     }
     std::vector<int4> items;
-    const double span_est = code.empty() ? 0.0 : plan_items4(code, ncols, best_su, nkb, pairs, &items);
+    const double span_est = code.empty() ? 0.0 : plan_items4(code, nb, ncols, best_su, nkb, pairs, &items);
     const int32_t smax = best_su.empty() ? 1 : *std::max_element(best_su.begin(), best_su.end());
     const char* trace = std::getenv("TB_TRACE");
     if (trace && trace[0] == '1')
@@ -483,11 +495,9 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.job_hi = job_hi;
     p.num = num;
     if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
-    CUtensorMap ta, tbm, tbe;
+    CUtensorMap ta, tbm;
     if ((rc = make_tmap(&ta, S, m, kbytes, ldS, g4::BM))) return rc;
     if ((rc = make_tmap(&tbm, S, m, kbytes, ldS, g4::BNH))) return rc;
-    p.n_edge = (int32_t)(((m % g4::BN) + 15) / 16 * 16);  // multiple of 16 in [16, 240] or 0
-    if ((rc = make_tmap(&tbe, S, m, kbytes, ldS, p.n_edge ? (uint32_t)p.n_edge / 2 : g4::BNH))) return rc;
     TB_CUDA_TRY(cudaFuncSetAttribute(gemm_fp4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)g4::SMEM_BYTES));
     const unsigned grid = (unsigned)(2 * std::max<int64_t>(1, std::min<int64_t>(p.nitems, pairs)));
@@ -498,7 +508,7 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
         TB_CUDA_TRY(cudaMemsetAsync(p.trace, 0, grid * 16 * sizeof(unsigned long long), st));
         TB_CUDA_TRY(cudaStreamSynchronize(st));
     }
-    gemm_fp4_kernel<<<grid, g4::THREADS, g4::SMEM_BYTES, st>>>(ta, tbm, tbe, p);
+    gemm_fp4_kernel<<<grid, g4::THREADS, g4::SMEM_BYTES, st>>>(ta, tbm, p);
     if ((rc = check_launch("gemm_fp4_kernel"))) return rc;
     if (p.trace) {
         TB_CUDA_TRY(cudaStreamSynchronize(st));
@@ -522,8 +532,8 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
             cudaMemcpy(items.data(), p.items, items.size() * sizeof(int4), cudaMemcpyDeviceToHost);
             for (unsigned b = 0; b < grid; b += 2) {
                 const int4 it = items[b / 2];
-                const long long yb = it.x >> 16, xb = it.x & 0xFFFF;
-                fprintf(stderr, "  pair %3u unit (%lld,%lld) kb [%d,%d) tfull %.1f us\n", b / 2, yb, xb, it.y, it.z,
+                const long long yb = it.x, xb = (long long)((uint32_t)it.w >> 16), xb1 = it.w & 0xFFFF;
+                fprintf(stderr, "  pair %3u unit (yb %lld, blocks %lld,%lld) kb [%d,%d) tfull %.1f us\n", b / 2, yb, xb, xb1, it.y, it.z,
                         tr[b * 16] ? (tr[b * 16] - t0) * 1e-3 : -1.0);
             }
         }
