@@ -36,11 +36,12 @@ constexpr int STAGES = 4;
 constexpr uint32_t A_BYTES = BM * BK;    // 16 KiB
 constexpr uint32_t B_BYTES = BNH * BK;   // 15 KiB per N block
 constexpr uint32_t STAGE_BYTES = A_BYTES + NB * B_BYTES;
-constexpr int THREADS = 256;
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, splitting each block's 16-column chunks by parity
+constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t SF_COL = 480;
 constexpr int STG_LD = 17;    // epilogue staging tile: 32 rows x 16 columns, padded row stride
-constexpr uint32_t STG_BYTES = 4 * (32 * STG_LD * 4 + 32 * 8);  // 4 epilogue warps: tile + row bases
+constexpr uint32_t STG_BYTES = EPI_WARPS * (32 * STG_LD * 4 + 32 * 8);  // per epilogue warp: tile + row bases
 constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + STG_BYTES;
 }  // namespace g4
 
@@ -127,7 +128,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
-        mbar_init(tempty, 8);  // 4 epilogue warps x 2 CTAs
+        mbar_init(tempty, 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
@@ -135,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    if (warp >= 4) {  // scale factors: every byte 0x7F (ue8m0 2^0) in this CTA's lanes, columns [480, 512)
+    if (warp >= 4 && warp < 8) {  // scale factors: every byte 0x7F (ue8m0 2^0) in this CTA's lanes, columns [480, 512)
         tmem_st_32x32b_x32(tmem_base + (uint32_t((warp & 3) * 32) << 16) + SF_COL, 0x7F7F7F7Fu);
         tmem_st_wait();
     }
@@ -217,8 +218,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
         // transposed through shared memory: half a warp covers 16 consecutive columns of one row,
         // i.e. 16 consecutive job ids, so every store touches 2 short runs instead of 32 rows m ints
         // apart.  Split partials are added lane-per-row with aligned 16-byte f32 reds.
-        const int q = warp & 3;
-        int32_t* stg = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256) + q * (32 * STG_LD + 64);
+        const int q = warp & 3;              // TMEM lane quarter
+        const int par = (warp - 4) >> 2;     // this warp's 16-column chunks: c / 16 = par (mod 2)
+        int32_t* stg = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * STG_LD + 64);
         int64_t* rowbase = reinterpret_cast<int64_t*>(stg + 32 * STG_LD);
         uint32_t acc_phase = 0;
         const int64_t m = p.m;
@@ -239,10 +241,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             mbar_wait(tfull, acc_phase);
             tc_fence_after();
             int item = (int)((cur - pair) / npairs) - 1;
-            if (p.trace && q == 0 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2] = globaltimer();
+            if (p.trace && warp == 4 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2] = globaltimer();
             for (int h = 0; h < t.nblk; ++h) {
 #pragma unroll 1
-                for (int c = 0; c < BN; c += 16) {
+                for (int c = 16 * par; c < BN; c += 32) {
                     uint32_t r[16];
                     tmem_ld_32x32b_x16(tmem_base + (uint32_t(q * 32) << 16) + h * BN + c, r);
                     tmem_ld_wait();
@@ -296,7 +298,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (p.trace && q == 0 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2 + 1] = globaltimer();
+            if (p.trace && warp == 4 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2 + 1] = globaltimer();
             if (lane == 0) mbar_arrive_cluster(tempty_leader);
             acc_phase ^= 1;
         }
