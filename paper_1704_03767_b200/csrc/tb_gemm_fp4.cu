@@ -36,7 +36,8 @@ constexpr int STAGES = 4;
 constexpr uint32_t A_BYTES = BM * BK;    // 16 KiB
 constexpr uint32_t B_BYTES = BNH * BK;   // 15 KiB per N block
 constexpr uint32_t STAGE_BYTES = A_BYTES + NB * B_BYTES;
-constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, splitting each block's 16-column chunks by parity
+constexpr int EPI_WARPS = 16;  // EPI_WARPS / 4 per TMEM lane quarter, splitting each block's 16-column chunks
+constexpr int EPI_PAR = EPI_WARPS / 4;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t SF_COL = 480;
@@ -219,7 +220,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
         // i.e. 16 consecutive job ids, so every store touches 2 short runs instead of 32 rows m ints
         // apart.  Split partials are added lane-per-row with aligned 16-byte f32 reds.
         const int q = warp & 3;              // TMEM lane quarter
-        const int par = (warp - 4) >> 2;     // this warp's 16-column chunks: c / 16 = par (mod 2)
+        const int par = (warp - 4) >> 2;     // this warp's 16-column chunks: c / 16 = par (mod EPI_PAR)
         int32_t* stg = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * STG_LD + 64);
         int64_t* rowbase = reinterpret_cast<int64_t*>(stg + 32 * STG_LD);
         uint32_t acc_phase = 0;
@@ -244,7 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             if (p.trace && warp == 4 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2] = globaltimer();
             for (int h = 0; h < t.nblk; ++h) {
 #pragma unroll 1
-                for (int c = 16 * par; c < BN; c += 32) {
+                for (int c = 16 * par; c < BN; c += 16 * EPI_PAR) {
                     uint32_t r[16];
                     tmem_ld_32x32b_x16(tmem_base + (uint32_t(q * 32) << 16) + h * BN + c, r);
                     tmem_ld_wait();
