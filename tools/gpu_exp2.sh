@@ -1,10 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/plain_bench.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_fp4 -s 2 -c 1 -o gpurun_out/prof_gemm_fp4_v6 -f \
-    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_g.log 2>&1; echo full2=$?
-timeout 600 python bench.py --config 3 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/plain3.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_fp4 -s 1 -c 1 -o gpurun_out/prof_gemm_fp4_c3_v6 -f \
-    python bench.py --config 3 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_g3.log 2>&1; echo full3=$?
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/plain_bench.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 14 --csv --log-file gpurun_out/launches_bench.csv \
-    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_l.log 2>&1; echo launches=$?
+for sl in 0 1; do
+  TB_PLAN_SLICE=$sl TB_TRACE=1 timeout 300 python tools/exp_epi.py 2 3 > gpurun_out/exp_slice_$sl.log 2>&1
+  echo "slice=$sl $(grep 'gemm ms' gpurun_out/exp_slice_$sl.log | tr '\n' ' ')"
+done
+TB_PLAN_SLICE=1 timeout 1800 python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout 900 -x > gpurun_out/pytest_slice.log 2>&1; echo pytest=$?
