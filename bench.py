@@ -200,7 +200,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic", "config": {"workload": spec.name, "m": m, "n": n, "pairs": m * (m - 1) // 2},
+        "data": "synthetic",
+        "config": {"workload": f"config{args.config}_{spec.name}", "m": m, "n": n, "pairs_per_rank": m * (m - 1) // 2,
+                   "path": "gemm" if n <= 8192 else "merge",
+                   "outputs": "numerator i32 + tau_a f64 + tau_b f64 in job-id order"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)

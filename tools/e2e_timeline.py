@@ -17,9 +17,9 @@ def call(name, *a):
     return r
 dv._lib.call = call
 verbose = os.environ.get("TL_VERBOSE") == "1"
-for fr in [(0.55, 0.30, 0.15), (0.65, 0.25, 0.1)]:
-  for pb in (1 << 20, 2 << 20, 4 << 20, 64 << 20):
-    for hc in (1, 2):
+for fr in [(0.65, 0.25, 0.1)]:
+  for pb in (4 << 20,):
+    for hc in (2,):
         tt = []
         for it in range(8):
             marks.clear()
