@@ -180,11 +180,11 @@ __global__ void __launch_bounds__(256) rank_rows_hist_kernel(const int32_t* __re
     const int nn = (int)n;
     uint32_t k[E];
     uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+    // unconditional loads (out-of-range slots re-read the last element, masked below): predicated
+    // loads let the compiler serialise each load with its use -- one DRAM latency per element
+    const int32_t* xr = x + r * ldx;
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-        const int e = lane + 32 * i;
-        k[i] = e < nn ? (uint32_t)x[r * ldx + e] ^ 0x80000000u : 0u;
-    }
+    for (int i = 0; i < E; ++i) k[i] = (uint32_t)__ldg(&xr[min(lane + 32 * i, nn - 1)]) ^ 0x80000000u;
 #pragma unroll
     for (int i = 0; i < E; ++i)
         if (lane + 32 * i < nn) {
@@ -239,14 +239,17 @@ __global__ void __launch_bounds__(256) rank_rows_warp_kernel(const T* __restrict
     const int nn = (int)n;
     uint64_t v[E];
     bool bad = false;
+    T xv[E];  // unconditional loads first (see rank_rows_hist_kernel), then keys
+    const T* xr = x + r * ldx;
+#pragma unroll
+    for (int i = 0; i < E; ++i) xv[i] = __ldg(&xr[min(lane + 32 * i, nn - 1)]);
 #pragma unroll
     for (int i = 0; i < E; ++i) {
         const int e = lane + 32 * i;  // coalesced load, any slot assignment works before the sort
         uint64_t key = 0xFFFFFFFFull;
         if (e < nn) {
-            const T xv = x[r * ldx + e];
-            bad |= (xv != xv);
-            key = order_key(xv);
+            bad |= (xv[i] != xv[i]);
+            key = order_key(xv[i]);
         }
         v[i] = (key << 16) | (uint64_t)e;
     }
