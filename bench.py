@@ -427,7 +427,9 @@ def run_ours(args):
         tt = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_t = float(tt.item())
-    e2e_pairs = strict_pairs(0, total_jobs) * world
+    # every rank runs the full host entry point: weak scaling counts each rank's copy, strong scaling
+    # (one shared job range) does not shard this leg, so it counts the pairs once
+    e2e_pairs = strict_pairs(0, total_jobs) * (world if args.scaling == "weak" else 1)
     e2e_value = e2e_pairs * len(e2e_times) / e2e_t
     h2d = xh.numel() * xh.element_size()
     d2h = total_jobs * 8
