@@ -13,24 +13,23 @@
 
 namespace tb {
 
-// Block b owns job ids [job_lo + b * FIN_CHUNK, +FIN_CHUNK); thread t decodes its first
+// Block b owns job ids [job_lo + b * chunk, +chunk); thread t decodes its first
 // cell (y, x) once and then steps 256 job ids at a time, walking the row-major upper triangle
 // incrementally (x += 256, wrapping to row y + 1 at column y + 1), so the per-element work is the
 // IEEE tau sequence plus a few integer ops -- no per-element sqrt-based job_coord.  Loads and stores
 // stay coalesced (consecutive threads = consecutive job ids).
 constexpr int FIN_THREADS = 256;
-constexpr int FIN_ITERS = 16;
-constexpr int64_t FIN_CHUNK = (int64_t)FIN_THREADS * FIN_ITERS;
+constexpr int FIN_ITERS_MAX = 16;  // cells per thread for large ranges; small ranges use fewer (more CTAs)
 
 __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32_t* __restrict__ num,
                                                                       const unsigned long long* __restrict__ n1,
                                                                       int64_t m, int64_t n0, int64_t job_lo,
                                                                       int64_t count, double* __restrict__ tau_a,
-                                                                      double* __restrict__ tau_b) {
+                                                                      double* __restrict__ tau_b, int64_t chunk) {
     const double dn0 = (double)n0;
-    int64_t i = (int64_t)blockIdx.x * FIN_CHUNK + threadIdx.x;
+    int64_t i = (int64_t)blockIdx.x * chunk + threadIdx.x;
     if (i >= count) return;
-    const int64_t i_end = min(count, (int64_t)(blockIdx.x + 1) * FIN_CHUNK);
+    const int64_t i_end = min(count, (int64_t)(blockIdx.x + 1) * chunk);
     int64_t y, x;
     job_coord(job_lo + i, m, y, x);
     double ty = dn0 - (double)__ldg(&n1[y]);
@@ -68,10 +67,16 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     if (!num || !n1_rows) return fail(TB_ERR_INVALID, "finalize: null pointer");
     const int64_t count = job_hi - job_lo;
     if (count == 0) return TB_OK;
-    const int64_t blocks = (count + FIN_CHUNK - 1) / FIN_CHUNK;
+    // each thread walks `iters` cells 256 apart: 16 for large ranges (amortises the job_coord decode);
+    // small ranges shorten the walk so the grid still covers the GPU (~4 CTAs per SM)
+    const int64_t per_sm = (int64_t)num_sms() * 4 * FIN_THREADS;
+    const int64_t iters = std::max<int64_t>(1, std::min<int64_t>(FIN_ITERS_MAX, count / std::max<int64_t>(1, per_sm)));
+    const int64_t chunk = iters * FIN_THREADS;
+    const int64_t blocks = (count + chunk - 1) / chunk;
     if (blocks > INT32_MAX) return fail(TB_ERR_CAPACITY, "finalize: job range too large");
     finalize_chunk_kernel<<<(unsigned)blocks, FIN_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-        num, reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count, tau_a, tau_b);
+        num, reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count, tau_a, tau_b,
+        chunk);
     return check_launch("finalize_chunk_kernel");
 }
 
