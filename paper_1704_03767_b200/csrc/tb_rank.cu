@@ -299,6 +299,52 @@ __global__ void __launch_bounds__(256) rank_rows_warp_kernel(const T* __restrict
     for (int64_t i = nn + lane; i < ldr; i += 32) R[r * ldr + i] = 0;
 }
 
+// n <= 256 (any dtype): one CTA per row, one thread per element, O(n^2) comparisons against the
+// row's keys in shared memory -- dense rank = number of smaller first occurrences, n1 = number of
+// equal earlier elements summed over the row.  Short rows are too few for the warp sort to fill the
+// GPU (config 1: 256 rows of 200 f64) and the CTA bitonic sort pays a barrier per stage.
+constexpr int RK_SMALL_N = 256;
+template <typename T>
+__global__ void __launch_bounds__(RK_SMALL_N) rank_rows_small_kernel(const T* __restrict__ x, int64_t n, int64_t ldx,
+                                                                     uint16_t* __restrict__ R, int64_t ldr,
+                                                                     unsigned long long* __restrict__ n1,
+                                                                     int32_t* __restrict__ flags) {
+    __shared__ uint64_t key[RK_SMALL_N];
+    __shared__ uint8_t first[RK_SMALL_N];
+    __shared__ unsigned long long red[RK_SMALL_N / 32];
+    const int64_t r = blockIdx.x;
+    const int i = threadIdx.x, nn = (int)n;
+    bool bad = false;
+    uint64_t ki = ~0ull;
+    if (i < nn) {
+        const T v = x[r * ldx + i];
+        bad = v != v;
+        ki = order_key(v);
+        key[i] = ki;
+    }
+    if (__syncthreads_or(bad) && i == 0) atomicOr(flags, 1);
+    int eq_before = 0;
+    if (i < nn)
+        for (int j = 0; j < i; ++j) eq_before += key[j] == ki;
+    first[i] = (i < nn && eq_before == 0) ? 1 : 0;
+    __syncthreads();
+    if (i < nn) {
+        int less = 0;
+        for (int j = 0; j < nn; ++j) less += (key[j] < ki) & first[j];
+        R[r * ldr + i] = (uint16_t)less;
+    }
+    unsigned long long ties = (unsigned long long)eq_before;
+    for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
+    if ((i & 31) == 0) red[i >> 5] = ties;
+    __syncthreads();
+    if (i == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < RK_SMALL_N / 32; ++w) t += red[w];
+        n1[r] = t;
+    }
+    for (int64_t k = nn + i; k < ldr; k += RK_SMALL_N) R[r * ldr + k] = 0;
+}
+
 template <typename T>
 static int launch_rank_warp(const T* x, int64_t m, int64_t n, int64_t ldx, uint16_t* R, int64_t ldr,
                             unsigned long long* n1, int32_t* flags, int Np, cudaStream_t st) {
@@ -350,6 +396,22 @@ extern "C" int tb_rank_rows(const void* x, int dtype, int64_t m, int64_t n, int6
     const size_t smem = (size_t)Np * (8 + 2 + 2);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto* n1u = reinterpret_cast<unsigned long long*>(n1);
+    if (n <= RK_SMALL_N) {  // short rows: O(n^2) per-row ranks, one thread per element
+        switch (dtype) {
+            case TB_DTYPE_I32:
+                rank_rows_small_kernel<int32_t><<<(unsigned)m, RK_SMALL_N, 0, st>>>((const int32_t*)x, n, ldx, R, ldr, n1u, flags);
+                break;
+            case TB_DTYPE_F32:
+                rank_rows_small_kernel<float><<<(unsigned)m, RK_SMALL_N, 0, st>>>((const float*)x, n, ldx, R, ldr, n1u, flags);
+                break;
+            case TB_DTYPE_F64:
+                rank_rows_small_kernel<double><<<(unsigned)m, RK_SMALL_N, 0, st>>>((const double*)x, n, ldx, R, ldr, n1u, flags);
+                break;
+            default:
+                return fail(TB_ERR_INVALID, "rank_rows: unknown dtype %d", dtype);
+        }
+        return check_launch("rank_rows_small_kernel");
+    }
     if (Np <= 1024 && dtype != TB_DTYPE_F64) {  // 32-bit keys: warp-per-row register sort
         if (Np < 32) Np = 32;
         if (dtype == TB_DTYPE_I32) return launch_rank_warp((const int32_t*)x, m, n, ldx, R, ldr, n1u, flags, Np, st);
