@@ -68,8 +68,8 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     const int64_t count = job_hi - job_lo;
     if (count == 0) return TB_OK;
     // each thread walks `iters` cells 256 apart: 16 for large ranges (amortises the job_coord decode);
-    // small ranges shorten the walk so the grid still covers the GPU (~4 CTAs per SM)
-    const int64_t per_sm = (int64_t)num_sms() * 4 * FIN_THREADS;
+    // small ranges shorten the walk so the grid still covers the GPU
+    const int64_t per_sm = (int64_t)num_sms() * 8 * FIN_THREADS;  // ~8 CTAs per SM (measured 4 / 8 / 16 / 32)
     const int64_t iters = std::max<int64_t>(1, std::min<int64_t>(FIN_ITERS_MAX, count / std::max<int64_t>(1, per_sm)));
     const int64_t chunk = iters * FIN_THREADS;
     const int64_t blocks = (count + chunk - 1) / chunk;
