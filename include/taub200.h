@@ -152,6 +152,8 @@ int tb_finalize(const int32_t *num, const uint64_t *n1_rows, int64_t m, int64_t 
  *   ranks   [m, n] int32 dense ranks (0 <= rank < n)
  *   pos     [m, n] int32 out: pos[r, e] = position of element e in u-order
  *   sorted  [m, n] int32 out: sorted[r, p] = rank at position p
+ *   keys    [m, n] uint16 out: min-rank (competition rank) of every element, i.e. the number of
+ *           elements of the row with a strictly smaller rank; the merge keys of tb_merge_pairs
  *   n1      [m] uint64 out;  maxgrp [m] int32 out (largest tie group)
  *   work    [m, n] int32 out: compact tie-group list, work[r, 2k] = first
  *           u-order position and work[r, 2k+1] = length of the k-th rank value
@@ -160,17 +162,18 @@ int tb_finalize(const int32_t *num, const uint64_t *n1_rows, int64_t m, int64_t 
  *   flags   device int32; bit 1 is set when a rank is outside [0, n) (the
  *           caller raises InvalidInputError, as Dataset validation does)
  */
-int tb_presort(const int32_t *ranks, int64_t m, int64_t n, int32_t *pos, int32_t *sorted, uint64_t *n1,
-               int32_t *maxgrp, int32_t *work, int32_t *ngroups, int32_t *flags, void *stream);
+int tb_presort(const int32_t *ranks, int64_t m, int64_t n, int32_t *pos, int32_t *sorted, uint16_t *keys,
+               uint64_t *n1, int32_t *maxgrp, int32_t *work, int32_t *ngroups, int32_t *flags, void *stream);
 
 /*
  * K4 Knight merge-inversion counts (large n): for every job id in
  * [job_lo, job_hi): n_d (discordant pairs, strict), n3 (joint ties) and the
  * numerator n0 - n1 - n2 + n3 - 2 n_d (src/taucorr/result.py:42).  Replaces
  * steps 1-5 of sorted_counts (src/taucorr/kernel_sorted.py:195-212).
+ * keys, pos, sorted, n1_rows, maxgrp, groups and ngroups are tb_presort's outputs.
  * nd / n3 may be NULL.
  */
-int tb_merge_pairs(const int32_t *ranks, const int32_t *pos, const int32_t *sorted, const uint64_t *n1_rows,
+int tb_merge_pairs(const uint16_t *keys, const int32_t *pos, const int32_t *sorted, const uint64_t *n1_rows,
                    const int32_t *maxgrp, const int32_t *groups, const int32_t *ngroups, int64_t m, int64_t n,
                    int64_t job_lo, int64_t job_hi, int32_t *num, uint64_t *nd, uint64_t *n3, void *stream);
 

@@ -38,7 +38,7 @@ SIGNATURES = {
     "tb_gemm_pairs_simt": ([_p, _i64, _i64, _i64, _i64, _i64, _p, _p], ctypes.c_int),
     "tb_finalize": ([_p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "tb_full_counts": ([_p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
-    "tb_presort": ([_p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+    "tb_presort": ([_p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
     "tb_merge_pairs": ([_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
 }
 

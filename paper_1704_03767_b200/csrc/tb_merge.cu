@@ -14,13 +14,20 @@
 // elements in any order.  SURVEY 8 verified the identity against the oracle.
 //
 // K4 layout: one CTA of 1024 threads per pair (persistent over job ids);
-// w lives in shared memory as uint16 (ranks < n <= 65536).  inv(w) is a
-// bottom-up merge sort with merge-path partitioning and the reference's
-// counting rule (right element strictly smaller => + unconsumed left length,
-// kernel_sorted.py:72-73).  n <= 32768: one block of L = 2^ceil(log2 n) keys
-// plus an L-key ping-pong buffer; n > 32768: two sorted halves of 32768 kept
-// side by side and their cross inversions counted by a merge-path walk without
-// materialising the final merge (192 KiB of shared memory in total).
+// w lives in shared memory as uint16 keys.  The keys are MIN-RANKS (competition
+// ranks: key = # elements of the row with a strictly smaller rank, < n <= 65536),
+// which order and tie exactly like dense ranks.  inv(w) is a bottom-up merge sort
+// with merge-path partitioning and the reference's counting rule (right element
+// strictly smaller => + unconsumed left length, kernel_sorted.py:72-73).
+// n <= 32768: one block of L = 2^ceil(log2 n) keys plus an L-key ping-pong
+// buffer; n > 32768: two halves H1 = w[0, 32768), H2 = the rest, each sorted
+// with its own count (192 KiB of shared memory in total).  Their cross
+// inversions need no merge: with min-rank keys every a in H1 has exactly
+// key(a) smaller keys in the whole row, so
+//     sum_{a in H1} key(a) = #{(a, a') in H1^2 : a' < a} + cross(H1, H2)
+//                          = L1 (L1 - 1) / 2 - ties(H1) + cross(H1, H2),
+// and cross = sum key(H1) - L1 (L1 - 1) / 2 + ties(H1), ties(H1) being the
+// equal-key pairs inside H1 (a scan of sorted H1).
 #include "tb_common.cuh"
 
 namespace tb {
@@ -41,9 +48,11 @@ __device__ __forceinline__ int64_t block_reduce_sum(int64_t v, int64_t* red) {
     return t;  // valid in warp 0
 }
 
-// One CTA per variable.  work[r, k] = histogram -> exclusive start -> fill cursor.
+// One CTA per variable.  work[r, k] = histogram -> exclusive start -> fill cursor.  The exclusive
+// start of an element's rank is its min-rank: keys[r, e].
 __global__ void __launch_bounds__(PS_THREADS) presort_kernel(const int32_t* __restrict__ ranks, int64_t n,
                                                              int32_t* __restrict__ pos, int32_t* __restrict__ sorted,
+                                                             uint16_t* __restrict__ keys,
                                                              unsigned long long* __restrict__ n1,
                                                              int32_t* __restrict__ maxgrp, int32_t* __restrict__ work,
                                                              int32_t* __restrict__ flags) {
@@ -114,6 +123,12 @@ __global__ void __launch_bounds__(PS_THREADS) presort_kernel(const int32_t* __re
         for (int w = 0; w < PS_THREADS / 32; ++w) m2 = max(m2, chunk_base[w]);
         maxgrp[r] = m2;
         n1[r] = (unsigned long long)tsum;
+    }
+    __syncthreads();
+    uint16_t* ky = keys + r * n;
+    for (int64_t i = tid; i < n; i += PS_THREADS) {
+        int32_t vr = rk[i];
+        ky[i] = (vr >= 0 && vr < n) ? (uint16_t)cnt[vr] : (uint16_t)0;
     }
     __syncthreads();
     for (int64_t i = tid; i < n; i += PS_THREADS) {
@@ -385,7 +400,7 @@ __device__ __forceinline__ uint32_t sort_count_any(uint16_t* keys, uint16_t* tmp
 }
 
 struct MergeArgs {
-    const int32_t* ranks;
+    const uint16_t* keys;  // [m, n] min-rank keys (tb_presort)
     const int32_t* pos;
     const int32_t* sorted;
     const int32_t* maxgrp;
@@ -416,22 +431,24 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         job_coord(p.job_lo + idx, p.m, y, x);
         const int32_t* pu = p.pos + y * n;      // u-order positions
         const int32_t* su = p.sorted + y * n;   // u ranks in u-order
-        const int32_t* rv = p.ranks + x * n;    // v ranks
+        const uint16_t* kv = p.keys + x * n;    // v min-rank keys
 
-        // pads (max key) first, then scatter w[pos_u[e]] = rank_v[e]
+        // pads (max key: real keys are < n <= 65535 whenever pads exist) first, then scatter
+        // w[pos_u[e]] = key_v[e]
         for (int64_t i = n + tid; i < (int64_t)p.B * L; i += MG_THREADS) keys[sw((int)i)] = 0xFFFF;
-        if ((n & 3) == 0) {  // 16-byte loads of u-positions and v-ranks
+        if ((n & 3) == 0) {  // 16-byte loads of u-positions, 8-byte loads of v keys
             const int4* pu4 = reinterpret_cast<const int4*>(pu);
-            const int4* rv4 = reinterpret_cast<const int4*>(rv);
+            const uint2* kv4 = reinterpret_cast<const uint2*>(kv);
             for (int64_t e = tid; e < (n >> 2); e += MG_THREADS) {
-                const int4 P = pu4[e], V = rv4[e];
-                keys[sw(P.x)] = (uint16_t)V.x;
-                keys[sw(P.y)] = (uint16_t)V.y;
-                keys[sw(P.z)] = (uint16_t)V.z;
-                keys[sw(P.w)] = (uint16_t)V.w;
+                const int4 P = pu4[e];
+                const uint2 V = kv4[e];
+                keys[sw(P.x)] = (uint16_t)(V.x & 0xFFFFu);
+                keys[sw(P.y)] = (uint16_t)(V.x >> 16);
+                keys[sw(P.z)] = (uint16_t)(V.y & 0xFFFFu);
+                keys[sw(P.w)] = (uint16_t)(V.y >> 16);
             }
         } else {
-            for (int64_t e = tid; e < n; e += MG_THREADS) keys[sw(pu[e])] = (uint16_t)rv[e];
+            for (int64_t e = tid; e < n; e += MG_THREADS) keys[sw(pu[e])] = kv[e];
         }
         __syncthreads();
 
@@ -466,32 +483,37 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
 
         // inv(w)
         uint32_t inv = sort_count_any(keys, tmp, L);
+        int64_t cross = 0;
         if (p.B == 2) {
             inv += sort_count_any(keys + sw(L), tmp, L);  // L = 32768: sw(L + i) = sw(L) + sw(i)
-            // cross inversions: for each b in block 1, # of block-0 keys > b
-            const int64_t L2 = n - L1;
-            const int64_t per = (L2 + MG_THREADS - 1) / MG_THREADS;
-            const int64_t b0 = tid * per, b1 = min(b0 + per, L2);
-            if (b0 < b1) {
-                const uint16_t* H1 = keys;
-                const uint16_t* H2 = keys + sw(L);
-                uint16_t b = H2[sw((int)b0)];
-                int64_t lo = 0, hi = L1;  // upper_bound(H1, b)
+            // cross(H1, H2) = sum key(H1) - L1 (L1 - 1) / 2 + ties(H1) (header); the -L1 (L1 - 1) / 2
+            // is applied once after the reduction.  H1 = keys[0, L) is sorted and holds no pads.
+            constexpr int CE = MG_HALF / MG_THREADS;  // 32 sorted keys per thread
+            uint32_t v[CE];
+            load_run<CE>(keys, tid, v);
+            const int p0 = tid * CE;
+            uint32_t prev = tid ? keys[sw(p0 - 1)] : 0xFFFFFFFFu;
+            int first = p0;  // first index of the equal-key run holding the current key
+            if (v[0] == prev) {  // run continues from the previous thread: lower_bound(H1, v[0])
+                int lo = 0, hi = p0 - 1;
                 while (lo < hi) {
-                    int64_t mid = (lo + hi) >> 1;
-                    if (H1[sw((int)mid)] <= b) lo = mid + 1;
+                    const int mid = (lo + hi) >> 1;
+                    if (keys[sw(mid)] < v[0]) lo = mid + 1;
                     else hi = mid;
                 }
-                int64_t ub = lo;
-                for (int64_t k = b0; k < b1; ++k) {
-                    b = H2[sw((int)k)];
-                    while (ub < L1 && H1[sw((int)ub)] <= b) ++ub;
-                    inv += (uint32_t)(L1 - ub);
-                }
+                first = lo;
             }
+            uint32_t ksum = 0, ties = 0;
+#pragma unroll
+            for (int q = 0; q < CE; ++q) {
+                ksum += v[q];
+                if (q > 0 && v[q] != v[q - 1]) first = p0 + q;
+                ties += (uint32_t)(p0 + q - first);
+            }
+            cross = (int64_t)ksum + (int64_t)ties;
         }
 
-        const int64_t tot_inv = block_reduce_sum((int64_t)inv, red);
+        const int64_t tot_inv = block_reduce_sum((int64_t)inv + cross, red) - (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
         const int64_t tot_g = block_reduce_sum((int64_t)inv_g, red);
         const int64_t tot_t = block_reduce_sum((int64_t)ties, red);
         if (tid == 0) {
@@ -510,22 +532,23 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
 
 using namespace tb;
 
-extern "C" int tb_presort(const int32_t* ranks, int64_t m, int64_t n, int32_t* pos, int32_t* sorted, uint64_t* n1,
-                          int32_t* maxgrp, int32_t* work, int32_t* ngroups, int32_t* flags, void* stream) {
+extern "C" int tb_presort(const int32_t* ranks, int64_t m, int64_t n, int32_t* pos, int32_t* sorted, uint16_t* keys,
+                          uint64_t* n1, int32_t* maxgrp, int32_t* work, int32_t* ngroups, int32_t* flags,
+                          void* stream) {
     if (m < 1 || n < 1) return fail(TB_ERR_INVALID, "presort: empty input");
     if (n > TB_MAX_N) return fail(TB_ERR_CAPACITY, "presort: n=%lld exceeds %d", (long long)n, TB_MAX_N);
-    if (!ranks || !pos || !sorted || !n1 || !maxgrp || !work || !ngroups || !flags)
+    if (!ranks || !pos || !sorted || !keys || !n1 || !maxgrp || !work || !ngroups || !flags)
         return fail(TB_ERR_INVALID, "presort: null pointer");
     if (m > INT32_MAX) return fail(TB_ERR_CAPACITY, "presort: m too large");
     presort_kernel<<<(unsigned)m, PS_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-        ranks, n, pos, sorted, reinterpret_cast<unsigned long long*>(n1), maxgrp, work, flags);
+        ranks, n, pos, sorted, keys, reinterpret_cast<unsigned long long*>(n1), maxgrp, work, flags);
     int rc = check_launch("presort_kernel");
     if (rc) return rc;
     tie_groups_kernel<<<(unsigned)m, 256, 0, static_cast<cudaStream_t>(stream)>>>(sorted, n, work, ngroups);
     return check_launch("tie_groups_kernel");
 }
 
-extern "C" int tb_merge_pairs(const int32_t* ranks, const int32_t* pos, const int32_t* sorted,
+extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const int32_t* sorted,
                               const uint64_t* n1_rows, const int32_t* maxgrp, const int32_t* groups,
                               const int32_t* ngroups, int64_t m, int64_t n, int64_t job_lo, int64_t job_hi,
                               int32_t* num, uint64_t* nd, uint64_t* n3, void* stream) {
@@ -534,10 +557,10 @@ extern "C" int tb_merge_pairs(const int32_t* ranks, const int32_t* pos, const in
     if (n > TB_MAX_N) return fail(TB_ERR_CAPACITY, "merge: n=%lld exceeds %d", (long long)n, TB_MAX_N);
     const int64_t total = m * (m + 1) / 2;
     if (job_lo < 0 || job_hi < job_lo || job_hi > total) return fail(TB_ERR_CONFIG, "merge: bad job range");
-    if (!ranks || !pos || !sorted || !n1_rows || !num) return fail(TB_ERR_INVALID, "merge: null pointer");
+    if (!keys || !pos || !sorted || !n1_rows || !num) return fail(TB_ERR_INVALID, "merge: null pointer");
     if (job_hi == job_lo) return TB_OK;
     MergeArgs a{};
-    a.ranks = ranks;
+    a.keys = keys;
     a.pos = pos;
     a.sorted = sorted;
     a.maxgrp = maxgrp;

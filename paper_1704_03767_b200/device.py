@@ -308,7 +308,7 @@ class TauEngine:
             else:
                 for _, _, ev in chunks:
                     st_t.wait_event(ev)
-                pos, srt, maxgrp = self._merge_prepare(x, res, st)
+                pos, srt, keys, maxgrp = self._merge_prepare(x, res, st)
             cuts = self.bands(m, len(band_fracs), fracs=band_fracs)
             for r0, r1 in zip(cuts[:-1], cuts[1:]):
                 lo, hi = r0 * (2 * m - r0 + 1) // 2, r1 * (2 * m - r1 + 1) // 2
@@ -316,7 +316,7 @@ class TauEngine:
                 if path == "gemm":
                     self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st)
                 else:
-                    _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp[0]),
+                    _lib.call("tb_merge_pairs", _ptr(keys), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp[0]),
                               _ptr(maxgrp[1]), _ptr(maxgrp[2]), m, n, lo, hi, _ptr(num), None, None, st)
                 tb = res.tau_b[lo:hi]
                 _lib.call("tb_finalize", _ptr(num), _ptr(res.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
@@ -337,27 +337,29 @@ class TauEngine:
         return cs
 
     def _merge_prepare(self, x, res: PairResult, st):
-        """K1 presort of every variable (u-order positions, sorted ranks, n1, largest tie group)."""
+        """K1 presort of every variable (u-order positions, sorted ranks, min-rank merge keys, n1,
+        tie groups)."""
         m, n = res.m, res.n
         if x.dtype != torch.int32:
             raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
         pos = self._buf("pos", m * n, torch.int32)
         srt = self._buf("sorted", m * n, torch.int32)
+        keys = self._buf("mkeys", m * n, torch.int16)
         work = self._buf("work", m * n, torch.int32)
         maxgrp = self._buf("maxgrp", m, torch.int32)
         ngroups = self._buf("ngroups", m, torch.int32)
-        _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp),
-                  _ptr(work), _ptr(ngroups), _ptr(res.flags), st)
-        return pos, srt, (maxgrp, work, ngroups)
+        _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(keys), _ptr(res.n1_rows),
+                  _ptr(maxgrp), _ptr(work), _ptr(ngroups), _ptr(res.flags), st)
+        return pos, srt, keys, (maxgrp, work, ngroups)
 
     def _merge_path(self, x, res: PairResult, st):
         m, n = res.m, res.n
         x = x.contiguous()
-        pos, srt, (maxgrp, groups, ngroups) = self._merge_prepare(x, res, st)
+        pos, srt, keys, (maxgrp, groups, ngroups) = self._merge_prepare(x, res, st)
         res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
         res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
         self._mark(0)
-        _lib.call("tb_merge_pairs", _ptr(x), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), _ptr(groups),
+        _lib.call("tb_merge_pairs", _ptr(keys), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), _ptr(groups),
                   _ptr(ngroups), m, n,
                   res.job_lo, res.job_hi, _ptr(res.numerator), _ptr(res.n_d), _ptr(res.n3), st)
         self._mark(1)

@@ -220,6 +220,35 @@ def test_gemm_splits_and_shards(eng, oracle, splits):
     _check_full(full, oracle, ranks, full=False)
 
 
+@pytest.mark.parametrize("n", [32769, 40000, 65535, 65536])
+def test_merge_two_halves_vs_oracle(eng, oracle, n):
+    """n > 32768 (two sorted halves, cross inversions from min-rank key sums + the tie scan of the
+    first half): every pair of tie-heavy rows vs the reference's sorted_counts (kernel_sorted.py:195).
+    Rows: 4 and 2 distinct values (runs crossing every thread boundary of the half, the large-group
+    path), a constant row, ascending / descending permutations, ties only in the first half, a
+    random permutation with a few pairs tied."""
+    rng = np.random.default_rng(n)
+    perm = rng.permutation(n)
+    few = perm.copy()
+    few[rng.integers(0, n, 40)] = few[rng.integers(0, n, 40)]
+    head = np.arange(n)
+    head[: n // 2] = rng.integers(0, 3, n // 2)
+    rows = [rng.integers(0, 4, n), rng.integers(0, 2, n), np.zeros(n, np.int64), np.arange(n),
+            np.arange(n)[::-1], head, few, rng.integers(0, 1000, n)]
+    ranks = np.stack([oracle.rank_transform(r) for r in rows])
+    m = ranks.shape[0]
+    res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="merge", full_counts=True).validate()
+    pi, pj = oracle.upper_pairs(m)
+    got_nd = res.n_d.cpu().numpy()
+    got_n3 = res.n3.cpu().numpy()
+    got_num = res.numerator.cpu().numpy()
+    for k, (i, j) in enumerate(zip(pi.tolist(), pj.tolist())):
+        nd, n1, n2, n3 = oracle.sorted_counts(ranks[i], ranks[j])
+        assert (int(got_nd[k]), int(got_n3[k])) == (nd, n3), (n, i, j)
+        assert int(got_num[k]) == oracle.numerator_from_counts(n, nd, n1, n2, n3), (n, i, j)
+    eng.release()
+
+
 def test_merge_shards(eng, oracle):
     from paper_1704_03767_b200.pairindex import job_shard_range
     rng = np.random.default_rng(5)
