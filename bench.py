@@ -430,7 +430,7 @@ def run_ours(args):
     # every rank runs the full host entry point: weak scaling counts each rank's copy, strong scaling
     # (one shared job range) does not shard this leg, so it counts the pairs once
     e2e_pairs = strict_pairs(0, total_jobs) * (world if args.scaling == "weak" else 1)
-    e2e_value = e2e_pairs * len(e2e_times) / e2e_t
+    e2e_value = e2e_pairs * len(e2e_times) / e2e_t if e2e_times else None  # --e2e-steps 0: leg skipped
     h2d = xh.numel() * xh.element_size()
     d2h = total_jobs * 8
 
@@ -500,7 +500,7 @@ def run_ours(args):
                        "outputs": "numerator i32 + tau_a f64 + tau_b f64 in job-id order"},
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / len(e2e_times),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / len(e2e_times) if e2e_times else None,
                     "api": "TauEngine.all_pairs_host (pinned host values in, tau_b f64 for every job id out; "
                            "row bands overlap D2H with compute)", "gpu_launches_per_step": e2e_launches},
             "clocks": clocks, "gpu_launches": launches_per_step * args.steps,

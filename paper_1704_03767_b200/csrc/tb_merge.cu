@@ -255,35 +255,34 @@ __device__ uint32_t sort_count_block(uint16_t* keys, uint16_t* tmp, int L) {
 //
 // Shared-memory traffic of a thread's E keys uses 32-bit words at swizzled addresses: the thread's
 // E/2 words are w = (E/2) t + q and the swizzle (sw, above) makes each of those loads/stores
-// conflict-free across a warp.
+// conflict-free across a warp.  E/2 <= 16 words never leave the 16-word swizzle row of word
+// (E/2) t, so their padded indices are swp_words((E/2) t) + q: one base per thread.
+template <int E>
+__device__ __forceinline__ const uint32_t* run_words(const uint16_t* keys, int t) {
+    static_assert(E / 2 <= 16, "one swizzle row per thread");
+    return reinterpret_cast<const uint32_t*>(keys) + swp_words((E / 2) * t);
+}
 template <int E>
 __device__ __forceinline__ void load_run(const uint16_t* keys, int t, uint32_t (&v)[E]) {
-    const uint32_t* wk = reinterpret_cast<const uint32_t*>(keys);
+    const uint32_t* wk = run_words<E>(keys, t);
 #pragma unroll
     for (int q = 0; q < E / 2; ++q) {
-        const int w = (E / 2) * t + q;
-        const uint32_t word = wk[swp_words(w)];
+        const uint32_t word = wk[q];
         v[2 * q] = word & 0xFFFFu;
         v[2 * q + 1] = word >> 16;
     }
 }
 template <int E>
 __device__ __forceinline__ void store_words(uint16_t* keys, int t, const uint32_t (&ow)[E / 2]) {
-    uint32_t* wk = reinterpret_cast<uint32_t*>(keys);
+    uint32_t* wk = const_cast<uint32_t*>(run_words<E>(keys, t));
 #pragma unroll
-    for (int q = 0; q < E / 2; ++q) {
-        const int w = (E / 2) * t + q;
-        wk[swp_words(w)] = ow[q];
-    }
+    for (int q = 0; q < E / 2; ++q) wk[q] = ow[q];
 }
 template <int E>
 __device__ __forceinline__ void store_run(uint16_t* keys, int t, const uint32_t (&v)[E]) {
-    uint32_t* wk = reinterpret_cast<uint32_t*>(keys);
+    uint32_t* wk = const_cast<uint32_t*>(run_words<E>(keys, t));
 #pragma unroll
-    for (int q = 0; q < E / 2; ++q) {
-        const int w = (E / 2) * t + q;
-        wk[swp_words(w)] = (v[2 * q] & 0xFFFFu) | (v[2 * q + 1] << 16);
-    }
+    for (int q = 0; q < E / 2; ++q) wk[q] = (v[2 * q] & 0xFFFFu) | (v[2 * q + 1] << 16);
 }
 
 // Sort v[0..E) ascending (values are 16-bit keys), returning the strict inversion count.
@@ -328,8 +327,90 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
     return inv;
 }
 
+// Opaque multipliers (1, -1, 2, 4 read from the kernel arguments) keep the bookkeeping on IMAD: ptxas
+// cannot strength-reduce a multiply by an unknown register into ALU shifts / adds.
+struct MgConst {
+    uint32_t one, m1, two, four;
+};
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+
+// Merge-path search with IMAD addressing: s and s + W are multiples of 32, so sw(s + x) =
+// sw(s) + sw(x) and each probe is base + 2 x + 4 (x >> 5).
+__device__ __forceinline__ int mp_search(uint32_t baseA, uint32_t baseB, int d, int W, const MgConst& K) {
+    int lo = d > W ? d - W : 0, hi = d < W ? d : W;
+    const uint32_t dm1 = (uint32_t)(d - 1);
+    while (lo < hi) {  // i = #A among the first d outputs
+        const int mid = (lo + hi) >> 1;
+        const uint32_t x = imad((uint32_t)mid, K.m1, dm1);  // B index d - mid - 1
+        const uint32_t a = lds_u16(imad((uint32_t)mid >> 5, K.four, imad((uint32_t)mid, K.two, baseA)));
+        const uint32_t b = lds_u16(imad(x >> 5, K.four, imad(x, K.two, baseB)));
+        if (a <= b) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// One merge-path level (runs of W -> 2W): thread t merges outputs [d, d + E) of the run pair
+// A = src[s, s + W), B = src[s + W, s + 2W) into registers, then stores them as words.
+// The two run heads are composites (key << 1 | run), run 0 for A and 1 for B: min(h1, h2) is the next
+// output with A first on ties (the reference's order, kernel_sorted.py:72-73), the larger head stays,
+// and the low bit says which run's cursor (ia / ib, absolute indices) advances and reloads.  A run
+// that is used up (its cursor hits s + W or s + 2W) reads as INF.  A B output adds the unconsumed A
+// length s + W - ia, so inv = (#B outputs) (s + W) - sum_B ia.
+// The K4 kernel is bound by the B200 integer pipes (ALU: min/max, LOP3, SEL, ISETP, SHF; FMA: IMAD;
+// each issues one warp instruction per 2 cycles per SMSP), so the cursor and address arithmetic is
+// written as IMADs with opaque multipliers to split the step between the two pipes.
 template <int E>
-__device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L) {
+__device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_t* dst, int t, int W,
+                                                    const MgConst& K) {
+    const int d0 = t * E;
+    const int P = 2 * W;
+    const int s = d0 & ~(P - 1);
+    const int d = d0 - s;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(src);
+    const uint32_t baseA = base + 2u * (uint32_t)sw(s), baseB = base + 2u * (uint32_t)sw(s + W);
+    const int lo = mp_search(baseA, baseB, d, W, K);
+    constexpr uint32_t INF = 0x20000u;
+    const uint32_t sW = (uint32_t)(s + W);
+    uint32_t ia = (uint32_t)(s + lo), ib = sW + (uint32_t)(d - lo);
+    const uint32_t ib0 = ib;
+    uint32_t h1 = ia < sW ? ((uint32_t)src[sw((int)ia)] << 1) : INF;
+    uint32_t h2 = ib < sW + (uint32_t)W ? (((uint32_t)src[sw((int)ib)] << 1) | 1u) : INF;
+    uint32_t Y = 0, prev = 0;
+    uint32_t ow[E / 2];
+#pragma unroll
+    for (int o = 0; o < E; ++o) {
+        const uint32_t cm = min(h1, h2);
+        h1 = max(h1, h2);
+        const uint32_t org = cm & 1u;
+        Y = imad(org, ia, Y);
+        ia = ia + 1u - org;
+        ib = imad(org, K.one, ib);
+        if (o + 1 < E) {
+            const uint32_t idx = org ? ib : ia;
+            const uint32_t addr = imad(idx >> 5, K.four, imad(idx, K.two, base));
+            const uint32_t nv = lds_u16(addr);  // idx <= s + 2W: inside the buffers' 2-key slack
+            const uint32_t end = imad(org, (uint32_t)W, sW);
+            h2 = idx == end ? INF : imad(nv, K.two, org);
+        }
+        if (o & 1) ow[o >> 1] = (prev >> 1) | ((cm >> 1) << 16);
+        else prev = cm;
+    }
+    store_words<E>(dst, t, ow);
+    return (ib - ib0) * sW - Y;
+}
+
+template <int E>
+__device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, const MgConst& K) {
     const int t = threadIdx.x;
     const int active = L / E;  // L is a multiple of E
     uint32_t inv = 0;
@@ -343,37 +424,7 @@ __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L) {
     uint16_t* src = keys;
     uint16_t* dst = tmp;
     for (int W = E; W < L; W <<= 1) {
-        if (t < active) {
-            const int d0 = t * E;
-            const int P = 2 * W;
-            const int s = (d0 / P) * P;  // pair start
-            const int d = d0 - s;        // diagonal inside the pair (W >= E: a thread never spans pairs)
-            int lo = d > W ? d - W : 0, hi = d < W ? d : W;
-            while (lo < hi) {  // merge-path search: i = #A among the first d outputs
-                const int mid = (lo + hi) >> 1;
-                if (src[sw(s + mid)] <= src[sw(s + W + d - mid - 1)]) lo = mid + 1;
-                else hi = mid;
-            }
-            int i = lo, j = d - lo;
-            uint32_t a = src[sw(min(s + i, s + W - 1))];
-            uint32_t b = src[sw(min(s + W + j, s + 2 * W - 1))];
-            uint32_t ow[E / 2];
-#pragma unroll
-            for (int o = 0; o < E; ++o) {
-                const bool takeA = (j >= W) || ((i < W) && (a <= b));
-                const uint32_t val = takeA ? a : b;
-                if (o & 1) ow[o >> 1] |= val << 16;
-                else ow[o >> 1] = val;
-                inv += takeA ? 0u : (uint32_t)(W - i);
-                i += takeA;
-                j += !takeA;
-                const int idx = min(takeA ? (s + i) : (s + W + j), s + 2 * W - 1);  // exhausted runs: value unused
-                const uint32_t nv = src[sw(idx)];
-                a = takeA ? nv : a;
-                b = takeA ? b : nv;
-            }
-            store_words<E>(dst, t, ow);
-        }
+        if (t < active) inv += merge_level_cur<E>(src, dst, t, W, K);
         __syncthreads();
         uint16_t* tt = src;
         src = dst;
@@ -390,12 +441,12 @@ __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L) {
     return inv;
 }
 
-__device__ __forceinline__ uint32_t sort_count_any(uint16_t* keys, uint16_t* tmp, int L) {
-    if (L >= 32 * MG_THREADS) return sort_count_block_v2<32>(keys, tmp, L);
-    if (L >= 16 * MG_THREADS) return sort_count_block_v2<16>(keys, tmp, L);
-    if (L >= 8 * MG_THREADS) return sort_count_block_v2<8>(keys, tmp, L);
-    if (L >= 4 * MG_THREADS) return sort_count_block_v2<4>(keys, tmp, L);
-    if (L >= 2 * MG_THREADS) return sort_count_block_v2<2>(keys, tmp, L);
+__device__ __forceinline__ uint32_t sort_count_any(uint16_t* keys, uint16_t* tmp, int L, const MgConst& K) {
+    if (L >= 32 * MG_THREADS) return sort_count_block_v2<32>(keys, tmp, L, K);
+    if (L >= 16 * MG_THREADS) return sort_count_block_v2<16>(keys, tmp, L, K);
+    if (L >= 8 * MG_THREADS) return sort_count_block_v2<8>(keys, tmp, L, K);
+    if (L >= 4 * MG_THREADS) return sort_count_block_v2<4>(keys, tmp, L, K);
+    if (L >= 2 * MG_THREADS) return sort_count_block_v2<2>(keys, tmp, L, K);
     return sort_count_block(keys, tmp, L);
 }
 
@@ -414,6 +465,7 @@ struct MergeArgs {
     int32_t* num;
     unsigned long long* nd;
     unsigned long long* n3;
+    MgConst k;  // {1, -1, 2, 4}
 };
 
 __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p) {
@@ -425,6 +477,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
     const int64_t n = p.n;
     const int L = p.L;
     const int64_t L1 = p.B == 2 ? L : n;  // real keys in block 0
+    const MgConst K = p.k;
 
     for (int64_t idx = blockIdx.x; idx < p.count; idx += gridDim.x) {
         int64_t y, x;
@@ -482,10 +535,10 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         __syncthreads();
 
         // inv(w)
-        uint32_t inv = sort_count_any(keys, tmp, L);
+        uint32_t inv = sort_count_any(keys, tmp, L, K);
         int64_t cross = 0;
         if (p.B == 2) {
-            inv += sort_count_any(keys + sw(L), tmp, L);  // L = 32768: sw(L + i) = sw(L) + sw(i)
+            inv += sort_count_any(keys + sw(L), tmp, L, K);  // L = 32768: sw(L + i) = sw(L) + sw(i)
             // cross(H1, H2) = sum key(H1) - L1 (L1 - 1) / 2 + ties(H1) (header); the -L1 (L1 - 1) / 2
             // is applied once after the reduction.  H1 = keys[0, L) is sorted and holds no pads.
             constexpr int CE = MG_HALF / MG_THREADS;  // 32 sorted keys per thread
@@ -582,6 +635,7 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
     a.n3 = reinterpret_cast<unsigned long long*>(n3);
     const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> 5) + 2 + L + 2 * ((size_t)L >> 5) + 2;
     size_t smem = padded * sizeof(uint16_t);
+    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u};
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = std::min<int64_t>(a.count, (int64_t)num_sms());
     merge_pairs_kernel<<<(unsigned)grid, MG_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(a);
