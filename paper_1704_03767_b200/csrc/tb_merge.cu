@@ -171,7 +171,10 @@ constexpr int MG_THREADS = 1024;
 constexpr int MG_SMALL_GROUP = 64;  // tie groups up to this size: one thread per group
 constexpr int MG_HALF = 32768;  // largest block sorted in shared memory
 
-// Shared-memory key layout: 2 pad keys (one 32-bit word) after every 32 keys.  Merge-path threads
+// Shared-memory key layout: 2 pad keys (one 32-bit word) after every 32 keys.  The pad word in front
+// of 32-key block k doubles as the merge loop's look-ahead slot (merge_level_cur): its first key holds
+// INF (0xFFFF) when block k starts a run of the level being merged, else a copy of the block's first
+// key.  Data keys stay <= 0xFFFE (pads of a short row are 0xFFFE; key 65535 is clamped, see K4).  Merge-path threads
 // own contiguous output segments, so a warp's cursors sit ~16 keys apart; the padding spreads them
 // (and the per-thread 16-word runs of load_run/store_words, 17 words apart) over all 32 banks.
 // Logical key e lives at padded index e + 2 (e >> 5); word w at w + (w >> 4).
@@ -285,6 +288,17 @@ __device__ __forceinline__ void store_run(uint16_t* keys, int t, const uint32_t 
     for (int q = 0; q < E / 2; ++q) wk[q] = (v[2 * q] & 0xFFFFu) | (v[2 * q + 1] << 16);
 }
 
+// Look-ahead slot of the 32-key block starting at key E t (when one does): INF if that key starts a run of
+// length R (the next level's run length), else a copy of the key (first = the thread's first key word).
+template <int E>
+__device__ __forceinline__ void store_lookahead(uint16_t* keys, int t, int R, uint32_t first) {
+    const int k0 = E * t;
+    if ((k0 & 31) == 0 && k0 > 0) {
+        uint32_t* wk = reinterpret_cast<uint32_t*>(keys) + swp_words(k0 >> 1) - 1;
+        *wk = (k0 & (R - 1)) == 0 ? 0xFFFFFFFFu : (first | 0xFFFF0000u);
+    }
+}
+
 // Sort v[0..E) ascending (values are 16-bit keys), returning the strict inversion count.
 template <int E>
 __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
@@ -369,7 +383,7 @@ __device__ __forceinline__ int mp_search(uint32_t baseA, uint32_t baseB, int d, 
 // The K4 kernel is bound by the B200 integer pipes (ALU: min/max, LOP3, SEL, ISETP, SHF; FMA: IMAD;
 // each issues one warp instruction per 2 cycles per SMSP), so the cursor and address arithmetic is
 // written as IMADs with opaque multipliers to split the step between the two pipes.
-template <int E>
+template <int E, bool CHECKED>
 __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_t* dst, int t, int W,
                                                     const MgConst& K) {
     const int d0 = t * E;
@@ -397,15 +411,27 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
         ib = imad(org, K.one, ib);
         if (o + 1 < E) {
             const uint32_t idx = org ? ib : ia;
-            const uint32_t addr = imad(idx >> 5, K.four, imad(idx, K.two, base));
-            const uint32_t nv = lds_u16(addr);  // idx <= s + 2W: inside the buffers' 2-key slack
-            const uint32_t end = imad(org, (uint32_t)W, sW);
-            h2 = idx == end ? INF : imad(nv, K.two, org);
+            if (CHECKED) {  // runs shorter than a 32-key block: explicit end test
+                const uint32_t addr = imad(idx >> 5, K.four, imad(idx, K.two, base));
+                const uint32_t nv = lds_u16(addr);  // idx <= s + 2W: inside the buffers' 2-key slack
+                const uint32_t end = imad(org, (uint32_t)W, sW);
+                h2 = idx == end ? INF : imad(nv, K.two, org);
+            } else {
+                // W >= 32: every run boundary is a block boundary.  Key idx (idx >= 1) is read at
+                // padded index idx + 2 ((idx - 1) >> 5): inside a block that is the key itself; at a
+                // block start it is the pad slot in front of the block, which holds a copy of the
+                // key -- or INF when idx is the end of the run (the next run's start), so a used-up
+                // run reads as INF (composite >= 0x1FFFE, above every data composite) with no test.
+                const uint32_t c = idx - 1u;
+                const uint32_t addr = imad(c >> 5, K.four, imad(c, K.two, base + 2u));
+                h2 = imad(lds_u16(addr), K.two, org);
+            }
         }
         if (o & 1) ow[o >> 1] = (prev >> 1) | ((cm >> 1) << 16);
         else prev = cm;
     }
     store_words<E>(dst, t, ow);
+    store_lookahead<E>(dst, t, 2 * W, ow[0]);
     return (ib - ib0) * sW - Y;
 }
 
@@ -419,12 +445,16 @@ __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, co
         load_run<E>(keys, t, v);
         inv += reg_sort_count<E>(v);
         store_run<E>(keys, t, v);
+        store_lookahead<E>(keys, t, E, 0u);  // runs of E: every block start is a run start
     }
     __syncthreads();
     uint16_t* src = keys;
     uint16_t* dst = tmp;
     for (int W = E; W < L; W <<= 1) {
-        if (t < active) inv += merge_level_cur<E>(src, dst, t, W, K);
+        if (t < active) {
+            if (W < 32) inv += merge_level_cur<E, true>(src, dst, t, W, K);
+            else inv += merge_level_cur<E, false>(src, dst, t, W, K);
+        }
         __syncthreads();
         uint16_t* tt = src;
         src = dst;
@@ -478,6 +508,13 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
     const int L = p.L;
     const int64_t L1 = p.B == 2 ? L : n;  // real keys in block 0
     const MgConst K = p.k;
+    __shared__ int sX, sY;
+    __shared__ int slo[MG_THREADS];  // per-thread merge-path splits of the current level  // u-order positions of keys 0xFFFF / 0xFFFE (n = 65536 only)
+    if (tid == 0 && L >= 64) {  // INF look-ahead slots behind the last block of every sorted region
+        reinterpret_cast<uint32_t*>(keys)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
+        reinterpret_cast<uint32_t*>(tmp)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
+        if (p.B == 2) reinterpret_cast<uint32_t*>(keys + sw(L))[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
+    }
 
     for (int64_t idx = blockIdx.x; idx < p.count; idx += gridDim.x) {
         int64_t y, x;
@@ -486,9 +523,11 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         const int32_t* su = p.sorted + y * n;   // u ranks in u-order
         const uint16_t* kv = p.keys + x * n;    // v min-rank keys
 
-        // pads (max key: real keys are < n <= 65535 whenever pads exist) first, then scatter
-        // w[pos_u[e]] = key_v[e]
-        for (int64_t i = n + tid; i < (int64_t)p.B * L; i += MG_THREADS) keys[sw((int)i)] = 0xFFFF;
+        // pads (0xFFFE: real keys are < n <= 65535 whenever pads exist, and 0xFFFF is the merge
+        // loop's INF) first, then scatter w[pos_u[e]] = key_v[e]
+        for (int64_t i = n + tid; i < (int64_t)p.B * L; i += MG_THREADS) keys[sw((int)i)] = 0xFFFE;
+        if (tid == 0) sX = sY = -1;
+        __syncthreads();
         if ((n & 3) == 0) {  // 16-byte loads of u-positions, 8-byte loads of v keys
             const int4* pu4 = reinterpret_cast<const int4*>(pu);
             const uint2* kv4 = reinterpret_cast<const uint2*>(kv);
@@ -499,6 +538,16 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
                 keys[sw(P.y)] = (uint16_t)(V.x >> 16);
                 keys[sw(P.z)] = (uint16_t)(V.y & 0xFFFFu);
                 keys[sw(P.w)] = (uint16_t)(V.y >> 16);
+                if (n == 65536 && (V.x >= 0xFFFE0000u || V.y >= 0xFFFE0000u ||
+                                   (V.x & 0xFFFEu) == 0xFFFEu || (V.y & 0xFFFEu) == 0xFFFEu)) {
+                    const int pp[4] = {P.x, P.y, P.z, P.w};
+                    const uint32_t kk[4] = {V.x & 0xFFFFu, V.x >> 16, V.y & 0xFFFFu, V.y >> 16};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (kk[q] == 0xFFFFu) sX = pp[q];
+                        if (kk[q] == 0xFFFEu) sY = pp[q];
+                    }
+                }
             }
         } else {
             for (int64_t e = tid; e < n; e += MG_THREADS) keys[sw(pu[e])] = kv[e];
@@ -534,6 +583,21 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         }
         __syncthreads();
 
+        // n = 65536: key 65535 (a unique row maximum X) would collide with INF.  Sort it as 65534;
+        // that only merges it with a unique second maximum Y (key 65534, if any), so add back the
+        // X-before-Y inversion when both sit in the same half, and undo the change in the H1 key sum
+        // and tie scan of the cross term below.
+        int64_t clamp_fix = 0;
+        if (n == 65536 && sX >= 0) {
+            const bool x1 = sX < L, y1 = sY >= 0 && sY < L;
+            if (tid == 0) {
+                keys[sw(sX)] = 0xFFFE;
+                if (sY >= 0 && x1 == y1 && sX < sY) clamp_fix += 1;
+                if (x1) clamp_fix += 1 - (y1 ? 1 : 0);
+            }
+            __syncthreads();
+        }
+
         // inv(w)
         uint32_t inv = sort_count_any(keys, tmp, L, K);
         int64_t cross = 0;
@@ -566,7 +630,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
             cross = (int64_t)ksum + (int64_t)ties;
         }
 
-        const int64_t tot_inv = block_reduce_sum((int64_t)inv + cross, red) - (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
+        const int64_t tot_inv = block_reduce_sum((int64_t)inv + cross + clamp_fix, red) - (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
         const int64_t tot_g = block_reduce_sum((int64_t)inv_g, red);
         const int64_t tot_t = block_reduce_sum((int64_t)ties, red);
         if (tid == 0) {

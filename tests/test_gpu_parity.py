@@ -249,6 +249,35 @@ def test_merge_two_halves_vs_oracle(eng, oracle, n):
     eng.release()
 
 
+def test_merge_row_maximum_clamp(eng, oracle):
+    """n = 65536: key 65535 (a unique row maximum) is sorted as 65534 (0xFFFF is the merge loop's
+    look-ahead INF) and corrected.  The maximum and a unique second maximum placed in the same half
+    (either order) and in different halves; one row with a tied top pair (no key 65535)."""
+    n = 65536
+    rng = np.random.default_rng(65536)
+    rows = [np.arange(n)]
+    for p1, p2 in ((10, 40000), (40000, 10), (10, 20), (20, 10), (40000, 40010), (40010, 40000)):
+        v = rng.permutation(n - 2)
+        v = np.insert(v, min(p1, p2), -1)
+        v = np.insert(v, max(p1, p2), -1)
+        v[p1], v[p2] = n - 1, n - 2
+        rows.append(v)
+    tied = rng.permutation(n)
+    tied[tied == n - 1] = n - 2
+    rows.append(tied)
+    rows.append(rng.permutation(n))
+    ranks = np.stack([oracle.rank_transform(r) for r in rows])
+    m = ranks.shape[0]
+    res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="merge", full_counts=True).validate()
+    pi, pj = oracle.upper_pairs(m)
+    got_nd = res.n_d.cpu().numpy()
+    got_n3 = res.n3.cpu().numpy()
+    for k, (i, j) in enumerate(zip(pi.tolist(), pj.tolist())):
+        nd, n1, n2, n3 = oracle.sorted_counts(ranks[i], ranks[j])
+        assert (int(got_nd[k]), int(got_n3[k])) == (nd, n3), (i, j)
+    eng.release()
+
+
 def test_merge_shards(eng, oracle):
     from paper_1704_03767_b200.pairindex import job_shard_range
     rng = np.random.default_rng(5)
