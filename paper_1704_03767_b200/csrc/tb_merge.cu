@@ -508,8 +508,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
     const int L = p.L;
     const int64_t L1 = p.B == 2 ? L : n;  // real keys in block 0
     const MgConst K = p.k;
-    __shared__ int sX, sY;
-    __shared__ int slo[MG_THREADS];  // per-thread merge-path splits of the current level  // u-order positions of keys 0xFFFF / 0xFFFE (n = 65536 only)
+    __shared__ int sX, sY;  // u-order positions of keys 0xFFFF / 0xFFFE (n = 65536 only)
     if (tid == 0 && L >= 64) {  // INF look-ahead slots behind the last block of every sorted region
         reinterpret_cast<uint32_t*>(keys)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
         reinterpret_cast<uint32_t*>(tmp)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
