@@ -344,7 +344,7 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
 // Opaque multipliers (1, -1, 2, 4 read from the kernel arguments) keep the bookkeeping on IMAD: ptxas
 // cannot strength-reduce a multiply by an unknown register into ALU shifts / adds.
 struct MgConst {
-    uint32_t one, m1, two, four;
+    uint32_t one, m1, two, four, s16;
 };
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
@@ -375,7 +375,7 @@ __device__ __forceinline__ int mp_search(uint32_t baseA, uint32_t baseB, int d, 
 
 // One merge-path level (runs of W -> 2W): thread t merges outputs [d, d + E) of the run pair
 // A = src[s, s + W), B = src[s + W, s + 2W) into registers, then stores them as words.
-// The two run heads are composites (key << 1 | run), run 0 for A and 1 for B: min(h1, h2) is the next
+// The two run heads are composites (key << 16 | run), run 0 for A and 1 for B: min(h1, h2) is the next
 // output with A first on ties (the reference's order, kernel_sorted.py:72-73), the larger head stays,
 // and the low bit says which run's cursor (ia / ib, absolute indices) advances and reloads.  A run
 // that is used up (its cursor hits s + W or s + 2W) reads as INF.  A B output adds the unconsumed A
@@ -393,12 +393,12 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(src);
     const uint32_t baseA = base + 2u * (uint32_t)sw(s), baseB = base + 2u * (uint32_t)sw(s + W);
     const int lo = mp_search(baseA, baseB, d, W, K);
-    constexpr uint32_t INF = 0x20000u;
+    constexpr uint32_t INF = 0xFFFF0000u;  // above every data composite (keys <= 0xFFFE)
     const uint32_t sW = (uint32_t)(s + W);
     uint32_t ia = (uint32_t)(s + lo), ib = sW + (uint32_t)(d - lo);
     const uint32_t ib0 = ib;
-    uint32_t h1 = ia < sW ? ((uint32_t)src[sw((int)ia)] << 1) : INF;
-    uint32_t h2 = ib < sW + (uint32_t)W ? (((uint32_t)src[sw((int)ib)] << 1) | 1u) : INF;
+    uint32_t h1 = ia < sW ? ((uint32_t)src[sw((int)ia)] << 16) : INF;
+    uint32_t h2 = ib < sW + (uint32_t)W ? (((uint32_t)src[sw((int)ib)] << 16) | 1u) : INF;
     uint32_t Y = 0, prev = 0;
     uint32_t ow[E / 2];
 #pragma unroll
@@ -415,19 +415,19 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
                 const uint32_t addr = imad(idx >> 5, K.four, imad(idx, K.two, base));
                 const uint32_t nv = lds_u16(addr);  // idx <= s + 2W: inside the buffers' 2-key slack
                 const uint32_t end = imad(org, (uint32_t)W, sW);
-                h2 = idx == end ? INF : imad(nv, K.two, org);
+                h2 = idx == end ? INF : imad(nv, K.s16, org);
             } else {
                 // W >= 32: every run boundary is a block boundary.  Key idx (idx >= 1) is read at
                 // padded index idx + 2 ((idx - 1) >> 5): inside a block that is the key itself; at a
                 // block start it is the pad slot in front of the block, which holds a copy of the
                 // key -- or INF when idx is the end of the run (the next run's start), so a used-up
-                // run reads as INF (composite >= 0x1FFFE, above every data composite) with no test.
+                // run reads as INF (composite >= 0xFFFF0000, above every data composite) with no test.
                 const uint32_t c = idx - 1u;
                 const uint32_t addr = imad(c >> 5, K.four, imad(c, K.two, base + 2u));
-                h2 = imad(lds_u16(addr), K.two, org);
+                h2 = imad(lds_u16(addr), K.s16, org);
             }
         }
-        if (o & 1) ow[o >> 1] = (prev >> 1) | ((cm >> 1) << 16);
+        if (o & 1) ow[o >> 1] = __byte_perm(prev, cm, 0x7632);  // the two keys (high halves)
         else prev = cm;
     }
     store_words<E>(dst, t, ow);
@@ -495,7 +495,7 @@ struct MergeArgs {
     int32_t* num;
     unsigned long long* nd;
     unsigned long long* n3;
-    MgConst k;  // {1, -1, 2, 4}
+    MgConst k;  // {1, -1, 2, 4, 65536}
 };
 
 __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p) {
@@ -698,7 +698,7 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
     a.n3 = reinterpret_cast<unsigned long long*>(n3);
     const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> 5) + 2 + L + 2 * ((size_t)L >> 5) + 2;
     size_t smem = padded * sizeof(uint16_t);
-    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u};
+    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u};
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = std::min<int64_t>(a.count, (int64_t)num_sms());
     merge_pairs_kernel<<<(unsigned)grid, MG_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(a);
