@@ -344,7 +344,7 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
 // Opaque multipliers (1, -1, 2, 4 read from the kernel arguments) keep the bookkeeping on IMAD: ptxas
 // cannot strength-reduce a multiply by an unknown register into ALU shifts / adds.
 struct MgConst {
-    uint32_t one, m1, two, four, s16;
+    uint32_t one, m1, two, four, s16, c68, m68;
 };
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
@@ -358,14 +358,28 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
 }
 
 // Merge-path search with IMAD addressing: s and s + W are multiples of 32, so sw(s + x) =
-// sw(s) + sw(x) and each probe is base + 2 x + 4 (x >> 5).
+// sw(s) + sw(x) and each probe is base + 2 x + 4 (x >> 5).  Two phases: first over the block starts
+// i = 32 j only, where both probes are linear in j (A[32 j] at byte 68 j, B[d - 1 - 32 j] at
+// 2 sw(d - 1) - 68 j) -- one IMAD per address; then a plain search of the <= 32-wide bracket.
 __device__ __forceinline__ int mp_search(uint32_t baseA, uint32_t baseB, int d, int W, const MgConst& K) {
-    int lo = d > W ? d - W : 0, hi = d < W ? d : W;
+    const int lo0 = d > W ? d - W : 0, hi0 = d < W ? d : W;
+    int jl = (lo0 + 31) >> 5, jh = (hi0 + 31) >> 5;  // block starts 32 j in [lo0, hi0)
     const uint32_t dm1 = (uint32_t)(d - 1);
+    const uint32_t cB = baseB + 2u * (uint32_t)sw(d - 1);
+    while (jl < jh) {  // first j whose block start 32 j is not among the first d outputs
+        const int mid = (jl + jh) >> 1;
+        const uint32_t a = lds_u16(imad((uint32_t)mid, K.c68, baseA));
+        const uint32_t b = lds_u16(imad((uint32_t)mid, K.m68, cB));
+        if (a <= b) jl = mid + 1;
+        else jh = mid;
+    }
+    int lo = max(lo0, 32 * jl - 31), hi = min(hi0, 32 * jl);
+    // probes mid in [lo, hi) lie inside A block jl - 1: byte 2 mid + 4 (jl - 1)
+    const uint32_t cA = baseA + 4u * (uint32_t)(jl - 1);
     while (lo < hi) {  // i = #A among the first d outputs
         const int mid = (lo + hi) >> 1;
         const uint32_t x = imad((uint32_t)mid, K.m1, dm1);  // B index d - mid - 1
-        const uint32_t a = lds_u16(imad((uint32_t)mid >> 5, K.four, imad((uint32_t)mid, K.two, baseA)));
+        const uint32_t a = lds_u16(imad((uint32_t)mid, K.two, cA));
         const uint32_t b = lds_u16(imad(x >> 5, K.four, imad(x, K.two, baseB)));
         if (a <= b) lo = mid + 1;
         else hi = mid;
@@ -495,7 +509,7 @@ struct MergeArgs {
     int32_t* num;
     unsigned long long* nd;
     unsigned long long* n3;
-    MgConst k;  // {1, -1, 2, 4, 65536}
+    MgConst k;  // {1, -1, 2, 4, 65536, 68, -68}
 };
 
 __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p) {
@@ -698,7 +712,7 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
     a.n3 = reinterpret_cast<unsigned long long*>(n3);
     const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> 5) + 2 + L + 2 * ((size_t)L >> 5) + 2;
     size_t smem = padded * sizeof(uint16_t);
-    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u};
+    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u, 68u, (uint32_t)-68};
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = std::min<int64_t>(a.count, (int64_t)num_sms());
     merge_pairs_kernel<<<(unsigned)grid, MG_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(a);
