@@ -300,16 +300,20 @@ __device__ __forceinline__ void store_lookahead(uint16_t* keys, int t, int R, ui
 }
 
 // Sort v[0..E) ascending (values are 16-bit keys), returning the strict inversion count.
+// Composites key << 5 | i (i = the key's index in the run, E <= 32) are tagged once: stage k merges
+// the two sorted h-runs (h = k / 2) of each aligned k-block, whose elements are exactly those with
+// tags in that block, so an element came from the right run B iff bit log2(h) of its tag is set; and
+// a correct sort of the composites is a stable merge (A first on ties).  The B element of B-rank j at merged position p has h - (p - j) A elements strictly greater:
+// inv(A, B) = h^2 + h(h-1)/2 - sum(positions of B elements).
 template <int E>
 __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
+    static_assert(E <= 32, "5-bit tags");
     uint32_t inv = 0;
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] <<= 1;
+    for (int i = 0; i < E; ++i) v[i] = (v[i] << 5) | (uint32_t)i;
 #pragma unroll
     for (int k = 2; k <= E; k <<= 1) {
         const int h = k / 2;
-#pragma unroll
-        for (int i = 0; i < E; ++i) v[i] = (v[i] & ~1u) | ((i % k) >= h ? 1u : 0u);
         // first stage: compare i with its mirror in the run (turns two ascending runs into halves)
 #pragma unroll
         for (int base = 0; base < E; base += k) {
@@ -331,13 +335,13 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
                 v[i + j] = max(a, b);
             }
         }
-        uint32_t pos = 0;
+        uint32_t pos = 0;  // h * sum of the B positions
 #pragma unroll
-        for (int i = 0; i < E; ++i) pos += (v[i] & 1u) * (uint32_t)(i % k);
-        inv += (uint32_t)(E / k) * (uint32_t)(h * h + h * (h - 1) / 2) - pos;
+        for (int i = 0; i < E; ++i) pos += (v[i] & (uint32_t)h) * (uint32_t)(i % k);
+        inv += (uint32_t)(E / k) * (uint32_t)(h * h + h * (h - 1) / 2) - pos / (uint32_t)h;
     }
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] >>= 1;
+    for (int i = 0; i < E; ++i) v[i] >>= 5;
     return inv;
 }
 
