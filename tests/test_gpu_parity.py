@@ -249,6 +249,25 @@ def test_merge_two_halves_vs_oracle(eng, oracle, n):
     eng.release()
 
 
+@pytest.mark.parametrize("n", [2047, 2048, 4097, 8193, 16384, 20000, 32767, 32768])
+def test_merge_block_sizes_vs_oracle(eng, oracle, n):
+    """One sorted block (n <= 32768) at every per-thread run length E = L / 1024 (2 .. 32): the
+    register leaf, the checked merge levels (runs < 32 keys) and the look-ahead-slot levels, with
+    tie-heavy, tie-free, monotone and constant rows, every pair vs sorted_counts (kernel_sorted.py:195)."""
+    rng = np.random.default_rng(n + 7)
+    rows = [rng.integers(0, 5, n), rng.permutation(n), np.arange(n)[::-1], rng.integers(0, n // 3, n),
+            np.zeros(n, np.int64), rng.integers(0, 2, n)]
+    ranks = np.stack([oracle.rank_transform(r) for r in rows])
+    m = ranks.shape[0]
+    res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="merge", full_counts=True).validate()
+    pi, pj = oracle.upper_pairs(m)
+    got_nd = res.n_d.cpu().numpy()
+    got_n3 = res.n3.cpu().numpy()
+    for k, (i, j) in enumerate(zip(pi.tolist(), pj.tolist())):
+        nd, n1, n2, n3 = oracle.sorted_counts(ranks[i], ranks[j])
+        assert (int(got_nd[k]), int(got_n3[k])) == (nd, n3), (n, i, j)
+
+
 def test_merge_row_maximum_clamp(eng, oracle):
     """n = 65536: key 65535 (a unique row maximum) is sorted as 65534 (0xFFFF is the merge loop's
     look-ahead INF) and corrected.  The maximum and a unique second maximum placed in the same half
