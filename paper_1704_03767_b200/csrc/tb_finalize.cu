@@ -1,9 +1,9 @@
 // K5: fp64 finalize over a contiguous job-id range -- derive_taus
 // (result.py:62-82) on device.  Streaming kernel: reads the int32 numerator
 // (4 B) and writes tau_a/tau_b (8 + 8 B) per pair; per-row tie counts stay in L2.
-// Measured on config 3 (134M pairs): 721 us = 3.7 TB/s effective (57% of HBM),
-// bound by the fp64 div/sqrt chains (tools/exp_fin.py; the per-element job_coord
-// version took 1040 us).
+// Measured on config 3 (134M pairs): 715 us = 3.7 TB/s effective (56% of HBM;
+// ncu: issue 53%, fp64 pipe 30%: latency of the fp64 div/sqrt chains), one cell
+// in flight per thread; now FIN_UNROLL cells per thread.
 //
 // Bit-exactness: tau_a = (double)num / (double)n0 and tau_b = (double)num /
 // sqrt((n0 - n1_y) * (n0 - n1_x)) with IEEE round-to-nearest __ddiv_rn /
@@ -21,6 +21,16 @@ namespace tb {
 constexpr int FIN_THREADS = 256;
 constexpr int FIN_ITERS_MAX = 16;  // cells per thread for large ranges; small ranges use fewer (more CTAs)
 
+constexpr int FIN_UNROLL = 4;  // cells in flight per thread: independent div/sqrt chains overlap
+
+__device__ __forceinline__ void fin_step(int64_t m, int64_t& y, int64_t& x) {  // next cell, 256 ids on
+    x += FIN_THREADS;
+    while (x >= m) {
+        x -= m - (y + 1);
+        ++y;
+    }
+}
+
 __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32_t* __restrict__ num,
                                                                       const unsigned long long* __restrict__ n1,
                                                                       int64_t m, int64_t n0, int64_t job_lo,
@@ -32,23 +42,28 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32
     const int64_t i_end = min(count, (int64_t)(blockIdx.x + 1) * chunk);
     int64_t y, x;
     job_coord(job_lo + i, m, y, x);
-    double ty = dn0 - (double)__ldg(&n1[y]);
-    for (;;) {
-        const double v = (double)num[i];
-        if (tau_a) tau_a[i] = __ddiv_rn(v, dn0);
-        if (tau_b) {
-            const double denom = __dsqrt_rn(__dmul_rn(ty, dn0 - (double)__ldg(&n1[x])));
-            tau_b[i] = denom > 0.0 ? __ddiv_rn(v, denom) : __longlong_as_double(0x7ff8000000000000LL);
+    for (; i < i_end; i += FIN_UNROLL * FIN_THREADS) {
+        // FIN_UNROLL cells 256 ids apart: loads and row/column tie counts first, then the IEEE sequences
+        double v[FIN_UNROLL], t[FIN_UNROLL];
+        bool ok[FIN_UNROLL];
+#pragma unroll
+        for (int u = 0; u < FIN_UNROLL; ++u) {
+            const int64_t iu = i + (int64_t)u * FIN_THREADS;
+            ok[u] = iu < i_end;
+            if (u > 0 && ok[u]) fin_step(m, y, x);  // only walk to cells that exist (no row past m - 1)
+            v[u] = ok[u] ? (double)num[iu] : 0.0;
+            t[u] = ok[u] ? __dmul_rn(dn0 - (double)__ldg(&n1[y]), dn0 - (double)__ldg(&n1[x])) : 1.0;
         }
-        i += FIN_THREADS;
-        if (i >= i_end) break;
-        x += FIN_THREADS;
-        if (x >= m) {
-            do {
-                x -= m - (y + 1);
-                ++y;
-            } while (x >= m);
-            ty = dn0 - (double)__ldg(&n1[y]);
+        if (i + FIN_UNROLL * FIN_THREADS < i_end) fin_step(m, y, x);
+#pragma unroll
+        for (int u = 0; u < FIN_UNROLL; ++u) {
+            if (!ok[u]) continue;
+            const int64_t iu = i + (int64_t)u * FIN_THREADS;
+            if (tau_a) tau_a[iu] = __ddiv_rn(v[u], dn0);
+            if (tau_b) {
+                const double denom = __dsqrt_rn(t[u]);
+                tau_b[iu] = denom > 0.0 ? __ddiv_rn(v[u], denom) : __longlong_as_double(0x7ff8000000000000LL);
+            }
         }
     }
 }
