@@ -423,24 +423,38 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
     for (int o = 0; o < E; ++o) {
         const uint32_t cm = min(h1, h2);
         h1 = max(h1, h2);
-        const uint32_t org = cm & 1u;
-        Y = imad(org, ia, Y);
-        ia = ia + 1u - org;
-        ib = imad(org, K.one, ib);
-        if (o + 1 < E) {
-            const uint32_t idx = org ? ib : ia;
-            if (CHECKED) {  // runs shorter than a 32-key block: explicit end test
+        if constexpr (CHECKED) {  // runs shorter than a 32-key block: explicit end test
+            const uint32_t org = cm & 1u;
+            Y = imad(org, ia, Y);
+            ia = ia + 1u - org;
+            ib = imad(org, K.one, ib);
+            if (o + 1 < E) {
+                const uint32_t idx = org ? ib : ia;
                 const uint32_t addr = imad(idx >> 5, K.four, imad(idx, K.two, base));
                 const uint32_t nv = lds_u16(addr);  // idx <= s + 2W: inside the buffers' 2-key slack
                 const uint32_t end = imad(org, (uint32_t)W, sW);
                 h2 = idx == end ? INF : imad(nv, K.s16, org);
-            } else {
-                // W >= 32: every run boundary is a block boundary.  Key idx (idx >= 1) is read at
-                // padded index idx + 2 ((idx - 1) >> 5): inside a block that is the key itself; at a
-                // block start it is the pad slot in front of the block, which holds a copy of the
-                // key -- or INF when idx is the end of the run (the next run's start), so a used-up
-                // run reads as INF (composite >= 0xFFFF0000, above every data composite) with no test.
-                const uint32_t c = idx - 1u;
+            }
+        } else {
+            // W >= 32: every run boundary is a block boundary.  Key idx (idx >= 1) is read at padded
+            // index idx + 2 ((idx - 1) >> 5): inside a block that is the key itself; at a block start
+            // it is the pad slot in front of the block, which holds a copy of the key -- or INF when
+            // idx is the end of the run (the next run's start), so a used-up run reads as INF
+            // (composite >= 0xFFFF0000, above every data composite) with no test.  The key after the
+            // consumed one is idx = old cursor + 1, i.e. c = idx - 1 = the old cursor of the run
+            // taken.  Both cursor advances are predicated IMADs, keeping them off the ALU pipe.
+            uint32_t org, c;
+            asm("{\n\t.reg .pred p;\n\t"
+                "and.b32 %0, %5, 1;\n\t"
+                "setp.ne.u32 p, %0, 0;\n\t"
+                "mad.lo.u32 %3, %0, %1, %3;\n\t"  // Y += org * ia (ia unchanged by a B output)
+                "selp.b32 %4, %2, %1, p;\n\t"      // c = old cursor of the run taken
+                "@!p mad.lo.u32 %1, %6, %6, %1;\n\t"
+                "@p mad.lo.u32 %2, %6, %6, %2;\n\t"
+                "}"
+                : "=r"(org), "+r"(ia), "+r"(ib), "+r"(Y), "=r"(c)
+                : "r"(cm), "r"(K.one));
+            if (o + 1 < E) {
                 const uint32_t addr = imad(c >> 5, K.four, imad(c, K.two, base + 2u));
                 h2 = imad(lds_u16(addr), K.s16, org);
             }
