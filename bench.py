@@ -301,10 +301,19 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, local, world = dist_env()
+    # TB_BENCH_SHARE_GPU=1 (plumbing check only, never a measurement): ranks share the visible GPUs and
+    # talk over gloo, so the N > 1 code path can be exercised on a one-GPU box
+    share = os.environ.get("TB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if share else dev  # all_reduce tensors live where the backend wants them
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_1704_03767_b200 import _lib
     from paper_1704_03767_b200.device import TauEngine
@@ -397,7 +406,7 @@ def run_ours(args):
     gemm_avg = sum(gemm_s) / len(gemm_s)
     t_max = t_total
     if world > 1:
-        tt = torch.tensor([t_total], device=dev, dtype=torch.float64)
+        tt = torch.tensor([t_total], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     total_pairs = my_pairs * world
@@ -424,7 +433,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_t = sum(s.elapsed_time(e) for s, e in e2e_times) / 1e3
     if world > 1:
-        tt = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+        tt = torch.tensor([e2e_t], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_t = float(tt.item())
     # every rank runs the full host entry point: weak scaling counts each rank's copy, strong scaling
