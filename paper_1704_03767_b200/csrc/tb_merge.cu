@@ -300,17 +300,27 @@ __device__ __forceinline__ void store_lookahead(uint16_t* keys, int t, int R, ui
 }
 
 // Sort v[0..E) ascending (values are 16-bit keys), returning the strict inversion count.
-// Composites key << 5 | i (i = the key's index in the run, E <= 32) are tagged once: stage k merges
-// the two sorted h-runs (h = k / 2) of each aligned k-block, whose elements are exactly those with
-// tags in that block, so an element came from the right run B iff bit log2(h) of its tag is set; and
-// a correct sort of the composites is a stable merge (A first on ties).  The B element of B-rank j at merged position p has h - (p - j) A elements strictly greater:
-// inv(A, B) = h^2 + h(h-1)/2 - sum(positions of B elements).
-template <int E>
+// Composites key << (5 + XL) | g << 5 | i (i = the key's index in the thread's run, E <= 32; g = the
+// thread's index in its group of 2^XL lanes) are tagged once: stage k merges the two sorted h-runs
+// (h = k / 2) of each aligned k-block, whose elements are exactly those with tags in that block, so an
+// element came from the right run B iff bit log2(h) of its tag is set; and a correct sort of the
+// composites is a stable merge (A first on ties).  The B element of B-rank j at merged position p has
+// h - (p - j) A elements strictly greater: inv(A, B) = h^2 + h(h-1)/2 - sum(positions of B elements).
+// XL levels beyond the thread's 32 keys run across the lanes of the group (E = 32): a merged block of
+// 64 / 128 keys spans 2 / 4 lanes, its mirror stage pairs register i of lane g with register 31 - i of
+// lane g ^ (2^l - 1) (one xor shuffle), the 128-block's distance-32 stage pairs lane g with g ^ 1, and the
+// remaining stages are the in-register half-cleaners.  Lower lanes keep the minimum.
+__device__ __forceinline__ uint32_t mnmx(uint32_t a, uint32_t b, bool lower) { return lower ? min(a, b) : max(a, b); }
+
+template <int E, int XL = 0>
 __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
-    static_assert(E <= 32, "5-bit tags");
+    static_assert(E <= 32, "5-bit run index");
+    static_assert(XL == 0 || E == 32, "cross-lane levels need full 32-key runs");
+    constexpr int TB = 5 + XL;  // tag bits
+    const uint32_t g = (uint32_t)(threadIdx.x & ((1 << XL) - 1));
     uint32_t inv = 0;
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = (v[i] << 5) | (uint32_t)i;
+    for (int i = 0; i < E; ++i) v[i] = (v[i] << TB) | (g << 5) | (uint32_t)i;
 #pragma unroll
     for (int k = 2; k <= E; k <<= 1) {
         const int h = k / 2;
@@ -341,7 +351,51 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
         inv += (uint32_t)(E / k) * (uint32_t)(h * h + h * (h - 1) / 2) - pos / (uint32_t)h;
     }
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] >>= 5;
+    for (int l = 1; l <= XL; ++l) {  // cross-lane level: blocks of 32 << l keys over 2^l lanes
+        const uint32_t gl = g & ((1u << l) - 1);  // lane within the block
+        {  // mirror stage: lane gl <-> lane gl ^ (2^l - 1), register i <-> 31 - i
+            const bool lower = gl < (1u << (l - 1));
+            const int mask = (1 << l) - 1;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t a = __shfl_xor_sync(0xffffffffu, v[31 - i], mask);
+                const uint32_t b = __shfl_xor_sync(0xffffffffu, v[i], mask);
+                v[i] = mnmx(v[i], a, lower);
+                v[31 - i] = mnmx(v[31 - i], b, lower);
+            }
+        }
+        if (l == 2) {  // distance 32: lane gl <-> gl ^ 1, same register
+            const bool lower = (gl & 1u) == 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = mnmx(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1), lower);
+        }
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (i & j) continue;
+                const uint32_t a = v[i], b = v[i + j];
+                v[i] = min(a, b);
+                v[i + j] = max(a, b);
+            }
+        }
+        // this lane's share of inv(A, B), h = 16 << l: B = tag bit 4 + l; positions 32 gl + i.  Lanes other
+        // than the block's first add only -pos: a thread's total can be negative (the kernel reduces it as
+        // int32; the block total is exact)
+        const uint32_t hb = 16u << l, tb = 1u << (4 + l);
+        uint32_t pos = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pos += (v[i] & tb) * (uint32_t)i;
+        pos /= tb;
+        uint32_t nbv = 0;  // B elements held by this lane
+#pragma unroll
+        for (int i = 0; i < 32; ++i) nbv += (v[i] & tb);
+        nbv /= tb;
+        pos += 32u * gl * nbv;
+        inv += (gl == 0 ? hb * hb + hb * (hb - 1) / 2 : 0u) - pos;
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] >>= TB;
     return inv;
 }
 
@@ -468,6 +522,9 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
 }
 
 template <int E>
+constexpr int LEAF_XL = E == 32 ? 2 : 0;  // register leaf: 32 keys per lane, 128 across 4 lanes
+
+template <int E>
 __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, const MgConst& K) {
     const int t = threadIdx.x;
     const int active = L / E;  // L is a multiple of E
@@ -475,14 +532,14 @@ __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, co
     if (t < active) {
         uint32_t v[E];
         load_run<E>(keys, t, v);
-        inv += reg_sort_count<E>(v);
+        inv += reg_sort_count<E, LEAF_XL<E>>(v);
         store_run<E>(keys, t, v);
-        store_lookahead<E>(keys, t, E, 0u);  // runs of E: every block start is a run start
+        store_lookahead<E>(keys, t, E << LEAF_XL<E>, v[0]);  // INF at leaf-run starts, else a key copy
     }
     __syncthreads();
     uint16_t* src = keys;
     uint16_t* dst = tmp;
-    for (int W = E; W < L; W <<= 1) {
+    for (int W = E << LEAF_XL<E>; W < L; W <<= 1) {
         if (t < active) {
             if (W < 32) inv += merge_level_cur<E, true>(src, dst, t, W, K);
             else inv += merge_level_cur<E, false>(src, dst, t, W, K);
@@ -661,7 +718,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
             cross = (int64_t)ksum + (int64_t)ties;
         }
 
-        const int64_t tot_inv = block_reduce_sum((int64_t)inv + cross + clamp_fix, red) - (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
+        const int64_t tot_inv = block_reduce_sum((int64_t)(int32_t)inv + cross + clamp_fix, red) - (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
         const int64_t tot_g = block_reduce_sum((int64_t)inv_g, red);
         const int64_t tot_t = block_reduce_sum((int64_t)ties, red);
         if (tid == 0) {
