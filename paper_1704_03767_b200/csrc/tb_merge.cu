@@ -307,9 +307,9 @@ __device__ __forceinline__ void store_lookahead(uint16_t* keys, int t, int R, ui
 // composites is a stable merge (A first on ties).  The B element of B-rank j at merged position p has
 // h - (p - j) A elements strictly greater: inv(A, B) = h^2 + h(h-1)/2 - sum(positions of B elements).
 // XL levels beyond the thread's 32 keys run across the lanes of the group (E = 32): a merged block of
-// 64 / 128 keys spans 2 / 4 lanes, its mirror stage pairs register i of lane g with register 31 - i of
-// lane g ^ (2^l - 1) (one xor shuffle), the 128-block's distance-32 stage pairs lane g with g ^ 1, and the
-// remaining stages are the in-register half-cleaners.  Lower lanes keep the minimum.
+// 32 << l keys spans 2^l lanes, its mirror stage pairs register i of lane g with register 31 - i of
+// lane g ^ (2^l - 1) (one xor shuffle), the stages at distances 32 << d (d = l - 2 .. 0) pair lane g with
+// g ^ (1 << d), and the remaining stages are the in-register half-cleaners.  Lower lanes keep the minimum.
 __device__ __forceinline__ uint32_t mnmx(uint32_t a, uint32_t b, bool lower) { return lower ? min(a, b) : max(a, b); }
 
 template <int E, int XL = 0>
@@ -364,10 +364,11 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
                 v[31 - i] = mnmx(v[31 - i], b, lower);
             }
         }
-        if (l == 2) {  // distance 32: lane gl <-> gl ^ 1, same register
-            const bool lower = (gl & 1u) == 0;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = mnmx(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1), lower);
+        for (int d = l - 2; d >= 0; --d) {  // distances 32 << d: lane gl <-> gl ^ (1 << d), same register
+            const bool lower = (gl & (1u << d)) == 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = mnmx(v[i], __shfl_xor_sync(0xffffffffu, v[i], 1 << d), lower);
         }
 #pragma unroll
         for (int j = 16; j > 0; j >>= 1) {
@@ -522,7 +523,7 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
 }
 
 template <int E>
-constexpr int LEAF_XL = E == 32 ? 2 : 0;  // register leaf: 32 keys per lane, 128 across 4 lanes
+constexpr int LEAF_XL = E == 32 ? 2 : 0;  // measured: 1 -> 319.5 ms, 2 -> 315.5 ms, 3 -> 328.5 ms (config 4)  // register leaf: 32 keys per lane, 128 across 4 lanes
 
 template <int E>
 __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, const MgConst& K) {
