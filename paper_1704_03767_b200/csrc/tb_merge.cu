@@ -523,7 +523,9 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
 }
 
 template <int E>
-constexpr int LEAF_XL = E == 32 ? 2 : 0;  // measured: 1 -> 319.5 ms, 2 -> 315.5 ms, 3 -> 328.5 ms (config 4)  // register leaf: 32 keys per lane, 128 across 4 lanes
+// register leaf: 32 keys per lane, 128 across 4 lanes (cross-lane levels measured on config 4:
+// 1 -> 319.5 ms, 2 -> 315.5 ms, 3 -> 328.5 ms)
+constexpr int LEAF_XL = E == 32 ? 2 : 0;
 
 template <int E>
 __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, const MgConst& K) {
