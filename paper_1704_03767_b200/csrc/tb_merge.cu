@@ -310,6 +310,47 @@ __device__ __forceinline__ void store_lookahead(uint16_t* keys, int t, int R, ui
 // 32 << l keys spans 2^l lanes, its mirror stage pairs register i of lane g with register 31 - i of
 // lane g ^ (2^l - 1) (one xor shuffle), the stages at distances 32 << d (d = l - 2 .. 0) pair lane g with
 // g ^ (1 << d), and the remaining stages are the in-register half-cleaners.  Lower lanes keep the minimum.
+// Batcher's odd-even merge of the sorted halves of v[LO, LO + N) (stride R): 191 compare-exchanges for a
+// 32-key sort against the bitonic network's 240 (the leaf is min/max-bound on the ALU pipe).
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+template <int LO, int N, int R, int E>
+__device__ __forceinline__ void oe_merge(uint32_t (&v)[E]) {
+    constexpr int M = 2 * R;
+    if constexpr (M < N) {
+        oe_merge<LO, N, M>(v);
+        oe_merge<LO + R, N, M>(v);
+#pragma unroll
+        for (int i = LO + R; i + R < LO + N; i += M) cswap(v[i], v[i + R]);
+    } else {
+        cswap(v[LO], v[LO + R]);
+    }
+}
+template <int K, int B, int E>
+__device__ __forceinline__ void oe_blocks(uint32_t (&v)[E]) {
+    if constexpr (B < E) {
+        oe_merge<B, K, 1>(v);
+        oe_blocks<K, B + K>(v);
+    }
+}
+// In-register levels k = K .. E: merge the sorted halves of every aligned k-block, then add this
+// level's inversions from the tag bit log2(k / 2) (see reg_sort_count).
+template <int K, int E>
+__device__ __forceinline__ void reg_stages(uint32_t (&v)[E], uint32_t& inv) {
+    if constexpr (K <= E) {
+        constexpr int h = K / 2;
+        oe_blocks<K, 0>(v);
+        uint32_t pos = 0;  // h * sum of the B positions
+#pragma unroll
+        for (int i = 0; i < E; ++i) pos += (v[i] & (uint32_t)h) * (uint32_t)(i % K);
+        inv += (uint32_t)(E / K) * (uint32_t)(h * h + h * (h - 1) / 2) - pos / (uint32_t)h;
+        reg_stages<2 * K, E>(v, inv);
+    }
+}
+
 __device__ __forceinline__ uint32_t mnmx(uint32_t a, uint32_t b, bool lower) { return lower ? min(a, b) : max(a, b); }
 
 template <int E, int XL = 0>
@@ -321,35 +362,7 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
     uint32_t inv = 0;
 #pragma unroll
     for (int i = 0; i < E; ++i) v[i] = (v[i] << TB) | (g << 5) | (uint32_t)i;
-#pragma unroll
-    for (int k = 2; k <= E; k <<= 1) {
-        const int h = k / 2;
-        // first stage: compare i with its mirror in the run (turns two ascending runs into halves)
-#pragma unroll
-        for (int base = 0; base < E; base += k) {
-#pragma unroll
-            for (int i = 0; i < h; ++i) {
-                const uint32_t a = v[base + i], b = v[base + k - 1 - i];
-                v[base + i] = min(a, b);
-                v[base + k - 1 - i] = max(a, b);
-            }
-        }
-        // half-cleaners
-#pragma unroll
-        for (int j = h / 2; j > 0; j >>= 1) {
-#pragma unroll
-            for (int i = 0; i < E; ++i) {
-                if (i & j) continue;
-                const uint32_t a = v[i], b = v[i + j];
-                v[i] = min(a, b);
-                v[i + j] = max(a, b);
-            }
-        }
-        uint32_t pos = 0;  // h * sum of the B positions
-#pragma unroll
-        for (int i = 0; i < E; ++i) pos += (v[i] & (uint32_t)h) * (uint32_t)(i % k);
-        inv += (uint32_t)(E / k) * (uint32_t)(h * h + h * (h - 1) / 2) - pos / (uint32_t)h;
-    }
+    reg_stages<2, E>(v, inv);
 #pragma unroll
     for (int l = 1; l <= XL; ++l) {  // cross-lane level: blocks of 32 << l keys over 2^l lanes
         const uint32_t gl = g & ((1u << l) - 1);  // lane within the block
