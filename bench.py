@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--gather", action="store_true",
+                    help="strong scaling: all-gather every rank's tau_b shard inside the timed step "
+                         "(multi.gather_shards: NCCL all_gather over NVLink)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay the device step as one CUDA graph (auto: config 1, whose step is launch-bound)")
@@ -345,6 +348,10 @@ def run_ours(args):
     # instrumented step: events around the GEMM (dominant kernel) on the launching stream
     gemm_events = []
 
+    gather = args.gather and args.scaling == "strong" and world > 1
+    if gather:
+        from paper_1704_03767_b200.multi import gather_shards
+
     def step(instrument=False):
         with torch.cuda.stream(stream):
             if instrument:
@@ -354,6 +361,11 @@ def run_ours(args):
                 gemm_events.append((s, e))
             else:
                 res = eng.all_pairs(xd, kernel=path, job_range=job_range, stream=stream)
+            if gather:  # the only collective of the path: tau_b shards -> every rank (stream-ordered)
+                tb = res.tau_b if not share else res.tau_b.cpu()
+                full = gather_shards(tb, m)
+                if rank == 0:
+                    res.extra["tau_b_full"] = full
         return res
 
     for _ in range(args.warmup):
@@ -399,6 +411,13 @@ def run_ours(args):
     if graph is not None:
         res = res_graph
         res.validate()
+    gather_check = None
+    if gather and rank == 0:  # the gathered stream equals one device computing every job id
+        full_ref = eng.all_pairs(xd, kernel=path, stream=stream)
+        torch.cuda.synchronize()
+        got = res.extra["tau_b_full"].to(dev)
+        gather_check = bool(torch.equal(got.view(torch.int64), full_ref.tau_b.view(torch.int64)))
+        del full_ref, got
     if world > 1:
         dist.barrier()
     t_total = sum(s.elapsed_time(e) for s, e in times) / 1e3
@@ -506,7 +525,8 @@ def run_ours(args):
                        "pairs_per_rank": my_pairs, "path": path,
                        "l2": "flushed before every timed step (256 MiB write, untimed)",
                        "step": "one CUDA graph replay" if use_graph else "eager launches",
-                       "outputs": "numerator i32 + tau_a f64 + tau_b f64 in job-id order"},
+                       "outputs": "numerator i32 + tau_a f64 + tau_b f64 in job-id order"
+                       + ("; tau_b shards all-gathered to every rank inside the step" if gather else "")},
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / len(e2e_times) if e2e_times else None,
@@ -515,6 +535,8 @@ def run_ours(args):
             "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
             "abi": _lib.TB_MAX_N and "libtaub200.so",
         }
+        if gather:
+            out["gather_check"] = gather_check
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
