@@ -23,7 +23,9 @@ K5 fp64 finalize (tau_a, tau_b).
 (oracle port: the reference is Python/numba and does not travel to the box).
 Multi-GPU (torchrun): every rank computes its own copy of the workload
 (independent objects, no collective) -> "scaling": "weak"; ``--scaling strong``
-shards the job-id range instead (contiguous shards concatenate, pairindex.py:68-80).
+shards the job-id range instead (contiguous shards concatenate, pairindex.py:68-80);
+``--gather`` adds the path's only collective (all-gather of the tau_b shards) to every
+timed strong-scaling step.
 """
 
 from __future__ import annotations
