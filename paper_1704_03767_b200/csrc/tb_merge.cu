@@ -244,15 +244,14 @@ __device__ uint32_t sort_count_block(uint16_t* keys, uint16_t* tmp, int L) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// K4 v2 sort-and-count.  Thread t owns keys [E t, E t + E) of the block.
+// K4 sort-and-count.  Thread t owns keys [E t, E t + E) of the block.
 //
-// Level 1..log2(E) (runs up to E keys) run in registers: bitonic merges of composite keys
-// (key << 1 | origin), origin 0 for the left run A and 1 for the right run B of each merge.  A
-// correct sort of the composites is a stable merge with A first on ties, so the B element of
-// B-rank j at merged position p has exactly h - (p - j) A elements strictly greater than it:
+// The leaf (reg_sort_count) sorts the thread's E keys in registers with tagged composites -- odd-even
+// merge levels for runs up to E, then (E = 32) two cross-lane bitonic levels over groups of 4 lanes
+// (runs of 128) -- and counts each level's inversions from the positions of the right-run elements:
 // inv(A, B) = h^2 + h(h-1)/2 - sum(positions of B elements)   (h = run length).
 //
-// Levels log2(E)+1 .. log2(L) are merge-path merges: each thread merges its E outputs into
+// The remaining levels are merge-path merges: each thread merges its E outputs into
 // registers (statically indexed, fully unrolled) counting the reference's way (right element
 // strictly smaller => + unconsumed left length, kernel_sorted.py:72-73), then writes them back.
 //
