@@ -257,7 +257,7 @@ class TauEngine:
         return cuts
 
     def all_pairs_host(self, x_host: torch.Tensor, tau_b_out: torch.Tensor, kernel: str = "auto",
-                       band_fracs: tuple = (0.65, 0.25, 0.10), stream: torch.cuda.Stream | None = None,
+                       band_fracs: tuple | None = None, stream: torch.cuda.Stream | None = None,
                        copy_stream: torch.cuda.Stream | None = None, h2d_chunks: int = 2,
                        h2d_piece_bytes: int = 4 << 20) -> PairResult:
         """End-to-end from host buffers: H2D of the values, the device path, tau_b back to host.
@@ -309,6 +309,10 @@ class TauEngine:
                 for _, _, ev in chunks:
                     st_t.wait_event(ev)
                 pos, srt, keys, maxgrp = self._merge_prepare(x, res, st)
+            if band_fracs is None:
+                # measured (tools/exp_e2e_bands.py): two bands for small jobs (config 2: 0.850 ms vs 0.876 ms
+                # with three), three when the tau_b copy dominates (config 3: 24.7 ms vs 24.9 ms with two)
+                band_fracs = (0.7, 0.3) if total <= (8 << 20) else (0.65, 0.25, 0.10)
             cuts = self.bands(m, len(band_fracs), fracs=band_fracs)
             for r0, r1 in zip(cuts[:-1], cuts[1:]):
                 lo, hi = r0 * (2 * m - r0 + 1) // 2, r1 * (2 * m - r1 + 1) // 2

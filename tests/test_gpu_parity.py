@@ -386,9 +386,11 @@ def test_sign_formats_agree(eng, k):
     eng.release()
 
 
+@pytest.mark.parametrize("fracs", [None, (0.4, 0.3, 0.2, 0.1)])
 @pytest.mark.parametrize("path,m,n", [("gemm", 2048, 1000), ("gemm", 700, 90), ("merge", 60, 3000)])
-def test_host_entry_point_bands(eng, oracle, path, m, n):
-    """all_pairs_host (pinned host in, tau_b out, row bands overlapping D2H) == the device API."""
+def test_host_entry_point_bands(eng, oracle, path, m, n, fracs):
+    """all_pairs_host (pinned host in, tau_b out, row bands overlapping D2H) == the device API, with the
+    default (size-dependent) bands and an explicit four-band split."""
     rng = np.random.default_rng(m + n)
     x = rng.integers(0, max(2, n // 3), (m, n)).astype(np.int32)
     if path == "merge":
@@ -396,7 +398,7 @@ def test_host_entry_point_bands(eng, oracle, path, m, n):
     xh = torch.from_numpy(x).pin_memory()
     total = m * (m + 1) // 2
     out = torch.full((total,), -7.0, dtype=torch.float64).pin_memory()
-    eng.all_pairs_host(xh, out, kernel=path, band_fracs=(0.4, 0.3, 0.2, 0.1), h2d_chunks=3)
+    eng.all_pairs_host(xh, out, kernel=path, band_fracs=fracs, h2d_chunks=3)
     torch.cuda.synchronize()
     ref = eng.all_pairs(torch.from_numpy(x).cuda(), kernel=path, tau_a=False).validate()
     np.testing.assert_array_equal(out.numpy(), ref.tau_b.cpu().numpy())

@@ -1,0 +1,27 @@
+"""Config-2 end-to-end time (all_pairs_host, pinned host buffers, L2 flushed) vs row-band fractions."""
+import os, sys, statistics, torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, ROOT)
+from paper_1704_03767_b200 import workloads
+from paper_1704_03767_b200.device import TauEngine
+eng = TauEngine(0)
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+xh = torch.from_numpy(workloads.generate(cfg)).pin_memory()
+m = xh.shape[0]
+out = torch.empty(m * (m + 1) // 2, dtype=torch.float64).pin_memory()
+flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
+st = torch.cuda.Stream()
+for fr in ((0.65, 0.25, 0.10), (0.8, 0.2), (0.85, 0.15), (0.9, 0.1), (0.8, 0.15, 0.05), (0.75, 0.2, 0.05),
+           (0.85, 0.1, 0.05), (0.7, 0.3)):
+    ts = []
+    for it in range(12):
+        with torch.cuda.stream(st):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(st)
+            r = eng.all_pairs_host(xh, out, band_fracs=fr, stream=st)
+            e.record(st)
+        torch.cuda.synchronize()
+        if it >= 2:
+            ts.append(s.elapsed_time(e))
+        del r
+    print(f"bands {fr}: median {statistics.median(ts):.3f} ms  min {min(ts):.3f}", flush=True)
