@@ -170,6 +170,9 @@ __global__ void __launch_bounds__(256) tie_groups_kernel(const int32_t* __restri
 constexpr int MG_THREADS = 1024;
 constexpr int MG_SMALL_GROUP = 64;  // tie groups up to this size: one thread per group
 constexpr int MG_HALF = 32768;  // largest block sorted in shared memory
+#ifndef MG_PAD_SHIFT  // pad-block size 2^MG_PAD_SHIFT keys (config 4: 32 -> 310 ms, 64 -> 313 ms)
+#define MG_PAD_SHIFT 5
+#endif
 
 // Shared-memory key layout: 2 pad keys (one 32-bit word) after every 32 keys.  The pad word in front
 // of 32-key block k doubles as the merge loop's look-ahead slot (merge_level_cur): its first key holds
@@ -178,8 +181,10 @@ constexpr int MG_HALF = 32768;  // largest block sorted in shared memory
 // own contiguous output segments, so a warp's cursors sit ~16 keys apart; the padding spreads them
 // (and the per-thread 16-word runs of load_run/store_words, 17 words apart) over all 32 banks.
 // Logical key e lives at padded index e + 2 (e >> 5); word w at w + (w >> 4).
-__device__ __forceinline__ int sw(int e) { return e + ((e >> 5) << 1); }
-__device__ __forceinline__ int swp_words(int w) { return w + (w >> 4); }
+constexpr int PBS = MG_PAD_SHIFT;  // log2 of the keys per padded block
+constexpr int PB = 1 << PBS;        // keys per padded block (2 pad keys = one word after each)
+__device__ __forceinline__ int sw(int e) { return e + ((e >> PBS) << 1); }
+__device__ __forceinline__ int swp_words(int w) { return w + (w >> (PBS - 1)); }
 
 // Branch-free sequential merge of `count` outputs of the runs A = src[s, s+W), B = src[s+W, s+2W)
 // starting from (i, j); returns the strict-inversion contribution (kernel_sorted.py:72-73 rule:
@@ -261,7 +266,7 @@ __device__ uint32_t sort_count_block(uint16_t* keys, uint16_t* tmp, int L) {
 // (E/2) t, so their padded indices are swp_words((E/2) t) + q: one base per thread.
 template <int E>
 __device__ __forceinline__ const uint32_t* run_words(const uint16_t* keys, int t) {
-    static_assert(E / 2 <= 16, "one swizzle row per thread");
+    static_assert(E / 2 <= PB / 2, "one swizzle row per thread");
     return reinterpret_cast<const uint32_t*>(keys) + swp_words((E / 2) * t);
 }
 template <int E>
@@ -292,7 +297,7 @@ __device__ __forceinline__ void store_run(uint16_t* keys, int t, const uint32_t 
 template <int E>
 __device__ __forceinline__ void store_lookahead(uint16_t* keys, int t, int R, uint32_t first) {
     const int k0 = E * t;
-    if ((k0 & 31) == 0 && k0 > 0) {
+    if ((k0 & (PB - 1)) == 0 && k0 > 0) {
         uint32_t* wk = reinterpret_cast<uint32_t*>(keys) + swp_words(k0 >> 1) - 1;
         *wk = (k0 & (R - 1)) == 0 ? 0xFFFFFFFFu : (first | 0xFFFF0000u);
     }
@@ -434,7 +439,7 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
 // 2 sw(d - 1) - 68 j) -- one IMAD per address; then a plain search of the <= 32-wide bracket.
 __device__ __forceinline__ int mp_search(uint32_t baseA, uint32_t baseB, int d, int W, const MgConst& K) {
     const int lo0 = d > W ? d - W : 0, hi0 = d < W ? d : W;
-    int jl = (lo0 + 31) >> 5, jh = (hi0 + 31) >> 5;  // block starts 32 j in [lo0, hi0)
+    int jl = (lo0 + PB - 1) >> PBS, jh = (hi0 + PB - 1) >> PBS;  // block starts PB j in [lo0, hi0)
     const uint32_t dm1 = (uint32_t)(d - 1);
     const uint32_t cB = baseB + 2u * (uint32_t)sw(d - 1);
     while (jl < jh) {  // first j whose block start 32 j is not among the first d outputs
@@ -444,14 +449,14 @@ __device__ __forceinline__ int mp_search(uint32_t baseA, uint32_t baseB, int d, 
         if (a <= b) jl = mid + 1;
         else jh = mid;
     }
-    int lo = max(lo0, 32 * jl - 31), hi = min(hi0, 32 * jl);
+    int lo = max(lo0, PB * jl - (PB - 1)), hi = min(hi0, PB * jl);
     // probes mid in [lo, hi) lie inside A block jl - 1: byte 2 mid + 4 (jl - 1)
     const uint32_t cA = baseA + 4u * (uint32_t)(jl - 1);
     while (lo < hi) {  // i = #A among the first d outputs
         const int mid = (lo + hi) >> 1;
         const uint32_t x = imad((uint32_t)mid, K.m1, dm1);  // B index d - mid - 1
         const uint32_t a = lds_u16(imad((uint32_t)mid, K.two, cA));
-        const uint32_t b = lds_u16(imad(x >> 5, K.four, imad(x, K.two, baseB)));
+        const uint32_t b = lds_u16(imad(x >> PBS, K.four, imad(x, K.two, baseB)));
         if (a <= b) lo = mid + 1;
         else hi = mid;
     }
@@ -497,7 +502,7 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
             ib = imad(org, K.one, ib);
             if (o + 1 < E) {
                 const uint32_t idx = org ? ib : ia;
-                const uint32_t addr = imad(idx >> 5, K.four, imad(idx, K.two, base));
+                const uint32_t addr = imad(idx >> PBS, K.four, imad(idx, K.two, base));
                 const uint32_t nv = lds_u16(addr);  // idx <= s + 2W: inside the buffers' 2-key slack
                 const uint32_t end = imad(org, (uint32_t)W, sW);
                 h2 = idx == end ? INF : imad(nv, K.s16, org);
@@ -522,7 +527,7 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
                 : "=r"(org), "+r"(ia), "+r"(ib), "+r"(Y), "=r"(c)
                 : "r"(cm), "r"(K.one));
             if (o + 1 < E) {
-                const uint32_t addr = imad(c >> 5, K.four, imad(c, K.two, base + 2u));
+                const uint32_t addr = imad(c >> PBS, K.four, imad(c, K.two, base + 2u));
                 h2 = imad(lds_u16(addr), K.s16, org);
             }
         }
@@ -556,7 +561,7 @@ __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, co
     uint16_t* dst = tmp;
     for (int W = E << LEAF_XL<E>; W < L; W <<= 1) {
         if (t < active) {
-            if (W < 32) inv += merge_level_cur<E, true>(src, dst, t, W, K);
+            if (W < PB) inv += merge_level_cur<E, true>(src, dst, t, W, K);
             else inv += merge_level_cur<E, false>(src, dst, t, W, K);
         }
         __syncthreads();
@@ -800,9 +805,9 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
     a.num = num;
     a.nd = reinterpret_cast<unsigned long long*>(nd);
     a.n3 = reinterpret_cast<unsigned long long*>(n3);
-    const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> 5) + 2 + L + 2 * ((size_t)L >> 5) + 2;
+    const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> PBS) + 2 + L + 2 * ((size_t)L >> PBS) + 2;
     size_t smem = padded * sizeof(uint16_t);
-    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u, 68u, (uint32_t)-68};
+    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u, 2u * (PB + 2), (uint32_t)(-2 * (PB + 2))};
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = std::min<int64_t>(a.count, (int64_t)num_sms());
     merge_pairs_kernel<<<(unsigned)grid, MG_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(a);
