@@ -309,47 +309,84 @@ def test_merge_shards(eng, oracle):
     _check_full(full, oracle, ranks)
 
 
-def test_config3_gemm_sampled(eng):
-    """Config 3 (16384 x 500 gene-like f32, ties): sampled pairs vs the reference."""
+def _oracle_pairs_check(res, oracle, x, pi, pj, kernel, counts=False):
+    """SURVEY 8(c) parity protocol at full size: the listed pairs vs the pinned C oracle (its kernels
+    match the reference's golden vectors, tests/test_oracle_golden.py), bit-exact numerator / n1 / n2
+    (and n_d / n3 when the result carries them), tau compared with assert_array_equal (0 ulp; the
+    north-star tolerance 1e-12 is weaker)."""
+    rows, inv = np.unique(np.concatenate([pi, pj]), return_inverse=True)
+    ranks = np.stack([oracle.rank_transform(x[r]) for r in rows])
+    ci, cj = inv[: len(pi)], inv[len(pi):]
+    num, cnt = oracle.all_pairs(ranks, ci, cj, kernel, want_counts=True)
+    m, n = x.shape
+    jid = torch.from_numpy(pi * (2 * m - pi + 1) // 2 + pj - pi - res.job_lo).cuda()
+    np.testing.assert_array_equal(res.numerator.index_select(0, jid).cpu().numpy().astype(np.int64), num)
+    n1 = res.n1_rows.cpu().numpy()
+    np.testing.assert_array_equal(n1[pi], cnt[:, 1])
+    np.testing.assert_array_equal(n1[pj], cnt[:, 2])
+    if counts and res.n_d is not None:
+        np.testing.assert_array_equal(res.n_d.index_select(0, jid).cpu().numpy().astype(np.int64), cnt[:, 0])
+        np.testing.assert_array_equal(res.n3.index_select(0, jid).cpu().numpy().astype(np.int64), cnt[:, 3])
+    ta, tb = oracle.derive_taus(num, cnt[:, 1], cnt[:, 2], n)
+    if res.tau_a is not None:
+        np.testing.assert_array_equal(res.tau_a.index_select(0, jid).cpu().numpy(), ta)
+    np.testing.assert_array_equal(res.tau_b.index_select(0, jid).cpu().numpy(), tb)
+
+
+def _random_pairs(m, count, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, m, count)
+    b = rng.integers(0, m, count)
+    return np.minimum(a, b).astype(np.int64), np.maximum(a, b).astype(np.int64)
+
+
+def test_config3_gemm_sampled(eng, oracle):
+    """Config 3 (16384 x 500 gene-like f32, ties): sampled pairs vs the reference, and 10^4 seeded
+    random pairs vs the pinned oracle (SURVEY 8(c) parity protocol), counts included."""
     from paper_1704_03767_b200 import workloads
     z = load_npz("config3.npz")
     x = workloads.generate(3)
     assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
-    res = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="gemm").validate()
+    res = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="gemm", full_counts=True).validate()
     _sampled_check(res, z, 500)
     _diag_properties(res, 500)
-    eng.release()
-
-
-def test_config4_merge_sampled(eng, oracle):
-    """Config 4 (1024 x 65536, monotone family every 8th row): Knight merge path vs the reference."""
-    from paper_1704_03767_b200 import workloads
-    z = load_npz("config4.npz")
-    x = workloads.generate(4)
-    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
-    rows = np.unique(np.concatenate([z["pi"], z["pj"]]))
-    ranks = np.zeros(x.shape, np.int32)
-    for r in rows:
-        ranks[r] = oracle.rank_transform(x[r])
-    np.testing.assert_array_equal(ranks[:4], z["ranks_head"])
-    # only the sampled rows are ranked: compute exactly the sampled job ids' rows
-    xd = torch.from_numpy(ranks).cuda()
-    m = x.shape[0]
-    pi, pj = z["pi"], z["pj"]
-    jid = pi * (2 * m - pi + 1) // 2 + pj - pi
-    for k in np.argsort(jid)[:40]:
-        j = int(jid[k])
-        res = eng.all_pairs(xd, kernel="merge", job_range=(j, j + 1)).validate()
-        assert int(res.numerator.item()) == int(z["numerator"][k])
-        assert int(res.n_d.item()) == int(z["counts"][k, 0])
-        assert int(res.n3.item()) == int(z["counts"][k, 3])
-        assert res.tau_b.item() == z["tau_b"][k] or (math.isnan(res.tau_b.item()) and math.isnan(z["tau_b"][k]))
+    pi, pj = _random_pairs(x.shape[0], 10000, 3)
+    _oracle_pairs_check(res, oracle, x, pi, pj, oracle.KERNEL_PACKED, counts=True)
     eng.release()
 
 
 @pytest.mark.timeout(900)
-def test_config5_gemm_sampled(eng):
-    """Config 5 (65536 x 1024 low-rank f32, 2.15e9 pairs): sampled pairs vs the reference."""
+def test_config4_merge_sampled(eng, oracle):
+    """Config 4 (1024 x 65536, monotone family every 8th row): the Knight merge path over every job id
+    vs the reference's golden pairs, and 10^4 seeded random pairs plus row 0 against every member of
+    its monotone family vs the pinned oracle, counts included."""
+    from paper_1704_03767_b200 import workloads
+    z = load_npz("config4.npz")
+    x = workloads.generate(4)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
+    m = x.shape[0]
+    ranks = np.stack([oracle.rank_transform(r) for r in x])
+    np.testing.assert_array_equal(ranks[:4], z["ranks_head"])
+    res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="merge", full_counts=True).validate()
+    pi, pj = z["pi"], z["pj"]
+    jid = torch.from_numpy(pi * (2 * m - pi + 1) // 2 + pj - pi).cuda()
+    np.testing.assert_array_equal(res.numerator.index_select(0, jid).cpu().numpy(), z["numerator"])
+    np.testing.assert_array_equal(res.n_d.index_select(0, jid).cpu().numpy(), z["counts"][:, 0])
+    np.testing.assert_array_equal(res.n3.index_select(0, jid).cpu().numpy(), z["counts"][:, 3])
+    np.testing.assert_array_equal(res.tau_b.index_select(0, jid).cpu().numpy(), z["tau_b"])
+    ri, rj = _random_pairs(m, 10000, 4)
+    fam = np.arange(8, m, 8, dtype=np.int64)
+    ri = np.concatenate([ri, np.zeros_like(fam)])
+    rj = np.concatenate([rj, fam])
+    _oracle_pairs_check(res, oracle, ranks, ri, rj, oracle.KERNEL_SORTED, counts=True)
+    del res
+    eng.release()
+
+
+@pytest.mark.timeout(900)
+def test_config5_gemm_sampled(eng, oracle):
+    """Config 5 (65536 x 1024 low-rank f32, 2.15e9 pairs): sampled pairs vs the reference, and 10^4
+    seeded random pairs vs the pinned oracle."""
     from paper_1704_03767_b200 import workloads
     z = load_npz("config5.npz")
     x = workloads.generate(5)
@@ -361,6 +398,8 @@ def test_config5_gemm_sampled(eng):
     np.testing.assert_array_equal(res.numerator.index_select(0, jid).cpu().numpy(), z["numerator"])
     np.testing.assert_array_equal(res.tau_b.index_select(0, jid).cpu().numpy(), z["tau_b"])
     _diag_properties(res, 1024)
+    ri, rj = _random_pairs(m, 10000, 5)
+    _oracle_pairs_check(res, oracle, x, ri, rj, oracle.KERNEL_PACKED)
     del res
     eng.release()
     torch.cuda.empty_cache()
