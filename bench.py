@@ -134,11 +134,16 @@ def cpu_pairs_rate(ranks: np.ndarray, seconds: float, threads: int, seed: int = 
     m, n = ranks.shape
     kernel = orc.KERNEL_PACKED if (n <= 32767 and ranks.max() < 1 << 15) else orc.KERNEL_SORTED
     rng = np.random.default_rng(seed)
+    # size the sample from a probe long enough (>= 0.5 s) that thread start-up does not skew the rate
     probe = max(threads * 4, 64)
-    pi, pj = _sample_pairs(rng, m, probe)
-    t0 = time.perf_counter()
-    orc.all_pairs(ranks, pi, pj, kernel, threads=threads, want_counts=False)
-    dt = max(time.perf_counter() - t0, 1e-6)
+    while True:
+        pi, pj = _sample_pairs(rng, m, probe)
+        t0 = time.perf_counter()
+        orc.all_pairs(ranks, pi, pj, kernel, threads=threads, want_counts=False)
+        dt = max(time.perf_counter() - t0, 1e-6)
+        if dt >= 0.5 or probe >= m * (m - 1) // 2:
+            break
+        probe = int(probe * min(16.0, max(2.0, 0.6 / dt)))
     count = int(max(probe, min(m * (m - 1) // 2, probe / dt * seconds)))
     pi, pj = _sample_pairs(rng, m, count)
     t0 = time.perf_counter()
