@@ -10,18 +10,18 @@ m = xh.shape[0]
 out = torch.empty(m * (m + 1) // 2, dtype=torch.float64).pin_memory()
 flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 st = torch.cuda.Stream()
-for fr in ((0.65, 0.25, 0.10), (0.8, 0.2), (0.85, 0.15), (0.9, 0.1), (0.8, 0.15, 0.05), (0.75, 0.2, 0.05),
-           (0.85, 0.1, 0.05), (0.7, 0.3)):
+for fr, hc in (((0.7, 0.3), 1), ((0.7, 0.3), 2), ((0.7, 0.3), 3), ((0.7, 0.3), 4), ((0.7, 0.3), 8),
+               ((0.65, 0.25, 0.10), 2), ((0.65, 0.25, 0.10), 4)):
     ts = []
     for it in range(12):
         with torch.cuda.stream(st):
             flush.zero_()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(st)
-            r = eng.all_pairs_host(xh, out, band_fracs=fr, stream=st)
+            r = eng.all_pairs_host(xh, out, band_fracs=fr, stream=st, h2d_chunks=hc)
             e.record(st)
         torch.cuda.synchronize()
         if it >= 2:
             ts.append(s.elapsed_time(e))
         del r
-    print(f"bands {fr}: median {statistics.median(ts):.3f} ms  min {min(ts):.3f}", flush=True)
+    print(f"bands {fr} h2d_chunks {hc}: median {statistics.median(ts):.3f} ms  min {min(ts):.3f}", flush=True)
