@@ -333,7 +333,7 @@ struct UnitTable {
     int32_t* dev = nullptr;
     int64_t count = 0, cap = 0;
 };
-static UnitTable g_unit_cache[16];  // per (m, job range): the banded host path cycles through a few
+static UnitTable g_unit_cache[32];  // per (m, job range): the banded host path cycles through a few
 static int g_unit_next = 0;
 
 static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t st, const int32_t** out,
@@ -345,7 +345,7 @@ static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t s
             return TB_OK;
         }
     UnitTable& g_units = g_unit_cache[g_unit_next];
-    g_unit_next = (g_unit_next + 1) % 16;
+    g_unit_next = (g_unit_next + 1) % 32;
     g_units.m = -1;
     const int64_t T = gemm2::TILE, G = 4;
     const int64_t w = (m + T - 1) / T;

@@ -329,7 +329,8 @@ struct Plan4 {
     int32_t partial = 0;
 };
 // Plans are cached per (geometry, job range): the banded host path cycles through a few ranges.
-static Plan4 g_plans4[16];
+constexpr int PLAN_CACHE = 32;  // the banded host path cycles through up to ~15 job ranges
+static Plan4 g_plans4[PLAN_CACHE];
 static int g_plans4_next = 0;
 
 static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<int32_t>& code, std::vector<int32_t>& nb,
@@ -400,7 +401,7 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
             return TB_OK;
         }
     Plan4& g_plan4 = g_plans4[g_plans4_next];
-    g_plans4_next = (g_plans4_next + 1) % 16;
+    g_plans4_next = (g_plans4_next + 1) % PLAN_CACHE;
     g_plan4.m = -1;
     std::vector<int32_t> code, nb, ncols;
     list_units4(m, job_lo, job_hi, code, nb, ncols);

@@ -14,6 +14,8 @@ host except the optional ``validate()`` (one 4-byte flag read).
 
 from __future__ import annotations
 
+import math
+
 import ctypes
 from dataclasses import dataclass, field
 
@@ -256,6 +258,21 @@ class TauEngine:
         cuts.append(m)
         return cuts
 
+    @staticmethod
+    def default_band_fracs(total: int) -> tuple:
+        """Row-band shares of the pairs for all_pairs_host: more, geometrically shrinking bands as the
+        job grows, so the tau_b copy of every band but a small last one hides behind later bands'
+        kernels while each band stays large enough for an efficient GEMM launch.  Measured
+        (tools/exp_e2e_bands.py, profiles/r01_e2e_band_sweep_v3.log): config 2 (2.1 M job ids) two bands
+        0.850 ms (three: 0.876); config 3 (134 M) six-seven bands 22.5 ms (three: 24.4); config 5 (2.1 G)
+        twelve bands 417-427 ms (three: 627)."""
+        if total <= (8 << 20):
+            return (0.7, 0.3)
+        k = int(min(14, 2 + round(1.25 * math.log2(total / (8 << 20)))))
+        r = 0.7 + 0.01 * k
+        w = [r ** i for i in range(k)]
+        return tuple(x / sum(w) for x in w)
+
     def all_pairs_host(self, x_host: torch.Tensor, tau_b_out: torch.Tensor, kernel: str = "auto",
                        band_fracs: tuple | None = None, stream: torch.cuda.Stream | None = None,
                        copy_stream: torch.cuda.Stream | None = None, h2d_chunks: int = 2,
@@ -310,9 +327,7 @@ class TauEngine:
                     st_t.wait_event(ev)
                 pos, srt, keys, maxgrp = self._merge_prepare(x, res, st)
             if band_fracs is None:
-                # measured (tools/exp_e2e_bands.py): two bands for small jobs (config 2: 0.850 ms vs 0.876 ms
-                # with three), three when the tau_b copy dominates (config 3: 24.7 ms vs 24.9 ms with two)
-                band_fracs = (0.7, 0.3) if total <= (8 << 20) else (0.65, 0.25, 0.10)
+                band_fracs = self.default_band_fracs(total)
             cuts = self.bands(m, len(band_fracs), fracs=band_fracs)
             for r0, r1 in zip(cuts[:-1], cuts[1:]):
                 lo, hi = r0 * (2 * m - r0 + 1) // 2, r1 * (2 * m - r1 + 1) // 2

@@ -10,10 +10,20 @@ m = xh.shape[0]
 out = torch.empty(m * (m + 1) // 2, dtype=torch.float64).pin_memory()
 flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 st = torch.cuda.Stream()
-for fr, hc in (((0.7, 0.3), 1), ((0.7, 0.3), 2), ((0.7, 0.3), 3), ((0.7, 0.3), 4), ((0.7, 0.3), 8),
-               ((0.65, 0.25, 0.10), 2), ((0.65, 0.25, 0.10), 4)):
+def geo(k, r):  # k bands, each r times the previous one's share of the pairs
+    w = [r ** i for i in range(k)]
+    return tuple(x / sum(w) for x in w)
+
+
+VARIANTS = {
+    2: (((0.7, 0.3), 2), ((0.65, 0.25, 0.10), 2)),
+    3: ((geo(6, 0.7), 2), (geo(7, 0.75), 2), (geo(8, 0.75), 2), (geo(5, 0.65), 2)),
+    5: ((geo(12, 0.8), 2), (geo(12, 0.75), 2), (geo(14, 0.8), 2), (geo(10, 0.8), 2)),
+}
+iters = 12 if cfg != 5 else 5
+for fr, hc in VARIANTS.get(cfg, VARIANTS[2]):
     ts = []
-    for it in range(12):
+    for it in range(iters):
         with torch.cuda.stream(st):
             flush.zero_()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -21,7 +31,7 @@ for fr, hc in (((0.7, 0.3), 1), ((0.7, 0.3), 2), ((0.7, 0.3), 3), ((0.7, 0.3), 4
             r = eng.all_pairs_host(xh, out, band_fracs=fr, stream=st, h2d_chunks=hc)
             e.record(st)
         torch.cuda.synchronize()
-        if it >= 2:
+        if it >= (2 if iters > 5 else 1):
             ts.append(s.elapsed_time(e))
         del r
-    print(f"bands {fr} h2d_chunks {hc}: median {statistics.median(ts):.3f} ms  min {min(ts):.3f}", flush=True)
+    print(f"bands {len(fr)} first {fr[0]:.3f} last {fr[-1]:.3f} h2d_chunks {hc}: median {statistics.median(ts):.3f} ms  min {min(ts):.3f}", flush=True)
