@@ -226,11 +226,35 @@ class TauEngine:
         else:
             _lib.call("tb_gemm_pairs", _ptr(src), m, K, ldS, fmt, job_lo, job_hi, splits, _ptr(out), st)
 
+    # GEMM launches per call for very large job ranges (see _gemm_ranges); None = automatic
+    gemm_bands: int | None = None
+
+    def _gemm_ranges(self, m: int, job_lo: int, job_hi: int) -> list[tuple[int, int]]:
+        """Job sub-ranges the numerator GEMM is launched over.  Ranges of >= 2^30 job ids run as ~8
+        row bands of equal pair counts (aligned to the 256-row block): measured on config 5
+        (tools/exp_value_bands.py) a single 2.1e9-id launch takes 468-482 ms, eight band launches
+        436-443 ms; smaller ranges stay one launch (config 3 slows down when banded)."""
+        nb = self.gemm_bands
+        if nb is None:
+            nb = 8 if job_hi - job_lo >= (1 << 30) else 1
+        if nb <= 1:
+            return [(job_lo, job_hi)]
+        cuts = self.bands(m, nb)
+        out = []
+        for r0, r1 in zip(cuts[:-1], cuts[1:]):
+            lo = max(job_lo, r0 * (2 * m - r0 + 1) // 2)
+            hi = min(job_hi, r1 * (2 * m - r1 + 1) // 2)
+            if lo < hi:
+                out.append((lo, hi))
+        return out
+
     def _gemm_path(self, x, res: PairResult, st, full_counts: bool, splits: int, simt: bool):
         m, n = res.m, res.n
         S, K, ldS, fmt = self._gemm_prepare(x, res, st, simt)
         self._mark(0)
-        self._gemm_numerator(S, res.numerator, m, K, ldS, fmt, res.job_lo, res.job_hi, st, splits, simt)
+        for lo, hi in self._gemm_ranges(m, res.job_lo, res.job_hi):
+            num = res.numerator[lo - res.job_lo:hi - res.job_lo]
+            self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st, splits, simt)
         self._mark(1)
         if full_counts:
             A = self._buf("A", m * ldS, torch.int8)
