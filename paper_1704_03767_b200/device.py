@@ -23,6 +23,7 @@ import torch
 
 from . import _lib
 from .errors import CapacityExceededError, ConfigError, InvalidInputError
+from .pairindex import job_coord
 
 # Dispatcher crossover (numerator kernel per shape).  The GEMM costs 2K = n(n-1)
 # int8 ops per pair at tensor-core rate; the merge costs ~4 n log2 n INT32 ops
@@ -211,12 +212,18 @@ class TauEngine:
         K, fmt, ldS, ldr = self._gemm_layout(n, simt)
         R = self._buf("R", m * ldr, torch.int16)
         S = self._buf("S", m * ldS, torch.int8)
+        # every job id of [job_lo, job_hi) pairs rows >= y_lo (the row of job_lo): rows above it are ranked
+        # (their n1 is part of the result) but need no sign vector -- a late job-range shard (multi-GPU
+        # strong scaling) packs only its own share of S
+        y_lo = job_coord(res.job_lo, m)[0] if res.job_hi > res.job_lo else m
         for r0, r1, wait in (row_chunks or [(0, m, None)]):
             if wait is not None:
                 wait()
             _lib.call("tb_rank_rows", _ptr(x[r0:r1]), _dtype_code(x), r1 - r0, n, x.stride(0),
                       _ptr(R[r0 * ldr:]), ldr, _ptr(res.n1_rows[r0:]), _ptr(res.flags), st)
-            _lib.call("tb_sign_pack", _ptr(R[r0 * ldr:]), r1 - r0, n, ldr, _ptr(S[r0 * ldS:]), ldS, fmt, st)
+            p0 = max(r0, y_lo)
+            if p0 < r1:
+                _lib.call("tb_sign_pack", _ptr(R[p0 * ldr:]), r1 - p0, n, ldr, _ptr(S[p0 * ldS:]), ldS, fmt, st)
         res.extra["sign_format"] = fmt
         return S, K, ldS, fmt
 
