@@ -164,3 +164,38 @@ def test_sign_k_block_layout():
         assert k == 16 * chunks, n
         assert n * (n - 1) // 2 <= k < n * (n - 1) // 2 + 16 * (nbf + 16), n
     assert int(lib.tb_sign_k(1000)) == 499584
+
+
+def test_band_plans_cover_the_job_range():
+    """Host logic of the banded launches: row bands (aligned to the 256-row GEMM block) and the
+    size-dependent default shares of all_pairs_host; the GEMM sub-ranges of a (shard) job range are
+    contiguous and cover it exactly."""
+    import types
+
+    from paper_1704_03767_b200.device import TauEngine
+    from paper_1704_03767_b200.pairindex import job_shard_range
+
+    for total in (3, 2_098_176, 134_225_920, 2_147_516_416):
+        fr = TauEngine.default_band_fracs(total)
+        assert abs(sum(fr) - 1.0) < 1e-9 and all(a >= b for a, b in zip(fr, fr[1:]))
+        assert len(fr) == (2 if total <= (8 << 20) else len(fr)) and 2 <= len(fr) <= 14
+    for m in (1, 255, 256, 700, 2048, 16384, 65536):
+        for nb in (1, 2, 3, 7, 8, 12):
+            cuts = TauEngine.bands(m, nb)
+            assert cuts[0] == 0 and cuts[-1] == m and cuts == sorted(set(cuts))
+            assert all(c % 256 == 0 for c in cuts[1:-1])
+    for m in (300, 2048, 65536):
+        total = m * (m + 1) // 2
+        for nb in (1, 8):
+            eng = types.SimpleNamespace(gemm_bands=nb, bands=TauEngine.bands)
+            for p in (1, 3, 8):
+                for r in range(p):
+                    lo, hi = job_shard_range(r, p, m)
+                    rr = TauEngine._gemm_ranges(eng, m, lo, hi)
+                    if lo == hi:
+                        assert rr == []
+                        continue
+                    assert rr[0][0] == lo and rr[-1][1] == hi
+                    assert all(a[1] == b[0] for a, b in zip(rr, rr[1:])) and all(a < b for a, b in rr)
+        auto = types.SimpleNamespace(gemm_bands=None, bands=TauEngine.bands)
+        assert len(TauEngine._gemm_ranges(auto, m, 0, total)) == (8 if total >= (1 << 30) else 1)
