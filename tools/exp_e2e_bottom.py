@@ -1,4 +1,4 @@
-"""Config-2 end-to-end (all_pairs_host) with the bottom-rows-first schedule: split row fraction x
+"""(Reverted experiment; needs the all_pairs_host(bottom_first=...) option from git history.) Config-2
 top-band shares (diagnostics; checks the output against the default schedule)."""
 import os, sys, statistics, torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, ROOT)
