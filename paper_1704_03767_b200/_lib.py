@@ -15,8 +15,11 @@ from .errors import CapacityExceededError, ConfigError, InvalidInputError
 
 LIB_NAME = "libtaub200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-if os.environ.get("TB_LIB_VARIANT"):  # A/B experiments: an in-tree copy built from a variant source
-    LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ["TB_LIB_VARIANT"])
+_variant = os.environ.get("TB_LIB_VARIANT")
+if _variant:  # A/B experiments: an in-tree copy of this library built from a variant source
+    if os.path.basename(_variant) != _variant or not _variant.startswith("libtaub200") or not _variant.endswith(".so"):
+        raise ImportError(f"TB_LIB_VARIANT must name an in-tree libtaub200*.so, got {_variant!r}")
+    LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), _variant)
 
 TB_OK, TB_ERR_INVALID, TB_ERR_CAPACITY, TB_ERR_CONFIG, TB_ERR_CUDA = 0, 1, 2, 3, 4
 TB_DTYPE_I32, TB_DTYPE_F32, TB_DTYPE_F64 = 0, 1, 2
