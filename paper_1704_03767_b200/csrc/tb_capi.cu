@@ -1,5 +1,6 @@
-#include <atomic>
 // C-ABI plumbing: error state, device query.
+#include <atomic>
+#include <cstdlib>
 #include <algorithm>
 #include <cstdarg>
 #include <cstring>
@@ -39,6 +40,14 @@ int num_sms() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TB_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
 }
 
 }  // namespace tb

@@ -28,6 +28,33 @@ int num_sms();
 int accum_workspace(int64_t span, float** ws, cudaStream_t st);
 int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st);
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every kernel of the path is launched with launch_pdl: it may start while its stream predecessor is
+// still draining, so it calls pdl_wait() (griddepcontrol.wait: the predecessor grid has completed and
+// its memory is visible; a no-op without PDL) before touching any global data, and pdl_trigger()
+// (griddepcontrol.launch_dependents) once a block has issued its last stores, so the next kernel's launch
+// and prologue overlap this one's tail instead of following it.  TB_NO_PDL=1 launches plainly (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ------------------------------------------------------------------ geometry
 // pairindex.py:20-24 row_prefix: cells strictly above row y = y(2m - y + 1)/2.
 __host__ __device__ __forceinline__ int64_t row_prefix(int64_t y, int64_t m) { return y * (2 * m - y + 1) / 2; }

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32
                                                                       int64_t m, int64_t n0, int64_t job_lo,
                                                                       int64_t count, double* __restrict__ tau_a,
                                                                       double* __restrict__ tau_b, int64_t chunk) {
+    pdl_wait();
     const double dn0 = (double)n0;
     int64_t i = (int64_t)blockIdx.x * chunk + threadIdx.x;
     if (i >= count) return;
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32
             }
         }
     }
+    pdl_trigger();
 }
 
 }  // namespace tb
@@ -89,9 +91,10 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     const int64_t chunk = iters * FIN_THREADS;
     const int64_t blocks = (count + chunk - 1) / chunk;
     if (blocks > INT32_MAX) return fail(TB_ERR_CAPACITY, "finalize: job range too large");
-    finalize_chunk_kernel<<<(unsigned)blocks, FIN_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-        num, reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count, tau_a, tau_b,
-        chunk);
+    TB_CUDA_TRY(launch_pdl(finalize_chunk_kernel, dim3((unsigned)blocks), dim3(FIN_THREADS), 0,
+                           static_cast<cudaStream_t>(stream), num,
+                           reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count,
+                           tau_a, tau_b, chunk));
     return check_launch("finalize_chunk_kernel");
 }
 
@@ -102,6 +105,7 @@ __global__ void __launch_bounds__(256) full_counts_kernel(const int32_t* __restr
                                                           int64_t n0, int64_t job_lo, int64_t count,
                                                           unsigned long long* __restrict__ nd,
                                                           unsigned long long* __restrict__ n3) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = num[i], a = absdot[i];  // a = n_c + n_d, s = n_c - n_d
@@ -112,10 +116,16 @@ __global__ void __launch_bounds__(256) full_counts_kernel(const int32_t* __restr
             n3[i] = (unsigned long long)(a - n0 + (int64_t)n1[y] + (int64_t)n1[x]);
         }
     }
+    pdl_trigger();
 }
 // ------------------------------------------------------------------ split-K accumulation
 static float* g_accum = nullptr;
 static size_t g_accum_bytes = 0;
+
+// The workspace stays zero between calls: accum_convert clears every entry it converts, so a GEMM finds it
+// zeroed without a memset in front of it (which would also break the sign pack -> GEMM programmatic
+// launch).  A fresh allocation, or a call whose convert never ran (g_accum_dirty), is cleared here.
+static bool g_accum_dirty = false;
 
 int accum_workspace(int64_t span, float** ws, cudaStream_t st) {
     const size_t bytes = (size_t)((span + 3) & ~int64_t(3)) * sizeof(float);
@@ -125,23 +135,31 @@ int accum_workspace(int64_t span, float** ws, cudaStream_t st) {
         g_accum_bytes = 0;
         TB_CUDA_TRY(cudaMalloc(&g_accum, bytes));
         g_accum_bytes = bytes;
+        g_accum_dirty = true;
     }
-    TB_CUDA_TRY(cudaMemsetAsync(g_accum, 0, bytes, st));
+    if (g_accum_dirty) TB_CUDA_TRY(cudaMemsetAsync(g_accum, 0, g_accum_bytes, st));
+    g_accum_dirty = true;  // until accum_convert has been enqueued
     *ws = g_accum;
     return TB_OK;
 }
 
-__global__ void __launch_bounds__(256) accum_convert_kernel(const float* __restrict__ ws, int64_t span,
+__global__ void __launch_bounds__(256) accum_convert_kernel(float* __restrict__ ws, int64_t span,
                                                            int32_t* __restrict__ num) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < span; i += (int64_t)gridDim.x * blockDim.x)
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < span; i += (int64_t)gridDim.x * blockDim.x) {
         num[i] = __float2int_rn(ws[i]);
+        ws[i] = 0.0f;
+    }
+    pdl_trigger();
 }
 
 int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st) {
     if (span <= 0) return TB_OK;
     const int64_t blocks = std::min<int64_t>((span + 255) / 256, (int64_t)num_sms() * 8);
-    accum_convert_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, span, num);
-    return check_launch("accum_convert_kernel");
+    TB_CUDA_TRY(launch_pdl(accum_convert_kernel, dim3((unsigned)blocks), dim3(256), 0, st, const_cast<float*>(ws), span, num));
+    const int rc = check_launch("accum_convert_kernel");
+    if (rc == TB_OK) g_accum_dirty = false;
+    return rc;
 }
 
 }  // namespace tb
@@ -155,8 +173,9 @@ extern "C" int tb_full_counts(const int32_t* num, const int32_t* absdot, const u
     const int64_t count = job_hi - job_lo;
     if (count == 0) return TB_OK;
     int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 16);
-    full_counts_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        num, absdot, reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count,
-        reinterpret_cast<unsigned long long*>(nd), reinterpret_cast<unsigned long long*>(n3));
+    TB_CUDA_TRY(launch_pdl(full_counts_kernel, dim3((unsigned)blocks), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                           num, absdot, reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2,
+                           job_lo, count, reinterpret_cast<unsigned long long*>(nd),
+                           reinterpret_cast<unsigned long long*>(n3)));
     return check_launch("full_counts_kernel");
 }

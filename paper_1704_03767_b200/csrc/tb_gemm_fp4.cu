@@ -144,6 +144,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
+    pdl_wait();  // the setup above overlaps the sign pack's tail; S and the accumulators are read after it
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
@@ -304,6 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             acc_phase ^= 1;
         }
     }
+    pdl_trigger();
     tc_fence_before();
     cluster_sync();
     if (warp == 2) {
@@ -512,7 +514,7 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
         TB_CUDA_TRY(cudaMemsetAsync(p.trace, 0, grid * 16 * sizeof(unsigned long long), st));
         TB_CUDA_TRY(cudaStreamSynchronize(st));
     }
-    gemm_fp4_kernel<<<grid, g4::THREADS, g4::SMEM_BYTES, st>>>(ta, tbm, p);
+    TB_CUDA_TRY(launch_pdl(gemm_fp4_kernel, dim3(grid), dim3(g4::THREADS), g4::SMEM_BYTES, st, ta, tbm, p));
     if ((rc = check_launch("gemm_fp4_kernel"))) return rc;
     if (p.trace) {
         TB_CUDA_TRY(cudaStreamSynchronize(st));

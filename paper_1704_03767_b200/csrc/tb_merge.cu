@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(PS_THREADS) presort_kernel(const int32_t* __re
                                                              unsigned long long* __restrict__ n1,
                                                              int32_t* __restrict__ maxgrp, int32_t* __restrict__ work,
                                                              int32_t* __restrict__ flags) {
+    pdl_wait();
     __shared__ int64_t red[32];
     __shared__ int32_t chunk_base[PS_THREADS];
     const int64_t r = blockIdx.x;
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(PS_THREADS) presort_kernel(const int32_t* __re
         int32_t vr = rk[i];
         if (vr >= 0 && vr < n) ps[i] = atomicAdd(&cnt[vr], 1);
     }
+    pdl_trigger();
 }
 
 // Compact tie-group list per variable: groups[r, 2k] = first u-order position, groups[r, 2k+1] =
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(PS_THREADS) presort_kernel(const int32_t* __re
 __global__ void __launch_bounds__(256) tie_groups_kernel(const int32_t* __restrict__ sorted, int64_t n,
                                                          int32_t* __restrict__ groups,
                                                          int32_t* __restrict__ ngroups) {
+    pdl_wait();
     const int64_t r = blockIdx.x;
     const int32_t* so = sorted + r * n;
     int32_t* gr = groups + r * n;
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(256) tie_groups_kernel(const int32_t* __restri
     }
     __syncthreads();
     if (threadIdx.x == 0) ngroups[r] = cnt;
+    pdl_trigger();
 }
 
 // ===================================================================== K4
@@ -608,6 +612,7 @@ struct MergeArgs {
 };
 
 __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p) {
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t mg_smem[];
     uint16_t* keys = reinterpret_cast<uint16_t*>(mg_smem);  // B * L keys (padded layout)
     uint16_t* tmp = keys + sw(p.B * p.L) + 2;               // L keys (padded layout)
@@ -751,6 +756,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         }
         __syncthreads();
     }
+    pdl_trigger();
 }
 
 }  // namespace tb
@@ -765,11 +771,10 @@ extern "C" int tb_presort(const int32_t* ranks, int64_t m, int64_t n, int32_t* p
     if (!ranks || !pos || !sorted || !keys || !n1 || !maxgrp || !work || !ngroups || !flags)
         return fail(TB_ERR_INVALID, "presort: null pointer");
     if (m > INT32_MAX) return fail(TB_ERR_CAPACITY, "presort: m too large");
-    presort_kernel<<<(unsigned)m, PS_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-        ranks, n, pos, sorted, keys, reinterpret_cast<unsigned long long*>(n1), maxgrp, work, flags);
+    TB_CUDA_TRY(launch_pdl(presort_kernel, dim3((unsigned)m), dim3(PS_THREADS), 0, static_cast<cudaStream_t>(stream), ranks, n, pos, sorted, keys, reinterpret_cast<unsigned long long*>(n1), maxgrp, work, flags));
     int rc = check_launch("presort_kernel");
     if (rc) return rc;
-    tie_groups_kernel<<<(unsigned)m, 256, 0, static_cast<cudaStream_t>(stream)>>>(sorted, n, work, ngroups);
+    TB_CUDA_TRY(launch_pdl(tie_groups_kernel, dim3((unsigned)m), dim3(256), 0, static_cast<cudaStream_t>(stream), sorted, n, work, ngroups));
     return check_launch("tie_groups_kernel");
 }
 
@@ -810,6 +815,6 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
     a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u, 2u * (PB + 2), (uint32_t)(-2 * (PB + 2))};
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = std::min<int64_t>(a.count, (int64_t)num_sms());
-    merge_pairs_kernel<<<(unsigned)grid, MG_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    TB_CUDA_TRY(launch_pdl(merge_pairs_kernel, dim3((unsigned)grid), dim3(MG_THREADS), smem, static_cast<cudaStream_t>(stream), a));
     return check_launch("merge_pairs_kernel");
 }

@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(RK_THREADS) rank_rows_kernel(const T* __restri
                                                                uint16_t* __restrict__ R, int64_t ldr,
                                                                unsigned long long* __restrict__ n1,
                                                                int32_t* __restrict__ flags, int Np) {
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t rk_smem[];
     uint64_t* key = reinterpret_cast<uint64_t*>(rk_smem);
     uint16_t* idx = reinterpret_cast<uint16_t*>(key + Np);
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(RK_THREADS) rank_rows_kernel(const T* __restri
     }
     // zero the row padding [n, ldr) so vector loads of R see defined values
     for (int64_t i = nn + tid; i < ldr; i += RK_THREADS) R[r * ldr + i] = 0;
+    pdl_trigger();
 }
 
 
@@ -172,6 +174,7 @@ template <int E>
 __global__ void __launch_bounds__(256) rank_rows_hist_kernel(const int32_t* __restrict__ x, int64_t m, int64_t n,
                                                              int64_t ldx, uint16_t* __restrict__ R, int64_t ldr,
                                                              unsigned long long* __restrict__ n1) {
+    pdl_wait();
     constexpr int HR = 1024;
     __shared__ int32_t hist[8][HR];
     const int lane = threadIdx.x & 31;
@@ -225,6 +228,7 @@ __global__ void __launch_bounds__(256) rank_rows_hist_kernel(const int32_t* __re
     for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
     if (lane == 0) n1[r] = ties;
     for (int64_t i = nn + lane; i < ldr; i += 32) R[r * ldr + i] = 0;
+    pdl_trigger();
 }
 
 template <typename T, int E>
@@ -232,6 +236,7 @@ __global__ void __launch_bounds__(256) rank_rows_warp_kernel(const T* __restrict
                                                              int64_t ldx, uint16_t* __restrict__ R, int64_t ldr,
                                                              unsigned long long* __restrict__ n1,
                                                              int32_t* __restrict__ flags, int only_marked) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (r >= m) return;
@@ -297,6 +302,7 @@ __global__ void __launch_bounds__(256) rank_rows_warp_kernel(const T* __restrict
     for (int o = 16; o > 0; o >>= 1) ties += __shfl_xor_sync(0xffffffffu, ties, o);
     if (lane == 0) n1[r] = ties;
     for (int64_t i = nn + lane; i < ldr; i += 32) R[r * ldr + i] = 0;
+    pdl_trigger();
 }
 
 // n <= 256 (any dtype): one CTA per row, one thread per element, O(n^2) comparisons against the
@@ -309,6 +315,7 @@ __global__ void __launch_bounds__(RK_SMALL_N) rank_rows_small_kernel(const T* __
                                                                      uint16_t* __restrict__ R, int64_t ldr,
                                                                      unsigned long long* __restrict__ n1,
                                                                      int32_t* __restrict__ flags) {
+    pdl_wait();
     __shared__ uint64_t key[RK_SMALL_N];
     __shared__ uint8_t first[RK_SMALL_N];
     __shared__ unsigned long long red[RK_SMALL_N / 32];
@@ -343,6 +350,7 @@ __global__ void __launch_bounds__(RK_SMALL_N) rank_rows_small_kernel(const T* __
         n1[r] = t;
     }
     for (int64_t k = nn + i; k < ldr; k += RK_SMALL_N) R[r * ldr + k] = 0;
+    pdl_trigger();
 }
 
 template <typename T>
@@ -352,7 +360,7 @@ static int launch_rank_warp(const T* x, int64_t m, int64_t n, int64_t ldx, uint1
     int only_marked = 0;
     if constexpr (std::is_same<T, int32_t>::value) {  // histogram pass first; the sort takes the rest
         only_marked = 1;
-#define TB_RK_HIST(E) rank_rows_hist_kernel<E><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1); break
+#define TB_RK_HIST(E) TB_CUDA_TRY(launch_pdl(rank_rows_hist_kernel<E>, dim3(grid), dim3(256), 0, st, x, m, n, ldx, R, ldr, n1)); break
         switch (Np / 32) {
             case 1: TB_RK_HIST(1);
             case 2: TB_RK_HIST(2);
@@ -366,7 +374,7 @@ static int launch_rank_warp(const T* x, int64_t m, int64_t n, int64_t ldx, uint1
         int rc = check_launch("rank_rows_hist_kernel");
         if (rc) return rc;
     }
-#define TB_RK_WARP(E) rank_rows_warp_kernel<T, E><<<grid, 256, 0, st>>>(x, m, n, ldx, R, ldr, n1, flags, only_marked); break
+#define TB_RK_WARP(E) TB_CUDA_TRY(launch_pdl(rank_rows_warp_kernel<T, E>, dim3(grid), dim3(256), 0, st, x, m, n, ldx, R, ldr, n1, flags, only_marked)); break
     switch (Np / 32) {
         case 1: TB_RK_WARP(1);
         case 2: TB_RK_WARP(2);
@@ -399,13 +407,13 @@ extern "C" int tb_rank_rows(const void* x, int dtype, int64_t m, int64_t n, int6
     if (n <= RK_SMALL_N) {  // short rows: O(n^2) per-row ranks, one thread per element
         switch (dtype) {
             case TB_DTYPE_I32:
-                rank_rows_small_kernel<int32_t><<<(unsigned)m, RK_SMALL_N, 0, st>>>((const int32_t*)x, n, ldx, R, ldr, n1u, flags);
+                TB_CUDA_TRY(launch_pdl(rank_rows_small_kernel<int32_t>, dim3((unsigned)m), dim3(RK_SMALL_N), 0, st, (const int32_t*)x, n, ldx, R, ldr, n1u, flags));
                 break;
             case TB_DTYPE_F32:
-                rank_rows_small_kernel<float><<<(unsigned)m, RK_SMALL_N, 0, st>>>((const float*)x, n, ldx, R, ldr, n1u, flags);
+                TB_CUDA_TRY(launch_pdl(rank_rows_small_kernel<float>, dim3((unsigned)m), dim3(RK_SMALL_N), 0, st, (const float*)x, n, ldx, R, ldr, n1u, flags));
                 break;
             case TB_DTYPE_F64:
-                rank_rows_small_kernel<double><<<(unsigned)m, RK_SMALL_N, 0, st>>>((const double*)x, n, ldx, R, ldr, n1u, flags);
+                TB_CUDA_TRY(launch_pdl(rank_rows_small_kernel<double>, dim3((unsigned)m), dim3(RK_SMALL_N), 0, st, (const double*)x, n, ldx, R, ldr, n1u, flags));
                 break;
             default:
                 return fail(TB_ERR_INVALID, "rank_rows: unknown dtype %d", dtype);
@@ -420,18 +428,15 @@ extern "C" int tb_rank_rows(const void* x, int dtype, int64_t m, int64_t n, int6
     switch (dtype) {
         case TB_DTYPE_I32:
             cudaFuncSetAttribute(rank_rows_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            rank_rows_kernel<int32_t><<<(unsigned)m, RK_THREADS, smem, st>>>(
-                (const int32_t*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np);
+            TB_CUDA_TRY(launch_pdl(rank_rows_kernel<int32_t>, dim3((unsigned)m), dim3(RK_THREADS), smem, st, (const int32_t*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np));
             break;
         case TB_DTYPE_F32:
             cudaFuncSetAttribute(rank_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            rank_rows_kernel<float><<<(unsigned)m, RK_THREADS, smem, st>>>(
-                (const float*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np);
+            TB_CUDA_TRY(launch_pdl(rank_rows_kernel<float>, dim3((unsigned)m), dim3(RK_THREADS), smem, st, (const float*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np));
             break;
         case TB_DTYPE_F64:
             cudaFuncSetAttribute(rank_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            rank_rows_kernel<double><<<(unsigned)m, RK_THREADS, smem, st>>>(
-                (const double*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np);
+            TB_CUDA_TRY(launch_pdl(rank_rows_kernel<double>, dim3((unsigned)m), dim3(RK_THREADS), smem, st, (const double*)x, n, ldx, R, ldr, reinterpret_cast<unsigned long long*>(n1), flags, Np));
             break;
         default:
             return fail(TB_ERR_INVALID, "rank_rows: unknown dtype %d", dtype);

@@ -228,6 +228,7 @@ template <int FMT>
 __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t* __restrict__ R, int64_t n,
                                                               int64_t ldr, int8_t* __restrict__ S, int64_t ldS,
                                                               int nw, uint32_t neg1) {
+    pdl_wait();
     extern __shared__ __align__(16) uint32_t sp_words[];  // wp[nw] plain pairs, wb[nw] biased, masks[17]
     uint32_t* wp = sp_words;
     uint32_t* wb = sp_words + nw;
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
     const int64_t kb = (FMT == 2 ? 8 : 16) * (int64_t)nchunks;
     for (int64_t k = kb + ((int64_t)blockIdx.y * SP_THREADS + tid) * 8; k < ldS; k += (int64_t)gridDim.y * SP_THREADS * 8)
         *reinterpret_cast<uint2*>(row + k) = make_uint2(0u, 0u);
+    pdl_trigger();
 }
 
 }  // namespace tb
@@ -364,7 +366,7 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
     dim3 grid((unsigned)m, gy);
 #define TB_SP_LAUNCH(F)                                                                                   \
     TB_CUDA_TRY(cudaFuncSetAttribute(signpack_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    signpack_kernel<F><<<grid, SP_THREADS, smem, st>>>(R, n, ldr, S, ldS, nw, 0xFFFFFFFFu)
+    TB_CUDA_TRY(launch_pdl(signpack_kernel<F>, dim3(grid), dim3(SP_THREADS), smem, st, R, n, ldr, S, ldS, nw, 0xFFFFFFFFu))
     if (format == TB_SIGN_E2M1) {
         TB_SP_LAUNCH(2);
     } else if (format == TB_SIGN_E4M3) {
@@ -379,6 +381,7 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
 // |S| (0/1 int8) for the full-count GEMM, 16 bytes per thread.
 namespace tb {
 __global__ void abs_pack_kernel(const uint4* __restrict__ S, uint4* __restrict__ A, int64_t nvec, uint32_t mask) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
         uint4 v = S[i];
         // int8 bytes 0x00/0x01/0xFF: |s| = s & 1; e2m1 nibbles 0x0/0x2/0xA: |s| clears the sign bits
@@ -388,6 +391,7 @@ __global__ void abs_pack_kernel(const uint4* __restrict__ S, uint4* __restrict__
         v.w &= mask;
         A[i] = v;
     }
+    pdl_trigger();
 }
 }  // namespace tb
 
@@ -396,9 +400,8 @@ extern "C" int tb_abs_pack(const int8_t* S, int64_t m, int64_t ldS, int format, 
     if (!S || !A) return fail(TB_ERR_INVALID, "abs_pack: null pointer");
     const int64_t nvec = m * ldS / 16;
     const int64_t blocks = std::min<int64_t>((nvec + 255) / 256, (int64_t)num_sms() * 8);
-    abs_pack_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const uint4*>(S), reinterpret_cast<uint4*>(A), nvec,
-        format == TB_SIGN_E2M1 ? 0x77777777u : (format == TB_SIGN_E4M3 ? 0x7F7F7F7Fu : 0x01010101u));
+    TB_CUDA_TRY(launch_pdl(abs_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), reinterpret_cast<const uint4*>(S), reinterpret_cast<uint4*>(A), nvec,
+        format == TB_SIGN_E2M1 ? 0x77777777u : (format == TB_SIGN_E4M3 ? 0x7F7F7F7Fu : 0x01010101u)));
     return check_launch("abs_pack_kernel");
 }
 
