@@ -16,9 +16,9 @@ def geo(k, r):  # k bands, each r times the previous one's share of the pairs
 
 
 VARIANTS = {
-    2: (((0.7, 0.3), 2), ((0.65, 0.25, 0.10), 2)),
-    3: ((geo(6, 0.7), 2), (geo(7, 0.75), 2), (geo(8, 0.75), 2), (geo(5, 0.65), 2)),
-    5: ((geo(12, 0.8), 2), (geo(12, 0.75), 2), (geo(14, 0.8), 2), (geo(10, 0.8), 2)),
+    2: (((0.7, 0.3), 2), ((0.65, 0.25, 0.10), 2), ((0.8, 0.2), 2), ((0.6, 0.4), 2), ((1.0,), 2)),
+    3: ((geo(6, 0.7), 2), (geo(7, 0.77), 2)),
+    5: ((geo(12, 0.82), 2), (geo(10, 0.8), 2)),
 }
 iters = 12 if cfg != 5 else 5
 for fr, hc in VARIANTS.get(cfg, VARIANTS[2]):
