@@ -1,4 +1,4 @@
-# GEMM plan comparison: packed (default) vs round-robin (TB_NO_PACKED_PLAN) on configs 2 and 3.
+# (Reverted experiment: the packed plan and TB_NO_PACKED_PLAN are in git history.) GEMM plan comparison on configs 2 and 3.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 for c in 2 3; do
