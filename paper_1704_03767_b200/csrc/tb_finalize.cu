@@ -119,27 +119,40 @@ __global__ void __launch_bounds__(256) full_counts_kernel(const int32_t* __restr
     pdl_trigger();
 }
 // ------------------------------------------------------------------ split-K accumulation
-static float* g_accum = nullptr;
-static size_t g_accum_bytes = 0;
-
+// One workspace per device (a process may drive several GPUs: compute_all_pairs(devices=...)).
 // The workspace stays zero between calls: accum_convert clears every entry it converts, so a GEMM finds it
 // zeroed without a memset in front of it (which would also break the sign pack -> GEMM programmatic
-// launch).  A fresh allocation, or a call whose convert never ran (g_accum_dirty), is cleared here.
-static bool g_accum_dirty = false;
+// launch).  A fresh allocation, or a call whose convert never ran (dirty), is cleared here.
+struct AccumWs {
+    float* p = nullptr;
+    size_t bytes = 0;
+    bool dirty = false;
+};
+constexpr int TB_MAX_DEVICES = 64;
+static AccumWs g_accum[TB_MAX_DEVICES];
+
+static int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
 
 int accum_workspace(int64_t span, float** ws, cudaStream_t st) {
+    const int dev = current_device();
+    if (dev < 0 || dev >= TB_MAX_DEVICES) return fail(TB_ERR_CONFIG, "accum_workspace: device %d", dev);
+    AccumWs& w = g_accum[dev];
     const size_t bytes = (size_t)((span + 3) & ~int64_t(3)) * sizeof(float);
-    if (bytes > g_accum_bytes) {
-        if (g_accum) TB_CUDA_TRY(cudaFree(g_accum));
-        g_accum = nullptr;
-        g_accum_bytes = 0;
-        TB_CUDA_TRY(cudaMalloc(&g_accum, bytes));
-        g_accum_bytes = bytes;
-        g_accum_dirty = true;
+    if (bytes > w.bytes) {
+        if (w.p) TB_CUDA_TRY(cudaFree(w.p));
+        w.p = nullptr;
+        w.bytes = 0;
+        TB_CUDA_TRY(cudaMalloc(&w.p, bytes));
+        w.bytes = bytes;
+        w.dirty = true;
     }
-    if (g_accum_dirty) TB_CUDA_TRY(cudaMemsetAsync(g_accum, 0, g_accum_bytes, st));
-    g_accum_dirty = true;  // until accum_convert has been enqueued
-    *ws = g_accum;
+    if (w.dirty) TB_CUDA_TRY(cudaMemsetAsync(w.p, 0, w.bytes, st));
+    w.dirty = true;  // until accum_convert has been enqueued
+    *ws = w.p;
     return TB_OK;
 }
 
@@ -158,7 +171,8 @@ int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st) 
     const int64_t blocks = std::min<int64_t>((span + 255) / 256, (int64_t)num_sms() * 8);
     TB_CUDA_TRY(launch_pdl(accum_convert_kernel, dim3((unsigned)blocks), dim3(256), 0, st, const_cast<float*>(ws), span, num));
     const int rc = check_launch("accum_convert_kernel");
-    if (rc == TB_OK) g_accum_dirty = false;
+    const int dev = current_device();
+    if (rc == TB_OK && dev >= 0 && dev < TB_MAX_DEVICES) g_accum[dev].dirty = false;
     return rc;
 }
 

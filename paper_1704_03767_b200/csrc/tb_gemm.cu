@@ -329,6 +329,7 @@ static int check_job_args(int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int
 // by 4 x 4 super-tiles, row-halves outer, so ~74 concurrently running pairs share A and B rows
 // through L2.  Cached per (m, job range).
 struct UnitTable {
+    int ordinal = -1;  // the device whose memory holds the table
     int64_t m = -1, lo = -1, hi = -1;
     int32_t* dev = nullptr;
     int64_t count = 0, cap = 0;
@@ -338,8 +339,10 @@ static int g_unit_next = 0;
 
 static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t st, const int32_t** out,
                        int64_t* count) {
+    int ordinal = 0;
+    TB_CUDA_TRY(cudaGetDevice(&ordinal));
     for (const UnitTable& c : g_unit_cache)
-        if (c.m == m && c.lo == job_lo && c.hi == job_hi) {
+        if (c.ordinal == ordinal && c.m == m && c.lo == job_lo && c.hi == job_hi) {
             *out = c.dev;
             *count = c.count;
             return TB_OK;
@@ -347,6 +350,14 @@ static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t s
     UnitTable& g_units = g_unit_cache[g_unit_next];
     g_unit_next = (g_unit_next + 1) % 32;
     g_units.m = -1;
+    if (g_units.ordinal != ordinal && g_units.dev) {  // the slot held another device's table
+        TB_CUDA_TRY(cudaSetDevice(g_units.ordinal));
+        cudaFree(g_units.dev);
+        TB_CUDA_TRY(cudaSetDevice(ordinal));
+        g_units.dev = nullptr;
+        g_units.cap = 0;
+    }
+    g_units.ordinal = ordinal;
     const int64_t T = gemm2::TILE, G = 4;
     const int64_t w = (m + T - 1) / T;
     const int64_t W = (w + G - 1) / G;

@@ -324,6 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
 // item, so the plan gives two-block units 3k splits and one-block units 2k (equal-cost items) or a
 // uniform split, whichever a simulation of the static schedule finishes first.
 struct Plan4 {
+    int ordinal = -1;  // the device whose memory holds the item table
     int64_t m = -1, lo = -1, hi = -1;
     int32_t nkb = -1, forced = -1, pairs = -1;
     int4* dev = nullptr;
@@ -397,14 +398,25 @@ static double plan_items4(const std::vector<int32_t>& code, const std::vector<in
 
 static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, int32_t forced, int pairs,
                        cudaStream_t st, const Plan4** out) {
+    int ordinal = 0;
+    TB_CUDA_TRY(cudaGetDevice(&ordinal));
     for (const Plan4& c : g_plans4)
-        if (c.m == m && c.lo == job_lo && c.hi == job_hi && c.nkb == nkb && c.forced == forced && c.pairs == pairs) {
+        if (c.ordinal == ordinal && c.m == m && c.lo == job_lo && c.hi == job_hi && c.nkb == nkb && c.forced == forced &&
+            c.pairs == pairs) {
             *out = &c;
             return TB_OK;
         }
     Plan4& g_plan4 = g_plans4[g_plans4_next];
     g_plans4_next = (g_plans4_next + 1) % PLAN_CACHE;
     g_plan4.m = -1;
+    if (g_plan4.ordinal != ordinal && g_plan4.dev) {  // the slot held another device's item table
+        TB_CUDA_TRY(cudaSetDevice(g_plan4.ordinal));
+        cudaFree(g_plan4.dev);
+        TB_CUDA_TRY(cudaSetDevice(ordinal));
+        g_plan4.dev = nullptr;
+        g_plan4.cap = 0;
+    }
+    g_plan4.ordinal = ordinal;
     std::vector<int32_t> code, nb, ncols;
     list_units4(m, job_lo, job_hi, code, nb, ncols);
     std::vector<int32_t> su(code.size(), 1), best_su;
