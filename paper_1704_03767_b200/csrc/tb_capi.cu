@@ -42,6 +42,8 @@ int num_sms() {
     return n > 0 ? n : 148;
 }
 
+std::mutex g_native_state_mutex;
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("TB_NO_PDL");

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <algorithm>
 #include <cuda_runtime.h>
+#include <mutex>
 
 #include "../../include/taub200.h"
 
@@ -21,6 +22,9 @@ int check_launch(const char* what);
     } while (0)
 
 int num_sms();
+
+// Guards the per-device native caches (GEMM plans / unit tables, split-K workspaces) across host threads.
+extern std::mutex g_native_state_mutex;
 
 // Split-K accumulation (tb_finalize.cu): an f32 device buffer of span (rounded up to 4) sums the
 // split partials with vector reds (exact: every partial and every running sum is an integer of

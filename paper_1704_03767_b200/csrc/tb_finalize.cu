@@ -9,6 +9,8 @@
 // sqrt((n0 - n1_y) * (n0 - n1_x)) with IEEE round-to-nearest __ddiv_rn /
 // __dsqrt_rn / __dmul_rn (no FMA contraction), exactly the operation sequence
 // numpy executes in derive_taus.
+#include <mutex>
+
 #include "tb_common.cuh"
 
 namespace tb {
@@ -138,6 +140,7 @@ static int current_device() {
 }
 
 int accum_workspace(int64_t span, float** ws, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);  // host threads share the caches
     const int dev = current_device();
     if (dev < 0 || dev >= TB_MAX_DEVICES) return fail(TB_ERR_CONFIG, "accum_workspace: device %d", dev);
     AccumWs& w = g_accum[dev];
@@ -172,6 +175,7 @@ int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st) 
     TB_CUDA_TRY(launch_pdl(accum_convert_kernel, dim3((unsigned)blocks), dim3(256), 0, st, const_cast<float*>(ws), span, num));
     const int rc = check_launch("accum_convert_kernel");
     const int dev = current_device();
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);
     if (rc == TB_OK && dev >= 0 && dev < TB_MAX_DEVICES) g_accum[dev].dirty = false;
     return rc;
 }

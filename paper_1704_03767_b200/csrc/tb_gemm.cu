@@ -20,6 +20,8 @@
 #include <vector>
 #include <cudaTypedefs.h>
 
+#include <mutex>
+
 #include "tb_common.cuh"
 #include "tb_ptx.cuh"
 
@@ -339,6 +341,7 @@ static int g_unit_next = 0;
 
 static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t st, const int32_t** out,
                        int64_t* count) {
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);  // host threads share the caches
     int ordinal = 0;
     TB_CUDA_TRY(cudaGetDevice(&ordinal));
     for (const UnitTable& c : g_unit_cache)

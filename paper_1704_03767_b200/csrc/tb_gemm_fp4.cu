@@ -18,6 +18,8 @@
 #include <vector>
 #include <cudaTypedefs.h>
 
+#include <mutex>
+
 #include "tb_common.cuh"
 #include "tb_ptx.cuh"
 
@@ -398,6 +400,7 @@ static double plan_items4(const std::vector<int32_t>& code, const std::vector<in
 
 static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, int32_t forced, int pairs,
                        cudaStream_t st, const Plan4** out) {
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);  // host threads share the caches
     int ordinal = 0;
     TB_CUDA_TRY(cudaGetDevice(&ordinal));
     for (const Plan4& c : g_plans4)
