@@ -130,6 +130,18 @@ int tb_abs_pack(const int8_t *S, int64_t m, int64_t ldS, int format, int8_t *A, 
 int tb_full_counts(const int32_t *num, const int32_t *absdot, const uint64_t *n1_rows, int64_t m, int64_t n,
                    int64_t job_lo, int64_t job_hi, uint64_t *nd, uint64_t *n3, void *stream);
 
+/*
+ * Reference record stream: the 48-byte CELL_DTYPE records (src/taucorr/engine.py:45-55:
+ * i, j, numerator, n_d, n1, n2, n3) of tiles [tile_lo, tile_lo + ntiles) of the q x q tile matrix in the
+ * reference's emission order (pairindex.py:116-129; the per-tile loops of engine.py:170-238), gathered on the
+ * device from job-id-ordered counts (num / nd / n3 indexed by job id - job_lo, n1 per row).  tile_offsets[t]
+ * is the first record of tile t within the pass.  naive != 0 writes the naive kernel's zero counts.
+ * Replaces the host-side record assembly of compute_all_pairs (engine.py:366-376).
+ */
+int tb_records(const int32_t *num, const int64_t *nd, const int64_t *n3, const int64_t *n1_rows, int64_t m,
+               int64_t q, int64_t job_lo, int64_t tile_lo, int64_t ntiles, const int64_t *tile_offsets,
+               int naive, void *records, void *stream);
+
 /* Same contract on CUDA cores (dp4a, TB_SIGN_I8 only); a GPU-side cross-check, not the product path. */
 int tb_gemm_pairs_simt(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
                        int32_t *num, void *stream);

@@ -45,6 +45,7 @@ SIGNATURES = {
     "tb_full_counts": ([_p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "tb_presort": ([_p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
     "tb_merge_pairs": ([_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
+    "tb_records": ([_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, ctypes.c_int, _p, _p], ctypes.c_int),
 }
 
 

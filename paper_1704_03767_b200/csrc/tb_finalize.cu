@@ -197,3 +197,69 @@ extern "C" int tb_full_counts(const int32_t* num, const int32_t* absdot, const u
                            reinterpret_cast<unsigned long long*>(n3)));
     return check_launch("full_counts_kernel");
 }
+
+// ------------------------------------------------------------------ reference record stream (f1)
+// 48-byte CELL_DTYPE records (engine.py:45-55: i u4, j u4, numerator i8, n_d u8, n1 u8, n2 u8, n3 u8) of
+// the tiles [tile_lo, tile_lo + ntiles) of the q x q tile matrix, in the reference's emission order
+// (pairindex.py:116-129: ascending tile id, row-major inside a tile with j from max(i, tile column start)),
+// gathered on the device from job-id-ordered counts, so the host only copies the finished pass buffer.
+// off[t] = first record index of tile t within the pass (host prefix of the per-tile cell counts).
+namespace tb {
+__global__ void __launch_bounds__(256) records_kernel(const int32_t* __restrict__ num,
+                                                      const int64_t* __restrict__ nd,
+                                                      const int64_t* __restrict__ n3,
+                                                      const int64_t* __restrict__ n1, int64_t m, int64_t q,
+                                                      int64_t w, int64_t job_lo, int64_t tile_lo,
+                                                      const int64_t* __restrict__ off, int naive,
+                                                      uint4* __restrict__ out) {
+    pdl_wait();
+    const int64_t t = blockIdx.x;
+    int64_t ty, tx;
+    job_coord(tile_lo + t, w, ty, tx);  // the triangular bijection on the tile matrix (pairindex.py:58-65)
+    const int64_t c0 = tx * q, cend = min(c0 + q, m);
+    const int64_t base = __ldg(&off[t]);
+    for (int64_t k = threadIdx.x; k < q * q; k += blockDim.x) {
+        const int64_t r = k / q, c = k - r * q;
+        const int64_t i = ty * q + r, j = c0 + c;
+        if (i >= m || j >= m || j < i) continue;
+        int64_t pos = base + (j - max(i, c0));
+        for (int64_t rr = 0; rr < r; ++rr) {  // cells of the rows above in this tile
+            const int64_t ii = ty * q + rr;
+            if (ii < m) { const int64_t cnt = cend - max(ii, c0); pos += cnt > 0 ? cnt : 0; }
+        }
+        const int64_t jid = i * (2 * m - i + 1) / 2 + (j - i) - job_lo;
+        const uint64_t ij = (uint64_t)(uint32_t)i | ((uint64_t)(uint32_t)j << 32);
+        const int64_t numv = num[jid];
+        uint64_t v_nd = 0, v_n1 = 0, v_n2 = 0, v_n3 = 0;
+        if (!naive) {
+            v_nd = (uint64_t)nd[jid];
+            v_n3 = (uint64_t)n3[jid];
+            v_n1 = (uint64_t)__ldg(&n1[i]);
+            v_n2 = (uint64_t)__ldg(&n1[j]);
+        }
+        uint4* rec = out + 3 * pos;
+        rec[0] = make_uint4((uint32_t)ij, (uint32_t)(ij >> 32), (uint32_t)numv, (uint32_t)((uint64_t)numv >> 32));
+        rec[1] = make_uint4((uint32_t)v_nd, (uint32_t)(v_nd >> 32), (uint32_t)v_n1, (uint32_t)(v_n1 >> 32));
+        rec[2] = make_uint4((uint32_t)v_n2, (uint32_t)(v_n2 >> 32), (uint32_t)v_n3, (uint32_t)(v_n3 >> 32));
+    }
+    pdl_trigger();
+}
+}  // namespace tb
+
+extern "C" int tb_records(const int32_t* num, const int64_t* nd, const int64_t* n3, const int64_t* n1_rows, int64_t m,
+                          int64_t q, int64_t job_lo, int64_t tile_lo, int64_t ntiles, const int64_t* tile_offsets,
+                          int naive, void* records, void* stream) {
+    if (m < 1 || q < 1) return fail(TB_ERR_CONFIG, "records: need m >= 1 and q >= 1");
+    if (ntiles < 0 || tile_lo < 0) return fail(TB_ERR_CONFIG, "records: bad tile range");
+    if (ntiles == 0) return TB_OK;
+    if (!num || !tile_offsets || !records || (!naive && (!nd || !n3 || !n1_rows)))
+        return fail(TB_ERR_INVALID, "records: null pointer");
+    if (ntiles > INT32_MAX) return fail(TB_ERR_CAPACITY, "records: too many tiles per pass");
+    const int64_t w = (m + q - 1) / q;
+    if (tile_lo + ntiles > w * (w + 1) / 2) return fail(TB_ERR_CONFIG, "records: tile range outside the matrix");
+    const int threads = (int)std::min<int64_t>(256, ((q * q + 31) / 32) * 32);
+    TB_CUDA_TRY(launch_pdl(records_kernel, dim3((unsigned)ntiles), dim3(threads), 0, static_cast<cudaStream_t>(stream),
+                           num, nd, n3, n1_rows, m, q, w, job_lo, tile_lo, tile_offsets, naive,
+                           reinterpret_cast<uint4*>(records)));
+    return check_launch("records_kernel");
+}
