@@ -743,11 +743,12 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
             cross = (int64_t)ksum + (int64_t)ties;
         }
 
-        const int64_t tot_inv = block_reduce_sum((int64_t)(int32_t)inv + cross + clamp_fix, red) - (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
-        const int64_t tot_g = block_reduce_sum((int64_t)inv_g, red);
+        // n_d = inv(w) - sum_g inv_g(w): one reduction of (inv - inv_g), one of the joint ties
+        const int64_t nd_all = block_reduce_sum((int64_t)(int32_t)inv + cross + clamp_fix - (int64_t)inv_g, red) -
+                               (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
         const int64_t tot_t = block_reduce_sum((int64_t)ties, red);
         if (tid == 0) {
-            const int64_t nd = tot_inv - tot_g;
+            const int64_t nd = nd_all;
             const int64_t n3 = tot_t;
             const int64_t num = p.n0 - (int64_t)p.n1[y] - (int64_t)p.n1[x] + n3 - 2 * nd;  // result.py:42
             p.num[idx] = (int32_t)num;
