@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--gather", action="store_true",
@@ -64,7 +64,6 @@ def parse():
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay the device step as one CUDA graph (auto: config 1, whose step is launch-bound)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
 
@@ -126,40 +125,44 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def cpu_pairs_rate(ranks: np.ndarray, seconds: float, threads: int, seed: int = 99):
-    """Time the oracle port on a bounded random pair sample; returns (pairs/s, sample description)."""
+# SURVEY 8(d) CPU protocol: configs 1 and 2 run every pair; configs 3 and 5 a seeded subset of m' = 2048
+# variables (every pair among them), config 4 m' = 64, drawn with np.random.default_rng(99).choice(m, m').
+CPU_SUBSET = {1: None, 2: None, 3: 2048, 4: 64, 5: 2048}
+
+
+def cpu_subset(k: int, m: int, size: int | None = None) -> np.ndarray:
+    """Row indices of the CPU-timed variable subset of config k (sorted; all rows for configs 1-2)."""
+    sz = CPU_SUBSET.get(k) if size is None else size
+    if sz is None or sz >= m:
+        return np.arange(m)
+    return np.sort(np.random.default_rng(99).choice(m, sz, replace=False))
+
+
+def cpu_pairs_rate(x: np.ndarray, rows: np.ndarray, threads: int):
+    """Time the oracle port on every i<j pair of the variable subset ``rows`` of the raw values ``x``
+    (ranked first, outside the timer like the reference's rank_transform); returns
+    (pairs/s, kernel name, pair count, seconds)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc  # CPU baseline leg only
 
-    m, n = ranks.shape
-    kernel = orc.KERNEL_PACKED if (n <= 32767 and ranks.max() < 1 << 15) else orc.KERNEL_SORTED
-    rng = np.random.default_rng(seed)
-    # size the sample from a probe long enough (>= 0.5 s) that thread start-up does not skew the rate
-    probe = max(threads * 4, 64)
-    while True:
-        pi, pj = _sample_pairs(rng, m, probe)
-        t0 = time.perf_counter()
-        orc.all_pairs(ranks, pi, pj, kernel, threads=threads, want_counts=False)
-        dt = max(time.perf_counter() - t0, 1e-6)
-        if dt >= 0.5 or probe >= m * (m - 1) // 2:
-            break
-        probe = int(probe * min(16.0, max(2.0, 0.6 / dt)))
-    count = int(max(probe, min(m * (m - 1) // 2, probe / dt * seconds)))
-    pi, pj = _sample_pairs(rng, m, count)
+    sub = np.ascontiguousarray(host_ranks(x[rows]))
+    ms, n = sub.shape
+    kernel = orc.KERNEL_PACKED if (n <= 32767 and sub.max() < 1 << 15) else orc.KERNEL_SORTED
+    pi, pj = orc.upper_pairs(ms, diagonal=False)
     t0 = time.perf_counter()
-    orc.all_pairs(ranks, pi, pj, kernel, threads=threads, want_counts=False)
+    orc.all_pairs(sub, pi, pj, kernel, threads=threads, want_counts=True)
     dt = time.perf_counter() - t0
     kname = "packed (VSE semantics, kernel_vectorized.py:507-523)" if kernel == orc.KERNEL_PACKED else \
         "sorted (GSE, kernel_sorted.py:195-212)"
-    return count / dt, f"{count} random i<j pairs of the workload (rng 99), oracle {kname}, {dt:.1f}s", count, dt
+    return pi.shape[0] / dt, kname, int(pi.shape[0]), dt
 
 
-def _sample_pairs(rng, m, count):
-    i = rng.integers(0, m, count * 2)
-    j = rng.integers(0, m, count * 2)
-    keep = i != j
-    i, j = i[keep][:count], j[keep][:count]
-    return np.minimum(i, j).astype(np.int64), np.maximum(i, j).astype(np.int64)
+def cpu_sample_text(k: int, m: int, rows: np.ndarray, count: int, dt: float, kname: str, threads: int) -> str:
+    what = (f"every i<j pair of all {m} variables" if rows.shape[0] == m else
+            f"every i<j pair of a {rows.shape[0]}-variable subset (np.random.default_rng(99).choice({m}, "
+            f"{rows.shape[0]}, replace=False), SURVEY 8(d))")
+    return (f"{count} pairs = {what}; oracle port of the reference {kname} with all counts "
+            f"(n_d, n1, n2, n3), {threads} threads, {dt:.1f} s")
 
 
 def workload(k: int):
@@ -170,50 +173,45 @@ def workload(k: int):
 
 
 def host_ranks(x: np.ndarray) -> np.ndarray:
-    from paper_1704_03767_b200.ranks import rank_transform
-    if x.dtype == np.int32 and x.min() >= 0 and x.max() < x.shape[1]:
-        # already dense ranks when every value 0..max occurs (config 2); verify cheaply per row
-        ok = all(len(np.unique(r)) == int(r.max()) + 1 for r in x[:8])
-        if ok:
-            return np.stack([rank_transform(r) for r in x])
-    return np.stack([rank_transform(r) for r in x])
+    """Dense ranks per row for the CPU legs (the reference ranks outside its timer, dataio.py:194-196)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc  # CPU legs only
+    return orc.rank_matrix(x)
 
 
 def run_reference(args):
+    """The reference's CPU path (oracle port, all host threads) on this arm's workload: every step times
+    every pair of the SURVEY 8(d) variable subset (shrunk if the whole run would exceed ~3 min)."""
     rank, _, world = dist_env()
     if rank != 0:
         return
     spec, x = workload(args.config)
-    ranks = host_ranks(x)
     threads = os.cpu_count() or 1
-    m, n = ranks.shape
+    m, n = x.shape
     total_steps = args.steps + args.warmup
-    per_step = max(0.05, min(2.0, 150.0 / max(total_steps, 1)))
-    rate0, _, _, _ = cpu_pairs_rate(ranks, per_step, threads)
-    count = max(threads * 4, int(rate0 * per_step))
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as orc
-    kernel = orc.KERNEL_PACKED if (n <= 32767 and ranks.max() < 1 << 15) else orc.KERNEL_SORTED
-    rng = np.random.default_rng(99)
+    rows = cpu_subset(args.config, m)
+    # probe one step; shrink the subset (pairs ~ m'^2) so that all steps fit the budget
+    rate0, _, cnt0, dt0 = cpu_pairs_rate(x, rows, threads)
+    budget = 180.0 / max(total_steps, 1)
+    if dt0 > budget and rows.shape[0] > 64:
+        keep = max(64, int(rows.shape[0] * (budget / dt0) ** 0.5))
+        rows = cpu_subset(args.config, m, keep)
     times = []
     for s in range(total_steps):
-        pi, pj = _sample_pairs(rng, m, count)
-        t0 = time.perf_counter()
-        orc.all_pairs(ranks, pi, pj, kernel, threads=threads, want_counts=False)
+        rate, kname, count, dt = cpu_pairs_rate(x, rows, threads)
         if s >= args.warmup:
-            times.append(time.perf_counter() - t0)
+            times.append(dt)
     tot = sum(times)
     value = count * len(times) / tot
-    sample = (f"{count} random i<j pairs per step of {spec.name} (rng 99); oracle port of the reference "
-              f"{'packed/VSE' if kernel == orc.KERNEL_PACKED else 'GSE merge-sort'} kernel, {threads} threads")
+    sample = cpu_sample_text(args.config, m, rows, count, tot / len(times), kname, threads) + " per step"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
-        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic",
-        "config": {"workload": f"config{args.config}_{spec.name}", "m": m, "n": n, "pairs_per_rank": m * (m - 1) // 2,
-                   "path": "gemm" if n <= 8192 else "merge",
-                   "outputs": "numerator i32 + tau_a f64 + tau_b f64 in job-id order"},
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"config{args.config}_{spec.name}", "m": m, "n": n,
+                   "pairs_timed_per_step": count, "path": "cpu",
+                   "outputs": "numerator + n_d/n1/n2/n3 per pair (the reference's CELL_DTYPE fields)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -336,9 +334,7 @@ def run_ours(args):
     eng = TauEngine(local)
     stream = torch.cuda.Stream(device=dev)
     path = eng.choose_path(n)
-    xin = x
-    if path == "merge":
-        xin = host_ranks(x)
+    xin = x  # raw values: both paths rank on the device (K0 / K0w)
     xd = torch.from_numpy(np.ascontiguousarray(xin)).to(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     K = n * (n - 1) // 2
@@ -519,10 +515,11 @@ def run_ours(args):
                     "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            ranks = host_ranks(x)
             threads = os.cpu_count() or 1
-            rate, sample, _, _ = cpu_pairs_rate(ranks, args.cpu_seconds, threads)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+            rows = cpu_subset(args.config, m)
+            rate, kname, count, dt = cpu_pairs_rate(x, rows, threads)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": cpu_sample_text(args.config, m, rows, count, dt, kname, threads)}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

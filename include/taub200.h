@@ -86,6 +86,20 @@ int tb_rank_rows(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, ui
                  uint64_t *n1, int32_t *flags, void *stream);
 
 /*
+ * K0w rank transform for rows of any width (rank_transform, src/taucorr/ranks.py:37-61; the per-row loop
+ * of dataio.py:194-196): dense 0-based int32 ranks, ties share a rank, -0.0 == +0.0, +-inf orderable.
+ * The merge path's input stage (raw values -> tb_presort); one CTA per row, stable LSD radix sort.
+ *   x         [m, ldx] values (TB_DTYPE_*), any n >= 1
+ *   R         [m, ldr] int32 ranks out
+ *   n1        [m] uint64 tied-pair count sum_t t(t-1)/2 per row (kernel_sorted.py:163-176)
+ *   flags     device int32; bit 0 set when a NaN was seen (ranks.py:56-57)
+ *   workspace device scratch of >= tb_rank_dense_workspace(m, n, dtype) bytes (for the current device)
+ */
+int64_t tb_rank_dense_workspace(int64_t m, int64_t n, int dtype);
+int tb_rank_dense(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, int32_t *R, int64_t ldr, uint64_t *n1,
+                  int32_t *flags, void *workspace, int64_t ws_bytes, void *stream);
+
+/*
  * K2 sign pack.  Replaces the per-pair sign enumeration of naive_numerator
  * (src/taucorr/kernel_naive.py:26-44), materialising each variable's sign
  * vector once.
@@ -134,13 +148,20 @@ int tb_full_counts(const int32_t *num, const int32_t *absdot, const uint64_t *n1
  * Reference record stream: the 48-byte CELL_DTYPE records (src/taucorr/engine.py:45-55:
  * i, j, numerator, n_d, n1, n2, n3) of tiles [tile_lo, tile_lo + ntiles) of the q x q tile matrix in the
  * reference's emission order (pairindex.py:116-129; the per-tile loops of engine.py:170-238), gathered on the
- * device from job-id-ordered counts (num / nd / n3 indexed by job id - job_lo, n1 per row).  tile_offsets[t]
- * is the first record of tile t within the pass.  naive != 0 writes the naive kernel's zero counts.
- * Replaces the host-side record assembly of compute_all_pairs (engine.py:366-376).
+ * device from job-id-ordered counts (num / nd / n3 indexed by job id - job_lo, n1 per row).  Every cell of
+ * the tiles must have its job id in [job_lo, job_hi) (else TB_ERR_CONFIG).  Record k of the pass is the
+ * k-th cell of the tiles in emission order (offsets are closed forms, see tb_tile_cells).  naive != 0
+ * writes the naive kernel's zero counts.  Replaces the host-side record assembly of compute_all_pairs
+ * (engine.py:366-376) and _pass_geometry (engine.py:261-276).
  */
 int tb_records(const int32_t *num, const int64_t *nd, const int64_t *n3, const int64_t *n1_rows, int64_t m,
-               int64_t q, int64_t job_lo, int64_t tile_lo, int64_t ntiles, const int64_t *tile_offsets,
-               int naive, void *records, void *stream);
+               int64_t q, int64_t job_lo, int64_t job_hi, int64_t tile_lo, int64_t ntiles, int naive, void *records,
+               void *stream);
+
+/* Cells (records) in tiles [tile_lo, tile_hi) of the q x q tile matrix over m variables, diagonal
+ * included -- the sum of tile_cell_count (pairindex.py:107-112) in closed form; -1 on bad arguments.
+ * Host-only, no device work. */
+int64_t tb_tile_cells(int64_t m, int64_t q, int64_t tile_lo, int64_t tile_hi);
 
 /* Same contract on CUDA cores (dp4a, TB_SIGN_I8 only); a GPU-side cross-check, not the product path. */
 int tb_gemm_pairs_simt(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi,
@@ -183,11 +204,14 @@ int tb_presort(const int32_t *ranks, int64_t m, int64_t n, int32_t *pos, int32_t
  * numerator n0 - n1 - n2 + n3 - 2 n_d (src/taucorr/result.py:42).  Replaces
  * steps 1-5 of sorted_counts (src/taucorr/kernel_sorted.py:195-212).
  * keys, pos, sorted, n1_rows, maxgrp, groups and ngroups are tb_presort's outputs.
- * nd / n3 may be NULL.
+ * nd / n3 may be NULL.  workspace: device scratch of >= tb_merge_workspace(n) bytes (for the current
+ * device), used by pairs whose u variable has a tie group larger than 64 (the O(n log n) segmented count).
  */
+int64_t tb_merge_workspace(int64_t n);
 int tb_merge_pairs(const uint16_t *keys, const int32_t *pos, const int32_t *sorted, const uint64_t *n1_rows,
                    const int32_t *maxgrp, const int32_t *groups, const int32_t *ngroups, int64_t m, int64_t n,
-                   int64_t job_lo, int64_t job_hi, int32_t *num, uint64_t *nd, uint64_t *n3, void *stream);
+                   int64_t job_lo, int64_t job_hi, int32_t *num, uint64_t *nd, uint64_t *n3, void *workspace,
+                   int64_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

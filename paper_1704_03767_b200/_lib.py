@@ -27,7 +27,7 @@ TB_SIGN_I8, TB_SIGN_E4M3, TB_SIGN_E2M1 = 0, 1, 2
 TB_MAX_N = 65536
 
 # Every exported symbol and its ctypes signature (kept in sync with include/taub200.h;
-# tests/test_capi_symbols.py checks both directions).
+# tests/test_host.py::test_capi_exports_every_declared_symbol checks both directions).
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
 _p = ctypes.c_void_p
@@ -37,6 +37,8 @@ SIGNATURES = {
     "tb_query": ([ctypes.c_int, _p], ctypes.c_int),
     "tb_sign_k": ([_i64], _i64),
     "tb_rank_rows": ([_p, ctypes.c_int, _i64, _i64, _i64, _p, _i64, _p, _p, _p], ctypes.c_int),
+    "tb_rank_dense_workspace": ([_i64, _i64, ctypes.c_int], _i64),
+    "tb_rank_dense": ([_p, ctypes.c_int, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _i64, _p], ctypes.c_int),
     "tb_sign_pack": ([_p, _i64, _i64, _i64, _p, _i64, ctypes.c_int, _p], ctypes.c_int),
     "tb_abs_pack": ([_p, _i64, _i64, ctypes.c_int, _p, _p], ctypes.c_int),
     "tb_gemm_pairs": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _p], ctypes.c_int),
@@ -44,8 +46,10 @@ SIGNATURES = {
     "tb_finalize": ([_p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "tb_full_counts": ([_p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "tb_presort": ([_p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
-    "tb_merge_pairs": ([_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
-    "tb_records": ([_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _p, ctypes.c_int, _p, _p], ctypes.c_int),
+    "tb_merge_workspace": ([_i64], _i64),
+    "tb_merge_pairs": ([_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _p], ctypes.c_int),
+    "tb_records": ([_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _p, _p], ctypes.c_int),
+    "tb_tile_cells": ([_i64, _i64, _i64, _i64], _i64),
 }
 
 

@@ -44,6 +44,45 @@ int num_sms() {
 
 std::mutex g_native_state_mutex;
 
+int table_upload(DevTable& t, const void* src, size_t bytes, cudaStream_t st) {
+    int ordinal = 0;
+    TB_CUDA_TRY(cudaGetDevice(&ordinal));
+    if (t.ordinal != ordinal && t.ordinal >= 0) {  // the slot held another device's table
+        TB_CUDA_TRY(cudaSetDevice(t.ordinal));
+        if (t.inuse) cudaEventSynchronize(t.inuse);
+        if (t.dev) cudaFree(t.dev);
+        if (t.host) cudaFreeHost(t.host);
+        if (t.inuse) cudaEventDestroy(t.inuse);
+        TB_CUDA_TRY(cudaSetDevice(ordinal));
+        t = DevTable{};
+    }
+    t.ordinal = ordinal;
+    if (!t.inuse) TB_CUDA_TRY(cudaEventCreateWithFlags(&t.inuse, cudaEventDisableTiming));
+    else TB_CUDA_TRY(cudaEventSynchronize(t.inuse));  // earlier copies / readers of this slot are done
+    const size_t need = std::max<size_t>(bytes, 16);
+    if (need > t.cap) {
+        if (t.dev) cudaFree(t.dev);
+        if (t.host) cudaFreeHost(t.host);
+        t.dev = t.host = nullptr;
+        t.cap = 0;
+        TB_CUDA_TRY(cudaMalloc(&t.dev, need));
+        TB_CUDA_TRY(cudaHostAlloc(&t.host, need, cudaHostAllocDefault));
+        t.cap = need;
+    }
+    if (bytes) {
+        std::memcpy(t.host, src, bytes);
+        TB_CUDA_TRY(cudaMemcpyAsync(t.dev, t.host, bytes, cudaMemcpyHostToDevice, st));
+    }
+    TB_CUDA_TRY(cudaEventRecord(t.inuse, st));
+    return TB_OK;
+}
+
+int table_mark_used(DevTable& t, cudaStream_t st) {
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);
+    if (t.inuse) TB_CUDA_TRY(cudaEventRecord(t.inuse, st));
+    return TB_OK;
+}
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("TB_NO_PDL");

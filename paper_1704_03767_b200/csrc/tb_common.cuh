@@ -26,6 +26,21 @@ int num_sms();
 // Guards the per-device native caches (GEMM plans / unit tables, split-K workspaces) across host threads.
 extern std::mutex g_native_state_mutex;
 
+// A device-resident lookup table (GEMM item / unit tables) uploaded without a host sync: the bytes are
+// staged in pinned memory and copied on the caller's stream; `inuse` is recorded after the upload and
+// after every launch that reads the table, and a later upload into the same slot first waits for it
+// (normally long complete), so neither the staging buffer nor the device table is overwritten while a
+// copy or kernel on any stream may still read it.  Callers hold g_native_state_mutex.
+struct DevTable {
+    int ordinal = -1;
+    void* dev = nullptr;
+    void* host = nullptr;
+    size_t cap = 0;
+    cudaEvent_t inuse = nullptr;
+};
+int table_upload(DevTable& t, const void* src, size_t bytes, cudaStream_t st);
+int table_mark_used(DevTable& t, cudaStream_t st);
+
 // Split-K accumulation (tb_finalize.cu): an f32 device buffer of span (rounded up to 4) sums the
 // split partials with vector reds (exact: every partial and every running sum is an integer of
 // magnitude < 2^24 when K < 2^24), then accum_convert writes the int32 numerators.

@@ -203,31 +203,38 @@ extern "C" int tb_full_counts(const int32_t* num, const int32_t* absdot, const u
 // the tiles [tile_lo, tile_lo + ntiles) of the q x q tile matrix, in the reference's emission order
 // (pairindex.py:116-129: ascending tile id, row-major inside a tile with j from max(i, tile column start)),
 // gathered on the device from job-id-ordered counts, so the host only copies the finished pass buffer.
-// off[t] = first record index of tile t within the pass (host prefix of the per-tile cell counts).
+// Record offsets are closed forms (no host prefix array, no per-cell loop over the rows above):
+//   cells before tile (ty, tx) = row_prefix(ty q) + [tx > ty] sum_{i in tile rows} (tx q - i)
+//   cells before row r of that tile = r (c1 - c0) off the diagonal, r (c1 - r0) - r (r - 1) / 2 on it.
 namespace tb {
+__host__ __device__ __forceinline__ int64_t cells_before_tile(int64_t t, int64_t m, int64_t q, int64_t w) {
+    int64_t ty, tx;
+    job_coord(t, w, ty, tx);
+    const int64_t r0 = ty * q, s = min(r0 + q, m) - r0;
+    int64_t c = row_prefix(r0, m);
+    if (tx > ty) c += s * tx * q - (s * r0 + s * (s - 1) / 2);
+    return c;
+}
+
 __global__ void __launch_bounds__(256) records_kernel(const int32_t* __restrict__ num,
                                                       const int64_t* __restrict__ nd,
                                                       const int64_t* __restrict__ n3,
                                                       const int64_t* __restrict__ n1, int64_t m, int64_t q,
-                                                      int64_t w, int64_t job_lo, int64_t tile_lo,
-                                                      const int64_t* __restrict__ off, int naive,
-                                                      uint4* __restrict__ out) {
+                                                      int64_t w, int64_t job_lo, int64_t tile_lo, int64_t base0,
+                                                      int naive, uint4* __restrict__ out) {
     pdl_wait();
-    const int64_t t = blockIdx.x;
+    const int64_t t = tile_lo + blockIdx.x;
     int64_t ty, tx;
-    job_coord(tile_lo + t, w, ty, tx);  // the triangular bijection on the tile matrix (pairindex.py:58-65)
-    const int64_t c0 = tx * q, cend = min(c0 + q, m);
-    const int64_t base = __ldg(&off[t]);
+    job_coord(t, w, ty, tx);  // the triangular bijection on the tile matrix (pairindex.py:58-65)
+    const int64_t r0 = ty * q, c0 = tx * q, cend = min(c0 + q, m);
+    const int64_t base = cells_before_tile(t, m, q, w) - base0;
     for (int64_t k = threadIdx.x; k < q * q; k += blockDim.x) {
         const int64_t r = k / q, c = k - r * q;
-        const int64_t i = ty * q + r, j = c0 + c;
+        const int64_t i = r0 + r, j = c0 + c;
         if (i >= m || j >= m || j < i) continue;
-        int64_t pos = base + (j - max(i, c0));
-        for (int64_t rr = 0; rr < r; ++rr) {  // cells of the rows above in this tile
-            const int64_t ii = ty * q + rr;
-            if (ii < m) { const int64_t cnt = cend - max(ii, c0); pos += cnt > 0 ? cnt : 0; }
-        }
-        const int64_t jid = i * (2 * m - i + 1) / 2 + (j - i) - job_lo;
+        const int64_t above = tx > ty ? r * (cend - c0) : r * (cend - r0) - r * (r - 1) / 2;
+        const int64_t pos = base + above + (j - max(i, c0));
+        const int64_t jid = row_prefix(i, m) + (j - i) - job_lo;
         const uint64_t ij = (uint64_t)(uint32_t)i | ((uint64_t)(uint32_t)j << 32);
         const int64_t numv = num[jid];
         uint64_t v_nd = 0, v_n1 = 0, v_n2 = 0, v_n3 = 0;
@@ -246,20 +253,44 @@ __global__ void __launch_bounds__(256) records_kernel(const int32_t* __restrict_
 }
 }  // namespace tb
 
+extern "C" int64_t tb_tile_cells(int64_t m, int64_t q, int64_t tile_lo, int64_t tile_hi) {
+    if (m < 1 || q < 1) return -1;
+    const int64_t w = (m + q - 1) / q, tt = w * (w + 1) / 2;
+    if (tile_lo < 0 || tile_hi < tile_lo || tile_hi > tt) return -1;
+    const int64_t total = m * (m + 1) / 2;
+    const int64_t a = tile_lo == tt ? total : cells_before_tile(tile_lo, m, q, w);
+    const int64_t b = tile_hi == tt ? total : cells_before_tile(tile_hi, m, q, w);
+    return b - a;
+}
+
 extern "C" int tb_records(const int32_t* num, const int64_t* nd, const int64_t* n3, const int64_t* n1_rows, int64_t m,
-                          int64_t q, int64_t job_lo, int64_t tile_lo, int64_t ntiles, const int64_t* tile_offsets,
-                          int naive, void* records, void* stream) {
+                          int64_t q, int64_t job_lo, int64_t job_hi, int64_t tile_lo, int64_t ntiles, int naive,
+                          void* records, void* stream) {
     if (m < 1 || q < 1) return fail(TB_ERR_CONFIG, "records: need m >= 1 and q >= 1");
     if (ntiles < 0 || tile_lo < 0) return fail(TB_ERR_CONFIG, "records: bad tile range");
     if (ntiles == 0) return TB_OK;
-    if (!num || !tile_offsets || !records || (!naive && (!nd || !n3 || !n1_rows)))
+    if (!num || !records || (!naive && (!nd || !n3 || !n1_rows)))
         return fail(TB_ERR_INVALID, "records: null pointer");
     if (ntiles > INT32_MAX) return fail(TB_ERR_CAPACITY, "records: too many tiles per pass");
     const int64_t w = (m + q - 1) / q;
     if (tile_lo + ntiles > w * (w + 1) / 2) return fail(TB_ERR_CONFIG, "records: tile range outside the matrix");
+    // every cell of the tiles must lie in the counts' job range [job_lo, job_hi): the smallest job id is
+    // the first cell of the first tile, the largest the last cell of the last tile's bottom row (job ids
+    // are row-major, and the bottom tile row of the range holds its largest rows)
+    int64_t fy, fx, ly, lx;
+    job_coord(tile_lo, w, fy, fx);
+    job_coord(tile_lo + ntiles - 1, w, ly, lx);
+    const int64_t first = row_prefix(fy * q, m) + (std::max(fy * q, fx * q) - fy * q);
+    const int64_t li = std::min(ly * q + q, m) - 1, lj = std::min(lx * q + q, m) - 1;
+    const int64_t last = row_prefix(li, m) + (lj - li);
+    if (first < job_lo || last >= job_hi)
+        return fail(TB_ERR_CONFIG, "records: tiles [%lld, %lld) need job ids [%lld, %lld], counts cover [%lld, %lld)",
+                    (long long)tile_lo, (long long)(tile_lo + ntiles), (long long)first, (long long)last,
+                    (long long)job_lo, (long long)job_hi);
+    const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
     const int threads = (int)std::min<int64_t>(256, ((q * q + 31) / 32) * 32);
     TB_CUDA_TRY(launch_pdl(records_kernel, dim3((unsigned)ntiles), dim3(threads), 0, static_cast<cudaStream_t>(stream),
-                           num, nd, n3, n1_rows, m, q, w, job_lo, tile_lo, tile_offsets, naive,
+                           num, nd, n3, n1_rows, m, q, w, job_lo, tile_lo, base0, naive,
                            reinterpret_cast<uint4*>(records)));
     return check_launch("records_kernel");
 }

@@ -331,36 +331,28 @@ static int check_job_args(int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int
 // by 4 x 4 super-tiles, row-halves outer, so ~74 concurrently running pairs share A and B rows
 // through L2.  Cached per (m, job range).
 struct UnitTable {
-    int ordinal = -1;  // the device whose memory holds the table
+    DevTable table;  // the unit table on its device (async upload, see tb_common.cuh)
     int64_t m = -1, lo = -1, hi = -1;
-    int32_t* dev = nullptr;
-    int64_t count = 0, cap = 0;
+    int64_t count = 0;
 };
 static UnitTable g_unit_cache[32];  // per (m, job range): the banded host path cycles through a few
 static int g_unit_next = 0;
 
 static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t st, const int32_t** out,
-                       int64_t* count) {
+                       int64_t* count, DevTable** table) {
     std::lock_guard<std::mutex> lock(g_native_state_mutex);  // host threads share the caches
     int ordinal = 0;
     TB_CUDA_TRY(cudaGetDevice(&ordinal));
-    for (const UnitTable& c : g_unit_cache)
-        if (c.ordinal == ordinal && c.m == m && c.lo == job_lo && c.hi == job_hi) {
-            *out = c.dev;
+    for (UnitTable& c : g_unit_cache)
+        if (c.table.ordinal == ordinal && c.m == m && c.lo == job_lo && c.hi == job_hi) {
+            *out = static_cast<const int32_t*>(c.table.dev);
             *count = c.count;
+            *table = &c.table;
             return TB_OK;
         }
     UnitTable& g_units = g_unit_cache[g_unit_next];
     g_unit_next = (g_unit_next + 1) % 32;
     g_units.m = -1;
-    if (g_units.ordinal != ordinal && g_units.dev) {  // the slot held another device's table
-        TB_CUDA_TRY(cudaSetDevice(g_units.ordinal));
-        cudaFree(g_units.dev);
-        TB_CUDA_TRY(cudaSetDevice(ordinal));
-        g_units.dev = nullptr;
-        g_units.cap = 0;
-    }
-    g_units.ordinal = ordinal;
     const int64_t T = gemm2::TILE, G = 4;
     const int64_t w = (m + T - 1) / T;
     const int64_t W = (w + G - 1) / G;
@@ -384,21 +376,15 @@ static int build_units(int64_t m, int64_t job_lo, int64_t job_hi, cudaStream_t s
                         if (tid * 2 + 1 > INT32_MAX) return fail(TB_ERR_CAPACITY, "gemm: too many tiles");
                         v.push_back((int32_t)(tid * 2 + r));
                     }
-    if ((int64_t)v.size() > g_units.cap) {
-        if (g_units.dev) cudaFree(g_units.dev);
-        g_units.dev = nullptr;
-        TB_CUDA_TRY(cudaMalloc(&g_units.dev, std::max<size_t>(v.size(), 1) * sizeof(int32_t)));
-        g_units.cap = (int64_t)v.size();
-    }
-    if (!v.empty())
-        TB_CUDA_TRY(cudaMemcpyAsync(g_units.dev, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    TB_CUDA_TRY(cudaStreamSynchronize(st));  // v is pageable and dies here
+    int rc = table_upload(g_units.table, v.data(), v.size() * sizeof(int32_t), st);
+    if (rc) return rc;
     g_units.m = m;
     g_units.lo = job_lo;
     g_units.hi = job_hi;
     g_units.count = (int64_t)v.size();
-    *out = g_units.dev;
+    *out = static_cast<const int32_t*>(g_units.table.dev);
     *count = g_units.count;
+    *table = &g_units.table;
     return TB_OK;
 }
 
@@ -420,7 +406,8 @@ static int gemm_v2(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t j
     int rc;
     const int32_t* units = nullptr;
     int64_t nunits = 0;
-    if ((rc = build_units(m, job_lo, job_hi, st, &units, &nunits))) return rc;
+    DevTable* table = nullptr;
+    if ((rc = build_units(m, job_lo, job_hi, st, &units, &nunits, &table))) return rc;
     Gemm2Args p{};
     p.m = m;
     p.w = (m + gemm2::TILE - 1) / gemm2::TILE;
@@ -446,7 +433,8 @@ static int gemm_v2(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t j
     const int64_t work = nunits * splits;
     const unsigned grid = (unsigned)(2 * std::max<int64_t>(1, std::min<int64_t>(work, pairs)));
     gemm_tc2_kernel<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(tm, p);
-    return check_launch("gemm_tc2_kernel");
+    if ((rc = check_launch("gemm_tc2_kernel"))) return rc;
+    return table_mark_used(*table, st);
 }
 
 }  // namespace tb

@@ -326,12 +326,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
 // item, so the plan gives two-block units 3k splits and one-block units 2k (equal-cost items) or a
 // uniform split, whichever a simulation of the static schedule finishes first.
 struct Plan4 {
-    int ordinal = -1;  // the device whose memory holds the item table
+    DevTable table;  // the item table on its device (async upload, see tb_common.cuh)
     int64_t m = -1, lo = -1, hi = -1;
     int32_t nkb = -1, forced = -1, pairs = -1;
-    int4* dev = nullptr;
-    int64_t count = 0, cap = 0;
+    int64_t count = 0;
     int32_t partial = 0;
+    const int4* dev() const { return static_cast<const int4*>(table.dev); }
 };
 // Plans are cached per (geometry, job range): the banded host path cycles through a few ranges.
 constexpr int PLAN_CACHE = 32;  // the banded host path cycles through up to ~15 job ranges
@@ -399,12 +399,12 @@ static double plan_items4(const std::vector<int32_t>& code, const std::vector<in
 }
 
 static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, int32_t forced, int pairs,
-                       cudaStream_t st, const Plan4** out) {
+                       cudaStream_t st, Plan4** out) {
     std::lock_guard<std::mutex> lock(g_native_state_mutex);  // host threads share the caches
     int ordinal = 0;
     TB_CUDA_TRY(cudaGetDevice(&ordinal));
-    for (const Plan4& c : g_plans4)
-        if (c.ordinal == ordinal && c.m == m && c.lo == job_lo && c.hi == job_hi && c.nkb == nkb && c.forced == forced &&
+    for (Plan4& c : g_plans4)
+        if (c.table.ordinal == ordinal && c.m == m && c.lo == job_lo && c.hi == job_hi && c.nkb == nkb && c.forced == forced &&
             c.pairs == pairs) {
             *out = &c;
             return TB_OK;
@@ -412,14 +412,6 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
     Plan4& g_plan4 = g_plans4[g_plans4_next];
     g_plans4_next = (g_plans4_next + 1) % PLAN_CACHE;
     g_plan4.m = -1;
-    if (g_plan4.ordinal != ordinal && g_plan4.dev) {  // the slot held another device's item table
-        TB_CUDA_TRY(cudaSetDevice(g_plan4.ordinal));
-        cudaFree(g_plan4.dev);
-        TB_CUDA_TRY(cudaSetDevice(ordinal));
-        g_plan4.dev = nullptr;
-        g_plan4.cap = 0;
-    }
-    g_plan4.ordinal = ordinal;
     std::vector<int32_t> code, nb, ncols;
     list_units4(m, job_lo, job_hi, code, nb, ncols);
     std::vector<int32_t> su(code.size(), 1), best_su;
@@ -476,15 +468,8 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
     if (trace && trace[0] == '1')
         fprintf(stderr, "plan4: m %lld units %zu nkb %d max splits %d items %zu est %.0f\n", (long long)m,
                 code.size(), nkb, smax, items.size(), span_est);
-    if ((int64_t)items.size() > g_plan4.cap) {
-        if (g_plan4.dev) cudaFree(g_plan4.dev);
-        g_plan4.dev = nullptr;
-        TB_CUDA_TRY(cudaMalloc(&g_plan4.dev, std::max<size_t>(items.size(), 1) * sizeof(int4)));
-        g_plan4.cap = (int64_t)items.size();
-    }
-    if (!items.empty())
-        TB_CUDA_TRY(cudaMemcpyAsync(g_plan4.dev, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
-    TB_CUDA_TRY(cudaStreamSynchronize(st));
+    int rc = table_upload(g_plan4.table, items.data(), items.size() * sizeof(int4), st);
+    if (rc) return rc;
     g_plan4.m = m;
     g_plan4.lo = job_lo;
     g_plan4.hi = job_hi;
@@ -507,9 +492,9 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     const int64_t kbytes = K / 2;
     const int32_t nkb = (int32_t)((kbytes + g4::BK - 1) / g4::BK);
     const int pairs = std::max(1, num_sms() / 2);
-    const Plan4* plan = nullptr;
+    Plan4* plan = nullptr;
     if ((rc = build_plan4(m, job_lo, job_hi, nkb, splits, pairs, st, &plan))) return rc;
-    p.items = plan->dev;
+    p.items = plan->dev();
     p.nitems = plan->count;
     p.partial = plan->partial;
     p.job_lo = job_lo;
@@ -531,6 +516,7 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     }
     TB_CUDA_TRY(launch_pdl(gemm_fp4_kernel, dim3(grid), dim3(g4::THREADS), g4::SMEM_BYTES, st, ta, tbm, p));
     if ((rc = check_launch("gemm_fp4_kernel"))) return rc;
+    if ((rc = table_mark_used(plan->table, st))) return rc;
     if (p.trace) {
         TB_CUDA_TRY(cudaStreamSynchronize(st));
         tr.resize(grid * 16);

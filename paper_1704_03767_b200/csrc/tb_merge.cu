@@ -593,6 +593,134 @@ __device__ __forceinline__ uint32_t sort_count_any(uint16_t* keys, uint16_t* tmp
     return sort_count_block(keys, tmp, L);
 }
 
+
+// ------------------------------------------------------------------ large u tie groups
+// sum_g inv_g(w) and the joint ties n3 for rows whose largest u tie group exceeds MG_SMALL_GROUP, in
+// O(n log n) whatever the tie structure (the reference gets them from its per-pair lexicographic sort,
+// kernel_sorted.py:95-127, 179-192).  An MSD radix pass per key bit over segments that start as the u
+// groups: within a segment every 1 before a 0 of the current bit is one inversion, then the segment is
+// stably partitioned into its 0 part and its 1 part (the next level's segments).  After the last bit the
+// segments are the (u group, v key) classes, so n3 = sum_q (q - segment start).  Per element a level
+// costs a block scan of the bit and O(1) reads of the scan at q, at the segment start and at its end;
+// keys, segment starts and lengths - 1 ping-pong through a per-CTA global scratch (L2-resident), the
+// bit prefix E lives there too.
+struct HeavyWs {
+    uint16_t *keyA, *keyB, *segA, *segB;
+    uint16_t *lenA, *lenB;  // segment length - 1 (a segment can hold all 65536 elements)
+    int32_t* E;             // exclusive prefix of the level's bit, n + 1 entries
+};
+
+__host__ __device__ __forceinline__ int64_t heavy_ws_bytes_per_cta(int64_t n) { return 12 * n + 4 * (n + 1) + 64; }
+
+__device__ __forceinline__ HeavyWs heavy_ws(uint8_t* base, int64_t n) {
+    HeavyWs h;
+    uint8_t* b = base + (int64_t)blockIdx.x * heavy_ws_bytes_per_cta(n);
+    b = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(b) + 15) & ~uintptr_t(15));
+    h.E = reinterpret_cast<int32_t*>(b);
+    uint16_t* u = reinterpret_cast<uint16_t*>(b + 4 * (n + 1));
+    h.keyA = u; h.keyB = u + n;
+    h.segA = u + 2 * n; h.segB = u + 3 * n;
+    h.lenA = u + 4 * n; h.lenB = u + 5 * n;
+    return h;
+}
+
+// block exclusive scan of one int per thread (MG_THREADS threads)
+__device__ __forceinline__ int32_t mg_exscan(int32_t v, int32_t* wsm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t s = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += t;
+    }
+    if (lane == 31) wsm[w] = s;
+    __syncthreads();
+    if (w == 0) {
+        int32_t a = wsm[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t t = __shfl_up_sync(0xffffffffu, a, o);
+            if (lane >= o) a += t;
+        }
+        wsm[lane] = a;
+    }
+    __syncthreads();
+    const int32_t r = (w ? wsm[w - 1] : 0) + s - v;
+    __syncthreads();
+    return r;
+}
+
+__device__ void heavy_group_counts(const uint16_t* __restrict__ keys, const int32_t* __restrict__ gl, int32_t ng,
+                                   int64_t n, HeavyWs h, uint32_t& inv_g, uint32_t& ties) {
+    __shared__ int32_t wsm[32];
+    const int tid = threadIdx.x;
+    const int nn = (int)n;
+    uint16_t *K0 = h.keyA, *K1 = h.keyB, *S0 = h.segA, *S1 = h.segB, *L0 = h.lenA, *L1 = h.lenB;
+    int32_t* E = h.E;
+    for (int q = tid; q < nn; q += MG_THREADS) {
+        K0[q] = keys[sw(q)];
+        S0[q] = (uint16_t)q;
+        L0[q] = 0;
+    }
+    __syncthreads();
+    for (int32_t k = tid; k < ng; k += MG_THREADS) {  // u groups of >= 2 elements (tb_presort's list)
+        const int32_t g0 = gl[2 * k], glen = gl[2 * k + 1];
+        for (int32_t q = g0; q < g0 + glen; ++q) {
+            S0[q] = (uint16_t)g0;
+            L0[q] = (uint16_t)(glen - 1);
+        }
+    }
+    __syncthreads();
+    const int chunk = (nn + MG_THREADS - 1) / MG_THREADS;
+    const int c0 = min(nn, tid * chunk), c1 = min(nn, c0 + chunk);
+    int nbits = 0;
+    while ((1 << nbits) < nn) ++nbits;
+    uint32_t inv = 0;
+    for (int bit = nbits - 1; bit >= 0; --bit) {
+        int32_t cnt = 0;
+        for (int q = c0; q < c1; ++q) cnt += (K0[q] >> bit) & 1;
+        int32_t run = mg_exscan(cnt, wsm);
+        for (int q = c0; q < c1; ++q) {
+            E[q] = run;
+            run += (K0[q] >> bit) & 1;
+        }
+        if (c1 == nn && c0 < c1) E[nn] = run;
+        __syncthreads();
+        for (int q = c0; q < c1; ++q) {
+            const uint16_t k = K0[q];
+            const int st = S0[q], ln = (int)L0[q] + 1;
+            if (ln == 1) { K1[q] = k; S1[q] = (uint16_t)st; L1[q] = 0; continue; }
+            const int b = (k >> bit) & 1;
+            const int Es = E[st], Eq = E[q];
+            const int ones = E[st + ln] - Es, Z = ln - ones;
+            int np, ns, nl;
+            if (b == 0) {
+                inv += (uint32_t)(Eq - Es);  // ones before q in its segment
+                np = q - (Eq - Es);
+                ns = st;
+                nl = Z;
+            } else {
+                np = st + Z + (Eq - Es);
+                ns = st + Z;
+                nl = ones;
+            }
+            K1[np] = k;
+            S1[np] = (uint16_t)ns;
+            L1[np] = (uint16_t)(nl - 1);
+        }
+        __syncthreads();
+        uint16_t* t;
+        t = K0; K0 = K1; K1 = t;
+        t = S0; S0 = S1; S1 = t;
+        t = L0; L0 = L1; L1 = t;
+    }
+    uint32_t tt = 0;
+    for (int q = c0; q < c1; ++q) tt += (uint32_t)(q - (int)S0[q]);
+    inv_g = inv;
+    ties = tt;
+    __syncthreads();
+}
+
 struct MergeArgs {
     const uint16_t* keys;  // [m, n] min-rank keys (tb_presort)
     const int32_t* pos;
@@ -608,6 +736,7 @@ struct MergeArgs {
     int32_t* num;
     unsigned long long* nd;
     unsigned long long* n3;
+    uint8_t* heavy_ws;  // per-CTA scratch of heavy_group_counts
     MgConst k;  // {1, -1, 2, 4, 65536, 68, -68}
 };
 
@@ -683,16 +812,8 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
                     }
                 }
             }
-        } else
-        for (int64_t q = tid; q + 1 < n; q += MG_THREADS) {
-            const int32_t g = su[q];
-            if (su[q + 1] != g) continue;
-            const uint16_t wq = keys[sw((int)q)];
-            for (int64_t t = q + 1; t < n && su[t] == g; ++t) {
-                const uint16_t wt = keys[sw((int)t)];
-                inv_g += (wq > wt);
-                ties += (wq == wt);
-            }
+        } else {  // a large u tie group: the O(n log n) segmented radix count
+            heavy_group_counts(keys, p.groups + y * n, p.ngroups[y], n, heavy_ws(p.heavy_ws, n), inv_g, ties);
         }
         __syncthreads();
 
@@ -779,10 +900,16 @@ extern "C" int tb_presort(const int32_t* ranks, int64_t m, int64_t n, int32_t* p
     return check_launch("tie_groups_kernel");
 }
 
+extern "C" int64_t tb_merge_workspace(int64_t n) {
+    if (n < 1) return 0;
+    return (int64_t)num_sms() * heavy_ws_bytes_per_cta(n) + 64;
+}
+
 extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const int32_t* sorted,
                               const uint64_t* n1_rows, const int32_t* maxgrp, const int32_t* groups,
                               const int32_t* ngroups, int64_t m, int64_t n, int64_t job_lo, int64_t job_hi,
-                              int32_t* num, uint64_t* nd, uint64_t* n3, void* stream) {
+                              int32_t* num, uint64_t* nd, uint64_t* n3, void* workspace, int64_t ws_bytes,
+                              void* stream) {
     if (!maxgrp || !groups || !ngroups) return fail(TB_ERR_INVALID, "merge: null tie-group arrays");
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "merge: need m >= 1 and n >= 2");
     if (n > TB_MAX_N) return fail(TB_ERR_CAPACITY, "merge: n=%lld exceeds %d", (long long)n, TB_MAX_N);
@@ -790,7 +917,11 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
     if (job_lo < 0 || job_hi < job_lo || job_hi > total) return fail(TB_ERR_CONFIG, "merge: bad job range");
     if (!keys || !pos || !sorted || !n1_rows || !num) return fail(TB_ERR_INVALID, "merge: null pointer");
     if (job_hi == job_lo) return TB_OK;
+    if (!workspace || ws_bytes < tb_merge_workspace(n))
+        return fail(TB_ERR_CONFIG, "merge: workspace of %lld bytes, need tb_merge_workspace(n) = %lld",
+                    (long long)ws_bytes, (long long)tb_merge_workspace(n));
     MergeArgs a{};
+    a.heavy_ws = static_cast<uint8_t*>(workspace);
     a.keys = keys;
     a.pos = pos;
     a.sorted = sorted;

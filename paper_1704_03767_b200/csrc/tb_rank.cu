@@ -443,3 +443,230 @@ extern "C" int tb_rank_rows(const void* x, int dtype, int64_t m, int64_t n, int6
     }
     return check_launch("rank_rows_kernel");
 }
+
+// ------------------------------------------------------------------ K0w: dense ranks for any n (f4)
+// rank_transform (ranks.py:37-61) for rows too wide for K0's shared-memory sort (the merge path, n up
+// to 65536 and beyond): one 1024-thread CTA per row (persistent over rows), a stable LSD radix sort of
+// the row's (order key, index) pairs with 8-bit digits through a per-CTA global scratch (L2 / HBM
+// ping-pong; 32-bit keys for int32 / float32 take 4 passes, float64 keys 8; a pass whose digit is the
+// same for every element is skipped), then one block scan over "new value" flags gives the dense ranks
+// (int32, the merge path's K1 input) and a max-scan of run starts gives n1 = sum_i (i - runstart(i)) =
+// sum_t t(t-1)/2 (kernel_sorted.py:163-176).  -0.0 == +0.0, +-inf orderable, NaN flagged (bit 0).
+// Stability: warp w owns the contiguous index segment w; a digit's output offsets are warp-major and
+// inside a warp's 32-element step __match_any_sync ranks equal digits by lane (= index) order.
+namespace tb {
+constexpr int RW_THREADS = 1024;
+constexpr int RW_WARPS = RW_THREADS / 32;
+
+template <typename K>
+__device__ __forceinline__ K rw_key(int32_t v) { return (K)order_key(v); }
+template <typename K>
+__device__ __forceinline__ K rw_key(float v) { return (K)order_key(v); }
+template <typename K>
+__device__ __forceinline__ K rw_key(double v) { return (K)order_key(v); }
+
+// block-wide exclusive scan of one 64-bit value per thread (RW_THREADS threads); returns the total too
+__device__ __forceinline__ long long rw_exscan(long long v, long long* wsm, long long& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long s = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += t;
+    }
+    if (lane == 31) wsm[w] = s;
+    __syncthreads();
+    if (w == 0) {
+        long long a = wsm[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, a, o);
+            if (lane >= o) a += t;
+        }
+        wsm[lane] = a;  // inclusive per-warp prefix
+    }
+    __syncthreads();
+    total = wsm[RW_WARPS - 1];
+    const long long r = (w ? wsm[w - 1] : 0) + s - v;
+    __syncthreads();
+    return r;
+}
+
+// block-wide exclusive max-scan (identity -1)
+__device__ __forceinline__ long long rw_exmax(long long v, long long* wsm) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long s = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s = max(s, t);
+    }
+    if (lane == 31) wsm[w] = s;
+    __syncthreads();
+    if (w == 0) {
+        long long a = wsm[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, a, o);
+            if (lane >= o) a = max(a, t);
+        }
+        wsm[lane] = a;
+    }
+    __syncthreads();
+    long long prev = __shfl_up_sync(0xffffffffu, s, 1);
+    if (lane == 0) prev = -1;
+    const long long r = max(w ? wsm[w - 1] : -1LL, prev);
+    __syncthreads();
+    return r;
+}
+
+template <typename T, typename K>
+__global__ void __launch_bounds__(RW_THREADS, 1) rank_wide_kernel(const T* __restrict__ x, int64_t m, int64_t n,
+                                                                  int64_t ldx, int32_t* __restrict__ R, int64_t ldr,
+                                                                  unsigned long long* __restrict__ n1,
+                                                                  int32_t* __restrict__ flags, K* __restrict__ kws,
+                                                                  uint32_t* __restrict__ iws) {
+    pdl_wait();
+    __shared__ uint32_t hist[RW_WARPS][256];
+    __shared__ uint32_t tot[256];
+    __shared__ long long wsm[RW_WARPS];
+    __shared__ int skip;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    K* ka0 = kws + (int64_t)blockIdx.x * 2 * n;
+    uint32_t* ia0 = iws + (int64_t)blockIdx.x * 2 * n;
+    const int64_t seg = (n + RW_WARPS - 1) / RW_WARPS;
+    const int64_t s0 = min(n, (int64_t)w * seg), s1 = min(n, s0 + seg);
+    for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+        K* ka = ka0;
+        K* kb = ka0 + n;
+        uint32_t* ia = ia0;
+        uint32_t* ib = ia0 + n;
+        bool bad = false;
+        for (int64_t i = tid; i < n; i += RW_THREADS) {
+            const T v = x[row * ldx + i];
+            bad |= (v != v);
+            ka[i] = rw_key<K>(v);
+            ia[i] = (uint32_t)i;
+        }
+        if (__syncthreads_or(bad) && tid == 0) atomicOr(flags, 1);
+        for (int pass = 0; pass < (int)sizeof(K); ++pass) {
+            const int shift = 8 * pass;
+            for (int d = lane; d < 256; d += 32) hist[w][d] = 0;
+            __syncwarp();
+            for (int64_t i = s0 + lane; i < s1; i += 32) atomicAdd(&hist[w][(uint32_t)(ka[i] >> shift) & 255u], 1u);
+            __syncthreads();
+            if (tid < 256) {  // per digit: warp-major exclusive offsets, digit total
+                uint32_t acc = 0;
+                for (int ww = 0; ww < RW_WARPS; ++ww) {
+                    const uint32_t c = hist[ww][tid];
+                    hist[ww][tid] = acc;
+                    acc += c;
+                }
+                tot[tid] = acc;
+            }
+            if (tid == 0) skip = 0;
+            __syncthreads();
+            if (tid < 256 && tot[tid] == (uint32_t)n) skip = 1;  // every element has this digit
+            // exclusive scan of the digit totals (256 values; threads >= 256 contribute 0)
+            long long total;
+            const long long base = rw_exscan(tid < 256 ? (long long)tot[tid] : 0LL, wsm, total);
+            if (skip) continue;  // uniform: skip was written before rw_exscan's barriers
+            if (tid < 256)
+                for (int ww = 0; ww < RW_WARPS; ++ww) hist[ww][tid] += (uint32_t)base;
+            __syncthreads();
+            for (int64_t b = s0; b < s1; b += 32) {
+                const int64_t i = b + lane;
+                const bool act = i < s1;
+                const unsigned mask = __ballot_sync(0xffffffffu, act);
+                if (act) {
+                    const K k = ka[i];
+                    const uint32_t id = ia[i];
+                    const uint32_t d = (uint32_t)(k >> shift) & 255u;
+                    const unsigned peers = __match_any_sync(mask, d);
+                    const uint32_t pos = hist[w][d] + __popc(peers & lt);
+                    __syncwarp(mask);
+                    if ((peers & lt) == 0) hist[w][d] += __popc(peers);  // lowest lane of the digit group
+                    kb[pos] = k;
+                    ib[pos] = id;
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+            K* tk = ka; ka = kb; kb = tk;
+            uint32_t* ti = ia; ia = ib; ib = ti;
+        }
+        // dense ranks and n1 from the sorted keys: thread t owns the contiguous chunk [c0, c1)
+        const int64_t chunk = (n + RW_THREADS - 1) / RW_THREADS;
+        const int64_t c0 = min(n, (int64_t)tid * chunk), c1 = min(n, c0 + chunk);
+        long long cnt = 0, last_start = -1;
+        for (int64_t i = c0; i < c1; ++i)
+            if (i == 0 || ka[i] != ka[i - 1]) { ++cnt; last_start = i; }
+        long long total;
+        long long rank = rw_exscan(cnt, wsm, total) - 1;  // rank of the element before c0
+        long long start = rw_exmax(last_start, wsm);      // run start in force at c0
+        unsigned long long ties = 0;
+        for (int64_t i = c0; i < c1; ++i) {
+            if (i == 0 || ka[i] != ka[i - 1]) { ++rank; start = i; }
+            ties += (unsigned long long)(i - start);
+            R[row * ldr + ia[i]] = (int32_t)rank;
+        }
+        // block reduction of ties
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ties += __shfl_down_sync(0xffffffffu, ties, o);
+        if (lane == 0) wsm[w] = (long long)ties;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long t = 0;
+            for (int ww = 0; ww < RW_WARPS; ++ww) t += (unsigned long long)wsm[ww];
+            n1[row] = t;
+        }
+        __syncthreads();
+    }
+    pdl_trigger();
+}
+
+static int64_t rank_wide_grid(int64_t m) { return std::max<int64_t>(1, std::min<int64_t>(m, num_sms())); }
+static int64_t rank_wide_keybytes(int dtype) { return dtype == TB_DTYPE_F64 ? 8 : 4; }
+}  // namespace tb
+
+extern "C" int64_t tb_rank_dense_workspace(int64_t m, int64_t n, int dtype) {
+    if (m < 1 || n < 1) return 0;
+    const int64_t per = 2 * n * (rank_wide_keybytes(dtype) + 4);
+    return rank_wide_grid(m) * per + 256;
+}
+
+extern "C" int tb_rank_dense(const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, int32_t* R, int64_t ldr,
+                             uint64_t* n1, int32_t* flags, void* workspace, int64_t ws_bytes, void* stream) {
+    if (m < 1 || n < 1) return fail(TB_ERR_INVALID, "rank_dense: empty input");
+    if (n > INT32_MAX) return fail(TB_ERR_CAPACITY, "rank_dense: n=%lld too large", (long long)n);
+    if (ldx < n || ldr < n) return fail(TB_ERR_CONFIG, "rank_dense: bad leading dimensions");
+    if (!x || !R || !n1 || !flags || !workspace) return fail(TB_ERR_INVALID, "rank_dense: null pointer");
+    if (dtype < TB_DTYPE_I32 || dtype > TB_DTYPE_F64) return fail(TB_ERR_INVALID, "rank_dense: unknown dtype %d", dtype);
+    if (ws_bytes < tb_rank_dense_workspace(m, n, dtype))
+        return fail(TB_ERR_CONFIG, "rank_dense: workspace of %lld bytes, need %lld", (long long)ws_bytes,
+                    (long long)tb_rank_dense_workspace(m, n, dtype));
+    const int64_t grid = rank_wide_grid(m);
+    const int64_t kb = rank_wide_keybytes(dtype);
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(ws) + 15) & ~uintptr_t(15);
+    ws = reinterpret_cast<uint8_t*>(a);
+    uint32_t* iws = reinterpret_cast<uint32_t*>(ws + grid * 2 * n * kb);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* n1u = reinterpret_cast<unsigned long long*>(n1);
+    switch (dtype) {
+        case TB_DTYPE_I32:
+            TB_CUDA_TRY(launch_pdl(rank_wide_kernel<int32_t, uint32_t>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
+                                   (const int32_t*)x, m, n, ldx, R, ldr, n1u, flags, reinterpret_cast<uint32_t*>(ws), iws));
+            break;
+        case TB_DTYPE_F32:
+            TB_CUDA_TRY(launch_pdl(rank_wide_kernel<float, uint32_t>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
+                                   (const float*)x, m, n, ldx, R, ldr, n1u, flags, reinterpret_cast<uint32_t*>(ws), iws));
+            break;
+        default:
+            TB_CUDA_TRY(launch_pdl(rank_wide_kernel<double, uint64_t>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
+                                   (const double*)x, m, n, ldx, R, ldr, n1u, flags, reinterpret_cast<uint64_t*>(ws), iws));
+            break;
+    }
+    return check_launch("rank_wide_kernel");
+}

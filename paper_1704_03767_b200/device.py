@@ -14,9 +14,10 @@ host except the optional ``validate()`` (one 4-byte flag read).
 
 from __future__ import annotations
 
-import math
-
+import contextlib
 import ctypes
+import math
+import threading
 from dataclasses import dataclass, field
 
 import torch
@@ -37,7 +38,7 @@ def _ptr(t: torch.Tensor | None):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def _stream_ptr(stream: torch.cuda.Stream | None):
+def _stream_ptr(stream: torch.cuda.Stream | None = None):
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
 
@@ -90,8 +91,37 @@ class PairResult:
         return self
 
 
+@dataclass
+class Prepared:
+    """Device operands of one dataset (TauEngine.prepare): what every job range's numerator reads."""
+
+    path: str
+    m: int
+    n: int
+    full: bool
+    n1_rows: torch.Tensor             # int64 [m]
+    flags: torch.Tensor               # int32 [1]
+    simt: bool = False
+    S: torch.Tensor | None = None     # GEMM: sign matrix [m, ldS] bytes
+    A: torch.Tensor | None = None     # GEMM full counts: |S|
+    K: int = 0
+    ldS: int = 0
+    fmt: int = 0
+    keys: torch.Tensor | None = None  # merge: K1 presort outputs
+    pos: torch.Tensor | None = None
+    srt: torch.Tensor | None = None
+    maxgrp: torch.Tensor | None = None
+    groups: torch.Tensor | None = None
+    ngroups: torch.Tensor | None = None
+
+    def validate(self) -> "Prepared":
+        PairResult.validate(self)  # same flag bits
+        return self
+
+
 class TauEngine:
-    """Owns device workspaces; one instance per device/stream user."""
+    """Owns device workspaces; one instance per device.  Calls from several host threads serialise on
+    ``lock``; every kernel launches on this engine's device."""
 
     def __init__(self, device: int | torch.device | None = None):
         if not torch.cuda.is_available():
@@ -105,6 +135,30 @@ class TauEngine:
         self._ws: dict[str, torch.Tensor] = {}
         self._events = None
         self._stream = None
+        # One call at a time owns the workspaces (S, |S|, ranks, presort arrays): host threads serialise on
+        # the lock, and a call on another stream first waits for the previous call's stream work (_tail),
+        # so a workspace is never overwritten while kernels of an earlier call may still read it.
+        self.lock = threading.RLock()
+        self._tail: torch.cuda.Event | None = None
+
+    @contextlib.contextmanager
+    def _session(self, stream: torch.cuda.Stream | None):
+        """Enter this engine's device and stream (kernels launch on the current device: the C ABI uses
+        cudaGetDevice), holding the workspace lock; orders the stream after the previous call."""
+        with self.lock, torch.cuda.device(self.device):
+            st = stream if stream is not None else torch.cuda.current_stream(self.device)
+            if st.device != self.device:
+                raise ConfigError(f"stream is on {st.device}, engine on {self.device}")
+            if self._tail is not None:
+                st.wait_event(self._tail)
+            self._stream, self._events = st, None
+            try:
+                with torch.cuda.stream(st):
+                    yield st
+            finally:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                self._tail = ev
 
     # -------------------------------------------------------------- workspaces
     def _buf(self, name: str, numel: int, dtype: torch.dtype) -> torch.Tensor:
@@ -170,24 +224,28 @@ class TauEngine:
         path = self.choose_path(n) if kernel == "auto" else kernel
         if path not in PATHS:
             raise ConfigError(f"unknown device path {kernel!r}, expected one of {PATHS + ('auto',)}")
-        st = _stream_ptr(stream)
-        self._events = _events
-        self._stream = stream if stream is not None else torch.cuda.current_stream()
-        with torch.cuda.stream(self._stream):
-            return self._run(x, path, m, n, job_lo, job_hi, st, tau_a, tau_b, full_counts, splits, simt)
+        if x.device != self.device:
+            raise InvalidInputError(f"x is on {x.device}, engine on {self.device}")
+        with self._session(stream) as st_t:
+            self._events = _events
+            return self._run(x, path, m, n, job_lo, job_hi, _stream_ptr(st_t), tau_a, tau_b, full_counts,
+                             splits, simt)
 
     def _run(self, x, path, m, n, job_lo, job_hi, st, tau_a, tau_b, full_counts, splits, simt) -> PairResult:
         count = job_hi - job_lo
         dev = self.device
         c0 = _lib.load().tb_launch_count()
+        row_lo = job_coord(job_lo, m)[0] if job_hi > job_lo else m
+        prep = self.prepare(x, path, full_counts=full_counts, row_lo=row_lo, simt=simt)
         res = PairResult(m=m, n=n, job_lo=job_lo, job_hi=job_hi, path=path,
                          numerator=torch.empty(count, dtype=torch.int32, device=dev),
-                         n1_rows=torch.empty(m, dtype=torch.int64, device=dev),
-                         flags=torch.zeros(1, dtype=torch.int32, device=dev))
-        if path == "gemm":
-            self._gemm_path(x, res, st, full_counts, splits, simt)
-        else:
-            self._merge_path(x, res, st)
+                         n1_rows=prep.n1_rows, flags=prep.flags)
+        res.extra["sign_format"] = prep.fmt if path == "gemm" else None
+        if path == "merge" or full_counts:
+            res.n_d = torch.empty(count, dtype=torch.int64, device=dev)
+            res.n3 = torch.empty(count, dtype=torch.int64, device=dev)
+        self._mark(0)
+        self.numerators(prep, job_lo, job_hi, res.numerator, res.n_d, res.n3, splits=splits, _mark_after_num=True)
         if tau_a or tau_b:
             res.tau_a = torch.empty(count, dtype=torch.float64, device=dev) if tau_a else None
             res.tau_b = torch.empty(count, dtype=torch.float64, device=dev) if tau_b else None
@@ -195,6 +253,68 @@ class TauEngine:
                       _ptr(res.tau_a), _ptr(res.tau_b), st)
         res.launches = _lib.load().tb_launch_count() - c0
         return res
+
+    # -------------------------------------------------------------- prepared operands + job-range numerators
+    def session(self, stream: torch.cuda.Stream | None = None):
+        """Context manager for callers composing prepare() / numerators() themselves (the engine's
+        compute_all_pairs pipeline): this device, the workspace lock, ``stream`` (default: the device's
+        current stream) current and ordered after the previous call; yields the stream."""
+        return self._session(stream)
+
+    def prepare(self, x: torch.Tensor, path: str, full_counts: bool = False, row_lo: int = 0,
+                simt: bool = False) -> "Prepared":
+        """Per-dataset device operands, once per call (inside session()): ranks and n1 of every row, then
+        the sign matrix S of rows >= row_lo (and |S| for full counts) on the GEMM path, or the K1
+        presort of every row on the merge path.  Workspaces are the engine's (valid until the next
+        prepare on this engine)."""
+        m, n = x.shape
+        st = _stream_ptr(self._stream)
+        prep = Prepared(path=path, m=m, n=n, full=full_counts, simt=simt,
+                        n1_rows=torch.empty(m, dtype=torch.int64, device=self.device),
+                        flags=torch.zeros(1, dtype=torch.int32, device=self.device))
+        stub = PairResult(m=m, n=n, job_lo=row_prefix(min(row_lo, m), m), job_hi=m * (m + 1) // 2, path=path,
+                          numerator=None, n1_rows=prep.n1_rows, flags=prep.flags)
+        if path == "gemm":
+            prep.S, prep.K, prep.ldS, prep.fmt = self._gemm_prepare(x, stub, st, simt)
+            if full_counts:
+                prep.A = self._buf("A", m * prep.ldS, torch.int8)
+                y0 = min(row_lo, m)
+                _lib.call("tb_abs_pack", _ptr(prep.S[y0 * prep.ldS:]), m - y0, prep.ldS, prep.fmt,
+                          _ptr(prep.A[y0 * prep.ldS:]), st)
+        else:
+            prep.pos, prep.srt, prep.keys, (prep.maxgrp, prep.groups, prep.ngroups) = \
+                self._merge_prepare(x.contiguous(), stub, st)
+        return prep
+
+    def numerators(self, prep: "Prepared", lo: int, hi: int, num: torch.Tensor, nd: torch.Tensor | None = None,
+                   n3: torch.Tensor | None = None, splits: int = 0, _mark_after_num: bool = False) -> None:
+        """Numerator (and n_d / n3 when given) of job ids [lo, hi) into num[0:hi-lo] etc. (inside session())."""
+        if hi <= lo:
+            return
+        m, n = prep.m, prep.n
+        st = _stream_ptr(self._stream)
+        if prep.path == "merge":
+            ws, wsb = self._merge_ws(n)
+            _lib.call("tb_merge_pairs", _ptr(prep.keys), _ptr(prep.pos), _ptr(prep.srt), _ptr(prep.n1_rows),
+                      _ptr(prep.maxgrp), _ptr(prep.groups), _ptr(prep.ngroups), m, n, lo, hi, _ptr(num),
+                      _ptr(nd), _ptr(n3), _ptr(ws), wsb, st)
+            if _mark_after_num:
+                self._mark(1)
+            return
+        for a, b in self._gemm_ranges(m, lo, hi):
+            self._gemm_numerator(prep.S, num[a - lo:b - lo], m, prep.K, prep.ldS, prep.fmt, a, b, st, splits,
+                                 prep.simt)
+        if _mark_after_num:
+            self._mark(1)
+        if nd is not None or n3 is not None:
+            if prep.A is None:
+                raise ConfigError("n_d / n3 on the GEMM path need prepare(..., full_counts=True)")
+            absdot = self._buf("absdot", hi - lo, torch.int32)
+            for a, b in self._gemm_ranges(m, lo, hi):
+                self._gemm_numerator(prep.A, absdot[a - lo:b - lo], m, prep.K, prep.ldS, prep.fmt, a, b, st,
+                                     splits, prep.simt)
+            _lib.call("tb_full_counts", _ptr(num), _ptr(absdot), _ptr(prep.n1_rows), m, n, lo, hi, _ptr(nd),
+                      _ptr(n3), st)
 
     def _gemm_layout(self, n: int, simt: bool = False):
         """(K, sign format, row stride of S in bytes, row stride of R) for n samples."""
@@ -255,24 +375,6 @@ class TauEngine:
                 out.append((lo, hi))
         return out
 
-    def _gemm_path(self, x, res: PairResult, st, full_counts: bool, splits: int, simt: bool):
-        m, n = res.m, res.n
-        S, K, ldS, fmt = self._gemm_prepare(x, res, st, simt)
-        self._mark(0)
-        for lo, hi in self._gemm_ranges(m, res.job_lo, res.job_hi):
-            num = res.numerator[lo - res.job_lo:hi - res.job_lo]
-            self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st, splits, simt)
-        self._mark(1)
-        if full_counts:
-            A = self._buf("A", m * ldS, torch.int8)
-            _lib.call("tb_abs_pack", _ptr(S), m, ldS, fmt, _ptr(A), st)
-            absdot = self._buf("absdot", res.count, torch.int32)
-            self._gemm_numerator(A, absdot, m, K, ldS, fmt, res.job_lo, res.job_hi, st, splits, simt)
-            res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
-            res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
-            _lib.call("tb_full_counts", _ptr(res.numerator), _ptr(absdot), _ptr(res.n1_rows), m, n,
-                      res.job_lo, res.job_hi, _ptr(res.n_d), _ptr(res.n3), st)
-
     # -------------------------------------------------------------- host-buffer entry point
     @staticmethod
     def bands(m: int, nbands: int = 3, align: int = 256, fracs: tuple | None = None) -> list[int]:
@@ -314,18 +416,14 @@ class TauEngine:
         band i+1's numerator kernel.  ``x_host`` and ``tau_b_out`` should be pinned; the call is
         asynchronous on ``stream`` (which finally waits for the copies).
         """
-        st_t = stream if stream is not None else torch.cuda.current_stream()
-        cp_t = copy_stream if copy_stream is not None else self._copy_stream()
         m, n = x_host.shape
         total = m * (m + 1) // 2
         if tau_b_out.numel() < total:
             raise ConfigError(f"tau_b_out holds {tau_b_out.numel()} values, need {total}")
         path = self.choose_path(n) if kernel == "auto" else kernel
-        st = _stream_ptr(st_t)
-        self._events, self._stream = None, st_t
-        if path == "merge" and x_host.dtype != torch.int32:
-            raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
-        with torch.cuda.stream(st_t):
+        with self._session(stream) as st_t:
+            cp_t = copy_stream if copy_stream is not None else self._copy_stream()
+            st = _stream_ptr(st_t)
             # H2D in row chunks on the copy stream; rank + sign pack of chunk i overlap chunk i+1's copy
             x = self._buf("x_dev", m * n, x_host.dtype).view(m, n)
             nchunk = max(1, min(h2d_chunks, m // 256)) if path == "gemm" else 1
@@ -366,8 +464,10 @@ class TauEngine:
                 if path == "gemm":
                     self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st)
                 else:
+                    ws, wsb = self._merge_ws(n)
                     _lib.call("tb_merge_pairs", _ptr(keys), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp[0]),
-                              _ptr(maxgrp[1]), _ptr(maxgrp[2]), m, n, lo, hi, _ptr(num), None, None, st)
+                              _ptr(maxgrp[1]), _ptr(maxgrp[2]), m, n, lo, hi, _ptr(num), None, None, _ptr(ws), wsb,
+                              st)
                 tb = res.tau_b[lo:hi]
                 _lib.call("tb_finalize", _ptr(num), _ptr(res.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
                 ev = torch.cuda.Event()
@@ -386,12 +486,22 @@ class TauEngine:
             self._cs = cs
         return cs
 
+    def _merge_ws(self, n: int):
+        """K4's scratch for pairs with large u tie groups (tb_merge_workspace bytes)."""
+        wsb = int(_lib.load().tb_merge_workspace(n))
+        return self._buf("merge_ws", wsb, torch.uint8), wsb
+
     def _merge_prepare(self, x, res: PairResult, st):
-        """K1 presort of every variable (u-order positions, sorted ranks, min-rank merge keys, n1,
-        tie groups)."""
+        """K0w dense ranks of the raw values (any dtype, any n), then the K1 presort of every variable
+        (u-order positions, sorted ranks, min-rank merge keys, n1, tie groups)."""
         m, n = res.m, res.n
-        if x.dtype != torch.int32:
-            raise InvalidInputError("the merge path takes dense int32 ranks (rank_transform output)")
+        code = _dtype_code(x)
+        ranks = self._buf("R32", m * n, torch.int32)
+        wsb = int(_lib.load().tb_rank_dense_workspace(m, n, code))
+        ws = self._buf("rank_ws", wsb, torch.uint8)
+        _lib.call("tb_rank_dense", _ptr(x), code, m, n, x.stride(0), _ptr(ranks), n, _ptr(res.n1_rows),
+                  _ptr(res.flags), _ptr(ws), wsb, st)
+        x = ranks
         pos = self._buf("pos", m * n, torch.int32)
         srt = self._buf("sorted", m * n, torch.int32)
         keys = self._buf("mkeys", m * n, torch.int16)
@@ -401,18 +511,6 @@ class TauEngine:
         _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(keys), _ptr(res.n1_rows),
                   _ptr(maxgrp), _ptr(work), _ptr(ngroups), _ptr(res.flags), st)
         return pos, srt, keys, (maxgrp, work, ngroups)
-
-    def _merge_path(self, x, res: PairResult, st):
-        m, n = res.m, res.n
-        x = x.contiguous()
-        pos, srt, keys, (maxgrp, groups, ngroups) = self._merge_prepare(x, res, st)
-        res.n_d = torch.empty(res.count, dtype=torch.int64, device=self.device)
-        res.n3 = torch.empty(res.count, dtype=torch.int64, device=self.device)
-        self._mark(0)
-        _lib.call("tb_merge_pairs", _ptr(keys), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp), _ptr(groups),
-                  _ptr(ngroups), m, n,
-                  res.job_lo, res.job_hi, _ptr(res.numerator), _ptr(res.n_d), _ptr(res.n3), st)
-        self._mark(1)
 
 
 _ENGINES: dict[int, TauEngine] = {}

@@ -33,11 +33,7 @@ def _device_counts(ua: np.ndarray, va: np.ndarray, full: bool):
 
     eng = get_engine()
     path = eng.choose_path(ua.shape[0])
-    xs = np.stack([ua, va])
-    if path == "merge" and (xs.min() < 0 or xs.max() >= ua.shape[0]):
-        from .ranks import rank_transform
-        xs = np.stack([rank_transform(ua), rank_transform(va)])
-    x = torch.from_numpy(xs).to(eng.device)
+    x = torch.from_numpy(np.stack([ua, va])).to(eng.device)  # the device ranks them (K0 / K0w)
     res = eng.all_pairs(x, kernel=path, job_range=(1, 2),
                         tau_a=False, tau_b=False, full_counts=full)
     res.validate()

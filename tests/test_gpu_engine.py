@@ -112,3 +112,87 @@ def test_devices_split_matches_reference_stream(kernel):
     assert parts == full
     with pytest.raises(tb.ConfigError):
         tb.compute_all_pairs(ds, kernel, device=0, devices=[0])
+
+
+@pytest.mark.parametrize("kernel", ["sorted", "gemm", "merge", "naive"])
+def test_window_pipeline_matches_reference_stream(kernel):
+    """The bounded pass pipeline (job windows of <= window_jobs ids, per-pass device record gathers, async
+    D2H into pinned slots, GPU running ahead of the sink) gives the reference byte stream for any window
+    size -- from one window per pass to one window for the whole run -- and any pass size."""
+    import paper_1704_03767_b200 as tb
+    gold = load_json("engine_streams.json")
+    ds = tb.synth_dataset(512, 48, tie_fraction=0.3, seed=512)
+    ref = None
+    for wj in (1, 997, 40_000, 1 << 25):
+        for pass_tiles in (7, 300, 4096):
+            blob = _stream(ds, kernel, 4, window_jobs=wj, pass_tiles=pass_tiles)
+            if kernel != "naive":
+                assert hashlib.sha256(blob).hexdigest() == gold["m512_n48_t0.3_s512_q4"], (wj, pass_tiles)
+            ref = blob if ref is None else ref
+            assert blob == ref
+    for shard in range(3):  # shards through small windows still concatenate
+        parts = b"".join(_stream(ds, kernel, 4, shard=(i, 3), window_jobs=5000) for i in range(3))
+        assert parts == ref
+
+
+def test_naive_large_n_uses_merge_path():
+    """kernel='naive' for n above the GEMM path's limit: numerator-only records from the merge path
+    (the reference's naive kernel handles any n, kernel_naive.py:26-44)."""
+    import paper_1704_03767_b200 as tb
+    rng = np.random.default_rng(9)
+    ranks = np.stack([tb.rank_transform(rng.integers(0, 3000, 9000)) for _ in range(4)])
+    ds = tb.Dataset(labels=list("abcd"), ranks=ranks)
+    nv, so = [], []
+    s1 = tb.compute_all_pairs(ds, "naive", tile_size=2, sink=lambda r: nv.append(r.copy()))
+    tb.compute_all_pairs(ds, "sorted", tile_size=2, sink=lambda r: so.append(r.copy()))
+    nv, so = np.concatenate(nv), np.concatenate(so)
+    assert s1.device_path == "merge"
+    assert np.array_equal(nv["numerator"], so["numerator"])
+    assert (nv["n_d"] == 0).all() and (nv["n1"] == 0).all() and (nv["n3"] == 0).all()
+
+
+def test_concurrent_calls_from_threads():
+    """Two host threads calling compute_all_pairs on the same GPU (different datasets, different paths)
+    at once: the engine lock + stream ordering keep workspaces and pass buffers apart."""
+    import threading
+
+    import paper_1704_03767_b200 as tb
+    gold = load_json("engine_streams.json")
+    ds_a = tb.synth_dataset(512, 48, tie_fraction=0.3, seed=512)
+    ds_b = tb.synth_dataset(64, 48, tie_fraction=0.3, seed=512)
+    out, errs = {}, []
+
+    def run(name, ds, kernel):
+        try:
+            for _ in range(3):
+                out[name] = _stream(ds, kernel, 4, pass_tiles=50, window_jobs=3000)
+        except BaseException as exc:  # noqa: BLE001
+            errs.append(exc)
+
+    th = [threading.Thread(target=run, args=("a", ds_a, "gemm")), threading.Thread(target=run, args=("b", ds_b, "merge"))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    assert hashlib.sha256(out["a"]).hexdigest() == gold["m512_n48_t0.3_s512_q4"]
+    assert hashlib.sha256(out["b"]).hexdigest() == gold["m64_n48_t0.3_s512_q4"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_distinct_devices():
+    """devices=[0, 1]: each GPU's producer thread launches on its own device and stream (the engine
+    enters its device; the C ABI launches on the current device), and a TauEngine on GPU 1 works while
+    GPU 0 is the caller's current device."""
+    import paper_1704_03767_b200 as tb
+    from paper_1704_03767_b200.device import TauEngine
+    gold = load_json("engine_streams.json")
+    ds = tb.synth_dataset(512, 48, tie_fraction=0.3, seed=512)
+    for kernel in ("gemm", "merge"):
+        blob = _stream(ds, kernel, 4, devices=[0, 1], pass_tiles=97)
+        assert hashlib.sha256(blob).hexdigest() == gold["m512_n48_t0.3_s512_q4"], kernel
+    torch.cuda.set_device(0)
+    x = torch.from_numpy(ds.ranks).to("cuda:1")
+    r1 = TauEngine(1).all_pairs(x, kernel="gemm").validate()
+    r0 = TauEngine(0).all_pairs(x.to("cuda:0"), kernel="gemm").validate()
+    assert torch.equal(r1.numerator.cpu(), r0.numerator.cpu())

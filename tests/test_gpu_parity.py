@@ -182,8 +182,11 @@ def test_config1_full(eng, oracle, path):
     _diag_properties(res, 200)
 
 
-def test_config2_gemm_vs_golden_and_simt(eng):
-    """Config 2 (2048 x 1000, int 0..9): sampled golden pairs + every pair vs the dp4a cross-check."""
+@pytest.mark.timeout(600)
+def test_config2_every_pair_vs_oracle(eng, oracle):
+    """Config 2 (2048 x 1000, int 0..9): EVERY cell (2,098,176 job ids, SURVEY 8(d) parity protocol) vs
+    the pinned oracle's packed/VSE counts -- numerator, n1, n2, n_d, n3 bit-exact, tau_a / tau_b 0 ulp --
+    plus the reference's own golden pairs and the dp4a cross-check kernel."""
     from paper_1704_03767_b200 import workloads
     z = load_npz("config2.npz")
     x = workloads.generate(2)
@@ -192,16 +195,21 @@ def test_config2_gemm_vs_golden_and_simt(eng):
     res = eng.all_pairs(xd, kernel="gemm", full_counts=True).validate()
     _sampled_check(res, z, 1000)
     _diag_properties(res, 1000)
+    ranks = oracle.rank_matrix(x)
+    pi, pj = oracle.upper_pairs(x.shape[0])
+    num, cnt = oracle.all_pairs(ranks, pi, pj, oracle.KERNEL_PACKED)
+    np.testing.assert_array_equal(res.numerator.cpu().numpy().astype(np.int64), num)
+    n1 = res.n1_rows.cpu().numpy()
+    np.testing.assert_array_equal(n1[pi], cnt[:, 1])
+    np.testing.assert_array_equal(n1[pj], cnt[:, 2])
+    np.testing.assert_array_equal(res.n_d.cpu().numpy(), cnt[:, 0])
+    np.testing.assert_array_equal(res.n3.cpu().numpy(), cnt[:, 3])
+    ta, tb = oracle.derive_taus(num, cnt[:, 1], cnt[:, 2], 1000)
+    np.testing.assert_array_equal(res.tau_a.cpu().numpy(), ta)
+    np.testing.assert_array_equal(res.tau_b.cpu().numpy(), tb)
+    assert np.nanmax(np.abs(res.tau_b.cpu().numpy() - tb)) <= TAU_ATOL
     ref = eng.all_pairs(xd, kernel="gemm", simt=True, tau_a=False, tau_b=False).validate()
     assert torch.equal(res.numerator, ref.numerator)
-    # full-count identity: n_c + n_d + ties = n0 for every pair
-    n0 = 1000 * 999 // 2
-    m = 2048
-    pi, pj = np.triu_indices(m)
-    n1 = res.n1_rows
-    tot = (res.numerator.to(torch.int64) + 2 * res.n_d + n1[torch.from_numpy(pi).cuda()]
-           + n1[torch.from_numpy(pj).cuda()] - res.n3)
-    assert bool((tot == n0).all())
 
 
 @pytest.mark.parametrize("splits", [1, 2, 7])
@@ -367,7 +375,9 @@ def test_config4_merge_sampled(eng, oracle):
     m = x.shape[0]
     ranks = np.stack([oracle.rank_transform(r) for r in x])
     np.testing.assert_array_equal(ranks[:4], z["ranks_head"])
-    res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="merge", full_counts=True).validate()
+    # raw float32 values in: the device ranks every row (K0w) -- bit-exact vs the oracle's np.unique ranks
+    res = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="merge", full_counts=True).validate()
+    np.testing.assert_array_equal(eng._ws["R32"][: m * x.shape[1]].view(m, -1).cpu().numpy(), ranks)
     pi, pj = z["pi"], z["pj"]
     jid = torch.from_numpy(pi * (2 * m - pi + 1) // 2 + pj - pi).cuda()
     np.testing.assert_array_equal(res.numerator.index_select(0, jid).cpu().numpy(), z["numerator"])
@@ -391,15 +401,17 @@ def test_config5_gemm_sampled(eng, oracle):
     z = load_npz("config5.npz")
     x = workloads.generate(5)
     assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["x_sha256"])
-    res = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="gemm", tau_a=False).validate()
+    res = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="gemm", tau_a=False, full_counts=True).validate()
     pi, pj = z["pi"], z["pj"]
     m = x.shape[0]
     jid = torch.from_numpy(pi * (2 * m - pi + 1) // 2 + pj - pi).cuda()
     np.testing.assert_array_equal(res.numerator.index_select(0, jid).cpu().numpy(), z["numerator"])
     np.testing.assert_array_equal(res.tau_b.index_select(0, jid).cpu().numpy(), z["tau_b"])
+    np.testing.assert_array_equal(res.n_d.index_select(0, jid).cpu().numpy(), z["counts"][:, 0])
+    np.testing.assert_array_equal(res.n3.index_select(0, jid).cpu().numpy(), z["counts"][:, 3])
     _diag_properties(res, 1024)
     ri, rj = _random_pairs(m, 10000, 5)
-    _oracle_pairs_check(res, oracle, x, ri, rj, oracle.KERNEL_PACKED)
+    _oracle_pairs_check(res, oracle, x, ri, rj, oracle.KERNEL_PACKED, counts=True)
     del res
     eng.release()
     torch.cuda.empty_cache()
@@ -537,3 +549,74 @@ def test_gemm_workspace_beyond_hbm_is_capacity_error(eng):
         eng.all_pairs(x, kernel="gemm")
     eng.release()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [np.int32, np.float32, np.float64])
+def test_rank_dense_vs_oracle(oracle, dtype):
+    """K0w (any row width): dense int32 ranks + tie counts vs the oracle's rank_transform (np.unique,
+    ranks.py:37-61) -- -0.0 == +0.0, +-inf orderable, heavy ties, constant rows, rows wider than 65536;
+    NaN raises through the engine (flag bit 0)."""
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.device import _dtype_code, _ptr, _stream_ptr
+    lib = _lib.load()
+    rng = np.random.default_rng(77)
+    for n in (1, 2, 31, 33, 1000, 9000, 65536, 70001):
+        rows = [rng.integers(-5, 5, n), rng.integers(0, 3, n), np.full(n, 7), np.arange(n)[::-1],
+                rng.integers(-2**31, 2**31 - 1, n), rng.standard_normal(n) * 1e3]
+        x = np.stack(rows).astype(dtype)
+        if dtype is not np.int32:
+            x[0, : n // 3] = -0.0
+            x[0, n // 3: n // 2] = 0.0
+            x[1, ::7] = np.inf
+            x[1, 1::11] = -np.inf
+        m = x.shape[0]
+        xd = torch.from_numpy(x).cuda()
+        R = torch.empty(m * n, dtype=torch.int32, device="cuda")
+        n1 = torch.empty(m, dtype=torch.int64, device="cuda")
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        wsb = int(lib.tb_rank_dense_workspace(m, n, _dtype_code(xd)))
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        _lib.call("tb_rank_dense", _ptr(xd), _dtype_code(xd), m, n, n, _ptr(R), n, _ptr(n1), _ptr(flags), _ptr(ws),
+                  wsb, _stream_ptr(None))
+        torch.cuda.synchronize()
+        got = R.view(m, n).cpu().numpy()
+        for r in range(m):
+            ref = oracle.rank_transform(x[r])
+            np.testing.assert_array_equal(got[r], ref, err_msg=f"n={n} row={r}")
+            _, c = np.unique(ref, return_counts=True)
+            assert int(n1[r]) == int((c * (c - 1) // 2).sum()), (n, r)
+        assert int(flags.item()) == 0
+    if dtype is not np.int32:
+        from paper_1704_03767_b200 import InvalidInputError
+        from paper_1704_03767_b200.device import TauEngine
+        x = rng.standard_normal((3, 9000)).astype(dtype)
+        x[1, 5] = np.nan
+        with pytest.raises(InvalidInputError, match="NaN"):
+            TauEngine(0).all_pairs(torch.from_numpy(x).cuda(), kernel="merge").validate()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("n,levels", [(3000, 5), (40000, 7), (65536, 2), (65536, 10)])
+def test_merge_heavy_ties_vs_oracle(eng, oracle, n, levels):
+    """Rows with huge tie groups (<= 10 distinct values, groups of thousands): K4's O(n log n) segmented
+    radix count of the within-group inversions and joint ties, every pair vs the oracle's GSE counts
+    (kernel_sorted.py:195-212), with a time bound (the O(sum g^2) enumeration it replaces needed ~1-10 ms
+    per pair at n = 65536)."""
+    import time
+    rng = np.random.default_rng(n + levels)
+    m = 7
+    x = rng.integers(0, levels, (m, n)).astype(np.int32)
+    x[2] = rng.permutation(n)              # a tie-free row
+    x[3] = 4                               # a constant row (tau_b undefined)
+    x[4, : n // 2] = rng.integers(0, 50, n // 2)  # small and large groups mixed
+    xd = torch.from_numpy(x).cuda()
+    eng.all_pairs(xd, kernel="merge").validate()  # warm-up (allocations)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = eng.all_pairs(xd, kernel="merge", full_counts=True).validate()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    assert dt < 2.0, f"{m * (m + 1) // 2} pairs took {dt:.2f} s"
+    ranks = oracle.rank_matrix(x)
+    _check_full(res, oracle, ranks)

@@ -199,3 +199,44 @@ def test_band_plans_cover_the_job_range():
                     assert all(a[1] == b[0] for a, b in zip(rr, rr[1:])) and all(a < b for a, b in rr)
         auto = types.SimpleNamespace(gemm_bands=None, bands=TauEngine.bands)
         assert len(TauEngine._gemm_ranges(auto, m, 0, total)) == (8 if total >= (1 << 30) else 1)
+
+
+def test_closed_form_cell_counts_and_pass_spans():
+    """Pass planning in O(1) per pass (the reference plans with a per-tile Python loop,
+    engine.py:147-167): closed-form per-tile counts, cells before a tile, the job span a pass touches, and
+    the C ABI's tb_tile_cells, all against brute-force enumeration of tile_cells."""
+    import numpy as np
+
+    import paper_1704_03767_b200 as tb
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.engine import _cells_before, _pass_job_span, _tile_cells_vec, _window_groups
+
+    lib = _lib.load() if os.path.exists(_lib.LIB_PATH) else None
+    for m in (1, 2, 7, 13, 40, 97):
+        for q in (1, 2, 3, 8, 9, 100):
+            space = tb.JobSpace(m, q)
+            tt = space.total_tiles
+            brute = [space.tile_cell_count(*tb.tile_coord(t, space.w)) for t in range(tt)]
+            assert _tile_cells_vec(space, 0, tt).tolist() == brute
+            before = np.concatenate([[0], np.cumsum(brute)])
+            assert _cells_before(space, np.arange(tt + 1)).tolist() == before.tolist()
+            for pass_tiles in (1, 3, 7, 4096):
+                plans = tb.plan_passes(space, (0, tt), pass_tiles)
+                assert sum(p.cells for p in plans) == m * (m + 1) // 2
+                for p in plans:
+                    ii, jj = space.cells_in_tile_order(p.tile_lo, p.tile_hi)
+                    jid = ii * (2 * m - ii + 1) // 2 + jj - ii
+                    assert _pass_job_span(space, p) == (int(jid.min()), int(jid.max()) + 1)
+                    if lib is not None:
+                        assert lib.tb_tile_cells(m, q, p.tile_lo, p.tile_hi) == p.cells
+                for wj in (1, 50, 1 << 25):
+                    groups = _window_groups(space, plans, wj)
+                    assert [p for _, ps in groups for p in ps] == plans
+                    for (lo, hi), ps in groups:
+                        spans = [_pass_job_span(space, p) for p in ps]
+                        assert lo == spans[0][0] and hi == spans[-1][1]
+                        assert len(ps) == 1 or hi - lo <= wj
+    # config-5 scale: 33.6 M tiles planned without per-tile host arrays
+    space = tb.JobSpace(65536, 8)
+    plans = tb.plan_passes(space, (0, space.total_tiles), 4096)
+    assert sum(p.cells for p in plans) == 65536 * 65537 // 2
