@@ -2,30 +2,31 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl ours|reference]
 
-A "step" is one full pass of the hot path over the configured workload
-(BASELINE config 2 by default: m=2048 x n=1000 int32 0..9, every i<j pair):
-K0 rank -> K2 sign pack -> K3 tcgen05 sign GEMM (kind::mxf4, e2m1 signs) ->
-K5 fp64 finalize (tau_a, tau_b).
+Workload: BASELINE config 5 by default (m=65536 x n=1024 float32, 64-factor low-rank, 2.147e9 i<j
+pairs) -- the configuration BASELINE.json defines over 1/2/4/8 GPUs and the largest single-GPU one.
+A "step" is one full pass of the hot path over it: K0 rank -> K2 sign pack -> per row band a K3
+tcgen05 sign GEMM (kind::mxf4, e2m1 signs) + K5 fp64 finalize (tau_b for every job id).
 
-* value: pairs/s with inputs resident in HBM, CUDA-event timed on the launching
-  stream, L2 flushed (256 MiB write) before every timed step, max over ranks.
-* e2e: the same metric through the public host API (TauEngine.all_pairs_host)
-  with pinned HOST buffers: H2D of the values, the full path, D2H of tau_b for
-  every job id, all inside the events.
-* roofline: the GEMM (dominant kernel), algorithmic ops 2K per i<j pair
-  (K = n(n-1)/2 sample pairs), per-launch CUDA-event duration vs the dense
-  tensor peak of the MMA kind it runs (FP4: nominal 9 PFLOP/s, B200_PROFILING.md;
-  int8: measured here with torch._int_mm since MEASURED_PEAKS.json has no int8).
-* cpu_baseline: the oracle port (C restatement of the reference packed/VSE
-  merge kernel, pthreads over all host cores) on a bounded sample (rank 0, N=1).
+* value: pairs/s with inputs resident in HBM, CUDA-event timed on the launching stream, L2 flushed
+  (256 MiB write) before every timed step, max over ranks.
+* N > 1 (``--gpus N``; without a torchrun environment bench.py launches the N ranks itself):
+  strong scaling by default -- rank r computes a contiguous job-id shard of equal modelled cost and
+  streams each finished row band's tau_b to rank 0 (NCCL send/recv per band, overlapped with the next
+  band: the path's only collective); rank 0 checks the gathered stream bit-for-bit.
+  ``--scaling weak``: every rank its own copy of the workload, no collective.
+* e2e: the reference's plugin call, compute_all_pairs(ds, 'vectorized', sink=...) from a host Dataset
+  to 48-byte records delivered to a host sink (wall clock); e2e_tau_b: TauEngine.all_pairs_host
+  (pinned values in, tau_b out, CUDA events).
+* roofline: the GEMM (dominant kernel), algorithmic ops 2K per i<j pair (K = n(n-1)/2 sample pairs),
+  per-launch CUDA-event duration vs the dense tensor peak of the MMA kind it runs (FP4: nominal
+  9 PFLOP/s, B200_PROFILING.md; int8 measured here with torch._int_mm since MEASURED_PEAKS.json has
+  no int8); traffic from the committed ncu capture (profiles/ncu_traffic.json).
+* cpu_baseline: the oracle port (C restatement of the reference packed/VSE kernel, pthreads over all
+  host cores) on the SURVEY 8(d) subset: every pair of m' = 2048 variables drawn by
+  np.random.default_rng(99) for configs 3 and 5 (64 for config 4; configs 1-2 in full).
 
-``--impl reference`` times that CPU implementation alone on the host cores
-(oracle port: the reference is Python/numba and does not travel to the box).
-Multi-GPU (torchrun): every rank computes its own copy of the workload
-(independent objects, no collective) -> "scaling": "weak"; ``--scaling strong``
-shards the job-id range instead (contiguous shards concatenate, pairindex.py:68-80);
-``--gather`` adds the path's only collective (all-gather of the tau_b shards) to every
-timed strong-scaling step.
+``--impl reference`` times that CPU implementation alone on the host cores, each step the same subset
+(the reference is Python/numba and does not travel to the box; rank 0 only under torchrun).
 """
 
 from __future__ import annotations
@@ -56,11 +57,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
-    ap.add_argument("--gather", action="store_true",
-                    help="strong scaling: all-gather every rank's tau_b shard inside the timed step "
-                         "(multi.gather_shards: NCCL all_gather over NVLink)")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="strong (default): one workload sharded over the ranks, bands gathered to rank 0; "
+                         "weak: every rank computes its own copy, no collective")
+    ap.add_argument("--bands", type=int, default=8, help="row bands per rank (one numerator launch each)")
+    ap.add_argument("--e2e-steps", type=int, default=2, help="timed compute_all_pairs plugin calls")
+    ap.add_argument("--e2e-tau-steps", type=int, default=10, help="timed all_pairs_host calls")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay the device step as one CUDA graph (auto: config 1, whose step is launch-bound)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -304,11 +306,28 @@ def measure_int32_peak():
         return None
 
 
+def _strict_pairs(m: int, lo: int, hi: int) -> int:
+    """i<j pairs among job ids [lo, hi) (job ids include the diagonal)."""
+    ys = np.arange(m, dtype=np.int64)
+    dj = ys * (2 * m - ys + 1) // 2
+    return (hi - lo) - int(((dj >= lo) & (dj < hi)).sum())
+
+
+def _max_over_ranks(torch, dist, v: float, world: int, red_dev) -> float:
+    if world == 1:
+        return v
+    t = torch.tensor([v], device=red_dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     rank, local, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
     # TB_BENCH_SHARE_GPU=1 (plumbing check only, never a measurement): ranks share the visible GPUs and
     # talk over gloo, so the N > 1 code path can be exercised on a one-GPU box
     share = os.environ.get("TB_BENCH_SHARE_GPU") == "1"
@@ -324,60 +343,49 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
 
     from paper_1704_03767_b200 import _lib
-    from paper_1704_03767_b200.device import TauEngine
-    from paper_1704_03767_b200.pairindex import job_shard_range
+    from paper_1704_03767_b200.device import get_engine
+    from paper_1704_03767_b200.multi import BandGather, balanced_job_shards, shard_bands
 
     spec, x = workload(args.config)
     m, n = x.shape
     total_jobs = m * (m + 1) // 2
-    job_range = job_shard_range(rank, world, m) if args.scaling == "strong" else (0, total_jobs)
-    eng = TauEngine(local)
+    eng = get_engine(local)  # the engine compute_all_pairs uses too: one set of workspaces
     stream = torch.cuda.Stream(device=dev)
     path = eng.choose_path(n)
-    xin = x  # raw values: both paths rank on the device (K0 / K0w)
-    xd = torch.from_numpy(np.ascontiguousarray(xin)).to(dev)
+    strong = args.scaling == "strong"
+    # strong scaling: rank r owns a contiguous job-id shard of equal modelled cost (multi.balanced_job_shards,
+    # the reference's contiguous shard rule, pairindex.py:68-80); its bands stream to rank 0 (BandGather,
+    # the path's only collective) while later bands compute.  weak: every rank its own copy, no collective.
+    shards = balanced_job_shards(world, m, path) if strong else [(0, total_jobs)] * world
+    job_range = shards[rank]
+    nbands = args.bands
+    bands = shard_bands(*job_range, m, nbands)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # raw values: both paths rank on the device
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     K = n * (n - 1) // 2
+    my_pairs = _strict_pairs(m, *job_range)
+    gathering = strong and world > 1
+    out_full = torch.empty(total_jobs, dtype=torch.float64, device=dev) if (rank == 0 or not gathering) else None
+    local_out = out_full[job_range[0]:job_range[1]] if out_full is not None else \
+        torch.empty(job_range[1] - job_range[0], dtype=torch.float64, device=dev)
+    gather = BandGather(shards, m, nbands, out=out_full, host_staging=share) if gathering else None
+    gemm_events: list = []
 
-    # pairs (i<j) this rank computes
-    def strict_pairs(lo, hi):
-        # job ids include the diagonal; count diagonal cells in [lo, hi)
-        ys = np.arange(m, dtype=np.int64)
-        dj = ys * (2 * m - ys + 1) // 2
-        return (hi - lo) - int(((dj >= lo) & (dj < hi)).sum())
-
-    my_pairs = strict_pairs(*job_range)
-
-    # instrumented step: events around the GEMM (dominant kernel) on the launching stream
-    gemm_events = []
-
-    gather = args.gather and args.scaling == "strong" and world > 1
-    if gather:
-        from paper_1704_03767_b200.multi import gather_shards
-
-    def step(instrument=False):
-        with torch.cuda.stream(stream):
-            if instrument:
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                res = eng.all_pairs(xd, kernel=path, job_range=job_range, stream=stream,
-                                    _events=(s, e))
-                gemm_events.append((s, e))
-            else:
-                res = eng.all_pairs(xd, kernel=path, job_range=job_range, stream=stream)
-            if gather:  # the only collective of the path: tau_b shards -> every rank (stream-ordered)
-                tb = res.tau_b if not share else res.tau_b.cpu()
-                full = gather_shards(tb, m)
-                if rank == 0:
-                    res.extra["tau_b_full"] = full
-        return res
+    def step(timing=None):
+        eng.tau_b_bands(xd, bands, local_out, kernel=path, on_band=gather.band if gather else None, stream=stream,
+                        timing=timing)
+        if gather is not None:
+            with torch.cuda.stream(stream):
+                gather.finish()
 
     for _ in range(args.warmup):
-        res = step()
+        step()
     torch.cuda.synchronize()
-    res.validate()
-    launches_per_step = res.launches
-    sign_format = res.extra.get("sign_format")
-    del res
+    launches0 = _lib.load().tb_launch_count()
+    step()
+    torch.cuda.synchronize()
+    launches_per_step = _lib.load().tb_launch_count() - launches0
+    sign_format = eng.sign_format(int(_lib.load().tb_sign_k(n))) if path == "gemm" else None
 
     if world > 1:
         dist.barrier()
@@ -385,17 +393,17 @@ def run_ours(args):
     sampler = ClockSampler(local)
     sampler.start()
     times = []
-    use_graph = args.graph == "on" or (args.graph == "auto" and args.config == 1)
+    use_graph = args.graph == "on" or (args.graph == "auto" and args.config == 1 and world == 1)
     graph = None
     if use_graph:
         # config 1 is launch-bound; time back-to-back replays of the whole step captured
-        # in one CUDA graph.  The dominant kernel's time still comes from eager instrumented steps.
+        # in one CUDA graph.  The dominant kernel's time comes from instrumented eager steps.
         for _ in range(min(args.steps, 50)):
-            step(instrument=True)
+            step(gemm_events)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream, capture_error_mode="relaxed"):
-            res_graph = eng.all_pairs(xd, kernel=path, job_range=job_range, stream=stream)
+            step()
         torch.cuda.synchronize()
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
@@ -406,76 +414,111 @@ def run_ours(args):
             with torch.cuda.stream(stream):
                 graph.replay()
         else:
-            res = step(instrument=True)
+            step(gemm_events)
         e.record(stream)
         times.append((s, e))
     torch.cuda.synchronize()
     clocks = sampler.stop()
-    if graph is not None:
-        res = res_graph
-        res.validate()
+    eng._tail = None
     gather_check = None
-    if gather and rank == 0:  # the gathered stream equals one device computing every job id
-        full_ref = eng.all_pairs(xd, kernel=path, stream=stream)
+    if gathering and rank == 0:  # the gathered stream equals one device computing every job id
+        ref = eng.all_pairs(xd, kernel=path, tau_a=False, stream=stream)
         torch.cuda.synchronize()
-        got = res.extra["tau_b_full"].to(dev)
-        gather_check = bool(torch.equal(got.view(torch.int64), full_ref.tau_b.view(torch.int64)))
-        del full_ref, got
+        gather_check = bool(torch.equal(out_full.view(torch.int64), ref.tau_b.view(torch.int64)))
+        del ref
     if world > 1:
         dist.barrier()
     t_total = sum(s.elapsed_time(e) for s, e in times) / 1e3
-    gemm_s = [s.elapsed_time(e) / 1e3 for s, e in gemm_events]
-    gemm_avg = sum(gemm_s) / len(gemm_s)
-    t_max = t_total
-    if world > 1:
-        tt = torch.tensor([t_total], device=red_dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-    total_pairs = my_pairs * world
+    num_s = sum(s.elapsed_time(e) for s, e in gemm_events) / 1e3
+    t_max = _max_over_ranks(torch, dist, t_total, world, red_dev)
+    total_pairs = _strict_pairs(m, 0, total_jobs) if strong else my_pairs * world
     value = total_pairs * args.steps / t_max
     ms_per_step = 1e3 * t_max / args.steps
-    del res
+    del local_out, out_full, gather
+    torch.cuda.empty_cache()
 
-    # ---- e2e through the public API with pinned host buffers: H2D values -> device path -> tau_b D2H
-    xh = torch.from_numpy(np.ascontiguousarray(xin)).pin_memory()
-    out_tb = torch.empty(total_jobs, dtype=torch.float64).pin_memory()
+    # ---- e2e (a): the reference's plugin call, compute_all_pairs(ds, 'vectorized', sink=...), from a host
+    # Dataset (int32 ranks, ranked outside the timer like the reference) to 48-byte CELL_DTYPE records
+    # delivered pass by pass to a host sink; each rank runs its tile shard (shard=(rank, world), the
+    # reference's --shard semantics, cli.py:47-48) on its own GPU.  Synchronous host call: wall clock.
+    e2e = None
+    if args.e2e_steps > 0:
+        import paper_1704_03767_b200 as tb
+        ds = tb.Dataset(labels=[str(i) for i in range(m)], ranks=np.stack([tb.rank_transform(r) for r in x]))
+        got = {"records": 0}
+
+        def sink(recs):
+            got["records"] += recs.shape[0]
+
+        def plugin():
+            return tb.compute_all_pairs(ds, "vectorized", shard=(rank, world) if world > 1 else None,
+                                        device=local, sink=sink)
+        plugin()  # warm-up (pinned pass buffers, plans)
+        ts = []
+        for _ in range(args.e2e_steps):
+            got["records"] = 0
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            summary = plugin()
+            ts.append(time.perf_counter() - t0)
+        t_pl = _max_over_ranks(torch, dist, sum(ts), world, red_dev)
+        cells = summary.total_cells
+        assert got["records"] == cells
+        pairs_pl = _strict_pairs(m, 0, total_jobs)  # all shards together cover every pair once
+        e2e = {"value": pairs_pl * len(ts) / t_pl, "unit": UNIT,
+               "h2d_bytes_per_step": int(ds.ranks.nbytes) * world,
+               "d2h_bytes_per_step": int(m * (m + 1) // 2 * 48),
+               "ms_per_step": 1e3 * t_pl / len(ts), "steps": len(ts),
+               "api": ("compute_all_pairs(ds, 'vectorized', sink=...) -- the reference's plugin call "
+                       "(engine.py:300-310): H2D of the int32 ranks, every count on the device, 48-byte "
+                       "CELL_DTYPE records (diagonal included) D2H into pinned pass buffers, delivered to a host "
+                       "sink pass by pass; wall clock" + (f"; rank r runs shard=(r, {world})" if world > 1 else "")),
+               "timer": "wall clock around the synchronous host call"}
+        del ds
+
+    # ---- e2e (b): tau_b through the host-buffer API (pinned values in, tau_b f64 for the rank's job range
+    # out), row bands overlapping the D2H with compute; CUDA events; max over ranks
+    xh = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+    jr = shards[rank]
+    out_tb = torch.empty(jr[1] - jr[0], dtype=torch.float64).pin_memory()
     e2e_times = []
     e2e_launches = 0
-    for it in range(args.e2e_steps + 2):
+    for it in range(args.e2e_tau_steps + 2):
         with torch.cuda.stream(stream):
             flush.zero_()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
-            r = eng.all_pairs_host(xh, out_tb, kernel=path, stream=stream)
+            r = eng.all_pairs_host(xh, out_tb, kernel=path, stream=stream, job_range=jr)
             e.record(stream)
         if it >= 2:
             e2e_times.append((s, e))
         e2e_launches = r.launches
         del r
     torch.cuda.synchronize()
-    e2e_t = sum(s.elapsed_time(e) for s, e in e2e_times) / 1e3
-    if world > 1:
-        tt = torch.tensor([e2e_t], device=red_dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_t = float(tt.item())
-    # every rank runs the full host entry point: weak scaling counts each rank's copy, strong scaling
-    # (one shared job range) does not shard this leg, so it counts the pairs once
-    e2e_pairs = strict_pairs(0, total_jobs) * (world if args.scaling == "weak" else 1)
-    e2e_value = e2e_pairs * len(e2e_times) / e2e_t if e2e_times else None  # --e2e-steps 0: leg skipped
-    h2d = xh.numel() * xh.element_size()
-    d2h = total_jobs * 8
+    e2e_t = _max_over_ranks(torch, dist, sum(s.elapsed_time(e) for s, e in e2e_times) / 1e3, world, red_dev)
+    e2e_tau = {"value": total_pairs * len(e2e_times) / e2e_t if e2e_times else None, "unit": UNIT,
+               "h2d_bytes_per_step": int(xh.numel() * xh.element_size()) * world,
+               "d2h_bytes_per_step": int(total_jobs * 8) if strong else int(total_jobs * 8) * world,
+               "ms_per_step": 1e3 * e2e_t / len(e2e_times) if e2e_times else None,
+               "api": "TauEngine.all_pairs_host (pinned host values in, tau_b f64 for the rank's job range out; "
+                      "row bands overlap D2H with compute); CUDA events",
+               "gpu_launches_per_step": e2e_launches}
+    del xh, out_tb
 
     out = None
     if rank == 0:
         peak = measure_int8_peak(torch, dev) if path == "gemm" else None
         algo = 2 * K * my_pairs if path == "gemm" else 4 * n * int(np.ceil(np.log2(n))) * my_pairs
-        achieved = algo / gemm_avg
+        num_avg = num_s / max(1, args.steps + (min(args.steps, 50) if use_graph else 0))
+        achieved = algo / num_avg if num_avg > 0 else 0.0
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
             with open(tpath) as fh:
                 tj = json.load(fh)
             traffic = tj.get(f"config{args.config}", {}).get("dram_bytes_per_launch")
+        per_step_units = len(bands)
         if path == "gemm":
             fp4 = sign_format == _lib.TB_SIGN_E2M1
             fp4_lib = measure_fp4_peak(torch, dev) if fp4 else None
@@ -497,8 +540,11 @@ def run_ours(args):
                     "measured_mma_ceiling_tflops": mma_ceiling / 1e12 if mma_ceiling else None,
                     "frac_of_measured_mma_ceiling": (achieved / mma_ceiling) if mma_ceiling else None,
                     "measured_int8_peak_tops": peak / 1e12 if peak else None,
-                    "algorithmic": f"2*K ops per i<j pair, K=n(n-1)/2={K} sample pairs; {my_pairs} pairs per launch",
-                    "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}
+                    "algorithmic": (f"2*K ops per i<j pair, K=n(n-1)/2={K} sample pairs; {my_pairs} pairs per step "
+                                    f"in {per_step_units} row-band launches (achieved = per-launch algorithmic ops / "
+                                    f"per-launch CUDA-event time, same ratio as the step totals)"),
+                    "traffic_scope": "dram bytes of one row-band launch (ncu --set full, band 0)",
+                    "kernel_ms_per_step": 1e3 * num_avg, "kernel_share_of_step": num_avg / (t_total / args.steps)}
         else:
             # INT32 issue peak measured here: dependency-free IADD3/LOP3 chains on every SM
             # (csrc/tb_probe.cu); the nominal 128 lanes/clk/SM x SMs x max clock is reported beside it
@@ -511,8 +557,8 @@ def run_ours(args):
                     "peak_source": ("measured here: IADD3/LOP3 microbenchmark, best of 5 (libtbprobe.so)" if measured
                                     else "nominal INT32 issue 128 lanes/clk/SM x SMs x 1.965 GHz (probe failed)"),
                     "nominal_int32_tops": nominal / 1e12,
-                    "algorithmic": f"4*n*ceil(log2 n) INT32 ops per i<j pair, n={n}; {my_pairs} pairs per launch",
-                    "kernel_ms": 1e3 * gemm_avg, "kernel_share_of_step": gemm_avg / (t_total / args.steps)}
+                    "algorithmic": f"4*n*ceil(log2 n) INT32 ops per i<j pair, n={n}; {my_pairs} pairs per step",
+                    "kernel_ms_per_step": 1e3 * num_avg, "kernel_share_of_step": num_avg / (t_total / args.steps)}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
@@ -523,23 +569,24 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": ("e2m1" if sign_format == _lib.TB_SIGN_E2M1 else "i8") if path == "gemm" else "int32",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": ("e2m1" if sign_format == _lib.TB_SIGN_E2M1 else "i8") if path == "gemm" else "int32",
             "data": "synthetic",
             "config": {"workload": f"config{args.config}_{spec.name}", "m": m, "n": n,
-                       "pairs_per_rank": my_pairs, "path": path,
-                       "l2": "flushed before every timed step (256 MiB write, untimed)",
+                       "pairs": total_pairs, "pairs_per_rank": my_pairs, "path": path,
+                       "shards": "balanced contiguous job-id shards (multi.balanced_job_shards)" if gathering
+                       else "one job range", "bands_per_rank": len(bands),
+                       "l2": "flushed before every timed step (256 MiB write, untimed); config-5 operands (S = 17 GB) "
+                             "exceed L2 anyway",
                        "step": "one CUDA graph replay" if use_graph else "eager launches",
-                       "outputs": "numerator i32 + tau_a f64 + tau_b f64 in job-id order"
-                       + ("; tau_b shards all-gathered to every rank inside the step" if gather else "")},
-            "roofline": roof, "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_t / len(e2e_times) if e2e_times else None,
-                    "api": "TauEngine.all_pairs_host (pinned host values in, tau_b f64 for every job id out; "
-                           "row bands overlap D2H with compute)", "gpu_launches_per_step": e2e_launches},
+                       "outputs": "tau_b f64 for every job id in job-id order (numerators in a workspace)"
+                       + ("; every rank's bands gathered to rank 0 (NCCL send/recv per band) inside the step"
+                          if gathering else "")},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_tau_b": e2e_tau,
             "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
-            "abi": _lib.TB_MAX_N and "libtaub200.so",
+            "abi": "libtaub200.so",
         }
-        if gather:
+        if gathering:
             out["gather_check"] = gather_check
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -547,12 +594,29 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _relaunch(args) -> int:
+    """--gpus N without a torchrun environment: launch N ranks (one per GPU) through torch.distributed.run
+    on 127.0.0.1 and return their exit status."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines (NVLS / P2P transport) go to stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args))
+    run_ours(args)
 
 
 if __name__ == "__main__":

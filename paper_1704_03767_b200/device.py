@@ -149,16 +149,18 @@ class TauEngine:
             st = stream if stream is not None else torch.cuda.current_stream(self.device)
             if st.device != self.device:
                 raise ConfigError(f"stream is on {st.device}, engine on {self.device}")
-            if self._tail is not None:
+            capturing = torch.cuda.is_current_stream_capturing()
+            if self._tail is not None and not capturing:
                 st.wait_event(self._tail)
             self._stream, self._events = st, None
             try:
                 with torch.cuda.stream(st):
                     yield st
             finally:
-                ev = torch.cuda.Event()
-                ev.record(st)
-                self._tail = ev
+                if not capturing:  # (a graph replay is ordered by the stream it is replayed on)
+                    ev = torch.cuda.Event()
+                    ev.record(st)
+                    self._tail = ev
 
     # -------------------------------------------------------------- workspaces
     def _buf(self, name: str, numel: int, dtype: torch.dtype) -> torch.Tensor:
@@ -375,6 +377,36 @@ class TauEngine:
                 out.append((lo, hi))
         return out
 
+    def tau_b_bands(self, x: torch.Tensor, bands: list, out: torch.Tensor, kernel: str = "auto", on_band=None,
+                    stream: torch.cuda.Stream | None = None, timing: list | None = None) -> Prepared:
+        """tau_b of the consecutive job ranges ``bands`` (one rank's shard, multi.shard_bands) into
+        ``out`` (indexed from bands[0][0]), band by band -- one numerator launch and one finalize each --
+        calling ``on_band(b, out_slice)`` after band b's finalize is enqueued (multi.BandGather.band ships
+        it while band b+1 computes).  Asynchronous on ``stream``; ``timing`` collects (start, end) CUDA
+        events around each band's numerator kernels (bench instrumentation)."""
+        m, n = x.shape
+        path = self.choose_path(n) if kernel == "auto" else kernel
+        if not bands:
+            return None
+        base = bands[0][0]
+        with self._session(stream) as st_t:
+            st = _stream_ptr(st_t)
+            prep = self.prepare(x, path, row_lo=job_coord(base, m)[0])
+            num = self._buf("num_band", max(hi - lo for lo, hi in bands), torch.int32)
+            for b, (lo, hi) in enumerate(bands):
+                if timing is not None:  # (start, end) events around the band's numerator kernels
+                    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    ev[0].record(st_t)
+                self.numerators(prep, lo, hi, num)
+                if timing is not None:
+                    ev[1].record(st_t)
+                    timing.append(ev)
+                tb = out[lo - base:hi - base]
+                _lib.call("tb_finalize", _ptr(num), _ptr(prep.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
+                if on_band is not None:
+                    on_band(b, tb)
+        return prep
+
     # -------------------------------------------------------------- host-buffer entry point
     @staticmethod
     def bands(m: int, nbands: int = 3, align: int = 256, fracs: tuple | None = None) -> list[int]:
@@ -409,17 +441,21 @@ class TauEngine:
     def all_pairs_host(self, x_host: torch.Tensor, tau_b_out: torch.Tensor, kernel: str = "auto",
                        band_fracs: tuple | None = None, stream: torch.cuda.Stream | None = None,
                        copy_stream: torch.cuda.Stream | None = None, h2d_chunks: int = 2,
-                       h2d_piece_bytes: int = 4 << 20) -> PairResult:
+                       h2d_piece_bytes: int = 4 << 20, job_range: tuple[int, int] | None = None) -> PairResult:
         """End-to-end from host buffers: H2D of the values, the device path, tau_b back to host.
 
-        The job range is cut into row bands; band i's tau_b copy (on ``copy_stream``) overlaps
-        band i+1's numerator kernel.  ``x_host`` and ``tau_b_out`` should be pinned; the call is
-        asynchronous on ``stream`` (which finally waits for the copies).
+        The job range (default: every job id; a rank's shard under multi-GPU strong scaling) is cut into
+        row bands; band i's tau_b copy (on ``copy_stream``) overlaps band i+1's numerator kernel.
+        ``tau_b_out[j - job_lo]`` receives job id j.  ``x_host`` and ``tau_b_out`` should be pinned; the
+        call is asynchronous on ``stream`` (which finally waits for the copies).
         """
         m, n = x_host.shape
         total = m * (m + 1) // 2
-        if tau_b_out.numel() < total:
-            raise ConfigError(f"tau_b_out holds {tau_b_out.numel()} values, need {total}")
+        jlo, jhi = (0, total) if job_range is None else (int(job_range[0]), int(job_range[1]))
+        if not 0 <= jlo <= jhi <= total:
+            raise ConfigError(f"job range [{jlo}, {jhi}) outside [0, {total})")
+        if tau_b_out.numel() < jhi - jlo:
+            raise ConfigError(f"tau_b_out holds {tau_b_out.numel()} values, need {jhi - jlo}")
         path = self.choose_path(n) if kernel == "auto" else kernel
         with self._session(stream) as st_t:
             cp_t = copy_stream if copy_stream is not None else self._copy_stream()
@@ -443,11 +479,11 @@ class TauEngine:
                     ev_c.record(cp_t)
                 chunks.append((r0, r1, ev_c))
             c0 = _lib.load().tb_launch_count()
-            res = PairResult(m=m, n=n, job_lo=0, job_hi=total, path=path,
-                             numerator=self._buf("num_all", total, torch.int32),
+            res = PairResult(m=m, n=n, job_lo=jlo, job_hi=jhi, path=path,
+                             numerator=self._buf("num_all", jhi - jlo, torch.int32),
                              n1_rows=torch.empty(m, dtype=torch.int64, device=self.device),
                              flags=torch.zeros(1, dtype=torch.int32, device=self.device))
-            res.tau_b = self._buf("taub_all", total, torch.float64)
+            res.tau_b = self._buf("taub_all", jhi - jlo, torch.float64)
             if path == "gemm":
                 S, K, ldS, fmt = self._gemm_prepare(
                     x, res, st, row_chunks=[(r0, r1, (lambda e=ev: st_t.wait_event(e))) for r0, r1, ev in chunks])
@@ -456,11 +492,15 @@ class TauEngine:
                     st_t.wait_event(ev)
                 pos, srt, keys, maxgrp = self._merge_prepare(x, res, st)
             if band_fracs is None:
-                band_fracs = self.default_band_fracs(total)
-            cuts = self.bands(m, len(band_fracs), fracs=band_fracs)
-            for r0, r1 in zip(cuts[:-1], cuts[1:]):
-                lo, hi = r0 * (2 * m - r0 + 1) // 2, r1 * (2 * m - r1 + 1) // 2
-                num = res.numerator[lo:hi]
+                band_fracs = self.default_band_fracs(jhi - jlo)
+            y0 = job_coord(jlo, m)[0] if jhi > jlo else 0
+            # row bands of the job range's own rows (equal shares of its pairs)
+            sub = [y0 + c for c in self.bands(m - y0, len(band_fracs), fracs=band_fracs)]
+            for r0, r1 in zip(sub[:-1], sub[1:]):
+                lo, hi = max(jlo, r0 * (2 * m - r0 + 1) // 2), min(jhi, r1 * (2 * m - r1 + 1) // 2)
+                if hi <= lo:
+                    continue
+                num = res.numerator[lo - jlo:hi - jlo]
                 if path == "gemm":
                     self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st)
                 else:
@@ -468,13 +508,13 @@ class TauEngine:
                     _lib.call("tb_merge_pairs", _ptr(keys), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp[0]),
                               _ptr(maxgrp[1]), _ptr(maxgrp[2]), m, n, lo, hi, _ptr(num), None, None, _ptr(ws), wsb,
                               st)
-                tb = res.tau_b[lo:hi]
+                tb = res.tau_b[lo - jlo:hi - jlo]
                 _lib.call("tb_finalize", _ptr(num), _ptr(res.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
                 ev = torch.cuda.Event()
                 ev.record(st_t)
                 cp_t.wait_event(ev)
                 with torch.cuda.stream(cp_t):
-                    tau_b_out[lo:hi].copy_(tb, non_blocking=True)
+                    tau_b_out[lo - jlo:hi - jlo].copy_(tb, non_blocking=True)
             st_t.wait_stream(cp_t)
             res.launches = _lib.load().tb_launch_count() - c0
         return res

@@ -1,11 +1,18 @@
-"""Multi-GPU plumbing: one process per GPU, contiguous job-id shards, optional gather.
+"""Multi-GPU plumbing: one process per GPU, contiguous job-id shards, banded gather to one consumer.
 
-Every pair is independent, so ranks never exchange data while computing:
-rank r of p computes job ids ``job_shard_range(r, p, m)`` (the reference's
-contiguous ceil-chunk shard rule, pairindex.py:68-80, applied to job ids), and
-the shards concatenate to the full job-id stream.  The only collective is the
-optional gather of result shards to one consumer rank -- an all_gather of
-equal, padded chunks (NCCL over NVLink on a B200 box; gloo in the CPU tests).
+Every pair is independent, so ranks never exchange data while computing: rank r of p computes a
+contiguous job-id range (the reference's contiguous shard rule, pairindex.py:68-80, applied to job ids;
+PAPER.md:538), and the shards concatenate to the full job-id stream.  The only collective is the gather
+of result bands (tau_b) to one consumer rank, pipelined with the compute:
+
+* ``balanced_job_shards`` cuts the job range so every rank's *cost* is equal, not just its pair count:
+  on the GEMM path a shard also sign-packs every row from its first one to m, so early shards do more
+  packing per pair (cost model: pairs + ROW_COST_PAIRS x rows packed).
+* ``shard_bands`` splits a shard into row-aligned bands of equal pair counts; a rank finishes band b,
+  then hands it to ``BandGather.band``: point-to-point sends to the consumer (NCCL over NVLink on a B200
+  box: ncclSend/ncclRecv grouped per band; gloo in the CPU tests), issued right after the band's
+  finalize on the compute stream, so band b crosses NVLink while band b+1 is computed.  The consumer
+  posts the matching receives into its full-size output.
 """
 
 from __future__ import annotations
@@ -14,6 +21,88 @@ import torch
 import torch.distributed as dist
 
 from .pairindex import job_shard_range
+
+# Sign-pack cost of one row in units of one pair's GEMM cost, from the config-5 launch list
+# (profiles/r02_launches: signpack 3.9 ms for 65536 rows vs gemm 401 ms for 2.147e9 pairs: 59.5 ns vs
+# 0.187 ns).
+ROW_COST_PAIRS = 319
+
+
+def _row_prefix(y: int, m: int) -> int:
+    return y * (2 * m - y + 1) // 2
+
+
+def _row_of(j: int, m: int) -> int:
+    """Row of job id j (integer bisection; exact for any m)."""
+    lo, hi = 0, m - 1
+    while lo < hi:
+        mid = (lo + hi + 1) // 2
+        if _row_prefix(mid, m) <= j:
+            lo = mid
+        else:
+            hi = mid - 1
+    return lo
+
+
+def shard_cost(lo: int, hi: int, m: int, path: str = "gemm") -> float:
+    if hi <= lo:
+        return 0.0
+    return (hi - lo) + (ROW_COST_PAIRS * (m - _row_of(lo, m)) if path == "gemm" else 0)
+
+
+def balanced_job_shards(world: int, m: int, path: str = "gemm") -> list[tuple[int, int]]:
+    """Contiguous job-id shards of equal modelled cost covering [0, m(m+1)/2) (bisection on the
+    per-shard cost target; the merge path's cost is its pair count, i.e. job_shard_range)."""
+    total = m * (m + 1) // 2
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if path != "gemm" or world == 1:
+        return [job_shard_range(r, world, m) for r in range(world)]
+
+    def cut(target: float):
+        bounds, lo = [0], 0
+        for _ in range(world - 1):
+            a, b = lo, total  # largest hi with cost(lo, hi) <= target
+            while a < b:
+                mid = (a + b + 1) // 2
+                if shard_cost(lo, mid, m, path) <= target:
+                    a = mid
+                else:
+                    b = mid - 1
+            lo = a
+            bounds.append(lo)
+        bounds.append(total)
+        return bounds
+
+    t_lo, t_hi = 0.0, shard_cost(0, total, m, path)
+    for _ in range(100):
+        t = 0.5 * (t_lo + t_hi)
+        b = cut(t)
+        if shard_cost(b[-2], b[-1], m, path) <= t:
+            t_hi = t
+        else:
+            t_lo = t
+        if t_hi - t_lo < 1.0:
+            break
+    b = cut(t_hi)
+    return list(zip(b[:-1], b[1:]))
+
+
+def shard_bands(lo: int, hi: int, m: int, nbands: int) -> list[tuple[int, int]]:
+    """[lo, hi) split into <= nbands contiguous sub-ranges of (about) equal pair counts, cut at row
+    starts where the range spans rows (so each band is a row band of the GEMM), else evenly."""
+    if hi <= lo:
+        return []
+    cuts = [lo]
+    for k in range(1, nbands):
+        j = lo + (hi - lo) * k // nbands
+        y = _row_of(j, m)
+        r = _row_prefix(y, m)
+        j = r if r > cuts[-1] else j
+        if cuts[-1] < j < hi:
+            cuts.append(j)
+    cuts.append(hi)
+    return list(zip(cuts[:-1], cuts[1:]))
 
 
 def my_job_range(m: int, rank: int | None = None, world: int | None = None) -> tuple[int, int]:
@@ -24,13 +113,86 @@ def my_job_range(m: int, rank: int | None = None, world: int | None = None) -> t
     return job_shard_range(rank, world, m)
 
 
-def gather_shards(local: torch.Tensor, m: int, dst: int = 0, group=None) -> torch.Tensor | None:
-    """Concatenate every rank's job-range shard on rank ``dst`` (None elsewhere).
+class BandGather:
+    """Stream every rank's shard bands to ``dst`` as they finish.
 
-    ``local`` is this rank's per-pair tensor for ``my_job_range(m)``.  Shards
-    are padded to the common chunk length so one all_gather_into_tensor moves
-    them; ``dst`` trims the padding.
-    """
+    All ranks know every rank's shard and band plan (deterministic), so the consumer posts exactly the
+    matching receives: for band b, one receive per other rank into ``out[band]`` (job-id offsets).  On
+    NCCL the sends / receives of one band are one grouped launch (batch_isend_irecv) that waits for the
+    band's finalize on the current stream and runs on the communicator's stream, overlapping the next
+    band's kernels; ``finish()`` makes the current stream wait for all of them.  ``host_staging`` copies
+    device bands through host memory (gloo plumbing runs)."""
+
+    def __init__(self, shards: list[tuple[int, int]], m: int, nbands: int, out: torch.Tensor | None = None,
+                 dst: int = 0, group=None, host_staging: bool = False):
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if len(shards) != self.world:
+            raise ValueError(f"{len(shards)} shards for {self.world} ranks")
+        self.shards, self.m, self.dst, self.group = shards, m, dst, group
+        self.bands = [shard_bands(lo, hi, m, nbands) for lo, hi in shards]
+        self.nb = max(len(b) for b in self.bands)
+        self.out = out
+        self.host = host_staging
+        self.works: list = []
+        self._keep: list = []
+        self._pending: list = []
+        self._nccl = dist.get_backend(group) == "nccl"
+        self._next = 0  # next band index this rank ships (the consumer posts receives up to nb in finish)
+        if self.rank == dst and out is None:
+            raise ValueError("the consumer rank needs an output tensor")
+
+    def band(self, b: int, local: torch.Tensor) -> None:
+        """Rank's band b (job ids self.bands[rank][b]) is finished on the current stream: ship it."""
+        ops = []
+        self._next = b + 1
+        if self.rank == self.dst:
+            if local is not None and b < len(self.bands[self.rank]):
+                blo, bhi = self.bands[self.rank][b]
+                dst_view = self.out[blo:bhi]
+                if local.data_ptr() != dst_view.data_ptr():
+                    dst_view.copy_(local, non_blocking=True)
+            for r in range(self.world):
+                if r == self.rank or b >= len(self.bands[r]):
+                    continue
+                blo, bhi = self.bands[r][b]
+                view = self.out[blo:bhi]
+                if self.host:
+                    buf = torch.empty(bhi - blo, dtype=self.out.dtype)
+                    self._pending.append((view, buf))
+                    view = buf
+                ops.append(dist.P2POp(dist.irecv, view, r, self.group))
+        elif b < len(self.bands[self.rank]):
+            t = local
+            if self.host:
+                t = local.cpu()
+                self._keep.append(t)
+            ops.append(dist.P2POp(dist.isend, t, self.dst, self.group))
+        if not ops:
+            return
+        if self._nccl:
+            self.works.extend(dist.batch_isend_irecv(ops))
+        else:
+            for op in ops:
+                self.works.append(op.op(op.tensor, op.peer, op.group))
+
+    def finish(self) -> None:
+        """Post the consumer's receives for bands it had none of its own for, then make the current
+        stream (NCCL) / the host (gloo) wait for every transfer."""
+        if self.rank == self.dst:
+            for b in range(self._next, self.nb):
+                self.band(b, None)
+        self._next = 0
+        for w in self.works:
+            w.wait()
+        for view, buf in self._pending:
+            view.copy_(buf)
+        self.works, self._keep, self._pending = [], [], []
+
+
+def gather_shards(local: torch.Tensor, m: int, dst: int = 0, group=None) -> torch.Tensor | None:
+    """Concatenate every rank's job_shard_range shard on rank ``dst`` (None elsewhere): one
+    all_gather_into_tensor of equal padded chunks (the simple, un-pipelined form of BandGather)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     total = m * (m + 1) // 2

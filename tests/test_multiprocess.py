@@ -55,3 +55,60 @@ def test_gloo_two_rank_shards_gather(tmp_path, m):
     mp.spawn(_worker, args=(2, port, m, 33, out), nprocs=2, join=True)
     got, ref = np.load(out)
     np.testing.assert_array_equal(got, ref)
+
+
+def _band_worker(rank, world, port, m, nbands, out_path):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    from paper_1704_03767_b200.multi import BandGather, balanced_job_shards, shard_bands
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    shards = balanced_job_shards(world, m, "gemm")
+    lo, hi = shards[rank]
+    total = m * (m + 1) // 2
+    out = torch.full((total,), -1.0, dtype=torch.float64) if rank == 0 else None
+    local = out[lo:hi] if rank == 0 else torch.empty(hi - lo, dtype=torch.float64)
+    g = BandGather(shards, m, nbands, out=out)
+    for step in range(2):  # the gather object is reused across steps
+        for b, (blo, bhi) in enumerate(shard_bands(lo, hi, m, nbands)):
+            # "compute" band b: job id j -> j + 0.5 * step (what the device finalize would write)
+            local[blo - lo:bhi - lo] = torch.arange(blo, bhi, dtype=torch.float64) + 0.5 * step
+            g.band(b, local[blo - lo:bhi - lo])
+        g.finish()
+        if rank == 0:
+            ok = torch.equal(out, torch.arange(total, dtype=torch.float64) + 0.5 * step)
+            np.save(out_path + f".{step}.npy", np.array([ok]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m,nbands", [(2, 1, 3), (2, 40, 4), (3, 300, 5), (4, 7, 8)])
+def test_gloo_banded_gather(tmp_path, world, m, nbands):
+    """BandGather over gloo (world 2-4): every rank ships its shard's bands as they finish, the consumer
+    assembles the full job-id stream, also when ranks have different band counts (tiny shards)."""
+    out = str(tmp_path / "ok")
+    mp.spawn(_band_worker, args=(world, _free_port(), m, nbands, out), nprocs=world, join=True)
+    for step in range(2):
+        assert bool(np.load(out + f".{step}.npy")[0])
+
+
+def test_balanced_shards_partition_and_balance():
+    from paper_1704_03767_b200.multi import balanced_job_shards, shard_bands, shard_cost
+    for m in (1, 5, 300, 65536):
+        total = m * (m + 1) // 2
+        for world in (1, 2, 3, 8):
+            for path in ("gemm", "merge"):
+                sh = balanced_job_shards(world, m, path)
+                assert len(sh) == world and sh[0][0] == 0 and sh[-1][1] == total
+                assert all(a[1] == b[0] for a, b in zip(sh, sh[1:])) and all(lo <= hi for lo, hi in sh)
+                for lo, hi in sh:
+                    bands = shard_bands(lo, hi, m, 4)
+                    assert (not bands and lo == hi) or (bands[0][0] == lo and bands[-1][1] == hi)
+                    assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(bands, bands[1:]))
+    sh = balanced_job_shards(8, 65536, "gemm")
+    costs = [shard_cost(lo, hi, 65536) for lo, hi in sh]
+    assert max(costs) / min(costs) < 1.001
+    assert sh[0][1] - sh[0][0] < sh[-1][1] - sh[-1][0]  # early shards pack more rows: fewer pairs
