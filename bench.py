@@ -292,16 +292,18 @@ def measure_mxf4_ceiling():
         return None
 
 
-def measure_int32_peak():
-    """INT32 lane-ops/s of dependency-free IADD3/LOP3 chains on all SMs (csrc/tb_probe.cu)."""
+def measure_int32_peak(mixed: bool = False):
+    """INT32 lane-ops/s on all SMs (csrc/tb_probe.cu): dependency-free IADD3/LOP3 chains (ALU pipe only),
+    or with ``mixed`` half of them IMAD chains on the FMA pipe -- the issue ceiling of K4's ALU + FMA mix."""
     try:
         import ctypes
         lib = ctypes.CDLL(os.path.join(ROOT, "paper_1704_03767_b200", "libtbprobe.so"))
-        lib.tb_probe_int32_ops.restype = ctypes.c_double
-        lib.tb_probe_int32_ops.argtypes = [ctypes.c_int]
-        v = float(lib.tb_probe_int32_ops(5))
+        fn = lib.tb_probe_int32_mixed_ops if mixed else lib.tb_probe_int32_ops
+        fn.restype = ctypes.c_double
+        fn.argtypes = [ctypes.c_int]
+        v = float(fn(5))
         return v if v > 0 else None
-    except OSError as exc:
+    except (OSError, AttributeError) as exc:
         print(f"# int32 probe unavailable: {exc}", file=sys.stderr)
         return None
 
@@ -546,16 +548,21 @@ def run_ours(args):
                     "traffic_scope": "dram bytes of one row-band launch (ncu --set full, band 0)",
                     "kernel_ms_per_step": 1e3 * num_avg, "kernel_share_of_step": num_avg / (t_total / args.steps)}
         else:
-            # INT32 issue peak measured here: dependency-free IADD3/LOP3 chains on every SM
-            # (csrc/tb_probe.cu); the nominal 128 lanes/clk/SM x SMs x max clock is reported beside it
+            # INT32 roofline measured here: K4 splits its integer work over the ALU and FMA pipes,
+            # so its ceiling is the issue rate of a mixed IADD3/LOP3 + IMAD stream (csrc/tb_probe.cu); the
+            # ALU-only IADD3/LOP3 figure and the nominal 128 lanes/clk/SM x SMs x max clock are reported beside it
             props = torch.cuda.get_device_properties(dev)
             nominal = 128 * props.multi_processor_count * 1.965e9
-            measured = measure_int32_peak()
-            int32_peak = measured or nominal
+            mixed = measure_int32_peak(mixed=True)
+            alu = measure_int32_peak()
+            int32_peak = mixed or nominal
             roof = {"bound": "int32", "achieved": achieved / 1e12, "peak": int32_peak / 1e12, "unit": "TOP/s",
                     "frac": achieved / int32_peak, "traffic": traffic, "kernel": "merge_pairs_kernel",
-                    "peak_source": ("measured here: IADD3/LOP3 microbenchmark, best of 5 (libtbprobe.so)" if measured
+                    "peak_source": ("measured here: mixed IADD3/LOP3 + IMAD issue microbenchmark, best of 5 "
+                                    "(libtbprobe.so tb_probe_int32_mixed_ops)" if mixed
                                     else "nominal INT32 issue 128 lanes/clk/SM x SMs x 1.965 GHz (probe failed)"),
+                    "measured_alu_only_tops": alu / 1e12 if alu else None,
+                    "frac_of_alu_only": achieved / alu if alu else None,
                     "nominal_int32_tops": nominal / 1e12,
                     "algorithmic": f"4*n*ceil(log2 n) INT32 ops per i<j pair, n={n}; {my_pairs} pairs per step",
                     "kernel_ms_per_step": 1e3 * num_avg, "kernel_share_of_step": num_avg / (t_total / args.steps)}

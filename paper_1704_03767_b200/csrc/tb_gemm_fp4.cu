@@ -346,7 +346,12 @@ static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<i
     // right-edge remnants share units instead of each becoming a half-empty one.  Units are listed
     // per 8-row-block group (2048 rows) in windows of 8 column blocks, so concurrently running pairs
     // share S rows through L2.
-    const int64_t RB = (m + g4::UM - 1) / g4::UM, GR = 8;
+    // unit-order knobs (experiments; TB_GEMM_GR row blocks per group, TB_GEMM_WIN column blocks per window,
+    // TB_GEMM_SERP=1 reverses the window order of every other group)
+    static const int64_t kGR = [] { const char* e = std::getenv("TB_GEMM_GR"); return e ? std::max(1, atoi(e)) : 8; }();
+    static const int64_t kWIN = [] { const char* e = std::getenv("TB_GEMM_WIN"); return e ? std::max(1, atoi(e)) : 8; }();
+    static const bool kSERP = [] { const char* e = std::getenv("TB_GEMM_SERP"); return e && e[0] == '1'; }();
+    const int64_t RB = (m + g4::UM - 1) / g4::UM, GR = kGR;
     const int64_t b_last = (m - 1) / g4::BN;
     int64_t y_lo, x_lo, y_hi, x_hi;
     job_coord(job_lo, m, y_lo, x_lo);
@@ -362,9 +367,12 @@ static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<i
             const int64_t r0 = yb * g4::UM, r1 = std::min(r0 + g4::UM, m) - 1;
             if (r1 < y_lo || r0 > y_hi) continue;  // outside the job range rows
             for (int64_t b = r0 / g4::BN; b <= b_last; b += 2)
-                g.push_back(U{b / 8, yb, b, b + 1 <= b_last ? b + 1 : -1});
+                g.push_back(U{b / kWIN, yb, b, b + 1 <= b_last ? b + 1 : -1});
         }
-        std::stable_sort(g.begin(), g.end(), [](const U& a, const U& b) { return a.win < b.win; });
+        if (kSERP && (SY & 1))
+            std::stable_sort(g.begin(), g.end(), [](const U& a, const U& b) { return a.win > b.win; });
+        else
+            std::stable_sort(g.begin(), g.end(), [](const U& a, const U& b) { return a.win < b.win; });
         for (const U& u : g) {
             code.push_back((int32_t)u.yb);
             nb.push_back((int32_t)((u.b0 << 16) | (u.b1 < 0 ? 0xFFFF : u.b1)));

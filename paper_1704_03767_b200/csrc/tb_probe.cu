@@ -42,6 +42,44 @@ __global__ void __launch_bounds__(256) int32_probe_kernel(uint32_t* out, int ite
     if (s == 0x12345678u) out[0] = s;  // keeps the chains alive
 }
 
+// The issue ceiling of a kernel that splits its integer work over both integer-capable pipes, as K4 does
+// (ALU: IADD3 / LOP3 / min / max / SEL ...; FMA: IMAD): per iteration 8 IADD3 + 8 LOP3 chains on the ALU
+// pipe and 16 independent IMAD chains on the FMA pipe (mad.lo with a runtime multiplier, so ptxas cannot
+// turn it into shifts / adds).  Each pipe accepts one warp instruction per 2 cycles per SM sub-partition
+// and the scheduler issues one per cycle, so a 50/50 mix is bounded by issue: 128 lane-ops / clk / SM.
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+__global__ void __launch_bounds__(256) int32_mixed_probe_kernel(uint32_t* out, int iters, uint32_t seed, uint32_t mul) {
+    uint32_t a[8], b[8], f[16];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        a[k] = threadIdx.x * (k + 1) + seed;
+        b[k] = threadIdx.x ^ (seed + 977u * k);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) f[k] = threadIdx.x + 31u * k + seed;
+    const uint32_t c = seed | 1u;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            a[k] = iadd3(a[k], b[(k + 1) & 7], c);
+            f[2 * k] = imad(f[2 * k], mul, c);
+            b[k] = lop3(b[k], a[(k + 3) & 7], c);
+            f[2 * k + 1] = imad(f[2 * k + 1], mul, a[k]);
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= a[k] ^ b[k];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s ^= f[k];
+    if (s == 0x12345678u) out[0] = s;  // keeps the chains alive
+}
+
 // tcgen05.mma.cta_group::2.kind::mxf4.block_scale, M=256, the GEMM's two N=240 accumulators issued
 // alternately, back to back from shared memory by one thread per CTA pair (no TMA, no epilogue):
 // the MMA pipe's sustained rate for the numerator GEMM's instruction stream.
@@ -145,5 +183,35 @@ extern "C" double tb_probe_int32_ops(int reps) {
     cudaFree(out);
     if (cudaGetLastError() != cudaSuccess) return 0.0;
     const double ops = (double)blocks * threads * iters * 16.0;  // 8 IADD3 + 8 LOP3 per iteration
+    return ops / (best * 1e-3);
+}
+
+// Lane-ops/s of the mixed ALU + FMA integer probe (the issue ceiling K4's instruction mix is quoted
+// against next to the ALU-only figure above).
+extern "C" double tb_probe_int32_mixed_ops(int reps) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t* out = nullptr;
+    if (cudaMalloc(&out, 4) != cudaSuccess) return 0.0;
+    const int iters = 4096, blocks = sms * 8, threads = 256;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < reps + 1; ++r) {
+        cudaEventRecord(e0);
+        int32_mixed_probe_kernel<<<blocks, threads>>>(out, iters, 12345u + r, 0x9E3779B1u + r);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess) return 0.0;
+    const double ops = (double)blocks * threads * iters * 32.0;  // 8 IADD3 + 8 LOP3 + 16 IMAD per iteration
     return ops / (best * 1e-3);
 }

@@ -86,11 +86,15 @@ def test_nan_rejected(eng):
         eng.all_pairs(x, kernel="gemm").validate()
 
 
-def test_bad_ranks_rejected_merge(eng):
-    from paper_1704_03767_b200 import InvalidInputError
-    x = torch.tensor([[0, 1, 7], [0, 1, 2]], dtype=torch.int32, device="cuda")
-    with pytest.raises(InvalidInputError):
-        eng.all_pairs(x, kernel="merge").validate()
+def test_non_dense_values_merge(eng):
+    """The merge path ranks its input on the device (K0w), so any int32 / float values work -- as for the
+    reference's kernels, which compare values (kernel_sorted.py:30-57): same counts as dense ranks."""
+    x = torch.tensor([[0, 1, 7, 7, -3], [5, 1, 2, 2, 9]], dtype=torch.int32, device="cuda")
+    d = torch.tensor([[1, 2, 3, 3, 0], [3, 0, 1, 1, 4]], dtype=torch.int32, device="cuda")
+    a = eng.all_pairs(x, kernel="merge", full_counts=True).validate()
+    b = eng.all_pairs(d, kernel="merge", full_counts=True).validate()
+    for f in ("numerator", "n_d", "n3", "n1_rows", "tau_b"):
+        assert torch.equal(getattr(a, f), getattr(b, f)), f
 
 
 def test_kats_device(oracle):

@@ -1,5 +1,6 @@
-# Round 2: GPU test suite + smoke (new pipeline, K0w ranks, heavy-tie merge branch, config-2 every pair)
+# Round 2: GPU test suite + smoke + config-5 bench
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 2400 python -m pytest tests -m gpu -q -x --timeout 900 > gpurun_out/r2_pytest_gpu.log 2>&1; echo pytest=$?
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1; echo smoke=$?
+timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r2_bench_c5_v2.json 2> gpurun_out/r2_bench_c5_v2.err; echo bench=$?
