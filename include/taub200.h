@@ -90,14 +90,15 @@ int tb_rank_rows(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, ui
  * of dataio.py:194-196): dense 0-based int32 ranks, ties share a rank, -0.0 == +0.0, +-inf orderable.
  * The merge path's input stage (raw values -> tb_presort); one CTA per row, stable LSD radix sort.
  *   x         [m, ldx] values (TB_DTYPE_*), any n >= 1
- *   R         [m, ldr] int32 ranks out
+ *   R         [m, ldr] ranks out: int32, or uint16 when r_u16 != 0 (n <= 65536; the sign pack's input for
+ *             GEMM-path rows wider than tb_rank_rows takes; [n, ldr) zeroed)
  *   n1        [m] uint64 tied-pair count sum_t t(t-1)/2 per row (kernel_sorted.py:163-176)
  *   flags     device int32; bit 0 set when a NaN was seen (ranks.py:56-57)
  *   workspace device scratch of >= tb_rank_dense_workspace(m, n, dtype) bytes (for the current device)
  */
 int64_t tb_rank_dense_workspace(int64_t m, int64_t n, int dtype);
-int tb_rank_dense(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, int32_t *R, int64_t ldr, uint64_t *n1,
-                  int32_t *flags, void *workspace, int64_t ws_bytes, void *stream);
+int tb_rank_dense(const void *x, int dtype, int64_t m, int64_t n, int64_t ldx, void *R, int r_u16, int64_t ldr,
+                  uint64_t *n1, int32_t *flags, void *workspace, int64_t ws_bytes, void *stream);
 
 /*
  * K2 sign pack.  Replaces the per-pair sign enumeration of naive_numerator

@@ -38,7 +38,7 @@ SIGNATURES = {
     "tb_sign_k": ([_i64], _i64),
     "tb_rank_rows": ([_p, ctypes.c_int, _i64, _i64, _i64, _p, _i64, _p, _p, _p], ctypes.c_int),
     "tb_rank_dense_workspace": ([_i64, _i64, ctypes.c_int], _i64),
-    "tb_rank_dense": ([_p, ctypes.c_int, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _i64, _p], ctypes.c_int),
+    "tb_rank_dense": ([_p, ctypes.c_int, _i64, _i64, _i64, _p, ctypes.c_int, _i64, _p, _p, _p, _i64, _p], ctypes.c_int),
     "tb_sign_pack": ([_p, _i64, _i64, _i64, _p, _i64, ctypes.c_int, _p], ctypes.c_int),
     "tb_abs_pack": ([_p, _i64, _i64, ctypes.c_int, _p, _p], ctypes.c_int),
     "tb_gemm_pairs": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _p], ctypes.c_int),

@@ -520,9 +520,9 @@ __device__ __forceinline__ long long rw_exmax(long long v, long long* wsm) {
     return r;
 }
 
-template <typename T, typename K>
+template <typename T, typename K, typename RT>
 __global__ void __launch_bounds__(RW_THREADS, 1) rank_wide_kernel(const T* __restrict__ x, int64_t m, int64_t n,
-                                                                  int64_t ldx, int32_t* __restrict__ R, int64_t ldr,
+                                                                  int64_t ldx, RT* __restrict__ R, int64_t ldr,
                                                                   unsigned long long* __restrict__ n1,
                                                                   int32_t* __restrict__ flags, K* __restrict__ kws,
                                                                   uint32_t* __restrict__ iws) {
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(RW_THREADS, 1) rank_wide_kernel(const T* __res
         for (int64_t i = c0; i < c1; ++i) {
             if (i == 0 || ka[i] != ka[i - 1]) { ++rank; start = i; }
             ties += (unsigned long long)(i - start);
-            R[row * ldr + ia[i]] = (int32_t)rank;
+            R[row * ldr + ia[i]] = (RT)rank;
         }
         // block reduction of ties
 #pragma unroll
@@ -621,6 +621,8 @@ __global__ void __launch_bounds__(RW_THREADS, 1) rank_wide_kernel(const T* __res
             for (int ww = 0; ww < RW_WARPS; ++ww) t += (unsigned long long)wsm[ww];
             n1[row] = t;
         }
+        if (sizeof(RT) == 2)  // uint16 rows for the sign pack: zero the tail up to ldr (tb_rank_rows' contract)
+            for (int64_t i = n + tid; i < ldr; i += RW_THREADS) R[row * ldr + i] = 0;
         __syncthreads();
     }
     pdl_trigger();
@@ -636,10 +638,12 @@ extern "C" int64_t tb_rank_dense_workspace(int64_t m, int64_t n, int dtype) {
     return rank_wide_grid(m) * per + 256;
 }
 
-extern "C" int tb_rank_dense(const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, int32_t* R, int64_t ldr,
-                             uint64_t* n1, int32_t* flags, void* workspace, int64_t ws_bytes, void* stream) {
+extern "C" int tb_rank_dense(const void* x, int dtype, int64_t m, int64_t n, int64_t ldx, void* R, int r_u16,
+                             int64_t ldr, uint64_t* n1, int32_t* flags, void* workspace, int64_t ws_bytes,
+                             void* stream) {
     if (m < 1 || n < 1) return fail(TB_ERR_INVALID, "rank_dense: empty input");
     if (n > INT32_MAX) return fail(TB_ERR_CAPACITY, "rank_dense: n=%lld too large", (long long)n);
+    if (r_u16 && n > 65536) return fail(TB_ERR_CAPACITY, "rank_dense: uint16 ranks need n <= 65536");
     if (ldx < n || ldr < n) return fail(TB_ERR_CONFIG, "rank_dense: bad leading dimensions");
     if (!x || !R || !n1 || !flags || !workspace) return fail(TB_ERR_INVALID, "rank_dense: null pointer");
     if (dtype < TB_DTYPE_I32 || dtype > TB_DTYPE_F64) return fail(TB_ERR_INVALID, "rank_dense: unknown dtype %d", dtype);
@@ -654,19 +658,21 @@ extern "C" int tb_rank_dense(const void* x, int dtype, int64_t m, int64_t n, int
     uint32_t* iws = reinterpret_cast<uint32_t*>(ws + grid * 2 * n * kb);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto* n1u = reinterpret_cast<unsigned long long*>(n1);
-    switch (dtype) {
-        case TB_DTYPE_I32:
-            TB_CUDA_TRY(launch_pdl(rank_wide_kernel<int32_t, uint32_t>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
-                                   (const int32_t*)x, m, n, ldx, R, ldr, n1u, flags, reinterpret_cast<uint32_t*>(ws), iws));
-            break;
-        case TB_DTYPE_F32:
-            TB_CUDA_TRY(launch_pdl(rank_wide_kernel<float, uint32_t>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
-                                   (const float*)x, m, n, ldx, R, ldr, n1u, flags, reinterpret_cast<uint32_t*>(ws), iws));
-            break;
-        default:
-            TB_CUDA_TRY(launch_pdl(rank_wide_kernel<double, uint64_t>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
-                                   (const double*)x, m, n, ldx, R, ldr, n1u, flags, reinterpret_cast<uint64_t*>(ws), iws));
-            break;
-    }
+    auto go = [&](auto* rout) -> cudaError_t {
+        using RT = std::remove_pointer_t<decltype(rout)>;
+        switch (dtype) {
+            case TB_DTYPE_I32:
+                return launch_pdl(rank_wide_kernel<int32_t, uint32_t, RT>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
+                                  (const int32_t*)x, m, n, ldx, rout, ldr, n1u, flags, reinterpret_cast<uint32_t*>(ws), iws);
+            case TB_DTYPE_F32:
+                return launch_pdl(rank_wide_kernel<float, uint32_t, RT>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
+                                  (const float*)x, m, n, ldx, rout, ldr, n1u, flags, reinterpret_cast<uint32_t*>(ws), iws);
+            default:
+                return launch_pdl(rank_wide_kernel<double, uint64_t, RT>, dim3((unsigned)grid), dim3(RW_THREADS), 0, st,
+                                  (const double*)x, m, n, ldx, rout, ldr, n1u, flags, reinterpret_cast<uint64_t*>(ws), iws);
+        }
+    };
+    if (r_u16) TB_CUDA_TRY(go(static_cast<uint16_t*>(R)));
+    else TB_CUDA_TRY(go(static_cast<int32_t*>(R)));
     return check_launch("rank_wide_kernel");
 }

@@ -30,7 +30,9 @@ from .pairindex import job_coord
 # int8 ops per pair at tensor-core rate; the merge costs ~4 n log2 n INT32 ops
 # per pair at CUDA-core rate -- SURVEY 7 step 5.  Above this n the sign matrix
 # is also too large to materialise (m * n^2 / 2 bytes).
-GEMM_MAX_N = 8192  # also the device rank transform's row limit (tb_rank_rows)
+GEMM_MAX_N = 8192
+RANK_ROWS_MAX_N = 8192  # tb_rank_rows' row limit; wider GEMM-path rows are ranked by tb_rank_dense
+SIGN_MAX_N = 32767      # tb_sign_pack: 15-bit ranks
 PATHS = ("gemm", "merge")
 
 
@@ -341,8 +343,15 @@ class TauEngine:
         for r0, r1, wait in (row_chunks or [(0, m, None)]):
             if wait is not None:
                 wait()
-            _lib.call("tb_rank_rows", _ptr(x[r0:r1]), _dtype_code(x), r1 - r0, n, x.stride(0),
-                      _ptr(R[r0 * ldr:]), ldr, _ptr(res.n1_rows[r0:]), _ptr(res.flags), st)
+            if n <= RANK_ROWS_MAX_N:  # K0: shared-memory / register sorts
+                _lib.call("tb_rank_rows", _ptr(x[r0:r1]), _dtype_code(x), r1 - r0, n, x.stride(0),
+                          _ptr(R[r0 * ldr:]), ldr, _ptr(res.n1_rows[r0:]), _ptr(res.flags), st)
+            else:  # K0w: wide rows (uint16 ranks out)
+                code = _dtype_code(x)
+                wsb = int(_lib.load().tb_rank_dense_workspace(r1 - r0, n, code))
+                ws = self._buf("rank_ws", wsb, torch.uint8)
+                _lib.call("tb_rank_dense", _ptr(x[r0:r1]), code, r1 - r0, n, x.stride(0), _ptr(R[r0 * ldr:]), 1, ldr,
+                          _ptr(res.n1_rows[r0:]), _ptr(res.flags), _ptr(ws), wsb, st)
             p0 = max(r0, y_lo)
             if p0 < r1:
                 _lib.call("tb_sign_pack", _ptr(R[p0 * ldr:]), r1 - p0, n, ldr, _ptr(S[p0 * ldS:]), ldS, fmt, st)
@@ -539,7 +548,7 @@ class TauEngine:
         ranks = self._buf("R32", m * n, torch.int32)
         wsb = int(_lib.load().tb_rank_dense_workspace(m, n, code))
         ws = self._buf("rank_ws", wsb, torch.uint8)
-        _lib.call("tb_rank_dense", _ptr(x), code, m, n, x.stride(0), _ptr(ranks), n, _ptr(res.n1_rows),
+        _lib.call("tb_rank_dense", _ptr(x), code, m, n, x.stride(0), _ptr(ranks), 0, n, _ptr(res.n1_rows),
                   _ptr(res.flags), _ptr(ws), wsb, st)
         x = ranks
         pos = self._buf("pos", m * n, torch.int32)

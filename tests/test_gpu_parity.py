@@ -581,8 +581,8 @@ def test_rank_dense_vs_oracle(oracle, dtype):
         flags = torch.zeros(1, dtype=torch.int32, device="cuda")
         wsb = int(lib.tb_rank_dense_workspace(m, n, _dtype_code(xd)))
         ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-        _lib.call("tb_rank_dense", _ptr(xd), _dtype_code(xd), m, n, n, _ptr(R), n, _ptr(n1), _ptr(flags), _ptr(ws),
-                  wsb, _stream_ptr(None))
+        _lib.call("tb_rank_dense", _ptr(xd), _dtype_code(xd), m, n, n, _ptr(R), 0, n, _ptr(n1), _ptr(flags),
+                  _ptr(ws), wsb, _stream_ptr(None))
         torch.cuda.synchronize()
         got = R.view(m, n).cpu().numpy()
         for r in range(m):
