@@ -141,7 +141,9 @@ int tb_abs_pack(const int8_t *S, int64_t m, int64_t ldS, int format, int8_t *A, 
 
 /* Full counts on the GEMM path from num = S_y.S_x and absdot = |S_y|.|S_x|:
  * n_d = (absdot - num) / 2 and n3 = absdot - n0 + n1_y + n1_x (the CELL_DTYPE
- * fields of src/taucorr/engine.py:45-55).  nd / n3 may be NULL. */
+ * fields of src/taucorr/engine.py:45-55).  nd / n3 may be NULL.  absdot may be NULL when no variable of
+ * the range has ties (every n1 = 0): then |S_y|.|S_x| = n0 - n1_y - n1_x exactly (n3 = 0) and the
+ * second GEMM is skipped. */
 int tb_full_counts(const int32_t *num, const int32_t *absdot, const uint64_t *n1_rows, int64_t m, int64_t n,
                    int64_t job_lo, int64_t job_hi, uint64_t *nd, uint64_t *n3, void *stream);
 

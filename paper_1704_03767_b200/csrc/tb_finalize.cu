@@ -110,13 +110,14 @@ __global__ void __launch_bounds__(256) full_counts_kernel(const int32_t* __restr
     pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = num[i], a = absdot[i];  // a = n_c + n_d, s = n_c - n_d
+        int64_t y, x;
+        job_coord(job_lo + i, m, y, x);
+        const int64_t t1 = (int64_t)n1[y], t2 = (int64_t)n1[x];
+        // a = n_c + n_d = |S_y|.|S_x| = n0 - n1 - n2 + n3; without the |S| GEMM (absdot NULL: no row has
+        // ties) n3 = 0 and a = n0 - n1 - n2
+        const int64_t s = num[i], a = absdot ? (int64_t)absdot[i] : n0 - t1 - t2;  // s = n_c - n_d
         if (nd) nd[i] = (unsigned long long)((a - s) / 2);
-        if (n3) {
-            int64_t y, x;
-            job_coord(job_lo + i, m, y, x);
-            n3[i] = (unsigned long long)(a - n0 + (int64_t)n1[y] + (int64_t)n1[x]);
-        }
+        if (n3) n3[i] = (unsigned long long)(a - n0 + t1 + t2);
     }
     pdl_trigger();
 }
@@ -187,7 +188,7 @@ extern "C" int tb_full_counts(const int32_t* num, const int32_t* absdot, const u
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "full_counts: need m >= 1, n >= 2");
     const int64_t total = m * (m + 1) / 2;
     if (job_lo < 0 || job_hi < job_lo || job_hi > total) return fail(TB_ERR_CONFIG, "full_counts: bad job range");
-    if (!num || !absdot || !n1_rows) return fail(TB_ERR_INVALID, "full_counts: null pointer");
+    if (!num || !n1_rows) return fail(TB_ERR_INVALID, "full_counts: null pointer");
     const int64_t count = job_hi - job_lo;
     if (count == 0) return TB_OK;
     int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 16);

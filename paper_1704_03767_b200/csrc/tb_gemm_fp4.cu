@@ -57,7 +57,37 @@ struct Gemm4Args {
     int32_t* num;
     float* acc;      // split-K: f32 sums (exact integers < 2^24), red.global.add.v4.f32
     unsigned long long* trace;  // TB_TRACE=1 (diagnostics): per CTA, per item: [accumulator ready, epilogue done]
+    // K-lockstep throttle: prog[pair] = epoch << 32 | k-blocks this pair has issued (0xFFFFFFFF: done);
+    // a pair more than `lead` k-blocks ahead of the slowest running pair waits (see the producer)
+    unsigned long long* prog;
+    uint32_t epoch;
+    int32_t lead;
 };
+
+// ---- K-lockstep throttle.  The ~74 concurrently running CTA pairs stream the same S rows (units of one
+// row group share A, units of one column window share B) at the same k-block only if they stay in step:
+// an L2 line lives ~20 us at config-5 fill rates, so pairs that drift more than ~100 k-blocks apart
+// re-read S from DRAM (ncu: ~13x the operand bytes per band).  Every LOCK_CHK k-blocks the leader CTA's
+// producer publishes its progress and waits while it is more than `lead` k-blocks ahead of the slowest
+// pair still running.  Entries of another launch (epoch) count as finished, so a pair never waits on a
+// pair that has not published in this launch: the slowest running pair never waits, no deadlock.
+constexpr int LOCK_CHK = 16;
+#ifndef GEMM_LOCK_LEAD
+#define GEMM_LOCK_LEAD 0  // default allowed lead (k-blocks); 0 = throttle off
+#endif
+__device__ __forceinline__ void prog_publish(unsigned long long* prog, int64_t pair, uint32_t epoch, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(prog + pair), "l"(((unsigned long long)epoch << 32) | v)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t prog_min(const unsigned long long* prog, int64_t npairs, uint32_t epoch) {
+    uint32_t mn = 0xFFFFFFFFu;
+    for (int64_t q = 0; q < npairs; ++q) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(prog + q) : "memory");
+        if ((uint32_t)(v >> 32) == epoch) mn = min(mn, (uint32_t)v);
+    }
+    return mn;
+}
 
 struct Unit4 {
     int64_t y0;
@@ -154,11 +184,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             uint32_t phase = 0;
             int64_t cur = pair;
             Unit4 t;
+            const bool lock = p.lead > 0 && leader;
+            uint32_t done = 0;
+            if (lock) prog_publish(p.prog, pair, p.epoch, 0);
             while (next_unit4(p, cur, npairs, t)) {
                 // each block loads a full 120-row box per CTA; the 2-SM MMA with N reads N / 2 rows of
                 // each CTA, so CTA 1's box starts at N / 2 (partial blocks need no other tensor map)
                 const uint32_t bytes = 2 * (A_BYTES + t.nblk * B_BYTES);
-                for (int32_t kb = t.kb0; kb < t.kb1; ++kb) {
+                for (int32_t kb = t.kb0; kb < t.kb1; ++kb, ++done) {
+                    if (lock && (done % LOCK_CHK) == 0) {
+                        prog_publish(p.prog, pair, p.epoch, done);
+                        while (done > prog_min(p.prog, npairs, p.epoch) + (uint32_t)p.lead) __nanosleep(200);
+                    }
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
@@ -170,6 +207,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
+            if (lock) prog_publish(p.prog, pair, p.epoch, 0xFFFFFFFFu);
         }
     } else if (warp == 1) {
         if (leader) {  // ---------------- MMA issuer (leader CTA, warp 1; one elected lane issues)
@@ -490,6 +528,35 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
     return TB_OK;
 }
 
+// Per-device progress slots of the K-lockstep throttle (zeroed once; launches tell their entries apart by
+// epoch).  TB_GEMM_LEAD = the allowed lead in k-blocks (0 disables the throttle).
+static int lockstep_state(unsigned long long** prog, uint32_t* epoch, int32_t* lead) {
+    static const int32_t kLead = [] {
+        const char* e = std::getenv("TB_GEMM_LEAD");
+        return e ? std::max(0, atoi(e)) : GEMM_LOCK_LEAD;
+    }();
+    struct Slot { unsigned long long* p = nullptr; uint32_t epoch = 0; };
+    static Slot slots[64];
+    *lead = kLead;
+    *prog = nullptr;
+    *epoch = 0;
+    if (kLead <= 0) return TB_OK;
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);
+    int dev = 0;
+    TB_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) { *lead = 0; return TB_OK; }
+    Slot& sl = slots[dev];
+    if (!sl.p) {
+        TB_CUDA_TRY(cudaMalloc(&sl.p, 1024 * sizeof(unsigned long long)));
+        TB_CUDA_TRY(cudaMemset(sl.p, 0, 1024 * sizeof(unsigned long long)));
+        TB_CUDA_TRY(cudaDeviceSynchronize());
+    }
+    if (++sl.epoch == 0) sl.epoch = 1;
+    *prog = sl.p;
+    *epoch = sl.epoch;
+    return TB_OK;
+}
+
 int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi, int32_t splits,
              int32_t* num, cudaStream_t st) {
     if (K >= (int64_t(1) << 24)) return fail(TB_ERR_CAPACITY, "gemm fp4: K=%lld needs exact f32 sums (< 2^24)", (long long)K);
@@ -509,6 +576,7 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.job_hi = job_hi;
     p.num = num;
     if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
+    if ((rc = lockstep_state(&p.prog, &p.epoch, &p.lead))) return rc;
     CUtensorMap ta, tbm;
     if ((rc = make_tmap(&ta, S, m, kbytes, ldS, g4::BM))) return rc;
     if ((rc = make_tmap(&tbm, S, m, kbytes, ldS, g4::BNH))) return rc;

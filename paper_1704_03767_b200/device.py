@@ -109,6 +109,8 @@ class Prepared:
     K: int = 0
     ldS: int = 0
     fmt: int = 0
+    row_lo: int = 0
+    any_ties: bool | None = None      # GEMM full counts: does any row >= row_lo have ties (read lazily)
     keys: torch.Tensor | None = None  # merge: K1 presort outputs
     pos: torch.Tensor | None = None
     srt: torch.Tensor | None = None
@@ -190,6 +192,7 @@ class TauEngine:
             self._events[which].record(self._stream)
 
     sign_format_override: int | None = None  # tests / experiments: force TB_SIGN_*
+    force_abs_gemm: bool = False  # tests: run the |S| GEMM even when no variable has ties
 
     def sign_format(self, K: int) -> int:
         """e2m1 (kind::mxf4) while the f32 sums stay exact (K < 2^24), else int8 (kind::i8)."""
@@ -278,13 +281,9 @@ class TauEngine:
                         flags=torch.zeros(1, dtype=torch.int32, device=self.device))
         stub = PairResult(m=m, n=n, job_lo=row_prefix(min(row_lo, m), m), job_hi=m * (m + 1) // 2, path=path,
                           numerator=None, n1_rows=prep.n1_rows, flags=prep.flags)
+        prep.row_lo = min(row_lo, m)
         if path == "gemm":
             prep.S, prep.K, prep.ldS, prep.fmt = self._gemm_prepare(x, stub, st, simt)
-            if full_counts:
-                prep.A = self._buf("A", m * prep.ldS, torch.int8)
-                y0 = min(row_lo, m)
-                _lib.call("tb_abs_pack", _ptr(prep.S[y0 * prep.ldS:]), m - y0, prep.ldS, prep.fmt,
-                          _ptr(prep.A[y0 * prep.ldS:]), st)
         else:
             prep.pos, prep.srt, prep.keys, (prep.maxgrp, prep.groups, prep.ngroups) = \
                 self._merge_prepare(x.contiguous(), stub, st)
@@ -311,12 +310,24 @@ class TauEngine:
         if _mark_after_num:
             self._mark(1)
         if nd is not None or n3 is not None:
-            if prep.A is None:
+            if not prep.full:
                 raise ConfigError("n_d / n3 on the GEMM path need prepare(..., full_counts=True)")
-            absdot = self._buf("absdot", hi - lo, torch.int32)
-            for a, b in self._gemm_ranges(m, lo, hi):
-                self._gemm_numerator(prep.A, absdot[a - lo:b - lo], m, prep.K, prep.ldS, prep.fmt, a, b, st,
-                                     splits, prep.simt)
+            if prep.any_ties is None:
+                # one flag read per prepare (a host sync): with no tied variable among the rows the range
+                # touches, |S_y|.|S_x| = n0 - n1_y - n1_x and the |S| GEMM (as long as the numerator GEMM)
+                # is skipped -- config 5 (continuous data) takes this branch
+                prep.any_ties = bool((prep.n1_rows[prep.row_lo:] > 0).any().item())
+            absdot = None
+            if prep.any_ties or self.force_abs_gemm:
+                if prep.A is None:
+                    y0 = prep.row_lo
+                    prep.A = self._buf("A", m * prep.ldS, torch.int8)
+                    _lib.call("tb_abs_pack", _ptr(prep.S[y0 * prep.ldS:]), m - y0, prep.ldS, prep.fmt,
+                              _ptr(prep.A[y0 * prep.ldS:]), st)
+                absdot = self._buf("absdot", hi - lo, torch.int32)
+                for a, b in self._gemm_ranges(m, lo, hi):
+                    self._gemm_numerator(prep.A, absdot[a - lo:b - lo], m, prep.K, prep.ldS, prep.fmt, a, b, st,
+                                         splits, prep.simt)
             _lib.call("tb_full_counts", _ptr(num), _ptr(absdot), _ptr(prep.n1_rows), m, n, lo, hi, _ptr(nd),
                       _ptr(n3), st)
 

@@ -624,3 +624,24 @@ def test_merge_heavy_ties_vs_oracle(eng, oracle, n, levels):
     assert dt < 2.0, f"{m * (m + 1) // 2} pairs took {dt:.2f} s"
     ranks = oracle.rank_matrix(x)
     _check_full(res, oracle, ranks)
+
+
+def test_full_counts_tie_free_shortcut(eng, oracle):
+    """With no tied variable, n_d / n3 come from the closed form |S_y|.|S_x| = n0 - n1_y - n1_x (no |S|
+    GEMM); identical to the |S| GEMM path and to the oracle; one tied row switches the GEMM back on."""
+    rng = np.random.default_rng(31)
+    x = rng.standard_normal((300, 700)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    a = eng.all_pairs(xd, kernel="gemm", full_counts=True).validate()
+    try:
+        eng.force_abs_gemm = True
+        b = eng.all_pairs(xd, kernel="gemm", full_counts=True).validate()
+    finally:
+        eng.force_abs_gemm = False
+    assert int(a.n1_rows.max()) == 0
+    for f in ("numerator", "n_d", "n3"):
+        assert torch.equal(getattr(a, f), getattr(b, f)), f
+    _check_full(a, oracle, oracle.rank_matrix(x))
+    x[7, :50] = 1.0  # ties in one row
+    c = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="gemm", full_counts=True).validate()
+    _check_full(c, oracle, oracle.rank_matrix(x))
