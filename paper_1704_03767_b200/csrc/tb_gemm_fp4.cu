@@ -62,6 +62,7 @@ struct Gemm4Args {
     unsigned long long* prog;
     uint32_t epoch;
     int32_t lead;
+    int32_t lagq;  // pairs allowed to lag more than `lead` behind before a pair waits
 };
 
 // ---- K-lockstep throttle.  The ~74 concurrently running CTA pairs stream the same S rows (units of one
@@ -79,14 +80,16 @@ __device__ __forceinline__ void prog_publish(unsigned long long* prog, int64_t p
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(prog + pair), "l"(((unsigned long long)epoch << 32) | v)
                  : "memory");
 }
-__device__ __forceinline__ uint32_t prog_min(const unsigned long long* prog, int64_t npairs, uint32_t epoch) {
-    uint32_t mn = 0xFFFFFFFFu;
+// number of running pairs of this launch more than `lead` k-blocks behind `done`
+__device__ __forceinline__ int prog_behind(const unsigned long long* prog, int64_t npairs, uint32_t epoch,
+                                           uint32_t done, uint32_t lead) {
+    int c = 0;
     for (int64_t q = 0; q < npairs; ++q) {
         unsigned long long v;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(prog + q) : "memory");
-        if ((uint32_t)(v >> 32) == epoch) mn = min(mn, (uint32_t)v);
+        if ((uint32_t)(v >> 32) == epoch && (uint64_t)(uint32_t)v + lead < done) ++c;
     }
-    return mn;
+    return c;
 }
 
 struct Unit4 {
@@ -194,7 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                 for (int32_t kb = t.kb0; kb < t.kb1; ++kb, ++done) {
                     if (lock && (done % LOCK_CHK) == 0) {
                         prog_publish(p.prog, pair, p.epoch, done);
-                        while (done > prog_min(p.prog, npairs, p.epoch) + (uint32_t)p.lead) __nanosleep(200);
+                        while (prog_behind(p.prog, npairs, p.epoch, done, (uint32_t)p.lead) > p.lagq) __nanosleep(200);
                     }
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
@@ -382,12 +385,14 @@ static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<i
     // the first one touching its diagonal, b = floor(256 yb / 240), to the last column of the matrix,
     // and are paired left to right (an odd count leaves one single-block unit), so diagonal and
     // right-edge remnants share units instead of each becoming a half-empty one.  Units are listed
-    // per 8-row-block group (2048 rows) in windows of 8 column blocks, so concurrently running pairs
-    // share S rows through L2.
+    // per 16-row-block group (4096 rows) in windows of 4 column blocks, so the ~74 concurrently running
+    // pairs cover a squarer patch (~16 row blocks x ~9 column blocks) and share S rows through L2
+    // (config 5, r02: 8 x 8 -> 16 x 4 cut the GEMM from 389-397 to 375-382 ms and DRAM reads per band
+    // from 251 to 232 GB, profiles/r02_gemm_unit_order.log).
     // unit-order knobs (experiments; TB_GEMM_GR row blocks per group, TB_GEMM_WIN column blocks per window,
     // TB_GEMM_SERP=1 reverses the window order of every other group)
-    static const int64_t kGR = [] { const char* e = std::getenv("TB_GEMM_GR"); return e ? std::max(1, atoi(e)) : 8; }();
-    static const int64_t kWIN = [] { const char* e = std::getenv("TB_GEMM_WIN"); return e ? std::max(1, atoi(e)) : 8; }();
+    static const int64_t kGR = [] { const char* e = std::getenv("TB_GEMM_GR"); return e ? std::max(1, atoi(e)) : 16; }();
+    static const int64_t kWIN = [] { const char* e = std::getenv("TB_GEMM_WIN"); return e ? std::max(1, atoi(e)) : 4; }();
     static const bool kSERP = [] { const char* e = std::getenv("TB_GEMM_SERP"); return e && e[0] == '1'; }();
     const int64_t RB = (m + g4::UM - 1) / g4::UM, GR = kGR;
     const int64_t b_last = (m - 1) / g4::BN;
@@ -577,6 +582,10 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.num = num;
     if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
     if ((rc = lockstep_state(&p.prog, &p.epoch, &p.lead))) return rc;
+    {
+        static const int32_t kLagQ = [] { const char* e = std::getenv("TB_GEMM_LAGQ"); return e ? std::max(0, atoi(e)) : 0; }();
+        p.lagq = kLagQ;
+    }
     CUtensorMap ta, tbm;
     if ((rc = make_tmap(&ta, S, m, kbytes, ldS, g4::BM))) return rc;
     if ((rc = make_tmap(&tbm, S, m, kbytes, ldS, g4::BNH))) return rc;
