@@ -60,7 +60,10 @@ def parse():
     ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
                     help="strong (default): one workload sharded over the ranks, bands gathered to rank 0; "
                          "weak: every rank computes its own copy, no collective")
-    ap.add_argument("--bands", type=int, default=8, help="row bands per rank (one numerator launch each)")
+    ap.add_argument("--bands", type=int, default=0,
+                    help="row bands per rank, each gathered to rank 0 as it finishes (0: automatic -- one band "
+                         "per 2^27 job ids of the shard, at most 8, one band at N = 1; the engine still splits "
+                         "a >= 2^30-id numerator launch into 8 row-band GEMMs)")
     ap.add_argument("--e2e-steps", type=int, default=2, help="timed compute_all_pairs plugin calls")
     ap.add_argument("--e2e-tau-steps", type=int, default=10, help="timed all_pairs_host calls")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
@@ -353,7 +356,7 @@ def run_ours(args):
     total_jobs = m * (m + 1) // 2
     eng = get_engine(local)  # the engine compute_all_pairs uses too: one set of workspaces
     stream = torch.cuda.Stream(device=dev)
-    path = eng.choose_path(n)
+    path = eng.choose_path(n, m=m)
     strong = args.scaling == "strong"
     # strong scaling: rank r owns a contiguous job-id shard of equal modelled cost (multi.balanced_job_shards,
     # the reference's contiguous shard rule, pairindex.py:68-80); its bands stream to rank 0 (BandGather,
@@ -361,6 +364,8 @@ def run_ours(args):
     shards = balanced_job_shards(world, m, path) if strong else [(0, total_jobs)] * world
     job_range = shards[rank]
     nbands = args.bands
+    if nbands <= 0:  # bands exist to overlap the gather; small launches cost GEMM efficiency
+        nbands = 1 if world == 1 or not strong else int(min(8, max(1, (job_range[1] - job_range[0]) >> 27)))
     bands = shard_bands(*job_range, m, nbands)
     xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # raw values: both paths rank on the device
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
@@ -520,7 +525,7 @@ def run_ours(args):
             with open(tpath) as fh:
                 tj = json.load(fh)
             traffic = tj.get(f"config{args.config}", {}).get("dram_bytes_per_launch")
-        per_step_units = len(bands)
+        per_step_units = sum(len(eng._gemm_ranges(m, lo, hi)) for lo, hi in bands) if path == "gemm" else len(bands)
         if path == "gemm":
             fp4 = sign_format == _lib.TB_SIGN_E2M1
             fp4_lib = measure_fp4_peak(torch, dev) if fp4 else None

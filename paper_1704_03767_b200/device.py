@@ -26,11 +26,27 @@ from . import _lib
 from .errors import CapacityExceededError, ConfigError, InvalidInputError
 from .pairindex import job_coord
 
-# Dispatcher crossover (numerator kernel per shape).  The GEMM costs 2K = n(n-1)
-# int8 ops per pair at tensor-core rate; the merge costs ~4 n log2 n INT32 ops
-# per pair at CUDA-core rate -- SURVEY 7 step 5.  Above this n the sign matrix
-# is also too large to materialise (m * n^2 / 2 bytes).
-GEMM_MAX_N = 8192
+# Dispatcher (north star (3): the numerator kernel per shape from measured throughput; the reference's
+# analogue is the capacity-driven kernel switch, engine.py:338-346).  Per-unit costs measured on B200 by
+# tools/exp_dispatch.py (profiles/r02_dispatch_table.jsonl): for n, the GEMM path's sign-pack seconds per
+# row (K0/K0w + K2) and GEMM seconds per job id (K3: e2m1 kind::mxf4 up to n = 5792, int8 above; measured
+# at the largest m whose S fits, given as m_gemm), and the merge path's K0w + K1 seconds per row and K4
+# seconds per job id.  A shape (m, n) takes the path with the smaller m * per_row + J * per_job
+# (J = m(m+1)/2 job ids), the GEMM only while its sign matrix fits the free device memory.
+DISPATCH_TABLE = (
+    # n, gemm pack s/row, gemm s/job, m_gemm, merge prep s/row, merge s/job
+    (1024, 1.123e-07, 1.982e-10, 2048, 3.258e-07, 9.437e-08),
+    (2048, 3.748e-07, 9.585e-10, 2048, 3.764e-07, 8.978e-08),
+    (4096, 1.109e-06, 7.797e-09, 2048, 5.035e-07, 1.046e-07),
+    (5792, 2.324e-06, 1.560e-08, 2048, 6.497e-07, 1.372e-07),
+    (6144, 3.731e-06, 3.162e-08, 2048, 6.782e-07, 1.371e-07),
+    (8192, 5.975e-06, 5.664e-08, 1990, 8.467e-07, 1.388e-07),
+    (12288, 1.171e-05, 1.698e-07, 884, 1.131e-06, 1.936e-07),
+    (16384, 2.130e-05, 3.663e-07, 497, 1.640e-06, 1.989e-07),
+    (24576, 4.665e-05, 1.105e-06, 221, 2.675e-06, 2.904e-07),
+    (32767, 8.727e-05, 4.589e-06, 124, 4.203e-06, 3.008e-07),
+)
+GEMM_MAX_N = 8192  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides)
 RANK_ROWS_MAX_N = 8192  # tb_rank_rows' row limit; wider GEMM-path rows are ranked by tb_rank_dense
 SIGN_MAX_N = 32767      # tb_sign_pack: 15-bit ranks
 PATHS = ("gemm", "merge")
@@ -201,8 +217,32 @@ class TauEngine:
         return _lib.TB_SIGN_E2M1 if K < (1 << 24) else _lib.TB_SIGN_I8
 
     @staticmethod
-    def choose_path(n: int) -> str:
-        return "gemm" if n <= GEMM_MAX_N else "merge"
+    def path_costs(m: int, n: int) -> dict:
+        """Modelled seconds of each device path for an m x n all-pairs job (DISPATCH_TABLE, log-log
+        interpolation in n; below the table the GEMM scales with K ~ n^2, the merge with n log n)."""
+        tab = DISPATCH_TABLE
+        ns = [r[0] for r in tab]
+        J = m * (m + 1) / 2
+
+        def interp(col: int) -> float:
+            if n <= ns[0]:
+                v = tab[0][col]
+                return v * ((n / ns[0]) ** 2 if col in (1, 2) else (n * math.log2(max(n, 2))) / (ns[0] * 10.0))
+            if n >= ns[-1]:
+                return tab[-1][col] * (n / ns[-1]) ** (2 if col in (1, 2) else 1)
+            for a, b in zip(tab, tab[1:]):
+                if a[0] <= n <= b[0]:
+                    f = math.log(n / a[0]) / math.log(b[0] / a[0])
+                    return math.exp(math.log(a[col]) * (1 - f) + math.log(b[col]) * f)
+            raise AssertionError
+        out = {"merge": m * interp(4) + J * interp(5)}
+        if n <= SIGN_MAX_N:
+            out["gemm"] = m * interp(1) + J * interp(2)
+        return out
+
+    def choose_path(self, n: int, m: int | None = None, full_counts: bool = False) -> str:
+        """The numerator path for an (m x n) job on this device (module-level choose_path)."""
+        return choose_path(n, m=m, full_counts=full_counts, eng=self)
 
     # -------------------------------------------------------------- the hot path
     def all_pairs(self, x: torch.Tensor, kernel: str = "auto", job_range: tuple[int, int] | None = None,
@@ -228,7 +268,7 @@ class TauEngine:
         job_lo, job_hi = (0, total) if job_range is None else (int(job_range[0]), int(job_range[1]))
         if not 0 <= job_lo <= job_hi <= total:
             raise ConfigError(f"job range [{job_lo}, {job_hi}) outside [0, {total})")
-        path = self.choose_path(n) if kernel == "auto" else kernel
+        path = self.choose_path(n, m=m, full_counts=full_counts) if kernel == "auto" else kernel
         if path not in PATHS:
             raise ConfigError(f"unknown device path {kernel!r}, expected one of {PATHS + ('auto',)}")
         if x.device != self.device:
@@ -405,7 +445,7 @@ class TauEngine:
         it while band b+1 computes).  Asynchronous on ``stream``; ``timing`` collects (start, end) CUDA
         events around each band's numerator kernels (bench instrumentation)."""
         m, n = x.shape
-        path = self.choose_path(n) if kernel == "auto" else kernel
+        path = self.choose_path(n, m=m) if kernel == "auto" else kernel
         if not bands:
             return None
         base = bands[0][0]
@@ -476,7 +516,7 @@ class TauEngine:
             raise ConfigError(f"job range [{jlo}, {jhi}) outside [0, {total})")
         if tau_b_out.numel() < jhi - jlo:
             raise ConfigError(f"tau_b_out holds {tau_b_out.numel()} values, need {jhi - jlo}")
-        path = self.choose_path(n) if kernel == "auto" else kernel
+        path = self.choose_path(n, m=m) if kernel == "auto" else kernel
         with self._session(stream) as st_t:
             cp_t = copy_stream if copy_stream is not None else self._copy_stream()
             st = _stream_ptr(st_t)
@@ -571,6 +611,24 @@ class TauEngine:
         _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(keys), _ptr(res.n1_rows),
                   _ptr(maxgrp), _ptr(work), _ptr(ngroups), _ptr(res.flags), st)
         return pos, srt, keys, (maxgrp, work, ngroups)
+
+
+def choose_path(n: int, m: int | None = None, full_counts: bool = False, eng: "TauEngine | None" = None) -> str:
+    """The numerator path for an (m x n) job: the cheaper of the measured cost models (TauEngine.path_costs),
+    the GEMM only while its sign matrix (and |S| for full counts) fits 80% of the device's free memory.
+    Without m or a device, the large-m crossover GEMM_MAX_N decides."""
+    if m is None or eng is None:
+        return "gemm" if n <= GEMM_MAX_N else "merge"
+    costs = TauEngine.path_costs(m, n)
+    if "gemm" not in costs:
+        return "merge"
+    K, fmt, ldS, _ = eng._gemm_layout(n)
+    need = m * ldS * (2 if full_counts else 1)
+    have = eng._ws["S"].numel() if "S" in eng._ws else 0  # a cached S workspace is reusable
+    free = torch.cuda.mem_get_info(eng.device)[0] + have
+    if need > 0.8 * free:
+        return "merge"
+    return "gemm" if costs["gemm"] <= costs["merge"] else "merge"
 
 
 _ENGINES: dict[int, TauEngine] = {}

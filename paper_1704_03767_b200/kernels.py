@@ -32,7 +32,7 @@ def _device_counts(ua: np.ndarray, va: np.ndarray, full: bool):
     from .device import get_engine
 
     eng = get_engine()
-    path = eng.choose_path(ua.shape[0])
+    path = eng.choose_path(ua.shape[0], m=2, full_counts=full)
     x = torch.from_numpy(np.stack([ua, va])).to(eng.device)  # the device ranks them (K0 / K0w)
     res = eng.all_pairs(x, kernel=path, job_range=(1, 2),
                         tau_a=False, tau_b=False, full_counts=full)

@@ -630,7 +630,7 @@ def test_full_counts_tie_free_shortcut(eng, oracle):
     """With no tied variable, n_d / n3 come from the closed form |S_y|.|S_x| = n0 - n1_y - n1_x (no |S|
     GEMM); identical to the |S| GEMM path and to the oracle; one tied row switches the GEMM back on."""
     rng = np.random.default_rng(31)
-    x = rng.standard_normal((300, 700)).astype(np.float32)
+    x = np.stack([rng.permutation(700) for _ in range(300)]).astype(np.float32) * 0.25 - 40.0  # no ties
     xd = torch.from_numpy(x).cuda()
     a = eng.all_pairs(xd, kernel="gemm", full_counts=True).validate()
     try:

@@ -240,3 +240,31 @@ def test_closed_form_cell_counts_and_pass_spans():
     space = tb.JobSpace(65536, 8)
     plans = tb.plan_passes(space, (0, space.total_tiles), 4096)
     assert sum(p.cells for p in plans) == 65536 * 65537 // 2
+
+
+def test_dispatcher_cost_model(monkeypatch):
+    """The measured cost model picks the GEMM for the BASELINE GEMM configs and the merge for config 4
+    and for large n with few rows; the GEMM is refused when S does not fit the free memory."""
+    import types
+
+    import torch
+
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.device import DISPATCH_TABLE, TauEngine, choose_path
+
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libtaub200.so not built")
+    eng = types.SimpleNamespace(_ws={}, device=None, sign_format_override=None)
+    eng.sign_format = lambda K: TauEngine.sign_format(eng, K)
+    eng._gemm_layout = lambda n: TauEngine._gemm_layout(eng, n)
+    monkeypatch.setattr(torch.cuda, "mem_get_info", lambda dev=None: (170 << 30, 180 << 30))
+    for (m, n), want in {(256, 200): "gemm", (2048, 1000): "gemm", (16384, 500): "gemm", (65536, 1024): "gemm",
+                         (1024, 65536): "merge", (128, 32767): "merge", (4, 9000): "merge",
+                         (2000, 8192): "gemm"}.items():
+        assert choose_path(n, m=m, eng=eng) == want, (m, n)
+    assert choose_path(1000) == "gemm" and choose_path(9000) == "merge"  # no shape: the large-m crossover
+    monkeypatch.setattr(torch.cuda, "mem_get_info", lambda dev=None: (1 << 30, 180 << 30))
+    assert choose_path(1024, m=65536, eng=eng) == "merge"  # S = 17 GB does not fit 1 GiB
+    for n, *_ in DISPATCH_TABLE:  # the model is finite and increasing in m
+        c1, c2 = TauEngine.path_costs(100, n), TauEngine.path_costs(1000, n)
+        assert all(0 < c1[k] < c2[k] for k in c1)

@@ -14,7 +14,7 @@ print(f"config {cfg}: host ranks {time.perf_counter() - t0:.1f} s", flush=True)
 got = [0]
 def sink(r):
     got[0] += r.shape[0]
-for slot_mb, slots, overlap in [(64, 3, True), (64, 3, False), (256, 3, True), (16, 6, True), (12, 3, True)]:
+for slot_mb, slots, overlap in [(256, 3, True), (512, 3, True), (256, 4, True), (128, 6, True)]:
     engine.SLOT_BYTES, engine.PASS_SLOTS = slot_mb << 20, slots
     tb.compute_all_pairs(ds, "vectorized", sink=sink, overlap=overlap)
     ts = []
