@@ -9,6 +9,7 @@
 // sqrt((n0 - n1_y) * (n0 - n1_x)) with IEEE round-to-nearest __ddiv_rn /
 // __dsqrt_rn / __dmul_rn (no FMA contraction), exactly the operation sequence
 // numpy executes in derive_taus.
+#include <cstdlib>
 #include <mutex>
 
 #include "tb_common.cuh"
@@ -37,7 +38,8 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32
                                                                       const unsigned long long* __restrict__ n1,
                                                                       int64_t m, int64_t n0, int64_t job_lo,
                                                                       int64_t count, double* __restrict__ tau_a,
-                                                                      double* __restrict__ tau_b, int64_t chunk) {
+                                                                      double* __restrict__ tau_b, int64_t chunk,
+                                                                      const double* __restrict__ T) {
     pdl_wait();
     const double dn0 = (double)n0;
     int64_t i = (int64_t)blockIdx.x * chunk + threadIdx.x;
@@ -47,29 +49,89 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32
     job_coord(job_lo + i, m, y, x);
     for (; i < i_end; i += FIN_UNROLL * FIN_THREADS) {
         // FIN_UNROLL cells 256 ids apart: loads and row/column tie counts first, then the IEEE sequences
-        double v[FIN_UNROLL], t[FIN_UNROLL];
+        int32_t v[FIN_UNROLL];
+        unsigned long long t1[FIN_UNROLL], t2[FIN_UNROLL];
         bool ok[FIN_UNROLL];
 #pragma unroll
         for (int u = 0; u < FIN_UNROLL; ++u) {
             const int64_t iu = i + (int64_t)u * FIN_THREADS;
             ok[u] = iu < i_end;
             if (u > 0 && ok[u]) fin_step(m, y, x);  // only walk to cells that exist (no row past m - 1)
-            v[u] = ok[u] ? (double)num[iu] : 0.0;
-            t[u] = ok[u] ? __dmul_rn(dn0 - (double)__ldg(&n1[y]), dn0 - (double)__ldg(&n1[x])) : 1.0;
+            v[u] = ok[u] ? num[iu] : 0;
+            t1[u] = ok[u] ? __ldg(&n1[y]) : 0ull;
+            t2[u] = ok[u] ? __ldg(&n1[x]) : 0ull;
         }
         if (i + FIN_UNROLL * FIN_THREADS < i_end) fin_step(m, y, x);
 #pragma unroll
         for (int u = 0; u < FIN_UNROLL; ++u) {
             if (!ok[u]) continue;
             const int64_t iu = i + (int64_t)u * FIN_THREADS;
-            if (tau_a) tau_a[iu] = __ddiv_rn(v[u], dn0);
+            const double dv = (double)v[u];
+            // tau_a = num / n0 depends on num alone: the table (when present) holds every quotient
+            const double ta = T ? __ldg(&T[v[u] + n0]) : __ddiv_rn(dv, dn0);
+            if (tau_a) tau_a[iu] = ta;
             if (tau_b) {
-                const double denom = __dsqrt_rn(t[u]);
-                tau_b[iu] = denom > 0.0 ? __ddiv_rn(v[u], denom) : __longlong_as_double(0x7ff8000000000000LL);
+                double tb;
+                if (T && (t1[u] | t2[u]) == 0) {
+                    tb = ta;  // no ties: sqrt(n0 * n0) = n0 exactly (n0^2 < 2^53), so tau_b = num / n0
+                } else {
+                    const double denom = __dsqrt_rn(__dmul_rn(dn0 - (double)t1[u], dn0 - (double)t2[u]));
+                    tb = denom > 0.0 ? __ddiv_rn(dv, denom) : __longlong_as_double(0x7ff8000000000000LL);
+                }
+                tau_b[iu] = tb;
             }
         }
     }
     pdl_trigger();
+}
+
+// Quotient table T[k] = (k - n0) / n0 (IEEE round-to-nearest, the exact operation of the per-cell path)
+// for every possible numerator k - n0 in [-n0, n0]: tau_a for every cell and tau_b for tie-free cells
+// become one L2-resident load instead of an fp64 division (+ square root) chain.
+__global__ void __launch_bounds__(256) fin_table_kernel(double* __restrict__ T, int64_t n0) {
+    const double dn0 = (double)n0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= 2 * n0; k += (int64_t)gridDim.x * blockDim.x)
+        T[k] = __ddiv_rn((double)(k - n0), dn0);
+}
+
+constexpr int64_t FIN_TABLE_MAX_N0 = int64_t(1) << 21;  // 2^22 + 1 doubles = 32 MiB (n <= 2048)
+
+struct FinTable {
+    int ordinal = -1;
+    int64_t n0 = -1;
+    double* dev = nullptr;
+    cudaEvent_t ready = nullptr;
+};
+static FinTable g_fin[64];
+
+// The device's quotient table for n0 (built on first use on `st`; other streams wait for its event).
+static int fin_table(int64_t n0, cudaStream_t st, const double** out) {
+    *out = nullptr;
+    if (n0 < 1 || n0 > FIN_TABLE_MAX_N0 || std::getenv("TB_FIN_NO_TABLE")) return TB_OK;
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);
+    int dev = 0;
+    TB_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return TB_OK;
+    FinTable& t = g_fin[dev];
+    if (t.n0 != n0) {
+        if (t.ready) TB_CUDA_TRY(cudaEventSynchronize(t.ready));  // the old table's readers are done
+        if (t.dev) cudaFree(t.dev);
+        t.dev = nullptr;
+        t.n0 = -1;
+        TB_CUDA_TRY(cudaMalloc(&t.dev, (size_t)(2 * n0 + 1) * sizeof(double)));
+        if (!t.ready) TB_CUDA_TRY(cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming));
+        const int64_t blocks = std::min<int64_t>((2 * n0 + 256) / 256, (int64_t)num_sms() * 8);
+        fin_table_kernel<<<(unsigned)blocks, 256, 0, st>>>(t.dev, n0);
+        int rc = check_launch("fin_table_kernel");
+        if (rc) return rc;
+        TB_CUDA_TRY(cudaEventRecord(t.ready, st));
+        t.n0 = n0;
+        t.ordinal = dev;
+    } else {
+        TB_CUDA_TRY(cudaStreamWaitEvent(st, t.ready, 0));
+    }
+    *out = t.dev;
+    return TB_OK;
 }
 
 }  // namespace tb
@@ -93,10 +155,13 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     const int64_t chunk = iters * FIN_THREADS;
     const int64_t blocks = (count + chunk - 1) / chunk;
     if (blocks > INT32_MAX) return fail(TB_ERR_CAPACITY, "finalize: job range too large");
+    const double* T = nullptr;
+    int rc = fin_table(n * (n - 1) / 2, static_cast<cudaStream_t>(stream), &T);
+    if (rc) return rc;
     TB_CUDA_TRY(launch_pdl(finalize_chunk_kernel, dim3((unsigned)blocks), dim3(FIN_THREADS), 0,
                            static_cast<cudaStream_t>(stream), num,
                            reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count,
-                           tau_a, tau_b, chunk));
+                           tau_a, tau_b, chunk, T));
     return check_launch("finalize_chunk_kernel");
 }
 

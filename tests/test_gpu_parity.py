@@ -500,10 +500,11 @@ def test_finalize_ranges_vs_numpy():
     from paper_1704_03767_b200.device import _ptr, _stream_ptr
     from paper_1704_03767_b200.pairindex import job_coord
     rng = np.random.default_rng(77)
-    for m, n in ((1, 5), (3, 9), (40, 17), (300, 1000), (5000, 64)):
+    for m, n in ((1, 5), (3, 9), (40, 17), (300, 1000), (5000, 64), (70, 3000)):
         n0 = n * (n - 1) // 2
         total = m * (m + 1) // 2
         n1 = rng.integers(0, n0 + 1, m).astype(np.uint64)
+        n1[::2] = 0  # tie-free rows: tau_b of tie-free pairs comes from the quotient table (n <= 2048)
         n1[rng.integers(0, m)] = n0  # a constant row -> NaN tau_b
         for lo, hi in ((0, total), (total // 3, total // 3 + 1), (max(0, total // 2 - 777), total),
                        (1, min(total, 4097)), (0, min(total, 4096 * 3 + 5))):
