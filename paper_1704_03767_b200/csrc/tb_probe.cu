@@ -125,6 +125,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mxf4_probe_k
     }
 }
 
+
+// Sparse variant (throughput probe for a 2:4-structured-sparse operand A): tcgen05.mma.sp ... kind::mxf4
+// (logical K = 128 per instruction: A holds 64 kept e2m1 values per row + 2-of-4 metadata in TMEM, B the
+// full 128), M = 256, two N accumulators alternating.  Operand values are irrelevant to the rate; the
+// metadata holds a valid pattern (kept indices 0, 1 of every group of four).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mxf4_sparse_probe_kernel(int iters, int N) {
+    using namespace tb;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 64 * 1024);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+    const int warp = threadIdx.x >> 5;
+    const bool leader = cluster_ctarank() == 0;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc_2sm<512>(slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    const uint32_t sf_col = 2u * N, meta_col = 480;
+    tmem_st_32x32b_x32(tmem + (uint32_t(warp * 32) << 16) + sf_col, 0x7F7F7F7Fu);
+    tmem_st_wait();
+    tmem_st_32x32b_x32(tmem + (uint32_t(warp * 32) << 16) + meta_col, 0x44444444u);
+    tmem_st_wait();
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (leader && threadIdx.x == 0) {
+        const uint32_t idesc = idesc_mxf4(256, (uint32_t)N) | (1u << 2);  // sparse flag; K = 128 (k_size 0)
+        const uint32_t sf = tmem + sf_col, meta = tmem + meta_col;
+        const uint64_t adesc = umma_desc_k_sw128(smem_u32(smem));
+        const uint64_t bdesc = umma_desc_k_sw128(smem_u32(smem + 16384));
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                for (int h = 0; h < 2; ++h)
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.sp.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, [%7], %3, [%5], [%6], p;\n\t}"
+                        ::"r"(tmem + h * N), "l"(adesc + 2 * k), "l"(bdesc + 4 * k), "r"(idesc), "r"(1u), "r"(sf),
+                        "r"(sf), "r"(meta)
+                        : "memory");
+        mma_commit_2sm(bar, 0x3);
+        mbar_wait(bar, 0);
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_2sm<512>(tmem);
+    }
+}
 }  // namespace
 
 // Returns the FLOP/s (2 per MAC) of the MMA stream above on every SM pair, best of `reps`; 0 on error.
@@ -214,4 +269,33 @@ extern "C" double tb_probe_int32_mixed_ops(int reps) {
     if (cudaGetLastError() != cudaSuccess) return 0.0;
     const double ops = (double)blocks * threads * iters * 32.0;  // 8 IADD3 + 8 LOP3 + 16 IMAD per iteration
     return ops / (best * 1e-3);
+}
+
+// FLOP/s (2 per logical MAC) of the sparse MMA stream above (N per accumulator), best of `reps`; 0 on error.
+extern "C" double tb_probe_mxf4_sparse_flops(int reps, int N) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int pairs = sms / 2, iters = 4096;
+    const size_t smem = 64 * 1024 + 2048;
+    if (cudaFuncSetAttribute(mxf4_sparse_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 0.0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < reps + 1; ++r) {
+        cudaEventRecord(e0);
+        mxf4_sparse_probe_kernel<<<2 * pairs, 128, smem>>>(r == 0 ? 64 : iters, N);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (cudaGetLastError() != cudaSuccess) return 0.0;
+    const double flops = 2.0 * 256 * N * 128 * 4.0 * iters * pairs;
+    return flops / (best * 1e-3);
 }
