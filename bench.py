@@ -349,7 +349,7 @@ def run_ours(args):
 
     from paper_1704_03767_b200 import _lib
     from paper_1704_03767_b200.device import get_engine
-    from paper_1704_03767_b200.multi import BandGather, balanced_job_shards, shard_bands
+    from paper_1704_03767_b200.multi import BandGather, balanced_job_shards, gather_band_fracs, shard_bands
 
     spec, x = workload(args.config)
     m, n = x.shape
@@ -365,8 +365,9 @@ def run_ours(args):
     job_range = shards[rank]
     nbands = args.bands
     if nbands <= 0:  # bands exist to overlap the gather; small launches cost GEMM efficiency
-        nbands = 1 if world == 1 or not strong else int(min(8, max(1, (job_range[1] - job_range[0]) >> 27)))
-    bands = shard_bands(*job_range, m, nbands)
+        nbands = 1 if world == 1 or not strong else int(min(4, max(1, (job_range[1] - job_range[0]) >> 26)))
+    fracs = gather_band_fracs(nbands)  # shrinking bands: the exposed last transfer is small
+    bands = shard_bands(*job_range, m, nbands, fracs)
     xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # raw values: both paths rank on the device
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     K = n * (n - 1) // 2
@@ -375,7 +376,7 @@ def run_ours(args):
     out_full = torch.empty(total_jobs, dtype=torch.float64, device=dev) if (rank == 0 or not gathering) else None
     local_out = out_full[job_range[0]:job_range[1]] if out_full is not None else \
         torch.empty(job_range[1] - job_range[0], dtype=torch.float64, device=dev)
-    gather = BandGather(shards, m, nbands, out=out_full, host_staging=share) if gathering else None
+    gather = BandGather(shards, m, nbands, out=out_full, host_staging=share, fracs=fracs) if gathering else None
     gemm_events: list = []
 
     def step(timing=None):

@@ -67,12 +67,14 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32
             if (!ok[u]) continue;
             const int64_t iu = i + (int64_t)u * FIN_THREADS;
             const double dv = (double)v[u];
-            // tau_a = num / n0 depends on num alone: the table (when present) holds every quotient
-            const double ta = T ? __ldg(&T[v[u] + n0]) : __ddiv_rn(dv, dn0);
+            const bool tie_free = (t1[u] | t2[u]) == 0;
+            // tau_a = num / n0; a quotient table (when present) holds every one of them
+            double ta = 0.0;
+            if (tau_a || tie_free) ta = T ? __ldg(&T[v[u] + n0]) : __ddiv_rn(dv, dn0);
             if (tau_a) tau_a[iu] = ta;
             if (tau_b) {
                 double tb;
-                if (T && (t1[u] | t2[u]) == 0) {
+                if (tie_free) {
                     tb = ta;  // no ties: sqrt(n0 * n0) = n0 exactly (n0^2 < 2^53), so tau_b = num / n0
                 } else {
                     const double denom = __dsqrt_rn(__dmul_rn(dn0 - (double)t1[u], dn0 - (double)t2[u]));
@@ -87,7 +89,10 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32
 
 // Quotient table T[k] = (k - n0) / n0 (IEEE round-to-nearest, the exact operation of the per-cell path)
 // for every possible numerator k - n0 in [-n0, n0]: tau_a for every cell and tau_b for tie-free cells
-// become one L2-resident load instead of an fp64 division (+ square root) chain.
+// become one L2-resident load instead of an fp64 division.  Off by default (TB_FIN_TABLE=1): measured on
+// config 5 the random 8-byte gathers make the kernel L1-bound (L1/TEX 85%, 13.1 ms for 43 GB = 3.3 TB/s,
+// profiles/r02_ncu_finalize_table.txt); the tie-free shortcut alone (one division for tau_a and tau_b) is
+// the default.
 __global__ void __launch_bounds__(256) fin_table_kernel(double* __restrict__ T, int64_t n0) {
     const double dn0 = (double)n0;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= 2 * n0; k += (int64_t)gridDim.x * blockDim.x)
@@ -107,7 +112,8 @@ static FinTable g_fin[64];
 // The device's quotient table for n0 (built on first use on `st`; other streams wait for its event).
 static int fin_table(int64_t n0, cudaStream_t st, const double** out) {
     *out = nullptr;
-    if (n0 < 1 || n0 > FIN_TABLE_MAX_N0 || std::getenv("TB_FIN_NO_TABLE")) return TB_OK;
+    static const bool on = [] { const char* e = std::getenv("TB_FIN_TABLE"); return e && e[0] == '1'; }();
+    if (!on || n0 < 1 || n0 > FIN_TABLE_MAX_N0) return TB_OK;
     std::lock_guard<std::mutex> lock(g_native_state_mutex);
     int dev = 0;
     TB_CUDA_TRY(cudaGetDevice(&dev));

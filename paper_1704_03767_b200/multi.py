@@ -88,14 +88,27 @@ def balanced_job_shards(world: int, m: int, path: str = "gemm") -> list[tuple[in
     return list(zip(b[:-1], b[1:]))
 
 
-def shard_bands(lo: int, hi: int, m: int, nbands: int) -> list[tuple[int, int]]:
-    """[lo, hi) split into <= nbands contiguous sub-ranges of (about) equal pair counts, cut at row
-    starts where the range spans rows (so each band is a row band of the GEMM), else evenly."""
+def gather_band_fracs(nbands: int) -> tuple:
+    """Shares of a shard's pairs per band for the banded gather: geometrically shrinking (ratio 0.6), so
+    the last band -- whose transfer to the consumer is the only part not hidden behind compute -- is
+    small while the first bands stay large enough for efficient GEMM launches."""
+    if nbands <= 1:
+        return (1.0,)
+    w = [0.6 ** i for i in range(nbands)]
+    return tuple(x / sum(w) for x in w)
+
+
+def shard_bands(lo: int, hi: int, m: int, nbands: int, fracs: tuple | None = None) -> list[tuple[int, int]]:
+    """[lo, hi) split into <= nbands contiguous sub-ranges holding the given shares of its pairs (default:
+    equal), cut at row starts where the range spans rows (so each band is a row band of the GEMM)."""
     if hi <= lo:
         return []
-    cuts = [lo]
-    for k in range(1, nbands):
-        j = lo + (hi - lo) * k // nbands
+    if fracs is None:
+        fracs = (1.0 / nbands,) * nbands
+    cuts, acc = [lo], 0.0
+    for fr in fracs[:-1]:
+        acc += fr
+        j = lo + int((hi - lo) * min(acc, 1.0))
         y = _row_of(j, m)
         r = _row_prefix(y, m)
         j = r if r > cuts[-1] else j
@@ -124,13 +137,13 @@ class BandGather:
     device bands through host memory (gloo plumbing runs)."""
 
     def __init__(self, shards: list[tuple[int, int]], m: int, nbands: int, out: torch.Tensor | None = None,
-                 dst: int = 0, group=None, host_staging: bool = False):
+                 dst: int = 0, group=None, host_staging: bool = False, fracs: tuple | None = None):
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         if len(shards) != self.world:
             raise ValueError(f"{len(shards)} shards for {self.world} ranks")
         self.shards, self.m, self.dst, self.group = shards, m, dst, group
-        self.bands = [shard_bands(lo, hi, m, nbands) for lo, hi in shards]
+        self.bands = [shard_bands(lo, hi, m, nbands, fracs) for lo, hi in shards]
         self.nb = max(len(b) for b in self.bands)
         self.out = out
         self.host = host_staging

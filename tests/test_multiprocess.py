@@ -71,9 +71,11 @@ def _band_worker(rank, world, port, m, nbands, out_path):
     total = m * (m + 1) // 2
     out = torch.full((total,), -1.0, dtype=torch.float64) if rank == 0 else None
     local = out[lo:hi] if rank == 0 else torch.empty(hi - lo, dtype=torch.float64)
-    g = BandGather(shards, m, nbands, out=out)
+    from paper_1704_03767_b200.multi import gather_band_fracs
+    fr = gather_band_fracs(nbands)
+    g = BandGather(shards, m, nbands, out=out, fracs=fr)
     for step in range(2):  # the gather object is reused across steps
-        for b, (blo, bhi) in enumerate(shard_bands(lo, hi, m, nbands)):
+        for b, (blo, bhi) in enumerate(shard_bands(lo, hi, m, nbands, fr)):
             # "compute" band b: job id j -> j + 0.5 * step (what the device finalize would write)
             local[blo - lo:bhi - lo] = torch.arange(blo, bhi, dtype=torch.float64) + 0.5 * step
             g.band(b, local[blo - lo:bhi - lo])
