@@ -1,9 +1,9 @@
 // K5: fp64 finalize over a contiguous job-id range -- derive_taus
 // (result.py:62-82) on device.  Streaming kernel: reads the int32 numerator
 // (4 B) and writes tau_a/tau_b (8 + 8 B) per pair; per-row tie counts stay in L2.
-// Measured on config 3 (134M pairs): 715 us = 3.7 TB/s effective (56% of HBM;
-// ncu: issue 53%, fp64 pipe 30%: latency of the fp64 div/sqrt chains), one cell
-// in flight per thread; now FIN_UNROLL cells per thread.
+// History: config 3 (134M pairs) 715 us = 3.7 TB/s (one cell per thread, fp64 div/sqrt latency-bound);
+// config 5 tau_a + tau_b (2.1e9 cells, 43 GB): 13.1 ms = 3.3 TB/s (r01 kernel), 9.5 ms = 4.5 TB/s with the
+// tie-free shortcut; now 32-bit walking from one decode per block.
 //
 // Bit-exactness: tau_a = (double)num / (double)n0 and tau_b = (double)num /
 // sqrt((n0 - n1_y) * (n0 - n1_x)) with IEEE round-to-nearest __ddiv_rn /
@@ -16,73 +16,68 @@
 
 namespace tb {
 
-// Block b owns job ids [job_lo + b * chunk, +chunk); thread t decodes its first
-// cell (y, x) once and then steps 256 job ids at a time, walking the row-major upper triangle
-// incrementally (x += 256, wrapping to row y + 1 at column y + 1), so the per-element work is the
-// IEEE tau sequence plus a few integer ops -- no per-element sqrt-based job_coord.  Loads and stores
-// stay coalesced (consecutive threads = consecutive job ids).
+// Block b owns the 4096 job ids [job_lo + 4096 b, +4096): thread 0 decodes the block's first cell once
+// (job_coord), every thread walks the row-major triangle from there in 32-bit row / column arithmetic
+// (its first cell, then 256 ids at a time), so consecutive threads handle consecutive job ids (coalesced
+// loads and stores) and the per-cell work is the IEEE tau sequence plus a few integer ops.  Tie-free cells
+// (n1_y = n1_x = 0) have sqrt(n0 * n0) = n0 exactly (n0^2 < 2^53), so one division gives tau_a and tau_b.
 constexpr int FIN_THREADS = 256;
-constexpr int FIN_ITERS_MAX = 16;  // cells per thread for large ranges; small ranges use fewer (more CTAs)
+constexpr int FIN_CELLS = 16;  // cells per thread (256 ids apart)
 
-constexpr int FIN_UNROLL = 4;  // cells in flight per thread: independent div/sqrt chains overlap
-
-__device__ __forceinline__ void fin_step(int64_t m, int64_t& y, int64_t& x) {  // next cell, 256 ids on
-    x += FIN_THREADS;
-    while (x >= m) {
-        x -= m - (y + 1);
+__device__ __forceinline__ void fin_walk(int32_t m, int32_t r, int32_t& y, int32_t& x) {  // r ids on
+    while (x + r >= m) {
+        r -= m - x;
         ++y;
+        x = y;
     }
+    x += r;
 }
 
-__global__ void __launch_bounds__(FIN_THREADS) finalize_chunk_kernel(const int32_t* __restrict__ num,
-                                                                      const unsigned long long* __restrict__ n1,
-                                                                      int64_t m, int64_t n0, int64_t job_lo,
-                                                                      int64_t count, double* __restrict__ tau_a,
-                                                                      double* __restrict__ tau_b, int64_t chunk,
-                                                                      const double* __restrict__ T) {
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const int32_t* __restrict__ num,
+                                                               const unsigned long long* __restrict__ n1,
+                                                               int32_t m, int64_t n0, int64_t job_lo, int64_t count,
+                                                               double* __restrict__ tau_a, double* __restrict__ tau_b,
+                                                               const double* __restrict__ T) {
     pdl_wait();
+    __shared__ int32_t s_y, s_x;
+    const int64_t base = (int64_t)blockIdx.x * (FIN_THREADS * FIN_CELLS);
+    if (threadIdx.x == 0) {
+        int64_t y, x;
+        job_coord(job_lo + base, m, y, x);
+        s_y = (int32_t)y;
+        s_x = (int32_t)x;
+    }
+    __syncthreads();
+    const int64_t left = count - base;
+    const int32_t nmine = left > FIN_THREADS * FIN_CELLS ? FIN_CELLS
+                          : (int32_t)((left - threadIdx.x + FIN_THREADS - 1) / FIN_THREADS);
+    if (nmine <= 0) return;
+    int32_t y = s_y, x = s_x;
+    fin_walk(m, (int32_t)threadIdx.x, y, x);
     const double dn0 = (double)n0;
-    int64_t i = (int64_t)blockIdx.x * chunk + threadIdx.x;
-    if (i >= count) return;
-    const int64_t i_end = min(count, (int64_t)(blockIdx.x + 1) * chunk);
-    int64_t y, x;
-    job_coord(job_lo + i, m, y, x);
-    for (; i < i_end; i += FIN_UNROLL * FIN_THREADS) {
-        // FIN_UNROLL cells 256 ids apart: loads and row/column tie counts first, then the IEEE sequences
-        int32_t v[FIN_UNROLL];
-        unsigned long long t1[FIN_UNROLL], t2[FIN_UNROLL];
-        bool ok[FIN_UNROLL];
-#pragma unroll
-        for (int u = 0; u < FIN_UNROLL; ++u) {
-            const int64_t iu = i + (int64_t)u * FIN_THREADS;
-            ok[u] = iu < i_end;
-            if (u > 0 && ok[u]) fin_step(m, y, x);  // only walk to cells that exist (no row past m - 1)
-            v[u] = ok[u] ? num[iu] : 0;
-            t1[u] = ok[u] ? __ldg(&n1[y]) : 0ull;
-            t2[u] = ok[u] ? __ldg(&n1[x]) : 0ull;
-        }
-        if (i + FIN_UNROLL * FIN_THREADS < i_end) fin_step(m, y, x);
-#pragma unroll
-        for (int u = 0; u < FIN_UNROLL; ++u) {
-            if (!ok[u]) continue;
-            const int64_t iu = i + (int64_t)u * FIN_THREADS;
-            const double dv = (double)v[u];
-            const bool tie_free = (t1[u] | t2[u]) == 0;
-            // tau_a = num / n0; a quotient table (when present) holds every one of them
-            double ta = 0.0;
-            if (tau_a || tie_free) ta = T ? __ldg(&T[v[u] + n0]) : __ddiv_rn(dv, dn0);
-            if (tau_a) tau_a[iu] = ta;
-            if (tau_b) {
-                double tb;
-                if (tie_free) {
-                    tb = ta;  // no ties: sqrt(n0 * n0) = n0 exactly (n0^2 < 2^53), so tau_b = num / n0
-                } else {
-                    const double denom = __dsqrt_rn(__dmul_rn(dn0 - (double)t1[u], dn0 - (double)t2[u]));
-                    tb = denom > 0.0 ? __ddiv_rn(dv, denom) : __longlong_as_double(0x7ff8000000000000LL);
-                }
-                tau_b[iu] = tb;
+    const int32_t* np = num + base + threadIdx.x;
+    double* pa = TA ? tau_a + base + threadIdx.x : nullptr;
+    double* pb = TB ? tau_b + base + threadIdx.x : nullptr;
+#pragma unroll 4
+    for (int u = 0; u < FIN_CELLS; ++u) {
+        if (u >= nmine) break;
+        const int32_t v = np[u * FIN_THREADS];
+        const unsigned long long t1 = __ldg(&n1[y]), t2 = __ldg(&n1[x]);
+        const double dv = (double)v;
+        const bool tie_free = (t1 | t2) == 0;
+        double ta = 0.0;
+        if (TA || tie_free) ta = T ? __ldg(&T[v + n0]) : __ddiv_rn(dv, dn0);
+        if (TA) pa[u * FIN_THREADS] = ta;
+        if (TB) {
+            double tb = ta;
+            if (!tie_free) {
+                const double denom = __dsqrt_rn(__dmul_rn(dn0 - (double)t1, dn0 - (double)t2));
+                tb = denom > 0.0 ? __ddiv_rn(dv, denom) : __longlong_as_double(0x7ff8000000000000LL);
             }
+            pb[u * FIN_THREADS] = tb;
         }
+        if (u + 1 < nmine) fin_walk(m, FIN_THREADS, y, x);
     }
     pdl_trigger();
 }
@@ -154,21 +149,19 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     if (!num || !n1_rows) return fail(TB_ERR_INVALID, "finalize: null pointer");
     const int64_t count = job_hi - job_lo;
     if (count == 0) return TB_OK;
-    // each thread walks `iters` cells 256 apart: 16 for large ranges (amortises the job_coord decode);
-    // small ranges shorten the walk so the grid still covers the GPU
-    const int64_t per_sm = (int64_t)num_sms() * 8 * FIN_THREADS;  // ~8 CTAs per SM (measured 4 / 8 / 16 / 32)
-    const int64_t iters = std::max<int64_t>(1, std::min<int64_t>(FIN_ITERS_MAX, count / std::max<int64_t>(1, per_sm)));
-    const int64_t chunk = iters * FIN_THREADS;
-    const int64_t blocks = (count + chunk - 1) / chunk;
+    if (m > INT32_MAX) return fail(TB_ERR_CAPACITY, "finalize: m too large");
+    const int64_t blocks = (count + FIN_THREADS * FIN_CELLS - 1) / (FIN_THREADS * FIN_CELLS);
     if (blocks > INT32_MAX) return fail(TB_ERR_CAPACITY, "finalize: job range too large");
     const double* T = nullptr;
     int rc = fin_table(n * (n - 1) / 2, static_cast<cudaStream_t>(stream), &T);
     if (rc) return rc;
-    TB_CUDA_TRY(launch_pdl(finalize_chunk_kernel, dim3((unsigned)blocks), dim3(FIN_THREADS), 0,
-                           static_cast<cudaStream_t>(stream), num,
-                           reinterpret_cast<const unsigned long long*>(n1_rows), m, n * (n - 1) / 2, job_lo, count,
-                           tau_a, tau_b, chunk, T));
-    return check_launch("finalize_chunk_kernel");
+    auto kern = tau_a ? (tau_b ? finalize_kernel<true, true> : finalize_kernel<true, false>)
+                      : (tau_b ? finalize_kernel<false, true> : nullptr);
+    if (!kern) return TB_OK;
+    TB_CUDA_TRY(launch_pdl(kern, dim3((unsigned)blocks), dim3(FIN_THREADS), 0, static_cast<cudaStream_t>(stream), num,
+                           reinterpret_cast<const unsigned long long*>(n1_rows), (int32_t)m, n * (n - 1) / 2, job_lo,
+                           count, tau_a, tau_b, T));
+    return check_launch("finalize_kernel");
 }
 
 namespace tb {

@@ -22,10 +22,14 @@ import torch.distributed as dist
 
 from .pairindex import job_shard_range
 
-# Sign-pack cost of one row in units of one pair's GEMM cost, from the config-5 launch list
-# (profiles/r02_launches: signpack 3.9 ms for 65536 rows vs gemm 401 ms for 2.147e9 pairs: 59.5 ns vs
-# 0.187 ns).
-ROW_COST_PAIRS = 319
+# Cost model of one rank's shard on the GEMM path, in units of one pair's GEMM time, fitted to the
+# one-GPU shard timings of config 5 (tools/exp_shards.py, profiles/r02_strong_scaling_projection.log):
+# a pair in a row of width w = m - y costs 1 + ROW_WIDTH_COST * w / m (long rows stream more of S per
+# output and re-read it from DRAM more often: 0.236 ns per pair in the top shard vs 0.203 in the bottom
+# one), and every row the shard sign-packs (all rows from its first one to m) costs ROW_PACK_COST pairs
+# (K2: 42 ns per 1024-sample row against 0.196 ns per pair).
+ROW_WIDTH_COST = 0.21
+ROW_PACK_COST = 214
 
 
 def _row_prefix(y: int, m: int) -> int:
@@ -44,10 +48,33 @@ def _row_of(j: int, m: int) -> int:
     return lo
 
 
+def _weighted_rows(y0: int, y1: int, m: int) -> float:
+    """sum over full rows y in [y0, y1) of w (1 + ROW_WIDTH_COST w / m), w = m - y (closed form)."""
+    if y1 <= y0:
+        return 0.0
+    a, b = m - y1 + 1, m - y0  # widths a..b
+
+    def s1(k):
+        return k * (k + 1) / 2
+
+    def s2(k):
+        return k * (k + 1) * (2 * k + 1) / 6
+    return (s1(b) - s1(a - 1)) + ROW_WIDTH_COST / m * (s2(b) - s2(a - 1))
+
+
 def shard_cost(lo: int, hi: int, m: int, path: str = "gemm") -> float:
+    """Modelled cost of job ids [lo, hi) (GEMM path: width-weighted pairs + sign-pack rows; merge: pairs)."""
     if hi <= lo:
         return 0.0
-    return (hi - lo) + (ROW_COST_PAIRS * (m - _row_of(lo, m)) if path == "gemm" else 0)
+    if path != "gemm":
+        return float(hi - lo)
+    y0, y1 = _row_of(lo, m), _row_of(hi - 1, m)
+    wt = lambda y: 1.0 + ROW_WIDTH_COST * (m - y) / m  # noqa: E731
+    if y0 == y1:
+        c = (hi - lo) * wt(y0)
+    else:
+        c = (_row_prefix(y0 + 1, m) - lo) * wt(y0) + _weighted_rows(y0 + 1, y1, m) + (hi - _row_prefix(y1, m)) * wt(y1)
+    return c + ROW_PACK_COST * (m - y0)
 
 
 def balanced_job_shards(world: int, m: int, path: str = "gemm") -> list[tuple[int, int]]:
