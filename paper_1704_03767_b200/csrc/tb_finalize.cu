@@ -59,25 +59,40 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const int32_t* __
     const int32_t* np = num + base + threadIdx.x;
     double* pa = TA ? tau_a + base + threadIdx.x : nullptr;
     double* pb = TB ? tau_b + base + threadIdx.x : nullptr;
-#pragma unroll 4
-    for (int u = 0; u < FIN_CELLS; ++u) {
-        if (u >= nmine) break;
-        const int32_t v = np[u * FIN_THREADS];
-        const unsigned long long t1 = __ldg(&n1[y]), t2 = __ldg(&n1[x]);
-        const double dv = (double)v;
-        const bool tie_free = (t1 | t2) == 0;
-        double ta = 0.0;
-        if (TA || tie_free) ta = T ? __ldg(&T[v + n0]) : __ddiv_rn(dv, dn0);
-        if (TA) pa[u * FIN_THREADS] = ta;
-        if (TB) {
-            double tb = ta;
-            if (!tie_free) {
-                const double denom = __dsqrt_rn(__dmul_rn(dn0 - (double)t1, dn0 - (double)t2));
-                tb = denom > 0.0 ? __ddiv_rn(dv, denom) : __longlong_as_double(0x7ff8000000000000LL);
+    constexpr int G = 4;  // cells in flight: addresses first, then the loads, then the IEEE sequences
+#pragma unroll 1
+    for (int g = 0; g < FIN_CELLS; g += G) {
+        int32_t v[G];
+        unsigned long long t1[G], t2[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const int c = g + u;
+            if (c < nmine) {
+                v[u] = np[c * FIN_THREADS];
+                t1[u] = __ldg(&n1[y]);
+                t2[u] = __ldg(&n1[x]);
+                if (c + 1 < nmine) fin_walk(m, FIN_THREADS, y, x);
             }
-            pb[u * FIN_THREADS] = tb;
         }
-        if (u + 1 < nmine) fin_walk(m, FIN_THREADS, y, x);
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const int c = g + u;
+            if (c >= nmine) break;
+            const double dv = (double)v[u];
+            const bool tie_free = (t1[u] | t2[u]) == 0;
+            double ta = 0.0;
+            if (TA || tie_free) ta = T ? __ldg(&T[v[u] + n0]) : __ddiv_rn(dv, dn0);
+            if (TA) pa[c * FIN_THREADS] = ta;
+            if (TB) {
+                double tb = ta;
+                if (!tie_free) {
+                    const double denom = __dsqrt_rn(__dmul_rn(dn0 - (double)t1[u], dn0 - (double)t2[u]));
+                    tb = denom > 0.0 ? __ddiv_rn(dv, denom) : __longlong_as_double(0x7ff8000000000000LL);
+                }
+                pb[c * FIN_THREADS] = tb;
+            }
+        }
+        if (g + G >= nmine) break;
     }
     pdl_trigger();
 }

@@ -309,24 +309,24 @@ class TauEngine:
         return self._session(stream)
 
     def prepare(self, x: torch.Tensor, path: str, full_counts: bool = False, row_lo: int = 0,
-                simt: bool = False) -> "Prepared":
-        """Per-dataset device operands, once per call (inside session()): ranks and n1 of every row, then
-        the sign matrix S of rows >= row_lo (and |S| for full counts) on the GEMM path, or the K1
-        presort of every row on the merge path.  Workspaces are the engine's (valid until the next
-        prepare on this engine)."""
+                simt: bool = False, all_rows: bool = True) -> "Prepared":
+        """Per-dataset device operands, once per call (inside session()): ranks and n1 of every row (of rows
+        >= row_lo only with all_rows=False: a job range starting in row row_lo never reads the others), then
+        the sign matrix S of rows >= row_lo on the GEMM path, or the K1 presort on the merge path.
+        Workspaces are the engine's (valid until the next prepare on this engine)."""
         m, n = x.shape
         st = _stream_ptr(self._stream)
         prep = Prepared(path=path, m=m, n=n, full=full_counts, simt=simt,
-                        n1_rows=torch.empty(m, dtype=torch.int64, device=self.device),
+                        n1_rows=torch.zeros(m, dtype=torch.int64, device=self.device),
                         flags=torch.zeros(1, dtype=torch.int32, device=self.device))
         stub = PairResult(m=m, n=n, job_lo=row_prefix(min(row_lo, m), m), job_hi=m * (m + 1) // 2, path=path,
                           numerator=None, n1_rows=prep.n1_rows, flags=prep.flags)
         prep.row_lo = min(row_lo, m)
         if path == "gemm":
-            prep.S, prep.K, prep.ldS, prep.fmt = self._gemm_prepare(x, stub, st, simt)
+            prep.S, prep.K, prep.ldS, prep.fmt = self._gemm_prepare(x, stub, st, simt, all_rows=all_rows)
         else:
             prep.pos, prep.srt, prep.keys, (prep.maxgrp, prep.groups, prep.ngroups) = \
-                self._merge_prepare(x.contiguous(), stub, st)
+                self._merge_prepare(x.contiguous(), stub, st, row_from=0 if all_rows else prep.row_lo)
         return prep
 
     def numerators(self, prep: "Prepared", lo: int, hi: int, num: torch.Tensor, nd: torch.Tensor | None = None,
@@ -378,7 +378,7 @@ class TauEngine:
         kbytes = K // 2 if fmt == _lib.TB_SIGN_E2M1 else K
         return K, fmt, (kbytes + 15) // 16 * 16, (n + 7) // 8 * 8
 
-    def _gemm_prepare(self, x, res: PairResult, st, simt: bool = False, row_chunks=None):
+    def _gemm_prepare(self, x, res: PairResult, st, simt: bool = False, row_chunks=None, all_rows: bool = True):
         """K0 rank transform + K2 sign pack of every row: the GEMM operand S (m x K signs).
 
         ``row_chunks`` = [(r0, r1, wait_fn)]: prepare rows [r0, r1) after ``wait_fn()`` (the
@@ -387,13 +387,17 @@ class TauEngine:
         K, fmt, ldS, ldr = self._gemm_layout(n, simt)
         R = self._buf("R", m * ldr, torch.int16)
         S = self._buf("S", m * ldS, torch.int8)
-        # every job id of [job_lo, job_hi) pairs rows >= y_lo (the row of job_lo): rows above it are ranked
-        # (their n1 is part of the result) but need no sign vector -- a late job-range shard (multi-GPU
-        # strong scaling) packs only its own share of S
+        # every job id of [job_lo, job_hi) pairs rows >= y_lo (the row of job_lo): rows above it need no sign
+        # vector -- a late job-range shard (multi-GPU strong scaling) packs only its own share of S -- and
+        # with all_rows=False they are not ranked either (their n1 stays 0)
         y_lo = job_coord(res.job_lo, m)[0] if res.job_hi > res.job_lo else m
         for r0, r1, wait in (row_chunks or [(0, m, None)]):
             if wait is not None:
                 wait()
+            if not all_rows:
+                r0 = max(r0, y_lo)
+                if r0 >= r1:
+                    continue
             if n <= RANK_ROWS_MAX_N:  # K0: shared-memory / register sorts
                 _lib.call("tb_rank_rows", _ptr(x[r0:r1]), _dtype_code(x), r1 - r0, n, x.stride(0),
                           _ptr(R[r0 * ldr:]), ldr, _ptr(res.n1_rows[r0:]), _ptr(res.flags), st)
@@ -451,7 +455,7 @@ class TauEngine:
         base = bands[0][0]
         with self._session(stream) as st_t:
             st = _stream_ptr(st_t)
-            prep = self.prepare(x, path, row_lo=job_coord(base, m)[0])
+            prep = self.prepare(x, path, row_lo=job_coord(base, m)[0], all_rows=False)
             num = self._buf("num_band", max(hi - lo for lo, hi in bands), torch.int32)
             for b, (lo, hi) in enumerate(bands):
                 if timing is not None:  # (start, end) events around the band's numerator kernels
@@ -591,25 +595,27 @@ class TauEngine:
         wsb = int(_lib.load().tb_merge_workspace(n))
         return self._buf("merge_ws", wsb, torch.uint8), wsb
 
-    def _merge_prepare(self, x, res: PairResult, st):
+    def _merge_prepare(self, x, res: PairResult, st, row_from: int = 0):
         """K0w dense ranks of the raw values (any dtype, any n), then the K1 presort of every variable
-        (u-order positions, sorted ranks, min-rank merge keys, n1, tie groups)."""
+        (u-order positions, sorted ranks, min-rank merge keys, n1, tie groups) -- of rows >= row_from."""
         m, n = res.m, res.n
+        r0 = min(max(row_from, 0), m - 1)
+        mr = m - r0
         code = _dtype_code(x)
         ranks = self._buf("R32", m * n, torch.int32)
-        wsb = int(_lib.load().tb_rank_dense_workspace(m, n, code))
+        wsb = int(_lib.load().tb_rank_dense_workspace(mr, n, code))
         ws = self._buf("rank_ws", wsb, torch.uint8)
-        _lib.call("tb_rank_dense", _ptr(x), code, m, n, x.stride(0), _ptr(ranks), 0, n, _ptr(res.n1_rows),
-                  _ptr(res.flags), _ptr(ws), wsb, st)
-        x = ranks
+        _lib.call("tb_rank_dense", _ptr(x[r0:]), code, mr, n, x.stride(0), _ptr(ranks[r0 * n:]), 0, n,
+                  _ptr(res.n1_rows[r0:]), _ptr(res.flags), _ptr(ws), wsb, st)
         pos = self._buf("pos", m * n, torch.int32)
         srt = self._buf("sorted", m * n, torch.int32)
         keys = self._buf("mkeys", m * n, torch.int16)
         work = self._buf("work", m * n, torch.int32)
         maxgrp = self._buf("maxgrp", m, torch.int32)
         ngroups = self._buf("ngroups", m, torch.int32)
-        _lib.call("tb_presort", _ptr(x), m, n, _ptr(pos), _ptr(srt), _ptr(keys), _ptr(res.n1_rows),
-                  _ptr(maxgrp), _ptr(work), _ptr(ngroups), _ptr(res.flags), st)
+        _lib.call("tb_presort", _ptr(ranks[r0 * n:]), mr, n, _ptr(pos[r0 * n:]), _ptr(srt[r0 * n:]),
+                  _ptr(keys[r0 * n:]), _ptr(res.n1_rows[r0:]), _ptr(maxgrp[r0:]), _ptr(work[r0 * n:]),
+                  _ptr(ngroups[r0:]), _ptr(res.flags), st)
         return pos, srt, keys, (maxgrp, work, ngroups)
 
 

@@ -116,12 +116,12 @@ def balanced_job_shards(world: int, m: int, path: str = "gemm") -> list[tuple[in
 
 
 def gather_band_fracs(nbands: int) -> tuple:
-    """Shares of a shard's pairs per band for the banded gather: geometrically shrinking (ratio 0.6), so
+    """Shares of a shard's pairs per band for the banded gather: geometrically shrinking (ratio 0.5), so
     the last band -- whose transfer to the consumer is the only part not hidden behind compute -- is
     small while the first bands stay large enough for efficient GEMM launches."""
     if nbands <= 1:
         return (1.0,)
-    w = [0.6 ** i for i in range(nbands)]
+    w = [0.5 ** i for i in range(nbands)]
     return tuple(x / sum(w) for x in w)
 
 

@@ -42,7 +42,7 @@ def timed(bands, reps=3):
 
 full = timed([(0, total)])
 shards = balanced_job_shards(P, m, path)
-nb = int(min(4, max(1, (shards[0][1] - shards[0][0]) >> 26)))
+nb = int(min(4, max(1, (shards[0][1] - shards[0][0]) >> 26)))  # bench.py's automatic band count
 fr = gather_band_fracs(nb)
 print(f"config {cfg}: N=1 step {1e3 * full:.2f} ms; P={P} shards, {nb} bands per rank, shares {[round(f, 3) for f in fr]}",
       flush=True)
