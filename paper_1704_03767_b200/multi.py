@@ -115,13 +115,13 @@ def balanced_job_shards(world: int, m: int, path: str = "gemm") -> list[tuple[in
     return list(zip(b[:-1], b[1:]))
 
 
-def gather_band_fracs(nbands: int) -> tuple:
+def gather_band_fracs(nbands: int, ratio: float = 0.5) -> tuple:
     """Shares of a shard's pairs per band for the banded gather: geometrically shrinking (ratio 0.5), so
     the last band -- whose transfer to the consumer is the only part not hidden behind compute -- is
     small while the first bands stay large enough for efficient GEMM launches."""
     if nbands <= 1:
         return (1.0,)
-    w = [0.5 ** i for i in range(nbands)]
+    w = [ratio ** i for i in range(nbands)]
     return tuple(x / sum(w) for x in w)
 
 

@@ -13,6 +13,8 @@ from paper_1704_03767_b200.multi import balanced_job_shards, gather_band_fracs, 
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 P = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+NB = int(sys.argv[3]) if len(sys.argv) > 3 else 0        # bands per rank (0: bench.py's automatic count)
+RATIO = float(sys.argv[4]) if len(sys.argv) > 4 else 0.5  # band share ratio
 NVLINK = 770e9
 eng = get_engine(0)
 x = torch.from_numpy(workloads.generate(cfg)).cuda()
@@ -42,8 +44,8 @@ def timed(bands, reps=3):
 
 full = timed([(0, total)])
 shards = balanced_job_shards(P, m, path)
-nb = int(min(4, max(1, (shards[0][1] - shards[0][0]) >> 26)))  # bench.py's automatic band count
-fr = gather_band_fracs(nb)
+nb = NB or int(min(4, max(1, (shards[0][1] - shards[0][0]) >> 26)))  # bench.py's automatic band count
+fr = gather_band_fracs(nb, RATIO)
 print(f"config {cfg}: N=1 step {1e3 * full:.2f} ms; P={P} shards, {nb} bands per rank, shares {[round(f, 3) for f in fr]}",
       flush=True)
 worst = 0.0
