@@ -77,32 +77,54 @@ def shard_cost(lo: int, hi: int, m: int, path: str = "gemm") -> float:
     return c + ROW_PACK_COST * (m - y0)
 
 
-def balanced_job_shards(world: int, m: int, path: str = "gemm") -> list[tuple[int, int]]:
-    """Contiguous job-id shards of equal modelled cost covering [0, m(m+1)/2) (bisection on the
-    per-shard cost target; the merge path's cost is its pair count, i.e. job_shard_range)."""
+GEMM_ROW_BLOCK = 256  # the GEMM's unit height: a job range that cuts a row block computes all of it
+
+
+def balanced_job_shards(world: int, m: int, path: str = "gemm", align: int | None = None) -> list[tuple[int, int]]:
+    """Contiguous job-id shards of equal modelled cost covering [0, m(m+1)/2) (bisection on the per-shard
+    cost target; the merge path's cost is its pair count, i.e. job_shard_range).  On the GEMM path the
+    boundaries are row-block starts (``align`` rows, default the GEMM's 256 when m is large enough): a
+    boundary inside a row block would make both neighbouring shards run that block's full units."""
     total = m * (m + 1) // 2
     if world < 1:
         raise ValueError("world must be >= 1")
     if path != "gemm" or world == 1:
         return [job_shard_range(r, world, m) for r in range(world)]
+    if align is None:
+        align = GEMM_ROW_BLOCK if m >= 8 * GEMM_ROW_BLOCK * world else 1
+    cand = [_row_prefix(y, m) for y in range(0, m, align)] + [total] if align > 1 else None
 
-    def cut(target: float):
-        bounds, lo = [0], 0
-        for _ in range(world - 1):
-            a, b = lo, total  # largest hi with cost(lo, hi) <= target
+    def largest_hi(lo: int, target: float) -> int:
+        if cand is None:
+            a, b = lo, total
             while a < b:
                 mid = (a + b + 1) // 2
                 if shard_cost(lo, mid, m, path) <= target:
                     a = mid
                 else:
                     b = mid - 1
-            lo = a
+            return a
+        import bisect
+        i0 = bisect.bisect_left(cand, lo)
+        a, b = i0, len(cand) - 1
+        while a < b:
+            mid = (a + b + 1) // 2
+            if shard_cost(lo, cand[mid], m, path) <= target:
+                a = mid
+            else:
+                b = mid - 1
+        return cand[a]
+
+    def cut(target: float):
+        bounds, lo = [0], 0
+        for _ in range(world - 1):
+            lo = largest_hi(lo, target)
             bounds.append(lo)
         bounds.append(total)
         return bounds
 
     t_lo, t_hi = 0.0, shard_cost(0, total, m, path)
-    for _ in range(100):
+    for _ in range(200):
         t = 0.5 * (t_lo + t_hi)
         b = cut(t)
         if shard_cost(b[-2], b[-1], m, path) <= t:
@@ -125,19 +147,26 @@ def gather_band_fracs(nbands: int, ratio: float = 0.5) -> tuple:
     return tuple(x / sum(w) for x in w)
 
 
-def shard_bands(lo: int, hi: int, m: int, nbands: int, fracs: tuple | None = None) -> list[tuple[int, int]]:
+def shard_bands(lo: int, hi: int, m: int, nbands: int, fracs: tuple | None = None,
+                align: int = GEMM_ROW_BLOCK) -> list[tuple[int, int]]:
     """[lo, hi) split into <= nbands contiguous sub-ranges holding the given shares of its pairs (default:
-    equal), cut at row starts where the range spans rows (so each band is a row band of the GEMM)."""
+    equal), cut at row starts -- row-block starts (multiples of ``align``) when the range spans enough of
+    them, so no GEMM row block is split between two launches."""
     if hi <= lo:
         return []
     if fracs is None:
         fracs = (1.0 / nbands,) * nbands
+    y_lo, y_hi = _row_of(lo, m), _row_of(hi - 1, m)
+    if y_hi - y_lo < 4 * align * nbands:
+        align = 1
     cuts, acc = [lo], 0.0
     for fr in fracs[:-1]:
         acc += fr
         j = lo + int((hi - lo) * min(acc, 1.0))
         y = _row_of(j, m)
-        r = _row_prefix(y, m)
+        if align > 1:
+            y = (y + align // 2) // align * align
+        r = _row_prefix(min(y, m - 1), m)
         j = r if r > cuts[-1] else j
         if cuts[-1] < j < hi:
             cuts.append(j)

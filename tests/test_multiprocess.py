@@ -110,7 +110,18 @@ def test_balanced_shards_partition_and_balance():
                     bands = shard_bands(lo, hi, m, 4)
                     assert (not bands and lo == hi) or (bands[0][0] == lo and bands[-1][1] == hi)
                     assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(bands, bands[1:]))
-    sh = balanced_job_shards(8, 65536, "gemm")
+    from paper_1704_03767_b200.multi import _row_of, _row_prefix, gather_band_fracs
+    sh = balanced_job_shards(8, 65536, "gemm", align=1)
     costs = [shard_cost(lo, hi, 65536) for lo, hi in sh]
     assert max(costs) / min(costs) < 1.001
     assert sh[0][1] - sh[0][0] < sh[-1][1] - sh[-1][0]  # early shards pack more rows: fewer pairs
+    # default: boundaries at GEMM row-block starts (no row block split between two shards or two bands)
+    sh = balanced_job_shards(8, 65536, "gemm")
+    costs = [shard_cost(lo, hi, 65536) for lo, hi in sh]
+    assert max(costs) / min(costs) < 1.06
+    for lo, hi in sh:
+        y = _row_of(lo, 65536)
+        assert y % 256 == 0 and _row_prefix(y, 65536) == lo
+        for a, _ in shard_bands(lo, hi, 65536, 3, gather_band_fracs(3)):
+            ya = _row_of(a, 65536)
+            assert ya % 256 == 0 and _row_prefix(ya, 65536) == a
