@@ -23,6 +23,9 @@ namespace tb {
 // (n1_y = n1_x = 0) have sqrt(n0 * n0) = n0 exactly (n0^2 < 2^53), so one division gives tau_a and tau_b.
 constexpr int FIN_THREADS = 256;
 constexpr int FIN_CELLS = 16;  // cells per thread (256 ids apart)
+#ifndef FIN_G
+#define FIN_G 4  // cells whose loads are in flight together (config 5 tau_a + tau_b: G = 4 -> 8.17 ms)
+#endif
 
 __device__ __forceinline__ void fin_walk(int32_t m, int32_t r, int32_t& y, int32_t& x) {  // r ids on
     while (x + r >= m) {
@@ -59,7 +62,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const int32_t* __
     const int32_t* np = num + base + threadIdx.x;
     double* pa = TA ? tau_a + base + threadIdx.x : nullptr;
     double* pb = TB ? tau_b + base + threadIdx.x : nullptr;
-    constexpr int G = 4;  // cells in flight: addresses first, then the loads, then the IEEE sequences
+    constexpr int G = FIN_G;  // cells in flight: addresses first, then the loads, then the IEEE sequences
 #pragma unroll 1
     for (int g = 0; g < FIN_CELLS; g += G) {
         int32_t v[G];

@@ -22,13 +22,12 @@ import torch.distributed as dist
 
 from .pairindex import job_shard_range
 
-# Cost model of one rank's shard on the GEMM path, in units of one pair's GEMM time, fitted to the
-# one-GPU shard timings of config 5 (tools/exp_shards.py, profiles/r02_strong_scaling_projection.log):
-# a pair in a row of width w = m - y costs 1 + ROW_WIDTH_COST * w / m (long rows stream more of S per
-# output and re-read it from DRAM more often: 0.236 ns per pair in the top shard vs 0.203 in the bottom
-# one), and every row the shard sign-packs (all rows from its first one to m) costs ROW_PACK_COST pairs
-# (K2: 42 ns per 1024-sample row against 0.196 ns per pair).
-ROW_WIDTH_COST = 0.21
+# Cost model of one rank's shard on the GEMM path, in units of one pair's GEMM time: every pair costs 1
+# (one-GPU timings of row-block-aligned config-5 shards: 0.19-0.21 ns per pair whatever the rows, within
+# the run-to-run noise, profiles/r02_strong_scaling_projection.log -- the width dependence seen before the
+# alignment was the duplicated boundary row blocks), and every row the shard sign-packs (all rows from its
+# first one to m) costs ROW_PACK_COST pairs (K2: 42 ns per 1024-sample row against 0.196 ns per pair).
+ROW_WIDTH_COST = 0.0
 ROW_PACK_COST = 214
 
 
