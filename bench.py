@@ -548,6 +548,12 @@ def run_ours(args):
                     "frac_of_measured_fp4_library": (achieved / fp4_lib) if fp4_lib else None,
                     "measured_mma_ceiling_tflops": mma_ceiling / 1e12 if mma_ceiling else None,
                     "frac_of_measured_mma_ceiling": (achieved / mma_ceiling) if mma_ceiling else None,
+                    # the MMA-issue ceiling is measured at the 1965 MHz boost clock; a long GEMM runs at the
+                    # clock the 1 kW cap allows (clocks.sm_mhz), so this is the kernel's share of what the
+                    # tensor pipe can issue at that clock
+                    "frac_of_mma_ceiling_at_measured_clock": (
+                        achieved / (mma_ceiling * clocks["sm_mhz"] / 1965.0)
+                        if mma_ceiling and clocks.get("sm_mhz") else None),
                     "measured_int8_peak_tops": peak / 1e12 if peak else None,
                     "algorithmic": (f"2*K ops per i<j pair, K=n(n-1)/2={K} sample pairs; {my_pairs} pairs per step "
                                     f"in {per_step_units} row-band launches (achieved = per-launch algorithmic ops / "

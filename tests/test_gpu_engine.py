@@ -196,3 +196,52 @@ def test_distinct_devices():
     r1 = TauEngine(1).all_pairs(x, kernel="gemm").validate()
     r0 = TauEngine(0).all_pairs(x.to("cuda:0"), kernel="gemm").validate()
     assert torch.equal(r1.numerator.cpu(), r0.numerator.cpu())
+
+
+@pytest.mark.timeout(900)
+def test_config5_record_stream_properties():
+    """The plugin call at BASELINE config-5 scale (65536 variables, 2.1e9 cells, 103 GB of records through
+    the bounded window pipeline): size-independent properties of every pass -- record count and tile order
+    (i, j of the first and last record of every pass against the closed-form plan), the CELL_DTYPE identity
+    numerator = n0 - n1 - n2 + n3 - 2 n_d on a stride of every pass, n1 / n2 against the per-variable tie
+    counts -- and a sample of cells against the device all-pairs API."""
+    import paper_1704_03767_b200 as tb
+    from paper_1704_03767_b200 import workloads
+    from paper_1704_03767_b200.engine import JobSpace, plan_passes
+    x = workloads.generate(5)
+    m, n = x.shape
+    n0 = n * (n - 1) // 2
+    ranks = np.stack([tb.rank_transform(r) for r in x])
+    ds = tb.Dataset(labels=[str(i) for i in range(m)], ranks=ranks)
+    n1 = np.array([int((c * (c - 1) // 2).sum()) for c in (np.unique(r, return_counts=True)[1] for r in ranks)],
+                  dtype=np.uint64)
+    space = JobSpace(m, 8)
+    plans = plan_passes(space, (0, space.total_tiles), 4096)
+    state = {"k": 0, "cells": 0, "sample": []}
+
+    def sink(rec):
+        p = plans[state["k"]]
+        assert rec.shape[0] == p.cells
+        for t, row in ((p.tile_lo, rec[0]), (p.tile_hi - 1, rec[-1])):
+            ii, jj = space.cells_in_tile_order(t, t + 1)
+            assert (int(row["i"]), int(row["j"])) in ((int(ii[0]), int(jj[0])), (int(ii[-1]), int(jj[-1])))
+        s = rec[:: 997]
+        lhs = s["numerator"].astype(np.int64)
+        rhs = n0 - s["n1"].astype(np.int64) - s["n2"].astype(np.int64) + s["n3"].astype(np.int64) - 2 * s["n_d"].astype(np.int64)
+        assert np.array_equal(lhs, rhs)
+        assert np.array_equal(s["n1"], n1[s["i"]]) and np.array_equal(s["n2"], n1[s["j"]])
+        assert (s["i"] <= s["j"]).all()
+        if state["k"] % 512 == 0:
+            state["sample"].append(s[:8].copy())
+        state["k"] += 1
+        state["cells"] += rec.shape[0]
+
+    summary = tb.compute_all_pairs(ds, "vectorized", sink=sink)
+    assert state["k"] == len(plans) and state["cells"] == m * (m + 1) // 2 == summary.total_cells
+    from paper_1704_03767_b200.device import TauEngine
+    res = TauEngine(0).all_pairs(torch.from_numpy(x).cuda(), kernel="gemm", tau_a=False, tau_b=False).validate()
+    smp = np.concatenate(state["sample"])
+    i, j = smp["i"].astype(np.int64), smp["j"].astype(np.int64)
+    jid = torch.from_numpy(i * (2 * m - i + 1) // 2 + j - i).cuda()
+    np.testing.assert_array_equal(res.numerator.index_select(0, jid).cpu().numpy().astype(np.int64),
+                                  smp["numerator"].astype(np.int64))
