@@ -41,10 +41,10 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const int32_t* __
                                                                const unsigned long long* __restrict__ n1,
                                                                int32_t m, int64_t n0, int64_t job_lo, int64_t count,
                                                                double* __restrict__ tau_a, double* __restrict__ tau_b,
-                                                               const double* __restrict__ T) {
+                                                               const double* __restrict__ T, int32_t cpt) {
     pdl_wait();
     __shared__ int32_t s_y, s_x;
-    const int64_t base = (int64_t)blockIdx.x * (FIN_THREADS * FIN_CELLS);
+    const int64_t base = (int64_t)blockIdx.x * (FIN_THREADS * cpt);
     if (threadIdx.x == 0) {
         int64_t y, x;
         job_coord(job_lo + base, m, y, x);
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const int32_t* __
     }
     __syncthreads();
     const int64_t left = count - base;
-    const int32_t nmine = left > FIN_THREADS * FIN_CELLS ? FIN_CELLS
+    const int32_t nmine = left > FIN_THREADS * cpt ? cpt
                           : (int32_t)((left - threadIdx.x + FIN_THREADS - 1) / FIN_THREADS);
     if (nmine <= 0) return;
     int32_t y = s_y, x = s_x;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const int32_t* __
     double* pb = TB ? tau_b + base + threadIdx.x : nullptr;
     constexpr int G = FIN_G;  // cells in flight: addresses first, then the loads, then the IEEE sequences
 #pragma unroll 1
-    for (int g = 0; g < FIN_CELLS; g += G) {
+    for (int g = 0; g < cpt; g += G) {
         int32_t v[G];
         unsigned long long t1[G], t2[G];
 #pragma unroll
@@ -168,7 +168,11 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     const int64_t count = job_hi - job_lo;
     if (count == 0) return TB_OK;
     if (m > INT32_MAX) return fail(TB_ERR_CAPACITY, "finalize: m too large");
-    const int64_t blocks = (count + FIN_THREADS * FIN_CELLS - 1) / (FIN_THREADS * FIN_CELLS);
+    // cells per thread: FIN_CELLS for large ranges (one decode per 4096 cells), fewer for small ones so the
+    // grid still fills the GPU (~8 blocks per SM) -- a 33K-cell range otherwise ran as 9 blocks
+    const int64_t per_cell_blocks = (int64_t)num_sms() * 8 * FIN_THREADS;
+    const int32_t cpt = (int32_t)std::max<int64_t>(1, std::min<int64_t>(FIN_CELLS, count / std::max<int64_t>(1, per_cell_blocks)));
+    const int64_t blocks = (count + FIN_THREADS * cpt - 1) / (FIN_THREADS * cpt);
     if (blocks > INT32_MAX) return fail(TB_ERR_CAPACITY, "finalize: job range too large");
     const double* T = nullptr;
     int rc = fin_table(n * (n - 1) / 2, static_cast<cudaStream_t>(stream), &T);
@@ -178,7 +182,7 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     if (!kern) return TB_OK;
     TB_CUDA_TRY(launch_pdl(kern, dim3((unsigned)blocks), dim3(FIN_THREADS), 0, static_cast<cudaStream_t>(stream), num,
                            reinterpret_cast<const unsigned long long*>(n1_rows), (int32_t)m, n * (n - 1) / 2, job_lo,
-                           count, tau_a, tau_b, T));
+                           count, tau_a, tau_b, T, cpt));
     return check_launch("finalize_kernel");
 }
 

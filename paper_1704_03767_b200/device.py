@@ -317,7 +317,7 @@ class TauEngine:
         m, n = x.shape
         st = _stream_ptr(self._stream)
         prep = Prepared(path=path, m=m, n=n, full=full_counts, simt=simt,
-                        n1_rows=torch.zeros(m, dtype=torch.int64, device=self.device),
+                        n1_rows=(torch.empty if all_rows else torch.zeros)(m, dtype=torch.int64, device=self.device),
                         flags=torch.zeros(1, dtype=torch.int32, device=self.device))
         stub = PairResult(m=m, n=n, job_lo=row_prefix(min(row_lo, m), m), job_hi=m * (m + 1) // 2, path=path,
                           numerator=None, n1_rows=prep.n1_rows, flags=prep.flags)
