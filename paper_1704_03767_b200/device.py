@@ -46,6 +46,7 @@ DISPATCH_TABLE = (
     (24576, 4.665e-05, 1.105e-06, 221, 2.675e-06, 2.904e-07),
     (32767, 8.727e-05, 4.589e-06, 124, 4.203e-06, 3.008e-07),
 )
+D2H_PIECE_BYTES = 256 << 20
 GEMM_MAX_N = 8192  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides)
 RANK_ROWS_MAX_N = 8192  # tb_rank_rows' row limit; wider GEMM-path rows are ranked by tb_rank_dense
 SIGN_MAX_N = 32767      # tb_sign_pack: 15-bit ranks
@@ -578,7 +579,12 @@ class TauEngine:
                 ev.record(st_t)
                 cp_t.wait_event(ev)
                 with torch.cuda.stream(cp_t):
-                    tau_b_out[lo - jlo:hi - jlo].copy_(tb, non_blocking=True)
+                    # D2H in 256 MiB pieces (the record pipeline's slot size: 51-56 GB/s sustained); one copy of
+                    # several GB ran at ~30 GB/s on some hosts (profiles/r02_bench_config5_final_b.json)
+                    step = D2H_PIECE_BYTES // 8
+                    for p0 in range(lo, hi, step):
+                        p1 = min(hi, p0 + step)
+                        tau_b_out[p0 - jlo:p1 - jlo].copy_(res.tau_b[p0 - jlo:p1 - jlo], non_blocking=True)
             st_t.wait_stream(cp_t)
             res.launches = _lib.load().tb_launch_count() - c0
         return res
