@@ -646,3 +646,27 @@ def test_full_counts_tie_free_shortcut(eng, oracle):
     x[7, :50] = 1.0  # ties in one row
     c = eng.all_pairs(torch.from_numpy(x).cuda(), kernel="gemm", full_counts=True).validate()
     _check_full(c, oracle, oracle.rank_matrix(x))
+
+
+@pytest.mark.parametrize("path,m,n", [("gemm", 700, 90), ("merge", 60, 3000)])
+def test_host_entry_point_job_ranges(eng, oracle, path, m, n):
+    """all_pairs_host over a rank's job range (multi-GPU e2e): tau_b of [lo, hi) lands at out[0:hi-lo] and
+    equals the device API's; tau_b_bands (the bench / gather path) over shrinking bands of the same range
+    too, with rows above the range neither ranked nor packed."""
+    from paper_1704_03767_b200.multi import balanced_job_shards, gather_band_fracs, shard_bands
+    rng = np.random.default_rng(m * n)
+    x = rng.integers(0, max(2, n // 3), (m, n)).astype(np.int32)
+    ref = eng.all_pairs(torch.from_numpy(x).cuda(), kernel=path, tau_a=False).validate().tau_b.cpu().numpy()
+    xh = torch.from_numpy(x).pin_memory()
+    for lo, hi in balanced_job_shards(3, m, path):
+        out = torch.full((hi - lo,), -7.0, dtype=torch.float64).pin_memory()
+        eng.all_pairs_host(xh, out, kernel=path, job_range=(lo, hi))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.numpy(), ref[lo:hi])
+        dout = torch.full((hi - lo,), -7.0, dtype=torch.float64, device="cuda")
+        bands = shard_bands(lo, hi, m, 3, gather_band_fracs(3))
+        seen = []
+        eng.tau_b_bands(torch.from_numpy(x).cuda(), bands, dout, kernel=path, on_band=lambda b, t: seen.append(b))
+        torch.cuda.synchronize()
+        assert seen == list(range(len(bands)))
+        np.testing.assert_array_equal(dout.cpu().numpy(), ref[lo:hi])

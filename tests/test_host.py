@@ -268,3 +268,20 @@ def test_dispatcher_cost_model(monkeypatch):
     for n, *_ in DISPATCH_TABLE:  # the model is finite and increasing in m
         c1, c2 = TauEngine.path_costs(100, n), TauEngine.path_costs(1000, n)
         assert all(0 < c1[k] < c2[k] for k in c1)
+
+
+def test_bench_helpers():
+    """bench.py's pair counting and the SURVEY 8(d) CPU subset draw."""
+    import importlib.util
+
+    import numpy as np
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for m in (1, 2, 5, 300):
+        total = m * (m + 1) // 2
+        assert bench._strict_pairs(m, 0, total) == m * (m - 1) // 2
+        assert sum(bench._strict_pairs(m, a, b) for a, b in ((0, total // 3), (total // 3, total))) == m * (m - 1) // 2
+    rows = bench.cpu_subset(5, 65536)
+    assert rows.shape == (2048,) and np.array_equal(rows, np.sort(np.random.default_rng(99).choice(65536, 2048, replace=False)))
+    assert bench.cpu_subset(2, 2048).shape == (2048,) and bench.cpu_subset(4, 1024).shape == (64,)
