@@ -433,7 +433,8 @@ static double unit_cost4(int32_t ncols) { return 0.2 + 0.8 * ncols / 480.0; }  /
 static double plan_items4(const std::vector<int32_t>& code, const std::vector<int32_t>& blocks,
                           const std::vector<int32_t>& ncols, const std::vector<int32_t>& su, int32_t nkb, int pairs,
                           std::vector<int4>* out) {
-    const double t_epi = 100.0;  // per item: epilogue ~20 us + split-red contention + refill (fitted to
+    static const double kEpi = [] { const char* e = std::getenv("TB_PLAN_EPI"); return e ? atof(e) : 100.0; }();
+    const double t_epi = kEpi;  // per item: epilogue ~20 us + split-red contention + refill (fitted to
                                  // measured 1- vs 2-wave plans on config 2), in two-block k-blocks
     std::vector<double> load(pairs, 0.0);
     const int32_t rounds = *std::max_element(su.begin(), su.end());
