@@ -498,6 +498,21 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
             int64_t nitems = 0;
             for (int32_t v : best_su) nitems += v;
             su = best_su;
+            // one wave with the same split count for every unit: every round's items cover the same K range,
+            // so the concurrent pairs share S k-blocks through L2 (which the makespan model does not see);
+            // preferred on a tie (config 2: 390 us for 3 uniform splits vs 405 us for the model's best plan,
+            // tools/exp_splits.py, profiles/r02_gemm_split_plans.log)
+            if ((int64_t)code.size() <= pairs) {
+                const int32_t s_uni = (int32_t)std::max<int64_t>(1, std::min<int64_t>(nkb, pairs / (int64_t)code.size()));
+                std::vector<int32_t> uni(code.size(), s_uni);
+                const double t = plan_items4(code, nb, ncols, uni, nkb, pairs, nullptr);
+                if (t <= best * 1.0001) {
+                    best = t;
+                    best_su = uni;
+                    su = uni;
+                    nitems = (int64_t)code.size() * s_uni;
+                }
+            }
             while (nitems < pairs) {
                 size_t arg = 0;
                 double worst = -1.0;
