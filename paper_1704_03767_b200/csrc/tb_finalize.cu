@@ -256,6 +256,13 @@ __global__ void __launch_bounds__(256) accum_convert_kernel(float* __restrict__ 
     pdl_trigger();
 }
 
+int accum_mark_clean() {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);
+    if (dev >= 0 && dev < TB_MAX_DEVICES) g_accum[dev].dirty = false;
+    return TB_OK;
+}
+
 int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st) {
     if (span <= 0) return TB_OK;
     const int64_t blocks = std::min<int64_t>((span + 255) / 256, (int64_t)num_sms() * 8);

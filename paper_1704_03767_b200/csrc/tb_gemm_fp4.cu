@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 #include <cudaTypedefs.h>
 
@@ -63,6 +64,12 @@ struct Gemm4Args {
     uint32_t epoch;
     int32_t lead;
     int32_t lagq;  // pairs allowed to lag more than `lead` behind before a pair waits
+    // split-K fixup in the kernel (partial plans): item i belongs to unit item_unit[i], unit u has
+    // unit_splits[u] items; unit_cnt[2 u + rank] counts the finished items of each CTA half, and the last
+    // one converts that half's f32 sums to int32 numerators and re-zeroes them (no accum_convert launch)
+    const int32_t* item_unit;
+    const int32_t* unit_splits;
+    int32_t* unit_cnt;
 };
 
 // ---- K-lockstep throttle.  The ~74 concurrently running CTA pairs stream the same S rows (units of one
@@ -346,6 +353,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             if (p.trace && warp == 4 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2 + 1] = globaltimer();
             if (lane == 0) mbar_arrive_cluster(tempty_leader);
             acc_phase ^= 1;
+            if (t.partial && p.unit_cnt) {
+                // this CTA half's reds of the item are issued; the last of the unit's items converts the half
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+                volatile int* s_last = reinterpret_cast<volatile int*>(smem + STAGES * STAGE_BYTES + 128);
+                if (warp == 4 && lane == 0) {
+                    const int32_t u = __ldg(&p.item_unit[cur - npairs]);
+                    int32_t* cnt = p.unit_cnt + 2 * u + rank;
+                    const int old = atomicAdd(cnt, 1);
+                    const int last = old == __ldg(&p.unit_splits[u]) - 1;
+                    if (last) {
+                        *cnt = 0;  // ready for the next launch
+                        __threadfence();
+                    }
+                    *s_last = last;
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+                if (*s_last) {
+                    // rows y0 + rank * BM + [0, BM) of the unit: warp w takes rows w - 4, w + 12, ...
+                    for (int rr = warp - 4; rr < BM; rr += EPI_WARPS) {
+                        const int64_t y = t.y0 + rank * BM + rr;
+                        if (y >= m) break;
+                        const int64_t rj0 = row_prefix(y, m) - y - p.job_lo;
+                        for (int h = 0; h < t.nblk; ++h) {
+                            int64_t x_lo = t.xs[h], x_hi = t.xs[h] + t.nb[h];
+                            if (x_lo < y) x_lo = y;
+                            if (x_hi > m) x_hi = m;
+                            if (x_lo < -rj0) x_lo = -rj0;
+                            if (x_hi > span - rj0) x_hi = span - rj0;
+                            for (int64_t x = x_lo + lane; x < x_hi; x += 32) {
+                                const int64_t j = rj0 + x;
+                                p.num[j] = __float2int_rn(__ldcg(&p.acc[j]));
+                                p.acc[j] = 0.0f;
+                            }
+                        }
+                    }
+                }
+            }
         }
     }
     pdl_trigger();
@@ -372,7 +417,10 @@ struct Plan4 {
     int32_t nkb = -1, forced = -1, pairs = -1;
     int64_t count = 0;
     int32_t partial = 0;
+    int64_t off_unit = -1, off_splits = -1, off_cnt = -1;  // byte offsets of the split-K fixup arrays
     const int4* dev() const { return static_cast<const int4*>(table.dev); }
+    template <typename T>
+    T* at(int64_t off) const { return off < 0 ? nullptr : reinterpret_cast<T*>(static_cast<uint8_t*>(table.dev) + off); }
 };
 // Plans are cached per (geometry, job range): the banded host path cycles through a few ranges.
 constexpr int PLAN_CACHE = 32;  // the banded host path cycles through up to ~15 job ranges
@@ -432,7 +480,7 @@ static double unit_cost4(int32_t ncols) { return 0.2 + 0.8 * ncols / 480.0; }  /
 // (items split-round-major, pair p runs p, p + P, ...), in two-block k-block units.
 static double plan_items4(const std::vector<int32_t>& code, const std::vector<int32_t>& blocks,
                           const std::vector<int32_t>& ncols, const std::vector<int32_t>& su, int32_t nkb, int pairs,
-                          std::vector<int4>* out) {
+                          std::vector<int4>* out, std::vector<int32_t>* out_unit = nullptr) {
     static const double kEpi = [] { const char* e = std::getenv("TB_PLAN_EPI"); return e ? atof(e) : 100.0; }();
     const double t_epi = kEpi;  // per item: epilogue ~20 us + split-red contention + refill (fitted to
                                  // measured 1- vs 2-wave plans on config 2), in two-block k-blocks
@@ -445,6 +493,7 @@ static double plan_items4(const std::vector<int32_t>& code, const std::vector<in
             const int32_t kb0 = (int32_t)((int64_t)r * nkb / su[u]), kb1 = (int32_t)((int64_t)(r + 1) * nkb / su[u]);
             load[idx % pairs] += (kb1 - kb0) * unit_cost4(ncols[u]) + t_epi;
             if (out) out->push_back(make_int4(code[u], kb0, kb1, blocks[u]));
+            if (out_unit) out_unit->push_back((int32_t)u);
             ++idx;
         }
     return *std::max_element(load.begin(), load.end());
@@ -529,13 +578,29 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
         }
     }
     std::vector<int4> items;
-    const double span_est = code.empty() ? 0.0 : plan_items4(code, nb, ncols, best_su, nkb, pairs, &items);
+    std::vector<int32_t> item_unit;
+    const double span_est = code.empty() ? 0.0 : plan_items4(code, nb, ncols, best_su, nkb, pairs, &items, &item_unit);
     const int32_t smax = best_su.empty() ? 1 : *std::max_element(best_su.begin(), best_su.end());
     const char* trace = std::getenv("TB_TRACE");
     if (trace && trace[0] == '1')
         fprintf(stderr, "plan4: m %lld units %zu nkb %d max splits %d items %zu est %.0f\n", (long long)m,
                 code.size(), nkb, smax, items.size(), span_est);
-    int rc = table_upload(g_plan4.table, items.data(), items.size() * sizeof(int4), st);
+    // table: items (int4), then for split plans the item -> unit map, the splits per unit and the per-unit,
+    // per-CTA-half fixup counters (zero; each launch's last arrivers reset them)
+    std::vector<uint8_t> blob(items.size() * sizeof(int4));
+    if (!items.empty()) std::memcpy(blob.data(), items.data(), blob.size());
+    if (smax > 1) {
+        const size_t off_u = blob.size(), nu = best_su.size();
+        blob.resize(off_u + (item_unit.size() + nu + 2 * nu) * sizeof(int32_t), 0);
+        std::memcpy(blob.data() + off_u, item_unit.data(), item_unit.size() * sizeof(int32_t));
+        std::memcpy(blob.data() + off_u + item_unit.size() * sizeof(int32_t), best_su.data(), nu * sizeof(int32_t));
+        g_plan4.off_unit = (int64_t)off_u;
+        g_plan4.off_splits = (int64_t)(off_u + item_unit.size() * sizeof(int32_t));
+        g_plan4.off_cnt = (int64_t)(off_u + (item_unit.size() + nu) * sizeof(int32_t));
+    } else {
+        g_plan4.off_unit = g_plan4.off_splits = g_plan4.off_cnt = -1;
+    }
+    int rc = table_upload(g_plan4.table, blob.data(), blob.size(), st);
     if (rc) return rc;
     g_plan4.m = m;
     g_plan4.lo = job_lo;
@@ -597,6 +662,12 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.job_hi = job_hi;
     p.num = num;
     if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
+    static const bool kNoFixup = [] { const char* e = std::getenv("TB_GEMM_NO_FIXUP"); return e && e[0] == '1'; }();
+    if (p.partial && !kNoFixup) {
+        p.item_unit = plan->at<const int32_t>(plan->off_unit);
+        p.unit_splits = plan->at<const int32_t>(plan->off_splits);
+        p.unit_cnt = plan->at<int32_t>(plan->off_cnt);
+    }
     if ((rc = lockstep_state(&p.prog, &p.epoch, &p.lead))) return rc;
     {
         static const int32_t kLagQ = [] { const char* e = std::getenv("TB_GEMM_LAGQ"); return e ? std::max(0, atoi(e)) : 0; }();
@@ -646,7 +717,9 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
             }
         }
     }
-    return p.partial ? accum_convert(p.acc, job_hi - job_lo, num, st) : TB_OK;
+    if (!p.partial) return TB_OK;
+    if (p.unit_cnt) return accum_mark_clean();  // the kernel converted and re-zeroed every unit's sums
+    return accum_convert(p.acc, job_hi - job_lo, num, st);
 }
 
 }  // namespace tb
