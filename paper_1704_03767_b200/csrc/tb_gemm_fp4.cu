@@ -355,12 +355,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             acc_phase ^= 1;
             if (t.partial && p.unit_cnt) {
                 // this CTA half's reds of the item are issued; the last of the unit's items converts the half
-                __threadfence();
+                // (CUTLASS's barrier pattern: CTA barrier, then one thread fences and arrives)
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
                 volatile int* s_last = reinterpret_cast<volatile int*>(smem + STAGES * STAGE_BYTES + 128);
                 if (warp == 4 && lane == 0) {
                     const int32_t u = __ldg(&p.item_unit[cur - npairs]);
                     int32_t* cnt = p.unit_cnt + 2 * u + rank;
+                    __threadfence();
                     const int old = atomicAdd(cnt, 1);
                     const int last = old == __ldg(&p.unit_splits[u]) - 1;
                     if (last) {
@@ -382,10 +383,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                             if (x_hi > m) x_hi = m;
                             if (x_lo < -rj0) x_lo = -rj0;
                             if (x_hi > span - rj0) x_hi = span - rj0;
-                            for (int64_t x = x_lo + lane; x < x_hi; x += 32) {
-                                const int64_t j = rj0 + x;
-                                p.num[j] = __float2int_rn(__ldcg(&p.acc[j]));
-                                p.acc[j] = 0.0f;
+                            // up to 8 loads in flight per lane (one row block: <= 240 columns)
+                            float v[8];
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                const int64_t x = x_lo + lane + 32 * k;
+                                v[k] = x < x_hi ? __ldcg(&p.acc[rj0 + x]) : 0.0f;
+                            }
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                const int64_t x = x_lo + lane + 32 * k;
+                                if (x < x_hi) {
+                                    p.num[rj0 + x] = __float2int_rn(v[k]);
+                                    p.acc[rj0 + x] = 0.0f;
+                                }
                             }
                         }
                     }
