@@ -673,8 +673,11 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.job_hi = job_hi;
     p.num = num;
     if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
-    static const bool kNoFixup = [] { const char* e = std::getenv("TB_GEMM_NO_FIXUP"); return e && e[0] == '1'; }();
-    if (p.partial && !kNoFixup) {
+    // In-kernel split-K fixup: opt-in (TB_GEMM_FIXUP=1).  Measured slower than the separate accum_convert
+    // launch on configs 1-2 (config 1 0.039 -> 0.051 ms, config 2 0.540 -> 0.553 ms per step; config 3 within
+    // noise; profiles/r02_gemm_fixup_ab.log): the last item of a unit serialises the conversion behind it.
+    static const bool kFixup = [] { const char* e = std::getenv("TB_GEMM_FIXUP"); return e && e[0] == '1'; }();
+    if (p.partial && kFixup) {
         p.item_unit = plan->at<const int32_t>(plan->off_unit);
         p.unit_splits = plan->at<const int32_t>(plan->off_splits);
         p.unit_cnt = plan->at<int32_t>(plan->off_cnt);
