@@ -270,9 +270,11 @@ __device__ uint32_t sort_count_block(uint16_t* keys, uint16_t* tmp, int L) {
 // (E/2) t, so their padded indices are swp_words((E/2) t) + q: one base per thread.
 template <int E>
 __device__ __forceinline__ const uint32_t* run_words(const uint16_t* keys, int t) {
-    static_assert(E / 2 <= PB / 2, "one swizzle row per thread");
+    static_assert(E / 2 <= PB / 2 || (E / 2) % (PB / 2) == 0, "whole swizzle rows per thread");
     return reinterpret_cast<const uint32_t*>(keys) + swp_words((E / 2) * t);
 }
+// padded offset of the thread's word q from run_words (E = 64 spans two swizzle rows: one pad word between)
+__device__ __forceinline__ constexpr int run_word_off(int q) { return q + q / (PB / 2); }
 template <int E>
 __device__ __forceinline__ void load_run(const uint16_t* keys, int t, uint32_t (&v)[E]) {
     const uint32_t* wk = run_words<E>(keys, t);
@@ -287,7 +289,7 @@ template <int E>
 __device__ __forceinline__ void store_words(uint16_t* keys, int t, const uint32_t (&ow)[E / 2]) {
     uint32_t* wk = const_cast<uint32_t*>(run_words<E>(keys, t));
 #pragma unroll
-    for (int q = 0; q < E / 2; ++q) wk[q] = ow[q];
+    for (int q = 0; q < E / 2; ++q) wk[run_word_off(q)] = ow[q];
 }
 template <int E>
 __device__ __forceinline__ void store_run(uint16_t* keys, int t, const uint32_t (&v)[E]) {
@@ -304,6 +306,17 @@ __device__ __forceinline__ void store_lookahead(uint16_t* keys, int t, int R, ui
     if ((k0 & (PB - 1)) == 0 && k0 > 0) {
         uint32_t* wk = reinterpret_cast<uint32_t*>(keys) + swp_words(k0 >> 1) - 1;
         *wk = (k0 & (R - 1)) == 0 ? 0xFFFFFFFFu : (first | 0xFFFF0000u);
+    }
+}
+// E = 64 segments span two 32-key blocks: both pad words in front of them (first keys from the output words)
+template <int E>
+__device__ __forceinline__ void store_lookaheads(uint16_t* keys, int t, int R, const uint32_t (&ow)[E / 2]) {
+    store_lookahead<E>(keys, t, R, ow[0] & 0xFFFFu);
+#pragma unroll
+    for (int b = 1; b < E / PB; ++b) {
+        const int k0 = E * t + PB * b;
+        uint32_t* wk = reinterpret_cast<uint32_t*>(keys) + swp_words(k0 >> 1) - 1;
+        *wk = (k0 & (R - 1)) == 0 ? 0xFFFFFFFFu : ((ow[PB / 2 * b] & 0xFFFFu) | 0xFFFF0000u);
     }
 }
 
@@ -478,8 +491,8 @@ __device__ __forceinline__ int mp_search(uint32_t baseA, uint32_t baseB, int d, 
 // each issues one warp instruction per 2 cycles per SMSP), so the cursor and address arithmetic is
 // written as IMADs with opaque multipliers to split the step between the two pipes.
 template <int E, bool CHECKED>
-__device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_t* dst, int t, int W,
-                                                    const MgConst& K) {
+__device__ __forceinline__ uint32_t merge_level_regs(const uint16_t* src, int t, int W, const MgConst& K,
+                                                     uint32_t (&ow)[E / 2]) {
     const int d0 = t * E;
     const int P = 2 * W;
     const int s = d0 & ~(P - 1);
@@ -494,7 +507,6 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
     uint32_t h1 = ia < sW ? ((uint32_t)src[sw((int)ia)] << 16) : INF;
     uint32_t h2 = ib < sW + (uint32_t)W ? (((uint32_t)src[sw((int)ib)] << 16) | 1u) : INF;
     uint32_t Y = 0, prev = 0;
-    uint32_t ow[E / 2];
 #pragma unroll
     for (int o = 0; o < E; ++o) {
         const uint32_t cm = min(h1, h2);
@@ -538,9 +550,27 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
         if (o & 1) ow[o >> 1] = __byte_perm(prev, cm, 0x7632);  // the two keys (high halves)
         else prev = cm;
     }
-    store_words<E>(dst, t, ow);
-    store_lookahead<E>(dst, t, 2 * W, ow[0]);
     return (ib - ib0) * sW - Y;
+}
+template <int E, bool CHECKED>
+__device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_t* dst, int t, int W,
+                                                    const MgConst& K) {
+    uint32_t ow[E / 2];
+    const uint32_t inv = merge_level_regs<E, CHECKED>(src, t, W, K, ow);
+    store_words<E>(dst, t, ow);
+    store_lookaheads<E>(dst, t, 2 * W, ow);
+    return inv;
+}
+// In place: every thread's outputs stay in registers until all threads have read the level's runs.
+template <int E>
+__device__ __forceinline__ uint32_t merge_level_inplace(uint16_t* blk, int t, int W, const MgConst& K) {
+    uint32_t ow[E / 2];
+    const uint32_t inv = merge_level_regs<E, false>(blk, t, W, K, ow);
+    __syncthreads();
+    store_words<E>(blk, t, ow);
+    store_lookaheads<E>(blk, t, 2 * W, ow);
+    __syncthreads();
+    return inv;
 }
 
 template <int E>
@@ -581,6 +611,32 @@ __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, co
         }
         __syncthreads();
     }
+    return inv;
+}
+
+// n > 32768: both 32768-key halves.  Leaf: all threads, one half after the other (32 keys each).  Merge
+// levels: threads [0, 512) merge half 0 and [512, 1024) half 1 concurrently, EM = 64 outputs each, in place
+// (no ping-pong buffer): the merge-path search runs once per 64 outputs instead of once per 32.
+template <int EM>
+__device__ uint32_t sort_count_halves(uint16_t* keys, int L, const MgConst& K) {
+    constexpr int E = 32;
+    static_assert(EM * MG_THREADS == 2 * MG_HALF, "two halves of EM * 512 keys");
+    const int tid = threadIdx.x;
+    uint32_t inv = 0;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        uint16_t* blk = keys + h * sw(L);
+        uint32_t v[E];
+        load_run<E>(blk, tid, v);
+        inv += reg_sort_count<E, LEAF_XL<E>>(v);
+        store_run<E>(blk, tid, v);
+        store_lookahead<E>(blk, tid, E << LEAF_XL<E>, v[0]);
+    }
+    __syncthreads();
+    uint16_t* blk = keys + (tid >> 9) * sw(L);
+    const int t = tid & (MG_THREADS / 2 - 1);
+#pragma unroll 1
+    for (int W = E << LEAF_XL<E>; W < L; W <<= 1) inv += merge_level_inplace<EM>(blk, t, W, K);
     return inv;
 }
 
@@ -744,7 +800,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
     pdl_wait();
     extern __shared__ __align__(16) uint8_t mg_smem[];
     uint16_t* keys = reinterpret_cast<uint16_t*>(mg_smem);  // B * L keys (padded layout)
-    uint16_t* tmp = keys + sw(p.B * p.L) + 2;               // L keys (padded layout)
+    uint16_t* tmp = keys + sw(p.B * p.L) + 2;               // L keys (padded layout; B == 1 only)
     __shared__ int64_t red[32];
     const int tid = threadIdx.x;
     const int64_t n = p.n;
@@ -754,7 +810,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
     __shared__ int sX, sY;  // u-order positions of keys 0xFFFF / 0xFFFE (n = 65536 only)
     if (tid == 0 && L >= 64) {  // INF look-ahead slots behind the last block of every sorted region
         reinterpret_cast<uint32_t*>(keys)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
-        reinterpret_cast<uint32_t*>(tmp)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
+        if (p.B == 1) reinterpret_cast<uint32_t*>(tmp)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
         if (p.B == 2) reinterpret_cast<uint32_t*>(keys + sw(L))[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
     }
 
@@ -833,10 +889,12 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         }
 
         // inv(w)
-        uint32_t inv = sort_count_any(keys, tmp, L, K);
+        uint32_t inv;
         int64_t cross = 0;
-        if (p.B == 2) {
-            inv += sort_count_any(keys + sw(L), tmp, L, K);  // L = 32768: sw(L + i) = sw(L) + sw(i)
+        if (p.B == 1) {
+            inv = sort_count_any(keys, tmp, L, K);
+        } else {
+            inv = sort_count_halves<2 * MG_HALF / MG_THREADS>(keys, L, K);  // L = 32768: sw(L + i) = sw(L) + sw(i)
             // cross(H1, H2) = sum key(H1) - L1 (L1 - 1) / 2 + ties(H1) (header); the -L1 (L1 - 1) / 2
             // is applied once after the reduction.  H1 = keys[0, L) is sorted and holds no pads.
             constexpr int CE = MG_HALF / MG_THREADS;  // 32 sorted keys per thread
@@ -942,7 +1000,9 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
     a.num = num;
     a.nd = reinterpret_cast<unsigned long long*>(nd);
     a.n3 = reinterpret_cast<unsigned long long*>(n3);
-    const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> PBS) + 2 + L + 2 * ((size_t)L >> PBS) + 2;
+    // B == 2 merges in place (no ping-pong block)
+    const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> PBS) + 2 +
+                          (a.B == 1 ? L + 2 * ((size_t)L >> PBS) + 2 : 0);
     size_t smem = padded * sizeof(uint16_t);
     a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u, 2u * (PB + 2), (uint32_t)(-2 * (PB + 2))};
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
