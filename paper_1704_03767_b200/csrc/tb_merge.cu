@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(256) tie_groups_kernel(const int32_t* __restri
 constexpr int MG_THREADS = 1024;
 constexpr int MG_SMALL_GROUP = 64;  // tie groups up to this size: one thread per group
 constexpr int MG_HALF = 32768;  // largest block sorted in shared memory
-#ifndef MG_PAD_SHIFT  // pad-block size 2^MG_PAD_SHIFT keys (config 4: 32 -> 310 ms, 64 -> 313 ms)
-#define MG_PAD_SHIFT 5
+#ifndef MG_PAD_SHIFT  // pad-block size 2^MG_PAD_SHIFT keys (config 4 with 64-output in-place merges: 32 -> 292.6 ms,
+#define MG_PAD_SHIFT 6  // 64 -> 278 ms kernel: a 64-output segment is one padded block, 33-word stride, no store conflicts)
 #endif
 
 // Shared-memory key layout: 2 pad keys (one 32-bit word) after every 32 keys.  The pad word in front
@@ -417,16 +417,14 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
         // this lane's share of inv(A, B), h = 16 << l: B = tag bit 4 + l; positions 32 gl + i.  Lanes other
         // than the block's first add only -pos: a thread's total can be negative (the kernel reduces it as
         // int32; the block total is exact)
+        // one IMAD per key: sum (i + 512) [B] = sum_B i + 512 nbv (sum_B i <= 496), nbv = B keys in this lane
         const uint32_t hb = 16u << l, tb = 1u << (4 + l);
-        uint32_t pos = 0;
+        uint32_t acc = 0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) pos += (v[i] & tb) * (uint32_t)i;
-        pos /= tb;
-        uint32_t nbv = 0;  // B elements held by this lane
-#pragma unroll
-        for (int i = 0; i < 32; ++i) nbv += (v[i] & tb);
-        nbv /= tb;
-        pos += 32u * gl * nbv;
+        for (int i = 0; i < 32; ++i) acc += (v[i] & tb) * (uint32_t)(i + 512);
+        acc /= tb;
+        const uint32_t nbv = acc >> 9;
+        uint32_t pos = (acc & 511u) + 32u * gl * nbv;
         inv += (gl == 0 ? hb * hb + hb * (hb - 1) / 2 : 0u) - pos;
     }
 #pragma unroll
@@ -573,10 +571,12 @@ __device__ __forceinline__ uint32_t merge_level_inplace(uint16_t* blk, int t, in
     return inv;
 }
 
+#ifndef MG_LEAF_XL  // cross-lane leaf levels for E = 32 (round-1 kernel on config 4: 1 -> 319.5 ms, 2 -> 315.5 ms,
+#define MG_LEAF_XL 2  // 3 -> 328.5 ms)
+#endif
 template <int E>
-// register leaf: 32 keys per lane, 128 across 4 lanes (cross-lane levels measured on config 4:
-// 1 -> 319.5 ms, 2 -> 315.5 ms, 3 -> 328.5 ms)
-constexpr int LEAF_XL = E == 32 ? 2 : 0;
+// register leaf: 32 keys per lane, 32 << MG_LEAF_XL across 2^MG_LEAF_XL lanes
+constexpr int LEAF_XL = E == 32 ? MG_LEAF_XL : 0;
 
 template <int E>
 __device__ uint32_t sort_count_block_v2(uint16_t* keys, uint16_t* tmp, int L, const MgConst& K) {
