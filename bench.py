@@ -477,12 +477,14 @@ def run_ours(args):
         pairs_pl = _strict_pairs(m, 0, total_jobs)  # all shards together cover every pair once
         e2e = {"value": pairs_pl * len(ts) / t_pl, "unit": UNIT,
                "h2d_bytes_per_step": int(ds.ranks.nbytes) * world,
-               "d2h_bytes_per_step": int(m * (m + 1) // 2 * 48),
+               "d2h_bytes_per_step": int(summary.d2h_bytes) * world,
+               "records_bytes_per_step": int(m * (m + 1) // 2 * 48),
                "ms_per_step": 1e3 * t_pl / len(ts), "steps": len(ts),
                "api": ("compute_all_pairs(ds, 'vectorized', sink=...) -- the reference's plugin call "
                        "(engine.py:300-310): H2D of the int32 ranks, every count on the device, 48-byte "
-                       "CELL_DTYPE records (diagonal included) D2H into pinned pass buffers, delivered to a host "
-                       "sink pass by pass; wall clock" + (f"; rank r runs shard=(r, {world})" if world > 1 else "")),
+                       "CELL_DTYPE records (diagonal included) delivered to a host sink pass by pass -- one batch "
+                       f"in {tb.engine.FULL_EVERY} copied as full records, the others as the 8-byte (numerator, n3) stream "
+                       "expanded into the same bytes by host threads (tb_expand_records); wall clock" + (f"; rank r runs shard=(r, {world})" if world > 1 else "")),
                "timer": "wall clock around the synchronous host call"}
         del ds
 

@@ -147,6 +147,14 @@ int tb_abs_pack(const int8_t *S, int64_t m, int64_t ldS, int format, int8_t *A, 
 int tb_full_counts(const int32_t *num, const int32_t *absdot, const uint64_t *n1_rows, int64_t m, int64_t n,
                    int64_t job_lo, int64_t job_hi, uint64_t *nd, uint64_t *n3, void *stream);
 
+/* Sparse full counts: after tb_full_counts' closed form (absdot NULL), overwrite n_d / n3 of the pairs of
+ * two tied variables from the |S| GEMM over the tied rows only (absdot_t: job-id order of the nt tied rows
+ * rows_t, ascending).  Processes tied job ids [tj_lo, tj_hi); pairs outside [job_lo, job_hi) are skipped.
+ * n3 is zero for every pair with an untied variable, so this equals the full |S| GEMM path. */
+int tb_tied_counts(const int32_t *absdot_t, const int32_t *rows_t, int64_t nt, const uint64_t *n1_rows, int64_t m,
+                   int64_t n, int64_t job_lo, int64_t job_hi, int64_t tj_lo, int64_t tj_hi, const int32_t *num,
+                   uint64_t *nd, uint64_t *n3, void *stream);
+
 /*
  * Reference record stream: the 48-byte CELL_DTYPE records (src/taucorr/engine.py:45-55:
  * i, j, numerator, n_d, n1, n2, n3) of tiles [tile_lo, tile_lo + ntiles) of the q x q tile matrix in the
@@ -160,6 +168,23 @@ int tb_full_counts(const int32_t *num, const int32_t *absdot, const uint64_t *n1
 int tb_records(const int32_t *num, const int64_t *nd, const int64_t *n3, const int64_t *n1_rows, int64_t m,
                int64_t q, int64_t job_lo, int64_t job_hi, int64_t tile_lo, int64_t ntiles, int naive, void *records,
                void *stream);
+
+/*
+ * Compact record stream: the records of tb_records as 8 bytes each -- (int32 numerator, uint32 n3) in the
+ * same emission order -- for passes whose records are rebuilt on the host by tb_expand_records (PCIe
+ * carries 1/6 of the bytes).  Same arguments and checks as tb_records; naive != 0 writes n3 = 0.
+ */
+int tb_records_compact(const int32_t *num, const int64_t *n3, int64_t m, int64_t q, int64_t job_lo, int64_t job_hi,
+                       int64_t tile_lo, int64_t ntiles, int naive, void *compact, void *stream);
+
+/*
+ * Host-only: expand the compact stream of tiles [tile_lo, tile_lo + ntiles) into the 48-byte CELL_DTYPE
+ * records tb_records would have written (byte-identical): i, j from the tile order, n1 = n1_rows[i],
+ * n2 = n1_rows[j] (host array), n_d = (n0 - n1 - n2 + n3 - numerator) / 2 (result.py:42), n0 = n(n-1)/2.
+ * records must be 16-byte aligned; nthreads host threads with streaming stores.  No device work.
+ */
+int tb_expand_records(const void *compact, const uint64_t *n1_rows, int64_t m, int64_t n, int64_t q,
+                      int64_t tile_lo, int64_t ntiles, int naive, void *records, int nthreads);
 
 /* Cells (records) in tiles [tile_lo, tile_hi) of the q x q tile matrix over m variables, diagonal
  * included -- the sum of tile_cell_count (pairindex.py:107-112) in closed form; -1 on bad arguments.

@@ -95,6 +95,17 @@ __host__ __device__ __forceinline__ void job_coord(int64_t j, int64_t m, int64_t
     x = j + yy - row_prefix(yy, m);
 }
 
+// Records before tile t of the q x q tile matrix (w tile rows; emission order of pairindex.py:116-129):
+//   row_prefix(ty q) + [tx > ty] sum_{i in tile rows} (tx q - i)
+__host__ __device__ __forceinline__ int64_t cells_before_tile(int64_t t, int64_t m, int64_t q, int64_t w) {
+    int64_t ty, tx;
+    job_coord(t, w, ty, tx);
+    const int64_t r0 = ty * q, s = (r0 + q < m ? r0 + q : m) - r0;
+    int64_t c = row_prefix(r0, m);
+    if (tx > ty) c += s * tx * q - (s * r0 + s * (s - 1) / 2);
+    return c;
+}
+
 // Sample-pair enumeration for the sign vector: k(a, b) = a*n - a(a+1)/2 + (b - a - 1), a < b.
 __host__ __device__ __forceinline__ int64_t seg_offset(int64_t a, int64_t n) { return a * n - a * (a + 1) / 2; }
 

@@ -1,0 +1,83 @@
+// Host side of the compact record stream (tb_records_compact): expands (numerator, n3) pairs into the
+// reference's 48-byte CELL_DTYPE records (engine.py:45-55) in emission order (pairindex.py:116-129), on
+// host threads with streaming stores.  compute_all_pairs runs it for some passes while the copy engine
+// streams full records for the others, so a pass reaches the sink over two paths at once: PCIe carries
+// 8 bytes per record instead of 48 for the expanded ones.
+#include <algorithm>
+#include <cstdint>
+#include <thread>
+#include <vector>
+#include <emmintrin.h>
+
+#include "tb_common.cuh"
+
+namespace tb {
+
+// Records of tiles [t0, t1) (record offsets relative to the pass's first tile base0).
+static void expand_tiles(const uint2* cmp, const uint64_t* n1, int64_t m, int64_t n0, int64_t q, int64_t w,
+                         int64_t t0, int64_t t1, int64_t base0, int naive, uint8_t* out) {
+    int64_t pos = cells_before_tile(t0, m, q, w) - base0;
+    int64_t ty, tx;
+    job_coord(t0, w, ty, tx);
+    for (int64_t t = t0; t < t1; ++t) {
+        const int64_t r0 = ty * q, c0 = tx * q;
+        const int64_t r1 = std::min(r0 + q, m), c1 = std::min(c0 + q, m);
+        for (int64_t i = r0; i < r1; ++i) {
+            const int64_t jb = std::max(i, c0);
+            const uint64_t n1i = naive ? 0 : n1[i];
+            for (int64_t j = jb; j < c1; ++j, ++pos) {
+                const uint2 v = cmp[pos];
+                const int64_t num = (int32_t)v.x;
+                uint64_t nd = 0, n2 = 0, n3 = 0, n1v = 0;
+                if (!naive) {
+                    n1v = n1i;
+                    n2 = n1[j];
+                    n3 = v.y;
+                    nd = (uint64_t)(((int64_t)n0 - (int64_t)n1v - (int64_t)n2 + (int64_t)n3 - num) / 2);
+                }
+                __m128i* r = reinterpret_cast<__m128i*>(out + 48 * pos);
+                _mm_stream_si128(r, _mm_set_epi64x(num, (int64_t)((uint64_t)(uint32_t)i | ((uint64_t)(uint32_t)j << 32))));
+                _mm_stream_si128(r + 1, _mm_set_epi64x((int64_t)n1v, (int64_t)nd));
+                _mm_stream_si128(r + 2, _mm_set_epi64x((int64_t)n3, (int64_t)n2));
+            }
+        }
+        // next tile in id order: along the tile row, then the next row's diagonal tile
+        if (++tx >= w) {
+            ++ty;
+            tx = ty;
+        }
+    }
+    _mm_sfence();  // streaming stores are weakly ordered: drain them before the thread reports done
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" int tb_expand_records(const void* compact, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t q,
+                                 int64_t tile_lo, int64_t ntiles, int naive, void* records, int nthreads) {
+    if (m < 1 || q < 1 || n < 1) return fail(TB_ERR_CONFIG, "expand_records: need m, q, n >= 1");
+    const int64_t w = (m + q - 1) / q, tt = w * (w + 1) / 2;
+    if (ntiles < 0 || tile_lo < 0 || tile_lo + ntiles > tt) return fail(TB_ERR_CONFIG, "expand_records: bad tile range");
+    if (ntiles == 0) return TB_OK;
+    if (!compact || !records || (!naive && !n1_rows)) return fail(TB_ERR_INVALID, "expand_records: null pointer");
+    if ((reinterpret_cast<uintptr_t>(records) & 15) != 0) return fail(TB_ERR_INVALID, "expand_records: records not 16-byte aligned");
+    const int64_t n0 = n * (n - 1) / 2;
+    const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
+    const uint2* cmp = static_cast<const uint2*>(compact);
+    uint8_t* out = static_cast<uint8_t*>(records);
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads, ntiles));
+    if (nt == 1) {
+        expand_tiles(cmp, n1_rows, m, n0, q, w, tile_lo, tile_lo + ntiles, base0, naive, out);
+    } else {
+        std::vector<std::thread> th;
+        th.reserve(nt);
+        for (int k = 0; k < nt; ++k) {
+            const int64_t a = tile_lo + ntiles * k / nt, b = tile_lo + ntiles * (k + 1) / nt;
+            th.emplace_back(expand_tiles, cmp, n1_rows, m, n0, q, w, a, b, base0, naive, out);
+        }
+        for (auto& t : th) t.join();
+    }
+    _mm_sfence();
+    return TB_OK;
+}

@@ -207,6 +207,30 @@ __global__ void __launch_bounds__(256) full_counts_kernel(const int32_t* __restr
     }
     pdl_trigger();
 }
+// n_d / n3 of the pairs of two TIED variables (both n1 > 0) from the |S| GEMM over the tied rows only: every
+// other pair has n3 = 0 exactly (n3 counts sample pairs tied in both variables), which tb_full_counts' closed
+// form already wrote.  absdot_t is in the tied rows' own job-id order (t = (a, b), a <= b indexes rows_t).
+__global__ void __launch_bounds__(256) tied_counts_kernel(const int32_t* __restrict__ absdot_t,
+                                                          const int32_t* __restrict__ rows_t, int64_t nt,
+                                                          const unsigned long long* __restrict__ n1, int64_t m,
+                                                          int64_t n0, int64_t job_lo, int64_t job_hi, int64_t tj_lo,
+                                                          int64_t count, const int32_t* __restrict__ num,
+                                                          unsigned long long* __restrict__ nd,
+                                                          unsigned long long* __restrict__ n3) {
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a, b;
+        job_coord(tj_lo + i, nt, a, b);
+        const int64_t y = rows_t[a], x = rows_t[b];
+        const int64_t jid = row_prefix(y, m) + x - y;
+        if (jid < job_lo || jid >= job_hi) continue;
+        const int64_t A = absdot_t[tj_lo + i], k = jid - job_lo;
+        if (nd) nd[k] = (unsigned long long)((A - (int64_t)num[k]) / 2);
+        if (n3) n3[k] = (unsigned long long)(A - n0 + (int64_t)n1[y] + (int64_t)n1[x]);
+    }
+    pdl_trigger();
+}
 // ------------------------------------------------------------------ split-K accumulation
 // One workspace per device (a process may drive several GPUs: compute_all_pairs(devices=...)).
 // The workspace stays zero between calls: accum_convert clears every entry it converts, so a GEMM finds it
@@ -276,6 +300,24 @@ int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st) 
 
 }  // namespace tb
 
+extern "C" int tb_tied_counts(const int32_t* absdot_t, const int32_t* rows_t, int64_t nt, const uint64_t* n1_rows,
+                              int64_t m, int64_t n, int64_t job_lo, int64_t job_hi, int64_t tj_lo, int64_t tj_hi,
+                              const int32_t* num, uint64_t* nd, uint64_t* n3, void* stream) {
+    if (m < 1 || n < 2 || nt < 0 || nt > m) return fail(TB_ERR_INVALID, "tied_counts: need m >= 1, n >= 2, 0 <= nt <= m");
+    const int64_t total = m * (m + 1) / 2, ttot = nt * (nt + 1) / 2;
+    if (job_lo < 0 || job_hi < job_lo || job_hi > total) return fail(TB_ERR_CONFIG, "tied_counts: bad job range");
+    if (tj_lo < 0 || tj_hi < tj_lo || tj_hi > ttot) return fail(TB_ERR_CONFIG, "tied_counts: bad tied job range");
+    if (tj_hi == tj_lo || job_hi == job_lo) return TB_OK;
+    if (!absdot_t || !rows_t || !n1_rows || !num) return fail(TB_ERR_INVALID, "tied_counts: null pointer");
+    const int64_t count = tj_hi - tj_lo;
+    const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 16);
+    TB_CUDA_TRY(launch_pdl(tied_counts_kernel, dim3((unsigned)blocks), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                           absdot_t, rows_t, nt, reinterpret_cast<const unsigned long long*>(n1_rows), m,
+                           n * (n - 1) / 2, job_lo, job_hi, tj_lo, count, num,
+                           reinterpret_cast<unsigned long long*>(nd), reinterpret_cast<unsigned long long*>(n3)));
+    return check_launch("tied_counts_kernel");
+}
+
 extern "C" int tb_full_counts(const int32_t* num, const int32_t* absdot, const uint64_t* n1_rows, int64_t m,
                               int64_t n, int64_t job_lo, int64_t job_hi, uint64_t* nd, uint64_t* n3, void* stream) {
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "full_counts: need m >= 1, n >= 2");
@@ -301,14 +343,6 @@ extern "C" int tb_full_counts(const int32_t* num, const int32_t* absdot, const u
 //   cells before tile (ty, tx) = row_prefix(ty q) + [tx > ty] sum_{i in tile rows} (tx q - i)
 //   cells before row r of that tile = r (c1 - c0) off the diagonal, r (c1 - r0) - r (r - 1) / 2 on it.
 namespace tb {
-__host__ __device__ __forceinline__ int64_t cells_before_tile(int64_t t, int64_t m, int64_t q, int64_t w) {
-    int64_t ty, tx;
-    job_coord(t, w, ty, tx);
-    const int64_t r0 = ty * q, s = min(r0 + q, m) - r0;
-    int64_t c = row_prefix(r0, m);
-    if (tx > ty) c += s * tx * q - (s * r0 + s * (s - 1) / 2);
-    return c;
-}
 
 __global__ void __launch_bounds__(256) records_kernel(const int32_t* __restrict__ num,
                                                       const int64_t* __restrict__ nd,
@@ -345,6 +379,31 @@ __global__ void __launch_bounds__(256) records_kernel(const int32_t* __restrict_
     }
     pdl_trigger();
 }
+
+// Compact form of the same stream: 8 bytes per record, (numerator, n3) as (int32, uint32) in emission order.
+// i, j, n1, n2 and n_d = (n0 - n1 - n2 + n3 - numerator) / 2 (result.py:42) are re-derived on the host by
+// tb_expand_records, so a pass crosses PCIe in 1/6 of the bytes.
+__global__ void __launch_bounds__(256) records_compact_kernel(const int32_t* __restrict__ num,
+                                                              const int64_t* __restrict__ n3, int64_t m, int64_t q,
+                                                              int64_t w, int64_t job_lo, int64_t tile_lo,
+                                                              int64_t base0, int naive, uint2* __restrict__ out) {
+    pdl_wait();
+    const int64_t t = tile_lo + blockIdx.x;
+    int64_t ty, tx;
+    job_coord(t, w, ty, tx);
+    const int64_t r0 = ty * q, c0 = tx * q, cend = min(c0 + q, m);
+    const int64_t base = cells_before_tile(t, m, q, w) - base0;
+    for (int64_t k = threadIdx.x; k < q * q; k += blockDim.x) {
+        const int64_t r = k / q, c = k - r * q;
+        const int64_t i = r0 + r, j = c0 + c;
+        if (i >= m || j >= m || j < i) continue;
+        const int64_t above = tx > ty ? r * (cend - c0) : r * (cend - r0) - r * (r - 1) / 2;
+        const int64_t pos = base + above + (j - max(i, c0));
+        const int64_t jid = row_prefix(i, m) + (j - i) - job_lo;
+        out[pos] = make_uint2((uint32_t)num[jid], naive ? 0u : (uint32_t)n3[jid]);
+    }
+    pdl_trigger();
+}
 }  // namespace tb
 
 extern "C" int64_t tb_tile_cells(int64_t m, int64_t q, int64_t tile_lo, int64_t tile_hi) {
@@ -357,14 +416,8 @@ extern "C" int64_t tb_tile_cells(int64_t m, int64_t q, int64_t tile_lo, int64_t 
     return b - a;
 }
 
-extern "C" int tb_records(const int32_t* num, const int64_t* nd, const int64_t* n3, const int64_t* n1_rows, int64_t m,
-                          int64_t q, int64_t job_lo, int64_t job_hi, int64_t tile_lo, int64_t ntiles, int naive,
-                          void* records, void* stream) {
-    if (m < 1 || q < 1) return fail(TB_ERR_CONFIG, "records: need m >= 1 and q >= 1");
-    if (ntiles < 0 || tile_lo < 0) return fail(TB_ERR_CONFIG, "records: bad tile range");
-    if (ntiles == 0) return TB_OK;
-    if (!num || !records || (!naive && (!nd || !n3 || !n1_rows)))
-        return fail(TB_ERR_INVALID, "records: null pointer");
+// Shared argument checks of tb_records / tb_records_compact (pointers checked by the callers).
+static int records_range_check(int64_t m, int64_t q, int64_t job_lo, int64_t job_hi, int64_t tile_lo, int64_t ntiles) {
     if (ntiles > INT32_MAX) return fail(TB_ERR_CAPACITY, "records: too many tiles per pass");
     const int64_t w = (m + q - 1) / q;
     if (tile_lo + ntiles > w * (w + 1) / 2) return fail(TB_ERR_CONFIG, "records: tile range outside the matrix");
@@ -381,10 +434,40 @@ extern "C" int tb_records(const int32_t* num, const int64_t* nd, const int64_t* 
         return fail(TB_ERR_CONFIG, "records: tiles [%lld, %lld) need job ids [%lld, %lld], counts cover [%lld, %lld)",
                     (long long)tile_lo, (long long)(tile_lo + ntiles), (long long)first, (long long)last,
                     (long long)job_lo, (long long)job_hi);
+    return TB_OK;
+}
+
+extern "C" int tb_records(const int32_t* num, const int64_t* nd, const int64_t* n3, const int64_t* n1_rows, int64_t m,
+                          int64_t q, int64_t job_lo, int64_t job_hi, int64_t tile_lo, int64_t ntiles, int naive,
+                          void* records, void* stream) {
+    if (m < 1 || q < 1) return fail(TB_ERR_CONFIG, "records: need m >= 1 and q >= 1");
+    if (ntiles < 0 || tile_lo < 0) return fail(TB_ERR_CONFIG, "records: bad tile range");
+    if (ntiles == 0) return TB_OK;
+    if (!num || !records || (!naive && (!nd || !n3 || !n1_rows)))
+        return fail(TB_ERR_INVALID, "records: null pointer");
+    if (int rc = records_range_check(m, q, job_lo, job_hi, tile_lo, ntiles)) return rc;
+    const int64_t w = (m + q - 1) / q;
     const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
     const int threads = (int)std::min<int64_t>(256, ((q * q + 31) / 32) * 32);
     TB_CUDA_TRY(launch_pdl(records_kernel, dim3((unsigned)ntiles), dim3(threads), 0, static_cast<cudaStream_t>(stream),
                            num, nd, n3, n1_rows, m, q, w, job_lo, tile_lo, base0, naive,
                            reinterpret_cast<uint4*>(records)));
     return check_launch("records_kernel");
+}
+
+extern "C" int tb_records_compact(const int32_t* num, const int64_t* n3, int64_t m, int64_t q, int64_t job_lo,
+                                  int64_t job_hi, int64_t tile_lo, int64_t ntiles, int naive, void* compact,
+                                  void* stream) {
+    if (m < 1 || q < 1) return fail(TB_ERR_CONFIG, "records_compact: need m >= 1 and q >= 1");
+    if (ntiles < 0 || tile_lo < 0) return fail(TB_ERR_CONFIG, "records_compact: bad tile range");
+    if (ntiles == 0) return TB_OK;
+    if (!num || !compact || (!naive && !n3)) return fail(TB_ERR_INVALID, "records_compact: null pointer");
+    if (int rc = records_range_check(m, q, job_lo, job_hi, tile_lo, ntiles)) return rc;
+    const int64_t w = (m + q - 1) / q;
+    const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
+    const int threads = (int)std::min<int64_t>(256, ((q * q + 31) / 32) * 32);
+    TB_CUDA_TRY(launch_pdl(records_compact_kernel, dim3((unsigned)ntiles), dim3(threads), 0,
+                           static_cast<cudaStream_t>(stream), num, n3, m, q, w, job_lo, tile_lo, base0, naive,
+                           reinterpret_cast<uint2*>(compact)));
+    return check_launch("records_compact_kernel");
 }

@@ -20,6 +20,7 @@ import math
 import threading
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -47,6 +48,7 @@ DISPATCH_TABLE = (
     (32767, 8.727e-05, 4.589e-06, 124, 4.203e-06, 3.008e-07),
 )
 D2H_PIECE_BYTES = 256 << 20
+TIED_SPARSE_FRAC = 0.35  # |S| GEMM over the tied rows only while they are at most this share of the rows
 GEMM_MAX_N = 8192  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides)
 RANK_ROWS_MAX_N = 8192  # tb_rank_rows' row limit; wider GEMM-path rows are ranked by tb_rank_dense
 SIGN_MAX_N = 32767      # tb_sign_pack: 15-bit ranks
@@ -128,6 +130,9 @@ class Prepared:
     fmt: int = 0
     row_lo: int = 0
     any_ties: bool | None = None      # GEMM full counts: does any row >= row_lo have ties (read lazily)
+    tied_rows: np.ndarray | None = None   # sparse full counts: the tied rows >= row_lo (host, ascending)
+    tied_dev: torch.Tensor | None = None  # ... on the device (int32)
+    absdot_t: torch.Tensor | None = None  # |S_a|.|S_b| over the tied rows' own job ids (int32)
     keys: torch.Tensor | None = None  # merge: K1 presort outputs
     pos: torch.Tensor | None = None
     srt: torch.Tensor | None = None
@@ -210,6 +215,9 @@ class TauEngine:
 
     sign_format_override: int | None = None  # tests / experiments: force TB_SIGN_*
     force_abs_gemm: bool = False  # tests: run the |S| GEMM even when no variable has ties
+    # full counts with tied variables: "auto" runs the |S| GEMM over the tied rows only when they are at
+    # most TIED_SPARSE_FRAC of the rows (n3 = 0 for every pair with an untied variable), else over all rows
+    tied_mode: str = "auto"
 
     def sign_format(self, K: int) -> int:
         """e2m1 (kind::mxf4) while the f32 sums stay exact (K < 2^24), else int8 (kind::i8)."""
@@ -354,11 +362,19 @@ class TauEngine:
             if not prep.full:
                 raise ConfigError("n_d / n3 on the GEMM path need prepare(..., full_counts=True)")
             if prep.any_ties is None:
-                # one flag read per prepare (a host sync): with no tied variable among the rows the range
-                # touches, |S_y|.|S_x| = n0 - n1_y - n1_x and the |S| GEMM (as long as the numerator GEMM)
-                # is skipped -- config 5 (continuous data) takes this branch
-                prep.any_ties = bool((prep.n1_rows[prep.row_lo:] > 0).any().item())
+                # one read per prepare (a host sync): with no tied variable among the rows the range touches,
+                # |S_y|.|S_x| = n0 - n1_y - n1_x and the |S| GEMM (as long as the numerator GEMM) is skipped;
+                # with few tied variables only their pairs need it (n3 = 0 whenever one variable is untied)
+                tied = np.flatnonzero(prep.n1_rows[prep.row_lo:].cpu().numpy() > 0) + prep.row_lo
+                prep.any_ties = tied.size > 0
+                sparse = self.tied_mode == "sparse" or (
+                    self.tied_mode == "auto" and tied.size <= TIED_SPARSE_FRAC * (m - prep.row_lo))
+                if prep.any_ties and sparse:
+                    prep.tied_rows = tied
             absdot = None
+            if prep.tied_rows is not None and not self.force_abs_gemm:
+                self._tied_counts(prep, lo, hi, num, nd, n3, st, splits)
+                return
             if prep.any_ties or self.force_abs_gemm:
                 if prep.A is None:
                     y0 = prep.row_lo
@@ -371,6 +387,33 @@ class TauEngine:
                                          splits, prep.simt)
             _lib.call("tb_full_counts", _ptr(num), _ptr(absdot), _ptr(prep.n1_rows), m, n, lo, hi, _ptr(nd),
                       _ptr(n3), st)
+
+    def _tied_counts(self, prep: "Prepared", lo: int, hi: int, num, nd, n3, st, splits: int = 0) -> None:
+        """Sparse full counts: the closed form for every pair, then n_d / n3 of tied x tied pairs from the
+        |S| GEMM over the tied rows (computed once per prepare, in the tied rows' own job-id order)."""
+        m, n = prep.m, prep.n
+        T = prep.tied_rows
+        nt = int(T.size)
+        if prep.absdot_t is None:
+            prep.tied_dev = torch.from_numpy(T.astype(np.int32)).to(self.device)
+            S2 = prep.S[: m * prep.ldS].view(m, prep.ldS)
+            St = self._buf("S_tied", nt * prep.ldS, torch.int8)
+            torch.index_select(S2, 0, prep.tied_dev.long(), out=St[: nt * prep.ldS].view(nt, prep.ldS))
+            At = self._buf("A_tied", nt * prep.ldS, torch.int8)
+            _lib.call("tb_abs_pack", _ptr(St), nt, prep.ldS, prep.fmt, _ptr(At), st)
+            tt = nt * (nt + 1) // 2
+            prep.absdot_t = torch.empty(tt, dtype=torch.int32, device=self.device)
+            for a, b in self._gemm_ranges(nt, 0, tt):
+                self._gemm_numerator(At, prep.absdot_t[a:b], nt, prep.K, prep.ldS, prep.fmt, a, b, st, splits,
+                                     prep.simt)
+        _lib.call("tb_full_counts", _ptr(num), None, _ptr(prep.n1_rows), m, n, lo, hi, _ptr(nd), _ptr(n3), st)
+        # tied rows a whose row T[a] meets the job range: rows y_lo .. y_hi
+        y_lo, y_hi = job_coord(lo, m)[0], job_coord(hi - 1, m)[0]
+        a0, a1 = int(np.searchsorted(T, y_lo, "left")), int(np.searchsorted(T, y_hi, "right"))
+        if a1 > a0:
+            tj_lo, tj_hi = a0 * (2 * nt - a0 + 1) // 2, a1 * (2 * nt - a1 + 1) // 2
+            _lib.call("tb_tied_counts", _ptr(prep.absdot_t), _ptr(prep.tied_dev), nt, _ptr(prep.n1_rows), m, n, lo,
+                      hi, tj_lo, tj_hi, _ptr(num), _ptr(nd), _ptr(n3), st)
 
     def _gemm_layout(self, n: int, simt: bool = False):
         """(K, sign format, row stride of S in bytes, row stride of R) for n samples."""

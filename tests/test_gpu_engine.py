@@ -135,6 +135,29 @@ def test_window_pipeline_matches_reference_stream(kernel):
         assert parts == ref
 
 
+@pytest.mark.parametrize("full_every", [1, 2, 3, 10, 1 << 30])
+@pytest.mark.parametrize("kernel", ["sorted", "naive"])
+def test_compact_record_path_matches_reference_stream(monkeypatch, kernel, full_every):
+    """Records through the two host paths -- full 48-byte records by D2H, or the 8-byte compact stream
+    expanded on host threads (tb_records_compact + tb_expand_records) -- in any mix of batches give the
+    reference byte stream (every batch full: full_every = 1; none: 1 << 30)."""
+    import paper_1704_03767_b200 as tb
+    from paper_1704_03767_b200 import engine
+    monkeypatch.setattr(engine, "FULL_EVERY", full_every)
+    monkeypatch.setattr(engine, "SLOT_BYTES", 48 * 5000)  # many batches per run
+    gold = load_json("engine_streams.json")
+    ds = tb.synth_dataset(512, 48, tie_fraction=0.3, seed=512)
+    ref = None
+    for wj, pass_tiles in ((997, 7), (40_000, 300), (1 << 25, 4096)):
+        blob = _stream(ds, kernel, 4, window_jobs=wj, pass_tiles=pass_tiles)
+        if kernel != "naive":
+            assert hashlib.sha256(blob).hexdigest() == gold["m512_n48_t0.3_s512_q4"], (wj, pass_tiles)
+        ref = blob if ref is None else ref
+        assert blob == ref
+    monkeypatch.setattr(engine, "FULL_EVERY", 1)
+    assert _stream(ds, kernel, 4) == ref
+
+
 def test_naive_large_n_uses_merge_path():
     """kernel='naive' for n above the GEMM path's limit: numerator-only records from the merge path
     (the reference's naive kernel handles any n, kernel_naive.py:26-44)."""

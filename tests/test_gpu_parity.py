@@ -648,6 +648,36 @@ def test_full_counts_tie_free_shortcut(eng, oracle):
     _check_full(c, oracle, oracle.rank_matrix(x))
 
 
+@pytest.mark.parametrize("mode", ["auto", "sparse", "full"])
+def test_full_counts_sparse_tied_rows(eng, oracle, mode):
+    """With a few tied variables the |S| GEMM runs over the tied rows only (n3 = 0 for every pair with an
+    untied variable) and tb_tied_counts patches their pairs; identical to the full |S| GEMM and the oracle,
+    over the whole job space and over job sub-ranges that cut rows (the compute_all_pairs windows)."""
+    rng = np.random.default_rng(77)
+    m, n = 420, 260
+    x = rng.standard_normal((m, n)).astype(np.float32)
+    tied = [0, 5, 6, 131, 132, 300, 419]
+    for k, r in enumerate(tied):  # shared tie patterns (joint ties) and private ones
+        x[r, : 20 + 7 * k] = x[r, 0]
+        x[r, 100:110] = 2.5 if k % 2 else x[r, 100]
+    x[rng.integers(0, m), 200:203] = 0.125  # one more row with one small tie group
+    ranks = oracle.rank_matrix(x)
+    xd = torch.from_numpy(x).cuda()
+    try:
+        eng.tied_mode = "sparse" if mode == "sparse" else "auto"
+        eng.force_abs_gemm = mode == "full"
+        res = eng.all_pairs(xd, kernel="gemm", full_counts=True).validate()
+        _check_full(res, oracle, ranks)
+        total = m * (m + 1) // 2
+        for lo, hi in ((0, 1), (1000, 5000), (total // 3, total // 3 + 12345), (total - 999, total)):
+            part = eng.all_pairs(xd, kernel="gemm", full_counts=True, job_range=(lo, hi)).validate()
+            for f in ("numerator", "n_d", "n3"):
+                assert torch.equal(getattr(part, f), getattr(res, f)[lo:hi]), (f, lo, hi)
+    finally:
+        eng.tied_mode = "auto"
+        eng.force_abs_gemm = False
+
+
 @pytest.mark.parametrize("path,m,n", [("gemm", 700, 90), ("merge", 60, 3000)])
 def test_host_entry_point_job_ranges(eng, oracle, path, m, n):
     """all_pairs_host over a rank's job range (multi-GPU e2e): tau_b of [lo, hi) lands at out[0:hi-lo] and

@@ -285,3 +285,43 @@ def test_bench_helpers():
     rows = bench.cpu_subset(5, 65536)
     assert rows.shape == (2048,) and np.array_equal(rows, np.sort(np.random.default_rng(99).choice(65536, 2048, replace=False)))
     assert bench.cpu_subset(2, 2048).shape == (2048,) and bench.cpu_subset(4, 1024).shape == (64,)
+
+
+@pytest.mark.parametrize("m,q,naive", [(1, 8, 0), (37, 8, 0), (64, 8, 1), (101, 4, 0), (300, 16, 0), (257, 3, 0)])
+def test_expand_records_host(m, q, naive):
+    """tb_expand_records (host threads, no device) rebuilds the 48-byte CELL_DTYPE stream of tb_records from
+    the 8-byte (numerator, n3) compact stream: i, j from the tile order, n1/n2 per row, n_d from result.py:42,
+    for any tile sub-range and thread count."""
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.engine import CELL_DTYPE
+    from paper_1704_03767_b200.pairindex import JobSpace
+
+    rng = np.random.default_rng(m * 31 + q)
+    n = 50
+    n0 = n * (n - 1) // 2
+    space = JobSpace(m, q)
+    n1 = rng.integers(0, n0 // 3, m).astype(np.uint64)
+    n1[rng.integers(0, m)] = n0  # a constant row
+    lib = _lib.load()
+    tt = space.total_tiles
+    for lo, hi in ((0, tt), (tt // 3, tt // 3 + max(1, tt // 4)), (tt - 1, tt)):
+        ii, jj = space.cells_in_tile_order(lo, hi)
+        k = ii.size
+        n3 = rng.integers(0, 40, k).astype(np.int64)
+        nd = rng.integers(0, 200, k).astype(np.int64)
+        num = (n0 - n1[ii].astype(np.int64) - n1[jj].astype(np.int64) + n3 - 2 * nd).astype(np.int32)
+        exp = np.zeros(k, CELL_DTYPE)
+        exp["i"], exp["j"], exp["numerator"] = ii, jj, num
+        if not naive:
+            exp["n_d"], exp["n1"], exp["n2"], exp["n3"] = nd, n1[ii], n1[jj], n3
+        compact = np.empty((k, 2), np.uint32)
+        compact[:, 0] = num.view(np.uint32)
+        compact[:, 1] = 0 if naive else n3
+        for nthreads in (1, 4):
+            buf = np.zeros(k * 48 + 16, np.uint8)
+            off = (-buf.ctypes.data) % 16
+            out = buf[off:off + k * 48]
+            rc = lib.tb_expand_records(compact.ctypes.data, n1.ctypes.data, m, n, q, lo, hi - lo, naive,
+                                       out.ctypes.data, nthreads)
+            assert rc == 0, lib.tb_last_error()
+            assert out.tobytes() == exp.tobytes(), (lo, hi, nthreads)
