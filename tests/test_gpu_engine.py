@@ -145,6 +145,7 @@ def test_compact_record_path_matches_reference_stream(monkeypatch, kernel, full_
     from paper_1704_03767_b200 import engine
     monkeypatch.setattr(engine, "FULL_EVERY", full_every)
     monkeypatch.setattr(engine, "SLOT_BYTES", 48 * 5000)  # many batches per run
+    monkeypatch.setattr(engine, "COMPACT_MIN_BATCHES", 1)
     gold = load_json("engine_streams.json")
     ds = tb.synth_dataset(512, 48, tie_fraction=0.3, seed=512)
     ref = None

@@ -40,10 +40,17 @@ for fe in [int(a) for a in (sys.argv[1:] or ["1", "1000000"])]:
     for pt in (4096,):
         for _ in range(2):
             tb.compute_all_pairs(ds, "vectorized", sink=sink, pass_tiles=pt, window_jobs=wjs[-1])
-        acc.update(expand=0.0, n=0)
-        t0 = time.perf_counter()
-        s = tb.compute_all_pairs(ds, "vectorized", sink=sink, pass_tiles=pt, window_jobs=wjs[-1])
-        wall = time.perf_counter() - t0
+        reps = 1 if x.shape[0] > 20000 else 10
+        best = None
+        for _ in range(reps):
+            acc.update(expand=0.0, n=0)
+            t0 = time.perf_counter()
+            s = tb.compute_all_pairs(ds, "vectorized", sink=sink, pass_tiles=pt, window_jobs=wjs[-1])
+            wall = time.perf_counter() - t0
+            if best is None or wall < best[0]:
+                best = (wall, s, dict(acc))
+        wall, s, accb = best
+        acc.update(accb)
         wr = sum(p.write_seconds for p in s.passes)
         print(f"full_every {fe:8d} pass_tiles {pt:6d}: wall {1e3 * wall:7.1f} ms, event waits {1e3 * s.device_seconds:7.1f} ms, "
               f"expand {1e3 * acc['expand']:7.1f} ms ({acc['n']} batches), submit {1e3 * wr:6.1f} ms, passes {len(s.passes)}",
