@@ -500,7 +500,7 @@ def run_ours(args):
             flush.zero_()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
-            r = eng.all_pairs_host(xh, out_tb, kernel=path, stream=stream, job_range=jr)
+            r = eng.all_pairs_host(xh, out_tb, kernel=path, stream=stream, job_range=jr, numerators=False)
             e.record(stream)
         if it >= 2:
             e2e_times.append((s, e))

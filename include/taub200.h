@@ -204,6 +204,14 @@ int tb_gemm_pairs_simt(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int64
 int tb_finalize(const int32_t *num, const uint64_t *n1_rows, int64_t m, int64_t n, int64_t job_lo,
                 int64_t job_hi, double *tau_a, double *tau_b, void *stream);
 
+/* K3 + K5 fused: tau_b of job ids [job_lo, job_hi) straight from the GEMM epilogue (8 B per pair written,
+ * no numerator round trip through HBM), the same IEEE sequence as tb_finalize.  When the plan splits a
+ * unit over K (few units: small m) or the format is int8, the numerators go to num_ws (job_hi - job_lo
+ * int32, may be NULL only when neither happens) and tb_finalize runs after the GEMM.  Replaces the
+ * numerator + derive_taus sequence (kernel_naive.py:26-44, result.py:62-82) for tau_b-only callers. */
+int tb_gemm_tau_b(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo, int64_t job_hi,
+                  int32_t splits, const uint64_t *n1_rows, int64_t n, int32_t *num_ws, double *tau_b, void *stream);
+
 /*
  * K1 presort for the merge path (large n): per variable, the position of
  * every observation in ascending-rank order (u-order), the rank sequence in

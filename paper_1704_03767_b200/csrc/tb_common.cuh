@@ -106,6 +106,16 @@ __host__ __device__ __forceinline__ int64_t cells_before_tile(int64_t t, int64_t
     return c;
 }
 
+// tau_b of one cell, the IEEE sequence of derive_taus (result.py:62-82): num / sqrt((n0 - t1) (n0 - t2)),
+// NaN where the denominator is 0; tie-free cells (t1 = t2 = 0) take num / n0, which is the same double
+// (sqrt(n0 n0) = n0 exactly while n0^2 < 2^53).  Shared by K5 and the GEMM's fused epilogue.
+__device__ __forceinline__ double tau_b_ieee(int32_t num, uint64_t t1, uint64_t t2, double dn0) {
+    const double dv = (double)num;
+    if ((t1 | t2) == 0) return __ddiv_rn(dv, dn0);
+    const double denom = __dsqrt_rn(__dmul_rn(dn0 - (double)t1, dn0 - (double)t2));
+    return denom > 0.0 ? __ddiv_rn(dv, denom) : __longlong_as_double(0x7ff8000000000000LL);
+}
+
 // Sample-pair enumeration for the sign vector: k(a, b) = a*n - a(a+1)/2 + (b - a - 1), a < b.
 __host__ __device__ __forceinline__ int64_t seg_offset(int64_t a, int64_t n) { return a * n - a * (a + 1) / 2; }
 

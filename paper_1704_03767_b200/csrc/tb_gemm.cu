@@ -443,7 +443,8 @@ using namespace tb;
 
 namespace tb {
 int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi, int32_t splits,
-             int32_t* num, cudaStream_t st);
+             int32_t* num, cudaStream_t st, double* tau_b = nullptr, const uint64_t* n1 = nullptr, int64_t n = 0,
+             int* fused = nullptr);
 }
 
 extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
@@ -457,6 +458,28 @@ extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (format == TB_SIGN_E2M1) return gemm_fp4(S, m, K, ldS, job_lo, job_hi, splits, num, st);
     return gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, format, num, st);
+}
+
+extern "C" int tb_gemm_tau_b(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
+                             int64_t job_hi, int32_t splits, const uint64_t* n1_rows, int64_t n, int32_t* num_ws,
+                             double* tau_b, void* stream) {
+    if (format < TB_SIGN_I8 || format > TB_SIGN_E2M1) return fail(TB_ERR_CONFIG, "gemm_tau_b: unknown format %d", format);
+    int rc = check_job_args(m, format == TB_SIGN_E2M1 ? K / 2 : K, ldS, job_lo, job_hi);
+    if (rc) return rc;
+    if (!S || !n1_rows || !tau_b) return fail(TB_ERR_INVALID, "gemm_tau_b: null pointer");
+    if (n < 2) return fail(TB_ERR_INVALID, "gemm_tau_b: need n >= 2");
+    if (job_hi == job_lo) return TB_OK;
+    if (m > (int64_t)INT32_MAX - gemm2::TILE) return fail(TB_ERR_CAPACITY, "gemm: m too large for TMA coordinates");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int fused = 0;
+    if (format == TB_SIGN_E2M1) {
+        if ((rc = gemm_fp4(S, m, K, ldS, job_lo, job_hi, splits, num_ws, st, tau_b, n1_rows, n, &fused))) return rc;
+    } else {
+        if (!num_ws) return fail(TB_ERR_INVALID, "gemm_tau_b: the int8 path needs the numerator workspace");
+        if ((rc = gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, format, num_ws, st))) return rc;
+    }
+    if (fused) return TB_OK;
+    return tb_finalize(num_ws, n1_rows, m, n, job_lo, job_hi, nullptr, tau_b, stream);
 }
 
 extern "C" int tb_gemm_pairs_simt(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,

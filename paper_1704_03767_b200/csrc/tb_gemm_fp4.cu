@@ -45,7 +45,8 @@ constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t SF_COL = 480;
 constexpr int STG_LD = 17;    // epilogue staging tile: 32 rows x 16 columns, padded row stride
-constexpr uint32_t STG_BYTES = EPI_WARPS * (32 * STG_LD * 4 + 32 * 8);  // per epilogue warp: tile + row bases
+constexpr int STG_WORDS = 32 * STG_LD + 64 + 32;  // per epilogue warp: tile, 32 row bases (int64), 32 row n1 (u32)
+constexpr uint32_t STG_BYTES = EPI_WARPS * STG_WORDS * 4;
 constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + STG_BYTES;
 }  // namespace g4
 
@@ -70,6 +71,10 @@ struct Gemm4Args {
     const int32_t* item_unit;
     const int32_t* unit_splits;
     int32_t* unit_cnt;
+    // fused finalize (direct plans): tau_b[j] = tau_b_ieee(num, n1[y], n1[x], n0) instead of num[j]
+    double* tau_b;
+    const unsigned long long* n1;
+    double dn0;
 };
 
 // ---- K-lockstep throttle.  The ~74 concurrently running CTA pairs stream the same S rows (units of one
@@ -272,8 +277,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
         // apart.  Split partials are added lane-per-row with aligned 16-byte f32 reds.
         const int q = warp & 3;              // TMEM lane quarter
         const int par = (warp - 4) >> 2;     // this warp's 16-column chunks: c / 16 = par (mod EPI_PAR)
-        int32_t* stg = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * STG_LD + 64);
+        int32_t* stg = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * STG_WORDS;
         int64_t* rowbase = reinterpret_cast<int64_t*>(stg + 32 * STG_LD);
+        uint32_t* rown1 = reinterpret_cast<uint32_t*>(rowbase + 32);  // n1 < n0 < 2^31
         uint32_t acc_phase = 0;
         const int64_t m = p.m;
         const int64_t span = p.job_hi - p.job_lo;
@@ -288,6 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                 const int64_t y = y0 + lane;
                 row_j0 = (y < m) ? row_prefix(y, m) - y - p.job_lo : INT64_MIN / 2;
                 rowbase[lane] = row_j0;
+                if (p.tau_b) rown1[lane] = y < m ? (uint32_t)__ldg(&p.n1[y]) : 0u;
             }
             __syncwarp();
             mbar_wait(tfull, acc_phase);
@@ -334,7 +341,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 16; ++i) stg[lane * STG_LD + i] = (int32_t)r[i];
                     __syncwarp();
-                    {
+                    if (p.tau_b) {  // fused K5: tau_b straight from the accumulator (8 B per pair, no numerator)
+                        const int64_t x = xc + col;
+                        const uint64_t t2 = x < m ? (uint64_t)__ldg(&p.n1[x]) : 0;
+#pragma unroll 4
+                        for (int k = 0; k < 16; ++k) {
+                            const int rr = 2 * k + half;
+                            const int64_t y = y0 + rr;
+                            const int64_t j = rowbase[rr] + x;
+                            if (x >= y && x < m && j >= 0 && j < span)
+                                p.tau_b[j] = tau_b_ieee(__float2int_rn(__int_as_float(stg[rr * STG_LD + col])),
+                                                        rown1[rr], t2, p.dn0);
+                        }
+                    } else {
                         const int64_t x = xc + col;
 #pragma unroll 4
                         for (int k = 0; k < 16; ++k) {
@@ -654,8 +673,11 @@ static int lockstep_state(unsigned long long** prog, uint32_t* epoch, int32_t* l
     return TB_OK;
 }
 
+// tau_b != nullptr: fused finalize when the plan has no split unit (the kernel writes tau_b, num is not
+// written; *fused = 1); a split plan computes num (which must then be a buffer) and *fused = 0.
 int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi, int32_t splits,
-             int32_t* num, cudaStream_t st) {
+             int32_t* num, cudaStream_t st, double* tau_b, const uint64_t* n1, int64_t n, int* fused) {
+    if (fused) *fused = 0;
     if (K >= (int64_t(1) << 24)) return fail(TB_ERR_CAPACITY, "gemm fp4: K=%lld needs exact f32 sums (< 2^24)", (long long)K);
     if (m >= (int64_t(1) << 16) * g4::UM) return fail(TB_ERR_CAPACITY, "gemm fp4: m too large");
     int rc;
@@ -672,6 +694,14 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.job_lo = job_lo;
     p.job_hi = job_hi;
     p.num = num;
+    if (tau_b && !p.partial) {
+        p.tau_b = tau_b;
+        p.n1 = reinterpret_cast<const unsigned long long*>(n1);
+        p.dn0 = (double)(n * (n - 1) / 2);
+        if (fused) *fused = 1;
+    } else if (!num) {
+        return fail(TB_ERR_INVALID, "gemm fp4: a split plan needs the numerator buffer");
+    }
     if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
     // In-kernel split-K fixup: opt-in (TB_GEMM_FIXUP=1).  Measured slower than the separate accum_convert
     // launch on configs 1-2 (config 1 0.039 -> 0.051 ms, config 2 0.540 -> 0.553 ms per step; config 3 within

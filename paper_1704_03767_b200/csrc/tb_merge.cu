@@ -571,6 +571,9 @@ __device__ __forceinline__ uint32_t merge_level_inplace(uint16_t* blk, int t, in
     return inv;
 }
 
+#ifndef MG_PREFETCH  // L2 prefetch of the next pair's rows (A/B: profiles/r02_merge_ab.log)
+#define MG_PREFETCH 0
+#endif
 #ifndef MG_LEAF_XL  // cross-lane leaf levels for E = 32 (round-1 kernel on config 4: 1 -> 319.5 ms, 2 -> 315.5 ms,
 #define MG_LEAF_XL 2  // 3 -> 328.5 ms)
 #endif
@@ -818,8 +821,23 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
         int64_t y, x;
         job_coord(p.job_lo + idx, p.m, y, x);
         const int32_t* pu = p.pos + y * n;      // u-order positions
-        const int32_t* su = p.sorted + y * n;   // u ranks in u-order
         const uint16_t* kv = p.keys + x * n;    // v min-rank keys
+#if MG_PREFETCH
+        // the next pair's v keys (and u positions when its row changes) into L2 while this pair sorts: the
+        // scatter at the top of a pair is the kernel's one latency-bound phase
+        if (idx + gridDim.x < p.count) {
+            int64_t y2, x2;
+            job_coord(p.job_lo + idx + gridDim.x, p.m, y2, x2);
+            const char* k2 = reinterpret_cast<const char*>(p.keys + x2 * n);
+            for (int64_t b = (int64_t)tid * 128; b < 2 * n; b += (int64_t)MG_THREADS * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(k2 + b));
+            if (y2 != y) {
+                const char* p2 = reinterpret_cast<const char*>(p.pos + y2 * n);
+                for (int64_t b = (int64_t)tid * 128; b < 4 * n; b += (int64_t)MG_THREADS * 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p2 + b));
+            }
+        }
+#endif
 
         // pads (0xFFFE: real keys are < n <= 65535 whenever pads exist, and 0xFFFF is the merge
         // loop's INF) first, then scatter w[pos_u[e]] = key_v[e]

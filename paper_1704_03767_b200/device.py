@@ -17,6 +17,7 @@ from __future__ import annotations
 import contextlib
 import ctypes
 import math
+import os
 import threading
 from dataclasses import dataclass, field
 
@@ -218,6 +219,12 @@ class TauEngine:
     # full counts with tied variables: "auto" runs the |S| GEMM over the tied rows only when they are at
     # most TIED_SPARSE_FRAC of the rows (n3 = 0 for every pair with an untied variable), else over all rows
     tied_mode: str = "auto"
+    # tau_b-only callers (tau_b_bands, all_pairs_host(numerators=False)) on the FP4 GEMM path: the GEMM
+    # epilogue can write tau_b itself (tb_gemm_tau_b: no numerator round trip, no finalize launch).  Off by
+    # default: measured slower (config 5 step 407.7 -> 422.7 ms, SM clock under the power cap 1342-1365 ->
+    # 1282-1327 MHz; config 3 GEMM 5.5 -> 6.1 ms for the same step time; profiles/r02_fused_finalize_ab.log):
+    # the fp64 divisions sit in the epilogue window where the MMA waits for TMEM, and cost power.
+    fuse_finalize: bool = os.environ.get("TB_FUSE_FINALIZE", "0") == "1"
 
     def sign_format(self, K: int) -> int:
         """e2m1 (kind::mxf4) while the f32 sums stay exact (K < 2^24), else int8 (kind::i8)."""
@@ -415,6 +422,15 @@ class TauEngine:
             _lib.call("tb_tied_counts", _ptr(prep.absdot_t), _ptr(prep.tied_dev), nt, _ptr(prep.n1_rows), m, n, lo,
                       hi, tj_lo, tj_hi, _ptr(num), _ptr(nd), _ptr(n3), st)
 
+    def _fused_tau_b(self, prep: "Prepared") -> bool:
+        return self.fuse_finalize and prep.path == "gemm" and not prep.simt
+
+    def _gemm_tau_b(self, S, num, tb, n1_rows, m, n, K, ldS, fmt, lo, hi, st) -> None:
+        """tau_b of job ids [lo, hi) into tb[0:hi-lo] from the GEMM epilogue (num: fallback workspace)."""
+        for a, b in self._gemm_ranges(m, lo, hi):
+            _lib.call("tb_gemm_tau_b", _ptr(S), m, K, ldS, fmt, a, b, 0, _ptr(n1_rows), n, _ptr(num[a - lo:b - lo]),
+                      _ptr(tb[a - lo:b - lo]), st)
+
     def _gemm_layout(self, n: int, simt: bool = False):
         """(K, sign format, row stride of S in bytes, row stride of R) for n samples."""
         K = int(_lib.load().tb_sign_k(n))  # padded diagonal layout, >= n(n-1)/2 elements
@@ -501,16 +517,21 @@ class TauEngine:
             st = _stream_ptr(st_t)
             prep = self.prepare(x, path, row_lo=job_coord(base, m)[0], all_rows=False)
             num = self._buf("num_band", max(hi - lo for lo, hi in bands), torch.int32)
+            fused = self._fused_tau_b(prep)
             for b, (lo, hi) in enumerate(bands):
                 if timing is not None:  # (start, end) events around the band's numerator kernels
                     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                     ev[0].record(st_t)
-                self.numerators(prep, lo, hi, num)
+                tb = out[lo - base:hi - base]
+                if fused:
+                    self._gemm_tau_b(prep.S, num, tb, prep.n1_rows, m, n, prep.K, prep.ldS, prep.fmt, lo, hi, st)
+                else:
+                    self.numerators(prep, lo, hi, num)
                 if timing is not None:
                     ev[1].record(st_t)
                     timing.append(ev)
-                tb = out[lo - base:hi - base]
-                _lib.call("tb_finalize", _ptr(num), _ptr(prep.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
+                if not fused:
+                    _lib.call("tb_finalize", _ptr(num), _ptr(prep.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
                 if on_band is not None:
                     on_band(b, tb)
         return prep
@@ -549,7 +570,8 @@ class TauEngine:
     def all_pairs_host(self, x_host: torch.Tensor, tau_b_out: torch.Tensor, kernel: str = "auto",
                        band_fracs: tuple | None = None, stream: torch.cuda.Stream | None = None,
                        copy_stream: torch.cuda.Stream | None = None, h2d_chunks: int = 2,
-                       h2d_piece_bytes: int = 4 << 20, job_range: tuple[int, int] | None = None) -> PairResult:
+                       h2d_piece_bytes: int = 4 << 20, job_range: tuple[int, int] | None = None,
+                       numerators: bool = True) -> PairResult:
         """End-to-end from host buffers: H2D of the values, the device path, tau_b back to host.
 
         The job range (default: every job id; a rank's shard under multi-GPU strong scaling) is cut into
@@ -609,15 +631,19 @@ class TauEngine:
                 if hi <= lo:
                     continue
                 num = res.numerator[lo - jlo:hi - jlo]
-                if path == "gemm":
+                tb = res.tau_b[lo - jlo:hi - jlo]
+                fused = path == "gemm" and not numerators and self.fuse_finalize
+                if fused:  # tau_b from the GEMM epilogue; res.numerator is not filled
+                    self._gemm_tau_b(S, num, tb, res.n1_rows, m, n, K, ldS, fmt, lo, hi, st)
+                elif path == "gemm":
                     self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st)
                 else:
                     ws, wsb = self._merge_ws(n)
                     _lib.call("tb_merge_pairs", _ptr(keys), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp[0]),
                               _ptr(maxgrp[1]), _ptr(maxgrp[2]), m, n, lo, hi, _ptr(num), None, None, _ptr(ws), wsb,
                               st)
-                tb = res.tau_b[lo - jlo:hi - jlo]
-                _lib.call("tb_finalize", _ptr(num), _ptr(res.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
+                if not fused:
+                    _lib.call("tb_finalize", _ptr(num), _ptr(res.n1_rows), m, n, lo, hi, None, _ptr(tb), st)
                 ev = torch.cuda.Event()
                 ev.record(st_t)
                 cp_t.wait_event(ev)

@@ -700,3 +700,37 @@ def test_host_entry_point_job_ranges(eng, oracle, path, m, n):
         torch.cuda.synchronize()
         assert seen == list(range(len(bands)))
         np.testing.assert_array_equal(dout.cpu().numpy(), ref[lo:hi])
+
+
+@pytest.mark.parametrize("m,n,levels", [(300, 200, 0), (2600, 96, 7), (700, 90, 30)])
+def test_fused_tau_b_epilogue(eng, oracle, m, n, levels):
+    """tau_b straight from the FP4 GEMM epilogue (tb_gemm_tau_b: no numerator round trip, no finalize
+    launch) equals the numerator + tb_finalize path bit for bit -- tie-free rows (num / n0), tied rows
+    (the sqrt sequence), a constant row (NaN), one-launch and split-K plans (the split plan falls back to
+    numerator + finalize) -- through tau_b_bands and all_pairs_host(numerators=False)."""
+    rng = np.random.default_rng(m + n)
+    x = (rng.standard_normal((m, n)) if levels == 0 else rng.integers(0, levels, (m, n))).astype(np.float32)
+    x[3] = 1.5  # constant row: tau_b NaN
+    xd = torch.from_numpy(x).cuda()
+    ref = eng.all_pairs(xd, kernel="gemm", tau_a=False).validate().tau_b.cpu().numpy()
+    total = m * (m + 1) // 2
+    bands = [(0, total // 3), (total // 3, total // 3 + 777), (total // 3 + 777, total)]
+    try:
+        for fuse in (True, False):
+            eng.fuse_finalize = fuse
+            out = torch.empty(total, dtype=torch.float64, device="cuda")
+            eng.tau_b_bands(xd, bands, out, kernel="gemm")
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(out.cpu().numpy(), ref)
+            xh = torch.from_numpy(x).pin_memory()
+            outh = torch.empty(total, dtype=torch.float64).pin_memory()
+            eng.all_pairs_host(xh, outh, kernel="gemm", numerators=False)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(outh.numpy(), ref)
+    finally:
+        eng.fuse_finalize = False
+    pi, pj = oracle.upper_pairs(m)
+    sel = rng.integers(0, total, 4000)
+    num, counts = oracle.all_pairs(oracle.rank_matrix(x), pi[sel], pj[sel], oracle.KERNEL_SORTED, threads=8)
+    _, tb = oracle.derive_taus(num, counts[:, 1], counts[:, 2], n)
+    np.testing.assert_array_equal(ref[sel], tb)
