@@ -533,7 +533,15 @@ def run_ours(args):
         if path == "gemm":
             fp4 = sign_format == _lib.TB_SIGN_E2M1
             fp4_lib = measure_fp4_peak(torch, dev) if fp4 else None
-            mma_ceiling = measure_mxf4_ceiling() if fp4 else None
+            mma_clk = None
+            if fp4:  # the probe's own SM clock: it may run power-capped right after the timed region
+                cs = ClockSampler(local)
+                cs.start()
+                time.sleep(0.12)
+                mma_ceiling = measure_mxf4_ceiling()
+                mma_clk = cs.stop().get("sm_mhz")
+            else:
+                mma_ceiling = None
             if fp4:
                 pk, src = 9.0e15, "nominal dense FP4 (kind::mxf4) 9 PFLOP/s, B200_PROFILING.md table (no measured FP4 entry)"
             else:
@@ -550,11 +558,12 @@ def run_ours(args):
                     "frac_of_measured_fp4_library": (achieved / fp4_lib) if fp4_lib else None,
                     "measured_mma_ceiling_tflops": mma_ceiling / 1e12 if mma_ceiling else None,
                     "frac_of_measured_mma_ceiling": (achieved / mma_ceiling) if mma_ceiling else None,
-                    # the MMA-issue ceiling is measured at the 1965 MHz boost clock; a long GEMM runs at the
-                    # clock the 1 kW cap allows (clocks.sm_mhz), so this is the kernel's share of what the
-                    # tensor pipe can issue at that clock
+                    # the MMA-issue ceiling scaled from the probe's own SM clock (sampled while it ran) to the
+                    # clock of the timed region (the 1 kW cap sets it on long GEMMs): the kernel's share of what
+                    # the tensor pipe can issue at that clock
+                    "mma_probe_sm_mhz": mma_clk,
                     "frac_of_mma_ceiling_at_measured_clock": (
-                        achieved / (mma_ceiling * clocks["sm_mhz"] / 1965.0)
+                        achieved / (mma_ceiling * clocks["sm_mhz"] / (mma_clk or 1965.0))
                         if mma_ceiling and clocks.get("sm_mhz") else None),
                     "measured_int8_peak_tops": peak / 1e12 if peak else None,
                     "algorithmic": (f"2*K ops per i<j pair, K=n(n-1)/2={K} sample pairs; {my_pairs} pairs per step "
