@@ -175,12 +175,19 @@ def test_naive_large_n_uses_merge_path():
     assert (nv["n_d"] == 0).all() and (nv["n1"] == 0).all() and (nv["n3"] == 0).all()
 
 
-def test_concurrent_calls_from_threads():
+@pytest.mark.parametrize("compact", [False, True])
+def test_concurrent_calls_from_threads(monkeypatch, compact):
     """Two host threads calling compute_all_pairs on the same GPU (different datasets, different paths)
-    at once: the engine lock + stream ordering keep workspaces and pass buffers apart."""
+    at once: the engine lock + stream ordering keep workspaces and pass buffers apart -- also with both
+    record paths in use (compact batches expanded by each call's own expander thread)."""
     import threading
 
     import paper_1704_03767_b200 as tb
+    from paper_1704_03767_b200 import engine
+    if compact:
+        monkeypatch.setattr(engine, "SLOT_BYTES", 48 * 3000)
+        monkeypatch.setattr(engine, "COMPACT_MIN_BATCHES", 1)
+        monkeypatch.setattr(engine, "FULL_EVERY", 3)
     gold = load_json("engine_streams.json")
     ds_a = tb.synth_dataset(512, 48, tie_fraction=0.3, seed=512)
     ds_b = tb.synth_dataset(64, 48, tie_fraction=0.3, seed=512)
