@@ -86,15 +86,27 @@ def test_tsv_matches_reference():
     assert s.getvalue() == gold["tsv_m6_n9_t0.4_s12_q2"]
 
 
-def test_sink_failure_propagates():
+@pytest.mark.parametrize("compact", [False, True])
+def test_sink_failure_propagates(monkeypatch, compact):
     import paper_1704_03767_b200 as tb
-    ds = tb.synth_dataset(12, 8, seed=10)
+    from paper_1704_03767_b200 import engine
+    if compact:  # many batches, most of them expanded on the host: the abort must stop both threads
+        monkeypatch.setattr(engine, "SLOT_BYTES", 48 * 40)
+        monkeypatch.setattr(engine, "COMPACT_MIN_BATCHES", 1)
+    ds = tb.synth_dataset(120 if compact else 12, 8, seed=10)
+    calls = []
 
     def broken(_):
-        raise OSError("disk full")
+        calls.append(1)
+        if len(calls) == 3:
+            raise OSError("disk full")
 
     with pytest.raises(OSError, match="disk full"):
         tb.compute_all_pairs(ds, "sorted", tile_size=2, pass_tiles=2, sink=broken)
+    # the engine is usable afterwards
+    s = io.BytesIO()
+    tb.compute_all_pairs(ds, "sorted", tile_size=2, pass_tiles=2, sink=tb.BinaryWriter(s, ds.n))
+    assert len(s.getvalue()) > 0
 
 
 @pytest.mark.parametrize("kernel", ["sorted", "gemm"])
