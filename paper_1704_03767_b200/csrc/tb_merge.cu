@@ -338,16 +338,47 @@ __device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b) {
     a = lo;
     b = hi;
 }
+// The leaf's networks are min/max only, i.e. all on the ALU pipe (half rate) while the FMA pipe idles.
+// cswap_fma takes the maximum as a + b - min(a, b) in two IMADs with opaque multipliers (__constant__, so
+// ptxas cannot fold them back into a VIMNMX): one ALU op + two FMA ops instead of two ALU ops.  Every
+// MG_ALT_SWAP-th compare-exchange of a stage uses it (0: none).
+#ifndef MG_ALT_SWAP  // config 4 kernel: 0 -> 275.2 ms, every 3rd 271.9, every 2nd 270.3, all (1) 263.9 ms
+#define MG_ALT_SWAP 1
+#endif
+#ifndef MG_TAG_FMA  // leaf tags: IMAD / mul.hi instead of SHF + LOP3
+#define MG_TAG_FMA 0
+#endif
+__constant__ uint32_t c_mg_one = 1u;
+__constant__ uint32_t c_mg_m1 = 0xFFFFFFFFu;
+__device__ __forceinline__ void cswap_fma(uint32_t& a, uint32_t& b) {
+    const uint32_t lo = min(a, b);
+    uint32_t s, hi;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(a), "r"(c_mg_one), "r"(b));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"(lo), "r"(c_mg_m1), "r"(s));
+    a = lo;
+    b = hi;
+}
+template <int K>
+__device__ __forceinline__ void cswap_k(uint32_t& a, uint32_t& b) {  // K = index of the exchange in its stage
+    if constexpr (MG_ALT_SWAP > 0 && K % MG_ALT_SWAP == MG_ALT_SWAP - 1) cswap_fma(a, b);
+    else cswap(a, b);
+}
+template <int I, int IEND, int R, int M, int K, int E>
+__device__ __forceinline__ void oe_stage(uint32_t (&v)[E]) {
+    if constexpr (I + R < IEND) {
+        cswap_k<K>(v[I], v[I + R]);
+        oe_stage<I + M, IEND, R, M, K + 1>(v);
+    }
+}
 template <int LO, int N, int R, int E>
 __device__ __forceinline__ void oe_merge(uint32_t (&v)[E]) {
     constexpr int M = 2 * R;
     if constexpr (M < N) {
         oe_merge<LO, N, M>(v);
         oe_merge<LO + R, N, M>(v);
-#pragma unroll
-        for (int i = LO + R; i + R < LO + N; i += M) cswap(v[i], v[i + R]);
+        oe_stage<LO + R, LO + N, R, M, 0>(v);
     } else {
-        cswap(v[LO], v[LO + R]);
+        cswap_k<LO / M>(v[LO], v[LO + R]);
     }
 }
 template <int K, int B, int E>
@@ -382,7 +413,15 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
     const uint32_t g = (uint32_t)(threadIdx.x & ((1 << XL) - 1));
     uint32_t inv = 0;
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = (v[i] << TB) | (g << 5) | (uint32_t)i;
+    for (int i = 0; i < E; ++i) {
+        if constexpr (MG_TAG_FMA) {  // disjoint bit fields: v * 2^TB + (g << 5 | i) as one IMAD
+            uint32_t t;
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(v[i]), "r"(c_mg_one << TB), "r"((g << 5) | (uint32_t)i));
+            v[i] = t;
+        } else {
+            v[i] = (v[i] << TB) | (g << 5) | (uint32_t)i;
+        }
+    }
     reg_stages<2, E>(v, inv);
 #pragma unroll
     for (int l = 1; l <= XL; ++l) {  // cross-lane level: blocks of 32 << l keys over 2^l lanes
@@ -409,9 +448,8 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 if (i & j) continue;
-                const uint32_t a = v[i], b = v[i + j];
-                v[i] = min(a, b);
-                v[i + j] = max(a, b);
+                if (MG_ALT_SWAP > 0 && (i % MG_ALT_SWAP) == MG_ALT_SWAP - 1) cswap_fma(v[i], v[i + j]);
+                else cswap(v[i], v[i + j]);
             }
         }
         // this lane's share of inv(A, B), h = 16 << l: B = tag bit 4 + l; positions 32 gl + i.  Lanes other
@@ -428,15 +466,29 @@ __device__ __forceinline__ uint32_t reg_sort_count(uint32_t (&v)[E]) {
         inv += (gl == 0 ? hb * hb + hb * (hb - 1) / 2 : 0u) - pos;
     }
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] >>= TB;
+    for (int i = 0; i < E; ++i) {
+        if constexpr (MG_TAG_FMA) {  // v >> TB as mul.hi by 2^(32 - TB)
+            uint32_t t;
+            asm("mul.hi.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(c_mg_one << (32 - TB)));
+            v[i] = t;
+        } else {
+            v[i] >>= TB;
+        }
+    }
     return inv;
 }
 
 // Opaque multipliers (1, -1, 2, 4 read from the kernel arguments) keep the bookkeeping on IMAD: ptxas
 // cannot strength-reduce a multiply by an unknown register into ALU shifts / adds.
 struct MgConst {
-    uint32_t one, m1, two, four, s16, c68, m68;
+    uint32_t one, m1, two, four, s16, c68, m68, hi6;  // hi6 = 2^(32 - PBS): c >> PBS as mul.hi (FMA pipe)
 };
+#ifndef MG_LOOP_FMA_MAX  // merge loop: the larger head as h1 + h2 - min in two IMADs instead of a VIMNMX
+#define MG_LOOP_FMA_MAX 0
+#endif
+#ifndef MG_LOOP_HI  // merge loop: the pad term c >> PBS as mul.hi on the FMA pipe instead of SHF on the ALU
+#define MG_LOOP_HI 0
+#endif
 __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -508,7 +560,8 @@ __device__ __forceinline__ uint32_t merge_level_regs(const uint16_t* src, int t,
 #pragma unroll
     for (int o = 0; o < E; ++o) {
         const uint32_t cm = min(h1, h2);
-        h1 = max(h1, h2);
+        if constexpr (MG_LOOP_FMA_MAX && !CHECKED) h1 = imad(cm, K.m1, imad(h1, K.one, h2));
+        else h1 = max(h1, h2);
         if constexpr (CHECKED) {  // runs shorter than a 32-key block: explicit end test
             const uint32_t org = cm & 1u;
             Y = imad(org, ia, Y);
@@ -541,7 +594,10 @@ __device__ __forceinline__ uint32_t merge_level_regs(const uint16_t* src, int t,
                 : "=r"(org), "+r"(ia), "+r"(ib), "+r"(Y), "=r"(c)
                 : "r"(cm), "r"(K.one));
             if (o + 1 < E) {
-                const uint32_t addr = imad(c >> PBS, K.four, imad(c, K.two, base + 2u));
+                uint32_t blk;
+                if constexpr (MG_LOOP_HI) asm("mul.hi.u32 %0, %1, %2;" : "=r"(blk) : "r"(c), "r"(K.hi6));
+                else blk = c >> PBS;
+                const uint32_t addr = imad(blk, K.four, imad(c, K.two, base + 2u));
                 h2 = imad(lds_u16(addr), K.s16, org);
             }
         }
@@ -1022,7 +1078,7 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
     const size_t padded = (size_t)a.B * L + 2 * (((size_t)a.B * L) >> PBS) + 2 +
                           (a.B == 1 ? L + 2 * ((size_t)L >> PBS) + 2 : 0);
     size_t smem = padded * sizeof(uint16_t);
-    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u, 2u * (PB + 2), (uint32_t)(-2 * (PB + 2))};
+    a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u, 2u * (PB + 2), (uint32_t)(-2 * (PB + 2)), 1u << (32 - PBS)};
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = std::min<int64_t>(a.count, (int64_t)num_sms());
     TB_CUDA_TRY(launch_pdl(merge_pairs_kernel, dim3((unsigned)grid), dim3(MG_THREADS), smem, static_cast<cudaStream_t>(stream), a));
