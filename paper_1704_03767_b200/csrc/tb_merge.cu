@@ -28,6 +28,8 @@
 //                          = L1 (L1 - 1) / 2 - ties(H1) + cross(H1, H2),
 // and cross = sum key(H1) - L1 (L1 - 1) / 2 + ties(H1), ties(H1) being the
 // equal-key pairs inside H1 (a scan of sorted H1).
+#include <cstdlib>
+
 #include "tb_common.cuh"
 
 namespace tb {
@@ -848,12 +850,159 @@ struct MergeArgs {
     int64_t job_lo, count;
     int32_t B;       // 1 or 2 blocks
     int32_t L;       // padded block length (power of two)
+    int32_t P;       // merge_multi_kernel: pairs per CTA (65536 / L)
     int32_t* num;
     unsigned long long* nd;
     unsigned long long* n3;
     uint8_t* heavy_ws;  // per-CTA scratch of heavy_group_counts
     MgConst k;  // {1, -1, 2, 4, 65536, 68, -68}
 };
+
+// One pair on the whole CTA: B = 1 (n <= 32768) sorts keys with the ping-pong block tmp, B = 2 the two
+// 32768-key halves in place plus the closed-form cross term.  Every thread calls it (CTA barriers inside).
+__device__ __forceinline__ void merge_one_pair(const MergeArgs& p, int64_t idx, uint16_t* keys, uint16_t* tmp,
+                                            int64_t* red, int& sX, int& sY) {
+    const int tid = threadIdx.x;
+    const int64_t n = p.n;
+    const int L = p.L;
+    const int64_t L1 = p.B == 2 ? L : n;  // real keys in block 0
+    const MgConst K = p.k;
+    int64_t y, x;
+    job_coord(p.job_lo + idx, p.m, y, x);
+    const int32_t* pu = p.pos + y * n;      // u-order positions
+    const uint16_t* kv = p.keys + x * n;    // v min-rank keys
+#if MG_PREFETCH
+    // the next pair's v keys (and u positions when its row changes) into L2 while this pair sorts: the
+    // scatter at the top of a pair is the kernel's one latency-bound phase
+    if (idx + gridDim.x < p.count) {
+        int64_t y2, x2;
+        job_coord(p.job_lo + idx + gridDim.x, p.m, y2, x2);
+        const char* k2 = reinterpret_cast<const char*>(p.keys + x2 * n);
+        for (int64_t b = (int64_t)tid * 128; b < 2 * n; b += (int64_t)MG_THREADS * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(k2 + b));
+        if (y2 != y) {
+            const char* p2 = reinterpret_cast<const char*>(p.pos + y2 * n);
+            for (int64_t b = (int64_t)tid * 128; b < 4 * n; b += (int64_t)MG_THREADS * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p2 + b));
+        }
+    }
+#endif
+
+    // pads (0xFFFE: real keys are < n <= 65535 whenever pads exist, and 0xFFFF is the merge
+    // loop's INF) first, then scatter w[pos_u[e]] = key_v[e]
+    for (int64_t i = n + tid; i < (int64_t)p.B * L; i += MG_THREADS) keys[sw((int)i)] = 0xFFFE;
+    if (tid == 0) sX = sY = -1;
+    __syncthreads();
+    if ((n & 3) == 0) {  // 16-byte loads of u-positions, 8-byte loads of v keys
+        const int4* pu4 = reinterpret_cast<const int4*>(pu);
+        const uint2* kv4 = reinterpret_cast<const uint2*>(kv);
+        for (int64_t e = tid; e < (n >> 2); e += MG_THREADS) {
+            const int4 P = pu4[e];
+            const uint2 V = kv4[e];
+            keys[sw(P.x)] = (uint16_t)(V.x & 0xFFFFu);
+            keys[sw(P.y)] = (uint16_t)(V.x >> 16);
+            keys[sw(P.z)] = (uint16_t)(V.y & 0xFFFFu);
+            keys[sw(P.w)] = (uint16_t)(V.y >> 16);
+            if (n == 65536 && (V.x >= 0xFFFE0000u || V.y >= 0xFFFE0000u ||
+                               (V.x & 0xFFFEu) == 0xFFFEu || (V.y & 0xFFFEu) == 0xFFFEu)) {
+                const int pp[4] = {P.x, P.y, P.z, P.w};
+                const uint32_t kk[4] = {V.x & 0xFFFFu, V.x >> 16, V.y & 0xFFFFu, V.y >> 16};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (kk[q] == 0xFFFFu) sX = pp[q];
+                    if (kk[q] == 0xFFFEu) sY = pp[q];
+                }
+            }
+        }
+    } else {
+        for (int64_t e = tid; e < n; e += MG_THREADS) keys[sw(pu[e])] = kv[e];
+    }
+    __syncthreads();
+
+    // within-u-group pairs: inv_g and joint ties (n3)
+    uint32_t inv_g = 0, ties = 0;
+    if (p.maxgrp[y] <= MG_SMALL_GROUP) {  // few small groups (the usual case): walk the compact list
+        const int32_t* gl = p.groups + y * n;
+        const int32_t ng = p.ngroups[y];
+        for (int32_t k = tid; k < ng; k += MG_THREADS) {
+            const int32_t g0 = gl[2 * k], gl_len = gl[2 * k + 1];
+            for (int32_t qa = g0; qa < g0 + gl_len; ++qa) {
+                const uint16_t wq = keys[sw(qa)];
+                for (int32_t qb = qa + 1; qb < g0 + gl_len; ++qb) {
+                    const uint16_t wt = keys[sw(qb)];
+                    inv_g += (wq > wt);
+                    ties += (wq == wt);
+                }
+            }
+        }
+    } else {  // a large u tie group: the O(n log n) segmented radix count
+        heavy_group_counts(keys, p.groups + y * n, p.ngroups[y], n, heavy_ws(p.heavy_ws, n), inv_g, ties);
+    }
+    __syncthreads();
+
+    // n = 65536: key 65535 (a unique row maximum X) would collide with INF.  Sort it as 65534;
+    // that only merges it with a unique second maximum Y (key 65534, if any), so add back the
+    // X-before-Y inversion when both sit in the same half, and undo the change in the H1 key sum
+    // and tie scan of the cross term below.
+    int64_t clamp_fix = 0;
+    if (n == 65536 && sX >= 0) {
+        const bool x1 = sX < L, y1 = sY >= 0 && sY < L;
+        if (tid == 0) {
+            keys[sw(sX)] = 0xFFFE;
+            if (sY >= 0 && x1 == y1 && sX < sY) clamp_fix += 1;
+            if (x1) clamp_fix += 1 - (y1 ? 1 : 0);
+        }
+        __syncthreads();
+    }
+
+    // inv(w)
+    uint32_t inv;
+    int64_t cross = 0;
+    if (p.B == 1) {
+        inv = sort_count_any(keys, tmp, L, K);
+    } else {
+        inv = sort_count_halves<2 * MG_HALF / MG_THREADS>(keys, L, K);  // L = 32768: sw(L + i) = sw(L) + sw(i)
+        // cross(H1, H2) = sum key(H1) - L1 (L1 - 1) / 2 + ties(H1) (header); the -L1 (L1 - 1) / 2
+        // is applied once after the reduction.  H1 = keys[0, L) is sorted and holds no pads.
+        constexpr int CE = MG_HALF / MG_THREADS;  // 32 sorted keys per thread
+        uint32_t v[CE];
+        load_run<CE>(keys, tid, v);
+        const int p0 = tid * CE;
+        uint32_t prev = tid ? keys[sw(p0 - 1)] : 0xFFFFFFFFu;
+        int first = p0;  // first index of the equal-key run holding the current key
+        if (v[0] == prev) {  // run continues from the previous thread: lower_bound(H1, v[0])
+            int lo = 0, hi = p0 - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (keys[sw(mid)] < v[0]) lo = mid + 1;
+                else hi = mid;
+            }
+            first = lo;
+        }
+        uint32_t ksum = 0, ties = 0;
+#pragma unroll
+        for (int q = 0; q < CE; ++q) {
+            ksum += v[q];
+            if (q > 0 && v[q] != v[q - 1]) first = p0 + q;
+            ties += (uint32_t)(p0 + q - first);
+        }
+        cross = (int64_t)ksum + (int64_t)ties;
+    }
+
+    // n_d = inv(w) - sum_g inv_g(w): one reduction of (inv - inv_g), one of the joint ties
+    const int64_t nd_all = block_reduce_sum((int64_t)(int32_t)inv + cross + clamp_fix - (int64_t)inv_g, red) -
+                           (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
+    const int64_t tot_t = block_reduce_sum((int64_t)ties, red);
+    if (tid == 0) {
+        const int64_t nd = nd_all;
+        const int64_t n3 = tot_t;
+        const int64_t num = p.n0 - (int64_t)p.n1[y] - (int64_t)p.n1[x] + n3 - 2 * nd;  // result.py:42
+        p.num[idx] = (int32_t)num;
+        if (p.nd) p.nd[idx] = (unsigned long long)nd;
+        if (p.n3) p.n3[idx] = (unsigned long long)n3;
+    }
+    __syncthreads();
+}
 
 __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p) {
     pdl_wait();
@@ -862,157 +1011,152 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_pairs_kernel(MergeArgs p)
     uint16_t* tmp = keys + sw(p.B * p.L) + 2;               // L keys (padded layout; B == 1 only)
     __shared__ int64_t red[32];
     const int tid = threadIdx.x;
-    const int64_t n = p.n;
     const int L = p.L;
-    const int64_t L1 = p.B == 2 ? L : n;  // real keys in block 0
-    const MgConst K = p.k;
     __shared__ int sX, sY;  // u-order positions of keys 0xFFFF / 0xFFFE (n = 65536 only)
     if (tid == 0 && L >= 64) {  // INF look-ahead slots behind the last block of every sorted region
         reinterpret_cast<uint32_t*>(keys)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
         if (p.B == 1) reinterpret_cast<uint32_t*>(tmp)[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
         if (p.B == 2) reinterpret_cast<uint32_t*>(keys + sw(L))[swp_words(L >> 1) - 1] = 0xFFFFFFFFu;
     }
+    for (int64_t idx = blockIdx.x; idx < p.count; idx += gridDim.x) merge_one_pair(p, idx, keys, tmp, red, sX, sY);
+    pdl_trigger();
+}
 
-    for (int64_t idx = blockIdx.x; idx < p.count; idx += gridDim.x) {
-        int64_t y, x;
-        job_coord(p.job_lo + idx, p.m, y, x);
-        const int32_t* pu = p.pos + y * n;      // u-order positions
-        const uint16_t* kv = p.keys + x * n;    // v min-rank keys
-#if MG_PREFETCH
-        // the next pair's v keys (and u positions when its row changes) into L2 while this pair sorts: the
-        // scatter at the top of a pair is the kernel's one latency-bound phase
-        if (idx + gridDim.x < p.count) {
-            int64_t y2, x2;
-            job_coord(p.job_lo + idx + gridDim.x, p.m, y2, x2);
-            const char* k2 = reinterpret_cast<const char*>(p.keys + x2 * n);
-            for (int64_t b = (int64_t)tid * 128; b < 2 * n; b += (int64_t)MG_THREADS * 128)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(k2 + b));
-            if (y2 != y) {
-                const char* p2 = reinterpret_cast<const char*>(p.pos + y2 * n);
-                for (int64_t b = (int64_t)tid * 128; b < 4 * n; b += (int64_t)MG_THREADS * 128)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p2 + b));
-            }
-        }
-#endif
-
-        // pads (0xFFFE: real keys are < n <= 65535 whenever pads exist, and 0xFFFF is the merge
-        // loop's INF) first, then scatter w[pos_u[e]] = key_v[e]
-        for (int64_t i = n + tid; i < (int64_t)p.B * L; i += MG_THREADS) keys[sw((int)i)] = 0xFFFE;
-        if (tid == 0) sX = sY = -1;
-        __syncthreads();
-        if ((n & 3) == 0) {  // 16-byte loads of u-positions, 8-byte loads of v keys
-            const int4* pu4 = reinterpret_cast<const int4*>(pu);
-            const uint2* kv4 = reinterpret_cast<const uint2*>(kv);
-            for (int64_t e = tid; e < (n >> 2); e += MG_THREADS) {
-                const int4 P = pu4[e];
-                const uint2 V = kv4[e];
-                keys[sw(P.x)] = (uint16_t)(V.x & 0xFFFFu);
-                keys[sw(P.y)] = (uint16_t)(V.x >> 16);
-                keys[sw(P.z)] = (uint16_t)(V.y & 0xFFFFu);
-                keys[sw(P.w)] = (uint16_t)(V.y >> 16);
-                if (n == 65536 && (V.x >= 0xFFFE0000u || V.y >= 0xFFFE0000u ||
-                                   (V.x & 0xFFFEu) == 0xFFFEu || (V.y & 0xFFFEu) == 0xFFFEu)) {
-                    const int pp[4] = {P.x, P.y, P.z, P.w};
-                    const uint32_t kk[4] = {V.x & 0xFFFFu, V.x >> 16, V.y & 0xFFFFu, V.y >> 16};
+// ------------------------------------------------------------------ several pairs per CTA (n <= 32768)
+// With L <= 32768 keys per pair, P = 65536 / L pairs share a CTA: their blocks are consecutive in one
+// padded array of 65536 keys, so the register leaf runs over the array exactly as for the two halves of
+// n > 32768 (leaf runs never cross a block), and the merge levels run per pair, 1024 / P threads with 64
+// outputs each, in place -- the same 64-output levels instead of E = L / 1024 outputs with a ping-pong
+// block.  Leaf counts are credited to the block a warp's keys lie in, merge and tie-group counts to the
+// thread's own pair.  A batch holding a pair with a large u tie group (heavy_group_counts needs the whole
+// CTA) runs its pairs one at a time through merge_one_pair.
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (kk[q] == 0xFFFFu) sX = pp[q];
-                        if (kk[q] == 0xFFFEu) sY = pp[q];
-                    }
-                }
-            }
-        } else {
-            for (int64_t e = tid; e < n; e += MG_THREADS) keys[sw(pu[e])] = kv[e];
-        }
-        __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
-        // within-u-group pairs: inv_g and joint ties (n3)
-        uint32_t inv_g = 0, ties = 0;
-        if (p.maxgrp[y] <= MG_SMALL_GROUP) {  // few small groups (the usual case): walk the compact list
-            const int32_t* gl = p.groups + y * n;
-            const int32_t ng = p.ngroups[y];
-            for (int32_t k = tid; k < ng; k += MG_THREADS) {
-                const int32_t g0 = gl[2 * k], gl_len = gl[2 * k + 1];
-                for (int32_t qa = g0; qa < g0 + gl_len; ++qa) {
-                    const uint16_t wq = keys[sw(qa)];
-                    for (int32_t qb = qa + 1; qb < g0 + gl_len; ++qb) {
-                        const uint16_t wt = keys[sw(qb)];
-                        inv_g += (wq > wt);
-                        ties += (wq == wt);
-                    }
-                }
-            }
-        } else {  // a large u tie group: the O(n log n) segmented radix count
-            heavy_group_counts(keys, p.groups + y * n, p.ngroups[y], n, heavy_ws(p.heavy_ws, n), inv_g, ties);
-        }
+__global__ void __launch_bounds__(MG_THREADS, 1) merge_multi_kernel(MergeArgs p) {
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t mg_smem[];
+    uint16_t* keys = reinterpret_cast<uint16_t*>(mg_smem);  // P blocks of L keys = 65536 keys, padded layout
+    __shared__ int64_t red[32];
+    __shared__ int sX, sY, s_heavy;
+    __shared__ unsigned long long s_acc[2 * 32];  // per pair: inversions - within-group inversions, joint ties
+                                                  // (two's complement sums)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = p.n;
+    const int L = p.L, P = p.P;
+    const int G = MG_THREADS / P;  // threads per pair (>= 32: whole warps)
+    const int g = tid / G, t = tid - g * G;
+    uint16_t* blk = keys + g * sw(L);  // L is a multiple of the pad block: sw(g L) = g sw(L)
+    const MgConst K = p.k;
+    constexpr int TOT = 2 * MG_HALF;
+    if (tid < P + 1) {  // INF look-ahead slots in front of every block and behind the last
+        const int k0 = tid * L;
+        if (k0 > 0) reinterpret_cast<uint32_t*>(keys)[swp_words(k0 >> 1) - 1] = 0xFFFFFFFFu;
+    }
+    for (int64_t base = (int64_t)blockIdx.x * P; base < p.count; base += (int64_t)gridDim.x * P) {
+        if (tid == 0) s_heavy = 0;
+        if (tid < 2 * P) s_acc[tid] = 0;
         __syncthreads();
-
-        // n = 65536: key 65535 (a unique row maximum X) would collide with INF.  Sort it as 65534;
-        // that only merges it with a unique second maximum Y (key 65534, if any), so add back the
-        // X-before-Y inversion when both sit in the same half, and undo the change in the H1 key sum
-        // and tie scan of the cross term below.
-        int64_t clamp_fix = 0;
-        if (n == 65536 && sX >= 0) {
-            const bool x1 = sX < L, y1 = sY >= 0 && sY < L;
-            if (tid == 0) {
-                keys[sw(sX)] = 0xFFFE;
-                if (sY >= 0 && x1 == y1 && sX < sY) clamp_fix += 1;
-                if (x1) clamp_fix += 1 - (y1 ? 1 : 0);
+        const int64_t idx = base + g;
+        const bool valid = idx < p.count;
+        int64_t y = 0, x = 0;
+        if (valid) job_coord(p.job_lo + idx, p.m, y, x);
+        if (t == 0 && valid && p.maxgrp[y] > MG_SMALL_GROUP) atomicOr(&s_heavy, 1);
+        __syncthreads();
+        if (s_heavy) {  // one pair at a time on the whole CTA (keys = block 0, ping-pong = block 1)
+            MergeArgs q = p;
+            q.B = 1;
+            for (int k = 0; k < P && base + k < p.count; ++k)
+                merge_one_pair(q, base + k, keys, keys + sw(L), red, sX, sY);
+            if (tid < P + 1) {  // restore the block-boundary INF slots
+                const int k0 = tid * L;
+                if (k0 > 0) reinterpret_cast<uint32_t*>(keys)[swp_words(k0 >> 1) - 1] = 0xFFFFFFFFu;
             }
             __syncthreads();
+            continue;
         }
-
-        // inv(w)
-        uint32_t inv;
-        int64_t cross = 0;
-        if (p.B == 1) {
-            inv = sort_count_any(keys, tmp, L, K);
-        } else {
-            inv = sort_count_halves<2 * MG_HALF / MG_THREADS>(keys, L, K);  // L = 32768: sw(L + i) = sw(L) + sw(i)
-            // cross(H1, H2) = sum key(H1) - L1 (L1 - 1) / 2 + ties(H1) (header); the -L1 (L1 - 1) / 2
-            // is applied once after the reduction.  H1 = keys[0, L) is sorted and holds no pads.
-            constexpr int CE = MG_HALF / MG_THREADS;  // 32 sorted keys per thread
-            uint32_t v[CE];
-            load_run<CE>(keys, tid, v);
-            const int p0 = tid * CE;
-            uint32_t prev = tid ? keys[sw(p0 - 1)] : 0xFFFFFFFFu;
-            int first = p0;  // first index of the equal-key run holding the current key
-            if (v[0] == prev) {  // run continues from the previous thread: lower_bound(H1, v[0])
-                int lo = 0, hi = p0 - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (keys[sw(mid)] < v[0]) lo = mid + 1;
-                    else hi = mid;
+        // this pair's block: pads, then w[pos_u[e]] = key_v[e]
+        const int64_t real = valid ? n : 0;
+        for (int64_t i = real + t; i < L; i += G) blk[sw((int)i)] = 0xFFFE;
+        if (valid) {
+            const int32_t* pu = p.pos + y * n;
+            const uint16_t* kv = p.keys + x * n;
+            if ((n & 3) == 0) {
+                const int4* pu4 = reinterpret_cast<const int4*>(pu);
+                const uint2* kv4 = reinterpret_cast<const uint2*>(kv);
+                for (int64_t e = t; e < (n >> 2); e += G) {
+                    const int4 Pp = pu4[e];
+                    const uint2 V = kv4[e];
+                    blk[sw(Pp.x)] = (uint16_t)(V.x & 0xFFFFu);
+                    blk[sw(Pp.y)] = (uint16_t)(V.x >> 16);
+                    blk[sw(Pp.z)] = (uint16_t)(V.y & 0xFFFFu);
+                    blk[sw(Pp.w)] = (uint16_t)(V.y >> 16);
                 }
-                first = lo;
+            } else {
+                for (int64_t e = t; e < n; e += G) blk[sw(pu[e])] = kv[e];
             }
-            uint32_t ksum = 0, ties = 0;
-#pragma unroll
-            for (int q = 0; q < CE; ++q) {
-                ksum += v[q];
-                if (q > 0 && v[q] != v[q - 1]) first = p0 + q;
-                ties += (uint32_t)(p0 + q - first);
-            }
-            cross = (int64_t)ksum + (int64_t)ties;
         }
-
-        // n_d = inv(w) - sum_g inv_g(w): one reduction of (inv - inv_g), one of the joint ties
-        const int64_t nd_all = block_reduce_sum((int64_t)(int32_t)inv + cross + clamp_fix - (int64_t)inv_g, red) -
-                               (p.B == 2 ? L1 * (L1 - 1) / 2 : 0);
-        const int64_t tot_t = block_reduce_sum((int64_t)ties, red);
-        if (tid == 0) {
-            const int64_t nd = nd_all;
-            const int64_t n3 = tot_t;
+        __syncthreads();
+        // within-u-group pairs of this pair (small groups only here)
+        int64_t mine = 0, ties = 0;
+        if (valid) {
+            const int32_t* gl = p.groups + y * n;
+            const int32_t ng = p.ngroups[y];
+            uint32_t ig = 0, tt = 0;
+            for (int32_t k = t; k < ng; k += G) {
+                const int32_t g0 = gl[2 * k], gl_len = gl[2 * k + 1];
+                for (int32_t qa = g0; qa < g0 + gl_len; ++qa) {
+                    const uint16_t wq = blk[sw(qa)];
+                    for (int32_t qb = qa + 1; qb < g0 + gl_len; ++qb) {
+                        const uint16_t wt = blk[sw(qb)];
+                        ig += (wq > wt);
+                        tt += (wq == wt);
+                    }
+                }
+            }
+            mine = -(int64_t)ig;
+            ties = tt;
+        }
+        __syncthreads();
+        // register leaf over the whole 65536-key array, two passes of 32768 keys; a warp's 1024 keys lie
+        // in one block (L >= 2048), its leaf count goes to that block's pair
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            uint16_t* half = keys + h * sw(MG_HALF);
+            constexpr int E = 32;
+            uint32_t v[E];
+            load_run<E>(half, tid, v);
+            const int64_t lc = warp_sum64((int64_t)(int32_t)reg_sort_count<E, LEAF_XL<E>>(v));
+            store_run<E>(half, tid, v);
+            store_lookahead<E>(half, tid, E << LEAF_XL<E>, v[0]);
+            if (lane == 0) atomicAdd(&s_acc[2 * ((h * MG_HALF + warp * 32 * E) / L)], (unsigned long long)lc);
+        }
+        __syncthreads();
+        uint32_t inv = 0;
+#pragma unroll 1
+        for (int W = 32 << LEAF_XL<32>; W < L; W <<= 1) inv += merge_level_inplace<2 * MG_HALF / MG_THREADS>(blk, t, W, K);
+        mine += (int64_t)(int32_t)inv;
+        const int64_t wm = warp_sum64(mine), wt = warp_sum64(ties);
+        if (lane == 0) {
+            atomicAdd(&s_acc[2 * g], (unsigned long long)wm);
+            atomicAdd(&s_acc[2 * g + 1], (unsigned long long)wt);
+        }
+        __syncthreads();
+        if (t == 0 && valid) {
+            const int64_t nd = (int64_t)s_acc[2 * g], n3 = (int64_t)s_acc[2 * g + 1];
             const int64_t num = p.n0 - (int64_t)p.n1[y] - (int64_t)p.n1[x] + n3 - 2 * nd;  // result.py:42
             p.num[idx] = (int32_t)num;
             if (p.nd) p.nd[idx] = (unsigned long long)nd;
             if (p.n3) p.n3[idx] = (unsigned long long)n3;
         }
         __syncthreads();
+        (void)TOT;
     }
     pdl_trigger();
 }
-
 }  // namespace tb
 
 using namespace tb;
@@ -1079,6 +1223,17 @@ extern "C" int tb_merge_pairs(const uint16_t* keys, const int32_t* pos, const in
                           (a.B == 1 ? L + 2 * ((size_t)L >> PBS) + 2 : 0);
     size_t smem = padded * sizeof(uint16_t);
     a.k = MgConst{1u, 0xFFFFFFFFu, 2u, 4u, 0x10000u, 2u * (PB + 2), (uint32_t)(-2 * (PB + 2)), 1u << (32 - PBS)};
+    // n in (1024, 32768]: several pairs per CTA with 64-output in-place merge levels (TB_MERGE_MULTI=0: off)
+    static const bool kMulti = [] { const char* e = std::getenv("TB_MERGE_MULTI"); return !(e && e[0] == '0'); }();
+    if (kMulti && a.B == 1 && L >= 2048) {
+        a.P = 2 * MG_HALF / L;
+        const size_t msmem = ((size_t)2 * MG_HALF + 2 * (((size_t)2 * MG_HALF) >> PBS) + 2) * sizeof(uint16_t);
+        TB_CUDA_TRY(cudaFuncSetAttribute(merge_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+        const int64_t grid = std::min<int64_t>((a.count + a.P - 1) / a.P, (int64_t)num_sms());
+        TB_CUDA_TRY(launch_pdl(merge_multi_kernel, dim3((unsigned)grid), dim3(MG_THREADS), msmem,
+                               static_cast<cudaStream_t>(stream), a));
+        return check_launch("merge_multi_kernel");
+    }
     TB_CUDA_TRY(cudaFuncSetAttribute(merge_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = std::min<int64_t>(a.count, (int64_t)num_sms());
     TB_CUDA_TRY(launch_pdl(merge_pairs_kernel, dim3((unsigned)grid), dim3(MG_THREADS), smem, static_cast<cudaStream_t>(stream), a));

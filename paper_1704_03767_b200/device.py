@@ -36,21 +36,23 @@ from .pairindex import job_coord
 # seconds per job id.  A shape (m, n) takes the path with the smaller m * per_row + J * per_job
 # (J = m(m+1)/2 job ids), the GEMM only while its sign matrix fits the free device memory.
 DISPATCH_TABLE = (
-    # n, gemm pack s/row, gemm s/job, m_gemm, merge prep s/row, merge s/job
-    (1024, 1.123e-07, 1.982e-10, 2048, 3.258e-07, 9.437e-08),
-    (2048, 3.748e-07, 9.585e-10, 2048, 3.764e-07, 8.978e-08),
-    (4096, 1.109e-06, 7.797e-09, 2048, 5.035e-07, 1.046e-07),
-    (5792, 2.324e-06, 1.560e-08, 2048, 6.497e-07, 1.372e-07),
-    (6144, 3.731e-06, 3.162e-08, 2048, 6.782e-07, 1.371e-07),
-    (8192, 5.975e-06, 5.664e-08, 1990, 8.467e-07, 1.388e-07),
-    (12288, 1.171e-05, 1.698e-07, 884, 1.131e-06, 1.936e-07),
-    (16384, 2.130e-05, 3.663e-07, 497, 1.640e-06, 1.989e-07),
-    (24576, 4.665e-05, 1.105e-06, 221, 2.675e-06, 2.904e-07),
-    (32767, 8.727e-05, 4.589e-06, 124, 4.203e-06, 3.008e-07),
+    # n, gemm pack s/row, gemm s/job, m_gemm, merge prep s/row, merge s/job  (tools/exp_dispatch.py on a B200,
+    # profiles/r02_dispatch_table.jsonl; merge with several pairs per CTA for 1024 < n <= 32768)
+    (1024, 1.113e-07, 2.028e-10, 2048, 3.645e-07, 9.205e-08),
+    (2048, 3.730e-07, 9.779e-10, 2048, 3.954e-07, 1.133e-08),
+    (4096, 1.108e-06, 7.871e-09, 2048, 5.259e-07, 2.457e-08),
+    (5792, 2.328e-06, 1.575e-08, 2048, 6.789e-07, 5.301e-08),
+    (6144, 3.744e-06, 3.086e-08, 2048, 7.029e-07, 5.312e-08),
+    (8192, 6.047e-06, 5.775e-08, 1990, 8.813e-07, 5.447e-08),
+    (12288, 1.178e-05, 1.726e-07, 884, 1.155e-06, 1.150e-07),
+    (16384, 2.141e-05, 3.643e-07, 497, 1.672e-06, 1.185e-07),
+    (24576, 4.700e-05, 1.424e-06, 221, 2.760e-06, 2.508e-07),
+    (32767, 8.747e-05, 4.628e-06, 124, 4.324e-06, 2.633e-07),
 )
 D2H_PIECE_BYTES = 256 << 20
 TIED_SPARSE_FRAC = 0.35  # |S| GEMM over the tied rows only while they are at most this share of the rows
-GEMM_MAX_N = 8192  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides)
+GEMM_MAX_N = 7680  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides; merge
+# with several pairs per CTA: n = 6144 GEMM 31 vs merge 53 ns per job, n = 8192 58 vs 54 ns)
 RANK_ROWS_MAX_N = 8192  # tb_rank_rows' row limit; wider GEMM-path rows are ranked by tb_rank_dense
 SIGN_MAX_N = 32767      # tb_sign_pack: 15-bit ranks
 PATHS = ("gemm", "merge")

@@ -280,6 +280,34 @@ def test_merge_block_sizes_vs_oracle(eng, oracle, n):
         assert (int(got_nd[k]), int(got_n3[k])) == (nd, n3), (n, i, j)
 
 
+@pytest.mark.parametrize("n", [2048, 3001, 8193, 16384, 20000, 32768])
+def test_merge_multi_pair_ctas_vs_oracle(eng, oracle, n):
+    """n <= 32768: 65536 / L pairs share a CTA (merge_multi_kernel: one padded array, per-pair in-place
+    64-output merge levels, leaf counts credited per block).  Tie-free, light-tie (small u groups), monotone
+    and short-run rows, plus one heavy-tie row whose batches fall back to one pair at a time; every pair's
+    n_d / n3 / numerator vs the oracle."""
+    rng = np.random.default_rng(n + 11)
+    m = 37
+    rows = []
+    for r in range(m):
+        k = r % 4
+        if k == 0:
+            rows.append(rng.permutation(n))
+        elif k == 1:
+            rows.append(rng.integers(0, n // 2, n))  # many groups of 2-3
+        elif k == 2:
+            rows.append(np.arange(n) if r % 8 == 2 else np.arange(n)[::-1])
+        else:
+            rows.append(rng.permutation(n) // 2)  # pairs
+    rows[20] = rng.integers(0, 4, n)  # heavy groups: batches holding row 20 run pair by pair
+    ranks = np.stack([oracle.rank_transform(r) for r in rows])
+    res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="merge", full_counts=True).validate()
+    pi, pj, num, counts = _full_oracle(oracle, ranks)
+    np.testing.assert_array_equal(res.numerator.cpu().numpy().astype(np.int64), num)
+    np.testing.assert_array_equal(res.n_d.cpu().numpy(), counts[:, 0])
+    np.testing.assert_array_equal(res.n3.cpu().numpy(), counts[:, 3])
+
+
 def test_merge_row_maximum_clamp(eng, oracle):
     """n = 65536: key 65535 (a unique row maximum) is sorted as 65534 (0xFFFF is the merge loop's
     look-ahead INF) and corrected.  The maximum and a unique second maximum placed in the same half

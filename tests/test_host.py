@@ -260,7 +260,7 @@ def test_dispatcher_cost_model(monkeypatch):
     monkeypatch.setattr(torch.cuda, "mem_get_info", lambda dev=None: (170 << 30, 180 << 30))
     for (m, n), want in {(256, 200): "gemm", (2048, 1000): "gemm", (16384, 500): "gemm", (65536, 1024): "gemm",
                          (1024, 65536): "merge", (128, 32767): "merge", (4, 9000): "merge",
-                         (2000, 8192): "gemm"}.items():
+                         (2000, 6144): "gemm", (2000, 8192): "merge"}.items():
         assert choose_path(n, m=m, eng=eng) == want, (m, n)
     assert choose_path(1000) == "gemm" and choose_path(9000) == "merge"  # no shape: the large-m crossover
     monkeypatch.setattr(torch.cuda, "mem_get_info", lambda dev=None: (1 << 30, 180 << 30))
