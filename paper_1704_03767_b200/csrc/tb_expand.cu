@@ -1,10 +1,13 @@
 // Host side of the compact record stream (tb_records_compact): expands (numerator, n3) pairs into the
 // reference's 48-byte CELL_DTYPE records (engine.py:45-55) in emission order (pairindex.py:116-129), on
-// host threads with streaming stores.  compute_all_pairs runs it for some passes while the copy engine
+// host threads (a persistent pool) with streaming stores.  compute_all_pairs runs it for some passes while the copy engine
 // streams full records for the others, so a pass reaches the sink over two paths at once: PCIe carries
 // 8 bytes per record instead of 48 for the expanded ones.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 #include <emmintrin.h>
@@ -50,6 +53,60 @@ static void expand_tiles(const uint2* cmp, const uint64_t* n1, int64_t m, int64_
     _mm_sfence();  // streaming stores are weakly ordered: drain them before the thread reports done
 }
 
+// Persistent expansion workers: a config-5 call expands ~400 batches; spawning a dozen std::threads per
+// batch cost more than the batch's own page of work at the small end.  One call at a time owns the pool
+// (concurrent callers queue on `call_mu`); the caller thread runs part 0 itself.
+class ExpandPool {
+  public:
+    void run(int parts, const std::function<void(int)>& fn) {
+        std::lock_guard<std::mutex> call(call_mu_);
+        ensure(parts - 1);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            next_ = 1;
+            parts_ = parts;
+            pending_ = parts - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+  private:
+    void ensure(int n) {
+        while ((int)workers_.size() < n) workers_.emplace_back([this] { loop(); });
+    }
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return gen_ != seen && next_ < parts_; });
+            const int part = next_++;
+            if (next_ >= parts_) seen = gen_;
+            const std::function<void(int)>* fn = fn_;
+            lk.unlock();
+            (*fn)(part);
+            lk.lock();
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> workers_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int next_ = 0, parts_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+};
+
+static ExpandPool& expand_pool() {
+    static ExpandPool* pool = new ExpandPool();  // never destroyed: workers live for the process
+    return *pool;
+}
+
 }  // namespace tb
 
 using namespace tb;
@@ -70,13 +127,11 @@ extern "C" int tb_expand_records(const void* compact, const uint64_t* n1_rows, i
     if (nt == 1) {
         expand_tiles(cmp, n1_rows, m, n0, q, w, tile_lo, tile_lo + ntiles, base0, naive, out);
     } else {
-        std::vector<std::thread> th;
-        th.reserve(nt);
-        for (int k = 0; k < nt; ++k) {
+        const std::function<void(int)> part = [&](int k) {
             const int64_t a = tile_lo + ntiles * k / nt, b = tile_lo + ntiles * (k + 1) / nt;
-            th.emplace_back(expand_tiles, cmp, n1_rows, m, n0, q, w, a, b, base0, naive, out);
-        }
-        for (auto& t : th) t.join();
+            expand_tiles(cmp, n1_rows, m, n0, q, w, a, b, base0, naive, out);
+        };
+        expand_pool().run(nt, part);
     }
     _mm_sfence();
     return TB_OK;
