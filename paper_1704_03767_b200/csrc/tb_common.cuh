@@ -46,6 +46,8 @@ int table_mark_used(DevTable& t, cudaStream_t st);
 // magnitude < 2^24 when K < 2^24), then accum_convert writes the int32 numerators.
 int accum_workspace(int64_t span, float** ws, cudaStream_t st);
 int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st);
+// The same workspace holding int32 sums (wide-K FP4 items add exact int32 partials): copy out, re-zero.
+int accum_convert_i32(int32_t* ws, int64_t span, int32_t* num, cudaStream_t st);
 // The current device's workspace was converted and re-zeroed inside the GEMM (split-K fixup): clean.
 int accum_mark_clean();
 

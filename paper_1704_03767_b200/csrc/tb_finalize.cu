@@ -280,6 +280,27 @@ __global__ void __launch_bounds__(256) accum_convert_kernel(float* __restrict__ 
     pdl_trigger();
 }
 
+__global__ void __launch_bounds__(256) accum_convert_i32_kernel(int32_t* __restrict__ ws, int64_t span,
+                                                               int32_t* __restrict__ num) {
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < span; i += (int64_t)gridDim.x * blockDim.x) {
+        num[i] = ws[i];
+        ws[i] = 0;  // 0 is also 0.0f: the workspace stays clean for either kind of sum
+    }
+    pdl_trigger();
+}
+
+int accum_convert_i32(int32_t* ws, int64_t span, int32_t* num, cudaStream_t st) {
+    if (span <= 0) return TB_OK;
+    const int64_t blocks = std::min<int64_t>((span + 255) / 256, (int64_t)num_sms() * 8);
+    TB_CUDA_TRY(launch_pdl(accum_convert_i32_kernel, dim3((unsigned)blocks), dim3(256), 0, st, ws, span, num));
+    const int rc = check_launch("accum_convert_i32_kernel");
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);
+    if (rc == TB_OK && dev >= 0 && dev < TB_MAX_DEVICES) g_accum[dev].dirty = false;
+    return rc;
+}
+
 int accum_mark_clean() {
     const int dev = current_device();
     std::lock_guard<std::mutex> lock(g_native_state_mutex);

@@ -71,6 +71,9 @@ struct Gemm4Args {
     const int32_t* item_unit;
     const int32_t* unit_splits;
     int32_t* unit_cnt;
+    // K >= 2^24 (n > 5792): every unit is split into items of <= 65535 k-blocks, whose f32 sums stay exact
+    // integers (< 2^24); the items then add them as int32 (red.add.s32 into acc reinterpreted as int32)
+    int32_t int_red;
     // fused finalize (direct plans): tau_b[j] = tau_b_ieee(num, n1[y], n1[x], n0) instead of num[j]
     double* tau_b;
     const unsigned long long* n1;
@@ -321,7 +324,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                             if (hi64 > span - j0) hi64 = span - j0;
                             const int lo = (int)(lo64 < 0 ? 0 : (lo64 > 16 ? 16 : lo64));
                             const int hi = (int)(hi64 < 0 ? 0 : (hi64 > 16 ? 16 : hi64));
-                            if (lo < hi) {
+                            if (lo < hi && p.int_red) {  // exact int32 partial sums (wide K)
+                                int32_t* q0 = reinterpret_cast<int32_t*>(p.acc) + j0;
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    if (i >= lo && i < hi)
+                                        asm volatile("red.global.add.s32 [%0], %1;" ::"l"(q0 + i),
+                                                     "r"(__float2int_rn(__uint_as_float(r[i]))) : "memory");
+                            } else if (lo < hi) {
                                 uint32_t v[16];
 #pragma unroll
                                 for (int i = 0; i < 16; ++i) v[i] = (i >= lo && i < hi) ? r[i] : 0u;
@@ -529,6 +539,9 @@ static double plan_items4(const std::vector<int32_t>& code, const std::vector<in
     return *std::max_element(load.begin(), load.end());
 }
 
+// K-blocks per item for exact f32 partial sums: 65535 x 256 e2m1 elements < 2^24
+constexpr int32_t KB_EXACT = 65535;
+
 static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, int32_t forced, int pairs,
                        cudaStream_t st, Plan4** out) {
     std::lock_guard<std::mutex> lock(g_native_state_mutex);  // host threads share the caches
@@ -607,6 +620,9 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
             }
         }
     }
+    // wide K: no item may span more than KB_EXACT k-blocks (its f32 sums must stay exact integers)
+    const int32_t min_splits = (nkb + KB_EXACT - 1) / KB_EXACT;
+    for (int32_t& v : best_su) v = std::max(v, min_splits);
     std::vector<int4> items;
     std::vector<int32_t> item_unit;
     const double span_est = code.empty() ? 0.0 : plan_items4(code, nb, ncols, best_su, nkb, pairs, &items, &item_unit);
@@ -678,7 +694,7 @@ static int lockstep_state(unsigned long long** prog, uint32_t* epoch, int32_t* l
 int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi, int32_t splits,
              int32_t* num, cudaStream_t st, double* tau_b, const uint64_t* n1, int64_t n, int* fused) {
     if (fused) *fused = 0;
-    if (K >= (int64_t(1) << 24)) return fail(TB_ERR_CAPACITY, "gemm fp4: K=%lld needs exact f32 sums (< 2^24)", (long long)K);
+    const bool wide = K >= (int64_t(1) << 24);  // items of <= KB_EXACT k-blocks, int32 partial sums
     if (m >= (int64_t(1) << 16) * g4::UM) return fail(TB_ERR_CAPACITY, "gemm fp4: m too large");
     int rc;
     Gemm4Args p{};
@@ -694,6 +710,8 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.job_lo = job_lo;
     p.job_hi = job_hi;
     p.num = num;
+    p.int_red = wide ? 1 : 0;
+    if (wide && !p.partial) return fail(TB_ERR_CONFIG, "gemm fp4: wide K needs a split plan");
     if (tau_b && !p.partial) {
         p.tau_b = tau_b;
         p.n1 = reinterpret_cast<const unsigned long long*>(n1);
@@ -707,7 +725,7 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     // launch on configs 1-2 (config 1 0.039 -> 0.051 ms, config 2 0.540 -> 0.553 ms per step; config 3 within
     // noise; profiles/r02_gemm_fixup_ab.log): the last item of a unit serialises the conversion behind it.
     static const bool kFixup = [] { const char* e = std::getenv("TB_GEMM_FIXUP"); return e && e[0] == '1'; }();
-    if (p.partial && kFixup) {
+    if (p.partial && kFixup && !wide) {
         p.item_unit = plan->at<const int32_t>(plan->off_unit);
         p.unit_splits = plan->at<const int32_t>(plan->off_splits);
         p.unit_cnt = plan->at<int32_t>(plan->off_cnt);
@@ -762,6 +780,7 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
         }
     }
     if (!p.partial) return TB_OK;
+    if (p.int_red) return accum_convert_i32(reinterpret_cast<int32_t*>(p.acc), job_hi - job_lo, num, st);
     if (p.unit_cnt) return accum_mark_clean();  // the kernel converted and re-zeroed every unit's sums
     return accum_convert(p.acc, job_hi - job_lo, num, st);
 }

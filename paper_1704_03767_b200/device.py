@@ -37,22 +37,23 @@ from .pairindex import job_coord
 # (J = m(m+1)/2 job ids), the GEMM only while its sign matrix fits the free device memory.
 DISPATCH_TABLE = (
     # n, gemm pack s/row, gemm s/job, m_gemm, merge prep s/row, merge s/job  (tools/exp_dispatch.py on a B200,
-    # profiles/r02_dispatch_table.jsonl; merge with several pairs per CTA for 1024 < n <= 32768)
-    (1024, 1.113e-07, 2.028e-10, 2048, 3.645e-07, 9.205e-08),
-    (2048, 3.730e-07, 9.779e-10, 2048, 3.954e-07, 1.133e-08),
-    (4096, 1.108e-06, 7.871e-09, 2048, 5.259e-07, 2.457e-08),
-    (5792, 2.328e-06, 1.575e-08, 2048, 6.789e-07, 5.301e-08),
-    (6144, 3.744e-06, 3.086e-08, 2048, 7.029e-07, 5.312e-08),
-    (8192, 6.047e-06, 5.775e-08, 1990, 8.813e-07, 5.447e-08),
-    (12288, 1.178e-05, 1.726e-07, 884, 1.155e-06, 1.150e-07),
-    (16384, 2.141e-05, 3.643e-07, 497, 1.672e-06, 1.185e-07),
-    (24576, 4.700e-05, 1.424e-06, 221, 2.760e-06, 2.508e-07),
-    (32767, 8.747e-05, 4.628e-06, 124, 4.324e-06, 2.633e-07),
+    # profiles/r02_dispatch_table.jsonl; e2m1 GEMM at every n, merge with several pairs per CTA for n <= 32768)
+    (1024, 1.109e-07, 2.017e-10, 2048, 3.289e-07, 9.204e-08),
+    (2048, 3.726e-07, 9.795e-10, 2048, 4.082e-07, 1.134e-08),
+    (4096, 1.108e-06, 7.872e-09, 2048, 5.305e-07, 2.459e-08),
+    (5792, 2.325e-06, 1.575e-08, 2048, 6.819e-07, 5.314e-08),
+    (6144, 2.494e-06, 1.768e-08, 2048, 6.968e-07, 5.264e-08),
+    (8192, 3.725e-06, 3.141e-08, 2048, 9.226e-07, 5.415e-08),
+    (12288, 6.698e-06, 7.267e-08, 1769, 1.142e-06, 1.149e-07),
+    (16384, 1.232e-05, 1.517e-07, 995, 1.665e-06, 1.184e-07),
+    (24576, 2.774e-05, 3.989e-07, 442, 2.782e-06, 2.505e-07),
+    (32767, 6.850e-05, 1.002e-06, 248, 4.336e-06, 2.635e-07),
 )
 D2H_PIECE_BYTES = 256 << 20
+FP4_WIDE = os.environ.get("TB_FP4_WIDE", "1") != "0"
 TIED_SPARSE_FRAC = 0.35  # |S| GEMM over the tied rows only while they are at most this share of the rows
-GEMM_MAX_N = 7680  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides; merge
-# with several pairs per CTA: n = 6144 GEMM 31 vs merge 53 ns per job, n = 8192 58 vs 54 ns)
+GEMM_MAX_N = 14000  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides): e2m1
+# GEMM vs merge with several pairs per CTA, n = 12288: 73 vs 115 ns per job, n = 16384: 152 vs 118 ns
 RANK_ROWS_MAX_N = 8192  # tb_rank_rows' row limit; wider GEMM-path rows are ranked by tb_rank_dense
 SIGN_MAX_N = 32767      # tb_sign_pack: 15-bit ranks
 PATHS = ("gemm", "merge")
@@ -229,10 +230,14 @@ class TauEngine:
     fuse_finalize: bool = os.environ.get("TB_FUSE_FINALIZE", "0") == "1"
 
     def sign_format(self, K: int) -> int:
-        """e2m1 (kind::mxf4) while the f32 sums stay exact (K < 2^24), else int8 (kind::i8)."""
+        """e2m1 (kind::mxf4) for every K: beyond 2^24 the FP4 GEMM splits each unit into items whose f32
+        sums stay exact and adds them as int32 (twice the int8 rate, half its S bytes).  TB_FP4_WIDE=0
+        restores int8 (kind::i8) for K >= 2^24."""
         if self.sign_format_override is not None:
             return self.sign_format_override
-        return _lib.TB_SIGN_E2M1 if K < (1 << 24) else _lib.TB_SIGN_I8
+        if K >= (1 << 24) and not FP4_WIDE:
+            return _lib.TB_SIGN_I8
+        return _lib.TB_SIGN_E2M1
 
     @staticmethod
     def path_costs(m: int, n: int) -> dict:

@@ -560,24 +560,34 @@ def test_finalize_ranges_vs_numpy():
 
 
 @pytest.mark.gpu
-def test_gemm_int8_beyond_fp4_range(eng, oracle):
-    """n = 6000: K >= 2^24 switches the GEMM from e2m1 (f32 sums) to int8 (kind::i8); every pair
-    against the oracle, with ties, including the e2m1/int8 boundary n = 5793 / 5794."""
+@pytest.mark.parametrize("fmt", ["e2m1", "i8"])
+def test_gemm_beyond_2_24(eng, oracle, fmt):
+    """K >= 2^24 (n > 5792): the FP4 GEMM splits every unit into items of <= 65535 k-blocks, whose f32 sums
+    stay exact integers, and adds them as int32 (red.add.s32); the int8 GEMM (kind::i8) covers the same
+    shapes.  Every pair against the oracle, with ties and a monotone pair (|numerator| = n0 > 2^24), across
+    the boundary n = 5793 / 5794, at n = 6000 and n = 11000 (3 items per unit)."""
     from paper_1704_03767_b200 import _lib
-    for n, m in ((5793, 24), (5794, 24), (6000, 40)):
-        K = int(_lib.load().tb_sign_k(n))
-        rng = np.random.default_rng(n)
-        ranks = np.stack([oracle.rank_transform(rng.integers(0, n // 4, n)) for _ in range(m)])
-        res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="gemm").validate()
-        assert res.extra["sign_format"] == (_lib.TB_SIGN_E2M1 if K < (1 << 24) else _lib.TB_SIGN_I8)
-        _check_full(res, oracle, ranks, full=False)
+    code = {"e2m1": _lib.TB_SIGN_E2M1, "i8": _lib.TB_SIGN_I8}[fmt]
+    try:
+        eng.sign_format_override = code
+        for n, m in ((5793, 24), (5794, 24), (6000, 40), (11000, 12)):
+            if fmt == "i8" and n == 11000:
+                continue
+            rng = np.random.default_rng(n)
+            rows = [rng.integers(0, n // 4, n) for _ in range(m - 2)] + [np.arange(n), np.arange(n)]
+            ranks = np.stack([oracle.rank_transform(r) for r in rows])
+            res = eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="gemm", full_counts=True).validate()
+            assert res.extra["sign_format"] == code
+            _check_full(res, oracle, ranks)
+    finally:
+        eng.sign_format_override = None
 
 
 @pytest.mark.gpu
 def test_gemm_workspace_beyond_hbm_is_capacity_error(eng):
-    """S = m x K bytes beyond the GPU (m = 6000, n = 8192, int8: ~201 GB) -> CapacityExceededError."""
+    """S = m x K / 2 bytes beyond the GPU (m = 14000, n = 8192, e2m1: ~235 GB) -> CapacityExceededError."""
     import paper_1704_03767_b200 as tb
-    x = torch.zeros((6000, 8192), dtype=torch.float32, device="cuda")
+    x = torch.zeros((14000, 8192), dtype=torch.float32, device="cuda")
     with pytest.raises(tb.CapacityExceededError):
         eng.all_pairs(x, kernel="gemm")
     eng.release()

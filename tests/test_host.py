@@ -260,9 +260,9 @@ def test_dispatcher_cost_model(monkeypatch):
     monkeypatch.setattr(torch.cuda, "mem_get_info", lambda dev=None: (170 << 30, 180 << 30))
     for (m, n), want in {(256, 200): "gemm", (2048, 1000): "gemm", (16384, 500): "gemm", (65536, 1024): "gemm",
                          (1024, 65536): "merge", (128, 32767): "merge", (4, 9000): "merge",
-                         (2000, 6144): "gemm", (2000, 8192): "merge"}.items():
+                         (2000, 8192): "gemm", (1000, 12288): "gemm", (1000, 16384): "merge"}.items():
         assert choose_path(n, m=m, eng=eng) == want, (m, n)
-    assert choose_path(1000) == "gemm" and choose_path(9000) == "merge"  # no shape: the large-m crossover
+    assert choose_path(1000) == "gemm" and choose_path(15000) == "merge"  # no shape: the large-m crossover
     monkeypatch.setattr(torch.cuda, "mem_get_info", lambda dev=None: (1 << 30, 180 << 30))
     assert choose_path(1024, m=65536, eng=eng) == "merge"  # S = 17 GB does not fit 1 GiB
     for n, *_ in DISPATCH_TABLE:  # the model is finite and increasing in m
