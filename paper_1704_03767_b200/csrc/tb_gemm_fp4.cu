@@ -595,7 +595,11 @@ static int build_plan4(int64_t m, int64_t job_lo, int64_t job_hi, int32_t nkb, i
             // preferred on a tie (config 2: 390 us for 3 uniform splits vs 405 us for the model's best plan,
             // tools/exp_splits.py, profiles/r02_gemm_split_plans.log)
             if ((int64_t)code.size() <= pairs) {
-                const int32_t s_uni = (int32_t)std::max<int64_t>(1, std::min<int64_t>(nkb, pairs / (int64_t)code.size()));
+                // ... with at least 3 k-blocks per item: an item's epilogue reds its whole 256 x 480 tile, so
+                // items of one k-block (config 1: 74 of them) spend more on reds than on MMAs (config 1 GEMM
+                // 23.6 us at 74 splits, 19.5 us at 24-48; tools/exp_splits.py, profiles/r02_gemm_split_plans.log)
+                const int32_t s_uni = (int32_t)std::max<int64_t>(
+                    1, std::min<int64_t>(std::max<int64_t>(1, nkb / 3), pairs / (int64_t)code.size()));
                 std::vector<int32_t> uni(code.size(), s_uni);
                 const double t = plan_items4(code, nb, ncols, uni, nkb, pairs, nullptr);
                 if (t <= best * 1.0001) {

@@ -14,7 +14,7 @@ flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 num = torch.empty(total, dtype=torch.int32, device="cuda")
 with eng.session() as st:
     prep = eng.prepare(x, "gemm")
-    for s in [0, 1, 2, 3, 4, 5, 6, 8]:
+    for s in [int(a) for a in os.environ.get('SPLITS', '0,1,2,3,4,5,6,8').split(',')]:
         ts = []
         for it in range(23):
             flush.zero_()
