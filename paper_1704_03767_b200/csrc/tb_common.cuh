@@ -46,6 +46,9 @@ int table_mark_used(DevTable& t, cudaStream_t st);
 // magnitude < 2^24 when K < 2^24), then accum_convert writes the int32 numerators.
 int accum_workspace(int64_t span, float** ws, cudaStream_t st);
 int accum_convert(const float* ws, int64_t span, int32_t* num, cudaStream_t st);
+// tau_b straight from the f32 workspace (split plans, tau_b-only callers): convert + finalize in one launch.
+int accum_finalize(float* ws, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t job_lo, int64_t job_hi,
+                   double* tau_b, cudaStream_t st);
 // The same workspace holding int32 sums (wide-K FP4 items add exact int32 partials): copy out, re-zero.
 int accum_convert_i32(int32_t* ws, int64_t span, int32_t* num, cudaStream_t st);
 // The current device's workspace was converted and re-zeroed inside the GEMM (split-K fixup): clean.

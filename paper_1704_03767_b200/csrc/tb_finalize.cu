@@ -36,7 +36,7 @@ __device__ __forceinline__ void fin_walk(int32_t m, int32_t r, int32_t& y, int32
     x += r;
 }
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, bool ACC = false>
 __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const int32_t* __restrict__ num,
                                                                const unsigned long long* __restrict__ n1,
                                                                int32_t m, int64_t n0, int64_t job_lo, int64_t count,
@@ -71,11 +71,19 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const int32_t* __
         for (int u = 0; u < G; ++u) {
             const int c = g + u;
             if (c < nmine) {
-                v[u] = np[c * FIN_THREADS];
+                if constexpr (ACC)  // split-K f32 sums (exact integers); re-zeroed after the batch's loads
+                    v[u] = __float2int_rn(__ldcg(reinterpret_cast<const float*>(np) + c * FIN_THREADS));
+                else
+                    v[u] = np[c * FIN_THREADS];
                 t1[u] = __ldg(&n1[y]);
                 t2[u] = __ldg(&n1[x]);
                 if (c + 1 < nmine) fin_walk(m, FIN_THREADS, y, x);
             }
+        }
+        if constexpr (ACC) {
+#pragma unroll
+            for (int u = 0; u < G; ++u)
+                if (g + u < nmine) const_cast<float*>(reinterpret_cast<const float*>(np))[(g + u) * FIN_THREADS] = 0.0f;
         }
 #pragma unroll
         for (int u = 0; u < G; ++u) {
@@ -157,8 +165,19 @@ static int fin_table(int64_t n0, cudaStream_t st, const double** out) {
 
 using namespace tb;
 
+namespace tb {
+static int finalize_launch(const int32_t* num, bool acc, const uint64_t* n1_rows, int64_t m, int64_t n,
+                           int64_t job_lo, int64_t job_hi, double* tau_a, double* tau_b, void* stream);
+}  // namespace tb
+
 extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t job_lo,
                            int64_t job_hi, double* tau_a, double* tau_b, void* stream) {
+    return finalize_launch(num, false, n1_rows, m, n, job_lo, job_hi, tau_a, tau_b, stream);
+}
+
+namespace tb {
+static int finalize_launch(const int32_t* num, bool acc, const uint64_t* n1_rows, int64_t m, int64_t n,
+                           int64_t job_lo, int64_t job_hi, double* tau_a, double* tau_b, void* stream) {
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "finalize: need m >= 1, n >= 2");
     const int64_t total = m * (m + 1) / 2;
     if (job_lo < 0 || job_hi < job_lo || job_hi > total)
@@ -177,14 +196,16 @@ extern "C" int tb_finalize(const int32_t* num, const uint64_t* n1_rows, int64_t 
     const double* T = nullptr;
     int rc = fin_table(n * (n - 1) / 2, static_cast<cudaStream_t>(stream), &T);
     if (rc) return rc;
-    auto kern = tau_a ? (tau_b ? finalize_kernel<true, true> : finalize_kernel<true, false>)
-                      : (tau_b ? finalize_kernel<false, true> : nullptr);
-    if (!kern) return TB_OK;
+    auto kern = acc ? (tau_b && !tau_a ? finalize_kernel<false, true, true> : nullptr)
+                    : tau_a ? (tau_b ? finalize_kernel<true, true> : finalize_kernel<true, false>)
+                            : (tau_b ? finalize_kernel<false, true> : nullptr);
+    if (!kern) return acc ? fail(TB_ERR_CONFIG, "finalize: the workspace form writes tau_b only") : TB_OK;
     TB_CUDA_TRY(launch_pdl(kern, dim3((unsigned)blocks), dim3(FIN_THREADS), 0, static_cast<cudaStream_t>(stream), num,
                            reinterpret_cast<const unsigned long long*>(n1_rows), (int32_t)m, n * (n - 1) / 2, job_lo,
                            count, tau_a, tau_b, T, cpt));
     return check_launch("finalize_kernel");
 }
+}  // namespace tb
 
 namespace tb {
 __global__ void __launch_bounds__(256) full_counts_kernel(const int32_t* __restrict__ num,
@@ -295,6 +316,18 @@ int accum_convert_i32(int32_t* ws, int64_t span, int32_t* num, cudaStream_t st) 
     const int64_t blocks = std::min<int64_t>((span + 255) / 256, (int64_t)num_sms() * 8);
     TB_CUDA_TRY(launch_pdl(accum_convert_i32_kernel, dim3((unsigned)blocks), dim3(256), 0, st, ws, span, num));
     const int rc = check_launch("accum_convert_i32_kernel");
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(g_native_state_mutex);
+    if (rc == TB_OK && dev >= 0 && dev < TB_MAX_DEVICES) g_accum[dev].dirty = false;
+    return rc;
+}
+
+// tau_b straight from the split-K f32 workspace (the GEMM's partial sums; one launch instead of
+// accum_convert + finalize), re-zeroing it as accum_convert does.
+int accum_finalize(float* ws, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t job_lo, int64_t job_hi,
+                   double* tau_b, cudaStream_t st) {
+    const int rc = finalize_launch(reinterpret_cast<const int32_t*>(ws), true, n1_rows, m, n, job_lo, job_hi, nullptr,
+                                   tau_b, st);
     const int dev = current_device();
     std::lock_guard<std::mutex> lock(g_native_state_mutex);
     if (rc == TB_OK && dev >= 0 && dev < TB_MAX_DEVICES) g_accum[dev].dirty = false;

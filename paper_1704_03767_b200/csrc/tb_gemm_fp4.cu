@@ -716,13 +716,18 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.num = num;
     p.int_red = wide ? 1 : 0;
     if (wide && !p.partial) return fail(TB_ERR_CONFIG, "gemm fp4: wide K needs a split plan");
-    if (tau_b && !p.partial) {
+    // tau_b callers: a split plan finalizes straight from the f32 workspace (accum_finalize); a one-launch
+    // plan writes the numerators and the caller finalizes -- or, with TB_FUSE_EPILOGUE=1, the epilogue writes
+    // tau_b itself (measured slower under the power cap: profiles/r02_fused_finalize_ab.log)
+    static const bool kEpiFuse = [] { const char* e = std::getenv("TB_FUSE_EPILOGUE"); return e && e[0] == '1'; }();
+    const bool acc_fin = tau_b && p.partial && !wide;
+    if (tau_b && !p.partial && kEpiFuse) {
         p.tau_b = tau_b;
         p.n1 = reinterpret_cast<const unsigned long long*>(n1);
         p.dn0 = (double)(n * (n - 1) / 2);
         if (fused) *fused = 1;
-    } else if (!num) {
-        return fail(TB_ERR_INVALID, "gemm fp4: a split plan needs the numerator buffer");
+    } else if (!num && !acc_fin) {
+        return fail(TB_ERR_INVALID, "gemm fp4: this plan needs the numerator buffer");
     }
     if (p.partial && (rc = accum_workspace(job_hi - job_lo, &p.acc, st))) return rc;
     // In-kernel split-K fixup: opt-in (TB_GEMM_FIXUP=1).  Measured slower than the separate accum_convert
@@ -785,6 +790,10 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     }
     if (!p.partial) return TB_OK;
     if (p.int_red) return accum_convert_i32(reinterpret_cast<int32_t*>(p.acc), job_hi - job_lo, num, st);
+    if (acc_fin) {
+        if (fused) *fused = 1;
+        return accum_finalize(p.acc, n1, m, n, job_lo, job_hi, tau_b, st);
+    }
     if (p.unit_cnt) return accum_mark_clean();  // the kernel converted and re-zeroed every unit's sums
     return accum_convert(p.acc, job_hi - job_lo, num, st);
 }

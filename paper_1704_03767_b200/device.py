@@ -222,12 +222,11 @@ class TauEngine:
     # full counts with tied variables: "auto" runs the |S| GEMM over the tied rows only when they are at
     # most TIED_SPARSE_FRAC of the rows (n3 = 0 for every pair with an untied variable), else over all rows
     tied_mode: str = "auto"
-    # tau_b-only callers (tau_b_bands, all_pairs_host(numerators=False)) on the FP4 GEMM path: the GEMM
-    # epilogue can write tau_b itself (tb_gemm_tau_b: no numerator round trip, no finalize launch).  Off by
-    # default: measured slower (config 5 step 407.7 -> 422.7 ms, SM clock under the power cap 1342-1365 ->
-    # 1282-1327 MHz; config 3 GEMM 5.5 -> 6.1 ms for the same step time; profiles/r02_fused_finalize_ab.log):
-    # the fp64 divisions sit in the epilogue window where the MMA waits for TMEM, and cost power.
-    fuse_finalize: bool = os.environ.get("TB_FUSE_FINALIZE", "0") == "1"
+    # tau_b-only callers (tau_b_bands, all_pairs_host(numerators=False)) on the GEMM path go through
+    # tb_gemm_tau_b: split plans finalize straight from the f32 workspace (one launch instead of convert +
+    # finalize), one-launch plans write numerators and finalize after the GEMM (the epilogue fusion,
+    # TB_FUSE_EPILOGUE=1, measured slower under the power cap: profiles/r02_fused_finalize_ab.log)
+    fuse_finalize: bool = os.environ.get("TB_FUSE_FINALIZE", "1") != "0"
 
     def sign_format(self, K: int) -> int:
         """e2m1 (kind::mxf4) for every K: beyond 2^24 the FP4 GEMM splits each unit into items whose f32

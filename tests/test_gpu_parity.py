@@ -766,9 +766,36 @@ def test_fused_tau_b_epilogue(eng, oracle, m, n, levels):
             torch.cuda.synchronize()
             np.testing.assert_array_equal(outh.numpy(), ref)
     finally:
-        eng.fuse_finalize = False
+        eng.fuse_finalize = True
     pi, pj = oracle.upper_pairs(m)
     sel = rng.integers(0, total, 4000)
     num, counts = oracle.all_pairs(oracle.rank_matrix(x), pi[sel], pj[sel], oracle.KERNEL_SORTED, threads=8)
     _, tb = oracle.derive_taus(num, counts[:, 1], counts[:, 2], n)
     np.testing.assert_array_equal(ref[sel], tb)
+
+
+def test_fused_epilogue_opt_in_subprocess(tmp_path):
+    """TB_FUSE_EPILOGUE=1 (read once per process): the FP4 GEMM epilogue writes tau_b itself on one-launch
+    plans; identical to the default numerator + finalize sequence (run in a child process)."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+from paper_1704_03767_b200.device import TauEngine
+eng = TauEngine(0)
+rng = np.random.default_rng(5)
+x = torch.from_numpy(rng.integers(0, 40, (8192, 64)).astype(np.float32)).cuda()  # short K: a one-launch plan
+ref = eng.all_pairs(x, kernel="gemm", tau_a=False).validate().tau_b
+m = x.shape[0]; total = m * (m + 1) // 2
+out = torch.empty(total, dtype=torch.float64, device="cuda")
+eng.gemm_bands = 1
+eng.tau_b_bands(x, [(0, total)], out, kernel="gemm")
+torch.cuda.synchronize()
+assert torch.equal(out.isnan(), ref.isnan())
+assert torch.equal(torch.nan_to_num(out), torch.nan_to_num(ref))
+print("ok")
+""" % (str(__import__("conftest").ROOT),)
+    env = dict(__import__("os").environ, TB_FUSE_EPILOGUE="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
