@@ -11,6 +11,7 @@
 #include <thread>
 #include <vector>
 #include <emmintrin.h>
+#include <unistd.h>
 
 #include "tb_common.cuh"
 
@@ -102,8 +103,17 @@ class ExpandPool {
     uint64_t gen_ = 0;
 };
 
+// One pool per process, never destroyed (workers live for the process).  A fork()ed child inherits the pool
+// object but not its threads, so a child builds its own (the parent's copy is abandoned, not touched).
 static ExpandPool& expand_pool() {
-    static ExpandPool* pool = new ExpandPool();  // never destroyed: workers live for the process
+    static std::mutex mu;
+    static ExpandPool* pool = nullptr;
+    static pid_t owner = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pool || owner != getpid()) {
+        pool = new ExpandPool();
+        owner = getpid();
+    }
     return *pool;
 }
 

@@ -325,3 +325,37 @@ def test_expand_records_host(m, q, naive):
                                        out.ctypes.data, nthreads)
             assert rc == 0, lib.tb_last_error()
             assert out.tobytes() == exp.tobytes(), (lo, hi, nthreads)
+
+
+def test_expand_records_after_fork():
+    """The host expansion pool survives fork(): a child process that expands after the parent did builds its
+    own workers instead of waiting on the parent's (which it does not have)."""
+    import multiprocessing as mp
+
+    from paper_1704_03767_b200 import _lib
+    lib = _lib.load()
+    m, q, n = 40, 4, 30
+    from paper_1704_03767_b200.pairindex import JobSpace
+    tt = JobSpace(m, q).total_tiles
+    cells = int(lib.tb_tile_cells(m, q, 0, tt))
+    compact = np.zeros((cells, 2), np.uint32)
+    n1 = np.zeros(m, np.uint64)
+    out = np.zeros(cells * 48 + 16, np.uint8)
+    off = (-out.ctypes.data) % 16
+    assert lib.tb_expand_records(compact.ctypes.data, n1.ctypes.data, m, n, q, 0, tt, 0, out.ctypes.data + off, 4) == 0
+    ctx = mp.get_context("fork")
+    p = ctx.Process(target=_expand_child, args=(m, q, n, tt, cells))
+    p.start()
+    p.join(60)
+    assert p.exitcode == 0
+
+
+def _expand_child(m, q, n, tt, cells):
+    from paper_1704_03767_b200 import _lib
+    lib = _lib.load()
+    compact = np.zeros((cells, 2), np.uint32)
+    n1 = np.zeros(m, np.uint64)
+    out = np.zeros(cells * 48 + 16, np.uint8)
+    off = (-out.ctypes.data) % 16
+    rc = lib.tb_expand_records(compact.ctypes.data, n1.ctypes.data, m, n, q, 0, tt, 0, out.ctypes.data + off, 4)
+    raise SystemExit(0 if rc == 0 else 1)
