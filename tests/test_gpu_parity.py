@@ -308,6 +308,22 @@ def test_merge_multi_pair_ctas_vs_oracle(eng, oracle, n):
     np.testing.assert_array_equal(res.n3.cpu().numpy(), counts[:, 3])
 
 
+@pytest.mark.parametrize("path,n", [("merge", 1025), ("merge", 4096), ("merge", 32767), ("gemm", 6500)])
+def test_job_subranges_match_full_run(eng, path, n):
+    """Job sub-ranges that start and end anywhere (multi-pair merge CTAs whose first pair is not a multiple
+    of P; wide-K FP4 split plans over row fragments) give exactly the full run's counts."""
+    rng = np.random.default_rng(n)
+    m = 29
+    x = np.stack([rng.permutation(n) if r % 3 else rng.integers(0, n // 2, n) for r in range(m)]).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    full = eng.all_pairs(xd, kernel=path, full_counts=True).validate()
+    total = m * (m + 1) // 2
+    for lo, hi in ((0, 1), (1, 2), (3, 100), (37, total - 5), (total - 1, total)):
+        part = eng.all_pairs(xd, kernel=path, full_counts=True, job_range=(lo, hi)).validate()
+        for f in ("numerator", "n_d", "n3"):
+            assert torch.equal(getattr(part, f), getattr(full, f)[lo:hi]), (f, lo, hi)
+
+
 def test_merge_row_maximum_clamp(eng, oracle):
     """n = 65536: key 65535 (a unique row maximum) is sorted as 65534 (0xFFFF is the merge loop's
     look-ahead INF) and corrected.  The maximum and a unique second maximum placed in the same half
