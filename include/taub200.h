@@ -186,6 +186,19 @@ int tb_records_compact(const int32_t *num, const int64_t *n3, int64_t m, int64_t
 int tb_expand_records(const void *compact, const uint64_t *n1_rows, int64_t m, int64_t n, int64_t q,
                       int64_t tile_lo, int64_t ntiles, int naive, void *records, int nthreads);
 
+/* The numerator alone (int32, 4 bytes per record, emission order) for runs whose n3 is known on the host:
+ * n3 = 0 for every pair with an untied variable, and the tied rows' pairs come from a table
+ * (tb_expand_records_num).  Same checks as tb_records. */
+int tb_records_num(const int32_t *num, int64_t m, int64_t q, int64_t job_lo, int64_t job_hi, int64_t tile_lo,
+                   int64_t ntiles, int32_t *out, void *stream);
+
+/* Host-only: 48-byte records from the 4-byte numerator stream; tidx[m] maps a row to its index among the nt
+ * tied rows (-1: untied), n3t[nt(nt+1)/2] holds n3 of the tied rows' pairs in their own job-id order.
+ * nt = 0: no tied pair (tidx / n3t unused). */
+int tb_expand_records_num(const int32_t *nums, const uint64_t *n1_rows, const int32_t *tidx, const int64_t *n3t,
+                          int64_t nt, int64_t m, int64_t n, int64_t q, int64_t tile_lo, int64_t ntiles, int naive,
+                          void *records, int nthreads);
+
 /* Cells (records) in tiles [tile_lo, tile_hi) of the q x q tile matrix over m variables, diagonal
  * included -- the sum of tile_cell_count (pairindex.py:107-112) in closed form; -1 on bad arguments.
  * Host-only, no device work. */

@@ -53,6 +53,9 @@ SIGNATURES = {
     "tb_gemm_tau_b": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _i64, _p, _p, _p], ctypes.c_int),
     "tb_tied_counts": ([_p, _p, _i64, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p], ctypes.c_int),
     "tb_records_compact": ([_p, _p, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _p, _p], ctypes.c_int),
+    "tb_records_num": ([_p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p], ctypes.c_int),
+    "tb_expand_records_num": ([_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _p, ctypes.c_int],
+                              ctypes.c_int),
     "tb_expand_records": ([_p, _p, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _p, ctypes.c_int], ctypes.c_int),
 }
 

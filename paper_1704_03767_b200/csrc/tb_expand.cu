@@ -17,9 +17,21 @@
 
 namespace tb {
 
+// Where n3 comes from: the 8-byte stream (uint2: numerator, n3), or a 4-byte numerator stream plus the
+// tied rows' table (n3 of a pair is 0 unless both variables are tied: tidx[i], tidx[j] >= 0 index the
+// nt tied rows, n3t holds their pairs in the tied rows' own job-id order).
+struct N3Src {
+    const int32_t* tidx = nullptr;
+    const int64_t* n3t = nullptr;
+    int64_t nt = 0;
+};
+
 // Records of tiles [t0, t1) (record offsets relative to the pass's first tile base0).
-static void expand_tiles(const uint2* cmp, const uint64_t* n1, int64_t m, int64_t n0, int64_t q, int64_t w,
-                         int64_t t0, int64_t t1, int64_t base0, int naive, uint8_t* out) {
+template <bool NUM_ONLY>
+static void expand_tiles(const void* cmpv, const uint64_t* n1, int64_t m, int64_t n0, int64_t q, int64_t w,
+                         int64_t t0, int64_t t1, int64_t base0, int naive, uint8_t* out, N3Src tab) {
+    const uint2* cmp = static_cast<const uint2*>(cmpv);
+    const int32_t* nums = static_cast<const int32_t*>(cmpv);
     int64_t pos = cells_before_tile(t0, m, q, w) - base0;
     int64_t ty, tx;
     job_coord(t0, w, ty, tx);
@@ -29,14 +41,28 @@ static void expand_tiles(const uint2* cmp, const uint64_t* n1, int64_t m, int64_
         for (int64_t i = r0; i < r1; ++i) {
             const int64_t jb = std::max(i, c0);
             const uint64_t n1i = naive ? 0 : n1[i];
+            const int64_t ti = NUM_ONLY && !naive && tab.tidx ? tab.tidx[i] : -1;
+            const int64_t trow = ti >= 0 ? ti * (2 * tab.nt - ti + 1) / 2 - ti : 0;  // tied job id of (ti, tj) = trow + tj
             for (int64_t j = jb; j < c1; ++j, ++pos) {
-                const uint2 v = cmp[pos];
-                const int64_t num = (int32_t)v.x;
-                uint64_t nd = 0, n2 = 0, n3 = 0, n1v = 0;
-                if (!naive) {
+                int64_t num;
+                uint64_t n3 = 0;
+                if constexpr (NUM_ONLY) {
+                    num = nums[pos];
+                    if (ti >= 0) {
+                        const int64_t tj = tab.tidx[j];
+                        if (tj >= 0) n3 = (uint64_t)tab.n3t[trow + tj];
+                    }
+                } else {
+                    const uint2 v = cmp[pos];
+                    num = (int32_t)v.x;
+                    n3 = v.y;
+                }
+                uint64_t nd = 0, n2 = 0, n1v = 0;
+                if (naive) {
+                    n3 = 0;
+                } else {
                     n1v = n1i;
                     n2 = n1[j];
-                    n3 = v.y;
                     nd = (uint64_t)(((int64_t)n0 - (int64_t)n1v - (int64_t)n2 + (int64_t)n3 - num) / 2);
                 }
                 __m128i* r = reinterpret_cast<__m128i*>(out + 48 * pos);
@@ -121,8 +147,9 @@ static ExpandPool& expand_pool() {
 
 using namespace tb;
 
-extern "C" int tb_expand_records(const void* compact, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t q,
-                                 int64_t tile_lo, int64_t ntiles, int naive, void* records, int nthreads) {
+template <bool NUM_ONLY>
+static int expand_impl(const void* compact, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t q,
+                       int64_t tile_lo, int64_t ntiles, int naive, void* records, int nthreads, N3Src tab) {
     if (m < 1 || q < 1 || n < 1) return fail(TB_ERR_CONFIG, "expand_records: need m, q, n >= 1");
     const int64_t w = (m + q - 1) / q, tt = w * (w + 1) / 2;
     if (ntiles < 0 || tile_lo < 0 || tile_lo + ntiles > tt) return fail(TB_ERR_CONFIG, "expand_records: bad tile range");
@@ -131,18 +158,34 @@ extern "C" int tb_expand_records(const void* compact, const uint64_t* n1_rows, i
     if ((reinterpret_cast<uintptr_t>(records) & 15) != 0) return fail(TB_ERR_INVALID, "expand_records: records not 16-byte aligned");
     const int64_t n0 = n * (n - 1) / 2;
     const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
-    const uint2* cmp = static_cast<const uint2*>(compact);
     uint8_t* out = static_cast<uint8_t*>(records);
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads, ntiles));
     if (nt == 1) {
-        expand_tiles(cmp, n1_rows, m, n0, q, w, tile_lo, tile_lo + ntiles, base0, naive, out);
+        expand_tiles<NUM_ONLY>(compact, n1_rows, m, n0, q, w, tile_lo, tile_lo + ntiles, base0, naive, out, tab);
     } else {
         const std::function<void(int)> part = [&](int k) {
             const int64_t a = tile_lo + ntiles * k / nt, b = tile_lo + ntiles * (k + 1) / nt;
-            expand_tiles(cmp, n1_rows, m, n0, q, w, a, b, base0, naive, out);
+            expand_tiles<NUM_ONLY>(compact, n1_rows, m, n0, q, w, a, b, base0, naive, out, tab);
         };
         expand_pool().run(nt, part);
     }
     _mm_sfence();
     return TB_OK;
+}
+
+extern "C" int tb_expand_records(const void* compact, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t q,
+                                 int64_t tile_lo, int64_t ntiles, int naive, void* records, int nthreads) {
+    return expand_impl<false>(compact, n1_rows, m, n, q, tile_lo, ntiles, naive, records, nthreads, N3Src{});
+}
+
+extern "C" int tb_expand_records_num(const int32_t* nums, const uint64_t* n1_rows, const int32_t* tidx,
+                                     const int64_t* n3t, int64_t nt, int64_t m, int64_t n, int64_t q, int64_t tile_lo,
+                                     int64_t ntiles, int naive, void* records, int nthreads) {
+    if (nt < 0 || nt > m || (nt > 0 && (!tidx || !n3t)))
+        return fail(TB_ERR_INVALID, "expand_records_num: bad tied-row table");
+    N3Src tab;
+    tab.tidx = nt > 0 ? tidx : nullptr;
+    tab.n3t = n3t;
+    tab.nt = nt;
+    return expand_impl<true>(nums, n1_rows, m, n, q, tile_lo, ntiles, naive, records, nthreads, tab);
 }

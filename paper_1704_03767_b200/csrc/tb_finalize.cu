@@ -437,10 +437,13 @@ __global__ void __launch_bounds__(256) records_kernel(const int32_t* __restrict_
 // Compact form of the same stream: 8 bytes per record, (numerator, n3) as (int32, uint32) in emission order.
 // i, j, n1, n2 and n_d = (n0 - n1 - n2 + n3 - numerator) / 2 (result.py:42) are re-derived on the host by
 // tb_expand_records, so a pass crosses PCIe in 1/6 of the bytes.
+// NUM_ONLY: 4 bytes per record (the numerator); the host takes n3 from the tied rows' table (n3 = 0 for any
+// pair with an untied variable).
+template <bool NUM_ONLY>
 __global__ void __launch_bounds__(256) records_compact_kernel(const int32_t* __restrict__ num,
                                                               const int64_t* __restrict__ n3, int64_t m, int64_t q,
                                                               int64_t w, int64_t job_lo, int64_t tile_lo,
-                                                              int64_t base0, int naive, uint2* __restrict__ out) {
+                                                              int64_t base0, int naive, void* __restrict__ outv) {
     pdl_wait();
     const int64_t t = tile_lo + blockIdx.x;
     int64_t ty, tx;
@@ -454,7 +457,10 @@ __global__ void __launch_bounds__(256) records_compact_kernel(const int32_t* __r
         const int64_t above = tx > ty ? r * (cend - c0) : r * (cend - r0) - r * (r - 1) / 2;
         const int64_t pos = base + above + (j - max(i, c0));
         const int64_t jid = row_prefix(i, m) + (j - i) - job_lo;
-        out[pos] = make_uint2((uint32_t)num[jid], naive ? 0u : (uint32_t)n3[jid]);
+        if constexpr (NUM_ONLY)
+            static_cast<int32_t*>(outv)[pos] = num[jid];
+        else
+            static_cast<uint2*>(outv)[pos] = make_uint2((uint32_t)num[jid], naive ? 0u : (uint32_t)n3[jid]);
     }
     pdl_trigger();
 }
@@ -520,8 +526,23 @@ extern "C" int tb_records_compact(const int32_t* num, const int64_t* n3, int64_t
     const int64_t w = (m + q - 1) / q;
     const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
     const int threads = (int)std::min<int64_t>(256, ((q * q + 31) / 32) * 32);
-    TB_CUDA_TRY(launch_pdl(records_compact_kernel, dim3((unsigned)ntiles), dim3(threads), 0,
-                           static_cast<cudaStream_t>(stream), num, n3, m, q, w, job_lo, tile_lo, base0, naive,
-                           reinterpret_cast<uint2*>(compact)));
+    TB_CUDA_TRY(launch_pdl(records_compact_kernel<false>, dim3((unsigned)ntiles), dim3(threads), 0,
+                           static_cast<cudaStream_t>(stream), num, n3, m, q, w, job_lo, tile_lo, base0, naive, compact));
     return check_launch("records_compact_kernel");
+}
+
+extern "C" int tb_records_num(const int32_t* num, int64_t m, int64_t q, int64_t job_lo, int64_t job_hi,
+                              int64_t tile_lo, int64_t ntiles, int32_t* out, void* stream) {
+    if (m < 1 || q < 1) return fail(TB_ERR_CONFIG, "records_num: need m >= 1 and q >= 1");
+    if (ntiles < 0 || tile_lo < 0) return fail(TB_ERR_CONFIG, "records_num: bad tile range");
+    if (ntiles == 0) return TB_OK;
+    if (!num || !out) return fail(TB_ERR_INVALID, "records_num: null pointer");
+    if (int rc = records_range_check(m, q, job_lo, job_hi, tile_lo, ntiles)) return rc;
+    const int64_t w = (m + q - 1) / q;
+    const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
+    const int threads = (int)std::min<int64_t>(256, ((q * q + 31) / 32) * 32);
+    TB_CUDA_TRY(launch_pdl(records_compact_kernel<true>, dim3((unsigned)ntiles), dim3(threads), 0,
+                           static_cast<cudaStream_t>(stream), num, (const int64_t*)nullptr, m, q, w, job_lo, tile_lo,
+                           base0, 0, (void*)out));
+    return check_launch("records_num_kernel");
 }

@@ -171,6 +171,33 @@ def test_compact_record_path_matches_reference_stream(monkeypatch, kernel, full_
     assert _stream(ds, kernel, 4) == ref
 
 
+@pytest.mark.parametrize("kernel", ["vectorized", "naive", "merge"])
+def test_compact_numerator_stream_with_tied_table(monkeypatch, kernel):
+    """The 4-byte numerator stream (n3 from the tied rows' table on the host: the sparse tied-row |S| GEMM)
+    gives the same byte stream as full records, with tied rows, shared tie patterns (n3 > 0), a constant
+    row, and a job shard; the merge path keeps the 8-byte (numerator, n3) stream."""
+    import paper_1704_03767_b200 as tb
+    from paper_1704_03767_b200 import engine
+    rng = np.random.default_rng(3)
+    m, n = 300, 60
+    x = rng.standard_normal((m, n))
+    for r in rng.choice(m, 25, replace=False):
+        x[r, :12] = x[r, 0]  # tied rows sharing a tie pattern: joint ties
+        x[r, 30:33] = 7.0 + r % 2
+    x[5] = 1.0  # a constant row
+    ds = tb.Dataset(labels=[str(i) for i in range(m)], ranks=np.stack([tb.rank_transform(r) for r in x]))
+    monkeypatch.setattr(engine, "SLOT_BYTES", 48 * 3000)
+    monkeypatch.setattr(engine, "COMPACT_MIN_BATCHES", 1)
+    monkeypatch.setattr(engine, "FULL_EVERY", 1)
+    ref = _stream(ds, kernel, 8)
+    ref_shard = _stream(ds, kernel, 8, shard=(1, 3))
+    monkeypatch.setattr(engine, "FULL_EVERY", 4)
+    for compact_num in (True, False):
+        monkeypatch.setattr(engine, "COMPACT_NUM", compact_num)
+        assert _stream(ds, kernel, 8) == ref
+        assert _stream(ds, kernel, 8, shard=(1, 3)) == ref_shard
+
+
 def test_naive_large_n_uses_merge_path():
     """kernel='naive' for n above the GEMM path's limit: numerator-only records from the merge path
     (the reference's naive kernel handles any n, kernel_naive.py:26-44)."""

@@ -359,3 +359,45 @@ def _expand_child(m, q, n, tt, cells):
     off = (-out.ctypes.data) % 16
     rc = lib.tb_expand_records(compact.ctypes.data, n1.ctypes.data, m, n, q, 0, tt, 0, out.ctypes.data + off, 4)
     raise SystemExit(0 if rc == 0 else 1)
+
+
+@pytest.mark.parametrize("m,q,naive", [(37, 8, 0), (101, 4, 0), (64, 8, 1), (257, 3, 0)])
+def test_expand_records_num_host(m, q, naive):
+    """tb_expand_records_num: 48-byte records from a 4-byte numerator stream, n3 from the tied rows' table
+    (zero for any pair with an untied variable), for any tile sub-range and thread count."""
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.engine import CELL_DTYPE
+    from paper_1704_03767_b200.pairindex import JobSpace
+
+    rng = np.random.default_rng(m * 7 + q)
+    n = 60
+    n0 = n * (n - 1) // 2
+    space = JobSpace(m, q)
+    tied = np.sort(rng.choice(m, m // 5, replace=False))
+    n1 = np.zeros(m, np.uint64)
+    n1[tied] = rng.integers(1, 50, tied.size)
+    tidx = np.full(m, -1, np.int32)
+    tidx[tied] = np.arange(tied.size, dtype=np.int32)
+    nt = tied.size
+    n3t = rng.integers(0, 9, nt * (nt + 1) // 2).astype(np.int64)
+    lib = _lib.load()
+    tt = space.total_tiles
+    for lo, hi in ((0, tt), (tt // 4, tt // 4 + max(1, tt // 3)), (tt - 1, tt)):
+        ii, jj = space.cells_in_tile_order(lo, hi)
+        a, b = tidx[ii].astype(np.int64), tidx[jj].astype(np.int64)
+        both = (a >= 0) & (b >= 0)
+        n3 = np.where(both, n3t[np.where(both, a * (2 * nt - a + 1) // 2 + b - a, 0)], 0)
+        nd = rng.integers(0, 300, ii.size)
+        num = (n0 - n1[ii].astype(np.int64) - n1[jj].astype(np.int64) + n3 - 2 * nd).astype(np.int32)
+        exp = np.zeros(ii.size, CELL_DTYPE)
+        exp["i"], exp["j"], exp["numerator"] = ii, jj, num
+        if not naive:
+            exp["n_d"], exp["n1"], exp["n2"], exp["n3"] = nd, n1[ii], n1[jj], n3
+        for nthreads in (1, 5):
+            buf = np.zeros(ii.size * 48 + 16, np.uint8)
+            off = (-buf.ctypes.data) % 16
+            out = buf[off:off + ii.size * 48]
+            rc = lib.tb_expand_records_num(num.ctypes.data, n1.ctypes.data, tidx.ctypes.data, n3t.ctypes.data, nt,
+                                           m, n, q, lo, hi - lo, naive, out.ctypes.data, nthreads)
+            assert rc == 0, lib.tb_last_error()
+            assert out.tobytes() == exp.tobytes(), (lo, hi, nthreads)
