@@ -107,6 +107,10 @@ __device__ __forceinline__ int prog_behind(const unsigned long long* prog, int64
     return c;
 }
 
+#ifndef GEMM_DIAG_ALIGN  // 1: a row block's column blocks start at its diagonal (0: at multiples of 240)
+#define GEMM_DIAG_ALIGN 1
+#endif
+
 struct Unit4 {
     int64_t y0;
     int64_t xs[2];       // first column of each 240-column block (two consecutive blocks of one row block)
@@ -122,8 +126,13 @@ __device__ __forceinline__ bool next_unit4(const Gemm4Args& p, int64_t& cur, int
     t.y0 = (int64_t)it.x * g4::UM;
     const int32_t b0 = (int32_t)((uint32_t)it.w >> 16), b1 = it.w & 0xFFFF;
     t.nblk = b1 == 0xFFFF ? 1 : 2;
+#if GEMM_DIAG_ALIGN  // column blocks start at the row block's diagonal: x = y0 + 240 k
+    t.xs[0] = t.y0 + (int64_t)b0 * g4::BN;
+    t.xs[1] = t.y0 + (int64_t)(b1 == 0xFFFF ? b0 : b1) * g4::BN;
+#else
     t.xs[0] = (int64_t)b0 * g4::BN;
     t.xs[1] = (int64_t)(b1 == 0xFFFF ? b0 : b1) * g4::BN;
+#endif
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int64_t live = p.m - t.xs[h];
@@ -487,18 +496,31 @@ static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<i
     int64_t y_lo, x_lo, y_hi, x_hi;
     job_coord(job_lo, m, y_lo, x_lo);
     job_coord(job_hi - 1, m, y_hi, x_hi);
-    auto nmma = [m](int64_t b) -> int32_t {
-        const int64_t live = m - b * g4::BN;
+    auto nmma_x = [m](int64_t x0) -> int32_t {
+        const int64_t live = m - x0;
         return live >= g4::BN ? g4::BN : (int32_t)((live + 15) / 16 * 16);
     };
-    struct U { int64_t win, yb, b0, b1; };
+    struct U { int64_t win, yb, b0, b1; int32_t nc; };
     for (int64_t SY = 0; SY < (RB + GR - 1) / GR; ++SY) {
         std::vector<U> g;
         for (int64_t yb = SY * GR; yb < std::min(RB, (SY + 1) * GR); ++yb) {
             const int64_t r0 = yb * g4::UM, r1 = std::min(r0 + g4::UM, m) - 1;
             if (r1 < y_lo || r0 > y_hi) continue;  // outside the job range rows
+#if GEMM_DIAG_ALIGN
+            // blocks k = 0, 1, ... at x = r0 + 240 k: only the 256 x 256 diagonal square is partly wasted
+            // (config 2: ~24% of the MMA area below the diagonal with 240-aligned blocks, ~12% here)
+            const int64_t k_last = (m - 1 - r0) / g4::BN;
+            for (int64_t k = 0; k <= k_last; k += 2) {
+                const int64_t x0 = r0 + k * g4::BN, x1 = x0 + g4::BN;
+                const bool two = k + 1 <= k_last;
+                g.push_back(U{(x0 / g4::BN) / kWIN, yb, k, two ? k + 1 : -1,
+                              nmma_x(x0) + (two ? nmma_x(x1) : 0)});
+            }
+#else
             for (int64_t b = r0 / g4::BN; b <= b_last; b += 2)
-                g.push_back(U{b / kWIN, yb, b, b + 1 <= b_last ? b + 1 : -1});
+                g.push_back(U{b / kWIN, yb, b, b + 1 <= b_last ? b + 1 : -1,
+                              nmma_x(b * g4::BN) + (b + 1 <= b_last ? nmma_x((b + 1) * g4::BN) : 0)});
+#endif
         }
         if (kSERP && (SY & 1))
             std::stable_sort(g.begin(), g.end(), [](const U& a, const U& b) { return a.win > b.win; });
@@ -507,7 +529,7 @@ static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<i
         for (const U& u : g) {
             code.push_back((int32_t)u.yb);
             nb.push_back((int32_t)((u.b0 << 16) | (u.b1 < 0 ? 0xFFFF : u.b1)));
-            ncols.push_back(nmma(u.b0) + (u.b1 < 0 ? 0 : nmma(u.b1)));
+            ncols.push_back(u.nc);
         }
     }
 }
