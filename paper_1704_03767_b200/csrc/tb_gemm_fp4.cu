@@ -107,6 +107,9 @@ __device__ __forceinline__ int prog_behind(const unsigned long long* prog, int64
     return c;
 }
 
+#ifndef GEMM_DB  // 1: single-block units alternating between the two TMEM accumulator sets, so a unit's MMAs
+#define GEMM_DB 0  // run while the epilogue drains the previous unit (0: two-block units, one accumulator set)
+#endif
 #ifndef GEMM_DIAG_ALIGN  // 1: a row block's column blocks start at its diagonal (0: at multiples of 240)
 #define GEMM_DIAG_ALIGN 1
 #endif
@@ -169,9 +172,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    uint64_t* tfull = empty + STAGES;   // [2]: accumulator set 0 / 1 (GEMM_DB alternates; else set 0)
+    uint64_t* tempty = tfull + 2;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -187,8 +190,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
+        }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
@@ -249,12 +254,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             const uint32_t d0 = tmem_base, d1 = tmem_base + BN;
             int stage = 0;
             uint32_t phase = 0;
-            uint32_t acc_phase = 0;
+            uint32_t acc_ph[2] = {0u, 0u};
+            int it = 0;
             int64_t cur = pair;
             Unit4 t;
             while (next_unit4(p, cur, npairs, t)) {
-                mbar_wait(tempty, acc_phase ^ 1);
+                const int aset = GEMM_DB ? (it & 1) : 0;
+                mbar_wait(&tempty[aset], acc_ph[aset] ^ 1);
                 tc_fence_after();
+                const uint32_t dA = GEMM_DB ? tmem_base + (uint32_t)aset * BN : d0;
                 const uint32_t id0 = t.nb[0] == BN ? idesc : idesc_mxf4(UM, (uint32_t)t.nb[0]);
                 const uint32_t id1 = t.nb[1] == BN ? idesc : idesc_mxf4(UM, (uint32_t)t.nb[1]);
                 const int mode = t.nblk;  // 2: both blocks, 1: block 0 only
@@ -273,13 +281,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                     } else {
 #pragma unroll
                         for (int k = 0; k < BK / UKB; ++k)
-                            mma_mxf4_2sm_warp(d0, ad + 2 * k, ad + B0_D + 2 * k, id0, sf, sf, k ? 1u : a0);
+                            mma_mxf4_2sm_warp(dA, ad + 2 * k, ad + B0_D + 2 * k, id0, sf, sf, k ? 1u : a0);
                     }
                     mma_commit_2sm_warp(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit_2sm_warp(tfull, 0x3);
-                acc_phase ^= 1;
+                mma_commit_2sm_warp(&tfull[aset], 0x3);
+                acc_ph[aset] ^= 1;
+                ++it;
             }
         }
     } else if (warp >= 4) {  // ---------------- epilogue (both CTAs)
@@ -292,10 +301,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
         int32_t* stg = reinterpret_cast<int32_t*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * STG_WORDS;
         int64_t* rowbase = reinterpret_cast<int64_t*>(stg + 32 * STG_LD);
         uint32_t* rown1 = reinterpret_cast<uint32_t*>(rowbase + 32);  // n1 < n0 < 2^31
-        uint32_t acc_phase = 0;
+        uint32_t acc_ph[2] = {0u, 0u};
+        int it = 0;
         const int64_t m = p.m;
         const int64_t span = p.job_hi - p.job_lo;
-        const uint32_t tempty_leader = mapa_shared(tempty, 0);
+        const uint32_t tempty_leader[2] = {mapa_shared(&tempty[0], 0), mapa_shared(&tempty[1], 0)};
         const int half = lane >> 4, col = lane & 15;
         int64_t cur = pair;
         Unit4 t;
@@ -309,7 +319,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                 if (p.tau_b) rown1[lane] = y < m ? (uint32_t)__ldg(&p.n1[y]) : 0u;
             }
             __syncwarp();
-            mbar_wait(tfull, acc_phase);
+            const int aset = GEMM_DB ? (it & 1) : 0;
+            mbar_wait(&tfull[aset], acc_ph[aset]);
             tc_fence_after();
             int item = (int)((cur - pair) / npairs) - 1;
             if (p.trace && warp == 4 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2] = globaltimer();
@@ -317,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
 #pragma unroll 1
                 for (int c = 16 * par; c < BN; c += 16 * EPI_PAR) {
                     uint32_t r[16];
-                    tmem_ld_32x32b_x16(tmem_base + (uint32_t(q * 32) << 16) + h * BN + c, r);
+                    tmem_ld_32x32b_x16(tmem_base + (uint32_t(q * 32) << 16) + (GEMM_DB ? aset : h) * BN + c, r);
                     tmem_ld_wait();
                     const int64_t xc = t.xs[h] + c;
                     if (xc >= m || xc + 15 < y0) continue;  // chunk right of the matrix or below the diagonal
@@ -389,8 +400,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (p.trace && warp == 4 && lane == 0 && item < 8) p.trace[(blockIdx.x * 8 + item) * 2 + 1] = globaltimer();
-            if (lane == 0) mbar_arrive_cluster(tempty_leader);
-            acc_phase ^= 1;
+            if (lane == 0) mbar_arrive_cluster(tempty_leader[aset]);
+            acc_ph[aset] ^= 1;
+            ++it;
             if (t.partial && p.unit_cnt) {
                 // this CTA half's reds of the item are issued; the last of the unit's items converts the half
                 // (CUTLASS's barrier pattern: CTA barrier, then one thread fences and arrives)
@@ -510,9 +522,9 @@ static void list_units4(int64_t m, int64_t job_lo, int64_t job_hi, std::vector<i
             // blocks k = 0, 1, ... at x = r0 + 240 k: only the 256 x 256 diagonal square is partly wasted
             // (config 2: ~24% of the MMA area below the diagonal with 240-aligned blocks, ~12% here)
             const int64_t k_last = (m - 1 - r0) / g4::BN;
-            for (int64_t k = 0; k <= k_last; k += 2) {
+            for (int64_t k = 0; k <= k_last; k += (GEMM_DB ? 1 : 2)) {
                 const int64_t x0 = r0 + k * g4::BN, x1 = x0 + g4::BN;
-                const bool two = k + 1 <= k_last;
+                const bool two = !GEMM_DB && k + 1 <= k_last;
                 g.push_back(U{(x0 / g4::BN) / kWIN, yb, k, two ? k + 1 : -1,
                               nmma_x(x0) + (two ? nmma_x(x1) : 0)});
             }
