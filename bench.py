@@ -464,7 +464,10 @@ def run_ours(args):
         for _ in range(2):  # warm-up (pinned pass buffers, device window buffers, GEMM plans)
             plugin()
         ts = []
-        for _ in range(args.e2e_steps):
+        # short calls (configs 1-4: milliseconds) are timed over >= 20 calls so one slow call (a page fault,
+        # a collector pass) does not set the mean; config 5's calls take ~0.8 s each
+        n_e2e = args.e2e_steps if total_jobs > (1 << 27) else max(args.e2e_steps, 20)
+        for _ in range(n_e2e):
             got["records"] = 0
             if world > 1:
                 dist.barrier()
