@@ -486,7 +486,7 @@ def run_ours(args):
                "api": ("compute_all_pairs(ds, 'vectorized', sink=...) -- the reference's plugin call "
                        "(engine.py:300-310): H2D of the int32 ranks, every count on the device, 48-byte "
                        "CELL_DTYPE records (diagonal included) delivered to a host sink pass by pass -- one batch "
-                       f"in {tb.engine.FULL_EVERY} copied as full records, the others as the 8-byte (numerator, n3) stream "
+                       f"in {tb.engine.FULL_EVERY} copied as full records, the others as the 4-byte numerator stream (8-byte (numerator, n3) when many rows have ties) "
                        "expanded into the same bytes by host threads (tb_expand_records); wall clock" + (f"; rank r runs shard=(r, {world})" if world > 1 else "")),
                "timer": "wall clock around the synchronous host call"}
         del ds
