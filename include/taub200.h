@@ -11,6 +11,7 @@
  *   TB_ERR_CAPACITY   2  -> CapacityExceededError (errors.py:12-17)
  *   TB_ERR_CONFIG     3  -> ConfigError           (errors.py:23-24)
  *   TB_ERR_CUDA       4  -> RuntimeError (CUDA launch/driver failure)
+ *   TB_ERR_ABORTED    5  -> (host pass ring only) the caller raised the ring's abort flag
  *
  * tb_last_error() returns the message of the last failing call on the calling
  * thread.
@@ -39,6 +40,7 @@ extern "C" {
 #define TB_ERR_CAPACITY 2
 #define TB_ERR_CONFIG 3
 #define TB_ERR_CUDA 4
+#define TB_ERR_ABORTED 5
 
 #define TB_DTYPE_I32 0
 #define TB_DTYPE_F32 1
@@ -198,6 +200,27 @@ int tb_records_num(const int32_t *num, int64_t m, int64_t q, int64_t job_lo, int
 int tb_expand_records_num(const int32_t *nums, const uint64_t *n1_rows, const int32_t *tidx, const int64_t *n3t,
                           int64_t nt, int64_t m, int64_t n, int64_t q, int64_t tile_lo, int64_t ntiles, int naive,
                           void *records, int nthreads);
+
+/* Host-only: store policy of tb_expand_records / tb_expand_records_num.  0 (default): non-temporal stores,
+ * for record slots far larger than the host's last-level cache; 1: plain stores, for a small ring of pass
+ * buffers that stays cache-resident (the records are handed to the sink hot).  Returns the previous mode. */
+int tb_expand_store_mode(int plain);
+
+/* Host-only: one compact batch (width 4: tb_records_num stream + tied-row table as tb_expand_records_num;
+ * width 8: tb_records_compact stream) expanded pass by pass into a ring of nslots pass buffers of slot_bytes
+ * each, with plain stores, so the records stay cache-resident until the sink has seen them
+ * (compute_all_pairs hands each pass to the sink as a view of its ring slot: engine.py:353-416 recycles
+ * pass buffers the same way).  Pass p covers tiles [pass_tile[p], pass_tile[p + 1]) and is ring pass
+ * seq0 + p of the run, written to ring + ((seq0 + p) % nslots) * slot_bytes.  ctl is the run's control block
+ * (int64[3], zeroed by the caller): ctl[0] = passes produced (stored by this call, in order, once every
+ * worker finished the pass), ctl[1] = passes released by the consumer (this call waits while
+ * seq - ctl[1] >= nslots), ctl[2] != 0 aborts (TB_ERR_ABORTED).  Blocks until the batch is expanded. */
+int tb_expand_ring(const void *compact, int width, const uint64_t *n1_rows, const int32_t *tidx, const int64_t *n3t,
+                   int64_t nt, int64_t m, int64_t n, int64_t q, const int64_t *pass_tile, int64_t npass, int naive,
+                   void *ring, int64_t slot_bytes, int64_t nslots, int64_t seq0, int64_t *ctl, int nthreads);
+
+/* Host-only: block until ring pass seq is produced (ctl[0] > seq); TB_ERR_ABORTED if ctl[2] != 0. */
+int tb_ring_wait(const int64_t *ctl, int64_t seq);
 
 /* Cells (records) in tiles [tile_lo, tile_hi) of the q x q tile matrix over m variables, diagonal
  * included -- the sum of tile_cell_count (pairindex.py:107-112) in closed form; -1 on bad arguments.

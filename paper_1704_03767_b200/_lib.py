@@ -21,7 +21,7 @@ if _variant:  # A/B experiments: an in-tree copy of this library built from a va
         raise ImportError(f"TB_LIB_VARIANT must name an in-tree libtaub200*.so, got {_variant!r}")
     LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), _variant)
 
-TB_OK, TB_ERR_INVALID, TB_ERR_CAPACITY, TB_ERR_CONFIG, TB_ERR_CUDA = 0, 1, 2, 3, 4
+TB_OK, TB_ERR_INVALID, TB_ERR_CAPACITY, TB_ERR_CONFIG, TB_ERR_CUDA, TB_ERR_ABORTED = 0, 1, 2, 3, 4, 5
 TB_DTYPE_I32, TB_DTYPE_F32, TB_DTYPE_F64 = 0, 1, 2
 TB_SIGN_I8, TB_SIGN_E4M3, TB_SIGN_E2M1 = 0, 1, 2
 TB_MAX_N = 65536
@@ -56,6 +56,10 @@ SIGNATURES = {
     "tb_records_num": ([_p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p], ctypes.c_int),
     "tb_expand_records_num": ([_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _p, ctypes.c_int],
                               ctypes.c_int),
+    "tb_expand_store_mode": ([ctypes.c_int], ctypes.c_int),
+    "tb_expand_ring": ([_p, ctypes.c_int, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _i64, ctypes.c_int, _p, _i64, _i64,
+                        _i64, _p, ctypes.c_int], ctypes.c_int),
+    "tb_ring_wait": ([_p, _i64], ctypes.c_int),
     "tb_expand_records": ([_p, _p, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _p, ctypes.c_int], ctypes.c_int),
 }
 

@@ -4,6 +4,7 @@
 // streams full records for the others, so a pass reaches the sink over two paths at once: PCIe carries
 // 8 bytes per record instead of 48 for the expanded ones.
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <functional>
@@ -27,7 +28,9 @@ struct N3Src {
 };
 
 // Records of tiles [t0, t1) (record offsets relative to the pass's first tile base0).
-template <bool NUM_ONLY>
+// STREAM: non-temporal stores (records bound for DRAM: slots far larger than the last-level cache);
+// otherwise plain stores, for destinations small enough to stay cache-resident (the pass ring).
+template <bool NUM_ONLY, bool STREAM>
 static void expand_tiles(const void* cmpv, const uint64_t* n1, int64_t m, int64_t n0, int64_t q, int64_t w,
                          int64_t t0, int64_t t1, int64_t base0, int naive, uint8_t* out, N3Src tab) {
     const uint2* cmp = static_cast<const uint2*>(cmpv);
@@ -66,9 +69,18 @@ static void expand_tiles(const void* cmpv, const uint64_t* n1, int64_t m, int64_
                     nd = (uint64_t)(((int64_t)n0 - (int64_t)n1v - (int64_t)n2 + (int64_t)n3 - num) / 2);
                 }
                 __m128i* r = reinterpret_cast<__m128i*>(out + 48 * pos);
-                _mm_stream_si128(r, _mm_set_epi64x(num, (int64_t)((uint64_t)(uint32_t)i | ((uint64_t)(uint32_t)j << 32))));
-                _mm_stream_si128(r + 1, _mm_set_epi64x((int64_t)n1v, (int64_t)nd));
-                _mm_stream_si128(r + 2, _mm_set_epi64x((int64_t)n3, (int64_t)n2));
+                const __m128i v0 = _mm_set_epi64x(num, (int64_t)((uint64_t)(uint32_t)i | ((uint64_t)(uint32_t)j << 32)));
+                const __m128i v1 = _mm_set_epi64x((int64_t)n1v, (int64_t)nd);
+                const __m128i v2 = _mm_set_epi64x((int64_t)n3, (int64_t)n2);
+                if constexpr (STREAM) {
+                    _mm_stream_si128(r, v0);
+                    _mm_stream_si128(r + 1, v1);
+                    _mm_stream_si128(r + 2, v2);
+                } else {
+                    _mm_store_si128(r, v0);
+                    _mm_store_si128(r + 1, v1);
+                    _mm_store_si128(r + 2, v2);
+                }
             }
         }
         // next tile in id order: along the tile row, then the next row's diagonal tile
@@ -77,7 +89,7 @@ static void expand_tiles(const void* cmpv, const uint64_t* n1, int64_t m, int64_
             tx = ty;
         }
     }
-    _mm_sfence();  // streaming stores are weakly ordered: drain them before the thread reports done
+    if constexpr (STREAM) _mm_sfence();  // streaming stores are weakly ordered: drain them before the thread reports done
 }
 
 // Persistent expansion workers: a config-5 call expands ~400 batches; spawning a dozen std::threads per
@@ -147,6 +159,12 @@ static ExpandPool& expand_pool() {
 
 using namespace tb;
 
+// 0: streaming stores (default), 1: plain stores (cache-resident destinations)
+static std::atomic<int> g_expand_plain{0};
+extern "C" int tb_expand_store_mode(int plain) {
+    return g_expand_plain.exchange(plain ? 1 : 0);
+}
+
 template <bool NUM_ONLY>
 static int expand_impl(const void* compact, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t q,
                        int64_t tile_lo, int64_t ntiles, int naive, void* records, int nthreads, N3Src tab) {
@@ -160,17 +178,103 @@ static int expand_impl(const void* compact, const uint64_t* n1_rows, int64_t m, 
     const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
     uint8_t* out = static_cast<uint8_t*>(records);
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads, ntiles));
+    const bool plain = g_expand_plain.load(std::memory_order_relaxed) != 0;
+    auto run = [&](int64_t a, int64_t b) {
+        if (plain) expand_tiles<NUM_ONLY, false>(compact, n1_rows, m, n0, q, w, a, b, base0, naive, out, tab);
+        else expand_tiles<NUM_ONLY, true>(compact, n1_rows, m, n0, q, w, a, b, base0, naive, out, tab);
+    };
     if (nt == 1) {
-        expand_tiles<NUM_ONLY>(compact, n1_rows, m, n0, q, w, tile_lo, tile_lo + ntiles, base0, naive, out, tab);
+        run(tile_lo, tile_lo + ntiles);
     } else {
         const std::function<void(int)> part = [&](int k) {
-            const int64_t a = tile_lo + ntiles * k / nt, b = tile_lo + ntiles * (k + 1) / nt;
-            expand_tiles<NUM_ONLY>(compact, n1_rows, m, n0, q, w, a, b, base0, naive, out, tab);
+            run(tile_lo + ntiles * k / nt, tile_lo + ntiles * (k + 1) / nt);
         };
         expand_pool().run(nt, part);
     }
     _mm_sfence();
     return TB_OK;
+}
+
+// ---- pass ring: one compact batch expanded pass by pass into a small ring of pass buffers.
+// The big record slots are DRAM-bound (non-temporal stores, ~150-195 GB/s on the B200 boxes' 16 cores, less
+// next to a D2H); a ring of a few pass buffers stays in the cores' caches, so the plain stores never reach
+// DRAM before the sink has seen the pass (tools/probe_expand_ring.py).  The pool is entered once per batch;
+// its workers run the passes back to back, each taking the same share of every pass (the same ring bytes
+// every lap: they stay in that core's L2), synchronised only by two counters: ctl[0] = passes produced,
+// ctl[1] = passes the consumer released (ctl[2] != 0 aborts).
+static inline int64_t ctl_load(const int64_t* p) { return __atomic_load_n(p, __ATOMIC_ACQUIRE); }
+
+template <typename Cond>
+static bool ring_spin(const int64_t* ctl, Cond ok) {
+    for (int64_t spins = 0;; ++spins) {
+        if (ok()) return true;
+        if (ctl_load(ctl + 2) != 0) return false;
+        if (spins < 2000) _mm_pause();
+        else if (spins < 4000) std::this_thread::yield();
+        else usleep(50);
+    }
+}
+
+extern "C" int tb_ring_wait(const int64_t* ctl, int64_t seq) {
+    if (!ctl) return fail(TB_ERR_INVALID, "ring_wait: null control block");
+    return ring_spin(ctl, [&] { return ctl_load(ctl) > seq; }) ? TB_OK : TB_ERR_ABORTED;
+}
+
+extern "C" int tb_expand_ring(const void* compact, int width, const uint64_t* n1_rows, const int32_t* tidx,
+                              const int64_t* n3t, int64_t nt_rows, int64_t m, int64_t n, int64_t q,
+                              const int64_t* pass_tile, int64_t npass, int naive, void* ring, int64_t slot_bytes,
+                              int64_t nslots, int64_t seq0, int64_t* ctl, int nthreads) {
+    if (m < 1 || q < 1 || n < 1) return fail(TB_ERR_CONFIG, "expand_ring: need m, q, n >= 1");
+    if (width != 4 && width != 8) return fail(TB_ERR_CONFIG, "expand_ring: width must be 4 or 8");
+    if (npass < 0 || nslots < 1 || slot_bytes < 0 || seq0 < 0) return fail(TB_ERR_CONFIG, "expand_ring: bad ring geometry");
+    if (npass == 0) return TB_OK;
+    if (!compact || !ring || !ctl || !pass_tile || (!naive && !n1_rows))
+        return fail(TB_ERR_INVALID, "expand_ring: null pointer");
+    if ((reinterpret_cast<uintptr_t>(ring) & 15) != 0 || (slot_bytes & 15) != 0)
+        return fail(TB_ERR_INVALID, "expand_ring: ring slots not 16-byte aligned");
+    if (width == 4 && (nt_rows < 0 || nt_rows > m || (nt_rows > 0 && (!tidx || !n3t))))
+        return fail(TB_ERR_INVALID, "expand_ring: bad tied-row table");
+    const int64_t w = (m + q - 1) / q, tt = w * (w + 1) / 2;
+    for (int64_t p = 0; p < npass; ++p)
+        if (pass_tile[p] < 0 || pass_tile[p + 1] < pass_tile[p] || pass_tile[p + 1] > tt)
+            return fail(TB_ERR_CONFIG, "expand_ring: bad pass tile ranges");
+    const int64_t n0 = n * (n - 1) / 2;
+    const int64_t base_batch = cells_before_tile(pass_tile[0], m, q, w);
+    std::vector<int64_t> base(npass + 1);
+    for (int64_t p = 0; p <= npass; ++p)
+        base[p] = pass_tile[p] >= tt ? m * (m + 1) / 2 : cells_before_tile(pass_tile[p], m, q, w);
+    for (int64_t p = 0; p < npass; ++p)
+        if ((base[p + 1] - base[p]) * 48 > slot_bytes) return fail(TB_ERR_CAPACITY, "expand_ring: a pass exceeds the ring slot");
+    N3Src tab;
+    tab.tidx = (width == 4 && nt_rows > 0) ? tidx : nullptr;
+    tab.n3t = n3t;
+    tab.nt = width == 4 ? nt_rows : 0;
+    const int nthr = (int)std::max<int64_t>(1, nthreads);
+    std::vector<std::atomic<int>> done(npass);
+    for (auto& d : done) d.store(0, std::memory_order_relaxed);
+    std::atomic<int> aborted{0};
+    const std::function<void(int)> part = [&](int k) {
+        for (int64_t p = 0; p < npass; ++p) {
+            const int64_t seq = seq0 + p;
+            if (!ring_spin(ctl, [&] { return seq - ctl_load(ctl + 1) < nslots; })) {
+                aborted.store(1);
+                return;
+            }
+            const int64_t t_lo = pass_tile[p], nti = pass_tile[p + 1] - t_lo;
+            const int64_t a = t_lo + nti * k / nthr, b = t_lo + nti * (k + 1) / nthr;
+            uint8_t* out = static_cast<uint8_t*>(ring) + (seq % nslots) * slot_bytes;
+            const uint8_t* src = static_cast<const uint8_t*>(compact) + (base[p] - base_batch) * width;
+            if (a < b) {
+                if (width == 4) expand_tiles<true, false>(src, n1_rows, m, n0, q, w, a, b, base[p], naive, out, tab);
+                else expand_tiles<false, false>(src, n1_rows, m, n0, q, w, a, b, base[p], naive, out, tab);
+            }
+            if (done[p].fetch_add(1, std::memory_order_acq_rel) == nthr - 1)
+                __atomic_store_n(ctl, seq + 1, __ATOMIC_RELEASE);  // every worker finished pass p (and all before it)
+        }
+    };
+    if (nthr == 1) part(0);
+    else expand_pool().run(nthr, part);
+    return aborted.load() ? TB_ERR_ABORTED : TB_OK;
 }
 
 extern "C" int tb_expand_records(const void* compact, const uint64_t* n1_rows, int64_t m, int64_t n, int64_t q,

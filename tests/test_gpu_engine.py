@@ -147,9 +147,10 @@ def test_window_pipeline_matches_reference_stream(kernel):
         assert parts == ref
 
 
+@pytest.mark.parametrize("ring_slots", [0, 1, 3])
 @pytest.mark.parametrize("full_every", [1, 2, 3, 10, 1 << 30])
 @pytest.mark.parametrize("kernel", ["sorted", "naive"])
-def test_compact_record_path_matches_reference_stream(monkeypatch, kernel, full_every):
+def test_compact_record_path_matches_reference_stream(monkeypatch, kernel, full_every, ring_slots):
     """Records through the two host paths -- full 48-byte records by D2H, or the 8-byte compact stream
     expanded on host threads (tb_records_compact + tb_expand_records) -- in any mix of batches give the
     reference byte stream (every batch full: full_every = 1; none: 1 << 30)."""
@@ -194,8 +195,10 @@ def test_compact_numerator_stream_with_tied_table(monkeypatch, kernel):
     monkeypatch.setattr(engine, "FULL_EVERY", 4)
     for compact_num in (True, False):
         monkeypatch.setattr(engine, "COMPACT_NUM", compact_num)
-        assert _stream(ds, kernel, 8) == ref
-        assert _stream(ds, kernel, 8, shard=(1, 3)) == ref_shard
+        for ring_slots in (0, 2):
+            monkeypatch.setattr(engine, "RING_SLOTS", ring_slots)
+            assert _stream(ds, kernel, 8) == ref
+            assert _stream(ds, kernel, 8, shard=(1, 3)) == ref_shard
 
 
 def test_naive_large_n_uses_merge_path():

@@ -327,6 +327,80 @@ def test_expand_records_host(m, q, naive):
             assert out.tobytes() == exp.tobytes(), (lo, hi, nthreads)
 
 
+def test_expand_ring_host():
+    """tb_expand_ring (host threads, no device): a compact stream expanded pass by pass into a ring of pass
+    buffers, in two batches, while a consumer takes each pass (tb_ring_wait) and releases its slot -- the
+    concatenated passes are the reference CELL_DTYPE stream; the abort flag ends a blocked call."""
+    import threading
+    import time
+
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.engine import CELL_DTYPE
+    from paper_1704_03767_b200.pairindex import JobSpace
+
+    lib = _lib.load()
+    m, q, n = 301, 4, 50
+    n0 = n * (n - 1) // 2
+    rng = np.random.default_rng(1)
+    space = JobSpace(m, q)
+    n1 = rng.integers(0, n0 // 3, m).astype(np.uint64)
+    lo, hi = 5, space.total_tiles
+    ii, jj = space.cells_in_tile_order(lo, hi)
+    k = ii.size
+    n3 = rng.integers(0, 40, k).astype(np.int64)
+    nd = rng.integers(0, 200, k).astype(np.int64)
+    num = (n0 - n1[ii].astype(np.int64) - n1[jj].astype(np.int64) + n3 - 2 * nd).astype(np.int32)
+    exp = np.zeros(k, CELL_DTYPE)
+    exp["i"], exp["j"], exp["numerator"] = ii, jj, num
+    exp["n_d"], exp["n1"], exp["n2"], exp["n3"] = nd, n1[ii], n1[jj], n3
+    compact = np.empty((k, 2), np.uint32)
+    compact[:, 0] = num.view(np.uint32)
+    compact[:, 1] = n3
+    bounds = np.array(list(range(lo, hi, 37)) + [hi], np.int64)
+    npass = bounds.size - 1
+    cells = [int(lib.tb_tile_cells(m, q, int(a), int(b))) for a, b in zip(bounds[:-1], bounds[1:])]
+    assert sum(cells) == k
+    slot = (max(cells) * 48 + 63) // 64 * 64
+    for R, nthreads in ((1, 1), (3, 4)):
+        raw = np.zeros(R * slot + 64, np.uint8)
+        off = (-raw.ctypes.data) % 64
+        ring = raw[off:off + R * slot]
+        ctl = np.zeros(3, np.int64)
+        got = []
+
+        def consumer():
+            for p in range(npass):
+                assert lib.tb_ring_wait(ctl.ctypes.data, p) == 0
+                got.append(ring[(p % R) * slot:(p % R) * slot + cells[p] * 48].tobytes())
+                time.sleep(0.0002)
+                ctl[1] = p + 1
+
+        t = threading.Thread(target=consumer)
+        t.start()
+        h = npass // 2
+        args = (n1.ctypes.data, None, None, 0, m, n, q)
+        rc = lib.tb_expand_ring(compact.ctypes.data, 8, *args, bounds.ctypes.data, h, 0, ring.ctypes.data, slot, R, 0,
+                                ctl.ctypes.data, nthreads)
+        assert rc == 0, lib.tb_last_error()
+        rc = lib.tb_expand_ring(compact.ctypes.data + 8 * sum(cells[:h]), 8, *args, bounds[h:].ctypes.data, npass - h, 0,
+                                ring.ctypes.data, slot, R, h, ctl.ctypes.data, nthreads)
+        assert rc == 0, lib.tb_last_error()
+        t.join()
+        assert b"".join(got) == exp.tobytes()
+    # nobody releases: the call blocks on a full ring until the abort flag is raised
+    ctl = np.zeros(3, np.int64)
+    threading.Timer(0.05, lambda: ctl.__setitem__(2, 1)).start()
+    rc = lib.tb_expand_ring(compact.ctypes.data, 8, n1.ctypes.data, None, None, 0, m, n, q, bounds.ctypes.data, npass, 0,
+                            ring.ctypes.data, slot, R, 0, ctl.ctypes.data, 4)
+    assert rc == _lib.TB_ERR_ABORTED
+    assert lib.tb_ring_wait(ctl.ctypes.data, 10 ** 6) == _lib.TB_ERR_ABORTED
+    # a pass larger than the ring slot is refused
+    ctl[:] = 0
+    rc = lib.tb_expand_ring(compact.ctypes.data, 8, n1.ctypes.data, None, None, 0, m, n, q, bounds.ctypes.data, npass, 0,
+                            ring.ctypes.data, 48, R, 0, ctl.ctypes.data, 1)
+    assert rc == _lib.TB_ERR_CAPACITY
+
+
 def test_expand_records_after_fork():
     """The host expansion pool survives fork(): a child process that expands after the parent did builds its
     own workers instead of waiting on the parent's (which it does not have)."""

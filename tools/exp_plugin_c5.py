@@ -28,6 +28,18 @@ def timed_expand(self, batch, slot):
 
 
 engine._DevicePipe.expand = timed_expand
+orig_ring = engine._DevicePipe.expand_ring
+
+
+def timed_ring(self, batch, slot):
+    t0 = time.perf_counter()
+    orig_ring(self, batch, slot)
+    acc["expand"] += time.perf_counter() - t0
+    acc["n"] += 1
+
+
+engine._DevicePipe.expand_ring = timed_ring
+print("ring slots", engine.RING_SLOTS, "expand threads", engine.EXPAND_THREADS, "pass slots", engine.PASS_SLOTS, flush=True)
 wjs = [int(a) for a in os.environ.get("WJ", str(engine.WINDOW_JOBS)).split(",")]
 for wj in wjs:
     for _ in range(2):
