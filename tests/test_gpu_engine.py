@@ -156,7 +156,13 @@ def test_compact_record_path_matches_reference_stream(monkeypatch, kernel, full_
     reference byte stream (every batch full: full_every = 1; none: 1 << 30)."""
     import paper_1704_03767_b200 as tb
     from paper_1704_03767_b200 import engine
+    if full_every == 1 and ring_slots != 3:
+        pytest.skip("no compact batch: the ring is not used")
+    # ring_slots = 0: compact batches expanded whole into their pinned slots; else pass by pass into the
+    # cache-resident pass ring (tb_expand_ring)
+    monkeypatch.setattr(engine, "RING_SLOTS", ring_slots)
     monkeypatch.setattr(engine, "FULL_EVERY", full_every)
+    monkeypatch.setattr(engine, "FULL_EVERY_RING", full_every)
     monkeypatch.setattr(engine, "SLOT_BYTES", 48 * 5000)  # many batches per run
     monkeypatch.setattr(engine, "COMPACT_MIN_BATCHES", 1)
     gold = load_json("engine_streams.json")
@@ -199,6 +205,47 @@ def test_compact_numerator_stream_with_tied_table(monkeypatch, kernel):
             monkeypatch.setattr(engine, "RING_SLOTS", ring_slots)
             assert _stream(ds, kernel, 8) == ref
             assert _stream(ds, kernel, 8, shard=(1, 3)) == ref_shard
+
+
+@pytest.mark.parametrize("data", ["few_tied", "all_tied"])
+@pytest.mark.parametrize("kernel", ["vectorized", "naive"])
+def test_row_block_aligned_windows(monkeypatch, kernel, data):
+    """GEMM windows aligned to 256-row blocks (ids of a straddling pass carried over from the previous
+    window, device n_d / n3 skipped once every batch is a 4-byte numerator stream) give the same byte
+    stream as pass-aligned windows and as one window with full records, whole run and shards."""
+    import paper_1704_03767_b200 as tb
+    from paper_1704_03767_b200 import engine
+    from paper_1704_03767_b200.pairindex import JobSpace
+    m, n = 1300, 40
+    if data == "all_tied":
+        ds = tb.synth_dataset(m, n, tie_fraction=0.3, seed=77)
+    else:
+        rng = np.random.default_rng(77)
+        x = rng.standard_normal((m, n))
+        for r in rng.choice(m, 60, replace=False):
+            x[r, :5] = x[r, 0]
+        ds = tb.Dataset(labels=[str(i) for i in range(m)], ranks=np.stack([tb.rank_transform(r) for r in x]))
+    space = JobSpace(m, 8)
+    plans = engine.plan_passes(space, (0, space.total_tiles), 50)
+    groups, gemm_lo = engine._aligned_window_groups(space, plans, 400_000)
+    assert len(groups) >= 3 and any(ga > lo for ((lo, _), _), ga in zip(groups, gemm_lo))  # carried ids exist
+    monkeypatch.setattr(engine, "FULL_EVERY", 1)
+    monkeypatch.setattr(engine, "ALIGN_WINDOWS", False)
+    ref = _stream(ds, kernel, 8, pass_tiles=50)
+    ref_shard = _stream(ds, kernel, 8, pass_tiles=50, shard=(1, 3))
+    monkeypatch.setattr(engine, "SLOT_BYTES", 48 * 9000)
+    monkeypatch.setattr(engine, "COMPACT_MIN_BATCHES", 1)
+    for align in (False, True):
+        monkeypatch.setattr(engine, "ALIGN_WINDOWS", align)
+        for fe, ring in ((1, 0), (3, 0), (3, 2), (1 << 30, 3)):
+            monkeypatch.setattr(engine, "FULL_EVERY", fe)
+            monkeypatch.setattr(engine, "FULL_EVERY_RING", fe)
+            monkeypatch.setattr(engine, "RING_SLOTS", ring)
+            assert _stream(ds, kernel, 8, pass_tiles=50, window_jobs=400_000) == ref, (align, fe, ring)
+            assert _stream(ds, kernel, 8, pass_tiles=50, window_jobs=400_000, shard=(1, 3)) == ref_shard, (align, fe, ring)
+    # sink=None (no records): the summary still counts every cell
+    monkeypatch.setattr(engine, "ALIGN_WINDOWS", True)
+    assert tb.compute_all_pairs(ds, kernel, pass_tiles=50, window_jobs=400_000).total_cells == m * (m + 1) // 2
 
 
 def test_naive_large_n_uses_merge_path():
