@@ -393,7 +393,7 @@ def run_ours(args):
     step()
     torch.cuda.synchronize()
     launches_per_step = _lib.load().tb_launch_count() - launches0
-    sign_format = eng.sign_format(int(_lib.load().tb_sign_k(n))) if path == "gemm" else None
+    sign_format = eng.sign_format(int(_lib.load().tb_sign_k(n)), m) if path == "gemm" else None
 
     if world > 1:
         dist.barrier()
@@ -534,7 +534,7 @@ def run_ours(args):
             traffic = tj.get(f"config{args.config}", {}).get("dram_bytes_per_launch")
         per_step_units = sum(len(eng._gemm_ranges(m, lo, hi)) for lo, hi in bands) if path == "gemm" else len(bands)
         if path == "gemm":
-            fp4 = sign_format == _lib.TB_SIGN_E2M1
+            fp4 = sign_format in (_lib.TB_SIGN_E2M1, _lib.TB_SIGN_E2M1_OFS)
             fp4_lib = measure_fp4_peak(torch, dev) if fp4 else None
             mma_clk = None
             if fp4:  # the probe's own SM clock: it may run power-capped right after the timed region
@@ -604,7 +604,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None,
-            "dtype": ("e2m1" if sign_format == _lib.TB_SIGN_E2M1 else "i8") if path == "gemm" else "int32",
+            "dtype": ("e2m1" if sign_format in (_lib.TB_SIGN_E2M1, _lib.TB_SIGN_E2M1_OFS) else "i8")
+            if path == "gemm" else "int32",
             "data": "synthetic",
             "config": {"workload": f"config{args.config}_{spec.name}", "m": m, "n": n,
                        "pairs": total_pairs, "pairs_per_rank": my_pairs, "path": path,
@@ -613,6 +614,8 @@ def run_ours(args):
                        "l2": "flushed before every timed step (256 MiB write, untimed); config-5 operands (S = 17 GB) "
                              "exceed L2 anyway",
                        "step": "one CUDA graph replay" if use_graph else "eager launches",
+                       "operands": ("S + 1 offset coding (TB_SIGN_E2M1_OFS), row-sum correction in the epilogue"
+                                    if sign_format == _lib.TB_SIGN_E2M1_OFS else "-1/0/+1") if path == "gemm" else None,
                        "outputs": "tau_b f64 for every job id in job-id order (numerators in a workspace)"
                        + ("; every rank's bands gathered to rank 0 (NCCL send/recv per band) inside the step"
                           if gathering else "")},

@@ -54,6 +54,12 @@ extern "C" {
 #define TB_SIGN_I8 0
 #define TB_SIGN_E4M3 1
 #define TB_SIGN_E2M1 2
+/*   TB_SIGN_E2M1_OFS  e2m1 S + 1 (0 / 1 / 2 for -1 / tie / +1; unused slots 0), same layout as
+ *                 TB_SIGN_E2M1.  (S_y + 1).(S_x + 1) = S_y.S_x + s_y + s_x + n0 with s = the row sums of S
+ *                 (tb_sign_row_sums), so tb_gemm_pairs_fix(fix = s, fix_c = n0) returns the same numerators.
+ *                 Exact while 4 K < 2^24 (n <= 2896).  Non-negative, half-zero operands toggle fewer
+ *                 tensor-pipe bits than +-1: the power-capped GEMM of a long run is ~12% faster (DESIGN 3). */
+#define TB_SIGN_E2M1_OFS 3
 
 /* Largest n the device paths accept: the int32 numerator holds |n_c - n_d| <=
  * n(n-1)/2 < 2^31 exactly up to here.  Larger n raises
@@ -137,8 +143,20 @@ int tb_sign_pack(const uint16_t *R, int64_t m, int64_t n, int64_t ldr, int8_t *S
 int tb_gemm_pairs(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo, int64_t job_hi,
                   int32_t splits, int32_t *num, void *stream);
 
+/* The same GEMM over offset operands (e2m1 formats): num[j - job_lo] = S_y . S_x - fix[y] - fix[x] - fix_c,
+ * fix[m] int32 on the device (NULL = tb_gemm_pairs).  TB_SIGN_E2M1_OFS numerators: fix = tb_sign_row_sums,
+ * fix_c = n0 = n(n-1)/2; its tie-indicator matrix (tb_abs_pack of an OFS matrix, Z = [S == 0]) with
+ * fix = n1 per row and fix_c = -n0 returns |S_y|.|S_x| = n0 - n1_y - n1_x + Z_y.Z_x, tb_full_counts' absdot. */
+int tb_gemm_pairs_fix(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
+                      int64_t job_hi, int32_t splits, const int32_t *fix, int64_t fix_c, int32_t *num, void *stream);
+
+/* fix[r] = sum_k S[r, k] of a TB_SIGN_E2M1_OFS matrix (the nibble values' sum minus n0): the Kendall
+ * numerator of row r against the sample order, the correction term of tb_gemm_pairs_fix. */
+int tb_sign_row_sums(const int8_t *S, int64_t m, int64_t ldS, int64_t n, int32_t *fix, void *stream);
+
 /* |S| for the full-count mode: A[r, k] = |S[r, k]| (0/1 int8), same layout.
- * The second GEMM A A^T gives n_c + n_d per pair (SURVEY 8 identities). */
+ * The second GEMM A A^T gives n_c + n_d per pair (SURVEY 8 identities).
+ * TB_SIGN_E2M1_OFS: A = the tie indicator Z = [S == 0] instead (unused slots stay 0), see tb_gemm_pairs_fix. */
 int tb_abs_pack(const int8_t *S, int64_t m, int64_t ldS, int format, int8_t *A, void *stream);
 
 /* Full counts on the GEMM path from num = S_y.S_x and absdot = |S_y|.|S_x|:
@@ -247,6 +265,10 @@ int tb_finalize(const int32_t *num, const uint64_t *n1_rows, int64_t m, int64_t 
  * numerator + derive_taus sequence (kernel_naive.py:26-44, result.py:62-82) for tau_b-only callers. */
 int tb_gemm_tau_b(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo, int64_t job_hi,
                   int32_t splits, const uint64_t *n1_rows, int64_t n, int32_t *num_ws, double *tau_b, void *stream);
+/* tb_gemm_tau_b over offset operands (fix / fix_c as in tb_gemm_pairs_fix). */
+int tb_gemm_tau_b_fix(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
+                      int64_t job_hi, int32_t splits, const int32_t *fix, int64_t fix_c, const uint64_t *n1_rows,
+                      int64_t n, int32_t *num_ws, double *tau_b, void *stream);
 
 /*
  * K1 presort for the merge path (large n): per variable, the position of

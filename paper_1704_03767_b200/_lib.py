@@ -23,7 +23,7 @@ if _variant:  # A/B experiments: an in-tree copy of this library built from a va
 
 TB_OK, TB_ERR_INVALID, TB_ERR_CAPACITY, TB_ERR_CONFIG, TB_ERR_CUDA, TB_ERR_ABORTED = 0, 1, 2, 3, 4, 5
 TB_DTYPE_I32, TB_DTYPE_F32, TB_DTYPE_F64 = 0, 1, 2
-TB_SIGN_I8, TB_SIGN_E4M3, TB_SIGN_E2M1 = 0, 1, 2
+TB_SIGN_I8, TB_SIGN_E4M3, TB_SIGN_E2M1, TB_SIGN_E2M1_OFS = 0, 1, 2, 3
 TB_MAX_N = 65536
 
 # Every exported symbol and its ctypes signature (kept in sync with include/taub200.h;
@@ -42,6 +42,10 @@ SIGNATURES = {
     "tb_sign_pack": ([_p, _i64, _i64, _i64, _p, _i64, ctypes.c_int, _p], ctypes.c_int),
     "tb_abs_pack": ([_p, _i64, _i64, ctypes.c_int, _p, _p], ctypes.c_int),
     "tb_gemm_pairs": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _p], ctypes.c_int),
+    "tb_gemm_pairs_fix": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _i64, _p, _p], ctypes.c_int),
+    "tb_sign_row_sums": ([_p, _i64, _i64, _i64, _p, _p], ctypes.c_int),
+    "tb_gemm_tau_b_fix": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _i64, _p, _i64, _p, _p, _p],
+                          ctypes.c_int),
     "tb_gemm_pairs_simt": ([_p, _i64, _i64, _i64, _i64, _i64, _p, _p], ctypes.c_int),
     "tb_finalize": ([_p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),
     "tb_full_counts": ([_p, _p, _p, _i64, _i64, _i64, _i64, _p, _p, _p], ctypes.c_int),

@@ -11,7 +11,7 @@
 #include <mutex>
 #include <thread>
 #include <vector>
-#include <emmintrin.h>
+#include <immintrin.h>
 #include <unistd.h>
 
 #include "tb_common.cuh"
@@ -26,6 +26,75 @@ struct N3Src {
     const int64_t* n3t = nullptr;
     int64_t nt = 0;
 };
+
+// Four records at a time (AVX2): the six fields of records j .. j+3 of row i as 4 x 64-bit vectors, transposed
+// into the 24 quadwords of four consecutive 48-byte records (6 unpacks + 6 lane permutes + 6 stores).  Rows
+// whose n3 comes from the tied-row table stay on the scalar loop.  Returns the first j not written.
+static const bool g_has_avx2 = __builtin_cpu_supports("avx2");
+
+template <bool NUM_ONLY, bool STREAM>
+__attribute__((target("avx2"))) static inline int64_t expand_row_avx2(const void* cmpv, int64_t pos, int64_t i,
+                                                                     int64_t jb, int64_t c1, const uint64_t* n1,
+                                                                     uint64_t n1i, int64_t n0, int naive,
+                                                                     uint8_t* out) {
+    const __m256i vn1 = _mm256_set1_epi64x((int64_t)n1i);
+    const __m256i vbase = _mm256_set1_epi64x(n0 - (int64_t)n1i);
+    const __m256i zero = _mm256_setzero_si256();
+    const __m256i sbit = _mm256_set1_epi64x((int64_t)0x8000000000000000ull);
+    __m256i ij = _mm256_add_epi64(_mm256_set1_epi64x((int64_t)(uint64_t)(uint32_t)i),
+                                  _mm256_slli_epi64(_mm256_add_epi64(_mm256_set1_epi64x(jb), _mm256_set_epi64x(3, 2, 1, 0)), 32));
+    const __m256i ij_step = _mm256_set1_epi64x((int64_t)4 << 32);
+    int64_t j = jb;
+    for (; j + 4 <= c1; j += 4, pos += 4, ij = _mm256_add_epi64(ij, ij_step)) {
+        __m256i num, n3;
+        if constexpr (NUM_ONLY) {
+            num = _mm256_cvtepi32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i*>(static_cast<const int32_t*>(cmpv) + pos)));
+            n3 = zero;
+        } else {
+            const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(static_cast<const uint2*>(cmpv) + pos));
+            n3 = _mm256_srli_epi64(v, 32);
+            const __m256i lo = _mm256_and_si256(v, _mm256_set1_epi64x(0xFFFFFFFFll));
+            const __m256i s31 = _mm256_set1_epi64x(0x80000000ll);
+            num = _mm256_sub_epi64(_mm256_xor_si256(lo, s31), s31);  // sign-extend the low 32 bits
+        }
+        __m256i nd, n2, n1v;
+        if (naive) {
+            nd = n2 = n1v = n3 = zero;
+        } else {
+            n1v = vn1;
+            n2 = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(n1 + j));
+            // nd = (n0 - n1 - n2 + n3 - num) / 2, C division (toward zero): add 1 to negatives, shift, keep the sign
+            __m256i t = _mm256_sub_epi64(_mm256_add_epi64(_mm256_sub_epi64(vbase, n2), n3), num);
+            const __m256i neg = _mm256_cmpgt_epi64(zero, t);
+            t = _mm256_sub_epi64(t, neg);
+            nd = _mm256_or_si256(_mm256_srli_epi64(t, 1), _mm256_and_si256(t, sbit));
+        }
+        const __m256i A = _mm256_unpacklo_epi64(ij, num), B = _mm256_unpackhi_epi64(ij, num);
+        const __m256i C = _mm256_unpacklo_epi64(nd, n1v), D = _mm256_unpackhi_epi64(nd, n1v);
+        const __m256i E = _mm256_unpacklo_epi64(n2, n3), F = _mm256_unpackhi_epi64(n2, n3);
+        const __m256i v0 = _mm256_permute2x128_si256(A, C, 0x20), v1 = _mm256_permute2x128_si256(E, B, 0x20);
+        const __m256i v2 = _mm256_permute2x128_si256(D, F, 0x20), v3 = _mm256_permute2x128_si256(A, C, 0x31);
+        const __m256i v4 = _mm256_permute2x128_si256(E, B, 0x31), v5 = _mm256_permute2x128_si256(D, F, 0x31);
+        uint8_t* r = out + 48 * pos;
+        if constexpr (STREAM) {  // records are 16-byte aligned only: 128-bit non-temporal halves
+            __m128i* r16 = reinterpret_cast<__m128i*>(r);
+            const __m256i vs[6] = {v0, v1, v2, v3, v4, v5};
+            for (int k = 0; k < 6; ++k) {
+                _mm_stream_si128(r16 + 2 * k, _mm256_castsi256_si128(vs[k]));
+                _mm_stream_si128(r16 + 2 * k + 1, _mm256_extracti128_si256(vs[k], 1));
+            }
+        } else {
+            __m256i* r32 = reinterpret_cast<__m256i*>(r);
+            _mm256_storeu_si256(r32, v0);
+            _mm256_storeu_si256(r32 + 1, v1);
+            _mm256_storeu_si256(r32 + 2, v2);
+            _mm256_storeu_si256(r32 + 3, v3);
+            _mm256_storeu_si256(r32 + 4, v4);
+            _mm256_storeu_si256(r32 + 5, v5);
+        }
+    }
+    return j;
+}
 
 // Records of tiles [t0, t1) (record offsets relative to the pass's first tile base0).
 // STREAM: non-temporal stores (records bound for DRAM: slots far larger than the last-level cache);
@@ -46,7 +115,12 @@ static void expand_tiles(const void* cmpv, const uint64_t* n1, int64_t m, int64_
             const uint64_t n1i = naive ? 0 : n1[i];
             const int64_t ti = NUM_ONLY && !naive && tab.tidx ? tab.tidx[i] : -1;
             const int64_t trow = ti >= 0 ? ti * (2 * tab.nt - ti + 1) / 2 - ti : 0;  // tied job id of (ti, tj) = trow + tj
-            for (int64_t j = jb; j < c1; ++j, ++pos) {
+            int64_t j = jb;
+            if (g_has_avx2 && ti < 0 && c1 - jb >= 4) {
+                j = expand_row_avx2<NUM_ONLY, STREAM>(cmpv, pos, i, jb, c1, n1, n1i, n0, naive, out);
+                pos += j - jb;
+            }
+            for (; j < c1; ++j, ++pos) {
                 int64_t num;
                 uint64_t n3 = 0;
                 if constexpr (NUM_ONLY) {

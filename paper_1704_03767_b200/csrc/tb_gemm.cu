@@ -444,27 +444,48 @@ using namespace tb;
 namespace tb {
 int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi, int32_t splits,
              int32_t* num, cudaStream_t st, double* tau_b = nullptr, const uint64_t* n1 = nullptr, int64_t n = 0,
-             int* fused = nullptr);
+             int* fused = nullptr, const int32_t* fix = nullptr, int64_t fix_c = 0);
 }
+static bool is_e2m1(int format) { return format == TB_SIGN_E2M1 || format == TB_SIGN_E2M1_OFS; }
 
-extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
-                             int64_t job_hi, int32_t splits, int32_t* num, void* stream) {
-    if (format < TB_SIGN_I8 || format > TB_SIGN_E2M1) return fail(TB_ERR_CONFIG, "gemm: unknown format %d", format);
-    int rc = check_job_args(m, format == TB_SIGN_E2M1 ? K / 2 : K, ldS, job_lo, job_hi);
+extern "C" int tb_gemm_pairs_fix(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
+                                 int64_t job_hi, int32_t splits, const int32_t* fix, int64_t fix_c, int32_t* num,
+                                 void* stream) {
+    if (format < TB_SIGN_I8 || format > TB_SIGN_E2M1_OFS) return fail(TB_ERR_CONFIG, "gemm: unknown format %d", format);
+    if (fix && !is_e2m1(format)) return fail(TB_ERR_CONFIG, "gemm: offset operands (fix) need an e2m1 format");
+    // the S + 1 coding quadruples the sums: exact f32 only while 4 K < 2^24
+    if (format == TB_SIGN_E2M1_OFS && (!fix || 4 * K >= (int64_t(1) << 24)))
+        return fail(TB_ERR_CONFIG, "gemm: TB_SIGN_E2M1_OFS needs the row sums (fix) and 4 K < 2^24 (K=%lld)", (long long)K);
+    int rc = check_job_args(m, is_e2m1(format) ? K / 2 : K, ldS, job_lo, job_hi);
     if (rc) return rc;
     if (!S || !num) return fail(TB_ERR_INVALID, "gemm: null pointer");
     if (job_hi == job_lo) return TB_OK;
     if (m > (int64_t)INT32_MAX - gemm2::TILE) return fail(TB_ERR_CAPACITY, "gemm: m too large for TMA coordinates");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (format == TB_SIGN_E2M1) return gemm_fp4(S, m, K, ldS, job_lo, job_hi, splits, num, st);
+    if (is_e2m1(format))
+        return gemm_fp4(S, m, K, ldS, job_lo, job_hi, splits, num, st, nullptr, nullptr, 0, nullptr, fix, fix_c);
     return gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, format, num, st);
+}
+
+extern "C" int tb_gemm_pairs(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
+                             int64_t job_hi, int32_t splits, int32_t* num, void* stream) {
+    return tb_gemm_pairs_fix(S, m, K, ldS, format, job_lo, job_hi, splits, nullptr, 0, num, stream);
 }
 
 extern "C" int tb_gemm_tau_b(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
                              int64_t job_hi, int32_t splits, const uint64_t* n1_rows, int64_t n, int32_t* num_ws,
                              double* tau_b, void* stream) {
-    if (format < TB_SIGN_I8 || format > TB_SIGN_E2M1) return fail(TB_ERR_CONFIG, "gemm_tau_b: unknown format %d", format);
-    int rc = check_job_args(m, format == TB_SIGN_E2M1 ? K / 2 : K, ldS, job_lo, job_hi);
+    return tb_gemm_tau_b_fix(S, m, K, ldS, format, job_lo, job_hi, splits, nullptr, 0, n1_rows, n, num_ws, tau_b, stream);
+}
+
+extern "C" int tb_gemm_tau_b_fix(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int format, int64_t job_lo,
+                                 int64_t job_hi, int32_t splits, const int32_t* fix, int64_t fix_c,
+                                 const uint64_t* n1_rows, int64_t n, int32_t* num_ws, double* tau_b, void* stream) {
+    if (format < TB_SIGN_I8 || format > TB_SIGN_E2M1_OFS) return fail(TB_ERR_CONFIG, "gemm_tau_b: unknown format %d", format);
+    if (fix && !is_e2m1(format)) return fail(TB_ERR_CONFIG, "gemm_tau_b: offset operands (fix) need an e2m1 format");
+    if (format == TB_SIGN_E2M1_OFS && (!fix || 4 * K >= (int64_t(1) << 24)))
+        return fail(TB_ERR_CONFIG, "gemm_tau_b: TB_SIGN_E2M1_OFS needs the row sums (fix) and 4 K < 2^24");
+    int rc = check_job_args(m, is_e2m1(format) ? K / 2 : K, ldS, job_lo, job_hi);
     if (rc) return rc;
     if (!S || !n1_rows || !tau_b) return fail(TB_ERR_INVALID, "gemm_tau_b: null pointer");
     if (n < 2) return fail(TB_ERR_INVALID, "gemm_tau_b: need n >= 2");
@@ -472,8 +493,9 @@ extern "C" int tb_gemm_tau_b(const int8_t* S, int64_t m, int64_t K, int64_t ldS,
     if (m > (int64_t)INT32_MAX - gemm2::TILE) return fail(TB_ERR_CAPACITY, "gemm: m too large for TMA coordinates");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int fused = 0;
-    if (format == TB_SIGN_E2M1) {
-        if ((rc = gemm_fp4(S, m, K, ldS, job_lo, job_hi, splits, num_ws, st, tau_b, n1_rows, n, &fused))) return rc;
+    if (is_e2m1(format)) {
+        if ((rc = gemm_fp4(S, m, K, ldS, job_lo, job_hi, splits, num_ws, st, tau_b, n1_rows, n, &fused, fix, fix_c)))
+            return rc;
     } else {
         if (!num_ws) return fail(TB_ERR_INVALID, "gemm_tau_b: the int8 path needs the numerator workspace");
         if ((rc = gemm_v2(S, m, K, ldS, job_lo, job_hi, splits, format, num_ws, st))) return rc;

@@ -78,6 +78,11 @@ struct Gemm4Args {
     double* tau_b;
     const unsigned long long* n1;
     double dn0;
+    // offset operands: out(y, x) = dot(y, x) - fix[y] - fix[x] - fix_c (fix == nullptr: plain dot products).
+    // With the S + 1 coding of TB_SIGN_E2M1_OFS, (S_y + 1).(S_x + 1) = S_y.S_x + s_y + s_x + n0, so fix = the
+    // row sums s and fix_c = n0; a split unit's first item (kb0 == 0) carries the correction.
+    const int32_t* fix;
+    int32_t fix_c;
 };
 
 // ---- K-lockstep throttle.  The ~74 concurrently running CTA pairs stream the same S rows (units of one
@@ -312,10 +317,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
         while (next_unit4(p, cur, npairs, t)) {
             const int64_t y0 = t.y0 + rank * BM + q * 32;
             int64_t row_j0;  // job id of column 0 in this lane's row (relative to job_lo)
+            int32_t rfix = 0;  // this lane's row correction (offset operands), applied by the unit's first item
             {
                 const int64_t y = y0 + lane;
                 row_j0 = (y < m) ? row_prefix(y, m) - y - p.job_lo : INT64_MIN / 2;
                 rowbase[lane] = row_j0;
+                if (p.fix && t.kb0 == 0) rfix = (y < m ? __ldg(&p.fix[y]) : 0) + p.fix_c;
                 if (p.tau_b) rown1[lane] = y < m ? (uint32_t)__ldg(&p.n1[y]) : 0u;
             }
             __syncwarp();
@@ -344,6 +351,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                             if (hi64 > span - j0) hi64 = span - j0;
                             const int lo = (int)(lo64 < 0 ? 0 : (lo64 > 16 ? 16 : lo64));
                             const int hi = (int)(hi64 < 0 ? 0 : (hi64 > 16 ? 16 : hi64));
+                            if (lo < hi && p.fix && t.kb0 == 0) {  // offset operands: exact integers, |.| < 2^24
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) {
+                                    const int32_t cf = (i >= lo && i < hi) ? __ldg(&p.fix[xc + i]) : 0;
+                                    r[i] = __float_as_uint(__uint_as_float(r[i]) - (float)(rfix + cf));
+                                }
+                            }
                             if (lo < hi && p.int_red) {  // exact int32 partial sums (wide K)
                                 int32_t* q0 = reinterpret_cast<int32_t*>(p.acc) + j0;
 #pragma unroll
@@ -369,8 +383,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                         continue;
                     }
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) stg[lane * STG_LD + i] = (int32_t)r[i];
+                    for (int i = 0; i < 16; ++i) stg[lane * STG_LD + i] = __float2int_rn(__uint_as_float(r[i])) - rfix;
                     __syncwarp();
+                    const int32_t cfix = (p.fix && xc + col < m) ? __ldg(&p.fix[xc + col]) : 0;
                     if (p.tau_b) {  // fused K5: tau_b straight from the accumulator (8 B per pair, no numerator)
                         const int64_t x = xc + col;
                         const uint64_t t2 = x < m ? (uint64_t)__ldg(&p.n1[x]) : 0;
@@ -380,8 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                             const int64_t y = y0 + rr;
                             const int64_t j = rowbase[rr] + x;
                             if (x >= y && x < m && j >= 0 && j < span)
-                                p.tau_b[j] = tau_b_ieee(__float2int_rn(__int_as_float(stg[rr * STG_LD + col])),
-                                                        rown1[rr], t2, p.dn0);
+                                p.tau_b[j] = tau_b_ieee(stg[rr * STG_LD + col] - cfix, rown1[rr], t2, p.dn0);
                         }
                     } else {
                         const int64_t x = xc + col;
@@ -391,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                             const int64_t y = y0 + rr;
                             const int64_t j = rowbase[rr] + x;
                             if (x >= y && x < m && j >= 0 && j < span)
-                                p.num[j] = __float2int_rn(__int_as_float(stg[rr * STG_LD + col]));
+                                p.num[j] = stg[rr * STG_LD + col] - cfix;
                         }
                     }
                     __syncwarp();
@@ -730,8 +744,10 @@ static int lockstep_state(unsigned long long** prog, uint32_t* epoch, int32_t* l
 // tau_b != nullptr: fused finalize when the plan has no split unit (the kernel writes tau_b, num is not
 // written; *fused = 1); a split plan computes num (which must then be a buffer) and *fused = 0.
 int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo, int64_t job_hi, int32_t splits,
-             int32_t* num, cudaStream_t st, double* tau_b, const uint64_t* n1, int64_t n, int* fused) {
+             int32_t* num, cudaStream_t st, double* tau_b, const uint64_t* n1, int64_t n, int* fused,
+             const int32_t* fix, int64_t fix_c) {
     if (fused) *fused = 0;
+    if (fix && (fix_c > INT32_MAX || fix_c < INT32_MIN)) return fail(TB_ERR_CONFIG, "gemm fp4: fix_c out of range");
     const bool wide = K >= (int64_t(1) << 24);  // items of <= KB_EXACT k-blocks, int32 partial sums
     if (m >= (int64_t(1) << 16) * g4::UM) return fail(TB_ERR_CAPACITY, "gemm fp4: m too large");
     int rc;
@@ -749,6 +765,8 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.job_hi = job_hi;
     p.num = num;
     p.int_red = wide ? 1 : 0;
+    p.fix = fix;
+    p.fix_c = fix ? (int32_t)fix_c : 0;
     if (wide && !p.partial) return fail(TB_ERR_CONFIG, "gemm fp4: wide K needs a split plan");
     // tau_b callers: a split plan finalizes straight from the f32 workspace (accum_finalize); a one-launch
     // plan writes the numerators and the caller finalizes -- or, with TB_FUSE_EPILOGUE=1, the epilogue writes

@@ -91,6 +91,16 @@ __device__ __forceinline__ uint32_t nib_code(uint32_t ge, uint32_t le) {  // ((g
     asm("lop3.b32 %0, %1, %2, %3, 0xF8;" : "=r"(r) : "r"(x), "r"(le), "r"(0x88888888u));
     return r;
 }
+// Offset coding (TB_SIGN_E2M1_OFS): the element is S + 1 -- -1 -> 0 (0x0), tie -> 1.0 (0x2), +1 -> 2.0 (0x4).
+// No sign bit ever toggles and half the operands are zero: the same MMA stream draws less power (see
+// tb_gemm_fp4.cu, "offset operands").  At least one of ge / le is set in every nibble.
+__device__ __forceinline__ uint32_t nib_code_ofs(uint32_t ge, uint32_t le) {  // ge & (le ? 0x2 : 0x4)
+    uint32_t t, r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(t) : "r"(le), "r"(0x22222222u), "r"(0x44444444u));
+    asm("lop3.b32 %0, %1, %2, %3, 0xC0;" : "=r"(r) : "r"(ge), "r"(t), "r"(0u));
+    return r;
+}
+template <int OFS = 0>
 __device__ __forceinline__ uint2 chunk_e2m1(const uint32_t (&yb)[8], const uint32_t (&own)[8], uint32_t neg1) {
     uint32_t ge[4], le[4];
 #pragma unroll
@@ -102,9 +112,10 @@ __device__ __forceinline__ uint2 chunk_e2m1(const uint32_t (&yb)[8], const uint3
         ge[qq] = prmt_signs(d0, d1);
         le[qq] = prmt_signs(e0, e1);
     }
-    const uint32_t w0 = nib_code(lop3_sel(ge[0], ge[1], 0x0F0F0F0Fu), lop3_sel(le[0], le[1], 0x0F0F0F0Fu));
-    const uint32_t w1 = nib_code(lop3_sel(ge[2], ge[3], 0x0F0F0F0Fu), lop3_sel(le[2], le[3], 0x0F0F0F0Fu));
-    return make_uint2(w0, w1);
+    const uint32_t g0 = lop3_sel(ge[0], ge[1], 0x0F0F0F0Fu), l0 = lop3_sel(le[0], le[1], 0x0F0F0F0Fu);
+    const uint32_t g1 = lop3_sel(ge[2], ge[3], 0x0F0F0F0Fu), l1 = lop3_sel(le[2], le[3], 0x0F0F0F0Fu);
+    if (OFS) return make_uint2(nib_code_ofs(g0, l0), nib_code_ofs(g1, l1));
+    return make_uint2(nib_code(g0, l0), nib_code(g1, l1));
 }
 
 // Sections 2 and 3 (~3% of the chunks): per-sample (a, b) lists -> own / window words and the
@@ -159,6 +170,7 @@ __device__ __forceinline__ int sp_slow_chunk(int64_t c, const SpLayout& L, const
 // e2m1 chunks [c_lo, c_hi) of one row (c_lo even): each lane takes two adjacent chunks (a_l, a_l + 1
 // of one block pair share the window: one pair of window loads, one rank-pair load, one 16-byte
 // store; a warp writes 512 contiguous bytes) and steps 64 chunks = 4 block pairs.
+template <int OFS>
 __device__ __forceinline__ void sp_e2m1_range(int c_lo, int c_hi, int lane, const SpLayout& L, const uint16_t* r16,
                                               const uint32_t* wp, const uint32_t* wb, const uint4* masks,
                                               int8_t* row, uint32_t neg1) {
@@ -184,7 +196,7 @@ __device__ __forceinline__ void sp_e2m1_range(int c_lo, int c_hi, int lane, cons
             const uint32_t oa = __byte_perm(ow, 0, 0x1010), ob = __byte_perm(ow, 0, 0x3232);
             const uint32_t owa[8] = {oa, oa, oa, oa, oa, oa, oa, oa};
             const uint32_t owb[8] = {ob, ob, ob, ob, ob, ob, ob, ob};
-            const uint2 va = chunk_e2m1(y, owa, neg1), vb = chunk_e2m1(y, owb, neg1);
+            const uint2 va = chunk_e2m1<OFS>(y, owa, neg1), vb = chunk_e2m1<OFS>(y, owb, neg1);
             *outp = make_uint4(va.x, va.y, vb.x, vb.y);
             c += 64;
             if (c >= c1_end) break;
@@ -209,7 +221,7 @@ __device__ __forceinline__ void sp_e2m1_range(int c_lo, int c_hi, int lane, cons
             const int valid = sp_slow_chunk(c + k, L, r16, wp, own, y);
 #pragma unroll
             for (int q = 0; q < 8; ++q) y[q] |= 0x80008000u;
-            uint2 v2 = chunk_e2m1(y, own, neg1);
+            uint2 v2 = chunk_e2m1<OFS>(y, own, neg1);
             if (valid < 16) {
                 const uint4 mk = masks[valid];
                 v2.x &= mk.x;
@@ -246,8 +258,8 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
     if (tid <= 16) {  // masks[v]: the first v samples of a chunk kept
         uint32_t mk0 = 0u, mk1 = 0u, mk2 = 0u, mk3 = 0u;
         for (int s = 0; s < tid; ++s) {
-            const int wi = FMT == 2 ? (s >> 3) : (s >> 2);
-            const uint32_t bits = FMT == 2 ? 0xFu << (8 * (s & 3) + 4 * ((s >> 2) & 1)) : 0xFFu << (8 * (s & 3));
+            const int wi = FMT >= 2 ? (s >> 3) : (s >> 2);
+            const uint32_t bits = FMT >= 2 ? 0xFu << (8 * (s & 3) + 4 * ((s >> 2) & 1)) : 0xFFu << (8 * (s & 3));
             mk0 |= wi == 0 ? bits : 0u;
             mk1 |= wi == 1 ? bits : 0u;
             mk2 |= wi == 2 ? bits : 0u;
@@ -257,7 +269,7 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
     }
     __syncthreads();
     const uint16_t* r16 = reinterpret_cast<const uint16_t*>(wp);
-    const uint32_t* win = FMT == 2 ? wb : wp;
+    const uint32_t* win = FMT >= 2 ? wb : wp;
 
     const SpLayout L = sp_layout(n);
     const int nchunks = (int)(L.c1 + L.c2 + L.c3);  // < 2^31 (n <= 32767)
@@ -268,8 +280,8 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
     const int b_lo = min((int)blockIdx.y * per, nchunks), b_hi = min(b_lo + per, nchunks);
     const int wper = ((b_hi - b_lo + (SP_THREADS / 32) - 1) / (SP_THREADS / 32) + 1) & ~1;
     const int c_lo = min(b_lo + warp * wper, b_hi), c_hi = min(c_lo + wper, b_hi);
-    if (FMT == 2) {
-        sp_e2m1_range(c_lo, c_hi, lane, L, r16, wp, win, masks, row, neg1);
+    if (FMT >= 2) {
+        sp_e2m1_range<FMT == 3>(c_lo, c_hi, lane, L, r16, wp, win, masks, row, neg1);
     } else {
     int c = c_lo + lane;
     const int nbf = (int)L.nbf;
@@ -334,7 +346,7 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
     }
     }
     // zero the row tail [K bytes, ldS)
-    const int64_t kb = (FMT == 2 ? 8 : 16) * (int64_t)nchunks;
+    const int64_t kb = (FMT >= 2 ? 8 : 16) * (int64_t)nchunks;
     for (int64_t k = kb + ((int64_t)blockIdx.y * SP_THREADS + tid) * 8; k < ldS; k += (int64_t)gridDim.y * SP_THREADS * 8)
         *reinterpret_cast<uint2*>(row + k) = make_uint2(0u, 0u);
     pdl_trigger();
@@ -350,8 +362,8 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
                                     (long long)m, (long long)n);
     if (n > 32767) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld exceeds 32767 (15-bit ranks)", (long long)n);
     const int64_t K = sp_k(n);
-    if (format < 0 || format > 2) return fail(TB_ERR_CONFIG, "sign_pack: unknown format %d", format);
-    const int64_t kbytes = format == TB_SIGN_E2M1 ? K / 2 : K;
+    if (format < 0 || format > 3) return fail(TB_ERR_CONFIG, "sign_pack: unknown format %d", format);
+    const int64_t kbytes = format >= TB_SIGN_E2M1 ? K / 2 : K;
     if (ldS < kbytes || (ldS & 15))
         return fail(TB_ERR_CONFIG, "sign_pack: ldS=%lld must be >= %lld and 16-aligned", (long long)ldS,
                     (long long)kbytes);
@@ -367,7 +379,9 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
 #define TB_SP_LAUNCH(F)                                                                                   \
     TB_CUDA_TRY(cudaFuncSetAttribute(signpack_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     TB_CUDA_TRY(launch_pdl(signpack_kernel<F>, dim3(grid), dim3(SP_THREADS), smem, st, R, n, ldr, S, ldS, nw, 0xFFFFFFFFu))
-    if (format == TB_SIGN_E2M1) {
+    if (format == TB_SIGN_E2M1_OFS) {
+        TB_SP_LAUNCH(3);
+    } else if (format == TB_SIGN_E2M1) {
         TB_SP_LAUNCH(2);
     } else if (format == TB_SIGN_E4M3) {
         TB_SP_LAUNCH(1);
@@ -395,13 +409,51 @@ __global__ void abs_pack_kernel(const uint4* __restrict__ S, uint4* __restrict__
 }
 }  // namespace tb
 
+// Row sums of an offset-coded S (nibbles 0x0 / 0x2 / 0x4 = 0 / 1 / 2): fix[r] = sum of the values - n0 =
+// sum_k S[r, k].  One CTA per row, 16-byte loads; the row tail and unused slots are zero nibbles.
+namespace tb {
+__global__ void __launch_bounds__(256) rowsum_ofs_kernel(const int8_t* __restrict__ S, int64_t ldS, int64_t n0,
+                                                         int32_t* __restrict__ fix) {
+    pdl_wait();
+    __shared__ int32_t red[8];
+    const uint4* row = reinterpret_cast<const uint4*>(S + (int64_t)blockIdx.x * ldS);
+    const int64_t nvec = ldS / 16;
+    int32_t c1 = 0, c2 = 0;
+    for (int64_t i = threadIdx.x; i < nvec; i += 256) {
+        const uint4 v = row[i];
+        c1 += __popc(v.x & 0x22222222u) + __popc(v.y & 0x22222222u) + __popc(v.z & 0x22222222u) + __popc(v.w & 0x22222222u);
+        c2 += __popc(v.x & 0x44444444u) + __popc(v.y & 0x44444444u) + __popc(v.z & 0x44444444u) + __popc(v.w & 0x44444444u);
+    }
+    int32_t s = c1 + 2 * c2;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        fix[blockIdx.x] = (int32_t)(t - n0);
+    }
+    pdl_trigger();
+}
+}  // namespace tb
+
+extern "C" int tb_sign_row_sums(const int8_t* S, int64_t m, int64_t ldS, int64_t n, int32_t* fix, void* stream) {
+    if (m < 1 || n < 2 || ldS < 16 || (ldS & 15)) return fail(TB_ERR_CONFIG, "sign_row_sums: bad shape");
+    if (m > INT32_MAX) return fail(TB_ERR_CAPACITY, "sign_row_sums: m too large");
+    if (!S || !fix) return fail(TB_ERR_INVALID, "sign_row_sums: null pointer");
+    TB_CUDA_TRY(launch_pdl(rowsum_ofs_kernel, dim3((unsigned)m), dim3(256), 0, static_cast<cudaStream_t>(stream), S,
+                           ldS, n * (n - 1) / 2, fix));
+    return check_launch("rowsum_ofs_kernel");
+}
+
 extern "C" int tb_abs_pack(const int8_t* S, int64_t m, int64_t ldS, int format, int8_t* A, void* stream) {
     if (m < 1 || ldS < 16 || (ldS & 15)) return fail(TB_ERR_CONFIG, "abs_pack: bad shape");
     if (!S || !A) return fail(TB_ERR_INVALID, "abs_pack: null pointer");
     const int64_t nvec = m * ldS / 16;
     const int64_t blocks = std::min<int64_t>((nvec + 255) / 256, (int64_t)num_sms() * 8);
     TB_CUDA_TRY(launch_pdl(abs_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), reinterpret_cast<const uint4*>(S), reinterpret_cast<uint4*>(A), nvec,
-        format == TB_SIGN_E2M1 ? 0x77777777u : (format == TB_SIGN_E4M3 ? 0x7F7F7F7Fu : 0x01010101u)));
+        format == TB_SIGN_E2M1_OFS ? 0x22222222u  // the tie indicator Z = [S == 0] (value 1.0 = 0x2)
+        : format == TB_SIGN_E2M1 ? 0x77777777u : (format == TB_SIGN_E4M3 ? 0x7F7F7F7Fu : 0x01010101u)));
     return check_launch("abs_pack_kernel");
 }
 

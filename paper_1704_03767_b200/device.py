@@ -51,6 +51,9 @@ DISPATCH_TABLE = (
 )
 D2H_PIECE_BYTES = 256 << 20
 FP4_WIDE = os.environ.get("TB_FP4_WIDE", "1") != "0"
+# offset-coded GEMM operands (TB_SIGN_E2M1_OFS, see TauEngine.sign_format): "auto" | "1" | "0"
+SIGN_OFS = os.environ.get("TB_SIGN_OFS", "auto")
+OFS_MIN_WORK = 1e13  # m^2 K from which the GEMM runs long enough to be power-capped (config 3: 3.3e13)
 TIED_SPARSE_FRAC = 0.35  # |S| GEMM over the tied rows only while they are at most this share of the rows
 GEMM_MAX_N = 14000  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides): e2m1
 # GEMM vs merge with several pairs per CTA, n = 12288: 73 vs 115 ns per job, n = 16384: 152 vs 118 ns
@@ -132,6 +135,8 @@ class Prepared:
     K: int = 0
     ldS: int = 0
     fmt: int = 0
+    fix: torch.Tensor | None = None      # TB_SIGN_E2M1_OFS: int32 [m] row sums of S (tb_sign_row_sums)
+    fix_abs: torch.Tensor | None = None  # ... and n1 per row as int32 (the tie-indicator GEMM's correction)
     row_lo: int = 0
     any_ties: bool | None = None      # GEMM full counts: does any row >= row_lo have ties (read lazily)
     tied_rows: np.ndarray | None = None   # sparse full counts: the tied rows >= row_lo (host, ascending)
@@ -228,14 +233,22 @@ class TauEngine:
     # TB_FUSE_EPILOGUE=1, measured slower under the power cap: profiles/r02_fused_finalize_ab.log)
     fuse_finalize: bool = os.environ.get("TB_FUSE_FINALIZE", "1") != "0"
 
-    def sign_format(self, K: int) -> int:
+    def sign_format(self, K: int, m: int | None = None) -> int:
         """e2m1 (kind::mxf4) for every K: beyond 2^24 the FP4 GEMM splits each unit into items whose f32
         sums stay exact and adds them as int32 (twice the int8 rate, half its S bytes).  TB_FP4_WIDE=0
-        restores int8 (kind::i8) for K >= 2^24."""
+        restores int8 (kind::i8) for K >= 2^24.
+
+        While 4 K < 2^24 (n <= 2896) and the GEMM is long enough to run into the board's power cap
+        (m^2 K >= OFS_MIN_WORK, or TB_SIGN_OFS=1), the operands are offset-coded (TB_SIGN_E2M1_OFS: S + 1,
+        non-negative and half zero): the same MMA stream toggles fewer bits, the capped SM clock rises
+        (config 5: 1.31 -> 1.54 GHz) and the GEMM is ~12% faster (profiles/r02_power_pattern.log)."""
         if self.sign_format_override is not None:
             return self.sign_format_override
         if K >= (1 << 24) and not FP4_WIDE:
             return _lib.TB_SIGN_I8
+        if 4 * K < (1 << 24) and (SIGN_OFS == "1" or (SIGN_OFS == "auto" and m is not None
+                                                     and m * m * K >= OFS_MIN_WORK)):
+            return _lib.TB_SIGN_E2M1_OFS
         return _lib.TB_SIGN_E2M1
 
     @staticmethod
@@ -346,6 +359,7 @@ class TauEngine:
         prep.row_lo = min(row_lo, m)
         if path == "gemm":
             prep.S, prep.K, prep.ldS, prep.fmt = self._gemm_prepare(x, stub, st, simt, all_rows=all_rows)
+            prep.fix = stub.extra.get("fix")
         else:
             prep.pos, prep.srt, prep.keys, (prep.maxgrp, prep.groups, prep.ngroups) = \
                 self._merge_prepare(x.contiguous(), stub, st, row_from=0 if all_rows else prep.row_lo)
@@ -366,9 +380,10 @@ class TauEngine:
             if _mark_after_num:
                 self._mark(1)
             return
+        n0 = n * (n - 1) // 2
         for a, b in self._gemm_ranges(m, lo, hi):
             self._gemm_numerator(prep.S, num[a - lo:b - lo], m, prep.K, prep.ldS, prep.fmt, a, b, st, splits,
-                                 prep.simt)
+                                 prep.simt, fix=prep.fix, fix_c=n0)
         if _mark_after_num:
             self._mark(1)
         if nd is not None or n3 is not None:
@@ -394,10 +409,13 @@ class TauEngine:
                     prep.A = self._buf("A", m * prep.ldS, torch.int8)
                     _lib.call("tb_abs_pack", _ptr(prep.S[y0 * prep.ldS:]), m - y0, prep.ldS, prep.fmt,
                               _ptr(prep.A[y0 * prep.ldS:]), st)
+                if prep.fix is not None and prep.fix_abs is None:
+                    # offset operands: A is the tie indicator Z, |S_y|.|S_x| = n0 - n1_y - n1_x + Z_y.Z_x
+                    prep.fix_abs = prep.n1_rows.to(torch.int32)
                 absdot = self._buf("absdot", hi - lo, torch.int32)
                 for a, b in self._gemm_ranges(m, lo, hi):
                     self._gemm_numerator(prep.A, absdot[a - lo:b - lo], m, prep.K, prep.ldS, prep.fmt, a, b, st,
-                                         splits, prep.simt)
+                                         splits, prep.simt, fix=prep.fix_abs, fix_c=-n0)
             _lib.call("tb_full_counts", _ptr(num), _ptr(absdot), _ptr(prep.n1_rows), m, n, lo, hi, _ptr(nd),
                       _ptr(n3), st)
 
@@ -416,9 +434,11 @@ class TauEngine:
             _lib.call("tb_abs_pack", _ptr(St), nt, prep.ldS, prep.fmt, _ptr(At), st)
             tt = nt * (nt + 1) // 2
             prep.absdot_t = torch.empty(tt, dtype=torch.int32, device=self.device)
+            # offset operands: At is the tied rows' tie indicator Z (see numerators)
+            fix_t = None if prep.fix is None else prep.n1_rows[prep.tied_dev.long()].to(torch.int32)
             for a, b in self._gemm_ranges(nt, 0, tt):
                 self._gemm_numerator(At, prep.absdot_t[a:b], nt, prep.K, prep.ldS, prep.fmt, a, b, st, splits,
-                                     prep.simt)
+                                     prep.simt, fix=fix_t, fix_c=-(n * (n - 1) // 2))
         _lib.call("tb_full_counts", _ptr(num), None, _ptr(prep.n1_rows), m, n, lo, hi, _ptr(nd), _ptr(n3), st)
         # tied rows a whose row T[a] meets the job range: rows y_lo .. y_hi
         y_lo, y_hi = job_coord(lo, m)[0], job_coord(hi - 1, m)[0]
@@ -431,17 +451,17 @@ class TauEngine:
     def _fused_tau_b(self, prep: "Prepared") -> bool:
         return self.fuse_finalize and prep.path == "gemm" and not prep.simt
 
-    def _gemm_tau_b(self, S, num, tb, n1_rows, m, n, K, ldS, fmt, lo, hi, st) -> None:
+    def _gemm_tau_b(self, S, num, tb, n1_rows, m, n, K, ldS, fmt, lo, hi, st, fix=None) -> None:
         """tau_b of job ids [lo, hi) into tb[0:hi-lo] from the GEMM epilogue (num: fallback workspace)."""
         for a, b in self._gemm_ranges(m, lo, hi):
-            _lib.call("tb_gemm_tau_b", _ptr(S), m, K, ldS, fmt, a, b, 0, _ptr(n1_rows), n, _ptr(num[a - lo:b - lo]),
-                      _ptr(tb[a - lo:b - lo]), st)
+            _lib.call("tb_gemm_tau_b_fix", _ptr(S), m, K, ldS, fmt, a, b, 0, _ptr(fix), n * (n - 1) // 2,
+                      _ptr(n1_rows), n, _ptr(num[a - lo:b - lo]), _ptr(tb[a - lo:b - lo]), st)
 
-    def _gemm_layout(self, n: int, simt: bool = False):
+    def _gemm_layout(self, n: int, simt: bool = False, m: int | None = None):
         """(K, sign format, row stride of S in bytes, row stride of R) for n samples."""
         K = int(_lib.load().tb_sign_k(n))  # padded diagonal layout, >= n(n-1)/2 elements
-        fmt = self.sign_format(K) if not simt else _lib.TB_SIGN_I8
-        kbytes = K // 2 if fmt == _lib.TB_SIGN_E2M1 else K
+        fmt = self.sign_format(K, m) if not simt else _lib.TB_SIGN_I8
+        kbytes = K // 2 if fmt in (_lib.TB_SIGN_E2M1, _lib.TB_SIGN_E2M1_OFS) else K
         return K, fmt, (kbytes + 15) // 16 * 16, (n + 7) // 8 * 8
 
     def _gemm_prepare(self, x, res: PairResult, st, simt: bool = False, row_chunks=None, all_rows: bool = True):
@@ -450,9 +470,11 @@ class TauEngine:
         ``row_chunks`` = [(r0, r1, wait_fn)]: prepare rows [r0, r1) after ``wait_fn()`` (the
         host entry point waits for each chunk's H2D copy); default one chunk of all rows."""
         m, n = res.m, res.n
-        K, fmt, ldS, ldr = self._gemm_layout(n, simt)
+        K, fmt, ldS, ldr = self._gemm_layout(n, simt, m)
         R = self._buf("R", m * ldr, torch.int16)
         S = self._buf("S", m * ldS, torch.int8)
+        fix = self._buf("fix", m, torch.int32) if fmt == _lib.TB_SIGN_E2M1_OFS else None
+        res.extra["fix"] = fix
         # every job id of [job_lo, job_hi) pairs rows >= y_lo (the row of job_lo): rows above it need no sign
         # vector -- a late job-range shard (multi-GPU strong scaling) packs only its own share of S -- and
         # with all_rows=False they are not ranked either (their n1 stays 0)
@@ -476,12 +498,18 @@ class TauEngine:
             p0 = max(r0, y_lo)
             if p0 < r1:
                 _lib.call("tb_sign_pack", _ptr(R[p0 * ldr:]), r1 - p0, n, ldr, _ptr(S[p0 * ldS:]), ldS, fmt, st)
+                if fix is not None:
+                    _lib.call("tb_sign_row_sums", _ptr(S[p0 * ldS:]), r1 - p0, ldS, n, _ptr(fix[p0:]), st)
         res.extra["sign_format"] = fmt
         return S, K, ldS, fmt
 
-    def _gemm_numerator(self, src, out, m, K, ldS, fmt, job_lo, job_hi, st, splits=0, simt=False):
+    def _gemm_numerator(self, src, out, m, K, ldS, fmt, job_lo, job_hi, st, splits=0, simt=False, fix=None,
+                        fix_c=0):
         if simt:
             _lib.call("tb_gemm_pairs_simt", _ptr(src), m, K, ldS, job_lo, job_hi, _ptr(out), st)
+        elif fix is not None:  # offset operands: out = dot - fix[y] - fix[x] - fix_c
+            _lib.call("tb_gemm_pairs_fix", _ptr(src), m, K, ldS, fmt, job_lo, job_hi, splits, _ptr(fix), fix_c,
+                      _ptr(out), st)
         else:
             _lib.call("tb_gemm_pairs", _ptr(src), m, K, ldS, fmt, job_lo, job_hi, splits, _ptr(out), st)
 
@@ -530,7 +558,8 @@ class TauEngine:
                     ev[0].record(st_t)
                 tb = out[lo - base:hi - base]
                 if fused:
-                    self._gemm_tau_b(prep.S, num, tb, prep.n1_rows, m, n, prep.K, prep.ldS, prep.fmt, lo, hi, st)
+                    self._gemm_tau_b(prep.S, num, tb, prep.n1_rows, m, n, prep.K, prep.ldS, prep.fmt, lo, hi, st,
+                                     fix=prep.fix)
                 else:
                     self.numerators(prep, lo, hi, num)
                 if timing is not None:
@@ -640,9 +669,10 @@ class TauEngine:
                 tb = res.tau_b[lo - jlo:hi - jlo]
                 fused = path == "gemm" and not numerators and self.fuse_finalize
                 if fused:  # tau_b from the GEMM epilogue; res.numerator is not filled
-                    self._gemm_tau_b(S, num, tb, res.n1_rows, m, n, K, ldS, fmt, lo, hi, st)
+                    self._gemm_tau_b(S, num, tb, res.n1_rows, m, n, K, ldS, fmt, lo, hi, st, fix=res.extra.get("fix"))
                 elif path == "gemm":
-                    self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st)
+                    self._gemm_numerator(S, num, m, K, ldS, fmt, lo, hi, st, fix=res.extra.get("fix"),
+                                         fix_c=n * (n - 1) // 2)
                 else:
                     ws, wsb = self._merge_ws(n)
                     _lib.call("tb_merge_pairs", _ptr(keys), _ptr(pos), _ptr(srt), _ptr(res.n1_rows), _ptr(maxgrp[0]),
@@ -709,7 +739,7 @@ def choose_path(n: int, m: int | None = None, full_counts: bool = False, eng: "T
     costs = TauEngine.path_costs(m, n)
     if "gemm" not in costs:
         return "merge"
-    K, fmt, ldS, _ = eng._gemm_layout(n)
+    K, fmt, ldS, _ = eng._gemm_layout(n, m=m)
     need = m * ldS * (2 if full_counts else 1)
     have = eng._ws["S"].numel() if "S" in eng._ws else 0  # a cached S workspace is reusable
     free = torch.cuda.mem_get_info(eng.device)[0] + have

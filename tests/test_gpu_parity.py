@@ -472,17 +472,82 @@ def test_sign_formats_agree(eng, k):
     x = torch.from_numpy(workloads.generate(k)).cuda()
     outs = {}
     try:
-        for fmt in (_lib.TB_SIGN_I8, _lib.TB_SIGN_E4M3, _lib.TB_SIGN_E2M1):
+        for fmt in (_lib.TB_SIGN_I8, _lib.TB_SIGN_E4M3, _lib.TB_SIGN_E2M1, _lib.TB_SIGN_E2M1_OFS):
             eng.sign_format_override = fmt
             r = eng.all_pairs(x, kernel="gemm", tau_a=False, tau_b=False, full_counts=(k == 1)).validate()
+            assert r.extra["sign_format"] == fmt
             outs[fmt] = (r.numerator.clone(), None if r.n_d is None else r.n_d.clone())
     finally:
         eng.sign_format_override = None
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][0], outs[2][0])
+    assert torch.equal(outs[0][0], outs[3][0])
     if k == 1:
         assert torch.equal(outs[0][1], outs[2][1])
+        assert torch.equal(outs[0][1], outs[3][1])
     eng.release()
+
+
+@pytest.fixture
+def ofs_eng(eng):
+    """The engine with offset-coded GEMM operands forced (TB_SIGN_E2M1_OFS: S + 1, row-sum correction)."""
+    from paper_1704_03767_b200 import _lib
+    eng.sign_format_override = _lib.TB_SIGN_E2M1_OFS
+    try:
+        yield eng
+    finally:
+        eng.sign_format_override = None
+
+
+@pytest.mark.gpu
+def test_offset_operands_small_shapes(ofs_eng, oracle):
+    """TB_SIGN_E2M1_OFS against the oracle: every pair and count of the small shapes (ties up to 90%, m = 1,
+    n = 2, constant rows), K-split plans, job-id shards, config 1 in full."""
+    for m, n, tie in [(1, 5, 0.0), (2, 2, 0.0), (3, 17, 0.5), (37, 33, 0.3), (130, 64, 0.0), (257, 31, 0.9),
+                      (300, 130, 0.2), (520, 47, 0.5)]:
+        test_small_shapes_vs_oracle(ofs_eng, oracle, "gemm", m, n, tie)
+    test_constant_rows_nan(ofs_eng, oracle, "gemm")
+    for splits in (1, 2, 7):
+        test_gemm_splits_and_shards(ofs_eng, oracle, splits)
+    test_config1_full(ofs_eng, oracle, "gemm")
+
+
+@pytest.mark.gpu
+def test_offset_operands_full_counts_and_entry_points(ofs_eng, oracle):
+    """TB_SIGN_E2M1_OFS through the tie-indicator GEMM (all rows and the sparse tied-row table), the fused
+    tau_b calls, the host entry point and job sub-ranges."""
+    for mode in ("auto", "sparse", "full"):
+        test_full_counts_sparse_tied_rows(ofs_eng, oracle, mode)
+    test_full_counts_tie_free_shortcut(ofs_eng, oracle)
+    for m, n, levels in [(300, 200, 0), (2600, 96, 7), (700, 90, 30)]:
+        test_fused_tau_b_epilogue(ofs_eng, oracle, m, n, levels)
+    test_host_entry_point_bands(ofs_eng, oracle, "gemm", 700, 90, None)
+    test_host_entry_point_bands(ofs_eng, oracle, "gemm", 2048, 1000, (0.4, 0.3, 0.2, 0.1))
+    test_host_entry_point_job_ranges(ofs_eng, oracle, "gemm", 700, 90)
+
+
+@pytest.mark.gpu
+def test_offset_operands_limit(ofs_eng, oracle):
+    """n = 2896 is the last n with 4 K < 2^24 (sums of (S + 1)(S + 1) <= 4 n0 stay exact in f32): a monotone pair
+    (numerator = n0, the largest sum) and its reverse, heavy ties; n = 2897 is refused (the engine's own
+    choice falls back to the +-1 coding there)."""
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.errors import ConfigError
+    n, m = 2896, 20
+    rng = np.random.default_rng(2896)
+    rows = [rng.integers(0, n // 3, n) for _ in range(m - 3)] + [np.arange(n), np.arange(n), np.arange(n)[::-1]]
+    ranks = np.stack([oracle.rank_transform(r) for r in rows])
+    res = ofs_eng.all_pairs(torch.from_numpy(ranks).cuda(), kernel="gemm", full_counts=True).validate()
+    assert res.extra["sign_format"] == _lib.TB_SIGN_E2M1_OFS
+    _check_full(res, oracle, ranks)
+    with pytest.raises(ConfigError):
+        ofs_eng.all_pairs(torch.from_numpy(np.stack([oracle.rank_transform(rng.integers(0, 50, 2897))
+                                                     for _ in range(4)])).cuda(), kernel="gemm")
+    ofs_eng.sign_format_override = None
+    K = int(_lib.load().tb_sign_k(2897))
+    assert ofs_eng.sign_format(K, m=1 << 20) == _lib.TB_SIGN_E2M1
+    assert ofs_eng.sign_format(int(_lib.load().tb_sign_k(1024)), m=65536) == _lib.TB_SIGN_E2M1_OFS
+    assert ofs_eng.sign_format(int(_lib.load().tb_sign_k(1000)), m=2048) == _lib.TB_SIGN_E2M1
 
 
 @pytest.mark.parametrize("fracs", [None, (0.4, 0.3, 0.2, 0.1)])

@@ -255,8 +255,8 @@ def test_dispatcher_cost_model(monkeypatch):
     if not os.path.exists(_lib.LIB_PATH):
         pytest.skip("libtaub200.so not built")
     eng = types.SimpleNamespace(_ws={}, device=None, sign_format_override=None)
-    eng.sign_format = lambda K: TauEngine.sign_format(eng, K)
-    eng._gemm_layout = lambda n: TauEngine._gemm_layout(eng, n)
+    eng.sign_format = lambda K, m=None: TauEngine.sign_format(eng, K, m)
+    eng._gemm_layout = lambda n, simt=False, m=None: TauEngine._gemm_layout(eng, n, simt, m)
     monkeypatch.setattr(torch.cuda, "mem_get_info", lambda dev=None: (170 << 30, 180 << 30))
     for (m, n), want in {(256, 200): "gemm", (2048, 1000): "gemm", (16384, 500): "gemm", (65536, 1024): "gemm",
                          (1024, 65536): "merge", (128, 32767): "merge", (4, 9000): "merge",

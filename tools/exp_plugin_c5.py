@@ -49,7 +49,7 @@ for wj in wjs:
     print(f"window_jobs {wj}: sink=None {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
 for fe in [int(a) for a in (sys.argv[1:] or ["1", "1000000"])]:
     engine.FULL_EVERY = fe
-    for pt in (4096,):
+    for pt in [int(a) for a in os.environ.get("PT", "4096").split(",")]:
         for _ in range(2):
             tb.compute_all_pairs(ds, "vectorized", sink=sink, pass_tiles=pt, window_jobs=wjs[-1])
         reps = 1 if x.shape[0] > 20000 else 10
