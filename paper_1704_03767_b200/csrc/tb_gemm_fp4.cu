@@ -92,9 +92,14 @@ struct Gemm4Args {
 // producer publishes its progress and waits while it is more than `lead` k-blocks ahead of the slowest
 // pair still running.  Entries of another launch (epoch) count as finished, so a pair never waits on a
 // pair that has not published in this launch: the slowest running pair never waits, no deadlock.
+// The poll is one round of parallel loads over the producer warp (prog_behind_warp) -- the first version
+// scanned the ~74 entries from one thread, ~16 us of serialized L2 round trips per check, which starved the
+// TMA ring and lost more than the clock gained (profiles/r02_gemm_lockstep.log).  With the warp-wide poll
+// config 5 drops from 367 to 322 ms per step (lead 32; DRAM reads / band ~3.6x lower, capped SM clock 1552 ->
+// 1717 MHz, profiles/r02_gemm_lockstep_v2.log).
 constexpr int LOCK_CHK = 16;
 #ifndef GEMM_LOCK_LEAD
-#define GEMM_LOCK_LEAD 0  // default allowed lead (k-blocks); 0 = throttle off
+#define GEMM_LOCK_LEAD 32  // default allowed lead (k-blocks); TB_GEMM_LEAD=0 turns the throttle off
 #endif
 __device__ __forceinline__ void prog_publish(unsigned long long* prog, int64_t pair, uint32_t epoch, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(prog + pair), "l"(((unsigned long long)epoch << 32) | v)
@@ -110,6 +115,18 @@ __device__ __forceinline__ int prog_behind(const unsigned long long* prog, int64
         if ((uint32_t)(v >> 32) == epoch && (uint64_t)(uint32_t)v + lead < done) ++c;
     }
     return c;
+}
+
+// warp-parallel form: lane l scans pairs l, l + 32, ...; every lane returns the warp's total
+__device__ __forceinline__ int prog_behind_warp(const unsigned long long* prog, int64_t npairs, uint32_t epoch,
+                                                uint32_t done, uint32_t lead, int lane) {
+    int c = 0;
+    for (int64_t q = lane; q < npairs; q += 32) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(prog + q) : "memory");
+        if ((uint32_t)(v >> 32) == epoch && (uint64_t)(uint32_t)v + lead < done) ++c;
+    }
+    return __reduce_add_sync(0xffffffffu, c);
 }
 
 #ifndef GEMM_DB  // 1: single-block units alternating between the two TMEM accumulator sets, so a unit's MMAs
@@ -215,24 +232,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
     tc_fence_after();
     pdl_wait();  // the setup above overlaps the sign pack's tail; S and the accumulators are read after it
 
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-            int stage = 0;
-            uint32_t phase = 0;
-            int64_t cur = pair;
-            Unit4 t;
-            const bool lock = p.lead > 0 && leader;
-            uint32_t done = 0;
-            if (lock) prog_publish(p.prog, pair, p.epoch, 0);
-            while (next_unit4(p, cur, npairs, t)) {
-                // each block loads a full 120-row box per CTA; the 2-SM MMA with N reads N / 2 rows of
-                // each CTA, so CTA 1's box starts at N / 2 (partial blocks need no other tensor map)
-                const uint32_t bytes = 2 * (A_BYTES + t.nblk * B_BYTES);
-                for (int32_t kb = t.kb0; kb < t.kb1; ++kb, ++done) {
-                    if (lock && (done % LOCK_CHK) == 0) {
-                        prog_publish(p.prog, pair, p.epoch, done);
-                        while (prog_behind(p.prog, npairs, p.epoch, done, (uint32_t)p.lead) > p.lagq) __nanosleep(200);
-                    }
+    if (warp == 0) {  // ---------------- TMA producer (both CTAs): the whole warp walks the loop, lane 0 issues
+        int stage = 0;
+        uint32_t phase = 0;
+        int64_t cur = pair;
+        Unit4 t;
+        const bool lock = p.lead > 0 && leader;
+        uint32_t done = 0;
+        if (lock && lane == 0) prog_publish(p.prog, pair, p.epoch, 0);
+        while (next_unit4(p, cur, npairs, t)) {
+            // each block loads a full 120-row box per CTA; the 2-SM MMA with N reads N / 2 rows of
+            // each CTA, so CTA 1's box starts at N / 2 (partial blocks need no other tensor map)
+            const uint32_t bytes = 2 * (A_BYTES + t.nblk * B_BYTES);
+            for (int32_t kb = t.kb0; kb < t.kb1; ++kb, ++done) {
+                if (lock && (done % LOCK_CHK) == 0) {
+                    // one poll = one round of parallel loads (lane l reads pairs l, l + 32, ...) and a warp
+                    // reduction: ~1 L2 latency every LOCK_CHK k-blocks, hidden behind the stages in flight
+                    if (lane == 0) prog_publish(p.prog, pair, p.epoch, done);
+                    while (prog_behind_warp(p.prog, npairs, p.epoch, done, (uint32_t)p.lead, lane) > p.lagq)
+                        __nanosleep(400);
+                }
+                if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
@@ -241,11 +261,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                     for (int h = 0; h < t.nblk; ++h)
                         tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
                                         (int32_t)(t.xs[h] + rank * (t.nb[h] / 2)));
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
-            if (lock) prog_publish(p.prog, pair, p.epoch, 0xFFFFFFFFu);
         }
+        if (lock && lane == 0) prog_publish(p.prog, pair, p.epoch, 0xFFFFFFFFu);
     } else if (warp == 1) {
         if (leader) {  // ---------------- MMA issuer (leader CTA, warp 1; one elected lane issues)
             // The issue loop is kept branch- and arithmetic-light: one thread feeds the 2-SM tensor pipe,
@@ -791,7 +812,9 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
         p.unit_splits = plan->at<const int32_t>(plan->off_splits);
         p.unit_cnt = plan->at<int32_t>(plan->off_cnt);
     }
-    if ((rc = lockstep_state(&p.prog, &p.epoch, &p.lead))) return rc;
+    // K-lockstep: multi-wave plans without K splits (every unit walks the same k-blocks, so the cumulative
+    // k-block count is the K position); one-wave plans start in step anyway
+    if (!p.partial && p.nitems > pairs && (rc = lockstep_state(&p.prog, &p.epoch, &p.lead))) return rc;
     {
         static const int32_t kLagQ = [] { const char* e = std::getenv("TB_GEMM_LAGQ"); return e ? std::max(0, atoi(e)) : 0; }();
         p.lagq = kLagQ;
