@@ -7,6 +7,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <functional>
 #include <mutex>
 #include <thread>
@@ -31,6 +32,10 @@ struct N3Src {
 // into the 24 quadwords of four consecutive 48-byte records (6 unpacks + 6 lane permutes + 6 stores).  Rows
 // whose n3 comes from the tied-row table stay on the scalar loop.  Returns the first j not written.
 static const bool g_has_avx2 = __builtin_cpu_supports("avx2");
+static const int64_t g_prefetch_ahead = [] {
+    const char* e = std::getenv("TB_EXPAND_PREFETCH");  // bytes ahead of the stores; 0 = off
+    return e ? (int64_t)std::max(0, atoi(e)) : (int64_t)0;
+}();
 
 template <bool NUM_ONLY, bool STREAM>
 __attribute__((target("avx2"))) static inline int64_t expand_row_avx2(const void* cmpv, int64_t pos, int64_t i,
@@ -76,6 +81,13 @@ __attribute__((target("avx2"))) static inline int64_t expand_row_avx2(const void
         const __m256i v2 = _mm256_permute2x128_si256(D, F, 0x20), v3 = _mm256_permute2x128_si256(A, C, 0x31);
         const __m256i v4 = _mm256_permute2x128_si256(E, B, 0x31), v5 = _mm256_permute2x128_si256(D, F, 0x31);
         uint8_t* r = out + 48 * pos;
+        if constexpr (!STREAM) {  // ring slots: fetch the next lines for writing ahead of the stores (TB_EXPAND_PREFETCH)
+            if (g_prefetch_ahead > 0) {
+                __builtin_prefetch(r + g_prefetch_ahead, 1, 3);
+                __builtin_prefetch(r + g_prefetch_ahead + 64, 1, 3);
+                __builtin_prefetch(r + g_prefetch_ahead + 128, 1, 3);
+            }
+        }
         if constexpr (STREAM) {  // records are 16-byte aligned only: 128-bit non-temporal halves
             __m128i* r16 = reinterpret_cast<__m128i*>(r);
             const __m256i vs[6] = {v0, v1, v2, v3, v4, v5};
