@@ -33,8 +33,11 @@ struct N3Src {
 // whose n3 comes from the tied-row table stay on the scalar loop.  Returns the first j not written.
 static const bool g_has_avx2 = __builtin_cpu_supports("avx2");
 static const int64_t g_prefetch_ahead = [] {
-    const char* e = std::getenv("TB_EXPAND_PREFETCH");  // bytes ahead of the stores; 0 = off
-    return e ? (int64_t)std::max(0, atoi(e)) : (int64_t)0;
+    // bytes ahead of the stores (0 = off).  The ring's lines come back from L3 on every lap; asking for them
+    // in write state ahead of the stores took the config-5 call from 487-491 to 412-438 ms (expansion 387 ->
+    // 293-339 ms; profiles/r02_plugin_prefetch.log)
+    const char* e = std::getenv("TB_EXPAND_PREFETCH");
+    return e ? (int64_t)std::max(0, atoi(e)) : (int64_t)512;
 }();
 
 template <bool NUM_ONLY, bool STREAM>

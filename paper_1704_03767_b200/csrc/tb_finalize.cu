@@ -464,6 +464,44 @@ __global__ void __launch_bounds__(256) records_compact_kernel(const int32_t* __r
     }
     pdl_trigger();
 }
+// q = 8 (the engine's default tile): 32 tiles per CTA, lane (tile, column) walks the tile's 8 rows.  One
+// tile decode (job_coord's sqrt, cells_before_tile) serves 8 records instead of 1, the job ids of a row
+// follow from the previous row's (row_prefix(i + 1) - row_prefix(i) = m - i), and for every row the four
+// tiles of a warp read 128 contiguous bytes of the numerators (consecutive tiles of a tile row).
+// Config-5 batch (87K tiles, 5.6M records): 90 -> ~15 us.
+template <bool NUM_ONLY>
+__global__ void __launch_bounds__(256) records_compact8_kernel(const int32_t* __restrict__ num,
+                                                               const int64_t* __restrict__ n3, int64_t m, int64_t w,
+                                                               int64_t job_lo, int64_t tile_lo, int64_t ntiles,
+                                                               int64_t base0, int naive, void* __restrict__ outv) {
+    pdl_wait();
+    const int tl = threadIdx.x >> 3, c = threadIdx.x & 7;
+    const int64_t t = tile_lo + (int64_t)blockIdx.x * 32 + tl;
+    if (t < tile_lo + ntiles) {
+        int64_t ty, tx;
+        job_coord(t, w, ty, tx);
+        const int64_t r0 = ty * 8, c0 = tx * 8, cend = min(c0 + 8, m);
+        const int64_t base = cells_before_tile(t, m, 8, w) - base0;
+        const int64_t j = c0 + c, width = cend - c0;
+        const bool diag = tx == ty;
+        int64_t rp = row_prefix(r0, m) - job_lo;  // relative job id of (i, i), i = r0 + r
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int64_t i = r0 + r;
+            if (i < m && j < m && j >= i) {
+                const int64_t above = diag ? r * width - r * (r - 1) / 2 : r * width;
+                const int64_t pos = base + above + (j - max(i, c0));
+                const int64_t jid = rp + (j - i);
+                if constexpr (NUM_ONLY)
+                    static_cast<int32_t*>(outv)[pos] = num[jid];
+                else
+                    static_cast<uint2*>(outv)[pos] = make_uint2((uint32_t)num[jid], naive ? 0u : (uint32_t)n3[jid]);
+            }
+            rp += m - i;
+        }
+    }
+    pdl_trigger();
+}
 }  // namespace tb
 
 extern "C" int64_t tb_tile_cells(int64_t m, int64_t q, int64_t tile_lo, int64_t tile_hi) {
@@ -525,6 +563,12 @@ extern "C" int tb_records_compact(const int32_t* num, const int64_t* n3, int64_t
     if (int rc = records_range_check(m, q, job_lo, job_hi, tile_lo, ntiles)) return rc;
     const int64_t w = (m + q - 1) / q;
     const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
+    if (q == 8) {
+        TB_CUDA_TRY(launch_pdl(records_compact8_kernel<false>, dim3((unsigned)((ntiles + 31) / 32)), dim3(256), 0,
+                               static_cast<cudaStream_t>(stream), num, n3, m, w, job_lo, tile_lo, ntiles, base0, naive,
+                               compact));
+        return check_launch("records_compact8_kernel");
+    }
     const int threads = (int)std::min<int64_t>(256, ((q * q + 31) / 32) * 32);
     TB_CUDA_TRY(launch_pdl(records_compact_kernel<false>, dim3((unsigned)ntiles), dim3(threads), 0,
                            static_cast<cudaStream_t>(stream), num, n3, m, q, w, job_lo, tile_lo, base0, naive, compact));
@@ -540,6 +584,12 @@ extern "C" int tb_records_num(const int32_t* num, int64_t m, int64_t q, int64_t 
     if (int rc = records_range_check(m, q, job_lo, job_hi, tile_lo, ntiles)) return rc;
     const int64_t w = (m + q - 1) / q;
     const int64_t base0 = cells_before_tile(tile_lo, m, q, w);
+    if (q == 8) {
+        TB_CUDA_TRY(launch_pdl(records_compact8_kernel<true>, dim3((unsigned)((ntiles + 31) / 32)), dim3(256), 0,
+                               static_cast<cudaStream_t>(stream), num, (const int64_t*)nullptr, m, w, job_lo, tile_lo,
+                               ntiles, base0, 0, (void*)out));
+        return check_launch("records_num8_kernel");
+    }
     const int threads = (int)std::min<int64_t>(256, ((q * q + 31) / 32) * 32);
     TB_CUDA_TRY(launch_pdl(records_compact_kernel<true>, dim3((unsigned)ntiles), dim3(threads), 0,
                            static_cast<cudaStream_t>(stream), num, (const int64_t*)nullptr, m, q, w, job_lo, tile_lo,
