@@ -420,13 +420,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                         }
                     } else {
                         const int64_t x = xc + col;
+                        // interior chunk (warp-uniform): right of the diagonal for all 32 rows, inside the
+                        // matrix and the job range -- plain stores, no per-element bounds (the epilogue is
+                        // instruction-bound: ~20 issued per element on the checked path, ~6 here)
+                        const bool interior = xc >= y0 + 31 && xc + 15 < m && y0 + 31 < m && rowbase[0] + xc >= 0 &&
+                                              rowbase[31] + xc + 15 < span;
+                        if (interior) {
+                            int32_t* colp = p.num + x;
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const int rr = 2 * k + half;
+                                colp[rowbase[rr]] = stg[rr * STG_LD + col] - cfix;
+                            }
+                        } else {
 #pragma unroll 4
-                        for (int k = 0; k < 16; ++k) {
-                            const int rr = 2 * k + half;
-                            const int64_t y = y0 + rr;
-                            const int64_t j = rowbase[rr] + x;
-                            if (x >= y && x < m && j >= 0 && j < span)
-                                p.num[j] = stg[rr * STG_LD + col] - cfix;
+                            for (int k = 0; k < 16; ++k) {
+                                const int rr = 2 * k + half;
+                                const int64_t y = y0 + rr;
+                                const int64_t j = rowbase[rr] + x;
+                                if (x >= y && x < m && j >= 0 && j < span)
+                                    p.num[j] = stg[rr * STG_LD + col] - cfix;
+                            }
                         }
                     }
                     __syncwarp();

@@ -12,5 +12,5 @@ def sink(r):
     got[0] += r.shape[0]
 for _ in range(int(os.environ.get("CALLS", "1"))):
     t0 = time.perf_counter()
-    tb.compute_all_pairs(ds, "vectorized", sink=sink)
+    tb.compute_all_pairs(ds, "vectorized", sink=sink, overlap=os.environ.get("OVERLAP", "1") == "1")
     print(f"call {1e3 * (time.perf_counter() - t0):.1f} ms, records {got[0]}", flush=True)
