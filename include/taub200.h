@@ -307,6 +307,12 @@ int tb_merge_pairs(const uint16_t *keys, const int32_t *pos, const int32_t *sort
                    int64_t job_lo, int64_t job_hi, int32_t *num, uint64_t *nd, uint64_t *n3, void *workspace,
                    int64_t ws_bytes, void *stream);
 
+/* Host utility: upload nbytes of pageable host memory to the device through two pinned staging buffers
+ * (stage_bytes each, >= 1 MiB), filled by nthreads host threads while the copy engine drains the other;
+ * the copies are enqueued on stream and complete before the call returns. */
+int tb_h2d_staged(const void *src, void *dst, int64_t nbytes, void *stage_a, void *stage_b, int64_t stage_bytes,
+                  int nthreads, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

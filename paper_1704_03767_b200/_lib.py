@@ -60,6 +60,7 @@ SIGNATURES = {
     "tb_records_num": ([_p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p], ctypes.c_int),
     "tb_expand_records_num": ([_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int, _p, ctypes.c_int],
                               ctypes.c_int),
+    "tb_h2d_staged": ([_p, _p, _i64, _p, _p, _i64, ctypes.c_int, _p], ctypes.c_int),
     "tb_expand_store_mode": ([ctypes.c_int], ctypes.c_int),
     "tb_expand_ring": ([_p, ctypes.c_int, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _i64, ctypes.c_int, _p, _i64, _i64,
                         _i64, _p, ctypes.c_int], ctypes.c_int),

@@ -8,6 +8,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 #include <mutex>
 #include <thread>
@@ -381,4 +382,52 @@ extern "C" int tb_expand_records_num(const int32_t* nums, const uint64_t* n1_row
     tab.n3t = n3t;
     tab.nt = nt;
     return expand_impl<true>(nums, n1_rows, m, n, q, tile_lo, ntiles, naive, records, nthreads, tab);
+}
+
+// Pageable host array -> device through two pinned staging buffers: the pool's threads fill one buffer
+// (parallel memcpy) while the copy engine drains the other in <= 4 MiB pieces.  One call for the whole
+// upload, so a Python caller holds no GIL while it runs (compute_all_pairs' early upload overlaps the
+// main thread's planning).  Replaces the host side of the reference's dataset hand-off to its workers
+// (engine.py:338-352: the rank matrix is shared with the worker threads as is).
+extern "C" int tb_h2d_staged(const void* src, void* dst, int64_t nbytes, void* stage_a, void* stage_b,
+                             int64_t stage_bytes, int nthreads, void* stream) {
+    if (nbytes < 0 || stage_bytes < (1 << 20)) return fail(TB_ERR_CONFIG, "h2d_staged: bad sizes");
+    if (nbytes == 0) return TB_OK;
+    if (!src || !dst || !stage_a || !stage_b) return fail(TB_ERR_INVALID, "h2d_staged: null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* stage[2] = {static_cast<uint8_t*>(stage_a), static_cast<uint8_t*>(stage_b)};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool used[2] = {false, false};
+    int rc = TB_OK;
+    for (int b = 0; b < 2; ++b)
+        if (cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming) != cudaSuccess) rc = fail(TB_ERR_CUDA, "h2d_staged: event");
+    const uint8_t* s8 = static_cast<const uint8_t*>(src);
+    uint8_t* d8 = static_cast<uint8_t*>(dst);
+    const int nt = std::max(1, nthreads);
+    int k = 0;
+    for (int64_t o = 0; o < nbytes && rc == TB_OK; o += stage_bytes, ++k) {
+        const int b = k & 1;
+        const int64_t n = std::min(stage_bytes, nbytes - o);
+        if (used[b] && cudaEventSynchronize(ev[b]) != cudaSuccess) { rc = fail(TB_ERR_CUDA, "h2d_staged: sync"); break; }
+        const std::function<void(int)> part = [&](int t) {
+            const int64_t a = n * t / nt, e = n * (t + 1) / nt;
+            memcpy(stage[b] + a, s8 + o + a, (size_t)(e - a));
+        };
+        if (nt == 1) part(0);
+        else expand_pool().run(nt, part);
+        for (int64_t q = 0; q < n; q += (4 << 20)) {
+            const int64_t e = std::min(n, q + (int64_t)(4 << 20));
+            if (cudaMemcpyAsync(d8 + o + q, stage[b] + q, (size_t)(e - q), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+                rc = fail(TB_ERR_CUDA, "h2d_staged: copy");
+                break;
+            }
+        }
+        if (rc == TB_OK && cudaEventRecord(ev[b], st) != cudaSuccess) rc = fail(TB_ERR_CUDA, "h2d_staged: record");
+        used[b] = true;
+    }
+    for (int b = 0; b < 2; ++b) {
+        if (used[b]) cudaEventSynchronize(ev[b]);  // the staging buffers are free again on return
+        if (ev[b]) cudaEventDestroy(ev[b]);
+    }
+    return rc;
 }
