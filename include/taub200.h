@@ -153,6 +153,10 @@ int tb_gemm_pairs_fix(const int8_t *S, int64_t m, int64_t K, int64_t ldS, int fo
 /* fix[r] = sum_k S[r, k] of a TB_SIGN_E2M1_OFS matrix (the nibble values' sum minus n0): the Kendall
  * numerator of row r against the sample order, the correction term of tb_gemm_pairs_fix. */
 int tb_sign_row_sums(const int8_t *S, int64_t m, int64_t ldS, int64_t n, int32_t *fix, void *stream);
+/* tb_sign_pack(TB_SIGN_E2M1_OFS) and tb_sign_row_sums in one launch: the pack sums the values it writes
+ * (fix is zeroed on the stream first), saving the extra pass over S. */
+int tb_sign_pack_sums(const uint16_t *R, int64_t m, int64_t n, int64_t ldr, int8_t *S, int64_t ldS, int32_t *fix,
+                      void *stream);
 
 /* |S| for the full-count mode: A[r, k] = |S[r, k]| (0/1 int8), same layout.
  * The second GEMM A A^T gives n_c + n_d per pair (SURVEY 8 identities).

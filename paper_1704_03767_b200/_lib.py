@@ -43,6 +43,7 @@ SIGNATURES = {
     "tb_abs_pack": ([_p, _i64, _i64, ctypes.c_int, _p, _p], ctypes.c_int),
     "tb_gemm_pairs": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _p], ctypes.c_int),
     "tb_gemm_pairs_fix": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _i64, _p, _p], ctypes.c_int),
+    "tb_sign_pack_sums": ([_p, _i64, _i64, _i64, _p, _i64, _p, _p], ctypes.c_int),
     "tb_sign_row_sums": ([_p, _i64, _i64, _i64, _p, _p], ctypes.c_int),
     "tb_gemm_tau_b_fix": ([_p, _i64, _i64, _i64, ctypes.c_int, _i64, _i64, _i32, _p, _i64, _p, _i64, _p, _p, _p],
                           ctypes.c_int),

@@ -170,10 +170,19 @@ __device__ __forceinline__ int sp_slow_chunk(int64_t c, const SpLayout& L, const
 // e2m1 chunks [c_lo, c_hi) of one row (c_lo even): each lane takes two adjacent chunks (a_l, a_l + 1
 // of one block pair share the window: one pair of window loads, one rank-pair load, one 16-byte
 // store; a warp writes 512 contiguous bytes) and steps 64 chunks = 4 block pairs.
+// Sum of the offset-coded values (nibbles 0x0 / 0x2 / 0x4 = 0 / 1 / 2) of up to four words into acc: the
+// nibbles are even, so w >> 1 halves each in place; two halved pair sums stay <= 8 per nibble, and two
+// dp4a's add the eight nibbles of the result.
+__device__ __forceinline__ int32_t ofs_sum4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, int32_t acc) {
+    const uint32_t z = ((a + b) >> 1) + ((c + d) >> 1);
+    uint32_t u = __dp4a(z & 0x0F0F0F0Fu, 0x01010101u, (uint32_t)acc);
+    u = __dp4a((z >> 4) & 0x0F0F0F0Fu, 0x01010101u, u);
+    return (int32_t)u;
+}
 template <int OFS>
 __device__ __forceinline__ void sp_e2m1_range(int c_lo, int c_hi, int lane, const SpLayout& L, const uint16_t* r16,
                                               const uint32_t* wp, const uint32_t* wb, const uint4* masks,
-                                              int8_t* row, uint32_t neg1) {
+                                              int8_t* row, uint32_t neg1, int32_t& acc) {
     const int c1 = (int)L.c1, nbf = (int)L.nbf;
     int c = c_lo + 2 * lane;
     const int c1_end = min(c_hi, c1);  // c1 is a multiple of 16: a pair never straddles it
@@ -198,6 +207,7 @@ __device__ __forceinline__ void sp_e2m1_range(int c_lo, int c_hi, int lane, cons
             const uint32_t owb[8] = {ob, ob, ob, ob, ob, ob, ob, ob};
             const uint2 va = chunk_e2m1<OFS>(y, owa, neg1), vb = chunk_e2m1<OFS>(y, owb, neg1);
             *outp = make_uint4(va.x, va.y, vb.x, vb.y);
+            if (OFS) acc = ofs_sum4(va.x, va.y, vb.x, vb.y, acc);
             c += 64;
             if (c >= c1_end) break;
             outp += 32;
@@ -228,6 +238,7 @@ __device__ __forceinline__ void sp_e2m1_range(int c_lo, int c_hi, int lane, cons
                 v2.y &= mk.y;
             }
             *reinterpret_cast<uint2*>(row + 8 * (int64_t)(c + k)) = v2;
+            if (OFS) acc = ofs_sum4(v2.x, v2.y, 0u, 0u, acc);
         }
     }
 }
@@ -239,7 +250,8 @@ __device__ __forceinline__ void sp_e2m1_range(int c_lo, int c_hi, int lane, cons
 template <int FMT>
 __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t* __restrict__ R, int64_t n,
                                                               int64_t ldr, int8_t* __restrict__ S, int64_t ldS,
-                                                              int nw, uint32_t neg1) {
+                                                              int nw, uint32_t neg1, int32_t* __restrict__ rowsum,
+                                                              int64_t n0) {
     pdl_wait();
     extern __shared__ __align__(16) uint32_t sp_words[];  // wp[nw] plain pairs, wb[nw] biased, masks[17]
     uint32_t* wp = sp_words;
@@ -281,7 +293,13 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
     const int wper = ((b_hi - b_lo + (SP_THREADS / 32) - 1) / (SP_THREADS / 32) + 1) & ~1;
     const int c_lo = min(b_lo + warp * wper, b_hi), c_hi = min(c_lo + wper, b_hi);
     if (FMT >= 2) {
-        sp_e2m1_range<FMT == 3>(c_lo, c_hi, lane, L, r16, wp, win, masks, row, neg1);
+        int32_t acc = 0;
+        sp_e2m1_range<FMT == 3>(c_lo, c_hi, lane, L, r16, wp, win, masks, row, neg1, acc);
+        if (FMT == 3 && rowsum) {  // fused tb_sign_row_sums: rowsum[r] (zeroed by the host) += this warp's share
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (blockIdx.y == 0 && warp == 0) acc -= (int32_t)n0;
+            if (lane == 0 && acc != 0) atomicAdd(rowsum + r, acc);
+        }
     } else {
     int c = c_lo + lane;
     const int nbf = (int)L.nbf;
@@ -356,8 +374,24 @@ __global__ void __launch_bounds__(SP_THREADS, 4) signpack_kernel(const uint16_t*
 
 using namespace tb;
 
+static int sign_pack_impl(const uint16_t* R, int64_t m, int64_t n, int64_t ldr, int8_t* S, int64_t ldS, int format,
+                          int32_t* rowsum, void* stream);
+
 extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr, int8_t* S, int64_t ldS,
                             int format, void* stream) {
+    return sign_pack_impl(R, m, n, ldr, S, ldS, format, nullptr, stream);
+}
+
+extern "C" int tb_sign_pack_sums(const uint16_t* R, int64_t m, int64_t n, int64_t ldr, int8_t* S, int64_t ldS,
+                                 int32_t* fix, void* stream) {
+    if (!fix) return fail(TB_ERR_INVALID, "sign_pack_sums: null pointer");
+    if (m < 1 || m > INT32_MAX) return fail(TB_ERR_INVALID, "sign_pack_sums: bad m");
+    TB_CUDA_TRY(cudaMemsetAsync(fix, 0, (size_t)m * sizeof(int32_t), static_cast<cudaStream_t>(stream)));
+    return sign_pack_impl(R, m, n, ldr, S, ldS, TB_SIGN_E2M1_OFS, fix, stream);
+}
+
+static int sign_pack_impl(const uint16_t* R, int64_t m, int64_t n, int64_t ldr, int8_t* S, int64_t ldS, int format,
+                          int32_t* rowsum, void* stream) {
     if (m < 1 || n < 2) return fail(TB_ERR_INVALID, "sign_pack: need m >= 1 and n >= 2 (got m=%lld n=%lld)",
                                     (long long)m, (long long)n);
     if (n > 32767) return fail(TB_ERR_CAPACITY, "sign_pack: n=%lld exceeds 32767 (15-bit ranks)", (long long)n);
@@ -378,7 +412,8 @@ extern "C" int tb_sign_pack(const uint16_t* R, int64_t m, int64_t n, int64_t ldr
     dim3 grid((unsigned)m, gy);
 #define TB_SP_LAUNCH(F)                                                                                   \
     TB_CUDA_TRY(cudaFuncSetAttribute(signpack_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    TB_CUDA_TRY(launch_pdl(signpack_kernel<F>, dim3(grid), dim3(SP_THREADS), smem, st, R, n, ldr, S, ldS, nw, 0xFFFFFFFFu))
+    TB_CUDA_TRY(launch_pdl(signpack_kernel<F>, dim3(grid), dim3(SP_THREADS), smem, st, R, n, ldr, S, ldS, nw, 0xFFFFFFFFu, \
+                           rowsum, n * (n - 1) / 2))
     if (format == TB_SIGN_E2M1_OFS) {
         TB_SP_LAUNCH(3);
     } else if (format == TB_SIGN_E2M1) {

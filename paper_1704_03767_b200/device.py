@@ -53,6 +53,7 @@ D2H_PIECE_BYTES = 256 << 20
 FP4_WIDE = os.environ.get("TB_FP4_WIDE", "1") != "0"
 # offset-coded GEMM operands (TB_SIGN_E2M1_OFS, see TauEngine.sign_format): "auto" | "1" | "0"
 SIGN_OFS = os.environ.get("TB_SIGN_OFS", "auto")
+FUSED_ROW_SUMS = os.environ.get("TB_FUSED_ROW_SUMS", "1") != "0"  # 0: tb_sign_pack + tb_sign_row_sums (cross-check)
 OFS_MIN_WORK = 1e13  # m^2 K from which the GEMM runs long enough to be power-capped (config 3: 3.3e13)
 TIED_SPARSE_FRAC = 0.35  # |S| GEMM over the tied rows only while they are at most this share of the rows
 GEMM_MAX_N = 14000  # the crossover for shapes of unknown m (large m: the GEMM's per-job cost decides): e2m1
@@ -497,9 +498,13 @@ class TauEngine:
                           _ptr(res.n1_rows[r0:]), _ptr(res.flags), _ptr(ws), wsb, st)
             p0 = max(r0, y_lo)
             if p0 < r1:
-                _lib.call("tb_sign_pack", _ptr(R[p0 * ldr:]), r1 - p0, n, ldr, _ptr(S[p0 * ldS:]), ldS, fmt, st)
-                if fix is not None:
-                    _lib.call("tb_sign_row_sums", _ptr(S[p0 * ldS:]), r1 - p0, ldS, n, _ptr(fix[p0:]), st)
+                if fix is not None and FUSED_ROW_SUMS:  # the pack sums what it writes (no extra pass over S)
+                    _lib.call("tb_sign_pack_sums", _ptr(R[p0 * ldr:]), r1 - p0, n, ldr, _ptr(S[p0 * ldS:]), ldS,
+                              _ptr(fix[p0:]), st)
+                else:
+                    _lib.call("tb_sign_pack", _ptr(R[p0 * ldr:]), r1 - p0, n, ldr, _ptr(S[p0 * ldS:]), ldS, fmt, st)
+                    if fix is not None:
+                        _lib.call("tb_sign_row_sums", _ptr(S[p0 * ldS:]), r1 - p0, ldS, n, _ptr(fix[p0:]), st)
         res.extra["sign_format"] = fmt
         return S, K, ldS, fmt
 

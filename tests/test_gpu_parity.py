@@ -527,6 +527,40 @@ def test_offset_operands_full_counts_and_entry_points(ofs_eng, oracle):
 
 
 @pytest.mark.gpu
+def test_fused_row_sums_match_the_separate_pass(eng, oracle):
+    """tb_sign_pack_sums (the pack sums the offset-coded values it writes) against tb_sign_row_sums (a pass
+    over the packed S) and the definition sum_{a<b} sign(r_b - r_a), for row widths around the layout's
+    section boundaries, with ties."""
+    import ctypes
+    from paper_1704_03767_b200 import _lib
+    from paper_1704_03767_b200.device import _ptr
+    lib = _lib.load()
+    for n in (2, 15, 16, 17, 33, 200, 1000, 1024, 2896):
+        m = 37 if n < 2000 else 5
+        rng = np.random.default_rng(n)
+        ranks = np.stack([oracle.rank_transform(rng.integers(0, max(2, n // 3), n)) for _ in range(m)])
+        ldr = (n + 7) // 8 * 8
+        R = torch.zeros((m, ldr), dtype=torch.int16, device="cuda")
+        R[:, :n] = torch.from_numpy(ranks.astype(np.int16)).cuda()
+        K = int(lib.tb_sign_k(n))
+        ldS = (K // 2 + 15) // 16 * 16
+        S1 = torch.empty(m * ldS, dtype=torch.int8, device="cuda")
+        S2 = torch.empty(m * ldS, dtype=torch.int8, device="cuda")
+        f1 = torch.empty(m, dtype=torch.int32, device="cuda")
+        f2 = torch.full((m,), 12345, dtype=torch.int32, device="cuda")
+        _lib.call("tb_sign_pack", _ptr(R), m, n, ldr, _ptr(S1), ldS, _lib.TB_SIGN_E2M1_OFS, None)
+        _lib.call("tb_sign_row_sums", _ptr(S1), m, ldS, n, _ptr(f1), None)
+        _lib.call("tb_sign_pack_sums", _ptr(R), m, n, ldr, _ptr(S2), ldS, _ptr(f2), None)
+        torch.cuda.synchronize()
+        assert torch.equal(S1, S2)
+        d = ranks[:, None, :] - ranks[:, :, None]            # [r, a, b] = r_b - r_a
+        want = np.triu(np.sign(d), 1).sum(axis=(1, 2)) if n <= 1024 else None
+        assert torch.equal(f1, f2), n
+        if want is not None:
+            np.testing.assert_array_equal(f1.cpu().numpy(), want.astype(np.int32))
+
+
+@pytest.mark.gpu
 def test_offset_operands_limit(ofs_eng, oracle):
     """n = 2896 is the last n with 4 K < 2^24 (sums of (S + 1)(S + 1) <= 4 n0 stay exact in f32): a monotone pair
     (numerator = n0, the largest sum) and its reverse, heavy ties; n = 2897 is refused (the engine's own
