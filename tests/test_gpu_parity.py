@@ -527,6 +527,42 @@ def test_offset_operands_full_counts_and_entry_points(ofs_eng, oracle):
 
 
 @pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_lockstep_gemm_concurrent_launches(oracle):
+    """The K-lockstep throttle (multi-wave unsplit plans) with two engines launching on two streams of one
+    device at once: the launches share the per-device progress slots (told apart by epoch), neither may hang
+    or wait on the other, and both results equal the throttle-free numerators (TB_GEMM_LEAD is read once per
+    process, so the reference run is the dp4a cross-check kernel) and, sampled, the oracle."""
+    import threading
+    from paper_1704_03767_b200.device import TauEngine
+    rng = np.random.default_rng(77)
+    m, n = 6400, 260  # 25 row blocks x 14 column-block pairs / 2 > 74 units: several waves, no K split
+    xs = [torch.from_numpy(rng.integers(0, 40, (m, n)).astype(np.int32)).cuda() for _ in range(2)]
+    engs = [TauEngine(0), TauEngine(0)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    out = [None, None]
+
+    def run(k):
+        for _ in range(3):
+            out[k] = engs[k].all_pairs(xs[k], kernel="gemm", stream=streams[k], tau_a=False)
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=240)
+        assert not t.is_alive(), "concurrent lockstep GEMM launches did not finish"
+    torch.cuda.synchronize()
+    for k in range(2):
+        ref = engs[k].all_pairs(xs[k], kernel="gemm", simt=True, tau_a=False, tau_b=False)
+        assert torch.equal(out[k].numerator, ref.numerator)
+        ri, rj = _random_pairs(m, 2000, 5 + k)
+        _oracle_pairs_check(out[k], oracle, xs[k].cpu().numpy(), ri, rj, oracle.KERNEL_PACKED, counts=False)
+    for e in engs:
+        e.release()
+
+
+@pytest.mark.gpu
 def test_fused_row_sums_match_the_separate_pass(eng, oracle):
     """tb_sign_pack_sums (the pack sums the offset-coded values it writes) against tb_sign_row_sums (a pass
     over the packed S) and the definition sum_{a<b} sign(r_b - r_a), for row widths around the layout's
