@@ -485,9 +485,10 @@ def run_ours(args):
                "ms_per_step": 1e3 * t_pl / len(ts), "steps": len(ts),
                "api": ("compute_all_pairs(ds, 'vectorized', sink=...) -- the reference's plugin call "
                        "(engine.py:300-310): H2D of the int32 ranks, every count on the device, 48-byte "
-                       "CELL_DTYPE records (diagonal included) delivered to a host sink pass by pass -- one batch "
-                       f"in {tb.engine.FULL_EVERY} copied as full records, the others as the 4-byte numerator stream (8-byte (numerator, n3) when many rows have ties) "
-                       "expanded into the same bytes by host threads (tb_expand_records); wall clock" + (f"; rank r runs shard=(r, {world})" if world > 1 else "")),
+                       "CELL_DTYPE records (diagonal included) delivered to a host sink pass by pass -- the records "
+                       "cross PCIe as the 4-byte numerator stream (8-byte (numerator, n3) when many rows have ties) and "
+                       "host threads expand them into the same bytes pass by pass in a cache-resident ring "
+                       f"(tb_expand_ring, {tb.engine.RING_SLOTS} slots; runs of few batches: full records by D2H); wall clock" + (f"; rank r runs shard=(r, {world})" if world > 1 else "")),
                "timer": "wall clock around the synchronous host call"}
         del ds
 

@@ -9,6 +9,8 @@ from paper_1704_03767_b200.device import TauEngine
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 eng = TauEngine(0)
+if os.environ.get("GB"):
+    eng.gemm_bands = int(os.environ["GB"])
 x = torch.from_numpy(workloads.generate(5)).cuda()
 st = torch.cuda.Stream()
 for _ in range(2):
@@ -31,7 +33,7 @@ for _ in range(reps):
 proc.terminate()
 mhz = [float(l.split(",")[0]) for l in clk if l.strip()]
 pw = [float(l.split(",")[1]) for l in clk if l.strip()]
-tag = " ".join(f"{k}={os.environ.get(k, '-')}" for k in ("TB_GEMM_GR", "TB_GEMM_WIN", "TB_GEMM_SERP", "TB_GEMM_LEAD", "TB_GEMM_LAGQ"))
+tag = f"GB={os.environ.get('GB', '-')} " + " ".join(f"{k}={os.environ.get(k, '-')}" for k in ("TB_GEMM_GR", "TB_GEMM_WIN", "TB_GEMM_SERP", "TB_GEMM_LEAD", "TB_GEMM_LAGQ"))
 print(f"{tag}: step {statistics.median(ts):.1f} ms, gemm {statistics.median(gs):.1f} ms "
       f"(min {min(gs):.1f}), sm clock median {statistics.median(mhz) if mhz else 0:.0f} MHz, "
       f"power median {statistics.median(pw) if pw else 0:.0f} W", flush=True)
