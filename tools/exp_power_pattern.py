@@ -38,6 +38,10 @@ def fill(S, pat):
         elif pat == "b01":
             r = torch.randint(0, 256, (c.numel(),), dtype=torch.uint8, device=c.device)
             v = (r & 0x22)
+        elif pat.startswith("nib"):  # random 0 / nibble value, e.g. nib1 = 0.5, nib2 = 1.0, nib4 = 2.0, nib6 = 4.0
+            v0 = int(pat[3:], 16)
+            r = torch.randint(0, 256, (c.numel(),), dtype=torch.uint8, device=c.device)
+            v = (r & 0x11) * v0
         elif pat == "b01q":
             r = torch.randint(0, 256, (c.numel(),), dtype=torch.uint8, device=c.device)
             r2 = torch.randint(0, 256, (c.numel(),), dtype=torch.uint8, device=c.device)
