@@ -10,6 +10,11 @@ ds = tb.Dataset(labels=[str(i) for i in range(x.shape[0])], ranks=np.stack([tb.r
 got = [0]
 def sink(r):
     got[0] += r.shape[0]
+import gc
+if os.environ.get("NOGC") == "1":
+    gc.disable()
+if os.environ.get("FREEZE") == "1":
+    gc.collect(); gc.freeze()
 for _ in range(int(os.environ.get("CALLS", "1"))):
     t0 = time.perf_counter()
     tb.compute_all_pairs(ds, "vectorized", sink=sink, overlap=os.environ.get("OVERLAP", "1") == "1")
