@@ -804,9 +804,11 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.fix_c = fix ? (int32_t)fix_c : 0;
     if (wide && !p.partial) return fail(TB_ERR_CONFIG, "gemm fp4: wide K needs a split plan");
     // tau_b callers: a split plan finalizes straight from the f32 workspace (accum_finalize); a one-launch
-    // plan writes the numerators and the caller finalizes -- or, with TB_FUSE_EPILOGUE=1, the epilogue writes
-    // tau_b itself (measured slower under the power cap: profiles/r02_fused_finalize_ab.log)
-    static const bool kEpiFuse = [] { const char* e = std::getenv("TB_FUSE_EPILOGUE"); return e && e[0] == '1'; }();
+    // plan's epilogue writes tau_b itself (TB_FUSE_EPILOGUE=0: it writes the numerators and the caller
+    // finalizes).  Slower before the lockstep throttle (config 5 407.7 -> 422.7 ms,
+    // profiles/r02_fused_finalize_ab.log), faster with it: 317.4 / 318.3 -> 315.3 / 315.4 ms per step, no
+    // 8.6 GB numerator round trip (profiles/r02_fused_finalize_ab_s5.log)
+    static const bool kEpiFuse = [] { const char* e = std::getenv("TB_FUSE_EPILOGUE"); return !e || e[0] != '0'; }();
     const bool acc_fin = tau_b && p.partial && !wide;
     if (tau_b && !p.partial && kEpiFuse) {
         p.tau_b = tau_b;

@@ -229,9 +229,9 @@ class TauEngine:
     # most TIED_SPARSE_FRAC of the rows (n3 = 0 for every pair with an untied variable), else over all rows
     tied_mode: str = "auto"
     # tau_b-only callers (tau_b_bands, all_pairs_host(numerators=False)) on the GEMM path go through
-    # tb_gemm_tau_b: split plans finalize straight from the f32 workspace (one launch instead of convert +
-    # finalize), one-launch plans write numerators and finalize after the GEMM (the epilogue fusion,
-    # TB_FUSE_EPILOGUE=1, measured slower under the power cap: profiles/r02_fused_finalize_ab.log)
+    # tb_gemm_tau_b: one-launch plans write tau_b from the GEMM epilogue (no numerator round trip, no
+    # finalize launch; TB_FUSE_EPILOGUE=0 restores numerators + tb_finalize), split plans finalize straight
+    # from the f32 workspace (one launch instead of convert + finalize)
     fuse_finalize: bool = os.environ.get("TB_FUSE_FINALIZE", "1") != "0"
 
     def sign_format(self, K: int, m: int | None = None) -> int:

@@ -925,9 +925,11 @@ def test_fused_tau_b_epilogue(eng, oracle, m, n, levels):
     np.testing.assert_array_equal(ref[sel], tb)
 
 
-def test_fused_epilogue_opt_in_subprocess(tmp_path):
-    """TB_FUSE_EPILOGUE=1 (read once per process): the FP4 GEMM epilogue writes tau_b itself on one-launch
-    plans; identical to the default numerator + finalize sequence (run in a child process)."""
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_fused_epilogue_switch_subprocess(tmp_path, fuse):
+    """TB_FUSE_EPILOGUE (read once per process; default on): the FP4 GEMM epilogue writes tau_b itself on
+    one-launch plans, or (0) writes numerators for a separate finalize; both identical to all_pairs'
+    numerator + finalize sequence (run in a child process)."""
     import subprocess
     import sys
     code = r"""
@@ -947,6 +949,6 @@ assert torch.equal(out.isnan(), ref.isnan())
 assert torch.equal(torch.nan_to_num(out), torch.nan_to_num(ref))
 print("ok")
 """ % (str(__import__("conftest").ROOT),)
-    env = dict(__import__("os").environ, TB_FUSE_EPILOGUE="1")
+    env = dict(__import__("os").environ, TB_FUSE_EPILOGUE=fuse)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
