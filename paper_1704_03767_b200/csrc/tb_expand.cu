@@ -340,9 +340,21 @@ extern "C" int tb_expand_ring(const void* compact, int width, const uint64_t* n1
     tab.n3t = n3t;
     tab.nt = width == 4 ? nt_rows : 0;
     const int nthr = (int)std::max<int64_t>(1, nthreads);
+    // Every pass is cut into SUB chunks per worker.  A worker expands its own chunks first (the same ring
+    // bytes every lap: they stay in its core's L2), then takes unclaimed chunks of workers that fell behind
+    // -- from their last chunk backwards, so a worker that is merely a little late keeps its share.  On a
+    // quiet host nothing is stolen; when a worker loses its core for a while (12 workers, the producer, the
+    // consumer and the writer share 16 cores) the pass no longer waits for it.  TB_EXPAND_STEAL=0: off.
+    static const bool kSteal = [] { const char* e = std::getenv("TB_EXPAND_STEAL"); return !e || e[0] != '0'; }();
+    constexpr int SUB = 4;
+    const int C = nthr * SUB;
+    std::vector<std::atomic<uint8_t>> claimed((size_t)npass * C);
+    for (auto& c : claimed) c.store(0, std::memory_order_relaxed);
     std::vector<std::atomic<int>> done(npass);
     for (auto& d : done) d.store(0, std::memory_order_relaxed);
     std::atomic<int> aborted{0};
+    std::mutex pub_mu;
+    int64_t published = 0;  // passes [0, published) are visible to the consumer (guarded by pub_mu)
     const std::function<void(int)> part = [&](int k) {
         for (int64_t p = 0; p < npass; ++p) {
             const int64_t seq = seq0 + p;
@@ -351,15 +363,31 @@ extern "C" int tb_expand_ring(const void* compact, int width, const uint64_t* n1
                 return;
             }
             const int64_t t_lo = pass_tile[p], nti = pass_tile[p + 1] - t_lo;
-            const int64_t a = t_lo + nti * k / nthr, b = t_lo + nti * (k + 1) / nthr;
             uint8_t* out = static_cast<uint8_t*>(ring) + (seq % nslots) * slot_bytes;
             const uint8_t* src = static_cast<const uint8_t*>(compact) + (base[p] - base_batch) * width;
-            if (a < b) {
-                if (width == 4) expand_tiles<true, false>(src, n1_rows, m, n0, q, w, a, b, base[p], naive, out, tab);
-                else expand_tiles<false, false>(src, n1_rows, m, n0, q, w, a, b, base[p], naive, out, tab);
-            }
-            if (done[p].fetch_add(1, std::memory_order_acq_rel) == nthr - 1)
-                __atomic_store_n(ctl, seq + 1, __ATOMIC_RELEASE);  // every worker finished pass p (and all before it)
+            auto chunk = [&](int c) {
+                std::atomic<uint8_t>& flag = claimed[(size_t)p * C + c];
+                if (flag.load(std::memory_order_relaxed) != 0 || flag.exchange(1, std::memory_order_acq_rel) != 0) return;
+                const int64_t a = t_lo + nti * c / C, b = t_lo + nti * (c + 1) / C;
+                if (a < b) {
+                    if (width == 4) expand_tiles<true, false>(src, n1_rows, m, n0, q, w, a, b, base[p], naive, out, tab);
+                    else expand_tiles<false, false>(src, n1_rows, m, n0, q, w, a, b, base[p], naive, out, tab);
+                }
+                if (done[p].fetch_add(1, std::memory_order_acq_rel) == C - 1) {
+                    // pass p is complete; publish it and any complete passes behind a late one, in order
+                    std::lock_guard<std::mutex> lk(pub_mu);
+                    while (published < npass && done[published].load(std::memory_order_acquire) == C) {
+                        ++published;
+                        __atomic_store_n(ctl, seq0 + published, __ATOMIC_RELEASE);
+                    }
+                }
+            };
+            for (int s2 = 0; s2 < SUB; ++s2) chunk(k * SUB + s2);
+            if (kSteal)
+                for (int off = 1; off < nthr; ++off) {
+                    const int v = (k + off) % nthr;
+                    for (int s2 = SUB - 1; s2 >= 0; --s2) chunk(v * SUB + s2);
+                }
         }
     };
     if (nthr == 1) part(0);
