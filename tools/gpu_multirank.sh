@@ -3,10 +3,8 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TB_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
-    --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3 --e2e-steps 2 > gpurun_out/mr_weak.log 2>&1; echo weak=$?
+    --master-port 29517 bench.py --gpus 2 --steps 2 --warmup 3 --e2e-steps 1 --e2e-tau-steps 1 --no-cpu-baseline > gpurun_out/mr_weak.log 2>&1; echo weak=$?
 TB_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
-    --master-port 29518 bench.py --gpus 2 --steps 5 --warmup 3 --e2e-steps 2 --scaling strong > gpurun_out/mr_strong.log 2>&1; echo strong=$?
+    --master-port 29518 bench.py --gpus 2 --steps 2 --warmup 3 --e2e-steps 1 --e2e-tau-steps 1 --no-cpu-baseline --scaling strong > gpurun_out/mr_strong.log 2>&1; echo strong=$?
 TB_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
     --master-port 29519 bench.py --impl reference --gpus 2 --steps 2 --warmup 1 > gpurun_out/mr_ref.log 2>&1; echo ref=$?
-TB_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
-    --master-port 29520 bench.py --gpus 2 --steps 3 --warmup 3 --e2e-steps 1 --scaling strong --gather > gpurun_out/mr_gather.log 2>&1; echo gather=$?
