@@ -617,15 +617,26 @@ __device__ __forceinline__ uint32_t merge_level_cur(const uint16_t* src, uint16_
     store_lookaheads<E>(dst, t, 2 * W, ow);
     return inv;
 }
+// Barrier of the threads merging one block: a named barrier (id 1..15) when several blocks of the CTA merge
+// side by side -- the two halves of n > 32768, the pairs of merge_multi_kernel -- so a block's threads wait
+// only for each other and the blocks' barrier stalls overlap; id 0 = the whole CTA.
+#ifndef MG_GROUP_BARRIERS
+#define MG_GROUP_BARRIERS 1
+#endif
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+    if (!MG_GROUP_BARRIERS || id == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 // In place: every thread's outputs stay in registers until all threads have read the level's runs.
 template <int E>
-__device__ __forceinline__ uint32_t merge_level_inplace(uint16_t* blk, int t, int W, const MgConst& K) {
+__device__ __forceinline__ uint32_t merge_level_inplace(uint16_t* blk, int t, int W, const MgConst& K, int bar_id,
+                                                        int bar_threads) {
     uint32_t ow[E / 2];
     const uint32_t inv = merge_level_regs<E, false>(blk, t, W, K, ow);
-    __syncthreads();
+    group_sync(bar_id, bar_threads);
     store_words<E>(blk, t, ow);
     store_lookaheads<E>(blk, t, 2 * W, ow);
-    __syncthreads();
+    group_sync(bar_id, bar_threads);
     return inv;
 }
 
@@ -697,7 +708,9 @@ __device__ uint32_t sort_count_halves(uint16_t* keys, int L, const MgConst& K) {
     uint16_t* blk = keys + (tid >> 9) * sw(L);
     const int t = tid & (MG_THREADS / 2 - 1);
 #pragma unroll 1
-    for (int W = E << LEAF_XL<E>; W < L; W <<= 1) inv += merge_level_inplace<EM>(blk, t, W, K);
+    for (int W = E << LEAF_XL<E>; W < L; W <<= 1)
+        inv += merge_level_inplace<EM>(blk, t, W, K, 1 + (tid >> 9), MG_THREADS / 2);
+    __syncthreads();  // the halves ran on their own barriers: the caller reads both sorted halves
     return inv;
 }
 
@@ -1136,8 +1149,10 @@ __global__ void __launch_bounds__(MG_THREADS, 1) merge_multi_kernel(MergeArgs p)
         }
         __syncthreads();
         uint32_t inv = 0;
+        const int bar_id = (2 * MG_HALF / L) <= 15 ? 1 + g : 0;  // 16 hardware barriers per CTA (0: __syncthreads)
 #pragma unroll 1
-        for (int W = 32 << LEAF_XL<32>; W < L; W <<= 1) inv += merge_level_inplace<2 * MG_HALF / MG_THREADS>(blk, t, W, K);
+        for (int W = 32 << LEAF_XL<32>; W < L; W <<= 1)
+            inv += merge_level_inplace<2 * MG_HALF / MG_THREADS>(blk, t, W, K, bar_id, G);
         mine += (int64_t)(int32_t)inv;
         const int64_t wm = warp_sum64(mine), wt = warp_sum64(ties);
         if (lane == 0) {
