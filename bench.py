@@ -106,6 +106,9 @@ class ClockSampler:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         time.sleep(0.06)
+        t_wait = time.time() + 1.0  # a timed region of a few ms ends before nvidia-smi prints its first line
+        while not self.lines and time.time() < t_wait:
+            time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
