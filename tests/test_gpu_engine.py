@@ -365,3 +365,23 @@ def test_config5_record_stream_properties():
     jid = torch.from_numpy(i * (2 * m - i + 1) // 2 + j - i).cuda()
     np.testing.assert_array_equal(res.numerator.index_select(0, jid).cpu().numpy().astype(np.int64),
                                   smp["numerator"].astype(np.int64))
+
+
+def test_staged_upload_matches_source(monkeypatch):
+    """engine._h2d_staged (tb_h2d_staged: host threads fill two pinned staging buffers, the copy engine drains
+    them in pieces): sizes that are not multiples of the staging buffer, the piece or the thread count, on a
+    side stream, and the small-array fallback."""
+    from paper_1704_03767_b200 import engine
+    rng = np.random.default_rng(3)
+    st = torch.cuda.Stream()
+    for shape in ((4099, 4421), (1 << 23,), (33, 7)):
+        src = rng.integers(-2**31, 2**31 - 1, shape, dtype=np.int64).astype(np.int32)
+        x = engine._h2d_staged(src, torch.device("cuda", 0), st)
+        st.synchronize()
+        assert x.shape == src.shape and x.dtype == torch.int32
+        np.testing.assert_array_equal(x.cpu().numpy(), src)
+    monkeypatch.setattr(engine, "H2D_STAGE_BYTES", 3 << 20)  # many stage swaps
+    src = rng.integers(0, 1000, (5000, 1021), dtype=np.int32)
+    x = engine._h2d_staged(src, torch.device("cuda", 0), st)
+    st.synchronize()
+    np.testing.assert_array_equal(x.cpu().numpy(), src)
