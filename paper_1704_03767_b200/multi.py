@@ -17,6 +17,8 @@ of result bands (tau_b) to one consumer rank, pipelined with the compute:
 
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -28,7 +30,7 @@ from .pairindex import job_shard_range
 # alignment was the duplicated boundary row blocks), and every row the shard sign-packs (all rows from its
 # first one to m) costs ROW_PACK_COST pairs (K2: 42 ns per 1024-sample row against 0.196 ns per pair).
 ROW_WIDTH_COST = 0.0
-ROW_PACK_COST = 214
+ROW_PACK_COST = float(os.environ.get("TB_ROW_PACK_COST", "214"))
 
 
 def _row_prefix(y: int, m: int) -> int:
