@@ -83,6 +83,7 @@ struct Gemm4Args {
     // row sums s and fix_c = n0; a split unit's first item (kb0 == 0) carries the correction.
     const int32_t* fix;
     int32_t fix_c;
+    int32_t l2hint;  // experiment (TB_GEMM_L2HINT): 1 = evict_last, 2 = evict_first on the operand loads
 };
 
 // ---- K-lockstep throttle.  The ~74 concurrently running CTA pairs stream the same S rows (units of one
@@ -240,6 +241,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
         const bool lock = p.lead > 0 && leader;
         uint32_t done = 0;
         if (lock && lane == 0) prog_publish(p.prog, pair, p.epoch, 0);
+        const uint64_t pol = p.l2hint == 1 ? l2_policy_evict_last() : (p.l2hint == 2 ? l2_policy_evict_first() : 0ull);
         while (next_unit4(p, cur, npairs, t)) {
             // each block loads a full 120-row box per CTA; the 2-SM MMA with N reads N / 2 rows of
             // each CTA, so CTA 1's box starts at N / 2 (partial blocks need no other tensor map)
@@ -257,10 +259,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g4::THREADS, 1)
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
                     uint8_t* sa = smem + stage * STAGE_BYTES;
-                    tma_load_2d_2sm(sa, &tmap_a, fb, kb * BK, (int32_t)(t.y0 + rank * BM));
-                    for (int h = 0; h < t.nblk; ++h)
-                        tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
-                                        (int32_t)(t.xs[h] + rank * (t.nb[h] / 2)));
+                    if (p.l2hint) {
+                        tma_load_2d_2sm_hint(sa, &tmap_a, fb, kb * BK, (int32_t)(t.y0 + rank * BM), pol);
+                        for (int h = 0; h < t.nblk; ++h)
+                            tma_load_2d_2sm_hint(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
+                                                 (int32_t)(t.xs[h] + rank * (t.nb[h] / 2)), pol);
+                    } else {
+                        tma_load_2d_2sm(sa, &tmap_a, fb, kb * BK, (int32_t)(t.y0 + rank * BM));
+                        for (int h = 0; h < t.nblk; ++h)
+                            tma_load_2d_2sm(sa + A_BYTES + h * B_BYTES, &tmap_b, fb, kb * BK,
+                                            (int32_t)(t.xs[h] + rank * (t.nb[h] / 2)));
+                    }
                 }
                 __syncwarp();
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -802,6 +811,8 @@ int gemm_fp4(const int8_t* S, int64_t m, int64_t K, int64_t ldS, int64_t job_lo,
     p.int_red = wide ? 1 : 0;
     p.fix = fix;
     p.fix_c = fix ? (int32_t)fix_c : 0;
+    static const int32_t kL2Hint = [] { const char* e = std::getenv("TB_GEMM_L2HINT"); return e ? atoi(e) : 0; }();
+    p.l2hint = kL2Hint;
     if (wide && !p.partial) return fail(TB_ERR_CONFIG, "gemm fp4: wide K needs a split plan");
     // tau_b callers: a split plan finalizes straight from the f32 workspace (accum_finalize); a one-launch
     // plan's epilogue writes tau_b itself (TB_FUSE_EPILOGUE=0: it writes the numerators and the caller
